@@ -1,0 +1,115 @@
+/*
+ * gpb200 -- C ABI of the B200-native tiled Gaussian-process hot path.
+ *
+ * This is the drop-in boundary for the reference's model API
+ * (taskgp 0.1.0, /root/reference/pkg/src/taskgp/model.py) and its tile-kernel
+ * plugin registry (tiles.py:98-117).  Plain pointers and sizes only: every
+ * array is float64, C-contiguous (row-major), in HOST memory unless the
+ * function name ends in _device.  Every entry point returns a gpb_status;
+ * gpb_last_error() gives the message of the last failure on this thread.
+ *
+ * Threading: calls on one model must be serialised by the caller
+ * (model.py:104-108); distinct models may be used from different threads.
+ * Every call blocks until its device work is complete (run_as_root,
+ * runtime.py:250-262).
+ */
+#ifndef GPB200_H
+#define GPB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The Python layer maps each onto the reference exception
+ * class of the same meaning (errors.py:4-52). */
+typedef enum gpb_status {
+  GPB_OK = 0,
+  GPB_INVALID_CONFIG = 1,  /* InvalidConfig        (errors.py:8)  */
+  GPB_ALREADY_RUNNING = 2, /* AlreadyRunning       (errors.py:12) */
+  GPB_NOT_RUNNING = 3,     /* NotRunning           (errors.py:16) */
+  GPB_TILING = 4,          /* TilingError          (errors.py:20) */
+  GPB_DIM = 5,             /* DimensionMismatch    (errors.py:24) */
+  GPB_NOT_PD = 6,          /* NotPositiveDefinite  (errors.py:28) */
+  GPB_SINGULAR = 7,        /* SingularTriangular   (errors.py:32) */
+  GPB_NUMERIC = 8,         /* NumericalConsistencyError (errors.py:36) */
+  GPB_CUDA = 9,            /* device error (no reference equivalent) */
+  GPB_NCCL = 10,
+  GPB_NO_MEMORY = 11
+} gpb_status;
+
+typedef struct gpb_ctx gpb_ctx;     /* a started runtime */
+typedef struct gpb_model gpb_model; /* a GP model bound to a runtime */
+
+/* ---- runtime lifecycle: start_runtime / stop_runtime (runtime.py:369-403) */
+int gpb_init(int device, gpb_ctx** out);      /* GPB_ALREADY_RUNNING if live */
+int gpb_finalize(gpb_ctx* ctx);               /* GPB_NOT_RUNNING if not live */
+gpb_ctx* gpb_current(void);                   /* current_runtime(), or NULL */
+const char* gpb_last_error(void);
+int gpb_abi_version(void);
+
+/* ---- model: GPModel(train, params, tiles_per_dim) (model.py:111-131) ------
+ * z: n x d, y: n.  GPB_TILING unless 1 <= tiles_per_dim and it divides n. */
+int gpb_model_create(gpb_ctx* ctx, const double* z, const double* y, int64_t n, int64_t d,
+                     int64_t tiles_per_dim, gpb_model** out);
+/* same, z and y already in device memory of ctx's GPU */
+int gpb_model_create_device(gpb_ctx* ctx, const double* z_dev, const double* y_dev, int64_t n,
+                            int64_t d, int64_t tiles_per_dim, gpb_model** out);
+int gpb_model_destroy(gpb_model* m);
+/* train setter (model.py:139-147): re-uploads, invalidates the factor */
+int gpb_model_set_train(gpb_model* m, const double* z, const double* y, int64_t n, int64_t d);
+/* params setter (model.py:153-156): (lengthscale, vertical_scale,
+ * noise_variance) + trainable flags; invalidates factor, beta, alpha.
+ * GPB_INVALID_CONFIG if l <= 0, nu <= 0 or s2 < 0 (covariance.py:50-62). */
+int gpb_model_set_params(gpb_model* m, double lengthscale, double vertical_scale,
+                         double noise_variance, const uint8_t trainable[3]);
+int gpb_model_get_params(gpb_model* m, double out[3]);
+
+/* ---- hot path ------------------------------------------------------------
+ * gpb_cholesky: assemble K + tiled Cholesky (model.py:169-177), cached.
+ *   L_out (n x n, lower, upper = 0) may be NULL.  GPB_NOT_PD on failure,
+ *   with gpb_last_pivot giving the first failing index; the cache is
+ *   invalidated (model.py:210-217). */
+int gpb_cholesky(gpb_model* m, double* L_out);
+int gpb_last_pivot(gpb_model* m, int64_t* pivot);
+/* log marginal likelihood (model.py:316-339); compute_loss = -this */
+int gpb_log_likelihood(gpb_model* m, double* out);
+/* dNLL/d(l, nu, s2) (model.py:341-435); zeros for non-trainable */
+int gpb_loss_gradients(gpb_model* m, double out[3]);
+/* Adam on log-parameters (model.py:437-485). history: iterations NLLs.
+ * On GPB_NOT_PD the message is prefixed "iteration k: ". */
+int gpb_optimize(gpb_model* m, double learning_rate, double beta1, double beta2,
+                 double epsilon, int64_t iterations, double* history);
+/* predict / predict_variance / predict_with_full_cov (model.py:221-314).
+ * zt: m x d.  mean (m) required; var (m) and cov (m x m) optional.
+ * Variances are clamped like _clamp_variances (model.py:488-496):
+ * GPB_NUMERIC if any < -1e-9.  GPB_DIM on a feature-count mismatch. */
+int gpb_predict(gpb_model* m, const double* zt, int64_t mt, int64_t d, double* mean,
+                double* var, double* cov);
+/* same with zt, mean, var in device memory (no clamp check; raw values) */
+int gpb_predict_device(gpb_model* m, const double* zt_dev, int64_t mt, int64_t d,
+                       double* mean_dev, double* var_dev);
+
+/* per-phase device times (ms, CUDA events on the model stream) of the last
+ * calls: [0] assembly, [1] factorisation, [2] alpha solves, [3] predict
+ * cross+mean, [4] predict TRSM+variance, [5] gradient, [6] full-cov SYRK */
+int gpb_model_timings(gpb_model* m, double* ms_out, int n);
+/* launches of this library's kernels since the model was created */
+int gpb_model_launch_count(gpb_model* m, int64_t* out);
+
+/* ---- tile-kernel plugin (tiles.py:23-46, 132-164) -------------------------
+ * Host buffers, fresh outputs, inputs never mutated.  Square tiles b x b;
+ * trsm solves X l^T = b_in for rows x b b_in. */
+int gpb_tile_potrf(gpb_ctx* ctx, const double* a, int64_t b, double* out);
+int gpb_tile_trsm(gpb_ctx* ctx, const double* l, const double* b_in, int64_t rows, int64_t b,
+                  double* out);
+int gpb_tile_syrk(gpb_ctx* ctx, const double* a, const double* c, int64_t b, int64_t k,
+                  double* out);
+int gpb_tile_gemm(gpb_ctx* ctx, const double* a, const double* bm, const double* c, int64_t m,
+                  int64_t n, int64_t k, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPB200_H */

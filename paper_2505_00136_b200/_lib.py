@@ -1,0 +1,119 @@
+"""ctypes binding of the C ABI in ``include/gpb200.h`` (libgpb200.so).
+
+The shared library is built in-tree (``make`` or ``__graft_entry__.build()``)
+and loaded from this package directory.  There is no fallback: if the
+library is missing, every entry point raises ``ExtensionMissing``.
+ctypes releases the GIL for the duration of each foreign call, so device
+work never holds the interpreter lock (the reference blocks its caller in
+``run_as_root``, runtime.py:250-262, with the same effect).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from . import errors
+
+LIB_NAME = "libgpb200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+_lock = threading.Lock()
+_lib = None
+
+_c_double_p = ctypes.POINTER(ctypes.c_double)
+_c_i64_p = ctypes.POINTER(ctypes.c_int64)
+_vp = ctypes.c_void_p
+
+# name -> (restype, argtypes); mirrors include/gpb200.h exactly
+SIGNATURES = {
+    "gpb_abi_version": (ctypes.c_int, []),
+    "gpb_init": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_vp)]),
+    "gpb_finalize": (ctypes.c_int, [_vp]),
+    "gpb_current": (_vp, []),
+    "gpb_last_error": (ctypes.c_char_p, []),
+    "gpb_model_create": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, ctypes.c_int64,
+                                        ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(_vp)]),
+    "gpb_model_create_device": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64,
+                                               ctypes.c_int64, ctypes.POINTER(_vp)]),
+    "gpb_model_destroy": (ctypes.c_int, [_vp]),
+    "gpb_model_set_train": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, ctypes.c_int64,
+                                           ctypes.c_int64]),
+    "gpb_model_set_params": (ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_double,
+                                            ctypes.c_double, ctypes.POINTER(ctypes.c_uint8)]),
+    "gpb_model_get_params": (ctypes.c_int, [_vp, _c_double_p]),
+    "gpb_cholesky": (ctypes.c_int, [_vp, _c_double_p]),
+    "gpb_last_pivot": (ctypes.c_int, [_vp, _c_i64_p]),
+    "gpb_log_likelihood": (ctypes.c_int, [_vp, _c_double_p]),
+    "gpb_loss_gradients": (ctypes.c_int, [_vp, _c_double_p]),
+    "gpb_optimize": (ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                    ctypes.c_double, ctypes.c_int64, _c_double_p]),
+    "gpb_predict": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_int64, ctypes.c_int64,
+                                   _c_double_p, _c_double_p, _c_double_p]),
+    "gpb_predict_device": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int64, _vp, _vp]),
+    "gpb_model_timings": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_int]),
+    "gpb_model_launch_count": (ctypes.c_int, [_vp, _c_i64_p]),
+    "gpb_tile_potrf": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_int64, _c_double_p]),
+    "gpb_tile_trsm": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, ctypes.c_int64,
+                                     ctypes.c_int64, _c_double_p]),
+    "gpb_tile_syrk": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, ctypes.c_int64,
+                                     ctypes.c_int64, _c_double_p]),
+    "gpb_tile_gemm": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, _c_double_p,
+                                     ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                     _c_double_p]),
+}
+
+_STATUS = {
+    1: errors.InvalidConfig,
+    2: errors.AlreadyRunning,
+    3: errors.NotRunning,
+    4: errors.TilingError,
+    5: errors.DimensionMismatch,
+    6: errors.NotPositiveDefinite,
+    7: errors.SingularTriangular,
+    8: errors.NumericalConsistencyError,
+    9: errors.DeviceError,
+    10: errors.DeviceError,
+    11: errors.DeviceError,
+}
+
+
+class ExtensionMissing(ImportError):
+    """libgpb200.so is not built; there is deliberately no CPU fallback."""
+
+
+def load():
+    """Load (once) and return the CDLL with all signatures declared."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ExtensionMissing(
+                f"{LIB_PATH} is missing: build it with `make` or "
+                "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)"
+            )
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def check(status: int) -> None:
+    """Raise the reference-equivalent exception for a non-zero gpb_status."""
+    if status == 0:
+        return
+    msg = load().gpb_last_error()
+    msg = msg.decode("utf-8", "replace") if msg else f"gpb status {status}"
+    raise _STATUS.get(status, errors.TaskGPError)(msg)
+
+
+def dptr(a):
+    """double* of a C-contiguous float64 ndarray (None -> NULL)."""
+    if a is None:
+        return None
+    return a.ctypes.data_as(_c_double_p)

@@ -1,0 +1,53 @@
+// Grouped FP64 tensor-core GEMM (DMMA.8x8x4) for the tiled-GP hot path.
+//
+// One launch executes a list of independent tile jobs ("grouped GEMM"): the
+// Cholesky trailing update of one step (taskgp tiles.py:41-46 SYRK/GEMM over
+// every trailing tile), the panel TRSM as a product with the inverted
+// diagonal tile, the prediction TRSM sweeps (tiled.py:263-298), the inverse
+// factor (model.py:358-361), K^-1 = X^T X (model.py:362-380) and the full
+// posterior covariance (model.py:258-269).
+//
+//   Cout[job] = alpha * A[job] * B[job]^T + beta * Cin[job]
+//
+// A is M x K, B is N x K (so the product is "NT"); each operand is either
+// K-MAJOR (k contiguous: element (m,k) at base[m*ld + k]) or MN-MAJOR (m
+// contiguous: element (m,k) at base[k*ld + m]).  A K-MAJOR operand may be
+// "tiled in k": element (m,k) at base[(k/ktile)*kstride + m*ld + k%ktile],
+// which walks a row panel of packed lower tiles without a copy.
+#pragma once
+#include "common.cuh"
+
+namespace gpb {
+
+constexpr int GBM = 128, GBN = 128, GBK = 16, GSTAGES = 4, GTHREADS = 256;
+
+enum GemmEpi : int { EPI_AXPBY = 0, EPI_SUMSQ = 1 };
+
+struct __align__(16) GemmJob {
+  const double* A;
+  const double* B;
+  const double* Cin;   // may alias Cout (in-place update) or be null if beta == 0
+  double* Cout;
+  double* aux;         // EPI_SUMSQ: base of this job's partial rows
+  int K;               // multiple of GBK, may be 0
+  int lower;           // 1: skip blocks above the block diagonal (diagonal tiles)
+  int64_t pad_;
+};
+
+struct GemmParams {
+  const GemmJob* jobs;
+  int njobs;
+  int mblk, nblk;            // BM x BN blocks per job
+  int64_t lda, ldb, ldc;
+  int64_t a_ktile, a_kstride;  // K-MAJOR tiled-k walk (ktile = 1<<30 for plain)
+  int64_t b_ktile, b_kstride;
+  double alpha, beta;
+  int64_t aux_ld;            // EPI_SUMSQ: stride between 128-row partial rows
+};
+
+// Host launcher (gemm.cu).  a_kmajor / b_kmajor choose operand layouts.
+cudaError_t launch_gemm(const GemmParams& p, bool a_kmajor, bool b_kmajor, int epi,
+                        cudaStream_t stream);
+cudaError_t gemm_init_attributes();
+
+}  // namespace gpb

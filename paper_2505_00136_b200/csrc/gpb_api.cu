@@ -1,0 +1,955 @@
+// Host runtime + C ABI (include/gpb200.h) of the B200 tiled-GP hot path.
+//
+// This is the native replacement of the reference's model layer
+// (taskgp model.py:91-485) and its task runtime (runtime.py): instead of
+// a Python work-stealing DAG of per-tile tasks, each algorithmic step is one
+// grouped launch on a CUDA stream, and whole phases run without host
+// round-trips.  Plans (the per-step GEMM job lists) are built once per model
+// shape and kept resident in HBM.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "gemm.cuh"
+#include "gpb200.h"
+#include "kernels.cuh"
+
+using namespace gpb;
+
+namespace {
+
+thread_local std::string g_err;
+std::mutex g_mu;
+gpb_ctx* g_ctx = nullptr;
+uint64_t g_gen = 0;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                 \
+  do {                                                                              \
+    cudaError_t e_ = (x);                                                           \
+    if (e_ != cudaSuccess) {                                                        \
+      return fail(e_ == cudaErrorMemoryAllocation ? GPB_NO_MEMORY : GPB_CUDA,       \
+                  std::string(#x) + ": " + cudaGetErrorString(e_));                 \
+    }                                                                               \
+  } while (0)
+
+#define GPB_TRY(x)                \
+  do {                            \
+    int s_ = (x);                 \
+    if (s_ != GPB_OK) return s_;  \
+  } while (0)
+
+constexpr double kHalfLog2Pi = 0.91893853320467274178;  // 0.5 * log(2 pi), model.py:35
+constexpr double kVarianceSlack = 1e-9;                  // model.py:33
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+  cudaError_t ensure(size_t nbytes) {
+    if (nbytes <= bytes && p) return cudaSuccess;
+    release();
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(nbytes, 16));
+    if (e == cudaSuccess) bytes = nbytes;
+    else p = nullptr;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct gpb_ctx {
+  int device = 0;
+  uint64_t gen = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex tile_mu;  // tile plugin calls share scratch
+};
+
+struct gpb_model {
+  gpb_ctx* ctx = nullptr;
+  uint64_t gen = 0;
+  int64_t n = 0, d = 0, T = 0;
+  int b = 0, bp = 0, bi = 0, Ti = 0;
+  int64_t np_ = 0;
+  PadMap pm{};
+  double l = 1.0, nu = 1.0, s2 = 0.1;
+  uint8_t trainable[3] = {1, 1, 1};
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+
+  DevBuf zp, yp, L, Dinv, scratch, logdiag, info, yhat, beta, alpha, bhat, red, tile_rm, tile_cm,
+      chol_jobs;
+  std::vector<int64_t> trsm_off, trsm_cnt, upd_off, upd_cnt;
+  bool plan_ok = false, factor_ok = false, weights_ok = false;
+  int64_t last_pivot = -1;
+
+  // gradient
+  DevBuf X, Kinv, Wg, part_l, part_v, part_x, inv_jobs;
+  std::vector<int64_t> invw_off, invx_off;
+  int64_t kinv_off = 0, kinv_cnt = 0;
+  bool inv_plan = false;
+
+  // prediction
+  DevBuf Bv, W, mpart, sq, pred_jobs, zt, mean, var, S, fc_jobs;
+  int64_t pred_mcp = -1, fc_mcp = -1;
+
+  double adam_m[3] = {0, 0, 0}, adam_v[3] = {0, 0, 0};
+  int64_t adam_step = 0;
+  double timing[8] = {0};
+  int64_t launches = 0;
+};
+
+namespace {
+
+int check_live(gpb_model* m) {
+  if (!m) return fail(GPB_INVALID_CONFIG, "null model");
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_ctx || g_ctx != m->ctx || g_ctx->gen != m->gen)
+    return fail(GPB_NOT_RUNNING, "the runtime this model was bound to is not running");
+  return GPB_OK;
+}
+
+int choose_internal_tile(int64_t n, int b, int* bp, int* bi) {
+  *bp = static_cast<int>(round_up(b, kTileAlign));
+  const char* env = getenv("GPB_TILE");
+  if (b % kTileAlign == 0) {
+    // no padding: the internal tile is a free parameter (results are
+    // tiling-invariant to round-off, test_acceptance.py:135-169)
+    int want = env ? atoi(env) : (n >= 4096 ? 512 : 256);
+    for (int c : {want, 512, 256, 128}) {
+      if (c > 0 && c % kTileAlign == 0 && n % c == 0) { *bi = c; *bp = b; return GPB_OK; }
+    }
+  }
+  for (int c : {512, 384, 256, 128}) {
+    if (*bp % c == 0) { *bi = c; return GPB_OK; }
+  }
+  *bi = kTileAlign;
+  return GPB_OK;
+}
+
+GemmParams base_params(const GemmJob* jobs, int njobs, int mblk, int nblk, int64_t lda,
+                       int64_t ldb, int64_t ldc, double alpha, double beta) {
+  GemmParams p{};
+  p.jobs = jobs;
+  p.njobs = njobs;
+  p.mblk = mblk;
+  p.nblk = nblk;
+  p.lda = lda;
+  p.ldb = ldb;
+  p.ldc = ldc;
+  p.a_ktile = p.b_ktile = int64_t(1) << 40;
+  p.a_kstride = p.b_kstride = 0;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.aux_ld = 0;
+  return p;
+}
+
+int gemm(gpb_model* m, const GemmParams& p, bool ak, bool bk, int epi) {
+  if (p.njobs == 0) return GPB_OK;
+  CUDA_TRY(launch_gemm(p, ak, bk, epi, m->st));
+  ++m->launches;
+  return GPB_OK;
+}
+
+int alloc_model_buffers(gpb_model* m) {
+  const int64_t bi2 = int64_t(m->bi) * m->bi;
+  const int64_t ntiles = int64_t(m->Ti) * (m->Ti + 1) / 2;
+  CUDA_TRY(m->zp.ensure(sizeof(double) * m->np_ * m->d));
+  CUDA_TRY(m->yp.ensure(sizeof(double) * m->np_));
+  CUDA_TRY(m->L.ensure(sizeof(double) * ntiles * bi2));
+  CUDA_TRY(m->Dinv.ensure(sizeof(double) * m->Ti * bi2));
+  CUDA_TRY(m->scratch.ensure(sizeof(double) * std::max<int64_t>(1, m->Ti - 1) * bi2));
+  CUDA_TRY(m->logdiag.ensure(sizeof(double) * m->Ti));
+  CUDA_TRY(m->info.ensure(sizeof(int) * 4));
+  for (DevBuf* v : {&m->yhat, &m->beta, &m->alpha, &m->bhat}) CUDA_TRY(v->ensure(sizeof(double) * m->np_));
+  CUDA_TRY(m->red.ensure(sizeof(double) * 16));
+  // tile tables
+  std::vector<int2> rm(ntiles), cm(ntiles);
+  for (int i = 0; i < m->Ti; ++i)
+    for (int j = 0; j <= i; ++j) {
+      rm[h_tri_rm(i, j)] = make_int2(i, j);
+      cm[h_tri_cm(i, j, m->Ti)] = make_int2(i, j);
+    }
+  CUDA_TRY(m->tile_rm.ensure(sizeof(int2) * ntiles));
+  CUDA_TRY(m->tile_cm.ensure(sizeof(int2) * ntiles));
+  CUDA_TRY(cudaMemcpy(m->tile_rm.p, rm.data(), sizeof(int2) * ntiles, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(m->tile_cm.p, cm.data(), sizeof(int2) * ntiles, cudaMemcpyHostToDevice));
+  return GPB_OK;
+}
+
+// Cholesky plan: per step k, TRSM jobs (panel tiles) and trailing-update jobs.
+int build_chol_plan(gpb_model* m) {
+  const int Ti = m->Ti;
+  const int64_t bi2 = int64_t(m->bi) * m->bi;
+  double* L = m->L.as<double>();
+  double* D = m->Dinv.as<double>();
+  double* S = m->scratch.as<double>();
+  std::vector<GemmJob> jobs;
+  m->trsm_off.assign(Ti, 0);
+  m->trsm_cnt.assign(Ti, 0);
+  m->upd_off.assign(Ti, 0);
+  m->upd_cnt.assign(Ti, 0);
+  for (int k = 0; k < Ti; ++k) {
+    m->trsm_off[k] = jobs.size();
+    for (int i = k + 1; i < Ti; ++i) {
+      GemmJob j{};
+      j.A = L + h_tri_rm(i, k) * bi2;
+      j.B = D + int64_t(k) * bi2;
+      j.Cout = S + int64_t(i - k - 1) * bi2;
+      j.K = m->bi;
+      jobs.push_back(j);
+    }
+    m->trsm_cnt[k] = jobs.size() - m->trsm_off[k];
+    m->upd_off[k] = jobs.size();
+    for (int i = k + 1; i < Ti; ++i)
+      for (int jj = k + 1; jj <= i; ++jj) {
+        GemmJob j{};
+        j.A = S + int64_t(i - k - 1) * bi2;
+        j.B = S + int64_t(jj - k - 1) * bi2;
+        j.Cin = j.Cout = L + h_tri_rm(i, jj) * bi2;
+        j.K = m->bi;
+        j.lower = (i == jj);
+        jobs.push_back(j);
+      }
+    m->upd_cnt[k] = jobs.size() - m->upd_off[k];
+  }
+  CUDA_TRY(m->chol_jobs.ensure(sizeof(GemmJob) * std::max<size_t>(1, jobs.size())));
+  if (!jobs.empty())
+    CUDA_TRY(cudaMemcpy(m->chol_jobs.p, jobs.data(), sizeof(GemmJob) * jobs.size(),
+                        cudaMemcpyHostToDevice));
+  m->plan_ok = true;
+  return GPB_OK;
+}
+
+SekParams sek_params(const gpb_model* m) {
+  SekParams sp;
+  sp.lengthscale = m->l;
+  sp.vertical = m->nu;
+  sp.noise = m->s2;
+  sp.neg_half_inv_l2 = -1.0 / (2.0 * (m->l * m->l));
+  return sp;
+}
+
+int upload_train(gpb_model* m, const double* z, const double* y, bool device_ptrs) {
+  // stage dense z, y on device, then scatter into the padded layout
+  DevBuf zd, yd;
+  const double* zsrc = z;
+  const double* ysrc = y;
+  if (!device_ptrs) {
+    CUDA_TRY(zd.ensure(sizeof(double) * m->n * m->d));
+    CUDA_TRY(yd.ensure(sizeof(double) * m->n));
+    CUDA_TRY(cudaMemcpyAsync(zd.p, z, sizeof(double) * m->n * m->d, cudaMemcpyHostToDevice, m->st));
+    CUDA_TRY(cudaMemcpyAsync(yd.p, y, sizeof(double) * m->n, cudaMemcpyHostToDevice, m->st));
+    zsrc = zd.as<double>();
+    ysrc = yd.as<double>();
+  }
+  CUDA_TRY(launch_pad_rows(zsrc, m->zp.as<double>(), m->np_, static_cast<int>(m->d), m->pm, m->st));
+  CUDA_TRY(launch_pad_vector(ysrc, m->yp.as<double>(), m->np_, m->pm, m->st));
+  m->launches += 2;
+  CUDA_TRY(cudaStreamSynchronize(m->st));
+  zd.release();
+  yd.release();
+  return GPB_OK;
+}
+
+void invalidate(gpb_model* m) {
+  m->factor_ok = false;
+  m->weights_ok = false;
+}
+
+struct PhaseTimer {
+  gpb_model* m;
+  int slot;
+  PhaseTimer(gpb_model* mm, int s) : m(mm), slot(s) { cudaEventRecord(m->e0, m->st); }
+  int stop() {
+    cudaEventRecord(m->e1, m->st);
+    CUDA_TRY(cudaEventSynchronize(m->e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, m->e0, m->e1);
+    m->timing[slot] = ms;
+    return GPB_OK;
+  }
+};
+
+// assemble + factor (model.py:169-177 _ensure_factor)
+int ensure_factor(gpb_model* m) {
+  if (m->factor_ok) return GPB_OK;
+  if (!m->plan_ok) GPB_TRY(build_chol_plan(m));
+  const int Ti = m->Ti, bi = m->bi;
+  const int64_t bi2 = int64_t(bi) * bi;
+  const int64_t ntiles = int64_t(Ti) * (Ti + 1) / 2;
+  double* L = m->L.as<double>();
+  double* D = m->Dinv.as<double>();
+  {
+    PhaseTimer pt(m, 0);
+    CUDA_TRY(launch_assemble_lower(L, m->tile_rm.as<int2>(), 0, ntiles, m->zp.as<double>(),
+                                   static_cast<int>(m->d), bi, m->pm, sek_params(m), true, m->st));
+    ++m->launches;
+    GPB_TRY(pt.stop());
+  }
+  if (getenv("GPB_DEBUG_ASSEMBLY_ONLY")) {  // debugging aid: leave K in the tiles
+    m->factor_ok = true;
+    return GPB_OK;
+  }
+  PhaseTimer pt(m, 1);
+  CUDA_TRY(cudaMemsetAsync(m->info.p, 0xff, sizeof(int), m->st));
+  const GemmJob* jobs = m->chol_jobs.as<GemmJob>();
+  const int nb = bi / GBM;
+  for (int k = 0; k < Ti; ++k) {
+    PotrfArgs a{};
+    a.tile = L + h_tri_rm(k, k) * bi2;
+    a.dinv = D + int64_t(k) * bi2;
+    a.logdiag = m->logdiag.as<double>();
+    a.info = m->info.as<int>();
+    a.bi = bi;
+    a.tile_index = k;
+    a.tile_off = k * bi;
+    a.bp_user = m->pm.bp_user;
+    a.b_user = m->pm.b_user;
+    CUDA_TRY(launch_potrf(a, m->st));
+    ++m->launches;
+    if (k + 1 < Ti) {
+      GemmParams tp = base_params(jobs + m->trsm_off[k], static_cast<int>(m->trsm_cnt[k]), nb, nb,
+                                  bi, bi, bi, 1.0, 0.0);
+      GPB_TRY(gemm(m, tp, true, true, EPI_AXPBY));
+      GemmParams up = base_params(jobs + m->upd_off[k], static_cast<int>(m->upd_cnt[k]), nb, nb,
+                                  bi, bi, bi, -1.0, 1.0);
+      GPB_TRY(gemm(m, up, true, true, EPI_AXPBY));
+      CUDA_TRY(launch_copy_panel(L, m->scratch.as<double>(), Ti, k, bi, m->st));
+      ++m->launches;
+    }
+  }
+  GPB_TRY(pt.stop());
+  int info = -1;
+  CUDA_TRY(cudaMemcpy(&info, m->info.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (info >= 0) {
+    m->last_pivot = info;
+    invalidate(m);
+    char buf[160];
+    snprintf(buf, sizeof(buf), "Matrix is not positive definite (non-positive pivot at index %d)",
+             info);
+    return fail(GPB_NOT_PD, buf);
+  }
+  m->last_pivot = -1;
+  m->factor_ok = true;
+  m->weights_ok = false;
+  return GPB_OK;
+}
+
+// beta = L^-1 y, alpha = L^-T beta (model.py:179-186)
+int ensure_weights(gpb_model* m) {
+  GPB_TRY(ensure_factor(m));
+  if (m->weights_ok) return GPB_OK;
+  const int Ti = m->Ti, bi = m->bi;
+  const int64_t bi2 = int64_t(bi) * bi;
+  double* L = m->L.as<double>();
+  double* D = m->Dinv.as<double>();
+  double* yhat = m->yhat.as<double>();
+  double* beta = m->beta.as<double>();
+  double* alpha = m->alpha.as<double>();
+  double* bhat = m->bhat.as<double>();
+  PhaseTimer pt(m, 2);
+  CUDA_TRY(cudaMemcpyAsync(yhat, m->yp.p, sizeof(double) * m->np_, cudaMemcpyDeviceToDevice, m->st));
+  for (int i = 0; i < Ti; ++i) {
+    CUDA_TRY(launch_fwd_diag(D + i * bi2, yhat + int64_t(i) * bi, beta + int64_t(i) * bi, bi, m->st));
+    CUDA_TRY(launch_fwd_update(L, Ti, i, bi, beta + int64_t(i) * bi, yhat, m->st));
+    m->launches += 2;
+  }
+  CUDA_TRY(cudaMemcpyAsync(bhat, beta, sizeof(double) * m->np_, cudaMemcpyDeviceToDevice, m->st));
+  for (int i = Ti - 1; i >= 0; --i) {
+    CUDA_TRY(launch_bwd_diag(D + i * bi2, bhat + int64_t(i) * bi, alpha + int64_t(i) * bi, bi, m->st));
+    CUDA_TRY(launch_bwd_update(L, i, bi, alpha + int64_t(i) * bi, bhat, m->st));
+    m->launches += 2;
+  }
+  GPB_TRY(pt.stop());
+  m->weights_ok = true;
+  return GPB_OK;
+}
+
+int log_likelihood(gpb_model* m, double* out) {
+  GPB_TRY(ensure_weights(m));
+  CUDA_TRY(launch_loss_terms(m->logdiag.as<double>(), m->Ti, m->beta.as<double>(), m->np_,
+                             m->red.as<double>(), m->st));
+  ++m->launches;
+  double h[2];
+  CUDA_TRY(cudaMemcpyAsync(h, m->red.p, sizeof(h), cudaMemcpyDeviceToHost, m->st));
+  CUDA_TRY(cudaStreamSynchronize(m->st));
+  // model.py:335-337
+  *out = -h[0] - 0.5 * h[1] - double(m->n) * kHalfLog2Pi;
+  return GPB_OK;
+}
+
+// ---- gradient (model.py:341-435) ------------------------------------------
+int build_inv_plan(gpb_model* m) {
+  const int Ti = m->Ti;
+  const int64_t bi2 = int64_t(m->bi) * m->bi;
+  const int64_t ntiles = int64_t(Ti) * (Ti + 1) / 2;
+  CUDA_TRY(m->X.ensure(sizeof(double) * ntiles * bi2));
+  CUDA_TRY(m->Kinv.ensure(sizeof(double) * ntiles * bi2));
+  CUDA_TRY(m->Wg.ensure(sizeof(double) * std::max(1, Ti - 1) * bi2));
+  const int64_t nblk = ntiles * (m->bi / 64) * (m->bi / 64);
+  CUDA_TRY(m->part_l.ensure(sizeof(double) * nblk));
+  CUDA_TRY(m->part_v.ensure(sizeof(double) * nblk));
+  CUDA_TRY(m->part_x.ensure(sizeof(double) * nblk));
+  double* L = m->L.as<double>();
+  double* D = m->Dinv.as<double>();
+  double* X = m->X.as<double>();
+  double* Kv = m->Kinv.as<double>();
+  double* Wg = m->Wg.as<double>();
+  std::vector<GemmJob> jobs;
+  m->invw_off.assign(Ti + 1, 0);
+  m->invx_off.assign(Ti + 1, 0);
+  for (int i = 1; i < Ti; ++i) {
+    m->invw_off[i] = jobs.size();
+    for (int j = 0; j < i; ++j) {  // W_j = L[i, j..i) X[j..i, j]
+      GemmJob g{};
+      g.A = L + h_tri_rm(i, j) * bi2;
+      g.B = X + h_tri_cm(j, j, Ti) * bi2;
+      g.Cout = Wg + int64_t(j) * bi2;
+      g.K = (i - j) * m->bi;
+      jobs.push_back(g);
+    }
+    m->invx_off[i] = jobs.size();
+    for (int j = 0; j < i; ++j) {  // X[i, j] = -Dinv_i W_j
+      GemmJob g{};
+      g.A = D + int64_t(i) * bi2;
+      g.B = Wg + int64_t(j) * bi2;
+      g.Cout = X + h_tri_cm(i, j, Ti) * bi2;
+      g.K = m->bi;
+      jobs.push_back(g);
+    }
+  }
+  m->kinv_off = jobs.size();
+  for (int r = 0; r < Ti; ++r)  // longest K first
+    for (int c = 0; c <= r; ++c) {
+      GemmJob g{};
+      g.A = X + h_tri_cm(r, r, Ti) * bi2;
+      g.B = X + h_tri_cm(r, c, Ti) * bi2;
+      g.Cout = Kv + h_tri_cm(r, c, Ti) * bi2;
+      g.K = (Ti - r) * m->bi;
+      jobs.push_back(g);
+    }
+  m->kinv_cnt = jobs.size() - m->kinv_off;
+  CUDA_TRY(m->inv_jobs.ensure(sizeof(GemmJob) * jobs.size()));
+  CUDA_TRY(cudaMemcpy(m->inv_jobs.p, jobs.data(), sizeof(GemmJob) * jobs.size(),
+                      cudaMemcpyHostToDevice));
+  m->inv_plan = true;
+  return GPB_OK;
+}
+
+int loss_gradients(gpb_model* m, double out[3]) {
+  const bool tl = m->trainable[0], tv = m->trainable[1], tn = m->trainable[2];
+  out[0] = out[1] = out[2] = 0.0;
+  if (!(tl || tv || tn)) return GPB_OK;  // model.py:350-352
+  GPB_TRY(ensure_weights(m));
+  if (!m->inv_plan) GPB_TRY(build_inv_plan(m));
+  const int Ti = m->Ti, bi = m->bi, nb = bi / GBM;
+  const int64_t bi2 = int64_t(bi) * bi;
+  const int64_t ntiles = int64_t(Ti) * (Ti + 1) / 2;
+  double* X = m->X.as<double>();
+  double* D = m->Dinv.as<double>();
+  const GemmJob* jobs = m->inv_jobs.as<GemmJob>();
+  PhaseTimer pt(m, 5);
+  // X = L^-1 (tiled.py:263-298 with the identity RHS, model.py:358-361)
+  for (int i = 0; i < Ti; ++i)
+    CUDA_TRY(cudaMemcpyAsync(X + h_tri_cm(i, i, Ti) * bi2, D + int64_t(i) * bi2,
+                             sizeof(double) * bi2, cudaMemcpyDeviceToDevice, m->st));
+  for (int i = 1; i < Ti; ++i) {
+    GemmParams w = base_params(jobs + m->invw_off[i], i, nb, nb, bi, bi, bi, 1.0, 0.0);
+    w.a_ktile = bi;
+    w.a_kstride = bi2;
+    GPB_TRY(gemm(m, w, true, false, EPI_AXPBY));
+    GemmParams x = base_params(jobs + m->invx_off[i], i, nb, nb, bi, bi, bi, -1.0, 0.0);
+    GPB_TRY(gemm(m, x, true, false, EPI_AXPBY));
+  }
+
+  double* red = m->red.as<double>();
+  const int64_t nblk = ntiles * (bi / 64) * (bi / 64);
+  if (tl || tv) {
+    // K^-1 = X^T X, lower tiles (model.py:362-380)
+    GemmParams kp = base_params(jobs + m->kinv_off, static_cast<int>(m->kinv_cnt), nb, nb, bi, bi,
+                                bi, 1.0, 0.0);
+    GPB_TRY(gemm(m, kp, false, false, EPI_AXPBY));
+    // fused trace pass (model.py:382-414 with covariance.py:196-220 regenerated)
+    CUDA_TRY(launch_trace(m->Kinv.as<double>(), m->tile_cm.as<int2>(), ntiles, Ti, m->zp.as<double>(),
+                          m->alpha.as<double>(), static_cast<int>(m->d), bi, m->pm, sek_params(m),
+                          m->part_l.as<double>(), m->part_v.as<double>(), m->st));
+    CUDA_TRY(launch_reduce(m->part_l.as<double>(), nblk, red + 0, m->st));
+    CUDA_TRY(launch_reduce(m->part_v.as<double>(), nblk, red + 1, m->st));
+    m->launches += 3;
+  }
+  if (tn) {
+    // ||L^-1||_F^2 and ||alpha||^2 (model.py:415-432)
+    CUDA_TRY(launch_tiles_sumsq(X, m->tile_cm.as<int2>(), ntiles, bi, m->pm, m->part_x.as<double>(),
+                                m->st));
+    CUDA_TRY(launch_reduce(m->part_x.as<double>(), nblk, red + 2, m->st));
+    CUDA_TRY(launch_loss_terms(nullptr, 0, m->alpha.as<double>(), m->np_, red + 4, m->st));
+    m->launches += 3;
+  }
+  double hh[6] = {0, 0, 0, 0, 0, 0};
+  CUDA_TRY(cudaMemcpyAsync(hh, red, sizeof(hh), cudaMemcpyDeviceToHost, m->st));
+  CUDA_TRY(cudaStreamSynchronize(m->st));
+  GPB_TRY(pt.stop());
+
+  if (tl) out[0] = 0.5 * (m->nu / (m->l * m->l * m->l)) * hh[0];
+  if (tv) out[1] = 0.5 * hh[1];
+  if (tn) out[2] = 0.5 * (hh[2] - hh[4]);
+  return GPB_OK;
+}
+
+// ---- prediction (model.py:221-314) ----------------------------------------
+int build_pred_plan(gpb_model* m, int64_t mcp) {
+  if (m->pred_mcp == mcp) return GPB_OK;
+  const int Ti = m->Ti, bi = m->bi;
+  const int64_t bi2 = int64_t(bi) * bi;
+  CUDA_TRY(m->Bv.ensure(sizeof(double) * m->np_ * mcp));
+  CUDA_TRY(m->W.ensure(sizeof(double) * int64_t(bi) * mcp));
+  CUDA_TRY(m->mpart.ensure(sizeof(double) * (m->np_ / 64) * mcp));
+  CUDA_TRY(m->sq.ensure(sizeof(double) * (m->np_ / GBM) * mcp));
+  CUDA_TRY(m->mean.ensure(sizeof(double) * mcp));
+  CUDA_TRY(m->var.ensure(sizeof(double) * mcp));
+  double* L = m->L.as<double>();
+  double* D = m->Dinv.as<double>();
+  double* Bv = m->Bv.as<double>();
+  std::vector<GemmJob> jobs;
+  for (int i = 0; i < Ti; ++i) {
+    GemmJob w{};  // W = B_i - L[i, 0..i) V[0..i)
+    w.A = L + h_tri_rm(i, 0) * bi2;
+    w.B = Bv;
+    w.Cin = Bv + int64_t(i) * bi * mcp;
+    w.Cout = m->W.as<double>();
+    w.K = i * bi;
+    jobs.push_back(w);
+    GemmJob v{};  // V_i = Dinv_i W  (+ column sum of squares)
+    v.A = D + int64_t(i) * bi2;
+    v.B = m->W.as<double>();
+    v.Cout = Bv + int64_t(i) * bi * mcp;
+    v.aux = m->sq.as<double>() + (int64_t(i) * bi / GBM) * mcp;
+    v.K = bi;
+    jobs.push_back(v);
+  }
+  CUDA_TRY(m->pred_jobs.ensure(sizeof(GemmJob) * jobs.size()));
+  CUDA_TRY(cudaMemcpy(m->pred_jobs.p, jobs.data(), sizeof(GemmJob) * jobs.size(),
+                      cudaMemcpyHostToDevice));
+  m->pred_mcp = mcp;
+  return GPB_OK;
+}
+
+// zt_dev: mt x d on device. Results (mean, var) left in m->mean / m->var (length mt).
+int predict_core(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var) {
+  GPB_TRY(ensure_weights(m));
+  const int Ti = m->Ti, bi = m->bi;
+  const int64_t mcp = round_up(std::max<int64_t>(mt, 1), GBM);
+  GPB_TRY(build_pred_plan(m, mcp));
+  double* Bv = m->Bv.as<double>();
+  const SekParams sp = sek_params(m);
+  {
+    PhaseTimer pt(m, 3);
+    CUDA_TRY(launch_cross(Bv, mcp, m->mpart.as<double>(), m->alpha.as<double>(), m->zp.as<double>(),
+                          m->np_, zt_dev, mt, mcp, static_cast<int>(m->d), m->pm, sp, m->st));
+    ++m->launches;
+    GPB_TRY(pt.stop());
+  }
+  if (want_var) {
+    PhaseTimer pt(m, 4);
+    const GemmJob* jobs = m->pred_jobs.as<GemmJob>();
+    for (int i = 0; i < Ti; ++i) {
+      GemmParams w = base_params(jobs + 2 * i, 1, bi / GBM, static_cast<int>(mcp / GBN), bi, mcp,
+                                 mcp, -1.0, 1.0);
+      w.a_ktile = bi;
+      w.a_kstride = int64_t(bi) * bi;
+      GPB_TRY(gemm(m, w, true, false, EPI_AXPBY));
+      GemmParams v = base_params(jobs + 2 * i + 1, 1, bi / GBM, static_cast<int>(mcp / GBN), bi,
+                                 mcp, mcp, 1.0, 0.0);
+      v.aux_ld = mcp;
+      GPB_TRY(gemm(m, v, true, false, EPI_SUMSQ));
+    }
+    GPB_TRY(pt.stop());
+  }
+  CUDA_TRY(launch_pred_finalize(m->mpart.as<double>(), m->np_ / 64, m->sq.as<double>(),
+                                m->np_ / GBM, mcp, mt, m->nu, m->mean.as<double>(),
+                                want_var ? m->var.as<double>() : nullptr, m->st));
+  ++m->launches;
+  return GPB_OK;
+}
+
+int full_cov(gpb_model* m, const double* zt_dev, int64_t mt, double* cov_host) {
+  const int64_t mcp = m->pred_mcp;
+  const int64_t nbk = mcp / GBM;
+  CUDA_TRY(m->S.ensure(sizeof(double) * mcp * mcp));
+  double* S = m->S.as<double>();
+  double* Bv = m->Bv.as<double>();
+  if (m->fc_mcp != mcp) {
+    std::vector<GemmJob> jobs;
+    for (int64_t r = 0; r < nbk; ++r)
+      for (int64_t c = 0; c <= r; ++c) {
+        GemmJob g{};
+        g.A = Bv + r * GBM;
+        g.B = Bv + c * GBM;
+        g.Cin = g.Cout = S + r * GBM * mcp + c * GBM;
+        g.K = static_cast<int>(m->np_);
+        jobs.push_back(g);
+      }
+    CUDA_TRY(m->fc_jobs.ensure(sizeof(GemmJob) * jobs.size()));
+    CUDA_TRY(cudaMemcpy(m->fc_jobs.p, jobs.data(), sizeof(GemmJob) * jobs.size(),
+                        cudaMemcpyHostToDevice));
+    m->fc_mcp = mcp;
+  }
+  PhaseTimer pt(m, 6);
+  CUDA_TRY(launch_prior(S, mcp, zt_dev, mt, static_cast<int>(m->d), sek_params(m), m->st));
+  ++m->launches;
+  // Sigma = K** - V^T V (model.py:254-269), lower blocks
+  GemmParams p = base_params(m->fc_jobs.as<GemmJob>(), static_cast<int>(nbk * (nbk + 1) / 2), 1, 1,
+                             mcp, mcp, mcp, -1.0, 1.0);
+  GPB_TRY(gemm(m, p, false, false, EPI_AXPBY));
+  CUDA_TRY(launch_symmetrize(S, mcp, mt, m->st));
+  ++m->launches;
+  GPB_TRY(pt.stop());
+  CUDA_TRY(cudaMemcpy2DAsync(cov_host, sizeof(double) * mt, S, sizeof(double) * mcp,
+                             sizeof(double) * mt, mt, cudaMemcpyDeviceToHost, m->st));
+  CUDA_TRY(cudaStreamSynchronize(m->st));
+  return GPB_OK;
+}
+
+int clamp_variances(double* v, int64_t n, int64_t stride) {
+  // model.py:488-496
+  double worst = 0.0;
+  bool bad = false;
+  for (int64_t i = 0; i < n; ++i) {
+    const double x = v[i * stride];
+    if (x < -kVarianceSlack) {
+      if (!bad || x < worst) worst = x;
+      bad = true;
+    }
+  }
+  if (bad) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "variance %g is below the round-off allowance -%g", worst,
+             kVarianceSlack);
+    return fail(GPB_NUMERIC, buf);
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (v[i * stride] < 0.0) v[i * stride] = 0.0;
+  return GPB_OK;
+}
+
+int model_create(gpb_ctx* ctx, const double* z, const double* y, int64_t n, int64_t d, int64_t T,
+                 bool device_ptrs, gpb_model** out) {
+  if (!out) return fail(GPB_INVALID_CONFIG, "null output pointer");
+  *out = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!ctx || ctx != g_ctx) return fail(GPB_NOT_RUNNING, "runtime is not running");
+  }
+  if (n < 1 || d < 1) return fail(GPB_DIM, "z must be N x D with N, D >= 1");
+  if (T < 1 || n % T != 0) {
+    return fail(GPB_TILING, "tiles_per_dim=" + std::to_string(T) + " must divide the " +
+                                std::to_string(n) + " training points");
+  }
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  gpb_model* m = new gpb_model();
+  m->ctx = ctx;
+  m->gen = ctx->gen;
+  m->n = n;
+  m->d = d;
+  m->T = T;
+  m->b = static_cast<int>(n / T);
+  int bp = 0, bi = 0;
+  choose_internal_tile(n, m->b, &bp, &bi);
+  m->bp = bp;
+  m->bi = bi;
+  m->np_ = T * int64_t(bp);
+  m->Ti = static_cast<int>(m->np_ / bi);
+  m->pm.bp_user = (m->b % kTileAlign == 0) ? static_cast<int>(std::min<int64_t>(m->np_, 1 << 30)) : bp;
+  m->pm.b_user = (m->b % kTileAlign == 0) ? m->pm.bp_user : m->b;
+  int s = GPB_OK;
+  if (cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&m->e0) != cudaSuccess || cudaEventCreate(&m->e1) != cudaSuccess) {
+    s = fail(GPB_CUDA, "stream/event creation failed");
+  }
+  if (s == GPB_OK) s = alloc_model_buffers(m);
+  if (s == GPB_OK) s = upload_train(m, z, y, device_ptrs);
+  if (s != GPB_OK) {
+    gpb_model_destroy(m);
+    return s;
+  }
+  *out = m;
+  return GPB_OK;
+}
+
+void free_model(gpb_model* m) {
+  for (DevBuf* b : {&m->zp, &m->yp, &m->L, &m->Dinv, &m->scratch, &m->logdiag, &m->info, &m->yhat,
+                    &m->beta, &m->alpha, &m->bhat, &m->red, &m->tile_rm, &m->tile_cm, &m->chol_jobs,
+                    &m->X, &m->Kinv, &m->Wg, &m->part_l, &m->part_v, &m->part_x, &m->inv_jobs,
+                    &m->Bv, &m->W, &m->mpart, &m->sq, &m->pred_jobs, &m->zt, &m->mean, &m->var,
+                    &m->S, &m->fc_jobs})
+    b->release();
+}
+
+}  // namespace
+
+// =========================== C ABI ==========================================
+extern "C" {
+
+int gpb_abi_version(void) { return 1; }
+
+// error sink for tile_plugin.cu (shares the thread-local message)
+int gpb_plugin_fail(int code, const char* msg) { return fail(code, msg); }
+
+const char* gpb_last_error(void) { return g_err.c_str(); }
+
+int gpb_init(int device, gpb_ctx** out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_ctx) return fail(GPB_ALREADY_RUNNING, "a runtime is already running in this process");
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(GPB_INVALID_CONFIG, "no such CUDA device");
+  CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(gemm_init_attributes());
+  CUDA_TRY(potrf_init_attributes());
+  gpb_ctx* c = new gpb_ctx();
+  c->device = device;
+  c->gen = ++g_gen;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return fail(GPB_CUDA, "stream creation failed");
+  }
+  g_ctx = c;
+  if (out) *out = c;
+  return GPB_OK;
+}
+
+int gpb_finalize(gpb_ctx* ctx) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_ctx || (ctx && ctx != g_ctx)) return fail(GPB_NOT_RUNNING, "no runtime is running");
+  cudaDeviceSynchronize();
+  cudaStreamDestroy(g_ctx->stream);
+  delete g_ctx;
+  g_ctx = nullptr;
+  return GPB_OK;
+}
+
+gpb_ctx* gpb_current(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return g_ctx;
+}
+
+int gpb_model_create(gpb_ctx* ctx, const double* z, const double* y, int64_t n, int64_t d,
+                     int64_t tiles_per_dim, gpb_model** out) {
+  if (!z || !y) return fail(GPB_INVALID_CONFIG, "null input");
+  return model_create(ctx, z, y, n, d, tiles_per_dim, false, out);
+}
+
+int gpb_model_create_device(gpb_ctx* ctx, const double* z_dev, const double* y_dev, int64_t n,
+                            int64_t d, int64_t tiles_per_dim, gpb_model** out) {
+  if (!z_dev || !y_dev) return fail(GPB_INVALID_CONFIG, "null input");
+  return model_create(ctx, z_dev, y_dev, n, d, tiles_per_dim, true, out);
+}
+
+int gpb_model_destroy(gpb_model* m) {
+  if (!m) return GPB_OK;
+  if (m->st) cudaStreamSynchronize(m->st);
+  free_model(m);
+  if (m->e0) cudaEventDestroy(m->e0);
+  if (m->e1) cudaEventDestroy(m->e1);
+  if (m->st) cudaStreamDestroy(m->st);
+  delete m;
+  return GPB_OK;
+}
+
+int gpb_model_set_train(gpb_model* m, const double* z, const double* y, int64_t n, int64_t d) {
+  GPB_TRY(check_live(m));
+  if (n % m->T != 0)
+    return fail(GPB_TILING, "tiles_per_dim=" + std::to_string(m->T) + " must divide the " +
+                                std::to_string(n) + " training points");
+  if (n < 1 || d < 1) return fail(GPB_DIM, "z must be N x D with N, D >= 1");
+  free_model(m);
+  m->plan_ok = m->inv_plan = false;
+  m->pred_mcp = m->fc_mcp = -1;
+  m->n = n;
+  m->d = d;
+  m->b = static_cast<int>(n / m->T);
+  int bp = 0, bi = 0;
+  choose_internal_tile(n, m->b, &bp, &bi);
+  m->bp = bp;
+  m->bi = bi;
+  m->np_ = m->T * int64_t(bp);
+  m->Ti = static_cast<int>(m->np_ / bi);
+  m->pm.bp_user = (m->b % kTileAlign == 0) ? static_cast<int>(std::min<int64_t>(m->np_, 1 << 30)) : bp;
+  m->pm.b_user = (m->b % kTileAlign == 0) ? m->pm.bp_user : m->b;
+  invalidate(m);
+  GPB_TRY(alloc_model_buffers(m));
+  return upload_train(m, z, y, false);
+}
+
+int gpb_model_set_params(gpb_model* m, double l, double nu, double s2, const uint8_t tr[3]) {
+  if (!m) return fail(GPB_INVALID_CONFIG, "null model");
+  if (!(l > 0)) return fail(GPB_INVALID_CONFIG, "lengthscale must be positive");
+  if (!(nu > 0)) return fail(GPB_INVALID_CONFIG, "vertical_scale must be positive");
+  if (!(s2 >= 0)) return fail(GPB_INVALID_CONFIG, "noise_variance must be non-negative");
+  m->l = l;
+  m->nu = nu;
+  m->s2 = s2;
+  if (tr) for (int i = 0; i < 3; ++i) m->trainable[i] = tr[i] ? 1 : 0;
+  invalidate(m);
+  return GPB_OK;
+}
+
+int gpb_model_get_params(gpb_model* m, double out[3]) {
+  if (!m || !out) return fail(GPB_INVALID_CONFIG, "null argument");
+  out[0] = m->l;
+  out[1] = m->nu;
+  out[2] = m->s2;
+  return GPB_OK;
+}
+
+int gpb_cholesky(gpb_model* m, double* L_out) {
+  GPB_TRY(check_live(m));
+  GPB_TRY(ensure_factor(m));
+  if (L_out) {
+    DevBuf tmp;
+    CUDA_TRY(tmp.ensure(sizeof(double) * m->n * m->n));
+    CUDA_TRY(launch_export_lower(m->L.as<double>(), m->Ti, m->bi, m->n, m->pm, tmp.as<double>(), m->st));
+    ++m->launches;
+    CUDA_TRY(cudaMemcpyAsync(L_out, tmp.p, sizeof(double) * m->n * m->n, cudaMemcpyDeviceToHost, m->st));
+    CUDA_TRY(cudaStreamSynchronize(m->st));
+    tmp.release();
+  }
+  return GPB_OK;
+}
+
+int gpb_last_pivot(gpb_model* m, int64_t* pivot) {
+  if (!m || !pivot) return fail(GPB_INVALID_CONFIG, "null argument");
+  *pivot = m->last_pivot;
+  return GPB_OK;
+}
+
+int gpb_log_likelihood(gpb_model* m, double* out) {
+  GPB_TRY(check_live(m));
+  return log_likelihood(m, out);
+}
+
+int gpb_loss_gradients(gpb_model* m, double out[3]) {
+  GPB_TRY(check_live(m));
+  return loss_gradients(m, out);
+}
+
+int gpb_optimize(gpb_model* m, double lr, double b1, double b2, double eps, int64_t iters,
+                 double* history) {
+  GPB_TRY(check_live(m));
+  // AdamConfig validation (model.py:61-74)
+  if (!(lr > 0)) return fail(GPB_INVALID_CONFIG, "learning_rate must be positive");
+  if (!(b1 >= 0 && b1 < 1)) return fail(GPB_INVALID_CONFIG, "beta1 must lie in [0, 1)");
+  if (!(b2 >= 0 && b2 < 1)) return fail(GPB_INVALID_CONFIG, "beta2 must lie in [0, 1)");
+  if (!(eps > 0)) return fail(GPB_INVALID_CONFIG, "epsilon must be positive");
+  if (iters < 1) return fail(GPB_INVALID_CONFIG, "iterations must be at least 1");
+  for (int64_t it = 0; it < iters; ++it) {
+    m->adam_step += 1;
+    double grads[3];
+    int s = loss_gradients(m, grads);
+    double theta[3] = {m->l, m->nu, m->s2};
+    if (s == GPB_OK) {
+      // model.py:462-479, same operation order
+      double step[3];
+      for (int i = 0; i < 3; ++i) {
+        const double g = grads[i] * theta[i];
+        m->adam_m[i] = b1 * m->adam_m[i] + (1 - b1) * g;
+        m->adam_v[i] = b2 * m->adam_v[i] + (1 - b2) * g * g;
+        const double mh = m->adam_m[i] / (1 - std::pow(b1, double(m->adam_step)));
+        const double vh = m->adam_v[i] / (1 - std::pow(b2, double(m->adam_step)));
+        step[i] = lr * mh / (std::sqrt(vh) + eps);
+      }
+      for (int i = 0; i < 3; ++i) {
+        if (m->trainable[i]) {
+          const double u = std::log(std::max(theta[i], 1e-300)) - step[i];
+          theta[i] = std::exp(u);
+        }
+      }
+      if (m->trainable[2]) theta[2] = std::max(theta[2], 1e-12);
+      m->l = theta[0];
+      m->nu = theta[1];
+      m->s2 = theta[2];
+      invalidate(m);
+      double ll = 0;
+      s = log_likelihood(m, &ll);
+      if (s == GPB_OK && history) history[it] = -ll;
+    }
+    if (s == GPB_NOT_PD) {
+      g_err = "iteration " + std::to_string(m->adam_step) + ": " + g_err;
+      return s;
+    }
+    if (s != GPB_OK) return s;
+  }
+  return GPB_OK;
+}
+
+int gpb_predict(gpb_model* m, const double* zt, int64_t mt, int64_t d, double* mean, double* var,
+                double* cov) {
+  GPB_TRY(check_live(m));
+  if (d != m->d)
+    return fail(GPB_DIM, "test has " + std::to_string(d) + " features, model was trained with " +
+                             std::to_string(m->d));
+  if (mt < 1) return fail(GPB_DIM, "need at least one test point");
+  if (!mean || !zt) return fail(GPB_INVALID_CONFIG, "null argument");
+  CUDA_TRY(m->zt.ensure(sizeof(double) * mt * d));
+  CUDA_TRY(cudaMemcpyAsync(m->zt.p, zt, sizeof(double) * mt * d, cudaMemcpyHostToDevice, m->st));
+  const bool want_var = var || cov;
+  int s = predict_core(m, m->zt.as<double>(), mt, want_var);
+  if (s != GPB_OK) {
+    invalidate(m);
+    return s;
+  }
+  CUDA_TRY(cudaMemcpyAsync(mean, m->mean.p, sizeof(double) * mt, cudaMemcpyDeviceToHost, m->st));
+  if (var) CUDA_TRY(cudaMemcpyAsync(var, m->var.p, sizeof(double) * mt, cudaMemcpyDeviceToHost, m->st));
+  CUDA_TRY(cudaStreamSynchronize(m->st));
+  if (cov) {
+    GPB_TRY(full_cov(m, m->zt.as<double>(), mt, cov));
+    GPB_TRY(clamp_variances(cov, mt, mt + 1));
+  }
+  if (var) GPB_TRY(clamp_variances(var, mt, 1));
+  return GPB_OK;
+}
+
+int gpb_predict_device(gpb_model* m, const double* zt_dev, int64_t mt, int64_t d, double* mean_dev,
+                       double* var_dev) {
+  GPB_TRY(check_live(m));
+  if (d != m->d) return fail(GPB_DIM, "feature count mismatch");
+  GPB_TRY(predict_core(m, zt_dev, mt, var_dev != nullptr));
+  if (mean_dev)
+    CUDA_TRY(cudaMemcpyAsync(mean_dev, m->mean.p, sizeof(double) * mt, cudaMemcpyDeviceToDevice, m->st));
+  if (var_dev)
+    CUDA_TRY(cudaMemcpyAsync(var_dev, m->var.p, sizeof(double) * mt, cudaMemcpyDeviceToDevice, m->st));
+  CUDA_TRY(cudaStreamSynchronize(m->st));
+  return GPB_OK;
+}
+
+int gpb_model_timings(gpb_model* m, double* ms_out, int n) {
+  if (!m || !ms_out) return fail(GPB_INVALID_CONFIG, "null argument");
+  for (int i = 0; i < n && i < 8; ++i) ms_out[i] = m->timing[i];
+  return GPB_OK;
+}
+
+int gpb_model_launch_count(gpb_model* m, int64_t* out) {
+  if (!m || !out) return fail(GPB_INVALID_CONFIG, "null argument");
+  *out = m->launches;
+  return GPB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,92 @@
+// Launch interfaces of the non-GEMM kernels (potrf.cu, sek.cu, solve.cu).
+#pragma once
+#include "common.cuh"
+
+namespace gpb {
+
+// Index map of the padded internal layout: padded position P is real iff
+// P % bp_user < b_user; its original index is (P / bp_user) * b_user + P % bp_user.
+struct PadMap {
+  int bp_user;
+  int b_user;
+  GPB_DEVINL bool valid(int64_t P) const { return (P % bp_user) < b_user; }
+};
+
+struct PotrfArgs {
+  double* tile;     // bi x bi, in place -> L_kk (upper zeroed)
+  double* dinv;     // bi x bi output: L_kk^-1
+  double* logdiag;  // [T] per-tile sum of log L_jj over real pivots
+  int* info;        // -1, or first failing original pivot index
+  int bi;
+  int tile_index;
+  int tile_off;     // padded global position of the tile's first row
+  int bp_user, b_user;
+  int trtri_only;   // 1: tile already holds L; only form dinv = L^-1
+};
+cudaError_t launch_potrf(const PotrfArgs& a, cudaStream_t s);
+cudaError_t potrf_init_attributes();
+
+// ---- squared-exponential tiles (sek.cu) -----------------------------------
+struct SekParams {
+  double lengthscale, vertical, noise;
+  double neg_half_inv_l2;  // -1 / (2 l^2)   (covariance.py:79)
+};
+
+// Lower tiles [t0, t1) of the packed row-major tile grid (tile list entries
+// are (i, j) pairs).  Noise goes on the global diagonal when add_noise.
+cudaError_t launch_assemble_lower(double* tiles, const int2* tile_ij, int64_t t0, int64_t t1,
+                                  const double* zp, int d, int bi, PadMap pm, SekParams sp,
+                                  bool add_noise, cudaStream_t s);
+
+// B = K*^T for one chunk of test points: rows = padded training positions
+// (np rows), cols = mcp (mc real).  Fused mean partials over 64-row blocks:
+// mpart[rb][c] = sum_{rows in rb} B[r][c] * alpha[r].
+cudaError_t launch_cross(double* B, int64_t ldb, double* mpart, const double* alpha,
+                         const double* zp, int64_t np_, const double* zt, int64_t mc,
+                         int64_t mcp, int d, PadMap pm, SekParams sp, cudaStream_t s);
+
+// Dense prior K** (mp x mp, row-major) of the test chunk, noise-free.
+cudaError_t launch_prior(double* S, int64_t mp, const double* zt, int64_t m, int d, SekParams sp,
+                         cudaStream_t s);
+
+// Gradient trace pass over the lower tiles of K^-1 (column-major tile order):
+// part[blk] = w * sum (Kinv - alpha alpha^T) e d2  and  w * sum (Kinv - ..) e.
+cudaError_t launch_trace(const double* kinv, const int2* tile_ij_cm, int64_t ntiles, int T,
+                         const double* zp, const double* alpha, int d, int bi, PadMap pm,
+                         SekParams sp, double* part_l, double* part_v, cudaStream_t s);
+// part[blk] = sum of squares of the real entries of lower tiles (column-major order).
+cudaError_t launch_tiles_sumsq(const double* x, const int2* tile_ij_cm, int64_t ntiles, int bi,
+                               PadMap pm, double* part, cudaStream_t s);
+
+// ---- solves and reductions (solve.cu) -------------------------------------
+cudaError_t launch_fwd_diag(const double* dinv, const double* yhat, double* beta, int bi,
+                            cudaStream_t s);
+cudaError_t launch_fwd_update(const double* ltiles, int T, int i, int bi, const double* beta_i,
+                              double* yhat, cudaStream_t s);
+cudaError_t launch_bwd_diag(const double* dinv, const double* bhat, double* alpha, int bi,
+                            cudaStream_t s);
+cudaError_t launch_bwd_update(const double* ltiles, int i, int bi, const double* alpha_i,
+                              double* bhat, cudaStream_t s);
+// out[0] = sum_k logdiag[k] (sequential k), out[1] = sum x^2 (fixed order)
+cudaError_t launch_loss_terms(const double* logdiag, int T, const double* x, int64_t n,
+                              double* out, cudaStream_t s);
+// out[i] = fixed-order sum of part[0..n)  (one output per call, slot i)
+cudaError_t launch_reduce(const double* part, int64_t n, double* out, cudaStream_t s);
+// mean[c] = sum_rb mpart[rb][c];  var[c] = nu - sum_rb sq[rb][c]  (either may be null)
+cudaError_t launch_pred_finalize(const double* mpart, int64_t nmrb, const double* sq,
+                                 int64_t nsrb, int64_t ld, int64_t mc, double nu, double* mean,
+                                 double* var, cudaStream_t s);
+// S[c][r] = S[r][c] for c > r (mirror the lower triangle)
+cudaError_t launch_symmetrize(double* S, int64_t mp, int64_t m, cudaStream_t s);
+// scatter padded vector -> dense, gather dense -> padded
+cudaError_t launch_pad_vector(const double* src, double* dst, int64_t np_, PadMap pm, cudaStream_t s);
+cudaError_t launch_pad_rows(const double* src, double* dst, int64_t np_, int d, PadMap pm,
+                            cudaStream_t s);
+// dense lower factor export: out[r][c] (n x n) from packed tiles
+cudaError_t launch_export_lower(const double* tiles, int T, int bi, int64_t n, PadMap pm,
+                                double* out, cudaStream_t s);
+// copy the solved panel (scratch tiles q = 0..T-k-2) back to tiles (k+1+q, k)
+cudaError_t launch_copy_panel(double* ltiles, const double* scratch, int T, int k, int bi,
+                              cudaStream_t s);
+
+}  // namespace gpb

@@ -1,0 +1,230 @@
+// Diagonal-tile factorisation: POTRF + TRTRI of one bi x bi tile in one CTA.
+//
+// Replaces taskgp tile_potrf (tiles.py:132-137 -> np.linalg.cholesky,
+// tiles.py:29-33) and provides the inverted diagonal tile that turns every
+// triangular solve of the hot path (panel TRSM tiles.py:140-146, vector
+// solves tiles.py:170-180, panel solves tiles.py:182-185) into DMMA products.
+//
+// Blocked left-looking Cholesky with 32-column panels; the panel update and
+// the below-diagonal solve run on the FP64 tensor pipe (DMMA.8x8x4) warp by
+// warp; the 32x32 diagonal block is factored and inverted in shared memory
+// by one warp.  TRTRI then forms Dinv = L^-1 block row by block row.
+// Epilogue: Sigma log L_jj over real (non-padding) pivots and a LAPACK-style
+// info word holding the first failing global pivot.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace gpb {
+
+namespace {
+
+constexpr int PT = 256;  // threads
+constexpr int NB = 32;   // panel width
+constexpr int SLD = NB + 1;
+
+// acc[i][j][e] <-> C[8i+g][8j+2t+e] of a 32x32 warp tile.
+GPB_DEVINL void zero_acc(double (&acc)[4][4][2]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+}
+
+// acc += A(32 x K) * B(32 x K)^T, both k-contiguous.
+GPB_DEVINL void warp_nt(double (&acc)[4][4][2], const double* A, int64_t lda, const double* B,
+                        int64_t ldb, int K, int g, int t) {
+#pragma unroll 2
+  for (int k = 0; k < K; k += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = A[(8 * i + g) * lda + k + t];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = B[(8 * j + g) * ldb + k + t];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+}
+
+// acc += A(32 x K) * B(K x 32), A k-contiguous, B row-major (n contiguous).
+GPB_DEVINL void warp_nn(double (&acc)[4][4][2], const double* A, int64_t lda, const double* B,
+                        int64_t ldb, int K, int g, int t) {
+#pragma unroll 2
+  for (int k = 0; k < K; k += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = A[(8 * i + g) * lda + k + t];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = B[(k + t) * ldb + 8 * j + g];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(PT) potrf_tile_kernel(PotrfArgs a) {
+  extern __shared__ double sm[];
+  double* Ld = sm;                 // [32][33] factor block
+  double* Li = Ld + NB * SLD;      // [32][33] its inverse
+  double* S = Li + NB * SLD;       // [8][32][33] per-warp scratch
+  __shared__ int s_fail;
+
+  if (*a.info >= 0) return;  // an earlier tile already failed
+  const int bi = a.bi;
+  double* T = a.tile;
+  double* D = a.dinv;
+  const int P = bi / NB;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  if (tid == 0) s_fail = -1;
+  double logsum = 0.0;  // meaningful in lane 0 of warp 0
+  __syncthreads();
+
+  for (int p = 0; p < P; ++p) {
+    const int c0 = p * NB;
+    // (1) left-looking panel update: T[r][c0:c0+32] -= L[r][0:c0] L[c0:c0+32][0:c0]^T
+    if (p > 0 && !a.trtri_only) {
+      for (int rb = p + warp; rb < P; rb += PT / 32) {
+        double acc[4][4][2];
+        zero_acc(acc);
+        warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi, bi, T + static_cast<int64_t>(c0) * bi, bi, c0, g, t);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            double* c = T + static_cast<int64_t>(rb * NB + 8 * i + g) * bi + c0 + 8 * j + 2 * t;
+            c[0] -= acc[i][j][0];
+            c[1] -= acc[i][j][1];
+          }
+      }
+    }
+    __syncthreads();
+    // (2) factor + invert the 32x32 diagonal block (one warp)
+    if (warp == 0) {
+      for (int c = 0; c < NB; ++c)
+        Ld[lane * SLD + c] = T[static_cast<int64_t>(c0 + lane) * bi + c0 + c];
+      __syncwarp();
+      int fail = -1;
+      for (int j = 0; j < (a.trtri_only ? 0 : NB); ++j) {
+        const double piv = Ld[j * SLD + j];
+        if (!(piv > 0.0)) { fail = j; break; }
+        const double ljj = sqrt(piv);
+        __syncwarp();
+        if (lane > j) Ld[lane * SLD + j] /= ljj;
+        if (lane == j) Ld[j * SLD + j] = ljj;
+        __syncwarp();
+        if (lane > j) {
+          const double lij = Ld[lane * SLD + j];
+          for (int c = j + 1; c <= lane; ++c) Ld[lane * SLD + c] -= lij * Ld[c * SLD + j];
+        }
+        __syncwarp();
+        if (lane == 0) {
+          const int pos = a.tile_off + c0 + j;  // padded global position
+          if (pos % a.bp_user < a.b_user) logsum += log(ljj);
+        }
+      }
+      if (fail >= 0) {
+        if (lane == 0) {
+          const int pos = a.tile_off + c0 + fail;
+          s_fail = (pos / a.bp_user) * a.b_user + pos % a.bp_user;
+        }
+      } else {
+        // column `lane` of the inverse by forward substitution
+        for (int r = 0; r < lane; ++r) Li[r * SLD + lane] = 0.0;
+        Li[lane * SLD + lane] = 1.0 / Ld[lane * SLD + lane];
+        for (int r = lane + 1; r < NB; ++r) {
+          double s = 0.0;
+          for (int k = lane; k < r; ++k) s += Ld[r * SLD + k] * Li[k * SLD + lane];
+          Li[r * SLD + lane] = -s / Ld[r * SLD + r];
+        }
+        __syncwarp();
+        for (int c = 0; c < NB; ++c) {
+          const int64_t o = static_cast<int64_t>(c0 + lane) * bi + c0 + c;
+          if (!a.trtri_only) T[o] = c <= lane ? Ld[lane * SLD + c] : 0.0;
+          D[o] = Li[lane * SLD + c];
+        }
+      }
+    }
+    __syncthreads();
+    if (s_fail >= 0) break;
+    // (3) below-diagonal panel: L[r][c0:c0+32] = T[r][c0:c0+32] * Li^T
+    for (int rb = p + 1 + warp; rb < (a.trtri_only ? 0 : P); rb += PT / 32) {
+      double acc[4][4][2];
+      zero_acc(acc);
+      double* blk = T + static_cast<int64_t>(rb) * NB * bi + c0;
+      warp_nt(acc, blk, bi, Li, SLD, NB, g, t);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          double* c = blk + static_cast<int64_t>(8 * i + g) * bi + 8 * j + 2 * t;
+          c[0] = acc[i][j][0];
+          c[1] = acc[i][j][1];
+        }
+    }
+    __syncthreads();
+  }
+  if (s_fail >= 0) {
+    if (tid == 0) *a.info = s_fail;
+    return;
+  }
+  // zero strictly-upper 32-blocks of L and Dinv (lower-triangular results)
+  for (int64_t idx = tid; idx < static_cast<int64_t>(bi) * bi; idx += PT) {
+    const int r = static_cast<int>(idx / bi), c = static_cast<int>(idx % bi);
+    if (c / NB > r / NB) {
+      if (!a.trtri_only) T[idx] = 0.0;
+      D[idx] = 0.0;
+    }
+  }
+  __syncthreads();
+  // TRTRI: D[I][J] = -D[I][I] * sum_{K=J}^{I-1} L[I][K] D[K][J]
+  double* Sw = S + warp * NB * SLD;
+  for (int I = 1; I < P; ++I) {
+    for (int J = warp; J < I; J += PT / 32) {
+      double acc[4][4][2];
+      zero_acc(acc);
+      warp_nn(acc, T + static_cast<int64_t>(I) * NB * bi + J * NB, bi,
+              D + static_cast<int64_t>(J) * NB * bi + J * NB, bi, (I - J) * NB, g, t);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          Sw[(8 * i + g) * SLD + 8 * j + 2 * t] = acc[i][j][0];
+          Sw[(8 * i + g) * SLD + 8 * j + 2 * t + 1] = acc[i][j][1];
+        }
+      __syncwarp();
+      zero_acc(acc);
+      warp_nn(acc, D + static_cast<int64_t>(I) * NB * bi + I * NB, bi, Sw, SLD, NB, g, t);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          double* c = D + static_cast<int64_t>(I * NB + 8 * i + g) * bi + J * NB + 8 * j + 2 * t;
+          c[0] = -acc[i][j][0];
+          c[1] = -acc[i][j][1];
+        }
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && a.logdiag) a.logdiag[a.tile_index] = logsum;
+}
+
+size_t potrf_smem_bytes() { return sizeof(double) * (2 * NB * SLD + (PT / 32) * NB * SLD); }
+
+cudaError_t launch_potrf(const PotrfArgs& a, cudaStream_t s) {
+  potrf_tile_kernel<<<1, PT, potrf_smem_bytes(), s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t potrf_init_attributes() {
+  return cudaFuncSetAttribute(potrf_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(potrf_smem_bytes()));
+}
+
+}  // namespace gpb
