@@ -97,6 +97,16 @@ int gpb_predict_device(gpb_model* m, const double* zt_dev, int64_t mt, int64_t d
 int gpb_model_timings(gpb_model* m, double* ms_out, int n);
 /* launches of this library's kernels since the model was created */
 int gpb_model_launch_count(gpb_model* m, int64_t* out);
+/* the CUDA stream (cudaStream_t) the model's kernels run on */
+int gpb_model_stream(gpb_model* m, void** stream);
+/* per-kernel-class profiling with CUDA events around every launch:
+ * class 0 grouped DMMA GEMM, 1 POTRF/TRTRI tile, 2 SEK assembly, 3 solves.
+ * set_profiling resets the counters; kernel_stats returns the totals
+ * (device ms, executed flops, launches) since then. */
+int gpb_model_set_profiling(gpb_model* m, int on);
+int gpb_model_kernel_stats(gpb_model* m, double ms[8], double flops[8], int64_t count[8]);
+/* sustained FP64 tensor-pipe (DMMA.8x8x4) throughput of this GPU, TFLOP/s */
+int gpb_fp64_peak_probe(gpb_ctx* ctx, double seconds, double* tflops);
 
 /* ---- tile-kernel plugin (tiles.py:23-46, 132-164) -------------------------
  * Host buffers, fresh outputs, inputs never mutated.  Square tiles b x b;

@@ -113,6 +113,19 @@ struct gpb_model {
   int64_t adam_step = 0;
   double timing[8] = {0};
   int64_t launches = 0;
+
+  // per-kernel-class profiling (CUDA events around each launch on st)
+  struct ProfRec {
+    int cls;
+    double flops;
+    cudaEvent_t a, b;
+  };
+  bool prof = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> evpool;
+  size_t evnext = 0;
+  double cls_ms[8] = {0}, cls_flops[8] = {0};
+  int64_t cls_n[8] = {0};
 };
 
 namespace {
@@ -161,8 +174,59 @@ GemmParams base_params(const GemmJob* jobs, int njobs, int mblk, int nblk, int64
   return p;
 }
 
-int gemm(gpb_model* m, const GemmParams& p, bool ak, bool bk, int epi) {
+enum KernelClass { KC_GEMM = 0, KC_POTRF = 1, KC_SEK = 2, KC_SOLVE = 3, KC_OTHER = 4 };
+
+cudaEvent_t prof_event(gpb_model* m) {
+  if (m->evnext == m->evpool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    m->evpool.push_back(e);
+  }
+  return m->evpool[m->evnext++];
+}
+
+// Bracket one launch with events when profiling is on.
+struct ProfScope {
+  gpb_model* m;
+  int cls;
+  double flops;
+  cudaEvent_t a = nullptr;
+  ProfScope(gpb_model* mm, int c, double f) : m(mm), cls(c), flops(f) {
+    if (m->prof) {
+      a = prof_event(m);
+      cudaEventRecord(a, m->st);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = prof_event(m);
+      cudaEventRecord(b, m->st);
+      m->recs.push_back({cls, flops, a, b});
+    }
+  }
+};
+
+int prof_collect(gpb_model* m) {
+  if (m->recs.empty()) return GPB_OK;
+  CUDA_TRY(cudaStreamSynchronize(m->st));
+  for (auto& r : m->recs) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    m->cls_ms[r.cls] += ms;
+    m->cls_flops[r.cls] += r.flops;
+    m->cls_n[r.cls] += 1;
+  }
+  m->recs.clear();
+  m->evnext = 0;
+  return GPB_OK;
+}
+
+// executed flops of a grouped launch: 2 * 128 * 128 * K per computed block
+double gemm_flops(int64_t blocks, int64_t K) { return 2.0 * GBM * GBN * double(blocks) * double(K); }
+
+int gemm(gpb_model* m, const GemmParams& p, bool ak, bool bk, int epi, double flops) {
   if (p.njobs == 0) return GPB_OK;
+  ProfScope ps(m, KC_GEMM, flops);
   CUDA_TRY(launch_gemm(p, ak, bk, epi, m->st));
   ++m->launches;
   return GPB_OK;
@@ -299,6 +363,7 @@ int ensure_factor(gpb_model* m) {
   double* D = m->Dinv.as<double>();
   {
     PhaseTimer pt(m, 0);
+    ProfScope ps(m, KC_SEK, 0.0);
     CUDA_TRY(launch_assemble_lower(L, m->tile_rm.as<int2>(), 0, ntiles, m->zp.as<double>(),
                                    static_cast<int>(m->d), bi, m->pm, sek_params(m), true, m->st));
     ++m->launches;
@@ -323,15 +388,20 @@ int ensure_factor(gpb_model* m) {
     a.tile_off = k * bi;
     a.bp_user = m->pm.bp_user;
     a.b_user = m->pm.b_user;
-    CUDA_TRY(launch_potrf(a, m->st));
+    {
+      ProfScope ps(m, KC_POTRF, 2.0 / 3.0 * double(bi) * bi * bi);
+      CUDA_TRY(launch_potrf(a, m->st));
+    }
     ++m->launches;
     if (k + 1 < Ti) {
+      const int64_t r = Ti - k - 1;
       GemmParams tp = base_params(jobs + m->trsm_off[k], static_cast<int>(m->trsm_cnt[k]), nb, nb,
                                   bi, bi, bi, 1.0, 0.0);
-      GPB_TRY(gemm(m, tp, true, true, EPI_AXPBY));
+      GPB_TRY(gemm(m, tp, true, true, EPI_AXPBY, gemm_flops(r * nb * nb, bi)));
       GemmParams up = base_params(jobs + m->upd_off[k], static_cast<int>(m->upd_cnt[k]), nb, nb,
                                   bi, bi, bi, -1.0, 1.0);
-      GPB_TRY(gemm(m, up, true, true, EPI_AXPBY));
+      GPB_TRY(gemm(m, up, true, true, EPI_AXPBY,
+                   gemm_flops(r * (r - 1) / 2 * nb * nb + r * nb * (nb + 1) / 2, bi)));
       CUDA_TRY(launch_copy_panel(L, m->scratch.as<double>(), Ti, k, bi, m->st));
       ++m->launches;
     }
@@ -475,9 +545,9 @@ int loss_gradients(gpb_model* m, double out[3]) {
     GemmParams w = base_params(jobs + m->invw_off[i], i, nb, nb, bi, bi, bi, 1.0, 0.0);
     w.a_ktile = bi;
     w.a_kstride = bi2;
-    GPB_TRY(gemm(m, w, true, false, EPI_AXPBY));
+    GPB_TRY(gemm(m, w, true, false, EPI_AXPBY, gemm_flops(int64_t(nb) * nb, int64_t(bi) * i * (i + 1) / 2)));
     GemmParams x = base_params(jobs + m->invx_off[i], i, nb, nb, bi, bi, bi, -1.0, 0.0);
-    GPB_TRY(gemm(m, x, true, false, EPI_AXPBY));
+    GPB_TRY(gemm(m, x, true, false, EPI_AXPBY, gemm_flops(int64_t(i) * nb * nb, bi)));
   }
 
   double* red = m->red.as<double>();
@@ -486,7 +556,8 @@ int loss_gradients(gpb_model* m, double out[3]) {
     // K^-1 = X^T X, lower tiles (model.py:362-380)
     GemmParams kp = base_params(jobs + m->kinv_off, static_cast<int>(m->kinv_cnt), nb, nb, bi, bi,
                                 bi, 1.0, 0.0);
-    GPB_TRY(gemm(m, kp, false, false, EPI_AXPBY));
+    GPB_TRY(gemm(m, kp, false, false, EPI_AXPBY,
+                 gemm_flops(int64_t(nb) * nb, int64_t(bi) * Ti * (Ti + 1) * (Ti + 2) / 6)));
     // fused trace pass (model.py:382-414 with covariance.py:196-220 regenerated)
     CUDA_TRY(launch_trace(m->Kinv.as<double>(), m->tile_cm.as<int2>(), ntiles, Ti, m->zp.as<double>(),
                           m->alpha.as<double>(), static_cast<int>(m->d), bi, m->pm, sek_params(m),
@@ -562,6 +633,7 @@ int predict_core(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var) 
   const SekParams sp = sek_params(m);
   {
     PhaseTimer pt(m, 3);
+    ProfScope ps(m, KC_SEK, 0.0);
     CUDA_TRY(launch_cross(Bv, mcp, m->mpart.as<double>(), m->alpha.as<double>(), m->zp.as<double>(),
                           m->np_, zt_dev, mt, mcp, static_cast<int>(m->d), m->pm, sp, m->st));
     ++m->launches;
@@ -575,11 +647,12 @@ int predict_core(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var) 
                                  mcp, -1.0, 1.0);
       w.a_ktile = bi;
       w.a_kstride = int64_t(bi) * bi;
-      GPB_TRY(gemm(m, w, true, false, EPI_AXPBY));
+      const int64_t blocks = int64_t(bi / GBM) * (mcp / GBN);
+      GPB_TRY(gemm(m, w, true, false, EPI_AXPBY, gemm_flops(blocks, int64_t(i) * bi)));
       GemmParams v = base_params(jobs + 2 * i + 1, 1, bi / GBM, static_cast<int>(mcp / GBN), bi,
                                  mcp, mcp, 1.0, 0.0);
       v.aux_ld = mcp;
-      GPB_TRY(gemm(m, v, true, false, EPI_SUMSQ));
+      GPB_TRY(gemm(m, v, true, false, EPI_SUMSQ, gemm_flops(blocks, bi)));
     }
     GPB_TRY(pt.stop());
   }
@@ -618,7 +691,7 @@ int full_cov(gpb_model* m, const double* zt_dev, int64_t mt, double* cov_host) {
   // Sigma = K** - V^T V (model.py:254-269), lower blocks
   GemmParams p = base_params(m->fc_jobs.as<GemmJob>(), static_cast<int>(nbk * (nbk + 1) / 2), 1, 1,
                              mcp, mcp, mcp, -1.0, 1.0);
-  GPB_TRY(gemm(m, p, false, false, EPI_AXPBY));
+  GPB_TRY(gemm(m, p, false, false, EPI_AXPBY, gemm_flops(nbk * (nbk + 1) / 2, m->np_)));
   CUDA_TRY(launch_symmetrize(S, mcp, mt, m->st));
   ++m->launches;
   GPB_TRY(pt.stop());
@@ -767,6 +840,7 @@ int gpb_model_destroy(gpb_model* m) {
   if (!m) return GPB_OK;
   if (m->st) cudaStreamSynchronize(m->st);
   free_model(m);
+  for (cudaEvent_t e : m->evpool) cudaEventDestroy(e);
   if (m->e0) cudaEventDestroy(m->e0);
   if (m->e1) cudaEventDestroy(m->e1);
   if (m->st) cudaStreamDestroy(m->st);
@@ -943,6 +1017,34 @@ int gpb_predict_device(gpb_model* m, const double* zt_dev, int64_t mt, int64_t d
 int gpb_model_timings(gpb_model* m, double* ms_out, int n) {
   if (!m || !ms_out) return fail(GPB_INVALID_CONFIG, "null argument");
   for (int i = 0; i < n && i < 8; ++i) ms_out[i] = m->timing[i];
+  return GPB_OK;
+}
+
+int gpb_model_stream(gpb_model* m, void** stream) {
+  if (!m || !stream) return fail(GPB_INVALID_CONFIG, "null argument");
+  *stream = static_cast<void*>(m->st);
+  return GPB_OK;
+}
+
+int gpb_model_set_profiling(gpb_model* m, int on) {
+  if (!m) return fail(GPB_INVALID_CONFIG, "null model");
+  GPB_TRY(prof_collect(m));
+  m->prof = on != 0;
+  for (int i = 0; i < 8; ++i) {
+    m->cls_ms[i] = m->cls_flops[i] = 0.0;
+    m->cls_n[i] = 0;
+  }
+  return GPB_OK;
+}
+
+int gpb_model_kernel_stats(gpb_model* m, double ms[8], double flops[8], int64_t count[8]) {
+  if (!m) return fail(GPB_INVALID_CONFIG, "null model");
+  GPB_TRY(prof_collect(m));
+  for (int i = 0; i < 8; ++i) {
+    if (ms) ms[i] = m->cls_ms[i];
+    if (flops) flops[i] = m->cls_flops[i];
+    if (count) count[i] = m->cls_n[i];
+  }
   return GPB_OK;
 }
 
