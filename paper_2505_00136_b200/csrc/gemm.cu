@@ -17,32 +17,56 @@ struct StageLayout {
   static constexpr int kElems = KMAJ ? ROWS * (GBK + 4) : GBK * (ROWS + 4);
 };
 
+// Streams one operand's BK-deep k chunks into shared memory.  Per-thread
+// source/destination offsets are fixed for the whole k loop; moving to the
+// next chunk is a pointer bump (plus a jump of `kstride` when a tiled-k walk
+// crosses into the next tile), so the mainloop carries no 64-bit division.
 template <bool KMAJ, int ROWS>
-GPB_DEVINL void load_stage(double* s, const double* base, int64_t ld, int64_t ktile,
-                           int64_t kstride, int row0, int k0, int tid) {
+struct StageLoader {
   using L = StageLayout<KMAJ, ROWS>;
-  const double* src = base + (k0 / ktile) * kstride;
-  const int64_t kin = k0 % ktile;
-  if (KMAJ) {
-    src += kin + static_cast<int64_t>(row0) * ld;
-    // ROWS x 16 doubles = ROWS * 8 chunks of 16 B
-#pragma unroll
-    for (int it = 0; it < ROWS * 8 / GTHREADS; ++it) {
-      int c = tid + it * GTHREADS;
-      int r = c >> 3, kc = c & 7;
-      cp_async16(s + r * L::kLd + kc * 2, src + r * ld + kc * 2);
-    }
-  } else {
-    src += kin * ld + row0;
-    constexpr int kChunksPerRow = ROWS / 2;
-#pragma unroll
-    for (int it = 0; it < GBK * kChunksPerRow / GTHREADS; ++it) {
-      int c = tid + it * GTHREADS;
-      int k = c / kChunksPerRow, mc = c % kChunksPerRow;
-      cp_async16(s + k * L::kLd + mc * 2, src + k * ld + mc * 2);
+  static constexpr int kIters = ROWS * GBK / 2 / GTHREADS;  // 16-byte chunks per thread
+  const double* cur;  // start of the current k chunk (row0 applied)
+  int64_t off0, step;  // thread's first source offset and per-iteration stride
+  int soff0;           // thread's first smem offset
+  int kin, ktile;
+  int64_t kstride;
+  int64_t kbump;       // pointer advance per chunk inside a tile
+
+  GPB_DEVINL void init(const double* base, int64_t ld, int64_t kt, int64_t ks, int row0, int tid) {
+    ktile = static_cast<int>(kt < (int64_t(1) << 30) ? kt : (int64_t(1) << 30));
+    kstride = ks;
+    kin = 0;
+    if (KMAJ) {
+      cur = base + static_cast<int64_t>(row0) * ld;
+      const int r = tid >> 3, kc = tid & 7;
+      off0 = r * ld + kc * 2;
+      step = (GTHREADS / 8) * ld;
+      soff0 = r * L::kLd + kc * 2;
+      kbump = GBK;
+    } else {
+      constexpr int kChunksPerRow = ROWS / 2;
+      cur = base + row0;
+      const int k = tid / kChunksPerRow, mc = tid % kChunksPerRow;
+      off0 = k * ld + mc * 2;
+      step = (GTHREADS / kChunksPerRow) * ld;
+      soff0 = k * L::kLd + mc * 2;
+      kbump = GBK * ld;
     }
   }
-}
+  GPB_DEVINL void load(double* s) {
+    constexpr int sstep = KMAJ ? (GTHREADS / 8) * L::kLd : (GTHREADS / (ROWS / 2)) * L::kLd;
+    const double* src = cur + off0;
+#pragma unroll
+    for (int it = 0; it < kIters; ++it) cp_async16(s + soff0 + it * sstep, src + it * step);
+    kin += GBK;
+    if (kin >= ktile) {  // next tile of a tiled-k walk
+      cur += kstride - static_cast<int64_t>(ktile / GBK - 1) * kbump;
+      kin = 0;
+    } else {
+      cur += kbump;
+    }
+  }
+};
 
 template <bool KMAJ, int ROWS>
 GPB_DEVINL double frag(const double* s, int row, int k) {
@@ -79,11 +103,15 @@ __global__ void __launch_bounds__(GTHREADS, 1) dgemm_grouped_kernel(const GemmPa
 
   const int nk = job.K / GBK;
   const int arow0 = mb * GBM, brow0 = nb * GBN;
+  StageLoader<AK, GBM> la;
+  StageLoader<BK, GBN> lb;
+  la.init(job.A, p.lda, p.a_ktile, p.a_kstride, arow0, tid);
+  lb.init(job.B, p.ldb, p.b_ktile, p.b_kstride, brow0, tid);
 #pragma unroll
   for (int s = 0; s < GSTAGES - 1; ++s) {
     if (s < nk) {
-      load_stage<AK, GBM>(sA + s * LA::kElems, job.A, p.lda, p.a_ktile, p.a_kstride, arow0, s * GBK, tid);
-      load_stage<BK, GBN>(sB + s * LB::kElems, job.B, p.ldb, p.b_ktile, p.b_kstride, brow0, s * GBK, tid);
+      la.load(sA + s * LA::kElems);
+      lb.load(sB + s * LB::kElems);
     }
     cp_async_commit();
   }
@@ -93,8 +121,8 @@ __global__ void __launch_bounds__(GTHREADS, 1) dgemm_grouped_kernel(const GemmPa
     const int nx = kc + GSTAGES - 1;
     if (nx < nk) {
       const int st = nx % GSTAGES;
-      load_stage<AK, GBM>(sA + st * LA::kElems, job.A, p.lda, p.a_ktile, p.a_kstride, arow0, nx * GBK, tid);
-      load_stage<BK, GBN>(sB + st * LB::kElems, job.B, p.ldb, p.b_ktile, p.b_kstride, brow0, nx * GBK, tid);
+      la.load(sA + st * LA::kElems);
+      lb.load(sB + st * LB::kElems);
     }
     cp_async_commit();
     const double* a_s = sA + (kc % GSTAGES) * LA::kElems;

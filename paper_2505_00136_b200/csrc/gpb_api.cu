@@ -90,12 +90,14 @@ struct gpb_model {
   PadMap pm{};
   double l = 1.0, nu = 1.0, s2 = 0.1;
   uint8_t trainable[3] = {1, 1, 1};
-  cudaStream_t st = nullptr;
+  cudaStream_t st = nullptr;    // main stream (trailing updates, solves, prediction)
+  cudaStream_t crit = nullptr;  // high-priority stream: the factorisation's critical path
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  std::vector<cudaEvent_t> sync_ev;  // cross-stream dependencies (timing disabled)
 
   DevBuf zp, yp, L, Dinv, scratch, logdiag, info, yhat, beta, alpha, bhat, red, tile_rm, tile_cm,
       chol_jobs;
-  std::vector<int64_t> trsm_off, trsm_cnt, upd_off, upd_cnt;
+  std::vector<int64_t> trsm_off, trsm_cnt, col_off, col_cnt, upd_off, upd_cnt;
   bool plan_ok = false, factor_ok = false, weights_ok = false;
   int64_t last_pivot = -1;
 
@@ -190,17 +192,19 @@ struct ProfScope {
   gpb_model* m;
   int cls;
   double flops;
+  cudaStream_t s;
   cudaEvent_t a = nullptr;
-  ProfScope(gpb_model* mm, int c, double f) : m(mm), cls(c), flops(f) {
+  ProfScope(gpb_model* mm, int c, double f, cudaStream_t ss = nullptr)
+      : m(mm), cls(c), flops(f), s(ss ? ss : mm->st) {
     if (m->prof) {
       a = prof_event(m);
-      cudaEventRecord(a, m->st);
+      cudaEventRecord(a, s);
     }
   }
   ~ProfScope() {
     if (a) {
       cudaEvent_t b = prof_event(m);
-      cudaEventRecord(b, m->st);
+      cudaEventRecord(b, s);
       m->recs.push_back({cls, flops, a, b});
     }
   }
@@ -224,10 +228,12 @@ int prof_collect(gpb_model* m) {
 // executed flops of a grouped launch: 2 * 128 * 128 * K per computed block
 double gemm_flops(int64_t blocks, int64_t K) { return 2.0 * GBM * GBN * double(blocks) * double(K); }
 
-int gemm(gpb_model* m, const GemmParams& p, bool ak, bool bk, int epi, double flops) {
+int gemm(gpb_model* m, const GemmParams& p, bool ak, bool bk, int epi, double flops,
+         cudaStream_t s = nullptr) {
   if (p.njobs == 0) return GPB_OK;
-  ProfScope ps(m, KC_GEMM, flops);
-  CUDA_TRY(launch_gemm(p, ak, bk, epi, m->st));
+  if (!s) s = m->st;
+  ProfScope ps(m, KC_GEMM, flops, s);
+  CUDA_TRY(launch_gemm(p, ak, bk, epi, s));
   ++m->launches;
   return GPB_OK;
 }
@@ -239,7 +245,7 @@ int alloc_model_buffers(gpb_model* m) {
   CUDA_TRY(m->yp.ensure(sizeof(double) * m->np_));
   CUDA_TRY(m->L.ensure(sizeof(double) * ntiles * bi2));
   CUDA_TRY(m->Dinv.ensure(sizeof(double) * m->Ti * bi2));
-  CUDA_TRY(m->scratch.ensure(sizeof(double) * std::max<int64_t>(1, m->Ti - 1) * bi2));
+  CUDA_TRY(m->scratch.ensure(sizeof(double) * 2 * std::max<int64_t>(1, m->Ti - 1) * bi2));
   CUDA_TRY(m->logdiag.ensure(sizeof(double) * m->Ti));
   CUDA_TRY(m->info.ensure(sizeof(int) * 4));
   for (DevBuf* v : {&m->yhat, &m->beta, &m->alpha, &m->bhat}) CUDA_TRY(v->ensure(sizeof(double) * m->np_));
@@ -258,19 +264,21 @@ int alloc_model_buffers(gpb_model* m) {
   return GPB_OK;
 }
 
-// Cholesky plan: per step k, TRSM jobs (panel tiles) and trailing-update jobs.
+// Cholesky plan.  Per step k the panel is solved into scratch buffer k % 2:
+//   TRSM(k):    X_i = L(i,k) Dinv_k^T                      (critical stream)
+//   COL(k):     L(i,k+1) -= X_i X_{k+1}^T, i >= k+1         (critical stream, lookahead)
+//   UPD(k):     L(i,j)   -= X_i X_j^T,     i >= j >= k+2    (main stream)
+// so POTRF/TRSM of step k+1 overlap the big trailing update of step k.
 int build_chol_plan(gpb_model* m) {
   const int Ti = m->Ti;
   const int64_t bi2 = int64_t(m->bi) * m->bi;
   double* L = m->L.as<double>();
   double* D = m->Dinv.as<double>();
-  double* S = m->scratch.as<double>();
   std::vector<GemmJob> jobs;
-  m->trsm_off.assign(Ti, 0);
-  m->trsm_cnt.assign(Ti, 0);
-  m->upd_off.assign(Ti, 0);
-  m->upd_cnt.assign(Ti, 0);
+  for (auto* v : {&m->trsm_off, &m->trsm_cnt, &m->col_off, &m->col_cnt, &m->upd_off, &m->upd_cnt})
+    v->assign(Ti, 0);
   for (int k = 0; k < Ti; ++k) {
+    double* S = m->scratch.as<double>() + int64_t(k % 2) * std::max(1, Ti - 1) * bi2;
     m->trsm_off[k] = jobs.size();
     for (int i = k + 1; i < Ti; ++i) {
       GemmJob j{};
@@ -281,9 +289,20 @@ int build_chol_plan(gpb_model* m) {
       jobs.push_back(j);
     }
     m->trsm_cnt[k] = jobs.size() - m->trsm_off[k];
+    m->col_off[k] = jobs.size();
+    for (int i = k + 1; i < Ti; ++i) {
+      GemmJob j{};
+      j.A = S + int64_t(i - k - 1) * bi2;
+      j.B = S;
+      j.Cin = j.Cout = L + h_tri_rm(i, k + 1) * bi2;
+      j.K = m->bi;
+      j.lower = (i == k + 1);
+      jobs.push_back(j);
+    }
+    m->col_cnt[k] = jobs.size() - m->col_off[k];
     m->upd_off[k] = jobs.size();
-    for (int i = k + 1; i < Ti; ++i)
-      for (int jj = k + 1; jj <= i; ++jj) {
+    for (int i = k + 2; i < Ti; ++i)
+      for (int jj = k + 2; jj <= i; ++jj) {
         GemmJob j{};
         j.A = S + int64_t(i - k - 1) * bi2;
         j.B = S + int64_t(jj - k - 1) * bi2;
@@ -298,6 +317,12 @@ int build_chol_plan(gpb_model* m) {
   if (!jobs.empty())
     CUDA_TRY(cudaMemcpy(m->chol_jobs.p, jobs.data(), sizeof(GemmJob) * jobs.size(),
                         cudaMemcpyHostToDevice));
+  // cross-stream events: per step, "panel solved" and "trailing update done"
+  while (m->sync_ev.size() < size_t(2 * Ti + 2)) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    m->sync_ev.push_back(e);
+  }
   m->plan_ok = true;
   return GPB_OK;
 }
@@ -377,6 +402,11 @@ int ensure_factor(gpb_model* m) {
   CUDA_TRY(cudaMemsetAsync(m->info.p, 0xff, sizeof(int), m->st));
   const GemmJob* jobs = m->chol_jobs.as<GemmJob>();
   const int nb = bi / GBM;
+  cudaEvent_t* ev_panel = m->sync_ev.data();       // [k]: TRSM(k) done (crit)
+  cudaEvent_t* ev_upd = m->sync_ev.data() + Ti;    // [k]: UPD(k) done (main)
+  // the critical stream starts after the assembly/memset on the main stream
+  CUDA_TRY(cudaEventRecord(ev_upd[Ti], m->st));
+  CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[Ti], 0));
   for (int k = 0; k < Ti; ++k) {
     PotrfArgs a{};
     a.tile = L + h_tri_rm(k, k) * bi2;
@@ -388,24 +418,42 @@ int ensure_factor(gpb_model* m) {
     a.tile_off = k * bi;
     a.bp_user = m->pm.bp_user;
     a.b_user = m->pm.b_user;
+    // tile (k,k) and column k are complete once COL(k-1) (crit, in order) and UPD(k-2) are done
+    if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[k - 2], 0));
     {
-      ProfScope ps(m, KC_POTRF, 2.0 / 3.0 * double(bi) * bi * bi);
-      CUDA_TRY(launch_potrf(a, m->st));
+      ProfScope ps(m, KC_POTRF, 2.0 / 3.0 * double(bi) * bi * bi, m->crit);
+      CUDA_TRY(launch_potrf(a, m->crit));
     }
     ++m->launches;
-    if (k + 1 < Ti) {
-      const int64_t r = Ti - k - 1;
-      GemmParams tp = base_params(jobs + m->trsm_off[k], static_cast<int>(m->trsm_cnt[k]), nb, nb,
-                                  bi, bi, bi, 1.0, 0.0);
-      GPB_TRY(gemm(m, tp, true, true, EPI_AXPBY, gemm_flops(r * nb * nb, bi)));
+    if (k + 1 == Ti) break;
+    const int64_t r = Ti - k - 1;
+    GemmParams tp = base_params(jobs + m->trsm_off[k], static_cast<int>(m->trsm_cnt[k]), nb, nb,
+                                bi, bi, bi, 1.0, 0.0);
+    GPB_TRY(gemm(m, tp, true, true, EPI_AXPBY, gemm_flops(r * nb * nb, bi), m->crit));
+    CUDA_TRY(cudaEventRecord(ev_panel[k], m->crit));
+    // lookahead: column k+1 needs UPD(k-1) (which covered columns >= k+1)
+    if (k >= 1) CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[k - 1], 0));
+    GemmParams cp = base_params(jobs + m->col_off[k], static_cast<int>(m->col_cnt[k]), nb, nb, bi,
+                                bi, bi, -1.0, 1.0);
+    GPB_TRY(gemm(m, cp, true, true, EPI_AXPBY,
+                 gemm_flops((r - 1) * nb * nb + nb * (nb + 1) / 2, bi), m->crit));
+    // main stream: copy the panel back and apply the rest of the trailing update
+    CUDA_TRY(cudaStreamWaitEvent(m->st, ev_panel[k], 0));
+    double* S = m->scratch.as<double>() + int64_t(k % 2) * std::max(1, Ti - 1) * bi2;
+    CUDA_TRY(launch_copy_panel(L, S, Ti, k, bi, m->st));
+    ++m->launches;
+    if (m->upd_cnt[k] > 0) {
+      const int64_t q = r - 1;
       GemmParams up = base_params(jobs + m->upd_off[k], static_cast<int>(m->upd_cnt[k]), nb, nb,
                                   bi, bi, bi, -1.0, 1.0);
       GPB_TRY(gemm(m, up, true, true, EPI_AXPBY,
-                   gemm_flops(r * (r - 1) / 2 * nb * nb + r * nb * (nb + 1) / 2, bi)));
-      CUDA_TRY(launch_copy_panel(L, m->scratch.as<double>(), Ti, k, bi, m->st));
-      ++m->launches;
+                   gemm_flops(q * (q - 1) / 2 * nb * nb + q * nb * (nb + 1) / 2, bi)));
     }
+    CUDA_TRY(cudaEventRecord(ev_upd[k], m->st));
   }
+  // join: the main stream waits for the last POTRF on the critical stream
+  CUDA_TRY(cudaEventRecord(ev_panel[Ti - 1], m->crit));
+  CUDA_TRY(cudaStreamWaitEvent(m->st, ev_panel[Ti - 1], 0));
   GPB_TRY(pt.stop());
   int info = -1;
   CUDA_TRY(cudaMemcpy(&info, m->info.p, sizeof(int), cudaMemcpyDeviceToHost));
@@ -753,7 +801,10 @@ int model_create(gpb_ctx* ctx, const double* z, const double* y, int64_t n, int6
   m->pm.bp_user = (m->b % kTileAlign == 0) ? static_cast<int>(std::min<int64_t>(m->np_, 1 << 30)) : bp;
   m->pm.b_user = (m->b % kTileAlign == 0) ? m->pm.bp_user : m->b;
   int s = GPB_OK;
-  if (cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking) != cudaSuccess ||
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (cudaStreamCreateWithPriority(&m->st, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&m->crit, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
       cudaEventCreate(&m->e0) != cudaSuccess || cudaEventCreate(&m->e1) != cudaSuccess) {
     s = fail(GPB_CUDA, "stream/event creation failed");
   }
@@ -841,6 +892,8 @@ int gpb_model_destroy(gpb_model* m) {
   if (m->st) cudaStreamSynchronize(m->st);
   free_model(m);
   for (cudaEvent_t e : m->evpool) cudaEventDestroy(e);
+  for (cudaEvent_t e : m->sync_ev) cudaEventDestroy(e);
+  if (m->crit) cudaStreamDestroy(m->crit);
   if (m->e0) cudaEventDestroy(m->e0);
   if (m->e1) cudaEventDestroy(m->e1);
   if (m->st) cudaStreamDestroy(m->st);
