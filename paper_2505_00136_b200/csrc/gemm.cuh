@@ -19,7 +19,9 @@
 
 namespace gpb {
 
-constexpr int GBM = 128, GBN = 128, GBK = 16, GSTAGES = 4, GTHREADS = 256;
+// CTA tile is GBM x GBN; every job's K must be a multiple of GBK (the
+// deepest k stage any kernel configuration uses).
+constexpr int GBM = 128, GBN = 128, GBK = 32;
 
 enum GemmEpi : int { EPI_AXPBY = 0, EPI_SUMSQ = 1 };
 
@@ -43,6 +45,7 @@ struct GemmParams {
   int64_t b_ktile, b_kstride;
   double alpha, beta;
   int64_t aux_ld;            // EPI_SUMSQ: stride between 128-row partial rows
+  int64_t max_k;             // largest job K (kernel-configuration hint), 0 if unknown
 };
 
 // Host launcher (gemm.cu).  a_kmajor / b_kmajor choose operand layouts.

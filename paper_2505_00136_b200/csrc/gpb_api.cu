@@ -593,6 +593,7 @@ int loss_gradients(gpb_model* m, double out[3]) {
     GemmParams w = base_params(jobs + m->invw_off[i], i, nb, nb, bi, bi, bi, 1.0, 0.0);
     w.a_ktile = bi;
     w.a_kstride = bi2;
+    w.max_k = int64_t(i) * bi;
     GPB_TRY(gemm(m, w, true, false, EPI_AXPBY, gemm_flops(int64_t(nb) * nb, int64_t(bi) * i * (i + 1) / 2)));
     GemmParams x = base_params(jobs + m->invx_off[i], i, nb, nb, bi, bi, bi, -1.0, 0.0);
     GPB_TRY(gemm(m, x, true, false, EPI_AXPBY, gemm_flops(int64_t(i) * nb * nb, bi)));
@@ -604,6 +605,7 @@ int loss_gradients(gpb_model* m, double out[3]) {
     // K^-1 = X^T X, lower tiles (model.py:362-380)
     GemmParams kp = base_params(jobs + m->kinv_off, static_cast<int>(m->kinv_cnt), nb, nb, bi, bi,
                                 bi, 1.0, 0.0);
+    kp.max_k = int64_t(Ti) * bi;
     GPB_TRY(gemm(m, kp, false, false, EPI_AXPBY,
                  gemm_flops(int64_t(nb) * nb, int64_t(bi) * Ti * (Ti + 1) * (Ti + 2) / 6)));
     // fused trace pass (model.py:382-414 with covariance.py:196-220 regenerated)
@@ -695,6 +697,7 @@ int predict_core(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var) 
                                  mcp, -1.0, 1.0);
       w.a_ktile = bi;
       w.a_kstride = int64_t(bi) * bi;
+      w.max_k = int64_t(i) * bi;
       const int64_t blocks = int64_t(bi / GBM) * (mcp / GBN);
       GPB_TRY(gemm(m, w, true, false, EPI_AXPBY, gemm_flops(blocks, int64_t(i) * bi)));
       GemmParams v = base_params(jobs + 2 * i + 1, 1, bi / GBM, static_cast<int>(mcp / GBN), bi,
@@ -739,6 +742,7 @@ int full_cov(gpb_model* m, const double* zt_dev, int64_t mt, double* cov_host) {
   // Sigma = K** - V^T V (model.py:254-269), lower blocks
   GemmParams p = base_params(m->fc_jobs.as<GemmJob>(), static_cast<int>(nbk * (nbk + 1) / 2), 1, 1,
                              mcp, mcp, mcp, -1.0, 1.0);
+  p.max_k = m->np_;
   GPB_TRY(gemm(m, p, false, false, EPI_AXPBY, gemm_flops(nbk * (nbk + 1) / 2, m->np_)));
   CUDA_TRY(launch_symmetrize(S, mcp, mt, m->st));
   ++m->launches;
