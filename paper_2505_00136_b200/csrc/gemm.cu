@@ -123,6 +123,16 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_grouped_kernel(cons
 
   const int nk = job.K / C::BK;
   const int arow0 = mb * GBM, brow0 = nb * GBN + half * C::BN;
+  if (p.beta != 0.0 && nk > 0) {
+    // warm L2 with this CTA's C block so the epilogue's read-modify-write
+    // does not wait on HBM (128 rows x BN doubles = 128 * BN / 16 lines)
+    constexpr int kLinesPerRow = C::BN * 8 / 128;
+    for (int l = tid; l < GBM * kLinesPerRow; l += C::THREADS) {
+      const double* a = job.Cin + static_cast<int64_t>(arow0 + l / kLinesPerRow) * p.ldc + brow0 +
+                        (l % kLinesPerRow) * 16;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+    }
+  }
   StageLoader<C, AK, GBM> la;
   StageLoader<C, BK, C::BN> lb;
   la.init(job.A, p.lda, p.a_ktile, p.a_kstride, arow0, tid);
