@@ -115,6 +115,7 @@ struct gpb_model {
   int64_t adam_step = 0;
   double timing[8] = {0};
   int64_t launches = 0;
+  long long* potrf_prof = nullptr;
 
   // per-kernel-class profiling (CUDA events around each launch on st)
   struct ProfRec {
@@ -418,6 +419,7 @@ int ensure_factor(gpb_model* m) {
     a.tile_off = k * bi;
     a.bp_user = m->pm.bp_user;
     a.b_user = m->pm.b_user;
+    a.prof = m->potrf_prof;
     // tile (k,k) and column k are complete once COL(k-1) (crit, in order) and UPD(k-2) are done
     if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[k - 2], 0));
     {
@@ -450,6 +452,14 @@ int ensure_factor(gpb_model* m) {
                    gemm_flops(q * (q - 1) / 2 * nb * nb + q * nb * (nb + 1) / 2, bi)));
     }
     CUDA_TRY(cudaEventRecord(ev_upd[k], m->st));
+  }
+  if (m->potrf_prof) {  // GPB_POTRF_PROF: per-phase cycles of the tile kernel
+    long long h[8];
+    cudaStreamSynchronize(m->crit);
+    cudaMemcpy(h, m->potrf_prof, sizeof(h), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "potrf cycles: update %lld diag %lld trsm %lld zero %lld trtri %lld\n", h[0], h[1],
+            h[2], h[3], h[4]);
+    cudaMemset(m->potrf_prof, 0, sizeof(h));
   }
   // join: the main stream waits for the last POTRF on the critical stream
   CUDA_TRY(cudaEventRecord(ev_panel[Ti - 1], m->crit));
@@ -813,6 +823,10 @@ int model_create(gpb_ctx* ctx, const double* z, const double* y, int64_t n, int6
     s = fail(GPB_CUDA, "stream/event creation failed");
   }
   if (s == GPB_OK) s = alloc_model_buffers(m);
+  if (s == GPB_OK && getenv("GPB_POTRF_PROF")) {
+    cudaMalloc(&m->potrf_prof, 8 * sizeof(long long));
+    cudaMemset(m->potrf_prof, 0, 8 * sizeof(long long));
+  }
   if (s == GPB_OK) s = upload_train(m, z, y, device_ptrs);
   if (s != GPB_OK) {
     gpb_model_destroy(m);

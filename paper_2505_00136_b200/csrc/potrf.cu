@@ -33,7 +33,7 @@ GPB_DEVINL void zero_acc(double (&acc)[4][4][2]) {
 // acc += A(32 x K) * B(32 x K)^T, both k-contiguous.
 GPB_DEVINL void warp_nt(double (&acc)[4][4][2], const double* A, int64_t lda, const double* B,
                         int64_t ldb, int K, int g, int t) {
-#pragma unroll 2
+#pragma unroll 8
   for (int k = 0; k < K; k += 4) {
     double a[4], b[4];
 #pragma unroll
@@ -50,7 +50,7 @@ GPB_DEVINL void warp_nt(double (&acc)[4][4][2], const double* A, int64_t lda, co
 // acc += A(32 x K) * B(K x 32), A k-contiguous, B row-major (n contiguous).
 GPB_DEVINL void warp_nn(double (&acc)[4][4][2], const double* A, int64_t lda, const double* B,
                         int64_t ldb, int K, int g, int t) {
-#pragma unroll 2
+#pragma unroll 8
   for (int k = 0; k < K; k += 4) {
     double a[4], b[4];
 #pragma unroll
@@ -66,7 +66,7 @@ GPB_DEVINL void warp_nn(double (&acc)[4][4][2], const double* A, int64_t lda, co
 
 }  // namespace
 
-__global__ void __launch_bounds__(PT) potrf_tile_kernel(PotrfArgs a) {
+__global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
   extern __shared__ double sm[];
   double* Ld = sm;                 // [32][33] factor block
   double* Li = Ld + NB * SLD;      // [32][33] its inverse
@@ -83,6 +83,8 @@ __global__ void __launch_bounds__(PT) potrf_tile_kernel(PotrfArgs a) {
   if (tid == 0) s_fail = -1;
   double logsum = 0.0;  // meaningful in lane 0 of warp 0
   __syncthreads();
+  long long t_last = clock64(), t_acc[5] = {0, 0, 0, 0, 0};
+#define PROF_MARK(i) if (a.prof && tid == 0) { const long long now_ = clock64(); t_acc[i] += now_ - t_last; t_last = now_; }
 
   for (int p = 0; p < P; ++p) {
     const int c0 = p * NB;
@@ -103,44 +105,84 @@ __global__ void __launch_bounds__(PT) potrf_tile_kernel(PotrfArgs a) {
       }
     }
     __syncthreads();
+    PROF_MARK(0)
     // (2) factor + invert the 32x32 diagonal block (one warp)
     if (warp == 0) {
-      for (int c = 0; c < NB; ++c)
-        Ld[lane * SLD + c] = T[static_cast<int64_t>(c0 + lane) * bi + c0 + c];
-      __syncwarp();
+      // lane i keeps row i of the block in registers; the right-looking
+      // unblocked factorisation (LAPACK dpotf2 order: scale by 1/l_jj, then
+      // rank-1 update) exchanges column j through warp shuffles.
+      double r[NB];
+#pragma unroll
+      for (int c = 0; c < NB; ++c) r[c] = T[static_cast<int64_t>(c0 + lane) * bi + c0 + c];
       int fail = -1;
-      for (int j = 0; j < (a.trtri_only ? 0 : NB); ++j) {
-        const double piv = Ld[j * SLD + j];
-        if (!(piv > 0.0)) { fail = j; break; }
-        const double ljj = sqrt(piv);
-        __syncwarp();
-        if (lane > j) Ld[lane * SLD + j] /= ljj;
-        if (lane == j) Ld[j * SLD + j] = ljj;
-        __syncwarp();
-        if (lane > j) {
-          const double lij = Ld[lane * SLD + j];
-          for (int c = j + 1; c <= lane; ++c) Ld[lane * SLD + c] -= lij * Ld[c * SLD + j];
+      double my_rinv = 0.0;  // lane j: 1 / l_jj
+      if (!a.trtri_only) {
+        // critical chain per pivot: shuffle -> rsqrt -> scale -> shuffle -> fma
+        // (no divide, no log inside the chain)
+        double my_l = 1.0;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          const double piv = __shfl_sync(0xffffffffu, r[j], j);
+          if (fail < 0 && !(piv > 0.0)) fail = j;
+          const double rinv = rsqrt(piv);
+          const double ljj = piv * rinv;
+          if (lane == j) {
+            r[j] = ljj;
+            my_l = ljj;
+            my_rinv = rinv;
+          } else if (lane > j) {
+            r[j] *= rinv;
+          }
+#pragma unroll
+          for (int c = 0; c < NB; ++c) {
+            if (c > j) {
+              const double lcj = __shfl_sync(0xffffffffu, r[j], c);
+              if (lane >= c) r[c] = fma(-r[j], lcj, r[c]);
+            }
+          }
         }
-        __syncwarp();
-        if (lane == 0) {
-          const int pos = a.tile_off + c0 + j;  // padded global position
-          if (pos % a.bp_user < a.b_user) logsum += log(ljj);
-        }
+        // log-determinant partial: every lane its own pivot, fixed-order butterfly
+        const int pos = a.tile_off + c0 + lane;  // padded global position
+        const bool real = (pos % a.bp_user < a.b_user) && (fail < 0 || lane < fail);
+        const double lsum = warp_sum(real ? log(my_l) : 0.0);
+        if (lane == 0) logsum += lsum;
+      } else {
+        my_rinv = 1.0 / r[lane];  // trtri-only: lane's diagonal entry of L
       }
+#pragma unroll
+      for (int c = 0; c < NB; ++c) Ld[lane * SLD + c] = (c <= lane) ? r[c] : 0.0;
+      Li[lane * SLD + lane] = my_rinv;  // diagonal reciprocals for the inverse
+      __syncwarp();
       if (fail >= 0) {
         if (lane == 0) {
           const int pos = a.tile_off + c0 + fail;
           s_fail = (pos / a.bp_user) * a.b_user + pos % a.bp_user;
         }
       } else {
-        // column `lane` of the inverse by forward substitution
-        for (int r = 0; r < lane; ++r) Li[r * SLD + lane] = 0.0;
-        Li[lane * SLD + lane] = 1.0 / Ld[lane * SLD + lane];
-        for (int r = lane + 1; r < NB; ++r) {
-          double s = 0.0;
-          for (int k = lane; k < r; ++k) s += Ld[r * SLD + k] * Li[k * SLD + lane];
-          Li[r * SLD + lane] = -s / Ld[r * SLD + r];
+        // lane j forms column j of the inverse by forward substitution; the
+        // rows of L are shared-memory broadcasts, the column stays in registers
+        // (four interleaved partial sums keep the dependent FMA chain short)
+        double x[NB], dinv[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) dinv[i] = Li[i * SLD + i];
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+          for (int k = 0; k < NB; ++k) {
+            if (k < i) {
+              const double t_ = -Ld[i * SLD + k] * x[k];
+              if ((k & 3) == 0) s0 += t_;
+              else if ((k & 3) == 1) s1 += t_;
+              else if ((k & 3) == 2) s2 += t_;
+              else s3 += t_;
+            }
+          }
+          x[i] = ((s0 + s1) + (s2 + s3)) * dinv[i];
         }
+#pragma unroll
+        for (int i = 0; i < NB; ++i) Li[i * SLD + lane] = x[i];
         __syncwarp();
         for (int c = 0; c < NB; ++c) {
           const int64_t o = static_cast<int64_t>(c0 + lane) * bi + c0 + c;
@@ -150,6 +192,7 @@ __global__ void __launch_bounds__(PT) potrf_tile_kernel(PotrfArgs a) {
       }
     }
     __syncthreads();
+    PROF_MARK(1)
     if (s_fail >= 0) break;
     // (3) below-diagonal panel: L[r][c0:c0+32] = T[r][c0:c0+32] * Li^T
     for (int rb = p + 1 + warp; rb < (a.trtri_only ? 0 : P); rb += PT / 32) {
@@ -168,20 +211,23 @@ __global__ void __launch_bounds__(PT) potrf_tile_kernel(PotrfArgs a) {
         }
     }
     __syncthreads();
+    PROF_MARK(2)
   }
   if (s_fail >= 0) {
     if (tid == 0) *a.info = s_fail;
     return;
   }
   // zero strictly-upper 32-blocks of L and Dinv (lower-triangular results)
-  for (int64_t idx = tid; idx < static_cast<int64_t>(bi) * bi; idx += PT) {
-    const int r = static_cast<int>(idx / bi), c = static_cast<int>(idx % bi);
-    if (c / NB > r / NB) {
-      if (!a.trtri_only) T[idx] = 0.0;
-      D[idx] = 0.0;
+  for (int r = warp; r < bi; r += PT / 32) {
+    const int c_begin = (r / NB + 1) * NB;  // first column of the strictly-upper blocks
+    for (int c = c_begin + 2 * lane; c < bi; c += 64) {
+      const int64_t idx = static_cast<int64_t>(r) * bi + c;
+      if (!a.trtri_only) *reinterpret_cast<double2*>(T + idx) = make_double2(0.0, 0.0);
+      *reinterpret_cast<double2*>(D + idx) = make_double2(0.0, 0.0);
     }
   }
   __syncthreads();
+    PROF_MARK(3)
   // TRTRI: D[I][J] = -D[I][I] * sum_{K=J}^{I-1} L[I][K] D[K][J]
   double* Sw = S + warp * NB * SLD;
   for (int I = 1; I < P; ++I) {
@@ -212,6 +258,8 @@ __global__ void __launch_bounds__(PT) potrf_tile_kernel(PotrfArgs a) {
     }
     __syncthreads();
   }
+  PROF_MARK(4)
+  if (a.prof && tid == 0) for (int i = 0; i < 5; ++i) a.prof[i] += t_acc[i];
   if (tid == 0 && a.logdiag) a.logdiag[a.tile_index] = logsum;
 }
 
