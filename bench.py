@@ -39,6 +39,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "tiled Cholesky FP64 TFLOP/s (n=32768) and predict+variance test points/s"
 CFG = {"n": 32768, "m": 32768, "d": 128, "tiles": 64}
+if os.environ.get("GPB_BENCH_SMALL"):  # plumbing checks only (tests); never a bench number
+    CFG = {"n": 4096, "m": 1024, "d": 8, "tiles": 8}
 WORKLOAD = ("config 2: n_train=32768, n_test=32768, n_regressors=128, 64 tiles of 512, FP64; "
             "step = SEK assembly + tiled Cholesky + alpha solves + loss + predict_with_uncertainty")
 DATA = "synthetic: BASELINE.json mass-spring-damper generator, seed 0 (stands in for the paper's MSD data)"
@@ -296,6 +298,71 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         dist.destroy_process_group()
 
 
+def run_distributed(args, rank: int, world: int, local_rank: int):
+    """N > 1: the config-2 problem factorised 2D block-cyclic over all ranks
+    (distributed.py) with NCCL panel broadcasts, prediction sharded over test
+    points.  Strong scaling: total work fixed, value = n^3/3 flops over the
+    slowest rank's factorisation time."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_00136_b200 as gpb
+    from paper_2505_00136_b200.distributed import DistributedGP
+
+    backend = os.environ.get("GPB_DIST_BACKEND", "nccl")
+    device = int(os.environ.get("GPB_FORCE_DEVICE", local_rank))
+    torch.cuda.set_device(device)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+    else:
+        dist.init_process_group(backend)
+    n, m, d, tiles = CFG["n"], CFG["m"], CFG["d"], CFG["tiles"]
+    train, test = gpb.make_msd_dataset(n, m, d, seed=0)
+    rt = gpb.start_runtime(gpb.RuntimeConfig(device=device))
+    times = []
+    clocks = ClockSampler(device)
+    for it in range(args.warmup + args.steps):
+        if it == args.warmup:
+            dist.barrier()
+            torch.cuda.synchronize()
+            clocks.start()
+        model = DistributedGP(train, gpb.KernelParams(1.0, 1.0, 0.1), tiles)
+        model.log_likelihood()
+        model.predict_with_uncertainty(test)
+        if it >= args.warmup:
+            times.append([model.timings["factor_ms"], model.timings["solve_ms"],
+                          model.timings["predict_ms"]])
+        model.close()
+        del model
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    t = torch.tensor(np.array(times).sum(axis=0), dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    factor_ms, solve_ms, pred_ms = t.tolist()
+    K = args.steps
+    if rank == 0:
+        from paper_2505_00136_b200.distributed import process_grid
+
+        p, q = process_grid(world)
+        line = {
+            "metric": METRIC, "value": K * chol_flops(n) / (factor_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+            "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": (factor_ms + solve_ms + pred_ms) / K, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": {"workload": WORKLOAD, "parallelism": f"2D block-cyclic {p}x{q} Cholesky, "
+                       f"NCCL panel broadcasts; prediction sharded over test points"},
+            "predict_variance": {"value": K * m / (pred_ms * 1e-3), "unit": "test points/s"},
+            "phases_ms_per_step": {"factor": factor_ms / K, "solves": solve_ms / K,
+                                   "predict_variance": pred_ms / K},
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    rt.stop()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -311,6 +378,9 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
         run_reference(args, rank)
+        return
+    if world > 1 and os.environ.get("GPB_REPLICAS") != "1":
+        run_distributed(args, rank, world, local_rank)
         return
     run_ours(args, rank, world, local_rank)
 

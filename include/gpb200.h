@@ -108,6 +108,61 @@ int gpb_model_kernel_stats(gpb_model* m, double ms[8], double flops[8], int64_t 
 /* sustained FP64 tensor-pipe (DMMA.8x8x4) throughput of this GPU, TFLOP/s */
 int gpb_fp64_peak_probe(gpb_ctx* ctx, double seconds, double* tflops);
 
+/* ---- device-level tile operations (external schedulers) -------------------
+ * Used by the multi-GPU driver (2D block-cyclic tiled Cholesky, tiled.py:168-204,
+ * and blocked solves, tiled.py:215-260, scheduled across ranks).  All pointers are
+ * device pointers on the runtime's GPU; `stream` is a cudaStream_t (NULL: legacy
+ * default stream).  Tiles are b x b row-major with b a multiple of 128.
+ *
+ * gpb_layout: the padded internal layout the library uses for (n, tiles_per_dim):
+ *   out = {tile size b, tiles per dim T, padded order n_p, pad.bp, pad.b, user tile}.
+ *   A padded position P is real iff P % pad.bp < pad.b. */
+int gpb_layout(int64_t n, int64_t tiles_per_dim, int64_t out[6]);
+typedef struct gpb_tile_desc { int32_t i, j; double* ptr; } gpb_tile_desc;
+typedef struct gpb_gemm_job {
+  const double* a; const double* b; const double* cin; double* cout;
+  int32_t k; int32_t lower;  /* lower: skip 128-blocks above the block diagonal */
+} gpb_gemm_job;
+typedef struct gpb_gemv_job { const double* a; const double* x; double* y; } gpb_gemv_job;
+/* pad rows of src (n x d, or a vector when d == 0) into the padded layout (n_p rows) */
+int gpb_dev_pad(gpb_ctx* ctx, void* stream, const double* src, int64_t n_p, int64_t d,
+                int64_t pad_bp, int64_t pad_b, double* dst);
+/* SEK tiles (covariance.py:118-164): tile (i,j) of K(zp) (+ s2 on the global diagonal) */
+int gpb_dev_assemble(gpb_ctx* ctx, void* stream, const double* zp, int64_t d, int64_t b,
+                     int64_t pad_bp, int64_t pad_b, double lengthscale, double vertical_scale,
+                     double noise_variance, int add_noise, const gpb_tile_desc* tiles,
+                     int64_t ntiles);
+/* POTRF + TRTRI of one diagonal tile in place (tiles.py:132-137); writes dinv = L^-1,
+ * *logdiag_out = sum log l_jj over real pivots, *info_dev = first failing index
+ * (must be -1 on entry; the kernel is skipped when it is already >= 0) */
+int gpb_dev_potrf(gpb_ctx* ctx, void* stream, double* tile, double* dinv, int64_t b,
+                  int64_t tile_off, int64_t pad_bp, int64_t pad_b, double* logdiag_out,
+                  int* info_dev);
+/* grouped DMMA GEMM, b x b outputs: cout = alpha * a b^T + beta * cin (operand
+ * layouts per a_kmajor / b_kmajor as in the single-GPU path) */
+int gpb_dev_gemm(gpb_ctx* ctx, void* stream, const gpb_gemm_job* jobs, int64_t njobs, int64_t b,
+                 int64_t lda, int64_t ldb, int64_t ldc, int a_kmajor, int b_kmajor, double alpha,
+                 double beta);
+/* batched tile GEMV: y (+)= alpha * op(a) x; outputs must be distinct per call */
+int gpb_dev_gemv(gpb_ctx* ctx, void* stream, const gpb_gemv_job* jobs, int64_t njobs, int64_t b,
+                 int trans, double alpha, int accumulate);
+/* batched device copies of `bytes` each: dst_i <- src_i (jobs: {src, dst} pairs) */
+typedef struct gpb_copy_job { const double* src; double* dst; } gpb_copy_job;
+int gpb_dev_copy(gpb_ctx* ctx, void* stream, const gpb_copy_job* jobs, int64_t njobs, int64_t bytes);
+/* out = base - sum_p parts[p] (fixed order), vectors of length len */
+int gpb_dev_combine(gpb_ctx* ctx, void* stream, const double* base, const double* parts,
+                    int64_t nparts, int64_t len, double* out);
+/* hand a factor computed elsewhere (packed row-major lower tiles in the model's layout,
+ * inverse diagonal tiles, per-tile log-diagonal sums, beta, alpha; all device) to a
+ * model: its caches become valid and prediction / likelihood use it */
+int gpb_model_adopt_factor(gpb_model* m, const double* tiles, const double* dinv,
+                           const double* logdiag, const double* beta, const double* alpha);
+/* the model's own device buffers (written in place by an external scheduler,
+ * then published with gpb_model_mark_factored) */
+int gpb_model_factor_buffers(gpb_model* m, double** tiles, double** dinv, double** logdiag,
+                             double** beta, double** alpha);
+int gpb_model_mark_factored(gpb_model* m);
+
 /* ---- tile-kernel plugin (tiles.py:23-46, 132-164) -------------------------
  * Host buffers, fresh outputs, inputs never mutated.  Square tiles b x b;
  * trsm solves X l^T = b_in for rows x b b_in. */

@@ -58,6 +58,25 @@ SIGNATURES = {
     "gpb_model_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),
     "gpb_model_kernel_stats": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, _c_i64_p]),
     "gpb_fp64_peak_probe": (ctypes.c_int, [_vp, ctypes.c_double, _c_double_p]),
+    "gpb_layout": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, _c_i64_p]),
+    "gpb_dev_pad": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                   ctypes.c_int64, _vp]),
+    "gpb_dev_assemble": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64,
+                                        ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+                                        ctypes.c_double, ctypes.c_double, ctypes.c_int, _vp,
+                                        ctypes.c_int64]),
+    "gpb_dev_potrf": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64,
+                                     ctypes.c_int64, ctypes.c_int64, _vp, _vp]),
+    "gpb_dev_gemm": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                    ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_double, ctypes.c_double]),
+    "gpb_dev_gemv": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                    ctypes.c_double, ctypes.c_int]),
+    "gpb_dev_copy": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64]),
+    "gpb_dev_combine": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, _vp]),
+    "gpb_model_adopt_factor": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "gpb_model_factor_buffers": (ctypes.c_int, [_vp] + [ctypes.POINTER(_vp)] * 5),
+    "gpb_model_mark_factored": (ctypes.c_int, [_vp]),
     "gpb_tile_potrf": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_int64, _c_double_p]),
     "gpb_tile_trsm": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, ctypes.c_int64,
                                      ctypes.c_int64, _c_double_p]),
@@ -81,6 +100,35 @@ _STATUS = {
     10: errors.DeviceError,
     11: errors.DeviceError,
 }
+
+
+class TileDesc(ctypes.Structure):
+    """gpb_tile_desc"""
+    _fields_ = [("i", ctypes.c_int32), ("j", ctypes.c_int32), ("ptr", ctypes.c_void_p)]
+
+
+class GemmJob(ctypes.Structure):
+    """gpb_gemm_job"""
+    _fields_ = [("a", ctypes.c_void_p), ("b", ctypes.c_void_p), ("cin", ctypes.c_void_p),
+                ("cout", ctypes.c_void_p), ("k", ctypes.c_int32), ("lower", ctypes.c_int32)]
+
+
+class GemvJob(ctypes.Structure):
+    """gpb_gemv_job"""
+    _fields_ = [("a", ctypes.c_void_p), ("x", ctypes.c_void_p), ("y", ctypes.c_void_p)]
+
+
+class CopyJob(ctypes.Structure):
+    """gpb_copy_job"""
+    _fields_ = [("src", ctypes.c_void_p), ("dst", ctypes.c_void_p)]
+
+
+def layout(n: int, tiles_per_dim: int) -> dict:
+    """The library's padded internal layout for (n, tiles_per_dim) (gpb_layout)."""
+    out = (ctypes.c_int64 * 6)()
+    check(load().gpb_layout(n, tiles_per_dim, out))
+    return {"b": out[0], "T": out[1], "np": out[2], "pad_bp": out[3], "pad_b": out[4],
+            "user_b": out[5]}
 
 
 class ExtensionMissing(ImportError):

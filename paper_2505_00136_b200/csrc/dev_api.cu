@@ -1,0 +1,249 @@
+// Device-level tile operations for external schedulers (C ABI, gpb200.h).
+//
+// The multi-GPU driver (paper_2505_00136_b200/distributed.py) keeps each
+// rank's 2D block-cyclic share of the tile grid in its own device buffers and
+// schedules the right-looking tiled Cholesky (taskgp tiled.py:168-204) and the
+// blocked solves (tiled.py:215-260) step by step, exchanging panels with
+// torch.distributed collectives.  These entry points run the same sm_100a
+// kernels as the single-GPU path on caller-provided device memory and stream:
+// SEK tile assembly, POTRF/TRTRI of a diagonal tile, grouped DMMA GEMM,
+// batched tile GEMV and a fixed-order partial-sum combine.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "gemm.cuh"
+#include "gpb200.h"
+#include "kernels.cuh"
+
+using namespace gpb;
+
+extern "C" int gpb_plugin_fail(int code, const char* msg);
+
+namespace {
+
+// Ring of device memory for per-call descriptor tables (copied in stream order).
+struct DescRing {
+  std::mutex mu;
+  char* base = nullptr;
+  size_t cap = 0, head = 0;
+  void* stage(const void* host, size_t bytes, cudaStream_t s, cudaError_t* err) {
+    std::lock_guard<std::mutex> lk(mu);
+    bytes = (bytes + 255) & ~size_t(255);
+    if (!base || bytes > cap) {
+      if (base) {
+        cudaDeviceSynchronize();
+        cudaFree(base);
+      }
+      cap = std::max<size_t>(bytes, size_t(64) << 20);
+      *err = cudaMalloc(&base, cap);
+      if (*err != cudaSuccess) {
+        base = nullptr;
+        cap = 0;
+        return nullptr;
+      }
+      head = 0;
+    }
+    if (head + bytes > cap) {  // wrap: earlier tables may still be in flight
+      cudaDeviceSynchronize();
+      head = 0;
+    }
+    void* dst = base + head;
+    head += bytes;
+    *err = cudaMemcpyAsync(dst, host, bytes, cudaMemcpyHostToDevice, s);
+    return dst;
+  }
+};
+DescRing g_ring;
+
+#define DEV_TRY(x)                                                                       \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess) return gpb_plugin_fail(GPB_CUDA, cudaGetErrorString(e_));     \
+  } while (0)
+
+int check_ctx(gpb_ctx* ctx) {
+  if (!ctx || ctx != gpb_current()) return gpb_plugin_fail(GPB_NOT_RUNNING, "runtime is not running");
+  return GPB_OK;
+}
+
+SekParams make_sek(double l, double nu, double s2) {
+  SekParams sp;
+  sp.lengthscale = l;
+  sp.vertical = nu;
+  sp.noise = s2;
+  sp.neg_half_inv_l2 = -1.0 / (2.0 * (l * l));
+  return sp;
+}
+
+__global__ void copy_jobs_kernel(const gpb_copy_job* jobs, int64_t words16) {
+  const gpb_copy_job jb = jobs[blockIdx.y];
+  const double2* src = reinterpret_cast<const double2*>(jb.src);
+  double2* dst = reinterpret_cast<double2*>(jb.dst);
+  for (int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w < words16;
+       w += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[w] = src[w];
+}
+
+}  // namespace
+
+extern "C" {
+
+int gpb_dev_copy(gpb_ctx* ctx, void* stream, const gpb_copy_job* jobs, int64_t njobs, int64_t bytes) {
+  if (int s = check_ctx(ctx)) return s;
+  if (njobs <= 0 || bytes <= 0) return GPB_OK;
+  if (bytes % 16) return gpb_plugin_fail(GPB_DIM, "copy size must be a multiple of 16 bytes");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSuccess;
+  const void* dj = g_ring.stage(jobs, sizeof(gpb_copy_job) * njobs, st, &e);
+  DEV_TRY(e);
+  for (int64_t q0 = 0; q0 < njobs; q0 += 65535) {  // gridDim.y limit
+    const int64_t nq = std::min<int64_t>(65535, njobs - q0);
+    dim3 grid(static_cast<unsigned>(std::min<int64_t>(64, (bytes / 16 + 255) / 256)),
+              static_cast<unsigned>(nq));
+    copy_jobs_kernel<<<grid, 256, 0, st>>>(static_cast<const gpb_copy_job*>(dj) + q0, bytes / 16);
+    DEV_TRY(cudaGetLastError());
+  }
+  return GPB_OK;
+}
+
+int gpb_layout(int64_t n, int64_t tiles_per_dim, int64_t out[6]) {
+  if (!out) return gpb_plugin_fail(GPB_INVALID_CONFIG, "null output");
+  if (tiles_per_dim < 1 || n < 1 || n % tiles_per_dim != 0)
+    return gpb_plugin_fail(GPB_TILING, "tiles_per_dim must divide n");
+  const int64_t b = n / tiles_per_dim;
+  int64_t bp = (b + kTileAlign - 1) / kTileAlign * kTileAlign;
+  int64_t bi = 0;
+  const char* env = getenv("GPB_TILE");
+  if (b % kTileAlign == 0) {
+    const int64_t want = env ? atoll(env) : (n >= 4096 ? 512 : 256);
+    for (int64_t c : {want, int64_t(512), int64_t(256), int64_t(128)})
+      if (c > 0 && c % kTileAlign == 0 && n % c == 0) {
+        bi = c;
+        break;
+      }
+    bp = b;
+  }
+  if (!bi)
+    for (int64_t c : {512, 384, 256, 128})
+      if (bp % c == 0) {
+        bi = c;
+        break;
+      }
+  const int64_t np_ = tiles_per_dim * bp;
+  const bool dense = (b % kTileAlign == 0);
+  out[0] = bi;                                   // internal tile size
+  out[1] = np_ / bi;                             // internal tiles per dimension
+  out[2] = np_;                                  // padded order
+  out[3] = dense ? std::min<int64_t>(np_, int64_t(1) << 30) : bp;  // PadMap.bp_user
+  out[4] = dense ? out[3] : b;                   // PadMap.b_user
+  out[5] = b;                                    // user tile size
+  return GPB_OK;
+}
+
+int gpb_dev_pad(gpb_ctx* ctx, void* stream, const double* src, int64_t np_, int64_t d,
+                int64_t bp_user, int64_t b_user, double* dst) {
+  if (int s = check_ctx(ctx)) return s;
+  PadMap pm{static_cast<int>(bp_user), static_cast<int>(b_user)};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DEV_TRY(d == 0 ? launch_pad_vector(src, dst, np_, pm, st)
+                 : launch_pad_rows(src, dst, np_, static_cast<int>(d), pm, st));
+  return GPB_OK;
+}
+
+int gpb_dev_assemble(gpb_ctx* ctx, void* stream, const double* zp, int64_t d, int64_t b,
+                     int64_t bp_user, int64_t b_user, double l, double nu, double s2,
+                     int add_noise, const gpb_tile_desc* tiles, int64_t ntiles) {
+  if (int s = check_ctx(ctx)) return s;
+  if (ntiles <= 0) return GPB_OK;
+  static_assert(sizeof(gpb_tile_desc) == sizeof(TileDesc), "descriptor layout");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSuccess;
+  const void* dd = g_ring.stage(tiles, sizeof(TileDesc) * ntiles, st, &e);
+  DEV_TRY(e);
+  PadMap pm{static_cast<int>(bp_user), static_cast<int>(b_user)};
+  DEV_TRY(launch_assemble_desc(static_cast<const TileDesc*>(dd), ntiles, zp, static_cast<int>(d),
+                               static_cast<int>(b), pm, make_sek(l, nu, s2), add_noise != 0, st));
+  return GPB_OK;
+}
+
+int gpb_dev_potrf(gpb_ctx* ctx, void* stream, double* tile, double* dinv, int64_t b,
+                  int64_t tile_off, int64_t bp_user, int64_t b_user, double* logdiag_out,
+                  int* info_dev) {
+  if (int s = check_ctx(ctx)) return s;
+  PotrfArgs a{};
+  a.tile = tile;
+  a.dinv = dinv;
+  a.logdiag = logdiag_out;
+  a.info = info_dev;
+  a.bi = static_cast<int>(b);
+  a.tile_index = 0;
+  a.tile_off = static_cast<int>(tile_off);
+  a.bp_user = static_cast<int>(bp_user);
+  a.b_user = static_cast<int>(b_user);
+  DEV_TRY(launch_potrf(a, static_cast<cudaStream_t>(stream)));
+  return GPB_OK;
+}
+
+int gpb_dev_gemm(gpb_ctx* ctx, void* stream, const gpb_gemm_job* jobs, int64_t njobs, int64_t b,
+                 int64_t lda, int64_t ldb, int64_t ldc, int a_kmajor, int b_kmajor, double alpha,
+                 double beta) {
+  if (int s = check_ctx(ctx)) return s;
+  if (njobs <= 0) return GPB_OK;
+  if (b % GBM) return gpb_plugin_fail(GPB_DIM, "tile size must be a multiple of 128");
+  std::vector<GemmJob> gj(njobs);
+  int64_t maxk = 0;
+  for (int64_t q = 0; q < njobs; ++q) {
+    GemmJob g{};
+    g.A = jobs[q].a;
+    g.B = jobs[q].b;
+    g.Cin = jobs[q].cin;
+    g.Cout = jobs[q].cout;
+    g.K = jobs[q].k;
+    g.lower = jobs[q].lower;
+    if (g.K % GBK) return gpb_plugin_fail(GPB_DIM, "K must be a multiple of 32");
+    maxk = std::max<int64_t>(maxk, g.K);
+    gj[q] = g;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSuccess;
+  const void* dj = g_ring.stage(gj.data(), sizeof(GemmJob) * njobs, st, &e);
+  DEV_TRY(e);
+  GemmParams p{};
+  p.jobs = static_cast<const GemmJob*>(dj);
+  p.njobs = static_cast<int>(njobs);
+  p.mblk = p.nblk = static_cast<int>(b / GBM);
+  p.lda = lda;
+  p.ldb = ldb;
+  p.ldc = ldc;
+  p.a_ktile = p.b_ktile = int64_t(1) << 40;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.max_k = maxk;
+  DEV_TRY(launch_gemm(p, a_kmajor != 0, b_kmajor != 0, EPI_AXPBY, st));
+  return GPB_OK;
+}
+
+int gpb_dev_gemv(gpb_ctx* ctx, void* stream, const gpb_gemv_job* jobs, int64_t njobs, int64_t b,
+                 int trans, double alpha, int accumulate) {
+  if (int s = check_ctx(ctx)) return s;
+  if (njobs <= 0) return GPB_OK;
+  static_assert(sizeof(gpb_gemv_job) == sizeof(GemvJob), "gemv job layout");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSuccess;
+  const void* dj = g_ring.stage(jobs, sizeof(GemvJob) * njobs, st, &e);
+  DEV_TRY(e);
+  DEV_TRY(launch_gemv_jobs(static_cast<const GemvJob*>(dj), njobs, static_cast<int>(b), trans,
+                           alpha, accumulate, st));
+  return GPB_OK;
+}
+
+int gpb_dev_combine(gpb_ctx* ctx, void* stream, const double* base, const double* parts,
+                    int64_t nparts, int64_t len, double* out) {
+  if (int s = check_ctx(ctx)) return s;
+  DEV_TRY(launch_combine(base, parts, nparts, len, out, static_cast<cudaStream_t>(stream)));
+  return GPB_OK;
+}
+
+}  // extern "C"

@@ -141,21 +141,19 @@ int check_live(gpb_model* m) {
   return GPB_OK;
 }
 
-int choose_internal_tile(int64_t n, int b, int* bp, int* bi) {
-  *bp = static_cast<int>(round_up(b, kTileAlign));
-  const char* env = getenv("GPB_TILE");
-  if (b % kTileAlign == 0) {
-    // no padding: the internal tile is a free parameter (results are
-    // tiling-invariant to round-off, test_acceptance.py:135-169)
-    int want = env ? atoi(env) : (n >= 4096 ? 512 : 256);
-    for (int c : {want, 512, 256, 128}) {
-      if (c > 0 && c % kTileAlign == 0 && n % c == 0) { *bi = c; *bp = b; return GPB_OK; }
-    }
-  }
-  for (int c : {512, 384, 256, 128}) {
-    if (*bp % c == 0) { *bi = c; return GPB_OK; }
-  }
-  *bi = kTileAlign;
+// Internal layout (dev_api.cu gpb_layout): user tiles padded to multiples of
+// 128 with decoupled identity; when no padding is needed the internal tile
+// size is a free parameter (results are tiling-invariant to round-off,
+// test_acceptance.py:135-169).
+int apply_layout(gpb_model* m) {
+  int64_t lay[6];
+  if (int s = gpb_layout(m->n, m->T, lay)) return s;
+  m->bi = static_cast<int>(lay[0]);
+  m->Ti = static_cast<int>(lay[1]);
+  m->np_ = lay[2];
+  m->pm.bp_user = static_cast<int>(lay[3]);
+  m->pm.b_user = static_cast<int>(lay[4]);
+  m->bp = static_cast<int>(m->np_ / m->T);
   return GPB_OK;
 }
 
@@ -806,14 +804,10 @@ int model_create(gpb_ctx* ctx, const double* z, const double* y, int64_t n, int6
   m->d = d;
   m->T = T;
   m->b = static_cast<int>(n / T);
-  int bp = 0, bi = 0;
-  choose_internal_tile(n, m->b, &bp, &bi);
-  m->bp = bp;
-  m->bi = bi;
-  m->np_ = T * int64_t(bp);
-  m->Ti = static_cast<int>(m->np_ / bi);
-  m->pm.bp_user = (m->b % kTileAlign == 0) ? static_cast<int>(std::min<int64_t>(m->np_, 1 << 30)) : bp;
-  m->pm.b_user = (m->b % kTileAlign == 0) ? m->pm.bp_user : m->b;
+  if (int s_l = apply_layout(m)) {
+    delete m;
+    return s_l;
+  }
   int s = GPB_OK;
   int prio_lo = 0, prio_hi = 0;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
@@ -931,14 +925,7 @@ int gpb_model_set_train(gpb_model* m, const double* z, const double* y, int64_t 
   m->n = n;
   m->d = d;
   m->b = static_cast<int>(n / m->T);
-  int bp = 0, bi = 0;
-  choose_internal_tile(n, m->b, &bp, &bi);
-  m->bp = bp;
-  m->bi = bi;
-  m->np_ = m->T * int64_t(bp);
-  m->Ti = static_cast<int>(m->np_ / bi);
-  m->pm.bp_user = (m->b % kTileAlign == 0) ? static_cast<int>(std::min<int64_t>(m->np_, 1 << 30)) : bp;
-  m->pm.b_user = (m->b % kTileAlign == 0) ? m->pm.bp_user : m->b;
+  GPB_TRY(apply_layout(m));
   invalidate(m);
   GPB_TRY(alloc_model_buffers(m));
   return upload_train(m, z, y, false);
@@ -1082,6 +1069,44 @@ int gpb_predict_device(gpb_model* m, const double* zt_dev, int64_t mt, int64_t d
   if (var_dev)
     CUDA_TRY(cudaMemcpyAsync(var_dev, m->var.p, sizeof(double) * mt, cudaMemcpyDeviceToDevice, m->st));
   CUDA_TRY(cudaStreamSynchronize(m->st));
+  return GPB_OK;
+}
+
+int gpb_model_adopt_factor(gpb_model* m, const double* tiles, const double* dinv,
+                           const double* logdiag, const double* beta, const double* alpha) {
+  GPB_TRY(check_live(m));
+  if (!tiles || !dinv || !logdiag || !beta || !alpha) return fail(GPB_INVALID_CONFIG, "null argument");
+  const int64_t bi2 = int64_t(m->bi) * m->bi;
+  const int64_t ntiles = int64_t(m->Ti) * (m->Ti + 1) / 2;
+  CUDA_TRY(cudaMemcpyAsync(m->L.p, tiles, sizeof(double) * ntiles * bi2, cudaMemcpyDeviceToDevice, m->st));
+  CUDA_TRY(cudaMemcpyAsync(m->Dinv.p, dinv, sizeof(double) * m->Ti * bi2, cudaMemcpyDeviceToDevice, m->st));
+  CUDA_TRY(cudaMemcpyAsync(m->logdiag.p, logdiag, sizeof(double) * m->Ti, cudaMemcpyDeviceToDevice, m->st));
+  CUDA_TRY(cudaMemcpyAsync(m->beta.p, beta, sizeof(double) * m->np_, cudaMemcpyDeviceToDevice, m->st));
+  CUDA_TRY(cudaMemcpyAsync(m->alpha.p, alpha, sizeof(double) * m->np_, cudaMemcpyDeviceToDevice, m->st));
+  CUDA_TRY(cudaStreamSynchronize(m->st));
+  m->factor_ok = true;
+  m->weights_ok = true;
+  m->last_pivot = -1;
+  return GPB_OK;
+}
+
+int gpb_model_factor_buffers(gpb_model* m, double** tiles, double** dinv, double** logdiag,
+                             double** beta, double** alpha) {
+  GPB_TRY(check_live(m));
+  if (tiles) *tiles = m->L.as<double>();
+  if (dinv) *dinv = m->Dinv.as<double>();
+  if (logdiag) *logdiag = m->logdiag.as<double>();
+  if (beta) *beta = m->beta.as<double>();
+  if (alpha) *alpha = m->alpha.as<double>();
+  return GPB_OK;
+}
+
+int gpb_model_mark_factored(gpb_model* m) {
+  GPB_TRY(check_live(m));
+  CUDA_TRY(cudaDeviceSynchronize());
+  m->factor_ok = true;
+  m->weights_ok = true;
+  m->last_pivot = -1;
   return GPB_OK;
 }
 

@@ -39,6 +39,28 @@ cudaError_t launch_assemble_lower(double* tiles, const int2* tile_ij, int64_t t0
                                   const double* zp, int d, int bi, PadMap pm, SekParams sp,
                                   bool add_noise, cudaStream_t s);
 
+// Tile descriptor for external schedulers: tile (i, j) of the padded grid,
+// written/read at `ptr` (bi x bi row-major).  Same layout as gpb_tile_desc.
+struct TileDesc {
+  int i, j;
+  double* ptr;
+};
+cudaError_t launch_assemble_desc(const TileDesc* desc, int64_t ntiles, const double* zp, int d,
+                                 int bi, PadMap pm, SekParams sp, bool add_noise, cudaStream_t s);
+
+// Batched tile GEMV: y_q (+)= alpha * op(A_q) x_q, one (A, x, y) triple per job; every
+// job's y is written by one CTA group, so outputs must be distinct within a launch.
+struct GemvJob {
+  const double* a;
+  const double* x;
+  double* y;
+};
+cudaError_t launch_gemv_jobs(const GemvJob* jobs, int64_t njobs, int bi, int trans, double alpha,
+                             int accumulate, cudaStream_t s);
+// out[e] = base[e] - sum_{p = 0..nparts-1} parts[p * len + e]   (fixed order)
+cudaError_t launch_combine(const double* base, const double* parts, int64_t nparts, int64_t len,
+                           double* out, cudaStream_t s);
+
 // B = K*^T for one chunk of test points: rows = padded training positions
 // (np rows), cols = mcp (mc real).  Fused mean partials over 64-row blocks:
 // mpart[rb][c] = sum_{rows in rb} B[r][c] * alpha[r].

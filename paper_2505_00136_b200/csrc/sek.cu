@@ -80,22 +80,16 @@ GPB_DEVINL double block_sum(double v, double* red, int tid) {
   return red[0];
 }
 
-__global__ void __launch_bounds__(ST) assemble_lower_kernel(double* tiles, const int2* tile_ij,
-                                                            int64_t t0, const double* zp, int d,
-                                                            int bi, PadMap pm, SekParams sp,
-                                                            int add_noise) {
-  __shared__ double sa[DC][SB], sb[DC][SB];
-  const int nbs = bi / SB;
-  const int64_t t = t0 + blockIdx.x / (nbs * nbs);
-  const int blk = blockIdx.x % (nbs * nbs);
-  const int rb = blk / nbs, cb = blk % nbs;
-  const int2 ij = tile_ij[t];
+// one 64x64 block (rb, cb) of tile (ti, tj), written to `tile`
+GPB_DEVINL void assemble_block(double* tile, int ti, int tj, int rb, int cb, const double* zp,
+                               int d, int bi, PadMap pm, SekParams sp, int add_noise,
+                               double (*sa)[SB], double (*sb)[SB]) {
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int64_t P0 = static_cast<int64_t>(ij.x) * bi + rb * SB;
-  const int64_t Q0 = static_cast<int64_t>(ij.y) * bi + cb * SB;
+  const int64_t P0 = static_cast<int64_t>(ti) * bi + rb * SB;
+  const int64_t Q0 = static_cast<int64_t>(tj) * bi + cb * SB;
   Frag d2;
   sq_dists_64(d2, zp, P0, zp, Q0, d, sa, sb, tx, ty, tid);
-  double* out = tiles + t * bi * bi + static_cast<int64_t>(rb * SB) * bi + cb * SB;
+  double* out = tile + static_cast<int64_t>(rb * SB) * bi + cb * SB;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int64_t P = P0 + ty + 16 * i;
@@ -112,6 +106,30 @@ __global__ void __launch_bounds__(ST) assemble_lower_kernel(double* tiles, const
       out[static_cast<int64_t>(ty + 16 * i) * bi + tx + 16 * j] = v;
     }
   }
+}
+
+__global__ void __launch_bounds__(ST) assemble_lower_kernel(double* tiles, const int2* tile_ij,
+                                                            int64_t t0, const double* zp, int d,
+                                                            int bi, PadMap pm, SekParams sp,
+                                                            int add_noise) {
+  __shared__ double sa[DC][SB], sb[DC][SB];
+  const int nbs = bi / SB;
+  const int64_t t = t0 + blockIdx.x / (nbs * nbs);
+  const int blk = blockIdx.x % (nbs * nbs);
+  const int2 ij = tile_ij[t];
+  assemble_block(tiles + t * bi * bi, ij.x, ij.y, blk / nbs, blk % nbs, zp, d, bi, pm, sp,
+                 add_noise, sa, sb);
+}
+
+// tiles given as (i, j, destination) descriptors (external schedulers)
+__global__ void __launch_bounds__(ST) assemble_desc_kernel(const TileDesc* desc, const double* zp,
+                                                           int d, int bi, PadMap pm, SekParams sp,
+                                                           int add_noise) {
+  __shared__ double sa[DC][SB], sb[DC][SB];
+  const int nbs = bi / SB;
+  const TileDesc td = desc[blockIdx.x / (nbs * nbs)];
+  const int blk = blockIdx.x % (nbs * nbs);
+  assemble_block(td.ptr, td.i, td.j, blk / nbs, blk % nbs, zp, d, bi, pm, sp, add_noise, sa, sb);
 }
 
 __global__ void __launch_bounds__(ST) cross_kernel(double* B, int64_t ldb, double* mpart,
@@ -312,6 +330,15 @@ cudaError_t launch_assemble_lower(double* tiles, const int2* tile_ij, int64_t t0
   if (blocks <= 0) return cudaSuccess;
   assemble_lower_kernel<<<static_cast<unsigned>(blocks), ST, 0, s>>>(tiles, tile_ij, t0, zp, d, bi,
                                                                      pm, sp, add_noise ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assemble_desc(const TileDesc* desc, int64_t ntiles, const double* zp, int d,
+                                 int bi, PadMap pm, SekParams sp, bool add_noise, cudaStream_t s) {
+  const int64_t nbs = bi / SB;
+  if (ntiles <= 0) return cudaSuccess;
+  assemble_desc_kernel<<<static_cast<unsigned>(ntiles * nbs * nbs), ST, 0, s>>>(desc, zp, d, bi, pm, sp,
+                                                                               add_noise ? 1 : 0);
   return cudaGetLastError();
 }
 

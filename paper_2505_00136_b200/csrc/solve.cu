@@ -152,7 +152,67 @@ __global__ void copy_panel_kernel(double* ltiles, const double* scratch, int k, 
   dst[w] = src[w];
 }
 
+__global__ void __launch_bounds__(256) gemv_n_jobs_kernel(const GemvJob* jobs, int bi, double alpha,
+                                                          int accumulate) {
+  const int per = bi / 8;
+  const GemvJob jb = jobs[blockIdx.x / per];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = (blockIdx.x % per) * 8 + warp;
+  const double* row = jb.a + static_cast<int64_t>(r) * bi;
+  double s = 0.0;
+  for (int c = lane; c < bi; c += 32) s += row[c] * jb.x[c];
+  s = warp_sum(s);
+  if (lane == 0) jb.y[r] = (accumulate ? jb.y[r] : 0.0) + alpha * s;
+}
+
+__global__ void __launch_bounds__(256) gemv_t_jobs_kernel(const GemvJob* jobs, int bi, double alpha,
+                                                          int accumulate) {
+  __shared__ double part[8][32];
+  const int per = bi / 32;
+  const GemvJob jb = jobs[blockIdx.x / per];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = (blockIdx.x % per) * 32 + lane;
+  double s = 0.0;
+  for (int r = warp; r < bi; r += 8) s += jb.a[static_cast<int64_t>(r) * bi + c] * jb.x[r];
+  part[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += part[w][lane];
+    jb.y[c] = (accumulate ? jb.y[c] : 0.0) + alpha * t;
+  }
+}
+
+__global__ void combine_kernel(const double* base, const double* parts, int64_t nparts, int64_t len,
+                               double* out) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= len) return;
+  double s = base[e];
+  for (int64_t p = 0; p < nparts; ++p) s -= parts[p * len + e];
+  out[e] = s;
+}
+
 }  // namespace
+
+cudaError_t launch_gemv_jobs(const GemvJob* jobs, int64_t njobs, int bi, int trans, double alpha,
+                             int accumulate, cudaStream_t s) {
+  if (njobs <= 0) return cudaSuccess;
+  if (trans)
+    gemv_t_jobs_kernel<<<static_cast<unsigned>(njobs * (bi / 32)), 256, 0, s>>>(jobs, bi, alpha,
+                                                                                 accumulate);
+  else
+    gemv_n_jobs_kernel<<<static_cast<unsigned>(njobs * (bi / 8)), 256, 0, s>>>(jobs, bi, alpha,
+                                                                                accumulate);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(const double* base, const double* parts, int64_t nparts, int64_t len,
+                           double* out, cudaStream_t s) {
+  if (len <= 0) return cudaSuccess;
+  combine_kernel<<<static_cast<unsigned>((len + 255) / 256), 256, 0, s>>>(base, parts, nparts, len, out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_fwd_diag(const double* dinv, const double* yhat, double* beta, int bi,
                             cudaStream_t s) {

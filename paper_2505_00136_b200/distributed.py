@@ -1,0 +1,474 @@
+"""Multi-GPU tiled GP: 2D block-cyclic Cholesky and test-point-sharded prediction.
+
+SURVEY.md §8(e).  One process per GPU (torchrun), ranks arranged in a P x Q
+process grid (8 -> 2x4, 4 -> 2x2, 2 -> 1x2).  Lower tile (i, j) of K/L lives
+on rank (i mod P) * Q + (j mod Q).  Per step k of the right-looking tiled
+Cholesky (taskgp tiled.py:168-204):
+
+1. the owner of (k, k) runs POTRF/TRTRI on it and broadcasts L_kk^-1;
+2. the ranks of process column k mod Q solve their panel tiles (i, k) with
+   one grouped DMMA launch (X_i = L_ik L_kk^-T) into per-process-row panel
+   buffers;
+3. each process row's share of the panel is broadcast (P broadcasts of
+   packed tiles) -- the panel exchange of the north star;
+4. every rank applies the trailing update to the tiles it owns (one grouped
+   DMMA launch with K = b).
+
+The alpha solve (tiled.py:215-260) runs right-looking over tile columns:
+each rank accumulates L_ij beta_j (resp. L_ji^T alpha_j) over the tiles it
+owns; the partial vectors of segment i are all-gathered and summed in rank
+order (deterministic), then L_ii^-1 gives beta_i.  Log-determinant partials
+are gathered the same way.
+
+Prediction is sharded over test points (no collective during the solve):
+every rank gathers the full lower factor into a local single-GPU model
+(owned tiles broadcast rank by rank), predicts its slice of the test points
+and the slices are all-gathered.
+
+All collectives go through torch.distributed (NCCL on GPUs, gloo on CPU);
+all arithmetic through a tile-ops backend: ``DeviceTileOps`` runs the
+library's sm_100a kernels through the device-level C ABI on CUDA tensors
+used as buffers.  Tests drive the same schedule with a host test double.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .covariance import KernelParams
+from .data import Dataset
+from .errors import DimensionMismatch, NotPositiveDefinite, NumericalConsistencyError, TilingError
+
+_HALF_LOG_2PI = 0.5 * math.log(2.0 * math.pi)
+_VARIANCE_SLACK = 1e-9
+
+
+def process_grid(world: int) -> tuple[int, int]:
+    """P x Q with P <= Q as square as possible (2D block-cyclic grid)."""
+    p = int(math.isqrt(world))
+    while world % p:
+        p -= 1
+    return p, world // p
+
+
+class BlockCyclic:
+    """Owner map of the lower tile grid."""
+
+    def __init__(self, tiles: int, p: int, q: int):
+        self.T, self.P, self.Q = tiles, p, q
+
+    def owner(self, i: int, j: int) -> int:
+        return (i % self.P) * self.Q + (j % self.Q)
+
+    def owned(self, rank: int) -> list[tuple[int, int]]:
+        return [(i, j) for i in range(self.T) for j in range(i + 1) if self.owner(i, j) == rank]
+
+    def panel_rows(self, k: int, p: int) -> list[int]:
+        """Panel tiles i > k held by process row p at step k (in order)."""
+        return [i for i in range(k + 1, self.T) if i % self.P == p]
+
+
+class DeviceTileOps:
+    """Tile operations on CUDA tensors via the device-level C ABI (gpb_dev_*)."""
+
+    def __init__(self, runtime, device: int):
+        self.rt = runtime
+        self.device = torch.device("cuda", device)
+        self.lib = _lib.load()
+
+    # buffers --------------------------------------------------------------
+    def zeros(self, *shape, dtype=torch.float64):
+        return torch.zeros(*shape, dtype=dtype, device=self.device)
+
+    def from_numpy(self, a):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
+
+    def to_numpy(self, t):
+        return t.detach().cpu().numpy()
+
+    def _s(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    @staticmethod
+    def _p(t):
+        return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+    # kernels --------------------------------------------------------------
+    def pad(self, src, n_p: int, d: int, lay: dict):
+        out = self.zeros(n_p, d) if d else self.zeros(n_p)
+        _lib.check(self.lib.gpb_dev_pad(self.rt.handle, self._s(), self._p(src), n_p, d,
+                                        lay["pad_bp"], lay["pad_b"], self._p(out)))
+        return out
+
+    def assemble(self, zp, d, lay, params: KernelParams, add_noise, tiles):
+        if not tiles:
+            return
+        arr = (_lib.TileDesc * len(tiles))(*[_lib.TileDesc(i, j, t.data_ptr()) for i, j, t in tiles])
+        _lib.check(self.lib.gpb_dev_assemble(
+            self.rt.handle, self._s(), self._p(zp), d, lay["b"], lay["pad_bp"], lay["pad_b"],
+            params.lengthscale, params.vertical_scale, params.noise_variance, int(add_noise),
+            arr, len(tiles)))
+
+    def potrf(self, tile, dinv, lay, tile_off, logdiag_slot, info):
+        _lib.check(self.lib.gpb_dev_potrf(self.rt.handle, self._s(), self._p(tile), self._p(dinv),
+                                          lay["b"], tile_off, lay["pad_bp"], lay["pad_b"],
+                                          self._p(logdiag_slot), self._p(info)))
+
+    def gemm(self, jobs, b, alpha, beta):
+        """jobs: (a, b_op, cin, cout, k, lower) on b x b tiles, NT product."""
+        if not jobs:
+            return
+        arr = (_lib.GemmJob * len(jobs))(*[
+            _lib.GemmJob(a.data_ptr(), bb.data_ptr(), ci.data_ptr() if ci is not None else None,
+                         co.data_ptr(), k, int(lo)) for a, bb, ci, co, k, lo in jobs])
+        _lib.check(self.lib.gpb_dev_gemm(self.rt.handle, self._s(), arr, len(jobs), b, b, b, b, 1,
+                                         1, alpha, beta))
+
+    def gemv(self, jobs, b, trans, alpha, accumulate):
+        if not jobs:
+            return
+        arr = (_lib.GemvJob * len(jobs))(*[_lib.GemvJob(a.data_ptr(), x.data_ptr(), y.data_ptr())
+                                           for a, x, y in jobs])
+        _lib.check(self.lib.gpb_dev_gemv(self.rt.handle, self._s(), arr, len(jobs), b, int(trans),
+                                         alpha, int(accumulate)))
+
+    def copy(self, pairs):
+        if not pairs:
+            return
+        nbytes = pairs[0][0].numel() * 8
+        arr = (_lib.CopyJob * len(pairs))(*[_lib.CopyJob(s.data_ptr(), d.data_ptr()) for s, d in pairs])
+        _lib.check(self.lib.gpb_dev_copy(self.rt.handle, self._s(), arr, len(pairs), nbytes))
+
+    def combine(self, base, parts, out):
+        _lib.check(self.lib.gpb_dev_combine(self.rt.handle, self._s(), self._p(base), self._p(parts),
+                                            parts.shape[0], base.numel(), self._p(out)))
+
+    # replica for sharded prediction ------------------------------------------
+    def make_replica(self, train: Dataset, params: KernelParams, tiles_per_dim: int):
+        return _DeviceReplica(self, train, params, tiles_per_dim)
+
+
+class _DeviceReplica:
+    """A local single-GPU model whose factor buffers receive the gathered L."""
+
+    def __init__(self, ops: DeviceTileOps, train: Dataset, params: KernelParams, tiles_per_dim: int):
+        self.ops = ops
+        lib = ops.lib
+        self.z = ops.from_numpy(train.z)
+        self.y = ops.from_numpy(train.y)
+        h = ctypes.c_void_p()
+        _lib.check(lib.gpb_model_create_device(ops.rt.handle, ctypes.c_void_p(self.z.data_ptr()),
+                                               ctypes.c_void_p(self.y.data_ptr()), train.n, train.d,
+                                               tiles_per_dim, ctypes.byref(h)))
+        self.h = h
+        flags = (ctypes.c_uint8 * 3)(*[1 if t else 0 for t in params.trainable])
+        _lib.check(lib.gpb_model_set_params(h, params.lengthscale, params.vertical_scale,
+                                            params.noise_variance, flags))
+        ptrs = [ctypes.c_void_p() for _ in range(5)]
+        _lib.check(lib.gpb_model_factor_buffers(h, *[ctypes.byref(p) for p in ptrs]))
+        self.ptr = dict(zip(("tiles", "dinv", "logdiag", "beta", "alpha"), [p.value for p in ptrs]))
+
+    def tile_view(self, index: int, b: int):
+        """A tensor aliasing packed tile `index` of the model's factor buffer."""
+        return _alias(self.ptr["tiles"] + index * b * b * 8, (b, b), self.ops.device)
+
+    def dinv_view(self, k: int, b: int):
+        return _alias(self.ptr["dinv"] + k * b * b * 8, (b, b), self.ops.device)
+
+    def vec_view(self, name: str, n: int):
+        return _alias(self.ptr[name], (n,), self.ops.device)
+
+    def export_lower(self, n: int) -> np.ndarray:
+        return _export(self, n)
+
+    def publish(self):
+        torch.cuda.current_stream(self.ops.device).synchronize()
+        _lib.check(self.ops.lib.gpb_model_mark_factored(self.h))
+
+    def predict(self, zt: np.ndarray, want_var: bool):
+        m = zt.shape[0]
+        if m == 0:
+            return np.zeros(0), (np.zeros(0) if want_var else None)
+        ztd = self.ops.from_numpy(zt)
+        mean = self.ops.zeros(m)
+        var = self.ops.zeros(m) if want_var else None
+        _lib.check(self.ops.lib.gpb_predict_device(
+            self.h, ctypes.c_void_p(ztd.data_ptr()), m, zt.shape[1],
+            ctypes.c_void_p(mean.data_ptr()), ctypes.c_void_p(var.data_ptr()) if want_var else None))
+        return mean, var
+
+    def full_cov(self, zt: np.ndarray):
+        m = zt.shape[0]
+        mean, cov = np.empty(m), np.empty((m, m))
+        _lib.check(self.ops.lib.gpb_predict(self.h, _lib.dptr(np.ascontiguousarray(zt)), m,
+                                            zt.shape[1], _lib.dptr(mean), None, _lib.dptr(cov)))
+        return mean, cov
+
+    def close(self):
+        if self.h is not None:
+            self.ops.lib.gpb_model_destroy(self.h)
+            self.h = None
+
+
+def _alias(ptr: int, shape, device):
+    """Wrap raw device memory owned by the library as a tensor (no copy)."""
+    class _Holder:
+        __cuda_array_interface__ = {
+            "shape": tuple(shape), "typestr": "<f8", "data": (ptr, False), "version": 3,
+            "strides": None,
+        }
+    return torch.as_tensor(_Holder(), device=device)
+
+
+class DistributedGP:
+    """The GPModel contract over a torch.distributed group (one rank per GPU).
+
+    Collective: every rank must call every method with the same arguments.
+    Results are returned on every rank.
+    """
+
+    def __init__(self, train, params: KernelParams | None = None, tiles_per_dim: int = 1,
+                 ops=None, group=None, grid: tuple[int, int] | None = None):
+        train = train if isinstance(train, Dataset) else Dataset(np.asarray(train.z), np.asarray(train.y))
+        if tiles_per_dim < 1 or train.n % tiles_per_dim != 0:
+            raise TilingError(f"tiles_per_dim={tiles_per_dim} must divide the {train.n} training points")
+        self.train = train
+        self.params = params if params is not None else KernelParams()
+        self.tiles_per_dim = tiles_per_dim
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.P, self.Q = grid or process_grid(self.world)
+        if self.P * self.Q != self.world:
+            raise ValueError(f"process grid {self.P}x{self.Q} does not match {self.world} ranks")
+        if ops is None:
+            from .runtime import require_runtime
+
+            rt = require_runtime()
+            ops = DeviceTileOps(rt, rt.device)
+        self.ops = ops
+        self.lay = _lib.layout(train.n, tiles_per_dim)
+        self.b, self.T, self.np_ = self.lay["b"], self.lay["T"], self.lay["np"]
+        self.cyc = BlockCyclic(self.T, self.P, self.Q)
+        self.owned = self.cyc.owned(self.rank)
+        self.slot = {ij: s for s, ij in enumerate(self.owned)}
+        self._factored = False
+        self._replica = None
+        self.timings = {}
+
+    # -- collectives (src/dst are global ranks of the group) --------------------
+    def _bcast(self, t, src):
+        dist.broadcast(t, src=dist.get_global_rank(self.group, src) if self.group else src,
+                       group=self.group)
+
+    def _allgather(self, t):
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t.contiguous(), group=self.group)
+        return torch.stack(out)
+
+    # -- device timing (CUDA events on the launching stream) -----------------------
+    def _event(self):
+        if getattr(self.ops, "device", None) is None or self.ops.device.type != "cuda":
+            return None
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(torch.cuda.current_stream(self.ops.device))
+        return ev
+
+    @staticmethod
+    def _elapsed(a, b):
+        if a is None or b is None:
+            return None
+        b.synchronize()
+        return a.elapsed_time(b)
+
+    # -- factorisation ---------------------------------------------------------
+    def _factor(self):
+        if self._factored:
+            return
+        ops, b, T, lay = self.ops, self.b, self.T, self.lay
+        d = self.train.d
+        self.zp = ops.pad(ops.from_numpy(self.train.z), self.np_, d, lay)
+        self.yp = ops.pad(ops.from_numpy(self.train.y), self.np_, 0, lay)
+        self.L = ops.zeros(max(1, len(self.owned)), b, b)
+        self.dinv = ops.zeros(T, b, b)
+        self.logdiag = ops.zeros(T)
+        info = ops.zeros(1, dtype=torch.int32) - 1
+        ops.assemble(self.zp, d, lay, self.params, True,
+                     [(i, j, self.L[s]) for s, (i, j) in enumerate(self.owned)])
+        rows_per = -(-T // self.P)
+        panel = [ops.zeros(max(1, rows_per), b, b) for _ in range(self.P)]
+        my_p, my_q = divmod(self.rank, self.Q)
+        t0 = self._event()
+        for k in range(T):
+            own = self.cyc.owner(k, k)
+            if self.rank == own:
+                ops.potrf(self.L[self.slot[k, k]], self.dinv[k], lay, k * b, self.logdiag[k:k + 1], info)
+            self._bcast(self.dinv[k], own)
+            if k + 1 == T:
+                break
+            if my_q == k % self.Q:  # this rank holds panel tiles of column k
+                mine = self.cyc.panel_rows(k, my_p)
+                ops.gemm([(self.L[self.slot[i, k]], self.dinv[k], None, panel[my_p][s], b, False)
+                          for s, i in enumerate(mine)], b, 1.0, 0.0)
+                ops.copy([(panel[my_p][s], self.L[self.slot[i, k]]) for s, i in enumerate(mine)])
+            where = {}
+            for p in range(self.P):
+                rows = self.cyc.panel_rows(k, p)
+                for s, i in enumerate(rows):
+                    where[i] = panel[p][s]
+                if rows:
+                    self._bcast(panel[p][:len(rows)], p * self.Q + k % self.Q)
+            ops.gemm([(where[i], where[j], self.L[s], self.L[s], b, i == j)
+                      for s, (i, j) in enumerate(self.owned) if j > k], b, -1.0, 1.0)
+        t1 = self._event()
+        infos = self._allgather(info).view(-1).cpu().numpy()
+        bad = [int(v) for v in infos if v >= 0]
+        if bad:
+            raise NotPositiveDefinite(
+                f"Matrix is not positive definite (non-positive pivot at index {min(bad)})")
+        t2 = self._event()
+        self._solve()
+        t3 = self._event()
+        self.timings = {"factor_ms": self._elapsed(t0, t1), "solve_ms": self._elapsed(t2, t3)}
+        self._factored = True
+
+    def _solve(self):
+        ops, b, T = self.ops, self.b, self.T
+        self.beta = ops.zeros(self.np_)
+        self.alpha = ops.zeros(self.np_)
+        acc = ops.zeros(self.np_)
+        tmp = ops.zeros(b)
+        seg = lambda i: slice(i * b, (i + 1) * b)  # noqa: E731
+        col = {}
+        for (i, j) in self.owned:
+            col.setdefault(j, []).append(i)
+        for i in range(T):  # beta = L^-1 y
+            parts = self._allgather(acc[seg(i)])
+            ops.combine(self.yp[seg(i)], parts, tmp)
+            ops.gemv([(self.dinv[i], tmp, self.beta[seg(i)])], b, False, 1.0, False)
+            ops.gemv([(self.L[self.slot[r, i]], self.beta[seg(i)], acc[seg(r)])
+                      for r in col.get(i, []) if r > i], b, False, 1.0, True)
+        acc.zero_()
+        row = {}
+        for (i, j) in self.owned:
+            row.setdefault(i, []).append(j)
+        for i in reversed(range(T)):  # alpha = L^-T beta
+            parts = self._allgather(acc[seg(i)])
+            ops.combine(self.beta[seg(i)], parts, tmp)
+            ops.gemv([(self.dinv[i], tmp, self.alpha[seg(i)])], b, True, 1.0, False)
+            ops.gemv([(self.L[self.slot[i, q]], self.alpha[seg(i)], acc[seg(q)])
+                      for q in row.get(i, []) if q < i], b, True, 1.0, True)
+        parts = self._allgather(self.logdiag).cpu().numpy()
+        self.logdiag_total = parts.sum(axis=0)  # one owner per tile: exact
+
+    # -- replica of the full factor for sharded prediction ---------------------------
+    def _ensure_replica(self):
+        self._factor()
+        if self._replica is not None:
+            return self._replica
+        ops, b = self.ops, self.b
+        rep = ops.make_replica(self.train, self.params, self.tiles_per_dim)
+        cap = max(len(self.cyc.owned(r)) for r in range(self.world))
+        stage = ops.zeros(max(1, cap), b, b)
+        for r in range(self.world):
+            tiles_r = self.cyc.owned(r)
+            if not tiles_r:
+                continue
+            if r == self.rank:
+                stage[:len(tiles_r)].copy_(self.L[:len(tiles_r)])
+            self._bcast(stage[:len(tiles_r)], r)
+            ops.copy([(stage[s], rep.tile_view(i * (i + 1) // 2 + j, b))
+                      for s, (i, j) in enumerate(tiles_r)])
+        rep.vec_view("beta", self.np_).copy_(self.beta)
+        rep.vec_view("alpha", self.np_).copy_(self.alpha)
+        rep.vec_view("logdiag", self.T).copy_(torch.as_tensor(self.logdiag_total).to(self.beta.device))
+        ops.copy([(self.dinv[k], rep.dinv_view(k, b)) for k in range(self.T)])
+        rep.publish()
+        self._replica = rep
+        return rep
+
+    # -- public API (model.py names) ---------------------------------------------
+    def log_likelihood(self) -> float:
+        self._factor()
+        beta = self.ops.to_numpy(self.beta)
+        half_log_det = float(sum(float(v) for v in self.logdiag_total))
+        return -half_log_det - 0.5 * float(beta @ beta) - self.train.n * _HALF_LOG_2PI
+
+    def compute_loss(self) -> float:
+        return -self.log_likelihood()
+
+    def cholesky(self) -> np.ndarray:
+        """Dense lower factor, gathered on every rank (small problems only)."""
+        return self._ensure_replica().export_lower(self.train.n)
+
+    def _shard(self, m: int) -> slice:
+        per = -(-m // self.world)
+        return slice(min(m, self.rank * per), min(m, (self.rank + 1) * per))
+
+    def _predict(self, test, want_var: bool):
+        test = test if isinstance(test, Dataset) else Dataset(np.asarray(test.z), np.asarray(test.y))
+        if test.d != self.train.d:
+            raise DimensionMismatch(f"test has {test.d} features, model was trained with {self.train.d}")
+        rep = self._ensure_replica()
+        m = test.n
+        sh = self._shard(m)
+        t0 = self._event()
+        per = -(-m // self.world)
+        mean, var = rep.predict(test.z[sh], want_var)
+        out_m = self.ops.zeros(per)
+        out_m[: sh.stop - sh.start] = torch.as_tensor(mean).to(out_m.device) if len(mean) else 0
+        gm = self._allgather(out_m).cpu().numpy().reshape(-1)[:m]
+        gv = None
+        if want_var:
+            out_v = self.ops.zeros(per)
+            out_v[: sh.stop - sh.start] = torch.as_tensor(var).to(out_v.device) if len(var) else 0
+            gv = self._allgather(out_v).cpu().numpy().reshape(-1)[:m]
+            bad = gv < -_VARIANCE_SLACK
+            if np.any(bad):
+                raise NumericalConsistencyError(
+                    f"variance {float(gv[bad].min()):g} is below the round-off allowance "
+                    f"-{_VARIANCE_SLACK:g}")
+            gv = np.where(gv < 0.0, 0.0, gv)
+        self.timings["predict_ms"] = self._elapsed(t0, self._event())
+        return gm, gv
+
+    def predict(self, test):
+        from .model import PredictionResult
+
+        mean, _ = self._predict(test, False)
+        return PredictionResult(mean=mean)
+
+    def predict_variance(self, test):
+        from .model import PredictionResult
+
+        mean, var = self._predict(test, True)
+        return PredictionResult(mean=mean, variance=var)
+
+    predict_with_uncertainty = predict_variance
+
+    def predict_with_full_cov(self, test):
+        """Full posterior covariance on every rank from its replica (not sharded yet)."""
+        from .model import PredictionResult
+
+        test = test if isinstance(test, Dataset) else Dataset(np.asarray(test.z), np.asarray(test.y))
+        if test.d != self.train.d:
+            raise DimensionMismatch(f"test has {test.d} features, model was trained with {self.train.d}")
+        mean, cov = self._ensure_replica().full_cov(test.z)
+        return PredictionResult(mean=mean, full_covariance=cov)
+
+    def close(self):
+        if self._replica is not None:
+            self._replica.close()
+            self._replica = None
+
+
+def _export(rep, n: int) -> np.ndarray:
+    out = np.empty((n, n))
+    _lib.check(rep.ops.lib.gpb_cholesky(rep.h, _lib.dptr(out)))
+    return out

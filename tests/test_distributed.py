@@ -1,0 +1,143 @@
+"""Multi-rank schedule of the 2D block-cyclic tiled GP (distributed.py).
+
+CPU: world_size 2, 3 and 4 under gloo with the host tile-ops test double,
+checked against the CPU oracle.  GPU: two ranks sharing cuda:0 under gloo run
+the real sm_100a kernels through the device-level C ABI (collectives are
+host-mediated, so the ranks never spin on each other's kernels).
+"""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _case(kind):
+    rng = np.random.default_rng(11)
+    if kind == "padded":  # b = 100 -> tiles padded to 128 (6 x 6 grid)
+        n, t, d, m = 600, 6, 3, 37
+    else:  # b = 128, no padding (GPB_TILE=128 forces an 8 x 8 grid)
+        n, t, d, m = 1024, 8, 4, 50
+    return (rng.normal(size=(n, d)), rng.normal(size=n), rng.normal(size=(m, d)), t)
+
+
+def _worker(rank, world, port, kind, device, out_q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), GPB_TILE="128")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        _body(rank, world, kind, device, out_q)
+    except BaseException as exc:  # report instead of leaving the parent waiting
+        import traceback
+
+        out_q.put((rank, "error", traceback.format_exc(), None, None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def _body(rank, world, kind, device, out_q):
+    if True:
+        import paper_2505_00136_b200 as gpb
+        from paper_2505_00136_b200.distributed import DistributedGP
+
+        z, y, zt, t = _case(kind)
+        rt = None
+        if device:
+            rt = gpb.start_runtime(gpb.RuntimeConfig(device=0))
+            ops = None
+        else:
+            from dist_host_ops import HostTileOps
+
+            ops = HostTileOps()
+        model = DistributedGP(gpb.Dataset(z, y), gpb.KernelParams(1.1, 0.9, 0.2), t, ops=ops)
+        ll = model.log_likelihood()
+        pv = model.predict_variance(gpb.Dataset(zt, np.zeros(len(zt))))
+        L = model.cholesky()
+        model.close()
+        if rt is not None:
+            rt.stop()
+        out_q.put((rank, ll, pv.mean, pv.variance, L if rank == 0 else None))
+
+
+def _run(world, kind, device=False):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, device, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    errors = [r[2] for r in res if isinstance(r[1], str)]
+    assert not errors, errors[0]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(res, key=lambda r: r[0])
+
+
+def _check(res, kind):
+    from oracle.tiled_gp import OracleGP, rel_fro
+
+    z, y, zt, t = _case(kind)
+    o = OracleGP(z, y, t, 1.1, 0.9, 0.2)
+    mean_o, var_o = o.predict_variance(zt)
+    ll_o = o.log_likelihood()
+    for rank, ll, mean, var, L in res:  # every rank returns the full result
+        assert abs(ll - ll_o) <= 1e-9 * abs(ll_o)
+        assert rel_fro(mean, mean_o) <= 1e-9
+        assert rel_fro(var, var_o) <= 1e-9
+        if L is not None:
+            assert rel_fro(L, o.factor_dense()) <= 1e-10
+
+
+@pytest.mark.parametrize("world,kind", [(2, "padded"), (3, "dense"), (4, "dense"), (4, "padded")])
+def test_block_cyclic_schedule_cpu(world, kind):
+    _check(_run(world, kind), kind)
+
+
+def test_process_grid_and_ownership():
+    from paper_2505_00136_b200.distributed import BlockCyclic, process_grid
+
+    assert process_grid(8) == (2, 4) and process_grid(4) == (2, 2) and process_grid(2) == (1, 2)
+    assert process_grid(1) == (1, 1) and process_grid(6) == (2, 3)
+    cyc = BlockCyclic(7, 2, 4)
+    owners = [cyc.owner(i, j) for i in range(7) for j in range(i + 1)]
+    assert sorted(set(owners)) == list(range(8))
+    assert sum(len(cyc.owned(r)) for r in range(8)) == 28
+    assert cyc.panel_rows(2, 1) == [3, 5]
+
+
+@pytest.mark.gpu
+def test_two_ranks_one_gpu_device_kernels():
+    _check(_run(2, "padded", device=True), "padded")
+
+
+@pytest.mark.gpu
+def test_bench_distributed_branch_two_ranks_one_gpu():
+    """bench.py's N>1 path end to end (torchrun, 2 ranks on cuda:0, gloo)."""
+    import json
+    import subprocess
+
+    env = dict(os.environ, GPB_DIST_BACKEND="gloo", GPB_FORCE_DEVICE="0", GPB_BENCH_SMALL="1")
+    out = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+         "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+         os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "3"],
+        capture_output=True, text=True, env=env, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong" and line["value"] > 0
