@@ -279,14 +279,18 @@ int build_chol_plan(gpb_model* m) {
   for (int k = 0; k < Ti; ++k) {
     double* S = m->scratch.as<double>() + int64_t(k % 2) * std::max(1, Ti - 1) * bi2;
     m->trsm_off[k] = jobs.size();
-    for (int i = k + 1; i < Ti; ++i) {
-      GemmJob j{};
-      j.A = L + h_tri_rm(i, k) * bi2;
-      j.B = D + int64_t(k) * bi2;
-      j.Cout = S + int64_t(i - k - 1) * bi2;
-      j.K = m->bi;
-      jobs.push_back(j);
-    }
+    // X_i = L(i,k) Dinv_k^T with Dinv_k lower triangular: output column block
+    // c only needs k < (c+1)*128, so each tile is split into bi/128 jobs with
+    // their own K (37.5% fewer flops at bi = 512); launched with nblk = 1.
+    for (int i = k + 1; i < Ti; ++i)
+      for (int c = 0; c < m->bi / GBN; ++c) {
+        GemmJob j{};
+        j.A = L + h_tri_rm(i, k) * bi2;
+        j.B = D + int64_t(k) * bi2 + int64_t(c) * GBN * m->bi;
+        j.Cout = S + int64_t(i - k - 1) * bi2 + c * GBN;
+        j.K = (c + 1) * GBN;
+        jobs.push_back(j);
+      }
     m->trsm_cnt[k] = jobs.size() - m->trsm_off[k];
     m->col_off[k] = jobs.size();
     for (int i = k + 1; i < Ti; ++i) {
@@ -427,9 +431,10 @@ int ensure_factor(gpb_model* m) {
     ++m->launches;
     if (k + 1 == Ti) break;
     const int64_t r = Ti - k - 1;
-    GemmParams tp = base_params(jobs + m->trsm_off[k], static_cast<int>(m->trsm_cnt[k]), nb, nb,
+    GemmParams tp = base_params(jobs + m->trsm_off[k], static_cast<int>(m->trsm_cnt[k]), nb, 1,
                                 bi, bi, bi, 1.0, 0.0);
-    GPB_TRY(gemm(m, tp, true, true, EPI_AXPBY, gemm_flops(r * nb * nb, bi), m->crit));
+    GPB_TRY(gemm(m, tp, true, true, EPI_AXPBY, gemm_flops(r * nb, int64_t(GBN) * nb * (nb + 1) / 2),
+                 m->crit));
     CUDA_TRY(cudaEventRecord(ev_panel[k], m->crit));
     // lookahead: column k+1 needs UPD(k-1) (which covered columns >= k+1)
     if (k >= 1) CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[k - 1], 0));
@@ -553,14 +558,15 @@ int build_inv_plan(gpb_model* m) {
       jobs.push_back(g);
     }
     m->invx_off[i] = jobs.size();
-    for (int j = 0; j < i; ++j) {  // X[i, j] = -Dinv_i W_j
-      GemmJob g{};
-      g.A = D + int64_t(i) * bi2;
-      g.B = Wg + int64_t(j) * bi2;
-      g.Cout = X + h_tri_cm(i, j, Ti) * bi2;
-      g.K = m->bi;
-      jobs.push_back(g);
-    }
+    for (int j = 0; j < i; ++j)  // X[i, j] = -Dinv_i W_j, row block r needs k < (r+1)*128
+      for (int r = 0; r < m->bi / GBM; ++r) {
+        GemmJob g{};
+        g.A = D + int64_t(i) * bi2 + int64_t(r) * GBM * m->bi;
+        g.B = Wg + int64_t(j) * bi2;
+        g.Cout = X + h_tri_cm(i, j, Ti) * bi2 + int64_t(r) * GBM * m->bi;
+        g.K = (r + 1) * GBM;
+        jobs.push_back(g);
+      }
   }
   m->kinv_off = jobs.size();
   for (int r = 0; r < Ti; ++r)  // longest K first
@@ -603,8 +609,9 @@ int loss_gradients(gpb_model* m, double out[3]) {
     w.a_kstride = bi2;
     w.max_k = int64_t(i) * bi;
     GPB_TRY(gemm(m, w, true, false, EPI_AXPBY, gemm_flops(int64_t(nb) * nb, int64_t(bi) * i * (i + 1) / 2)));
-    GemmParams x = base_params(jobs + m->invx_off[i], i, nb, nb, bi, bi, bi, -1.0, 0.0);
-    GPB_TRY(gemm(m, x, true, false, EPI_AXPBY, gemm_flops(int64_t(i) * nb * nb, bi)));
+    GemmParams x = base_params(jobs + m->invx_off[i], i * nb, 1, nb, bi, bi, bi, -1.0, 0.0);
+    GPB_TRY(gemm(m, x, true, false, EPI_AXPBY,
+                 gemm_flops(int64_t(i) * nb, int64_t(GBM) * nb * (nb + 1) / 2)));
   }
 
   double* red = m->red.as<double>();
@@ -666,13 +673,17 @@ int build_pred_plan(gpb_model* m, int64_t mcp) {
     w.Cout = m->W.as<double>();
     w.K = i * bi;
     jobs.push_back(w);
-    GemmJob v{};  // V_i = Dinv_i W  (+ column sum of squares)
-    v.A = D + int64_t(i) * bi2;
-    v.B = m->W.as<double>();
-    v.Cout = Bv + int64_t(i) * bi * mcp;
-    v.aux = m->sq.as<double>() + (int64_t(i) * bi / GBM) * mcp;
-    v.K = bi;
-    jobs.push_back(v);
+    // V_i = Dinv_i W (+ column sums of squares); Dinv_i is lower triangular,
+    // so output row block r only needs k < (r+1)*128: one job per row block
+    for (int r = 0; r < bi / GBM; ++r) {
+      GemmJob v{};
+      v.A = D + int64_t(i) * bi2 + int64_t(r) * GBM * bi;
+      v.B = m->W.as<double>();
+      v.Cout = Bv + (int64_t(i) * bi + r * GBM) * mcp;
+      v.aux = m->sq.as<double>() + (int64_t(i) * bi / GBM + r) * mcp;
+      v.K = (r + 1) * GBM;
+      jobs.push_back(v);
+    }
   }
   CUDA_TRY(m->pred_jobs.ensure(sizeof(GemmJob) * jobs.size()));
   CUDA_TRY(cudaMemcpy(m->pred_jobs.p, jobs.data(), sizeof(GemmJob) * jobs.size(),
@@ -701,17 +712,20 @@ int predict_core(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var) 
     PhaseTimer pt(m, 4);
     const GemmJob* jobs = m->pred_jobs.as<GemmJob>();
     for (int i = 0; i < Ti; ++i) {
-      GemmParams w = base_params(jobs + 2 * i, 1, bi / GBM, static_cast<int>(mcp / GBN), bi, mcp,
+      GemmParams w = base_params(jobs + int64_t(i) * (1 + bi / GBM), 1, bi / GBM,
+                                 static_cast<int>(mcp / GBN), bi, mcp,
                                  mcp, -1.0, 1.0);
       w.a_ktile = bi;
       w.a_kstride = int64_t(bi) * bi;
       w.max_k = int64_t(i) * bi;
       const int64_t blocks = int64_t(bi / GBM) * (mcp / GBN);
       GPB_TRY(gemm(m, w, true, false, EPI_AXPBY, gemm_flops(blocks, int64_t(i) * bi)));
-      GemmParams v = base_params(jobs + 2 * i + 1, 1, bi / GBM, static_cast<int>(mcp / GBN), bi,
-                                 mcp, mcp, 1.0, 0.0);
+      const int nbr = bi / GBM;
+      GemmParams v = base_params(jobs + int64_t(i) * (1 + nbr) + 1, nbr, 1,
+                                 static_cast<int>(mcp / GBN), bi, mcp, mcp, 1.0, 0.0);
       v.aux_ld = mcp;
-      GPB_TRY(gemm(m, v, true, false, EPI_SUMSQ, gemm_flops(blocks, bi)));
+      GPB_TRY(gemm(m, v, true, false, EPI_SUMSQ,
+                   gemm_flops(mcp / GBN, int64_t(GBM) * nbr * (nbr + 1) / 2)));
     }
     GPB_TRY(pt.stop());
   }

@@ -30,37 +30,66 @@ GPB_DEVINL void zero_acc(double (&acc)[4][4][2]) {
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 }
 
-// acc += A(32 x K) * B(32 x K)^T, both k-contiguous.
-GPB_DEVINL void warp_nt(double (&acc)[4][4][2], const double* A, int64_t lda, const double* B,
-                        int64_t ldb, int K, int g, int t) {
-#pragma unroll 8
-  for (int k = 0; k < K; k += 4) {
-    double a[4], b[4];
+// acc += A(32 x K) * B(32 x K)^T, both k-contiguous, K a multiple of 32.
+// Operands come straight from L2 (the tile is produced inside this kernel),
+// so the loop is latency-bound: fragments for a 16-deep k chunk (32 loads per
+// lane) are fetched one chunk ahead of the DMMAs that consume them.
+GPB_DEVINL void load_chunk(double (&a)[4][4], double (&b)[4][4], const double* A, int64_t lda,
+                           const double* B, int64_t ldb, int k, int g, int t) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = A[(8 * i + g) * lda + k + t];
+  for (int s = 0; s < 4; ++s)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = B[(8 * j + g) * ldb + k + t];
+    for (int i = 0; i < 4; ++i) {
+      a[s][i] = A[(8 * i + g) * lda + k + 4 * s + t];
+      b[s][i] = B[(8 * i + g) * ldb + k + 4 * s + t];
+    }
+}
+
+GPB_DEVINL void mma_chunk(double (&acc)[4][4][2], const double (&a)[4][4], const double (&b)[4][4]) {
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[s][i], b[s][j]);
+}
+
+GPB_DEVINL void warp_nt(double (&acc)[4][4][2], const double* A, int64_t lda, const double* B,
+                        int64_t ldb, int K, int g, int t) {
+  double a0[4][4], b0[4][4], a1[4][4], b1[4][4];
+  if (K <= 0) return;
+  load_chunk(a0, b0, A, lda, B, ldb, 0, g, t);
+  for (int k = 0; k < K; k += 32) {
+    load_chunk(a1, b1, A, lda, B, ldb, k + 16, g, t);
+    mma_chunk(acc, a0, b0);
+    if (k + 32 < K) load_chunk(a0, b0, A, lda, B, ldb, k + 32, g, t);
+    mma_chunk(acc, a1, b1);
   }
 }
 
-// acc += A(32 x K) * B(K x 32), A k-contiguous, B row-major (n contiguous).
+// acc += A(32 x K) * B(K x 32), A k-contiguous, B row-major (n contiguous);
+// same one-chunk-ahead fragment prefetch as warp_nt.
+GPB_DEVINL void load_chunk_nn(double (&a)[4][4], double (&b)[4][4], const double* A, int64_t lda,
+                              const double* B, int64_t ldb, int k, int g, int t) {
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      a[s][i] = A[(8 * i + g) * lda + k + 4 * s + t];
+      b[s][i] = B[(k + 4 * s + t) * ldb + 8 * i + g];
+    }
+}
+
 GPB_DEVINL void warp_nn(double (&acc)[4][4][2], const double* A, int64_t lda, const double* B,
                         int64_t ldb, int K, int g, int t) {
-#pragma unroll 8
-  for (int k = 0; k < K; k += 4) {
-    double a[4], b[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = A[(8 * i + g) * lda + k + t];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = B[(k + t) * ldb + 8 * j + g];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  double a0[4][4], b0[4][4], a1[4][4], b1[4][4];
+  if (K <= 0) return;
+  load_chunk_nn(a0, b0, A, lda, B, ldb, 0, g, t);
+  for (int k = 0; k < K; k += 32) {
+    load_chunk_nn(a1, b1, A, lda, B, ldb, k + 16, g, t);
+    mma_chunk(acc, a0, b0);
+    if (k + 32 < K) load_chunk_nn(a0, b0, A, lda, B, ldb, k + 32, g, t);
+    mma_chunk(acc, a1, b1);
   }
 }
 
@@ -88,12 +117,15 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
 
   for (int p = 0; p < P; ++p) {
     const int c0 = p * NB;
-    // (1) left-looking panel update: T[r][c0:c0+32] -= L[r][0:c0] L[c0:c0+32][0:c0]^T
+    // (1) left-looking panel update, last contribution only:
+    //     T[r][c0:c0+32] -= L[r][c0-32:c0] L[c0:c0+32][c0-32:c0]^T
+    //     (panels 0..p-2 were applied in step p-1 while warp 0 factored)
     if (p > 0 && !a.trtri_only) {
       for (int rb = p + warp; rb < P; rb += PT / 32) {
         double acc[4][4][2];
         zero_acc(acc);
-        warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi, bi, T + static_cast<int64_t>(c0) * bi, bi, c0, g, t);
+        warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi + c0 - NB, bi,
+                T + static_cast<int64_t>(c0) * bi + c0 - NB, bi, NB, g, t);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -106,6 +138,25 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
     }
     __syncthreads();
     PROF_MARK(0)
+    // (2') lookahead inside the tile: warps 1..7 apply panels 0..p-1 to panel
+    //      p+1 while warp 0 factors the diagonal block of panel p
+    if (warp > 0 && p > 0 && p + 1 < P && !a.trtri_only) {
+      const int c1 = c0 + NB;
+      for (int rb = p + warp; rb < P; rb += PT / 32 - 1) {
+        double acc[4][4][2];
+        zero_acc(acc);
+        warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi, bi, T + static_cast<int64_t>(c1) * bi,
+                bi, c0, g, t);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            double* c = T + static_cast<int64_t>(rb * NB + 8 * i + g) * bi + c1 + 8 * j + 2 * t;
+            c[0] -= acc[i][j][0];
+            c[1] -= acc[i][j][1];
+          }
+      }
+    }
     // (2) factor + invert the 32x32 diagonal block (one warp)
     if (warp == 0) {
       // lane i keeps row i of the block in registers; the right-looking
