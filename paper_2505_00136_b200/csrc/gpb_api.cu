@@ -81,6 +81,16 @@ struct gpb_ctx {
   std::mutex tile_mu;  // tile plugin calls share scratch
 };
 
+// One group of panels of the factorisation plan (build_chol_plan): job ranges
+// in the model's job array.
+constexpr int kMaxGroup = 4;
+struct CholGroup {
+  int k0, np;
+  int64_t trsm_off[kMaxGroup], trsm_cnt[kMaxGroup], in_off[kMaxGroup], in_cnt[kMaxGroup];
+  int64_t next_off, next_cnt, upd_off, upd_cnt;
+  double trsm_fl[kMaxGroup], in_fl[kMaxGroup], next_fl, upd_fl;  // executed flops per launch
+};
+
 struct gpb_model {
   gpb_ctx* ctx = nullptr;
   uint64_t gen = 0;
@@ -97,7 +107,9 @@ struct gpb_model {
 
   DevBuf zp, yp, L, Dinv, scratch, logdiag, info, yhat, beta, alpha, bhat, red, tile_rm, tile_cm,
       chol_jobs;
-  std::vector<int64_t> trsm_off, trsm_cnt, col_off, col_cnt, upd_off, upd_cnt;
+  int G = 2;  // panels per trailing-update group (GPB_PANELS)
+  std::vector<CholGroup> groups;
+  std::vector<double> chol_flops_exec;
   bool plan_ok = false, factor_ok = false, weights_ok = false;
   int64_t last_pivot = -1;
 
@@ -154,6 +166,8 @@ int apply_layout(gpb_model* m) {
   m->pm.bp_user = static_cast<int>(lay[3]);
   m->pm.b_user = static_cast<int>(lay[4]);
   m->bp = static_cast<int>(m->np_ / m->T);
+  const char* pg = getenv("GPB_PANELS");
+  m->G = std::max(1, std::min(kMaxGroup, pg ? atoi(pg) : 2));
   return GPB_OK;
 }
 
@@ -244,7 +258,7 @@ int alloc_model_buffers(gpb_model* m) {
   CUDA_TRY(m->yp.ensure(sizeof(double) * m->np_));
   CUDA_TRY(m->L.ensure(sizeof(double) * ntiles * bi2));
   CUDA_TRY(m->Dinv.ensure(sizeof(double) * m->Ti * bi2));
-  CUDA_TRY(m->scratch.ensure(sizeof(double) * 2 * std::max<int64_t>(1, m->Ti - 1) * bi2));
+  CUDA_TRY(m->scratch.ensure(sizeof(double) * 2 * m->G * std::max<int64_t>(1, m->Ti - 1) * bi2));
   CUDA_TRY(m->logdiag.ensure(sizeof(double) * m->Ti));
   CUDA_TRY(m->info.ensure(sizeof(int) * 4));
   for (DevBuf* v : {&m->yhat, &m->beta, &m->alpha, &m->bhat}) CUDA_TRY(v->ensure(sizeof(double) * m->np_));
@@ -263,65 +277,102 @@ int alloc_model_buffers(gpb_model* m) {
   return GPB_OK;
 }
 
-// Cholesky plan.  Per step k the panel is solved into scratch buffer k % 2:
-//   TRSM(k):    X_i = L(i,k) Dinv_k^T                      (critical stream)
-//   COL(k):     L(i,k+1) -= X_i X_{k+1}^T, i >= k+1         (critical stream, lookahead)
-//   UPD(k):     L(i,j)   -= X_i X_j^T,     i >= j >= k+2    (main stream)
-// so POTRF/TRSM of step k+1 overlap the big trailing update of step k.
+// Cholesky plan: panels are factored in groups of G (GPB_PANELS, default 2)
+// and the trailing matrix is updated once per group with K = G * bi, which
+// halves the read-modify-write passes over C at G = 2.  For group s
+// (panels k0 .. k0+G'-1), with the panels solved into scratch set s % 2:
+//   TRSM(k):  X_i = L(i,k) Dinv_k^T, i > k                      (critical stream)
+//   IN(k):    L(i,j) -= X_i X_j^T for k < j < k0+G', i >= j      (critical, K = bi)
+//   NEXT(s):  L(i,j) -= [X]_i [X]_j^T for the next group's columns (critical, K = G' bi)
+//   UPD(s):   L(i,j) -= [X]_i [X]_j^T for all later columns      (main stream, K = G' bi)
+// [X]_i concatenates row i of the group's panels, walked in k without a copy.
+// POTRF/TRSM/IN/NEXT of group s+1 overlap the big trailing update of group s.
 int build_chol_plan(gpb_model* m) {
-  const int Ti = m->Ti;
-  const int64_t bi2 = int64_t(m->bi) * m->bi;
+  const int Ti = m->Ti, G = m->G, bi = m->bi;
+  const int64_t bi2 = int64_t(bi) * bi;
+  const int64_t pstride = std::max(1, Ti - 1) * bi2;  // doubles between panel buffers
   double* L = m->L.as<double>();
   double* D = m->Dinv.as<double>();
   std::vector<GemmJob> jobs;
-  for (auto* v : {&m->trsm_off, &m->trsm_cnt, &m->col_off, &m->col_cnt, &m->upd_off, &m->upd_cnt})
-    v->assign(Ti, 0);
-  for (int k = 0; k < Ti; ++k) {
-    double* S = m->scratch.as<double>() + int64_t(k % 2) * std::max(1, Ti - 1) * bi2;
-    m->trsm_off[k] = jobs.size();
-    // X_i = L(i,k) Dinv_k^T with Dinv_k lower triangular: output column block
-    // c only needs k < (c+1)*128, so each tile is split into bi/128 jobs with
-    // their own K (37.5% fewer flops at bi = 512); launched with nblk = 1.
-    for (int i = k + 1; i < Ti; ++i)
-      for (int c = 0; c < m->bi / GBN; ++c) {
-        GemmJob j{};
-        j.A = L + h_tri_rm(i, k) * bi2;
-        j.B = D + int64_t(k) * bi2 + int64_t(c) * GBN * m->bi;
-        j.Cout = S + int64_t(i - k - 1) * bi2 + c * GBN;
-        j.K = (c + 1) * GBN;
-        jobs.push_back(j);
-      }
-    m->trsm_cnt[k] = jobs.size() - m->trsm_off[k];
-    m->col_off[k] = jobs.size();
-    for (int i = k + 1; i < Ti; ++i) {
-      GemmJob j{};
-      j.A = S + int64_t(i - k - 1) * bi2;
-      j.B = S;
-      j.Cin = j.Cout = L + h_tri_rm(i, k + 1) * bi2;
-      j.K = m->bi;
-      j.lower = (i == k + 1);
-      jobs.push_back(j);
+  m->groups.clear();
+  for (int k0 = 0, s = 0; k0 < Ti; k0 += G, ++s) {
+    CholGroup grp{};
+    grp.k0 = k0;
+    grp.np = std::min(G, Ti - k0);
+    double* set = m->scratch.as<double>() + int64_t(s % 2) * G * pstride;
+    auto panel_tile = [&](int g, int i) { return set + g * pstride + int64_t(i - (k0 + g) - 1) * bi2; };
+    for (int g = 0; g < grp.np; ++g) {
+      const int k = k0 + g;
+      grp.trsm_off[g] = jobs.size();
+      // Dinv_k is lower triangular: output column block c only needs k < (c+1)*128
+      for (int i = k + 1; i < Ti; ++i)
+        for (int c = 0; c < bi / GBN; ++c) {
+          GemmJob j{};
+          j.A = L + h_tri_rm(i, k) * bi2;
+          j.B = D + int64_t(k) * bi2 + int64_t(c) * GBN * bi;
+          j.Cout = panel_tile(g, i) + c * GBN;
+          j.K = (c + 1) * GBN;
+          jobs.push_back(j);
+        }
+      grp.trsm_cnt[g] = jobs.size() - grp.trsm_off[g];
+      grp.in_off[g] = jobs.size();
+      for (int jj = k + 1; jj < k0 + grp.np; ++jj)
+        for (int i = jj; i < Ti; ++i) {
+          GemmJob j{};
+          j.A = panel_tile(g, i);
+          j.B = panel_tile(g, jj);
+          j.Cin = j.Cout = L + h_tri_rm(i, jj) * bi2;
+          j.K = bi;
+          j.lower = (i == jj);
+          jobs.push_back(j);
+        }
+      grp.in_cnt[g] = jobs.size() - grp.in_off[g];
     }
-    m->col_cnt[k] = jobs.size() - m->col_off[k];
-    m->upd_off[k] = jobs.size();
-    for (int i = k + 2; i < Ti; ++i)
-      for (int jj = k + 2; jj <= i; ++jj) {
-        GemmJob j{};
-        j.A = S + int64_t(i - k - 1) * bi2;
-        j.B = S + int64_t(jj - k - 1) * bi2;
-        j.Cin = j.Cout = L + h_tri_rm(i, jj) * bi2;
-        j.K = m->bi;
-        j.lower = (i == jj);
-        jobs.push_back(j);
-      }
-    m->upd_cnt[k] = jobs.size() - m->upd_off[k];
+    // trailing updates with the whole group (tiled-k walk across the G panels)
+    const int c_next = k0 + grp.np, c_upd = std::min(Ti, c_next + G);
+    auto add_upd = [&](int jlo, int jhi) {
+      for (int i = jlo; i < Ti; ++i)
+        for (int jj = jlo; jj <= std::min(i, jhi - 1); ++jj) {
+          GemmJob j{};
+          j.A = panel_tile(0, i);
+          j.B = panel_tile(0, jj);
+          j.Cin = j.Cout = L + h_tri_rm(i, jj) * bi2;
+          j.K = grp.np * bi;
+          j.lower = (i == jj);
+          jobs.push_back(j);
+        }
+    };
+    grp.next_off = jobs.size();
+    add_upd(c_next, c_upd);
+    grp.next_cnt = jobs.size() - grp.next_off;
+    grp.upd_off = jobs.size();
+    add_upd(c_upd, Ti);
+    grp.upd_cnt = jobs.size() - grp.upd_off;
+    // executed flops of each launch (profiling): 2*128*128*K per computed block
+    const int nb = bi / GBM;
+    auto fl = [&](int64_t off, int64_t cnt, int blocks_per_job) {
+      double f = 0.0;
+      for (int64_t q = off; q < off + cnt; ++q)
+        f += 2.0 * GBM * GBN * double(jobs[q].K) *
+             (jobs[q].lower ? nb * (nb + 1) / 2 : blocks_per_job);
+      return f;
+    };
+    for (int g = 0; g < grp.np; ++g) {
+      grp.trsm_fl[g] = fl(grp.trsm_off[g], grp.trsm_cnt[g], nb);
+      grp.in_fl[g] = fl(grp.in_off[g], grp.in_cnt[g], nb * nb);
+    }
+    grp.next_fl = fl(grp.next_off, grp.next_cnt, nb * nb);
+    grp.upd_fl = fl(grp.upd_off, grp.upd_cnt, nb * nb);
+    m->groups.push_back(grp);
   }
   CUDA_TRY(m->chol_jobs.ensure(sizeof(GemmJob) * std::max<size_t>(1, jobs.size())));
   if (!jobs.empty())
     CUDA_TRY(cudaMemcpy(m->chol_jobs.p, jobs.data(), sizeof(GemmJob) * jobs.size(),
                         cudaMemcpyHostToDevice));
-  // cross-stream events: per step, "panel solved" and "trailing update done"
-  while (m->sync_ev.size() < size_t(2 * Ti + 2)) {
+  m->chol_flops_exec.assign(m->groups.size(), 0.0);
+  // cross-stream events: per group "panels solved" and "trailing update done"
+  const size_t ng = m->groups.size();
+  while (m->sync_ev.size() < 2 * ng + 2) {
     cudaEvent_t e;
     CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     m->sync_ev.push_back(e);
@@ -405,56 +456,68 @@ int ensure_factor(gpb_model* m) {
   CUDA_TRY(cudaMemsetAsync(m->info.p, 0xff, sizeof(int), m->st));
   const GemmJob* jobs = m->chol_jobs.as<GemmJob>();
   const int nb = bi / GBM;
-  cudaEvent_t* ev_panel = m->sync_ev.data();       // [k]: TRSM(k) done (crit)
-  cudaEvent_t* ev_upd = m->sync_ev.data() + Ti;    // [k]: UPD(k) done (main)
+  const int ng = static_cast<int>(m->groups.size());
+  const int64_t pstride = std::max(1, Ti - 1) * bi2;
+  cudaEvent_t* ev_panel = m->sync_ev.data();       // [s]: panels of group s solved (crit)
+  cudaEvent_t* ev_upd = m->sync_ev.data() + ng;    // [s]: UPD(s) done (main)
   // the critical stream starts after the assembly/memset on the main stream
-  CUDA_TRY(cudaEventRecord(ev_upd[Ti], m->st));
-  CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[Ti], 0));
-  for (int k = 0; k < Ti; ++k) {
-    PotrfArgs a{};
-    a.tile = L + h_tri_rm(k, k) * bi2;
-    a.dinv = D + int64_t(k) * bi2;
-    a.logdiag = m->logdiag.as<double>();
-    a.info = m->info.as<int>();
-    a.bi = bi;
-    a.tile_index = k;
-    a.tile_off = k * bi;
-    a.bp_user = m->pm.bp_user;
-    a.b_user = m->pm.b_user;
-    a.prof = m->potrf_prof;
-    // tile (k,k) and column k are complete once COL(k-1) (crit, in order) and UPD(k-2) are done
-    if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[k - 2], 0));
-    {
-      ProfScope ps(m, KC_POTRF, 2.0 / 3.0 * double(bi) * bi * bi, m->crit);
-      CUDA_TRY(launch_potrf(a, m->crit));
+  CUDA_TRY(cudaEventRecord(ev_upd[ng], m->st));
+  CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[ng], 0));
+  auto walk = [&](GemmParams p) {  // [X]_i: tiled-k walk across the group's panels
+    p.a_ktile = p.b_ktile = bi;
+    p.a_kstride = p.b_kstride = pstride - bi2;
+    return p;
+  };
+  for (int s = 0; s < ng; ++s) {
+    const CholGroup& grp = m->groups[s];
+    double* set = m->scratch.as<double>() + int64_t(s % 2) * m->G * pstride;
+    // the group's columns are complete once NEXT(s-1) (crit, in order) and UPD(s-2) are done
+    if (s >= 2) CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[s - 2], 0));
+    for (int g = 0; g < grp.np; ++g) {
+      const int k = grp.k0 + g;
+      PotrfArgs a{};
+      a.tile = L + h_tri_rm(k, k) * bi2;
+      a.dinv = D + int64_t(k) * bi2;
+      a.logdiag = m->logdiag.as<double>();
+      a.info = m->info.as<int>();
+      a.bi = bi;
+      a.tile_index = k;
+      a.tile_off = k * bi;
+      a.bp_user = m->pm.bp_user;
+      a.b_user = m->pm.b_user;
+      a.prof = m->potrf_prof;
+      {
+        ProfScope ps(m, KC_POTRF, 2.0 / 3.0 * double(bi) * bi * bi, m->crit);
+        CUDA_TRY(launch_potrf(a, m->crit));
+      }
+      ++m->launches;
+      GemmParams tp = base_params(jobs + grp.trsm_off[g], static_cast<int>(grp.trsm_cnt[g]), nb, 1,
+                                  bi, bi, bi, 1.0, 0.0);
+      GPB_TRY(gemm(m, tp, true, true, EPI_AXPBY, grp.trsm_fl[g], m->crit));
+      GemmParams ip = base_params(jobs + grp.in_off[g], static_cast<int>(grp.in_cnt[g]), nb, nb, bi,
+                                  bi, bi, -1.0, 1.0);
+      GPB_TRY(gemm(m, ip, true, true, EPI_AXPBY, grp.in_fl[g], m->crit));
     }
-    ++m->launches;
-    if (k + 1 == Ti) break;
-    const int64_t r = Ti - k - 1;
-    GemmParams tp = base_params(jobs + m->trsm_off[k], static_cast<int>(m->trsm_cnt[k]), nb, 1,
-                                bi, bi, bi, 1.0, 0.0);
-    GPB_TRY(gemm(m, tp, true, true, EPI_AXPBY, gemm_flops(r * nb, int64_t(GBN) * nb * (nb + 1) / 2),
-                 m->crit));
-    CUDA_TRY(cudaEventRecord(ev_panel[k], m->crit));
-    // lookahead: column k+1 needs UPD(k-1) (which covered columns >= k+1)
-    if (k >= 1) CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[k - 1], 0));
-    GemmParams cp = base_params(jobs + m->col_off[k], static_cast<int>(m->col_cnt[k]), nb, nb, bi,
-                                bi, bi, -1.0, 1.0);
-    GPB_TRY(gemm(m, cp, true, true, EPI_AXPBY,
-                 gemm_flops((r - 1) * nb * nb + nb * (nb + 1) / 2, bi), m->crit));
-    // main stream: copy the panel back and apply the rest of the trailing update
-    CUDA_TRY(cudaStreamWaitEvent(m->st, ev_panel[k], 0));
-    double* S = m->scratch.as<double>() + int64_t(k % 2) * std::max(1, Ti - 1) * bi2;
-    CUDA_TRY(launch_copy_panel(L, S, Ti, k, bi, m->st));
-    ++m->launches;
-    if (m->upd_cnt[k] > 0) {
-      const int64_t q = r - 1;
-      GemmParams up = base_params(jobs + m->upd_off[k], static_cast<int>(m->upd_cnt[k]), nb, nb,
-                                  bi, bi, bi, -1.0, 1.0);
-      GPB_TRY(gemm(m, up, true, true, EPI_AXPBY,
-                   gemm_flops(q * (q - 1) / 2 * nb * nb + q * nb * (nb + 1) / 2, bi)));
+    CUDA_TRY(cudaEventRecord(ev_panel[s], m->crit));
+    // lookahead: the next group's columns need UPD(s-1), which covered them
+    if (grp.next_cnt > 0) {
+      if (s >= 1) CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[s - 1], 0));
+      GemmParams np = walk(base_params(jobs + grp.next_off, static_cast<int>(grp.next_cnt), nb, nb,
+                                       bi, bi, bi, -1.0, 1.0));
+      GPB_TRY(gemm(m, np, true, true, EPI_AXPBY, grp.next_fl, m->crit));
     }
-    CUDA_TRY(cudaEventRecord(ev_upd[k], m->st));
+    // main stream: copy the panels back and apply the rest of the trailing update
+    CUDA_TRY(cudaStreamWaitEvent(m->st, ev_panel[s], 0));
+    for (int g = 0; g < grp.np; ++g) {
+      CUDA_TRY(launch_copy_panel(L, set + g * pstride, Ti, grp.k0 + g, bi, m->st));
+      ++m->launches;
+    }
+    if (grp.upd_cnt > 0) {
+      GemmParams up = walk(base_params(jobs + grp.upd_off, static_cast<int>(grp.upd_cnt), nb, nb,
+                                       bi, bi, bi, -1.0, 1.0));
+      GPB_TRY(gemm(m, up, true, true, EPI_AXPBY, grp.upd_fl));
+    }
+    CUDA_TRY(cudaEventRecord(ev_upd[s], m->st));
   }
   if (m->potrf_prof) {  // GPB_POTRF_PROF: per-phase cycles of the tile kernel
     long long h[8];
@@ -464,9 +527,9 @@ int ensure_factor(gpb_model* m) {
             h[2], h[3], h[4]);
     cudaMemset(m->potrf_prof, 0, sizeof(h));
   }
-  // join: the main stream waits for the last POTRF on the critical stream
-  CUDA_TRY(cudaEventRecord(ev_panel[Ti - 1], m->crit));
-  CUDA_TRY(cudaStreamWaitEvent(m->st, ev_panel[Ti - 1], 0));
+  // join: the main stream waits for the critical stream's last work
+  CUDA_TRY(cudaEventRecord(m->sync_ev[2 * ng + 1], m->crit));
+  CUDA_TRY(cudaStreamWaitEvent(m->st, m->sync_ev[2 * ng + 1], 0));
   GPB_TRY(pt.stop());
   int info = -1;
   CUDA_TRY(cudaMemcpy(&info, m->info.p, sizeof(int), cudaMemcpyDeviceToHost));
