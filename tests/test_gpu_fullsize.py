@@ -1,0 +1,81 @@
+"""Size-independent properties at the BASELINE.json full sizes (GPU).
+
+The CPU oracle cannot run config 2 (n = 32768, D = 128) or config 3
+(n = 65536) in test time, so parity there rests on the scaled fixtures in
+test_gpu_parity.py plus these properties of the full-size runs:
+
+* blocking invariance -- the same problem factored with internal tiles of 512
+  and of 256 (a different schedule, different rounding) agrees to 1e-10;
+* bitwise determinism across repeated runs;
+* linearity of the posterior mean in y;
+* variances inside [0, nu] and a finite, consistent likelihood.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2505_00136_b200 as gpb
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def _run(train, test, tiles, tile_env):
+    old = os.environ.get("GPB_TILE")
+    os.environ["GPB_TILE"] = str(tile_env)
+    try:
+        model = gpb.GPModel(train, gpb.KernelParams(1.0, 1.0, 0.1), tiles)
+        nll = model.compute_loss()
+        pv = model.predict_with_uncertainty(test) if test is not None else None
+        return nll, pv
+    finally:
+        if old is None:
+            os.environ.pop("GPB_TILE")
+        else:
+            os.environ["GPB_TILE"] = old
+
+
+def test_config2_blocking_invariance_and_determinism(runtime):
+    train, test = gpb.make_msd_dataset(32768, 4096, 128, seed=0)
+    nll_a, pv_a = _run(train, test, 64, 512)
+    nll_b, pv_b = _run(train, test, 64, 256)
+    nll_c, pv_c = _run(train, test, 64, 512)
+    assert abs(nll_a - nll_b) <= 1e-10 * abs(nll_a)
+    assert rel(pv_a.mean, pv_b.mean) <= 1e-9 and rel(pv_a.variance, pv_b.variance) <= 1e-10
+    assert nll_a == nll_c  # bitwise reproducible
+    assert np.array_equal(pv_a.mean, pv_c.mean) and np.array_equal(pv_a.variance, pv_c.variance)
+    assert np.all(pv_a.variance >= 0.0) and np.all(pv_a.variance <= 1.0 + 1e-12)
+
+
+def test_config2_wide_features_nondegenerate(runtime):
+    """config 2 with D = 128 is nearly diagonal; the same n with
+    D = 8 exercises a non-trivial K at the headline size."""
+    train, test = gpb.make_msd_dataset(32768, 2048, 8, seed=2)
+    nll_a, pv_a = _run(train, test, 64, 512)
+    nll_b, pv_b = _run(train, test, 64, 256)
+    assert abs(nll_a - nll_b) <= 1e-10 * abs(nll_a)
+    assert rel(pv_a.mean, pv_b.mean) <= 1e-9 and rel(pv_a.variance, pv_b.variance) <= 1e-9
+    assert np.all(pv_a.variance >= 0.0)
+
+
+def test_mean_is_linear_in_y(runtime):
+    tr, te = gpb.make_msd_dataset(16384, 1024, 8, seed=4)
+    y2 = np.sin(np.arange(tr.n) * 0.01)
+    m1 = gpb.GPModel(tr, tiles_per_dim=32).predict(te).mean
+    m2 = gpb.GPModel(gpb.Dataset(tr.z, y2), tiles_per_dim=32).predict(te).mean
+    m3 = gpb.GPModel(gpb.Dataset(tr.z, tr.y + 2.0 * y2), tiles_per_dim=32).predict(te).mean
+    assert rel(m3, m1 + 2.0 * m2) <= 1e-9
+
+
+def test_config3_factor_and_alpha_solve(runtime):
+    """BASELINE config 3 on one GPU: n = 65536, 128 tiles of 512, cholesky + alpha solve."""
+    train, _ = gpb.make_msd_dataset(65536, 0, 8, seed=0)
+    nll_a, _ = _run(train, None, 128, 512)
+    nll_b, _ = _run(train, None, 128, 256)
+    assert np.isfinite(nll_a)
+    assert abs(nll_a - nll_b) <= 1e-10 * abs(nll_a)
