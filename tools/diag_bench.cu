@@ -127,6 +127,52 @@ __device__ void diag_shift(const double* A, double* Lout, double* Linv, double* 
   Lout[lane] = Ld[lane * SLD + lane];
 }
 
+// variant 3: shared memory, uniform trip counts (predicated), unrolled by 4;
+// inverse: rolled forward substitution with the column in shared memory
+__device__ void diag_smem2(const double* A, double* Lout, double* Linv, double* Ld, double* Li) {
+  const int lane = threadIdx.x & 31;
+  for (int c = 0; c < NB; ++c) Ld[lane * SLD + c] = A[lane * NB + c];
+  __syncwarp();
+  double my_rinv = 0.0;
+#pragma unroll 1
+  for (int j = 0; j < NB; ++j) {
+    const double piv = Ld[j * SLD + j];
+    const double rinv = rsqrt(piv);
+    const double lij = (lane > j) ? Ld[lane * SLD + j] * rinv : (lane == j ? piv * rinv : 0.0);
+    if (lane == j) my_rinv = rinv;
+    __syncwarp();
+    if (lane >= j) Ld[lane * SLD + j] = lij;
+    __syncwarp();
+#pragma unroll 4
+    for (int c = j + 1; c < NB; ++c) {
+      const double lcj = Ld[c * SLD + j];
+      if (lane >= c) Ld[lane * SLD + c] = fma(-lij, lcj, Ld[lane * SLD + c]);
+    }
+    __syncwarp();
+  }
+  Li[lane * SLD + lane] = my_rinv;
+  __syncwarp();
+#pragma unroll 1
+  for (int i = 0; i < NB; ++i) {
+    double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int k = 0;
+#pragma unroll 1
+    for (; k + 3 < i; k += 4) {
+      s0 = fma(-Ld[i * SLD + k], Li[k * SLD + lane], s0);
+      s1 = fma(-Ld[i * SLD + k + 1], Li[(k + 1) * SLD + lane], s1);
+      s2 = fma(-Ld[i * SLD + k + 2], Li[(k + 2) * SLD + lane], s2);
+      s3 = fma(-Ld[i * SLD + k + 3], Li[(k + 3) * SLD + lane], s3);
+    }
+    for (; k < i; ++k) s0 = fma(-Ld[i * SLD + k], Li[k * SLD + lane], s0);
+    const double di = Li[i * SLD + i];
+    __syncwarp();
+    if (i != lane) Li[i * SLD + lane] = (i < lane) ? 0.0 : ((s0 + s1) + (s2 + s3)) * di;
+    __syncwarp();
+  }
+  for (int c = 0; c < NB; ++c) Linv[lane * NB + c] = Li[lane * SLD + c];
+  Lout[lane] = Ld[lane * SLD + lane];
+}
+
 template <int V>
 __global__ void bench(const double* A, double* Lout, double* Linv, long long* cyc, int reps) {
   __shared__ double Ld[NB * SLD], Li[NB * SLD];
@@ -134,7 +180,8 @@ __global__ void bench(const double* A, double* Lout, double* Linv, long long* cy
   for (int r = 0; r < reps; ++r) {
     if (V == 0) diag_regs(A, Lout, Linv, Ld, Li);
     else if (V == 1) diag_smem(A, Lout, Linv, Ld, Li);
-    else diag_shift(A, Lout, Linv, Ld, Li);
+    else if (V == 2) diag_shift(A, Lout, Linv, Ld, Li);
+    else diag_smem2(A, Lout, Linv, Ld, Li);
     __syncwarp();
   }
   long long t1 = clock64();
@@ -163,6 +210,14 @@ int main() {
   cudaMemcpy(got, Li, sizeof got, cudaMemcpyDeviceToHost);
   cudaMemcpy(lgot, L, sizeof lgot, cudaMemcpyDeviceToHost);
   double e = 0, el = 0;
+  for (int i = 0; i < NB * NB; ++i) e = fmax(e, fabs(got[i] - ref[i]));
+  for (int i = 0; i < NB; ++i) el = fmax(el, fabs(lgot[i] - lref[i]));
+  printf("max |Linv diff| %.3e  max |diag L diff| %.3e\n", e, el);
+  bench<3><<<1, 32>>>(A, L, Li, c, 100); cudaMemcpy(&cyc, c, 8, cudaMemcpyDeviceToHost);
+  printf("smem uniform unroll4:  %lld cycles\n", cyc);
+  cudaMemcpy(got, Li, sizeof got, cudaMemcpyDeviceToHost);
+  cudaMemcpy(lgot, L, sizeof lgot, cudaMemcpyDeviceToHost);
+  e = 0; el = 0;
   for (int i = 0; i < NB * NB; ++i) e = fmax(e, fabs(got[i] - ref[i]));
   for (int i = 0; i < NB; ++i) el = fmax(el, fabs(lgot[i] - lref[i]));
   printf("max |Linv diff| %.3e  max |diag L diff| %.3e\n", e, el);
