@@ -105,8 +105,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_grouped_kernel(cons
   const int half = blockIdx.x - lblock * C::CPB;
   const int job_id = lblock / per_job;
   const int local = lblock - job_id * per_job;
-  const int mb = local / p.nblk;
-  const int nb = local - mb * p.nblk;
+  // row blocks fastest: the CTAs that share a B column block (the big operand
+  // of the prediction sweep) are resident together and hit it in L2
+  const int nb = local / p.mblk;
+  const int mb = local - nb * p.mblk;
   const GemmJob job = p.jobs[job_id];
   if (job.lower && nb > mb) return;
 
