@@ -722,8 +722,6 @@ int build_pred_plan(gpb_model* m, int64_t mcp) {
   CUDA_TRY(m->W.ensure(sizeof(double) * int64_t(bi) * mcp));
   CUDA_TRY(m->mpart.ensure(sizeof(double) * (m->np_ / 64) * mcp));
   CUDA_TRY(m->sq.ensure(sizeof(double) * (m->np_ / GBM) * mcp));
-  CUDA_TRY(m->mean.ensure(sizeof(double) * mcp));
-  CUDA_TRY(m->var.ensure(sizeof(double) * mcp));
   double* L = m->L.as<double>();
   double* D = m->Dinv.as<double>();
   double* Bv = m->Bv.as<double>();
@@ -756,8 +754,25 @@ int build_pred_plan(gpb_model* m, int64_t mcp) {
 }
 
 // zt_dev: mt x d on device. Results (mean, var) left in m->mean / m->var (length mt).
-int predict_core(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var) {
-  GPB_TRY(ensure_weights(m));
+// Test points processed per chunk: the chunk's K*^T / V buffer (n_p x chunk)
+// must fit in device memory; GPB_PRED_CHUNK overrides (multiple of 128).
+int64_t pred_chunk(gpb_model* m, int64_t mt) {
+  const int64_t all = round_up(std::max<int64_t>(mt, 1), GBM);
+  if (const char* e = getenv("GPB_PRED_CHUNK")) {
+    const int64_t c = round_up(std::max<int64_t>(atoll(e), 1), GBM);
+    return std::min(c, all);
+  }
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const double per_col = 8.0 * double(m->np_ + m->bi + m->np_ / 64 + m->np_ / GBM + 4);
+  const double budget = std::min(48e9, 0.6 * (double(free_b) + double(m->Bv.bytes)));
+  const int64_t c = std::max<int64_t>(GBM, int64_t(budget / per_col) / GBM * GBM);
+  return std::min(c, all);
+}
+
+// one chunk of test points: results written to mean_out / var_out (device)
+int predict_chunk(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var, double* mean_out,
+                  double* var_out, double* t_cross, double* t_trsm) {
   const int Ti = m->Ti, bi = m->bi;
   const int64_t mcp = round_up(std::max<int64_t>(mt, 1), GBM);
   GPB_TRY(build_pred_plan(m, mcp));
@@ -770,6 +785,7 @@ int predict_core(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var) 
                           m->np_, zt_dev, mt, mcp, static_cast<int>(m->d), m->pm, sp, m->st));
     ++m->launches;
     GPB_TRY(pt.stop());
+    *t_cross += m->timing[3];
   }
   if (want_var) {
     PhaseTimer pt(m, 4);
@@ -791,11 +807,38 @@ int predict_core(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var) 
                    gemm_flops(mcp / GBN, int64_t(GBM) * nbr * (nbr + 1) / 2)));
     }
     GPB_TRY(pt.stop());
+    *t_trsm += m->timing[4];
   }
   CUDA_TRY(launch_pred_finalize(m->mpart.as<double>(), m->np_ / 64, m->sq.as<double>(),
-                                m->np_ / GBM, mcp, mt, m->nu, m->mean.as<double>(),
-                                want_var ? m->var.as<double>() : nullptr, m->st));
+                                m->np_ / GBM, mcp, mt, m->nu, mean_out,
+                                want_var ? var_out : nullptr, m->st));
   ++m->launches;
+  return GPB_OK;
+}
+
+// zt_dev: mt x d on device; results (mean, var) left in m->mean / m->var.
+// Test points are processed in chunks that fit in device memory;
+// single_chunk (full covariance) requires all of V at once.
+int predict_core(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var,
+                 bool single_chunk = false) {
+  GPB_TRY(ensure_weights(m));
+  const int64_t chunk = pred_chunk(m, mt);
+  const int64_t all = round_up(std::max<int64_t>(mt, 1), GBM);
+  if (single_chunk && chunk < all)
+    return fail(GPB_NO_MEMORY, "the full posterior covariance of " + std::to_string(mt) +
+                                   " test points needs V for all of them at once (" +
+                                   std::to_string(8.0 * double(m->np_) * double(all) / 1e9) +
+                                   " GB); predict in smaller batches");
+  CUDA_TRY(m->mean.ensure(sizeof(double) * all));
+  CUDA_TRY(m->var.ensure(sizeof(double) * all));
+  double t_cross = 0.0, t_trsm = 0.0;
+  for (int64_t c0 = 0; c0 < mt; c0 += chunk) {
+    const int64_t mc = std::min(chunk, mt - c0);
+    GPB_TRY(predict_chunk(m, zt_dev + c0 * m->d, mc, want_var, m->mean.as<double>() + c0,
+                          m->var.as<double>() + c0, &t_cross, &t_trsm));
+  }
+  m->timing[3] = t_cross;
+  m->timing[4] = t_trsm;
   return GPB_OK;
 }
 
@@ -1120,7 +1163,7 @@ int gpb_predict(gpb_model* m, const double* zt, int64_t mt, int64_t d, double* m
   CUDA_TRY(m->zt.ensure(sizeof(double) * mt * d));
   CUDA_TRY(cudaMemcpyAsync(m->zt.p, zt, sizeof(double) * mt * d, cudaMemcpyHostToDevice, m->st));
   const bool want_var = var || cov;
-  int s = predict_core(m, m->zt.as<double>(), mt, want_var);
+  int s = predict_core(m, m->zt.as<double>(), mt, want_var, cov != nullptr);
   if (s != GPB_OK) {
     invalidate(m);
     return s;

@@ -118,6 +118,22 @@ def test_ragged_tiles_against_oracle(runtime, n, m, t, d):
     assert rel(model.loss_gradients(), o.loss_gradients()) <= TOL
 
 
+def test_prediction_chunking(runtime, monkeypatch):
+    """Test points beyond the device-memory budget are processed in chunks;
+    every column's arithmetic is unchanged, so results are bitwise equal."""
+    from paper_2505_00136_b200.errors import DeviceError
+
+    rng = np.random.default_rng(77)
+    z, y, zt = rng.normal(size=(600, 3)), rng.normal(size=600), rng.normal(size=(700, 3))
+    model = gpb.GPModel(ds(z, y), tiles_per_dim=3)
+    ref = model.predict_variance(ds(zt))
+    monkeypatch.setenv("GPB_PRED_CHUNK", "128")
+    got = model.predict_variance(ds(zt))
+    assert np.array_equal(got.mean, ref.mean) and np.array_equal(got.variance, ref.variance)
+    with pytest.raises(DeviceError, match="full posterior covariance"):
+        model.predict_with_full_cov(ds(zt))
+
+
 def test_determinism_bitwise(runtime):
     """Fixed reduction orders: repeated runs are bitwise identical
     (the reference's determinism check, test_tiled.py:99-111)."""
