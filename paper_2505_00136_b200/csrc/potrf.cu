@@ -5,12 +5,17 @@
 // triangular solve of the hot path (panel TRSM tiles.py:140-146, vector
 // solves tiles.py:170-180, panel solves tiles.py:182-185) into DMMA products.
 //
-// Blocked left-looking Cholesky with 32-column panels; the panel update and
-// the below-diagonal solve run on the FP64 tensor pipe (DMMA.8x8x4) warp by
-// warp; the 32x32 diagonal block is factored and inverted in shared memory
-// by one warp.  TRTRI then forms Dinv = L^-1 block row by block row.
-// Epilogue: Sigma log L_jj over real (non-padding) pivots and a LAPACK-style
-// info word holding the first failing global pivot.
+// Blocked left-looking Cholesky with 32-column panels.  Per panel p:
+//   A (all warps)   last contribution (panel p-1) to panel p, DMMA warp tiles
+//   B (warp 0)      factor + invert the 32x32 diagonal block -- the serial
+//                   pivot chain, kept in registers / shuffles
+//     (warps 1..7)  concurrently: contributions of panels 0..p-1 to panel p+1
+//                   (in-tile lookahead) and block row p-1 of the inverse
+//                   Dinv = L^-1 (TRTRI interleaved with the factorisation)
+//   C (all warps)   solve the rows below the diagonal block (x Li^T)
+// so the DMMA work of the update and of TRTRI runs while the pivot chain
+// advances.  Epilogue: Sigma log L_jj over real (non-padding) pivots and a
+// LAPACK-style info word holding the first failing original pivot index.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -19,6 +24,7 @@ namespace gpb {
 namespace {
 
 constexpr int PT = 256;  // threads
+constexpr int NW = PT / 32;
 constexpr int NB = 32;   // panel width
 constexpr int SLD = NB + 1;
 
@@ -30,10 +36,9 @@ GPB_DEVINL void zero_acc(double (&acc)[4][4][2]) {
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 }
 
-// acc += A(32 x K) * B(32 x K)^T, both k-contiguous, K a multiple of 32.
 // Operands come straight from L2 (the tile is produced inside this kernel),
-// so the loop is latency-bound: fragments for a 16-deep k chunk (32 loads per
-// lane) are fetched one chunk ahead of the DMMAs that consume them.
+// so the warp GEMMs fetch the fragments of a 16-deep k chunk (32 loads per
+// lane) one chunk ahead of the DMMAs that consume them.
 GPB_DEVINL void load_chunk(double (&a)[4][4], double (&b)[4][4], const double* A, int64_t lda,
                            const double* B, int64_t ldb, int k, int g, int t) {
 #pragma unroll
@@ -42,6 +47,17 @@ GPB_DEVINL void load_chunk(double (&a)[4][4], double (&b)[4][4], const double* A
     for (int i = 0; i < 4; ++i) {
       a[s][i] = A[(8 * i + g) * lda + k + 4 * s + t];
       b[s][i] = B[(8 * i + g) * ldb + k + 4 * s + t];
+    }
+}
+
+GPB_DEVINL void load_chunk_nn(double (&a)[4][4], double (&b)[4][4], const double* A, int64_t lda,
+                              const double* B, int64_t ldb, int k, int g, int t) {
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      a[s][i] = A[(8 * i + g) * lda + k + 4 * s + t];
+      b[s][i] = B[(k + 4 * s + t) * ldb + 8 * i + g];
     }
 }
 
@@ -54,6 +70,7 @@ GPB_DEVINL void mma_chunk(double (&acc)[4][4][2], const double (&a)[4][4], const
       for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[s][i], b[s][j]);
 }
 
+// acc += A(32 x K) * B(32 x K)^T, both k-contiguous, K a multiple of 32.
 GPB_DEVINL void warp_nt(double (&acc)[4][4][2], const double* A, int64_t lda, const double* B,
                         int64_t ldb, int K, int g, int t) {
   double a0[4][4], b0[4][4], a1[4][4], b1[4][4];
@@ -67,19 +84,7 @@ GPB_DEVINL void warp_nt(double (&acc)[4][4][2], const double* A, int64_t lda, co
   }
 }
 
-// acc += A(32 x K) * B(K x 32), A k-contiguous, B row-major (n contiguous);
-// same one-chunk-ahead fragment prefetch as warp_nt.
-GPB_DEVINL void load_chunk_nn(double (&a)[4][4], double (&b)[4][4], const double* A, int64_t lda,
-                              const double* B, int64_t ldb, int k, int g, int t) {
-#pragma unroll
-  for (int s = 0; s < 4; ++s)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      a[s][i] = A[(8 * i + g) * lda + k + 4 * s + t];
-      b[s][i] = B[(k + 4 * s + t) * ldb + 8 * i + g];
-    }
-}
-
+// acc += A(32 x K) * B(K x 32), A k-contiguous, B row-major (n contiguous).
 GPB_DEVINL void warp_nn(double (&acc)[4][4][2], const double* A, int64_t lda, const double* B,
                         int64_t ldb, int K, int g, int t) {
   double a0[4][4], b0[4][4], a1[4][4], b1[4][4];
@@ -91,6 +96,44 @@ GPB_DEVINL void warp_nn(double (&acc)[4][4][2], const double* A, int64_t lda, co
     if (k + 32 < K) load_chunk_nn(a0, b0, A, lda, B, ldb, k + 32, g, t);
     mma_chunk(acc, a1, b1);
   }
+}
+
+// C[32x32 at c, ldc] -= acc  (or = acc when assign)
+GPB_DEVINL void store_acc(double* c, int64_t ldc, const double (&acc)[4][4][2], int g, int t,
+                          bool assign, double scale) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double* p = c + static_cast<int64_t>(8 * i + g) * ldc + 8 * j + 2 * t;
+      if (assign) {
+        p[0] = scale * acc[i][j][0];
+        p[1] = scale * acc[i][j][1];
+      } else {
+        p[0] -= acc[i][j][0];
+        p[1] -= acc[i][j][1];
+      }
+    }
+}
+
+// One TRTRI job: D[I][J] = -D[I][I] * sum_{K=J}^{I-1} L[I][K] D[K][J]  (32-blocks)
+GPB_DEVINL void trtri_job(double* T, double* D, int bi, int I, int J, double* Sw, int g, int t) {
+  double acc[4][4][2];
+  zero_acc(acc);
+  warp_nn(acc, T + static_cast<int64_t>(I) * NB * bi + J * NB, bi,
+          D + static_cast<int64_t>(J) * NB * bi + J * NB, bi, (I - J) * NB, g, t);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      Sw[(8 * i + g) * SLD + 8 * j + 2 * t] = acc[i][j][0];
+      Sw[(8 * i + g) * SLD + 8 * j + 2 * t + 1] = acc[i][j][1];
+    }
+  __syncwarp();
+  zero_acc(acc);
+  warp_nn(acc, D + static_cast<int64_t>(I) * NB * bi + I * NB, bi, Sw, SLD, NB, g, t);
+  store_acc(D + static_cast<int64_t>(I) * NB * bi + J * NB, bi, acc, g, t, true, -1.0);
+  __syncwarp();
 }
 
 }  // namespace
@@ -109,100 +152,93 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
   const int P = bi / NB;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
+  const bool factor = !a.trtri_only;
+  double* Sw = S + warp * NB * SLD;
   if (tid == 0) s_fail = -1;
   double logsum = 0.0;  // meaningful in lane 0 of warp 0
   __syncthreads();
   long long t_last = clock64(), t_acc[5] = {0, 0, 0, 0, 0};
-#define PROF_MARK(i) if (a.prof && tid == 0) { const long long now_ = clock64(); t_acc[i] += now_ - t_last; t_last = now_; }
+#define PROF_MARK(i)                                   \
+  if (a.prof && tid == 0) {                            \
+    const long long now_ = clock64();                  \
+    t_acc[i] += now_ - t_last;                         \
+    t_last = now_;                                     \
+  }
 
   for (int p = 0; p < P; ++p) {
     const int c0 = p * NB;
-    // (1) left-looking panel update, last contribution only:
-    //     T[r][c0:c0+32] -= L[r][c0-32:c0] L[c0:c0+32][c0-32:c0]^T
-    //     (panels 0..p-2 were applied in step p-1 while warp 0 factored)
-    if (p > 0 && !a.trtri_only) {
-      for (int rb = p + warp; rb < P; rb += PT / 32) {
+    // A: last contribution (panel p-1) to panel p, rows >= c0
+    if (p > 0 && factor) {
+      for (int rb = p + warp; rb < P; rb += NW) {
         double acc[4][4][2];
         zero_acc(acc);
         warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi + c0 - NB, bi,
                 T + static_cast<int64_t>(c0) * bi + c0 - NB, bi, NB, g, t);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            double* c = T + static_cast<int64_t>(rb * NB + 8 * i + g) * bi + c0 + 8 * j + 2 * t;
-            c[0] -= acc[i][j][0];
-            c[1] -= acc[i][j][1];
-          }
+        store_acc(T + static_cast<int64_t>(rb) * NB * bi + c0, bi, acc, g, t, false, 1.0);
       }
     }
     __syncthreads();
     PROF_MARK(0)
-    // (2') lookahead inside the tile: warps 1..7 apply panels 0..p-1 to panel
-    //      p+1 while warp 0 factors the diagonal block of panel p
-    if (warp > 0 && p > 0 && p + 1 < P && !a.trtri_only) {
-      const int c1 = c0 + NB;
-      for (int rb = p + warp; rb < P; rb += PT / 32 - 1) {
-        double acc[4][4][2];
-        zero_acc(acc);
-        warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi, bi, T + static_cast<int64_t>(c1) * bi,
-                bi, c0, g, t);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            double* c = T + static_cast<int64_t>(rb * NB + 8 * i + g) * bi + c1 + 8 * j + 2 * t;
-            c[0] -= acc[i][j][0];
-            c[1] -= acc[i][j][1];
-          }
+    if (warp > 0) {
+      // B, warps 1..7: lookahead update of panel p+1 (panels 0..p-1) and
+      // block row p-1 of the inverse, dealt round-robin
+      const int pre = (factor && p > 0 && p + 1 < P) ? P - p - 1 : 0;
+      const int inv = (p >= 2) ? p - 1 : 0;  // jobs J = 0..p-2 of row I = p-1
+      for (int q = warp - 1; q < pre + inv; q += NW - 1) {
+        if (q < pre) {
+          const int rb = p + 1 + q, c1 = c0 + NB;
+          double acc[4][4][2];
+          zero_acc(acc);
+          warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi, bi,
+                  T + static_cast<int64_t>(c1) * bi, bi, c0, g, t);
+          store_acc(T + static_cast<int64_t>(rb) * NB * bi + c1, bi, acc, g, t, false, 1.0);
+        } else {
+          trtri_job(T, D, bi, p - 1, q - pre, Sw, g, t);
+        }
       }
-    }
-    // (2) factor + invert the 32x32 diagonal block (one warp)
-    if (warp == 0) {
-      // lane i keeps row i of the block in registers; the right-looking
-      // unblocked factorisation (LAPACK dpotf2 order: scale by 1/l_jj, then
-      // rank-1 update) exchanges column j through warp shuffles.
+    } else {
+      // B, warp 0: lane i keeps row i of the diagonal block in registers,
+      // shifted so that register 0 always holds the current pivot column
+      // (short code: the pivot loop is not unrolled; LAPACK dpotf2 order)
       double r[NB];
 #pragma unroll
       for (int c = 0; c < NB; ++c) r[c] = T[static_cast<int64_t>(c0 + lane) * bi + c0 + c];
       int fail = -1;
-      double my_rinv = 0.0;  // lane j: 1 / l_jj
-      if (!a.trtri_only) {
-        // critical chain per pivot: shuffle -> rsqrt -> scale -> shuffle -> fma
-        // (no divide, no log inside the chain)
-        double my_l = 1.0;
-#pragma unroll
+      double my_l = 1.0, my_rinv = 0.0;
+      if (factor) {
+#pragma unroll 1
         for (int j = 0; j < NB; ++j) {
-          const double piv = __shfl_sync(0xffffffffu, r[j], j);
+          const double piv = __shfl_sync(0xffffffffu, r[0], j);
           if (fail < 0 && !(piv > 0.0)) fail = j;
           const double rinv = rsqrt(piv);
-          const double ljj = piv * rinv;
+          const double lcol = (lane == j) ? piv * rinv : (lane > j ? r[0] * rinv : 0.0);
           if (lane == j) {
-            r[j] = ljj;
-            my_l = ljj;
+            my_l = lcol;
             my_rinv = rinv;
-          } else if (lane > j) {
-            r[j] *= rinv;
+          }
+          Ld[lane * SLD + j] = lcol;
+#pragma unroll
+          for (int c = 1; c < NB; ++c) {
+            const double lcj = __shfl_sync(0xffffffffu, lcol, (j + c) & (NB - 1));
+            if (lane >= j + c) r[c] = fma(-lcol, lcj, r[c]);
           }
 #pragma unroll
-          for (int c = 0; c < NB; ++c) {
-            if (c > j) {
-              const double lcj = __shfl_sync(0xffffffffu, r[j], c);
-              if (lane >= c) r[c] = fma(-r[j], lcj, r[c]);
-            }
-          }
+          for (int c = 0; c < NB - 1; ++c) r[c] = r[c + 1];
         }
-        // log-determinant partial: every lane its own pivot, fixed-order butterfly
         const int pos = a.tile_off + c0 + lane;  // padded global position
         const bool real = (pos % a.bp_user < a.b_user) && (fail < 0 || lane < fail);
         const double lsum = warp_sum(real ? log(my_l) : 0.0);
         if (lane == 0) logsum += lsum;
-      } else {
-        my_rinv = 1.0 / r[lane];  // trtri-only: lane's diagonal entry of L
-      }
+      } else {  // trtri-only: the tile already holds L
 #pragma unroll
-      for (int c = 0; c < NB; ++c) Ld[lane * SLD + c] = (c <= lane) ? r[c] : 0.0;
-      Li[lane * SLD + lane] = my_rinv;  // diagonal reciprocals for the inverse
+        for (int c = 0; c < NB; ++c) Ld[lane * SLD + c] = (c <= lane) ? r[c] : 0.0;
+        my_rinv = 1.0 / Ld[lane * SLD + lane];
+      }
+      if (factor) {
+        __syncwarp();
+        for (int c = lane + 1; c < NB; ++c) Ld[lane * SLD + c] = 0.0;  // strictly upper
+      }
+      Li[lane * SLD + lane] = my_rinv;
       __syncwarp();
       if (fail >= 0) {
         if (lane == 0) {
@@ -210,34 +246,25 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
           s_fail = (pos / a.bp_user) * a.b_user + pos % a.bp_user;
         }
       } else {
-        // lane j forms column j of the inverse by forward substitution; the
-        // rows of L are shared-memory broadcasts, the column stays in registers
-        // (four interleaved partial sums keep the dependent FMA chain short)
-        double x[NB], dinv[NB];
-#pragma unroll
-        for (int i = 0; i < NB; ++i) dinv[i] = Li[i * SLD + i];
-        __syncwarp();
-#pragma unroll
+        // lane j forms column j of the inverse by forward substitution (rows
+        // of L broadcast from shared memory, the column in shared memory)
+#pragma unroll 1
         for (int i = 0; i < NB; ++i) {
-          double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-          for (int k = 0; k < NB; ++k) {
-            if (k < i) {
-              const double t_ = -Ld[i * SLD + k] * x[k];
-              if ((k & 3) == 0) s0 += t_;
-              else if ((k & 3) == 1) s1 += t_;
-              else if ((k & 3) == 2) s2 += t_;
-              else s3 += t_;
-            }
+          double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0;
+          int k = 0;
+          for (; k + 1 < i; k += 2) {
+            s0 = fma(-Ld[i * SLD + k], Li[k * SLD + lane], s0);
+            s1 = fma(-Ld[i * SLD + k + 1], Li[(k + 1) * SLD + lane], s1);
           }
-          x[i] = ((s0 + s1) + (s2 + s3)) * dinv[i];
+          if (k < i) s0 = fma(-Ld[i * SLD + k], Li[k * SLD + lane], s0);
+          const double di = Li[i * SLD + i];
+          __syncwarp();
+          if (i != lane) Li[i * SLD + lane] = (i < lane) ? 0.0 : (s0 + s1) * di;
+          __syncwarp();
         }
-#pragma unroll
-        for (int i = 0; i < NB; ++i) Li[i * SLD + lane] = x[i];
-        __syncwarp();
         for (int c = 0; c < NB; ++c) {
           const int64_t o = static_cast<int64_t>(c0 + lane) * bi + c0 + c;
-          if (!a.trtri_only) T[o] = c <= lane ? Ld[lane * SLD + c] : 0.0;
+          if (factor) T[o] = Ld[lane * SLD + c];
           D[o] = Li[lane * SLD + c];
         }
       }
@@ -245,21 +272,14 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
     __syncthreads();
     PROF_MARK(1)
     if (s_fail >= 0) break;
-    // (3) below-diagonal panel: L[r][c0:c0+32] = T[r][c0:c0+32] * Li^T
-    for (int rb = p + 1 + warp; rb < (a.trtri_only ? 0 : P); rb += PT / 32) {
+    // C: below-diagonal panel rows, L[r][c0:c0+32] = T[r][c0:c0+32] * Li^T
+    for (int rb = p + 1 + warp; rb < (factor ? P : 0); rb += NW) {
       double acc[4][4][2];
       zero_acc(acc);
       double* blk = T + static_cast<int64_t>(rb) * NB * bi + c0;
       warp_nt(acc, blk, bi, Li, SLD, NB, g, t);
       __syncwarp();
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          double* c = blk + static_cast<int64_t>(8 * i + g) * bi + 8 * j + 2 * t;
-          c[0] = acc[i][j][0];
-          c[1] = acc[i][j][1];
-        }
+      store_acc(blk, bi, acc, g, t, true, 1.0);
     }
     __syncthreads();
     PROF_MARK(2)
@@ -268,53 +288,27 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
     if (tid == 0) *a.info = s_fail;
     return;
   }
+  // last block row of the inverse (rows 1..P-2 were interleaved above)
+  if (P >= 2)
+    for (int J = warp; J < P - 1; J += NW) trtri_job(T, D, bi, P - 1, J, Sw, g, t);
+  PROF_MARK(3)
   // zero strictly-upper 32-blocks of L and Dinv (lower-triangular results)
-  for (int r = warp; r < bi; r += PT / 32) {
-    const int c_begin = (r / NB + 1) * NB;  // first column of the strictly-upper blocks
+  for (int r = warp; r < bi; r += NW) {
+    const int c_begin = (r / NB + 1) * NB;
     for (int c = c_begin + 2 * lane; c < bi; c += 64) {
       const int64_t idx = static_cast<int64_t>(r) * bi + c;
-      if (!a.trtri_only) *reinterpret_cast<double2*>(T + idx) = make_double2(0.0, 0.0);
+      if (factor) *reinterpret_cast<double2*>(T + idx) = make_double2(0.0, 0.0);
       *reinterpret_cast<double2*>(D + idx) = make_double2(0.0, 0.0);
     }
   }
-  __syncthreads();
-    PROF_MARK(3)
-  // TRTRI: D[I][J] = -D[I][I] * sum_{K=J}^{I-1} L[I][K] D[K][J]
-  double* Sw = S + warp * NB * SLD;
-  for (int I = 1; I < P; ++I) {
-    for (int J = warp; J < I; J += PT / 32) {
-      double acc[4][4][2];
-      zero_acc(acc);
-      warp_nn(acc, T + static_cast<int64_t>(I) * NB * bi + J * NB, bi,
-              D + static_cast<int64_t>(J) * NB * bi + J * NB, bi, (I - J) * NB, g, t);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          Sw[(8 * i + g) * SLD + 8 * j + 2 * t] = acc[i][j][0];
-          Sw[(8 * i + g) * SLD + 8 * j + 2 * t + 1] = acc[i][j][1];
-        }
-      __syncwarp();
-      zero_acc(acc);
-      warp_nn(acc, D + static_cast<int64_t>(I) * NB * bi + I * NB, bi, Sw, SLD, NB, g, t);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          double* c = D + static_cast<int64_t>(I * NB + 8 * i + g) * bi + J * NB + 8 * j + 2 * t;
-          c[0] = -acc[i][j][0];
-          c[1] = -acc[i][j][1];
-        }
-      __syncwarp();
-    }
-    __syncthreads();
-  }
   PROF_MARK(4)
-  if (a.prof && tid == 0) for (int i = 0; i < 5; ++i) a.prof[i] += t_acc[i];
+  if (a.prof && tid == 0)
+    for (int i = 0; i < 5; ++i) a.prof[i] += t_acc[i];
   if (tid == 0 && a.logdiag) a.logdiag[a.tile_index] = logsum;
+#undef PROF_MARK
 }
 
-size_t potrf_smem_bytes() { return sizeof(double) * (2 * NB * SLD + (PT / 32) * NB * SLD); }
+size_t potrf_smem_bytes() { return sizeof(double) * (2 * NB * SLD + NW * NB * SLD); }
 
 cudaError_t launch_potrf(const PotrfArgs& a, cudaStream_t s) {
   potrf_tile_kernel<<<1, PT, potrf_smem_bytes(), s>>>(a);
