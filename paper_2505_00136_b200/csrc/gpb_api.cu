@@ -448,10 +448,6 @@ int ensure_factor(gpb_model* m) {
     ++m->launches;
     GPB_TRY(pt.stop());
   }
-  if (getenv("GPB_DEBUG_ASSEMBLY_ONLY")) {  // debugging aid: leave K in the tiles
-    m->factor_ok = true;
-    return GPB_OK;
-  }
   PhaseTimer pt(m, 1);
   CUDA_TRY(cudaMemsetAsync(m->info.p, 0xff, sizeof(int), m->st));
   const GemmJob* jobs = m->chol_jobs.as<GemmJob>();
