@@ -24,25 +24,35 @@ extern "C" int gpb_plugin_fail(int code, const char* msg);
 namespace {
 
 // Ring of device memory for per-call descriptor tables (copied in stream order).
+// Tables are staged through a pinned host mirror of the ring, so the
+// host-to-device copy is truly asynchronous (a pageable source could make the
+// driver wait for the stream and stall the host-side scheduler).
 struct DescRing {
   std::mutex mu;
-  char* base = nullptr;
+  char* base = nullptr;  // device ring
+  char* host = nullptr;  // pinned mirror
   size_t cap = 0, head = 0;
-  void* stage(const void* host, size_t bytes, cudaStream_t s, cudaError_t* err) {
+  void release() {
+    if (base) cudaFree(base);
+    if (host) cudaFreeHost(host);
+    base = host = nullptr;
+    cap = 0;
+  }
+  void* stage(const void* src, size_t bytes, cudaStream_t s, cudaError_t* err) {
     std::lock_guard<std::mutex> lk(mu);
+    const size_t n = bytes;
     bytes = (bytes + 255) & ~size_t(255);
     if (!base || bytes > cap) {
-      if (base) {
-        cudaDeviceSynchronize();
-        cudaFree(base);
-      }
-      cap = std::max<size_t>(bytes, size_t(64) << 20);
-      *err = cudaMalloc(&base, cap);
+      if (base) cudaDeviceSynchronize();
+      release();
+      const size_t want = std::max<size_t>(bytes, size_t(64) << 20);
+      *err = cudaMalloc(&base, want);
+      if (*err == cudaSuccess) *err = cudaMallocHost(&host, want);
       if (*err != cudaSuccess) {
-        base = nullptr;
-        cap = 0;
+        release();
         return nullptr;
       }
+      cap = want;
       head = 0;
     }
     if (head + bytes > cap) {  // wrap: earlier tables may still be in flight
@@ -50,8 +60,9 @@ struct DescRing {
       head = 0;
     }
     void* dst = base + head;
+    std::memcpy(host + head, src, n);
+    *err = cudaMemcpyAsync(dst, host + head, n, cudaMemcpyHostToDevice, s);
     head += bytes;
-    *err = cudaMemcpyAsync(dst, host, bytes, cudaMemcpyHostToDevice, s);
     return dst;
   }
 };

@@ -33,6 +33,7 @@ used as buffers.  Tests drive the same schedule with a host test double.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import math
 
@@ -302,30 +303,64 @@ class DistributedGP:
         ops.assemble(self.zp, d, lay, self.params, True,
                      [(i, j, self.L[s]) for s, (i, j) in enumerate(self.owned)])
         rows_per = -(-T // self.P)
-        panel = [ops.zeros(max(1, rows_per), b, b) for _ in range(self.P)]
+        # panel buffers per process row, double-buffered across steps
+        panels = [[ops.zeros(max(1, rows_per), b, b) for _ in range(self.P)] for _ in range(2)]
         my_p, my_q = divmod(self.rank, self.Q)
+        by_col = {}
+        for s, (i, j) in enumerate(self.owned):
+            by_col.setdefault(j, []).append((s, i))
+        # Lookahead (as the single-GPU schedule): the critical stream runs
+        # POTRF(k), the L_kk^-1 / panel broadcasts, TRSM(k) and the update of
+        # column k+1 (COL); the main stream applies the rest of step k's
+        # trailing update (UPD), so the next panel's exchange overlaps it.
+        cuda = getattr(ops, "device", None) is not None and ops.device.type == "cuda"
+        main = torch.cuda.current_stream(ops.device) if cuda else None
+        crit = torch.cuda.Stream(device=ops.device, priority=-1) if cuda else None
+        on_crit = (lambda: torch.cuda.stream(crit)) if cuda else contextlib.nullcontext
+        ev_upd = {}
+        if cuda:
+            crit.wait_stream(main)  # assembly
         t0 = self._event()
         for k in range(T):
             own = self.cyc.owner(k, k)
-            if self.rank == own:
-                ops.potrf(self.L[self.slot[k, k]], self.dinv[k], lay, k * b, self.logdiag[k:k + 1], info)
-            self._bcast(self.dinv[k], own)
-            if k + 1 == T:
-                break
-            if my_q == k % self.Q:  # this rank holds panel tiles of column k
-                mine = self.cyc.panel_rows(k, my_p)
-                ops.gemm([(self.L[self.slot[i, k]], self.dinv[k], None, panel[my_p][s], b, False)
-                          for s, i in enumerate(mine)], b, 1.0, 0.0)
-                ops.copy([(panel[my_p][s], self.L[self.slot[i, k]]) for s, i in enumerate(mine)])
-            where = {}
-            for p in range(self.P):
-                rows = self.cyc.panel_rows(k, p)
-                for s, i in enumerate(rows):
-                    where[i] = panel[p][s]
-                if rows:
-                    self._bcast(panel[p][:len(rows)], p * self.Q + k % self.Q)
+            panel = panels[k % 2]
+            with on_crit():
+                if self.rank == own:
+                    ops.potrf(self.L[self.slot[k, k]], self.dinv[k], lay, k * b,
+                              self.logdiag[k:k + 1], info)
+                self._bcast(self.dinv[k], own)
+                if k + 1 == T:
+                    break
+                if my_q == k % self.Q:  # this rank holds panel tiles of column k
+                    mine = self.cyc.panel_rows(k, my_p)
+                    ops.gemm([(self.L[self.slot[i, k]], self.dinv[k], None, panel[my_p][s], b, False)
+                              for s, i in enumerate(mine)], b, 1.0, 0.0)
+                    ops.copy([(panel[my_p][s], self.L[self.slot[i, k]]) for s, i in enumerate(mine)])
+                where = {}
+                for p in range(self.P):
+                    rows = self.cyc.panel_rows(k, p)
+                    for s, i in enumerate(rows):
+                        where[i] = panel[p][s]
+                    if rows:
+                        self._bcast(panel[p][:len(rows)], p * self.Q + k % self.Q)
+                # COL(k): column k+1 also needs UPD(k-1), which covered it
+                if cuda and k >= 1:
+                    crit.wait_event(ev_upd[k - 1])
+                ops.gemm([(where[i], where[k + 1], self.L[s], self.L[s], b, i == k + 1)
+                          for s, i in by_col.get(k + 1, [])], b, -1.0, 1.0)
+                if cuda:
+                    ev_panel = torch.cuda.Event()
+                    ev_panel.record(crit)
+            # UPD(k) on the main stream: owned tiles (i, j), j >= k+2
+            if cuda:
+                main.wait_event(ev_panel)
             ops.gemm([(where[i], where[j], self.L[s], self.L[s], b, i == j)
-                      for s, (i, j) in enumerate(self.owned) if j > k], b, -1.0, 1.0)
+                      for j in range(k + 2, T) for s, i in by_col.get(j, [])], b, -1.0, 1.0)
+            if cuda:
+                ev_upd[k] = torch.cuda.Event()
+                ev_upd[k].record(main)
+        if cuda:
+            main.wait_stream(crit)
         t1 = self._event()
         infos = self._allgather(info).view(-1).cpu().numpy()
         bad = [int(v) for v in infos if v >= 0]
