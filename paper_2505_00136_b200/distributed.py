@@ -131,6 +131,22 @@ class DeviceTileOps:
         _lib.check(self.lib.gpb_dev_gemm(self.rt.handle, self._s(), arr, len(jobs), b, b, b, b, 1,
                                          1, alpha, beta))
 
+    _JOB_DTYPE = np.dtype([("a", "<u8"), ("b", "<u8"), ("cin", "<u8"), ("cout", "<u8"),
+                           ("k", "<i4"), ("lower", "<i4")])  # gpb_gemm_job
+
+    def gemm_addr(self, a_addr, b_addr, c_addr, lower, k, b, alpha, beta):
+        """Vectorised job table (device addresses as int64 arrays): the
+        trailing update of one step at large T without per-tile Python work."""
+        n = len(c_addr)
+        if n == 0:
+            return
+        tab = np.empty(n, dtype=self._JOB_DTYPE)
+        tab["a"], tab["b"], tab["cin"], tab["cout"] = a_addr, b_addr, c_addr, c_addr
+        tab["k"], tab["lower"] = k, lower
+        assert tab.dtype.itemsize == ctypes.sizeof(_lib.GemmJob)
+        _lib.check(self.lib.gpb_dev_gemm(self.rt.handle, self._s(), tab.ctypes.data, n, b, b, b, b,
+                                         1, 1, alpha, beta))
+
     def gemv(self, jobs, b, trans, alpha, accumulate):
         if not jobs:
             return
@@ -318,6 +334,14 @@ class DistributedGP:
         crit = torch.cuda.Stream(device=ops.device, priority=-1) if cuda else None
         on_crit = (lambda: torch.cuda.stream(crit)) if cuda else contextlib.nullcontext
         ev_upd = {}
+        vector_upd = hasattr(ops, "gemm_addr")
+        if vector_upd:
+            own_i = np.array([i for i, _ in self.owned], dtype=np.int64)
+            own_j = np.array([j for _, j in self.owned], dtype=np.int64)
+            tile_bytes = b * b * 8
+            c_addr = self.L.data_ptr() + np.arange(len(self.owned), dtype=np.int64) * tile_bytes
+            pbase = [np.array([panels[h][p].data_ptr() for p in range(self.P)], dtype=np.int64)
+                     for h in range(2)]
         if cuda:
             crit.wait_stream(main)  # assembly
         t0 = self._event()
@@ -354,8 +378,21 @@ class DistributedGP:
             # UPD(k) on the main stream: owned tiles (i, j), j >= k+2
             if cuda:
                 main.wait_event(ev_panel)
-            ops.gemm([(where[i], where[j], self.L[s], self.L[s], b, i == j)
-                      for j in range(k + 2, T) for s, i in by_col.get(j, [])], b, -1.0, 1.0)
+            if vector_upd:  # job table built with numpy (large T)
+                sel = own_j >= k + 2
+                ii, jj = own_i[sel], own_j[sel]
+                base = pbase[k % 2]
+
+                def addr(x):
+                    p = x % self.P
+                    first = k + 1 + (p - (k + 1)) % self.P
+                    return base[p] + ((x - first) // self.P) * tile_bytes
+
+                ops.gemm_addr(addr(ii), addr(jj), c_addr[sel], (ii == jj).astype(np.int32), b, b,
+                              -1.0, 1.0)
+            else:
+                ops.gemm([(where[i], where[j], self.L[s], self.L[s], b, i == j)
+                          for j in range(k + 2, T) for s, i in by_col.get(j, [])], b, -1.0, 1.0)
             if cuda:
                 ev_upd[k] = torch.cuda.Event()
                 ev_upd[k].record(main)
