@@ -594,7 +594,7 @@ int build_inv_plan(gpb_model* m) {
   CUDA_TRY(m->X.ensure(sizeof(double) * ntiles * bi2));
   CUDA_TRY(m->Kinv.ensure(sizeof(double) * ntiles * bi2));
   CUDA_TRY(m->Wg.ensure(sizeof(double) * std::max(1, Ti - 1) * bi2));
-  const int64_t nblk = ntiles * (m->bi / 64) * (m->bi / 64);
+  const int64_t nblk = ntiles * (m->bi / kSekBlock) * (m->bi / kSekBlock);
   CUDA_TRY(m->part_l.ensure(sizeof(double) * nblk));
   CUDA_TRY(m->part_v.ensure(sizeof(double) * nblk));
   CUDA_TRY(m->part_x.ensure(sizeof(double) * nblk));
@@ -674,7 +674,7 @@ int loss_gradients(gpb_model* m, double out[3]) {
   }
 
   double* red = m->red.as<double>();
-  const int64_t nblk = ntiles * (bi / 64) * (bi / 64);
+  const int64_t nblk = ntiles * (bi / kSekBlock) * (bi / kSekBlock);
   if (tl || tv) {
     // K^-1 = X^T X, lower tiles (model.py:362-380)
     GemmParams kp = base_params(jobs + m->kinv_off, static_cast<int>(m->kinv_cnt), nb, nb, bi, bi,
@@ -716,7 +716,7 @@ int build_pred_plan(gpb_model* m, int64_t mcp) {
   const int64_t bi2 = int64_t(bi) * bi;
   CUDA_TRY(m->Bv.ensure(sizeof(double) * m->np_ * mcp));
   CUDA_TRY(m->W.ensure(sizeof(double) * int64_t(bi) * mcp));
-  CUDA_TRY(m->mpart.ensure(sizeof(double) * (m->np_ / 64) * mcp));
+  CUDA_TRY(m->mpart.ensure(sizeof(double) * (m->np_ / kSekBlock) * mcp));
   CUDA_TRY(m->sq.ensure(sizeof(double) * (m->np_ / GBM) * mcp));
   double* L = m->L.as<double>();
   double* D = m->Dinv.as<double>();
@@ -760,7 +760,7 @@ int64_t pred_chunk(gpb_model* m, int64_t mt) {
   }
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  const double per_col = 8.0 * double(m->np_ + m->bi + m->np_ / 64 + m->np_ / GBM + 4);
+  const double per_col = 8.0 * double(m->np_ + m->bi + m->np_ / kSekBlock + m->np_ / GBM + 4);
   const double budget = std::min(48e9, 0.6 * (double(free_b) + double(m->Bv.bytes)));
   const int64_t c = std::max<int64_t>(GBM, int64_t(budget / per_col) / GBM * GBM);
   return std::min(c, all);
@@ -805,7 +805,7 @@ int predict_chunk(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var,
     GPB_TRY(pt.stop());
     *t_trsm += m->timing[4];
   }
-  CUDA_TRY(launch_pred_finalize(m->mpart.as<double>(), m->np_ / 64, m->sq.as<double>(),
+  CUDA_TRY(launch_pred_finalize(m->mpart.as<double>(), m->np_ / kSekBlock, m->sq.as<double>(),
                                 m->np_ / GBM, mcp, mt, m->nu, mean_out,
                                 want_var ? var_out : nullptr, m->st));
   ++m->launches;

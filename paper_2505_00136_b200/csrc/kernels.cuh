@@ -28,6 +28,10 @@ cudaError_t launch_potrf(const PotrfArgs& a, cudaStream_t s);
 cudaError_t potrf_init_attributes();
 
 // ---- squared-exponential tiles (sek.cu) -----------------------------------
+// Entries per CTA side of the SEK kernels (tile sizes are multiples of it);
+// the gradient trace pass writes one partial per kSekBlock^2 block and the
+// cross kernel one mean partial per kSekBlock training rows.
+constexpr int kSekBlock = 64;
 struct SekParams {
   double lengthscale, vertical, noise;
   double neg_half_inv_l2;  // -1 / (2 l^2)   (covariance.py:79)

@@ -19,21 +19,22 @@ namespace gpb {
 
 namespace {
 
-constexpr int SB = 64;   // entries per CTA side
-constexpr int DC = 32;   // feature chunk
+constexpr int SB = kSekBlock;  // entries per CTA side
+constexpr int DC = 32;  // feature chunk
+constexpr int R = SB / 16;  // entries per thread per dimension
 constexpr int ST = 256;  // threads
 
 struct Frag {
-  double v[4][4];
+  double v[R][R];
 };
 
 // d2[ii][jj] for rows ra0 + ty + 16 ii of za (ld d) and rows rb0 + tx + 16 jj of zb.
-GPB_DEVINL void sq_dists_64(Frag& d2, const double* za, int64_t ra0, const double* zb, int64_t rb0,
+GPB_DEVINL void sq_dists_blk(Frag& d2, const double* za, int64_t ra0, const double* zb, int64_t rb0,
                             int d, double (*sa)[SB], double (*sb)[SB], int tx, int ty, int tid) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < R; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) d2.v[i][j] = 0.0;
+    for (int j = 0; j < R; ++j) d2.v[i][j] = 0.0;
   for (int d0 = 0; d0 < d; d0 += DC) {
     const int dn = min(DC, d - d0);
     __syncthreads();
@@ -46,15 +47,15 @@ GPB_DEVINL void sq_dists_64(Frag& d2, const double* za, int64_t ra0, const doubl
     }
     __syncthreads();
     for (int dd = 0; dd < dn; ++dd) {
-      double a[4], b[4];
+      double a[R], b[R];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = sa[dd][ty + 16 * i];
+      for (int i = 0; i < R; ++i) a[i] = sa[dd][ty + 16 * i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = sb[dd][tx + 16 * j];
+      for (int j = 0; j < R; ++j) b[j] = sb[dd][tx + 16 * j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < R; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < R; ++j) {
           const double df = a[i] - b[j];
           d2.v[i][j] = fma(df, df, d2.v[i][j]);
         }
@@ -88,13 +89,13 @@ GPB_DEVINL void assemble_block(double* tile, int ti, int tj, int rb, int cb, con
   const int64_t P0 = static_cast<int64_t>(ti) * bi + rb * SB;
   const int64_t Q0 = static_cast<int64_t>(tj) * bi + cb * SB;
   Frag d2;
-  sq_dists_64(d2, zp, P0, zp, Q0, d, sa, sb, tx, ty, tid);
+  sq_dists_blk(d2, zp, P0, zp, Q0, d, sa, sb, tx, ty, tid);
   double* out = tile + static_cast<int64_t>(rb * SB) * bi + cb * SB;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < R; ++i) {
     const int64_t P = P0 + ty + 16 * i;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < R; ++j) {
       const int64_t Q = Q0 + tx + 16 * j;
       double v;
       if (pm.valid(P) && pm.valid(Q)) {
@@ -147,9 +148,9 @@ __global__ void __launch_bounds__(ST) cross_kernel(double* B, int64_t ldb, doubl
   // zt rows beyond mc: read a valid row instead (masked) by using min()
   {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < R; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) d2.v[i][j] = 0.0;
+      for (int j = 0; j < R; ++j) d2.v[i][j] = 0.0;
     for (int d0 = 0; d0 < d; d0 += DC) {
       const int dn = min(DC, d - d0);
       __syncthreads();
@@ -163,29 +164,29 @@ __global__ void __launch_bounds__(ST) cross_kernel(double* B, int64_t ldb, doubl
       }
       __syncthreads();
       for (int dd = 0; dd < dn; ++dd) {
-        double a[4], b[4];
+        double a[R], b[R];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = sa[dd][ty + 16 * i];
+        for (int i = 0; i < R; ++i) a[i] = sa[dd][ty + 16 * i];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = sb[dd][tx + 16 * j];
+        for (int j = 0; j < R; ++j) b[j] = sb[dd][tx + 16 * j];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < R; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < R; ++j) {
             const double df = a[i] - b[j];
             d2.v[i][j] = fma(df, df, d2.v[i][j]);
           }
       }
     }
   }
-  double msum[4] = {0.0, 0.0, 0.0, 0.0};
+  double msum[R] = {};
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < R; ++i) {
     const int64_t P = P0 + ty + 16 * i;
     const bool pv = pm.valid(P);
     const double a = alpha ? alpha[P] : 0.0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < R; ++j) {
       const int64_t c = C0 + tx + 16 * j;
       const double v = (pv && c < mc) ? sek(d2.v[i][j], sp) : 0.0;
       B[P * ldb + c] = v;
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(ST) cross_kernel(double* B, int64_t ldb, doubl
   }
   if (mpart) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) red[ty][tx + 16 * j] = msum[j];
+    for (int j = 0; j < R; ++j) red[ty][tx + 16 * j] = msum[j];
     __syncthreads();
     if (tid < SB) {
       double s = 0.0;
@@ -213,9 +214,9 @@ __global__ void __launch_bounds__(ST) prior_kernel(double* S, int64_t mp, const 
   const int64_t C0 = static_cast<int64_t>(blockIdx.y) * SB;
   Frag d2;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < R; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) d2.v[i][j] = 0.0;
+    for (int j = 0; j < R; ++j) d2.v[i][j] = 0.0;
   for (int d0 = 0; d0 < d; d0 += DC) {
     const int dn = min(DC, d - d0);
     __syncthreads();
@@ -228,25 +229,25 @@ __global__ void __launch_bounds__(ST) prior_kernel(double* S, int64_t mp, const 
     }
     __syncthreads();
     for (int dd = 0; dd < dn; ++dd) {
-      double a[4], b[4];
+      double a[R], b[R];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = sa[dd][ty + 16 * i];
+      for (int i = 0; i < R; ++i) a[i] = sa[dd][ty + 16 * i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = sb[dd][tx + 16 * j];
+      for (int j = 0; j < R; ++j) b[j] = sb[dd][tx + 16 * j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < R; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < R; ++j) {
           const double df = a[i] - b[j];
           d2.v[i][j] = fma(df, df, d2.v[i][j]);
         }
     }
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < R; ++i) {
     const int64_t r = R0 + ty + 16 * i;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < R; ++j) {
       const int64_t c = C0 + tx + 16 * j;
       S[r * mp + c] = (r < m && c < m) ? sek(d2.v[i][j], sp) : 0.0;
     }
@@ -268,14 +269,14 @@ __global__ void __launch_bounds__(ST) trace_kernel(const double* kinv, const int
   const int64_t P0 = static_cast<int64_t>(ij.x) * bi + rb * SB;
   const int64_t Q0 = static_cast<int64_t>(ij.y) * bi + cb * SB;
   Frag d2;
-  sq_dists_64(d2, zp, P0, zp, Q0, d, sa, sb, tx, ty, tid);
+  sq_dists_blk(d2, zp, P0, zp, Q0, d, sa, sb, tx, ty, tid);
   const double* kt = kinv + t * bi * bi + static_cast<int64_t>(rb * SB) * bi + cb * SB;
   double sl = 0.0, sv = 0.0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < R; ++i) {
     const int64_t P = P0 + ty + 16 * i;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < R; ++j) {
       const int64_t Q = Q0 + tx + 16 * j;
       if (pm.valid(P) && pm.valid(Q)) {
         const double e = exp(d2.v[i][j] * sp.neg_half_inv_l2);
@@ -308,9 +309,9 @@ __global__ void __launch_bounds__(ST) tiles_sumsq_kernel(const double* x, const 
   const double* xt = x + t * bi * bi + static_cast<int64_t>(rb * SB) * bi + cb * SB;
   double s = 0.0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < R; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < R; ++j) {
       if (pm.valid(P0 + ty + 16 * i) && pm.valid(Q0 + tx + 16 * j)) {
         const double v = xt[static_cast<int64_t>(ty + 16 * i) * bi + tx + 16 * j];
         s += v * v;
