@@ -204,6 +204,11 @@ class _DeviceReplica:
     def export_lower(self, n: int) -> np.ndarray:
         return _export(self, n)
 
+    def loss_gradients(self):
+        out = (ctypes.c_double * 3)()
+        _lib.check(self.ops.lib.gpb_loss_gradients(self.h, out))
+        return (float(out[0]), float(out[1]), float(out[2]))
+
     def publish(self):
         torch.cuda.current_stream(self.ops.device).synchronize()
         _lib.check(self.ops.lib.gpb_model_mark_factored(self.h))
@@ -533,6 +538,58 @@ class DistributedGP:
             raise DimensionMismatch(f"test has {test.d} features, model was trained with {self.train.d}")
         mean, cov = self._ensure_replica().full_cov(test.z)
         return PredictionResult(mean=mean, full_covariance=cov)
+
+    # -- training (model.py:341-485) ----------------------------------------------
+    def loss_gradients(self) -> tuple[float, float, float]:
+        """dNLL/d(l, nu, sigma^2) from the gathered factor (every rank computes
+        the same values on its replica; the K^-1 formation is not yet sharded)."""
+        tr = self.params.trainable
+        if not (tr[0] or tr[1] or tr[2]):
+            return (0.0, 0.0, 0.0)
+        return self._ensure_replica().loss_gradients()
+
+    def _set_params(self, params: KernelParams) -> None:
+        self.params = params
+        self.close()
+        self._factored = False
+
+    def optimize(self, opt=None) -> list[float]:
+        """Adam on the log-parameters (model.py:437-485); every iteration
+        re-factors K distributed.  Moments persist across calls."""
+        from dataclasses import replace
+
+        from .model import AdamConfig
+
+        opt = opt if opt is not None else AdamConfig()
+        if not hasattr(self, "_adam"):
+            self._adam = [np.zeros(3), np.zeros(3), 0]
+        m_, v_, _ = self._adam
+        history = []
+        for _ in range(opt.iterations):
+            self._adam[2] += 1
+            step_no = self._adam[2]
+            try:
+                grads = np.array(self.loss_gradients())
+                p = self.params
+                theta = np.array([p.lengthscale, p.vertical_scale, p.noise_variance])
+                g = grads * theta
+                m_[:] = opt.beta1 * m_ + (1 - opt.beta1) * g
+                v_[:] = opt.beta2 * v_ + (1 - opt.beta2) * g * g
+                m_hat = m_ / (1 - opt.beta1 ** step_no)
+                v_hat = v_ / (1 - opt.beta2 ** step_no)
+                step = opt.learning_rate * m_hat / (np.sqrt(v_hat) + opt.epsilon)
+                mask = np.array(p.trainable, dtype=bool)
+                u = np.where(mask, np.log(np.maximum(theta, 1e-300)) - step, 0.0)
+                theta = np.where(mask, np.exp(u), theta)
+                if mask[2]:
+                    theta[2] = max(theta[2], 1e-12)
+                self._set_params(replace(p, lengthscale=float(theta[0]),
+                                         vertical_scale=float(theta[1]),
+                                         noise_variance=float(theta[2])))
+                history.append(-self.log_likelihood())
+            except NotPositiveDefinite as exc:
+                raise NotPositiveDefinite(f"iteration {step_no}: {exc}") from exc
+        return history
 
     def close(self):
         if self._replica is not None:

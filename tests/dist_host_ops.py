@@ -46,13 +46,11 @@ class HostTileOps:
             a, c = z[i * b:(i + 1) * b], z[j * b:(j + 1) * b]
             d2 = ((a[:, None, :] - c[None, :, :]) ** 2).sum(-1)
             k = params.vertical_scale * np.exp(d2 * (-1.0 / (2.0 * params.lengthscale ** 2)))
-            for r in range(b):
-                for q in range(b):
-                    P, Q = i * b + r, j * b + q
-                    if not (self._valid(P, lay) and self._valid(Q, lay)):
-                        k[r, q] = 1.0 if P == Q else 0.0
-                    elif add_noise and P == Q:
-                        k[r, q] += params.noise_variance
+            P = i * b + np.arange(b)[:, None]
+            Q = j * b + np.arange(b)[None, :]
+            valid = self._valid(P, lay) & self._valid(Q, lay)
+            k = np.where(valid, k + (add_noise and params.noise_variance) * (P == Q),
+                         (P == Q).astype(np.float64))
             t.copy_(torch.from_numpy(k))
 
     def potrf(self, tile, dinv, lay, tile_off, logdiag_slot, info):
@@ -151,6 +149,21 @@ class HostReplica:
             v = np.linalg.solve(lo, ks.T)
             var = p.vertical_scale - (v * v).sum(0)
         return mean, var
+
+    def loss_gradients(self):
+        lo, real = self._dense()
+        z, p = self.train.z, self.params
+        d2 = ((z[:, None, :] - z[None, :, :]) ** 2).sum(-1)
+        e = np.exp(d2 * (-1.0 / (2.0 * p.lengthscale ** 2)))
+        linv = np.linalg.inv(lo)
+        kinv = linv.T @ linv
+        alpha = self.vecs["alpha"].numpy()[real]
+        w = kinv - np.outer(alpha, alpha)
+        tl, tv, tn = p.trainable
+        gl = 0.5 * float(np.sum(w * (p.vertical_scale / p.lengthscale ** 3) * e * d2)) if tl else 0.0
+        gv = 0.5 * float(np.sum(w * e)) if tv else 0.0
+        gn = 0.5 * (float(np.trace(kinv)) - float(alpha @ alpha)) if tn else 0.0
+        return (gl, gv, gn)
 
     def close(self):
         pass
