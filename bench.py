@@ -102,6 +102,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def _ncu_traffic():
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/r01_gemm_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)["traffic_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 # ---------------------------------------------------------------- CPU side
 def cpu_cholesky_sample(n: int, d: int, tiles: int, seed: int = 0):
     """Time the reference algorithm (oracle restatement of taskgp's tiled
@@ -283,7 +294,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "api": "GPModel(train).compute_loss() then predict_with_uncertainty(test), host numpy"},
         "roofline": {"bound": "tensor", "kernel": "dgemm_grouped_kernel (DMMA.8x8x4)",
                      "achieved": gemm_tf, "peak": peak.value, "unit": "TFLOP/s",
-                     "frac": gemm_tf / peak.value if peak.value else None, "traffic": None,
+                     "frac": gemm_tf / peak.value if peak.value else None,
+                     "traffic": _ncu_traffic(),
                      "peak_source": "in-run FP64 DMMA probe (MEASURED_PEAKS.json has no FP64 entry)",
                      "launches": int(kcnt[0]), "share_of_step": kms[0] / total_ms if total_ms else None,
                      "cholesky_frac_of_peak": value / world / peak.value if peak.value else None},
