@@ -17,8 +17,11 @@ inside the timed region).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): every rank runs its own replica (the multi-GPU factorisation
-is not built yet); value = total flops / max time.
+N > 1 (torchrun): the same config-2 problem factored 2D block-cyclic over all
+ranks with NCCL panel broadcasts and predicted sharded over test points
+(paper_2505_00136_b200/distributed.py, strong scaling); value = n^3/3 flops
+over the slowest rank's factorisation time.  GPB_REPLICAS=1 instead runs N
+independent single-GPU replicas.
 """
 
 from __future__ import annotations
