@@ -84,8 +84,15 @@ int main(int argc, char** argv) {
       best = std::min(best, ms);
     }
     const double flops = 2.0 * bi * bi * double(c.K) * c.ntiles;
-    printf("%-42s %8.3f ms  %6.2f TF/s  %s\n", c.name, best, flops / (best * 1e-3) / 1e12,
-           cudaGetErrorString(cudaGetLastError()));
+    // bitwise fingerprint of one launch from a fixed C (configs must agree)
+    fill(C, size_t(c.ntiles) * bi2);
+    launch_gemm(p, c.ak, c.bk, EPI_AXPBY, 0);
+    std::vector<unsigned long long> h(size_t(c.ntiles) * bi2);
+    cudaMemcpy(h.data(), C, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long fp = 1469598103934665603ull;
+    for (auto v : h) fp = (fp ^ v) * 1099511628211ull;
+    printf("%-42s %8.3f ms  %6.2f TF/s  %s  fp=%016llx\n", c.name, best,
+           flops / (best * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()), fp);
   }
   return 0;
 }
