@@ -77,6 +77,15 @@ int gpb_last_pivot(gpb_model* m, int64_t* pivot);
 int gpb_log_likelihood(gpb_model* m, double* out);
 /* dNLL/d(l, nu, s2) (model.py:341-435); zeros for non-trainable */
 int gpb_loss_gradients(gpb_model* m, double out[3]);
+/* Gradient terms of the internal K^-1 tile columns [col0, col1) (tiles of
+ * gpb_layout's out[0] size), for splitting loss_gradients across ranks that
+ * each hold the factor (model.py:362-432 restated per column panel):
+ *   out[0] = sum w (K^-1 - a a^T) o E o D2,  out[1] = sum w (K^-1 - a a^T) o E,
+ *   out[2] = sum of the real diagonal entries of K^-1   (w = 2 off the diagonal).
+ * Summed over a partition of [0, T): dNLL/dl = nu / (2 l^3) out[0],
+ * dNLL/dnu = out[1] / 2, dNLL/ds2 = (out[2] - |alpha|^2) / 2.
+ * GPB_NO_MEMORY if the (n - col0 b) x (col1 - col0) b panel does not fit. */
+int gpb_loss_gradient_terms(gpb_model* m, int64_t col0, int64_t col1, double out[3]);
 /* Adam on log-parameters (model.py:437-485). history: iterations NLLs.
  * On GPB_NOT_PD the message is prefixed "iteration k: ". */
 int gpb_optimize(gpb_model* m, double learning_rate, double beta1, double beta2,
@@ -90,6 +99,18 @@ int gpb_predict(gpb_model* m, const double* zt, int64_t mt, int64_t d, double* m
 /* same with zt, mean, var in device memory (no clamp check; raw values) */
 int gpb_predict_device(gpb_model* m, const double* zt_dev, int64_t mt, int64_t d,
                        double* mean_dev, double* var_dev);
+/* Building blocks of the test-point-sharded full covariance (multi-GPU):
+ * gpb_predict_solve_device writes V = L^-1 K*^T of mt test points into V_dev
+ * (n_p x ldv row-major, n_p = gpb_layout out[2]; rows at padded positions are
+ * 0) and optionally the mean.  GPB_NO_MEMORY if all mt columns do not fit at once.
+ * gpb_cov_block_device writes out (ma x mb, ld ldo) = K**(za, zb) - Va^T Vb
+ * (model.py:254-269 for one block of Sigma); Va / Vb are n_p x ldv blocks
+ * from gpb_predict_solve_device with ldv >= m rounded up to 128. */
+int gpb_predict_solve_device(gpb_model* m, const double* zt_dev, int64_t mt, int64_t d,
+                             double* mean_dev, double* V_dev, int64_t ldv);
+int gpb_cov_block_device(gpb_model* m, const double* za, int64_t ma, const double* Va, int64_t ldva,
+                         const double* zb, int64_t mb, const double* Vb, int64_t ldvb, double* out,
+                         int64_t ldo);
 
 /* per-phase device times (ms, CUDA events on the model stream) of the last
  * calls: [0] assembly, [1] factorisation, [2] alpha solves, [3] predict

@@ -47,6 +47,11 @@ SIGNATURES = {
     "gpb_last_pivot": (ctypes.c_int, [_vp, _c_i64_p]),
     "gpb_log_likelihood": (ctypes.c_int, [_vp, _c_double_p]),
     "gpb_loss_gradients": (ctypes.c_int, [_vp, _c_double_p]),
+    "gpb_predict_solve_device": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int64, _vp, _vp,
+                                                 ctypes.c_int64]),
+    "gpb_cov_block_device": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp,
+                                             ctypes.c_int64, _vp, ctypes.c_int64, _vp, ctypes.c_int64]),
+    "gpb_loss_gradient_terms": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, _c_double_p]),
     "gpb_optimize": (ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                     ctypes.c_double, ctypes.c_int64, _c_double_p]),
     "gpb_predict": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_int64, ctypes.c_int64,

@@ -115,6 +115,7 @@ struct gpb_model {
 
   // gradient
   DevBuf X, Kinv, Wg, part_l, part_v, part_x, inv_jobs;
+  DevBuf gp_panel, gp_h, gp_jobs, gp_tiles;  // column-panel gradient terms (multi-GPU split)
   std::vector<int64_t> invw_off, invx_off;
   int64_t kinv_off = 0, kinv_cnt = 0;
   bool inv_plan = false;
@@ -683,9 +684,10 @@ int loss_gradients(gpb_model* m, double out[3]) {
     GPB_TRY(gemm(m, kp, false, false, EPI_AXPBY,
                  gemm_flops(int64_t(nb) * nb, int64_t(bi) * Ti * (Ti + 1) * (Ti + 2) / 6)));
     // fused trace pass (model.py:382-414 with covariance.py:196-220 regenerated)
-    CUDA_TRY(launch_trace(m->Kinv.as<double>(), m->tile_cm.as<int2>(), ntiles, Ti, m->zp.as<double>(),
-                          m->alpha.as<double>(), static_cast<int>(m->d), bi, m->pm, sek_params(m),
-                          m->part_l.as<double>(), m->part_v.as<double>(), m->st));
+    CUDA_TRY(launch_trace(m->Kinv.as<double>(), m->tile_cm.as<int2>(), ntiles, TraceTiles{0, 0, 0},
+                          m->zp.as<double>(), m->alpha.as<double>(), static_cast<int>(m->d), bi,
+                          m->pm, sek_params(m), m->part_l.as<double>(), m->part_v.as<double>(),
+                          nullptr, m->st));
     CUDA_TRY(launch_reduce(m->part_l.as<double>(), nblk, red + 0, m->st));
     CUDA_TRY(launch_reduce(m->part_v.as<double>(), nblk, red + 1, m->st));
     m->launches += 3;
@@ -706,6 +708,137 @@ int loss_gradients(gpb_model* m, double out[3]) {
   if (tl) out[0] = 0.5 * (m->nu / (m->l * m->l * m->l)) * hh[0];
   if (tv) out[1] = 0.5 * hh[1];
   if (tn) out[2] = 0.5 * (hh[2] - hh[4]);
+  return GPB_OK;
+}
+
+// ---- gradient terms over a range of K^-1 tile columns (multi-GPU split) ----
+// The single-GPU gradient forms X = L^-1 then K^-1 = X^T X, which needs all of X
+// for every column of K^-1.  Split across ranks, each rank instead forms the
+// panel K^-1[:, J0*bi .. J1*bi) = L^-T (L^-1 E) directly from the (replicated)
+// factor: a forward solve of the identity panel from row block J0 (the
+// prediction sweep's jobs) and a right-looking backward solve with L^T, then
+// the trace pass over the panel's lower tiles.  Column panels are independent,
+// so ranks need no exchange until the three partial sums are combined.
+// out = {sum w (K^-1 - a a^T) e d2, sum w (K^-1 - a a^T) e, sum of real diag K^-1}.
+int grad_partial(gpb_model* m, int J0, int J1, double out[3]) {
+  const int Ti = m->Ti, bi = m->bi, nb = bi / GBM;
+  if (J0 < 0 || J1 > Ti || J0 >= J1)
+    return fail(GPB_INVALID_CONFIG, "tile column range [" + std::to_string(J0) + ", " +
+                                        std::to_string(J1) + ") outside [0, " + std::to_string(Ti) +
+                                        ")");
+  GPB_TRY(ensure_weights(m));
+  const int64_t bi2 = int64_t(bi) * bi;
+  const int64_t w = int64_t(J1 - J0) * bi;           // panel width
+  const int64_t rows = int64_t(Ti - J0) * bi;        // panel rows: global J0*bi ..
+  if (m->gp_panel.ensure(sizeof(double) * rows * w) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(GPB_NO_MEMORY, "gradient panel of " + std::to_string(rows) + " x " +
+                                   std::to_string(w) + " does not fit; use narrower column ranges");
+  }
+  CUDA_TRY(m->gp_h.ensure(sizeof(double) * bi * w));
+  double* G = m->gp_panel.as<double>();
+  double* H = m->gp_h.as<double>();
+  double* L = m->L.as<double>();
+  double* D = m->Dinv.as<double>();
+  // job table: forward (W, V per row block), backward (H, updates) per step
+  std::vector<GemmJob> jobs;
+  std::vector<int64_t> fw_off, bw_h_off, bw_u_off;
+  for (int i = J0; i < Ti; ++i) {
+    fw_off.push_back(jobs.size());
+    GemmJob g{};  // H = E_i - L[i, J0..i) V[J0..i)
+    g.A = L + h_tri_rm(i, J0) * bi2;
+    g.B = G;
+    g.Cin = G + int64_t(i - J0) * bi * w;
+    g.Cout = H;
+    g.K = (i - J0) * bi;
+    jobs.push_back(g);
+    for (int r = 0; r < nb; ++r) {  // V_i = Dinv_i H (lower: k < (r+1)*128)
+      GemmJob v{};
+      v.A = D + int64_t(i) * bi2 + int64_t(r) * GBM * bi;
+      v.B = H;
+      v.Cout = G + (int64_t(i - J0) * bi + r * GBM) * w;
+      v.K = (r + 1) * GBM;
+      jobs.push_back(v);
+    }
+  }
+  for (int i = Ti - 1; i >= J0; --i) {
+    bw_h_off.push_back(jobs.size());
+    for (int r = 0; r < nb; ++r) {  // H = Dinv_i^T G_i (upper: k >= r*128)
+      GemmJob h{};
+      h.A = D + int64_t(i) * bi2 + int64_t(r) * GBM * bi + r * GBM;
+      h.B = G + (int64_t(i - J0) * bi + r * GBM) * w;
+      h.Cout = H + int64_t(r) * GBM * w;
+      h.K = bi - r * GBM;
+      jobs.push_back(h);
+    }
+    bw_u_off.push_back(jobs.size());
+    for (int r = J0; r < i; ++r) {  // G_r -= L[i, r]^T H
+      GemmJob u{};
+      u.A = L + h_tri_rm(i, r) * bi2;
+      u.B = H;
+      u.Cin = u.Cout = G + int64_t(r - J0) * bi * w;
+      u.K = bi;
+      jobs.push_back(u);
+    }
+  }
+  std::vector<int2> tl;
+  for (int j = J0; j < J1; ++j)
+    for (int i = j; i < Ti; ++i) tl.push_back(make_int2(i, j));
+  const int64_t ntl = static_cast<int64_t>(tl.size());
+  const int64_t nblk = ntl * (bi / kSekBlock) * (bi / kSekBlock);
+  CUDA_TRY(m->gp_jobs.ensure(sizeof(GemmJob) * jobs.size()));
+  CUDA_TRY(m->gp_tiles.ensure(sizeof(int2) * tl.size()));
+  CUDA_TRY(m->part_l.ensure(sizeof(double) * nblk));
+  CUDA_TRY(m->part_v.ensure(sizeof(double) * nblk));
+  CUDA_TRY(m->part_x.ensure(sizeof(double) * nblk));
+  CUDA_TRY(cudaMemcpyAsync(m->gp_jobs.p, jobs.data(), sizeof(GemmJob) * jobs.size(),
+                           cudaMemcpyHostToDevice, m->st));
+  CUDA_TRY(cudaMemcpyAsync(m->gp_tiles.p, tl.data(), sizeof(int2) * tl.size(),
+                           cudaMemcpyHostToDevice, m->st));
+  const GemmJob* dj = m->gp_jobs.as<GemmJob>();
+  const int nbn = static_cast<int>(w / GBN);
+  PhaseTimer pt(m, 5);
+  CUDA_TRY(cudaMemsetAsync(G, 0, sizeof(double) * rows * w, m->st));
+  CUDA_TRY(launch_set_diag(G, w, w, m->st));
+  ++m->launches;
+  for (int i = J0; i < Ti; ++i) {
+    const int64_t o = fw_off[i - J0];
+    GemmParams f = base_params(dj + o, 1, nb, nbn, bi, w, w, -1.0, 1.0);
+    f.a_ktile = bi;
+    f.a_kstride = bi2;
+    f.max_k = int64_t(i - J0) * bi;
+    GPB_TRY(gemm(m, f, true, false, EPI_AXPBY, gemm_flops(int64_t(nb) * nbn, int64_t(i - J0) * bi)));
+    GemmParams v = base_params(dj + o + 1, nb, 1, nbn, bi, w, w, 1.0, 0.0);
+    GPB_TRY(gemm(m, v, true, false, EPI_AXPBY, gemm_flops(nbn, int64_t(GBM) * nb * (nb + 1) / 2)));
+  }
+  for (int i = Ti - 1; i >= J0; --i) {
+    const int s = Ti - 1 - i;
+    GemmParams h = base_params(dj + bw_h_off[s], nb, 1, nbn, bi, w, w, 1.0, 0.0);
+    GPB_TRY(gemm(m, h, false, false, EPI_AXPBY, gemm_flops(nbn, int64_t(GBM) * nb * (nb + 1) / 2)));
+    CUDA_TRY(cudaMemcpyAsync(G + int64_t(i - J0) * bi * w, H, sizeof(double) * bi * w,
+                             cudaMemcpyDeviceToDevice, m->st));
+    if (i > J0) {
+      GemmParams u = base_params(dj + bw_u_off[s], i - J0, nb, nbn, bi, w, w, -1.0, 1.0);
+      u.max_k = bi;
+      GPB_TRY(gemm(m, u, false, false, EPI_AXPBY, gemm_flops(int64_t(i - J0) * nb * nbn, bi)));
+    }
+  }
+  double* red = m->red.as<double>();
+  CUDA_TRY(launch_trace(G, m->gp_tiles.as<int2>(), ntl, TraceTiles{w, J0, J0}, m->zp.as<double>(),
+                        m->alpha.as<double>(), static_cast<int>(m->d), bi, m->pm, sek_params(m),
+                        m->part_l.as<double>(), m->part_v.as<double>(), m->part_x.as<double>(),
+                        m->st));
+  CUDA_TRY(launch_reduce(m->part_l.as<double>(), nblk, red + 0, m->st));
+  CUDA_TRY(launch_reduce(m->part_v.as<double>(), nblk, red + 1, m->st));
+  CUDA_TRY(launch_reduce(m->part_x.as<double>(), nblk, red + 2, m->st));
+  m->launches += 4;
+  double hh[3];
+  CUDA_TRY(cudaMemcpyAsync(hh, red, sizeof(hh), cudaMemcpyDeviceToHost, m->st));
+  CUDA_TRY(cudaStreamSynchronize(m->st));
+  GPB_TRY(pt.stop());
+  out[0] = hh[0];
+  out[1] = hh[1];
+  out[2] = hh[2];
   return GPB_OK;
 }
 
@@ -951,7 +1084,7 @@ void free_model(gpb_model* m) {
                     &m->beta, &m->alpha, &m->bhat, &m->red, &m->tile_rm, &m->tile_cm, &m->chol_jobs,
                     &m->X, &m->Kinv, &m->Wg, &m->part_l, &m->part_v, &m->part_x, &m->inv_jobs,
                     &m->Bv, &m->W, &m->mpart, &m->sq, &m->pred_jobs, &m->zt, &m->mean, &m->var,
-                    &m->S, &m->fc_jobs})
+                    &m->S, &m->fc_jobs, &m->gp_panel, &m->gp_h, &m->gp_jobs, &m->gp_tiles})
     b->release();
 }
 
@@ -1099,6 +1232,12 @@ int gpb_loss_gradients(gpb_model* m, double out[3]) {
   return loss_gradients(m, out);
 }
 
+int gpb_loss_gradient_terms(gpb_model* m, int64_t col0, int64_t col1, double out[3]) {
+  GPB_TRY(check_live(m));
+  if (!out) return fail(GPB_INVALID_CONFIG, "null output");
+  return grad_partial(m, static_cast<int>(col0), static_cast<int>(col1), out);
+}
+
 int gpb_optimize(gpb_model* m, double lr, double b1, double b2, double eps, int64_t iters,
                  double* history) {
   GPB_TRY(check_live(m));
@@ -1186,6 +1325,55 @@ int gpb_predict_device(gpb_model* m, const double* zt_dev, int64_t mt, int64_t d
     CUDA_TRY(cudaMemcpyAsync(var_dev, m->var.p, sizeof(double) * mt, cudaMemcpyDeviceToDevice, m->st));
   CUDA_TRY(cudaStreamSynchronize(m->st));
   return GPB_OK;
+}
+
+int gpb_predict_solve_device(gpb_model* m, const double* zt_dev, int64_t mt, int64_t d,
+                             double* mean_dev, double* V_dev, int64_t ldv) {
+  GPB_TRY(check_live(m));
+  if (d != m->d) return fail(GPB_DIM, "feature count mismatch");
+  if (mt < 0 || ldv < mt || !V_dev) return fail(GPB_INVALID_CONFIG, "V buffer must be n_p x ldv, ldv >= m");
+  if (mt == 0) return GPB_OK;
+  GPB_TRY(predict_core(m, zt_dev, mt, true, /*single_chunk=*/true));
+  if (mean_dev)
+    CUDA_TRY(cudaMemcpyAsync(mean_dev, m->mean.p, sizeof(double) * mt, cudaMemcpyDeviceToDevice, m->st));
+  CUDA_TRY(cudaMemcpy2DAsync(V_dev, sizeof(double) * ldv, m->Bv.p, sizeof(double) * m->pred_mcp,
+                             sizeof(double) * mt, m->np_, cudaMemcpyDeviceToDevice, m->st));
+  CUDA_TRY(cudaStreamSynchronize(m->st));
+  return GPB_OK;
+}
+
+int gpb_cov_block_device(gpb_model* m, const double* za, int64_t ma, const double* Va, int64_t ldva,
+                         const double* zb, int64_t mb, const double* Vb, int64_t ldvb, double* out,
+                         int64_t ldo) {
+  GPB_TRY(check_live(m));
+  const int64_t mpa = round_up(std::max<int64_t>(ma, 1), GBM);
+  const int64_t mpb = round_up(std::max<int64_t>(mb, 1), GBM);
+  if (ma < 0 || mb < 0 || ldva < mpa || ldvb < mpb || ldo < mb)
+    return fail(GPB_INVALID_CONFIG, "V blocks need ld >= m rounded up to 128, out ld >= mb");
+  if (ma == 0 || mb == 0) return GPB_OK;
+  GPB_TRY(ensure_weights(m));
+  CUDA_TRY(m->S.ensure(sizeof(double) * mpa * mpb));
+  double* S = m->S.as<double>();
+  PhaseTimer pt(m, 6);
+  CUDA_TRY(launch_prior2(S, mpb, mpa, mpb, za, ma, zb, mb, static_cast<int>(m->d), sek_params(m),
+                         m->st));
+  ++m->launches;
+  // Sigma_ab = K**(a, b) - Va^T Vb  (model.py:254-269 for one block)
+  GemmJob g{};
+  g.A = Va;
+  g.B = Vb;
+  g.Cin = g.Cout = S;
+  g.K = static_cast<int>(m->np_);
+  CUDA_TRY(m->gp_jobs.ensure(sizeof(GemmJob)));
+  CUDA_TRY(cudaMemcpyAsync(m->gp_jobs.p, &g, sizeof(g), cudaMemcpyHostToDevice, m->st));
+  GemmParams p = base_params(m->gp_jobs.as<GemmJob>(), 1, static_cast<int>(mpa / GBM),
+                             static_cast<int>(mpb / GBN), ldva, ldvb, mpb, -1.0, 1.0);
+  p.max_k = m->np_;
+  GPB_TRY(gemm(m, p, false, false, EPI_AXPBY, gemm_flops((mpa / GBM) * (mpb / GBN), m->np_)));
+  CUDA_TRY(cudaMemcpy2DAsync(out, sizeof(double) * ldo, S, sizeof(double) * mpb, sizeof(double) * mb,
+                             ma, cudaMemcpyDeviceToDevice, m->st));
+  CUDA_TRY(cudaStreamSynchronize(m->st));
+  return pt.stop();
 }
 
 int gpb_model_adopt_factor(gpb_model* m, const double* tiles, const double* dinv,

@@ -75,12 +75,26 @@ cudaError_t launch_cross(double* B, int64_t ldb, double* mpart, const double* al
 // Dense prior K** (mp x mp, row-major) of the test chunk, noise-free.
 cudaError_t launch_prior(double* S, int64_t mp, const double* zt, int64_t m, int d, SekParams sp,
                          cudaStream_t s);
+// Cross prior K**(za, zb): S (mpa x mpb, ld lds; multiples of kSekBlock), zero
+// outside the ma x mb real block.
+cudaError_t launch_prior2(double* S, int64_t lds, int64_t mpa, int64_t mpb, const double* za,
+                          int64_t ma, const double* zb, int64_t mb, int d, SekParams sp,
+                          cudaStream_t s);
 
-// Gradient trace pass over the lower tiles of K^-1 (column-major tile order):
-// part[blk] = w * sum (Kinv - alpha alpha^T) e d2  and  w * sum (Kinv - ..) e.
-cudaError_t launch_trace(const double* kinv, const int2* tile_ij_cm, int64_t ntiles, int T,
+// Gradient trace pass over lower tiles of K^-1, one partial per kSekBlock^2 block:
+// part_l = w * sum (Kinv - alpha alpha^T) e d2,  part_v = w * sum (Kinv - ..) e,
+// part_t (optional) = sum of the real diagonal entries of Kinv (w = 2 off the diagonal).
+// Tile t = tile_ij[t] is read from packed tiles (ld == 0: kinv + t * bi^2, column-major
+// tile order) or from a dense row-major panel whose entry (0, 0) is global
+// position (row0 * bi, col0 * bi) (ld > 0).
+struct TraceTiles {
+  int64_t ld;
+  int row0, col0;
+};
+cudaError_t launch_trace(const double* kinv, const int2* tile_ij, int64_t ntiles, TraceTiles tt,
                          const double* zp, const double* alpha, int d, int bi, PadMap pm,
-                         SekParams sp, double* part_l, double* part_v, cudaStream_t s);
+                         SekParams sp, double* part_l, double* part_v, double* part_t,
+                         cudaStream_t s);
 // part[blk] = sum of squares of the real entries of lower tiles (column-major order).
 cudaError_t launch_tiles_sumsq(const double* x, const int2* tile_ij_cm, int64_t ntiles, int bi,
                                PadMap pm, double* part, cudaStream_t s);
@@ -112,6 +126,8 @@ cudaError_t launch_pad_rows(const double* src, double* dst, int64_t np_, int d, 
 // dense lower factor export: out[r][c] (n x n) from packed tiles
 cudaError_t launch_export_lower(const double* tiles, int T, int bi, int64_t n, PadMap pm,
                                 double* out, cudaStream_t s);
+// G[c * ld + c] = 1 for c < count (identity right-hand side of a column panel)
+cudaError_t launch_set_diag(double* G, int64_t ld, int64_t count, cudaStream_t s);
 // copy the solved panel (scratch tiles q = 0..T-k-2) back to tiles (k+1+q, k)
 cudaError_t launch_copy_panel(double* ltiles, const double* scratch, int T, int k, int bi,
                               cudaStream_t s);

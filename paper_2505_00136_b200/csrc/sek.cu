@@ -206,8 +206,10 @@ __global__ void __launch_bounds__(ST) cross_kernel(double* B, int64_t ldb, doubl
   }
 }
 
-__global__ void __launch_bounds__(ST) prior_kernel(double* S, int64_t mp, const double* zt,
-                                                   int64_t m, int d, SekParams sp) {
+// S (ld lds) = nu exp(-|za_r - zb_c|^2 / 2l^2) for r < ma, c < mb, else 0
+__global__ void __launch_bounds__(ST) prior_kernel(double* S, int64_t lds, const double* za,
+                                                   int64_t ma, const double* zb, int64_t mb, int d,
+                                                   SekParams sp) {
   __shared__ double sa[DC][SB], sb[DC][SB];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int64_t R0 = static_cast<int64_t>(blockIdx.x) * SB;
@@ -223,8 +225,8 @@ __global__ void __launch_bounds__(ST) prior_kernel(double* S, int64_t mp, const 
     for (int e = tid; e < SB * DC; e += ST) {
       const int r = e / DC, dd = e % DC;
       if (dd < dn) {
-        sa[dd][r] = zt[min(R0 + r, m - 1) * d + d0 + dd];
-        sb[dd][r] = zt[min(C0 + r, m - 1) * d + d0 + dd];
+        sa[dd][r] = za[min(R0 + r, ma - 1) * d + d0 + dd];
+        sb[dd][r] = zb[min(C0 + r, mb - 1) * d + d0 + dd];
       }
     }
     __syncthreads();
@@ -249,15 +251,15 @@ __global__ void __launch_bounds__(ST) prior_kernel(double* S, int64_t mp, const 
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       const int64_t c = C0 + tx + 16 * j;
-      S[r * mp + c] = (r < m && c < m) ? sek(d2.v[i][j], sp) : 0.0;
+      S[r * lds + c] = (r < ma && c < mb) ? sek(d2.v[i][j], sp) : 0.0;
     }
   }
 }
 
 __global__ void __launch_bounds__(ST) trace_kernel(const double* kinv, const int2* tile_ij,
                                                    const double* zp, const double* alpha, int d,
-                                                   int bi, PadMap pm, SekParams sp,
-                                                   double* part_l, double* part_v) {
+                                                   int bi, PadMap pm, SekParams sp, TraceTiles tt,
+                                                   double* part_l, double* part_v, double* part_t) {
   __shared__ double sa[DC][SB], sb[DC][SB];
   __shared__ double red[ST];
   const int nbs = bi / SB;
@@ -270,8 +272,13 @@ __global__ void __launch_bounds__(ST) trace_kernel(const double* kinv, const int
   const int64_t Q0 = static_cast<int64_t>(ij.y) * bi + cb * SB;
   Frag d2;
   sq_dists_blk(d2, zp, P0, zp, Q0, d, sa, sb, tx, ty, tid);
-  const double* kt = kinv + t * bi * bi + static_cast<int64_t>(rb * SB) * bi + cb * SB;
-  double sl = 0.0, sv = 0.0;
+  // packed tiles (ld == 0): tile t at kinv + t * bi^2; dense column panel
+  // (ld > 0): entry (P, Q) at kinv + (P - row0 * bi) * ld + (Q - col0 * bi)
+  const int64_t ldk = tt.ld > 0 ? tt.ld : bi;
+  const double* kt = tt.ld > 0 ? kinv + (P0 - static_cast<int64_t>(tt.row0) * bi) * tt.ld +
+                                     (Q0 - static_cast<int64_t>(tt.col0) * bi)
+                               : kinv + t * bi * bi + static_cast<int64_t>(rb * SB) * bi + cb * SB;
+  double sl = 0.0, sv = 0.0, st = 0.0;
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const int64_t P = P0 + ty + 16 * i;
@@ -280,18 +287,22 @@ __global__ void __launch_bounds__(ST) trace_kernel(const double* kinv, const int
       const int64_t Q = Q0 + tx + 16 * j;
       if (pm.valid(P) && pm.valid(Q)) {
         const double e = exp(d2.v[i][j] * sp.neg_half_inv_l2);
-        const double coef = kt[static_cast<int64_t>(ty + 16 * i) * bi + tx + 16 * j] - alpha[P] * alpha[Q];
+        const double kv = kt[static_cast<int64_t>(ty + 16 * i) * ldk + tx + 16 * j];
+        const double coef = kv - alpha[P] * alpha[Q];
         sl += coef * e * d2.v[i][j];
         sv += coef * e;
+        if (P == Q) st += kv;
       }
     }
   }
   const double w = (ij.x == ij.y) ? 1.0 : 2.0;
   const double tl = block_sum(sl, red, tid);
   const double tv = block_sum(sv, red, tid);
+  const double ts = part_t ? block_sum(st, red, tid) : 0.0;
   if (tid == 0) {
     part_l[blockIdx.x] = w * tl;
     part_v[blockIdx.x] = w * tv;
+    if (part_t) part_t[blockIdx.x] = ts;
   }
 }
 
@@ -353,18 +364,26 @@ cudaError_t launch_cross(double* B, int64_t ldb, double* mpart, const double* al
 
 cudaError_t launch_prior(double* S, int64_t mp, const double* zt, int64_t m, int d, SekParams sp,
                          cudaStream_t s) {
-  dim3 grid(static_cast<unsigned>(mp / SB), static_cast<unsigned>(mp / SB));
-  prior_kernel<<<grid, ST, 0, s>>>(S, mp, zt, m, d, sp);
+  return launch_prior2(S, mp, mp, mp, zt, m, zt, m, d, sp, s);
+}
+
+cudaError_t launch_prior2(double* S, int64_t lds, int64_t mpa, int64_t mpb, const double* za,
+                          int64_t ma, const double* zb, int64_t mb, int d, SekParams sp,
+                          cudaStream_t s) {
+  if (mpa <= 0 || mpb <= 0) return cudaSuccess;
+  dim3 grid(static_cast<unsigned>(mpa / SB), static_cast<unsigned>(mpb / SB));
+  prior_kernel<<<grid, ST, 0, s>>>(S, lds, za, ma, zb, mb, d, sp);
   return cudaGetLastError();
 }
 
-cudaError_t launch_trace(const double* kinv, const int2* tile_ij_cm, int64_t ntiles, int T,
+cudaError_t launch_trace(const double* kinv, const int2* tile_ij, int64_t ntiles, TraceTiles tt,
                          const double* zp, const double* alpha, int d, int bi, PadMap pm,
-                         SekParams sp, double* part_l, double* part_v, cudaStream_t s) {
-  (void)T;
+                         SekParams sp, double* part_l, double* part_v, double* part_t,
+                         cudaStream_t s) {
   const int64_t nbs = bi / SB;
+  if (ntiles <= 0) return cudaSuccess;
   trace_kernel<<<static_cast<unsigned>(ntiles * nbs * nbs), ST, 0, s>>>(
-      kinv, tile_ij_cm, zp, alpha, d, bi, pm, sp, part_l, part_v);
+      kinv, tile_ij, zp, alpha, d, bi, pm, sp, tt, part_l, part_v, part_t);
   return cudaGetLastError();
 }
 

@@ -289,6 +289,19 @@ cudaError_t launch_export_lower(const double* tiles, int T, int bi, int64_t n, P
   return cudaGetLastError();
 }
 
+namespace {
+__global__ void set_diag_kernel(double* G, int64_t ld, int64_t count) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c < count) G[c * ld + c] = 1.0;
+}
+}  // namespace
+
+cudaError_t launch_set_diag(double* G, int64_t ld, int64_t count, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  set_diag_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(G, ld, count);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_copy_panel(double* ltiles, const double* scratch, int T, int k, int bi,
                               cudaStream_t s) {
   const int64_t e = static_cast<int64_t>(T - k - 1) * bi * bi / 2;

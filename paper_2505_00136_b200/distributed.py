@@ -20,6 +20,12 @@ owns; the partial vectors of segment i are all-gathered and summed in rank
 order (deterministic), then L_ii^-1 gives beta_i.  Log-determinant partials
 are gathered the same way.
 
+Gradients (model.py:341-435) are split by column panels of K^-1: each rank
+forms K^-1[:, panel] = L^-T (L^-1 E_panel) for the panels assigned to it
+(``gradient_column_chunks``) from its copy of the factor and runs the fused
+trace pass over them; the three partial sums are all-gathered and added in
+rank order.  Panels are independent, so this needs no other exchange.
+
 Prediction is sharded over test points (no collective during the solve):
 every rank gathers the full lower factor into a local single-GPU model
 (owned tiles broadcast rank by rank), predicts its slice of the test points
@@ -73,6 +79,26 @@ class BlockCyclic:
     def panel_rows(self, k: int, p: int) -> list[int]:
         """Panel tiles i > k held by process row p at step k (in order)."""
         return [i for i in range(k + 1, self.T) if i % self.P == p]
+
+
+def gradient_column_chunks(tiles: int, world: int, width: int | None = None) -> list[list[tuple[int, int]]]:
+    """Deterministic split of the internal tile columns of K^-1 into panels
+    [j0, j1) and their assignment to ranks for the distributed gradient.
+
+    A panel costs ~2 (T - j0)^2 (j1 - j0) tile GEMMs (forward + backward
+    solve from row block j0), so panels are narrow (T / (4 world) tiles) and
+    handed out longest-first to the least-loaded rank (LPT).
+    """
+    c = width or max(1, tiles // (4 * world))
+    chunks = [(j, min(tiles, j + c)) for j in range(0, tiles, c)]
+    cost = {ch: float(tiles - ch[0]) ** 2 * (ch[1] - ch[0]) for ch in chunks}
+    load = [0.0] * world
+    out: list[list[tuple[int, int]]] = [[] for _ in range(world)]
+    for ch in sorted(chunks, key=lambda ch: (-cost[ch], ch[0])):
+        r = min(range(world), key=lambda q: (load[q], q))
+        out[r].append(ch)
+        load[r] += cost[ch]
+    return [sorted(o) for o in out]
 
 
 class DeviceTileOps:
@@ -184,6 +210,7 @@ class _DeviceReplica:
                                                ctypes.c_void_p(self.y.data_ptr()), train.n, train.d,
                                                tiles_per_dim, ctypes.byref(h)))
         self.h = h
+        self.n, self.tiles_per_dim = train.n, tiles_per_dim
         flags = (ctypes.c_uint8 * 3)(*[1 if t else 0 for t in params.trainable])
         _lib.check(lib.gpb_model_set_params(h, params.lengthscale, params.vertical_scale,
                                             params.noise_variance, flags))
@@ -209,6 +236,21 @@ class _DeviceReplica:
         _lib.check(self.ops.lib.gpb_loss_gradients(self.h, out))
         return (float(out[0]), float(out[1]), float(out[2]))
 
+    def gradient_terms(self, j0: int, j1: int) -> np.ndarray:
+        """Trace partials of K^-1 tile columns [j0, j1) (gpb_loss_gradient_terms),
+        split into narrower panels when the (n - j0 b) x (j1 - j0) b panel would
+        not fit in device memory."""
+        lay = _lib.layout(self.n, self.tiles_per_dim)
+        free, _ = torch.cuda.mem_get_info(self.ops.device)
+        per_col = 8.0 * (lay["T"] - j0) * lay["b"] * lay["b"]
+        width = max(1, int(0.4 * free // max(per_col, 1.0)))
+        acc = np.zeros(3)
+        for a in range(j0, j1, width):
+            out = (ctypes.c_double * 3)()
+            _lib.check(self.ops.lib.gpb_loss_gradient_terms(self.h, a, min(j1, a + width), out))
+            acc += np.array(out[:3])
+        return acc
+
     def publish(self):
         torch.cuda.current_stream(self.ops.device).synchronize()
         _lib.check(self.ops.lib.gpb_model_mark_factored(self.h))
@@ -225,12 +267,27 @@ class _DeviceReplica:
             ctypes.c_void_p(mean.data_ptr()), ctypes.c_void_p(var.data_ptr()) if want_var else None))
         return mean, var
 
-    def full_cov(self, zt: np.ndarray):
+    def solve_cross(self, zt: np.ndarray, ldv: int):
+        """(mean, V) of a shard of test points: V = L^-1 K*^T, n_p x ldv on the device."""
+        lay = _lib.layout(self.n, self.tiles_per_dim)
+        v = self.ops.zeros(lay["np"], ldv)
         m = zt.shape[0]
-        mean, cov = np.empty(m), np.empty((m, m))
-        _lib.check(self.ops.lib.gpb_predict(self.h, _lib.dptr(np.ascontiguousarray(zt)), m,
-                                            zt.shape[1], _lib.dptr(mean), None, _lib.dptr(cov)))
-        return mean, cov
+        mean = self.ops.zeros(max(1, m))
+        if m:
+            ztd = self.ops.from_numpy(zt)
+            _lib.check(self.ops.lib.gpb_predict_solve_device(
+                self.h, ctypes.c_void_p(ztd.data_ptr()), m, zt.shape[1], ctypes.c_void_p(mean.data_ptr()),
+                ctypes.c_void_p(v.data_ptr()), ldv))
+        return mean[:m], v
+
+    def cov_block(self, za: np.ndarray, va, zb: np.ndarray, vb, rows, col0: int):
+        """rows[:ma, col0:col0+mb] = K**(za, zb) - Va^T Vb (gpb_cov_block_device)."""
+        zad, zbd = self.ops.from_numpy(za), self.ops.from_numpy(zb)
+        ldo = rows.shape[1]
+        _lib.check(self.ops.lib.gpb_cov_block_device(
+            self.h, ctypes.c_void_p(zad.data_ptr()), za.shape[0], ctypes.c_void_p(va.data_ptr()),
+            va.shape[1], ctypes.c_void_p(zbd.data_ptr()), zb.shape[0], ctypes.c_void_p(vb.data_ptr()),
+            vb.shape[1], ctypes.c_void_p(rows.data_ptr() + col0 * 8), ldo))
 
     def close(self):
         if self.h is not None:
@@ -530,23 +587,68 @@ class DistributedGP:
     predict_with_uncertainty = predict_variance
 
     def predict_with_full_cov(self, test):
-        """Full posterior covariance on every rank from its replica (not sharded yet)."""
+        """Mean and full posterior covariance, sharded over test points
+        (option (i)): rank a solves V_a = L^-1 K*(shard a)^T,
+        the V blocks are all-gathered, rank a forms its block row
+        Sigma[a, :] = K**(a, :) - V_a^T V (one DMMA GEMM per column block) and
+        the block rows are all-gathered.  Diagonal clamped as model.py:488-496."""
         from .model import PredictionResult
 
         test = test if isinstance(test, Dataset) else Dataset(np.asarray(test.z), np.asarray(test.y))
         if test.d != self.train.d:
             raise DimensionMismatch(f"test has {test.d} features, model was trained with {self.train.d}")
-        mean, cov = self._ensure_replica().full_cov(test.z)
-        return PredictionResult(mean=mean, full_covariance=cov)
+        rep = self._ensure_replica()
+        m = test.n
+        per = -(-m // self.world)
+        ldv = max(128, -(-per // 128) * 128)
+        sh = self._shard(m)
+        t0 = self._event()
+        mean_a, va = rep.solve_cross(test.z[sh], ldv)
+        vall = self._allgather(va)
+        rows = self.ops.zeros(per, m)
+        for r in range(self.world):
+            lo, hi = min(m, r * per), min(m, (r + 1) * per)
+            if sh.stop > sh.start and hi > lo:
+                rep.cov_block(test.z[sh], va, test.z[lo:hi], vall[r], rows, lo)
+        out_m = self.ops.zeros(per)
+        out_m[: sh.stop - sh.start] = mean_a
+        gm = self._allgather(out_m).cpu().numpy().reshape(-1)[:m]
+        cov = self._allgather(rows).cpu().numpy().reshape(-1, m)[:m]
+        diag = np.diagonal(cov).copy()
+        bad = diag < -_VARIANCE_SLACK
+        if np.any(bad):
+            raise NumericalConsistencyError(
+                f"variance {float(diag[bad].min()):g} is below the round-off allowance "
+                f"-{_VARIANCE_SLACK:g}")
+        np.fill_diagonal(cov, np.where(diag < 0.0, 0.0, diag))
+        self.timings["full_cov_ms"] = self._elapsed(t0, self._event())
+        return PredictionResult(mean=gm, full_covariance=cov)
 
     # -- training (model.py:341-485) ----------------------------------------------
     def loss_gradients(self) -> tuple[float, float, float]:
-        """dNLL/d(l, nu, sigma^2) from the gathered factor (every rank computes
-        the same values on its replica; the K^-1 formation is not yet sharded)."""
+        """dNLL/d(l, nu, sigma^2) (model.py:341-435), split over ranks by
+        column panels of K^-1 (``gradient_column_chunks``): each rank sums
+        the trace terms of its panels, the partials are all-gathered and
+        added in rank order, so every rank returns the same values."""
         tr = self.params.trainable
         if not (tr[0] or tr[1] or tr[2]):
             return (0.0, 0.0, 0.0)
-        return self._ensure_replica().loss_gradients()
+        rep = self._ensure_replica()
+        t0 = self._event()
+        acc = np.zeros(3)
+        for j0, j1 in gradient_column_chunks(self.T, self.world)[self.rank]:
+            acc += rep.gradient_terms(j0, j1)
+        parts = self._allgather(self.ops.from_numpy(acc)).cpu().numpy()
+        tot = np.zeros(3)
+        for r in range(self.world):  # fixed rank order
+            tot += parts[r]
+        alpha = self.ops.to_numpy(self.alpha)
+        p = self.params
+        gl = 0.5 * (p.vertical_scale / p.lengthscale ** 3) * tot[0] if tr[0] else 0.0
+        gv = 0.5 * tot[1] if tr[1] else 0.0
+        gn = 0.5 * (tot[2] - float(alpha @ alpha)) if tr[2] else 0.0
+        self.timings["gradient_ms"] = self._elapsed(t0, self._event())
+        return (float(gl), float(gv), float(gn))
 
     def _set_params(self, params: KernelParams) -> None:
         self.params = params

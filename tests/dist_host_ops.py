@@ -150,7 +150,31 @@ class HostReplica:
             var = p.vertical_scale - (v * v).sum(0)
         return mean, var
 
-    def loss_gradients(self):
+    def _cross(self, zt):
+        z, p = self.train.z, self.params
+        d2 = ((zt[:, None, :] - z[None, :, :]) ** 2).sum(-1)
+        return p.vertical_scale * np.exp(d2 * (-1.0 / (2.0 * p.lengthscale ** 2)))
+
+    def solve_cross(self, zt, ldv):
+        lo, real = self._dense()
+        v = np.zeros((self.lay["np"], ldv))
+        mean = np.zeros(zt.shape[0])
+        if zt.shape[0]:
+            ks = self._cross(zt)
+            v[real, : zt.shape[0]] = np.linalg.solve(lo, ks.T)
+            mean = ks @ self.vecs["alpha"].numpy()[real]
+        return torch.from_numpy(mean), torch.from_numpy(v)
+
+    def cov_block(self, za, va, zb, vb, rows, col0):
+        p = self.params
+        d2 = ((za[:, None, :] - zb[None, :, :]) ** 2).sum(-1)
+        prior = p.vertical_scale * np.exp(d2 * (-1.0 / (2.0 * p.lengthscale ** 2)))
+        blk = prior - va.numpy()[:, : za.shape[0]].T @ vb.numpy()[:, : zb.shape[0]]
+        rows[: za.shape[0], col0:col0 + zb.shape[0]] = torch.from_numpy(blk)
+
+    def gradient_terms(self, j0, j1):
+        """Numpy restatement of gpb_loss_gradient_terms over padded positions."""
+        b, n_p = self.lay["b"], self.lay["np"]
         lo, real = self._dense()
         z, p = self.train.z, self.params
         d2 = ((z[:, None, :] - z[None, :, :]) ** 2).sum(-1)
@@ -159,11 +183,21 @@ class HostReplica:
         kinv = linv.T @ linv
         alpha = self.vecs["alpha"].numpy()[real]
         w = kinv - np.outer(alpha, alpha)
-        tl, tv, tn = p.trainable
-        gl = 0.5 * float(np.sum(w * (p.vertical_scale / p.lengthscale ** 3) * e * d2)) if tl else 0.0
-        gv = 0.5 * float(np.sum(w * e)) if tv else 0.0
-        gn = 0.5 * (float(np.trace(kinv)) - float(alpha @ alpha)) if tn else 0.0
-        return (gl, gv, gn)
+        full = lambda a: self._embed(a, real, n_p)  # noqa: E731
+        ml, mv, kd = full(w * e * d2), full(w * e), full(np.diag(np.diag(kinv)))
+        out = np.zeros(3)
+        for jj in range(j0, j1):
+            for i in range(jj, self.lay["T"]):
+                blk = (slice(i * b, (i + 1) * b), slice(jj * b, (jj + 1) * b))
+                wt = 1.0 if i == jj else 2.0
+                out += [wt * ml[blk].sum(), wt * mv[blk].sum(), kd[blk].sum()]
+        return out
+
+    @staticmethod
+    def _embed(a, real, n_p):
+        out = np.zeros((n_p, n_p))
+        out[np.ix_(real, real)] = a
+        return out
 
     def close(self):
         pass

@@ -67,12 +67,14 @@ def _body(rank, world, kind, device, out_q):
         ll = model.log_likelihood()
         pv = model.predict_variance(gpb.Dataset(zt, np.zeros(len(zt))))
         L = model.cholesky()
+        fc = model.predict_with_full_cov(gpb.Dataset(zt, np.zeros(len(zt))))
         grads = model.loss_gradients()
         hist = model.optimize(gpb.AdamConfig(learning_rate=0.1, iterations=2))
         model.close()
         if rt is not None:
             rt.stop()
-        out_q.put((rank, ll, pv.mean, pv.variance, (L if rank == 0 else None, grads, hist)))
+        out_q.put((rank, ll, pv.mean, pv.variance,
+                   (L if rank == 0 else None, grads, hist, fc.mean, fc.full_covariance)))
 
 
 def _run(world, kind, device=False):
@@ -100,13 +102,16 @@ def _check(res, kind):
     ll_o = o.log_likelihood()
     L_o = o.factor_dense()
     grads_o = o.loss_gradients()
-    hist_o = o.optimize(lr=0.1, iterations=2)
-    for rank, ll, mean, var, (L, grads, hist) in res:  # every rank returns the full result
+    _, cov_o = o.predict_full_cov(zt)
+    hist_o = o.optimize(lr=0.1, iterations=2)  # changes o's parameters: last
+    for rank, ll, mean, var, (L, grads, hist, fc_mean, cov) in res:  # every rank: full result
         assert abs(ll - ll_o) <= 1e-9 * abs(ll_o)
         assert rel_fro(mean, mean_o) <= 1e-9
         assert rel_fro(var, var_o) <= 1e-9
         assert rel_fro(np.array(grads), np.array(grads_o)) <= 1e-9
         assert rel_fro(np.array(hist), np.array(hist_o)) <= 1e-9
+        assert rel_fro(fc_mean, mean_o) <= 1e-9
+        assert rel_fro(cov, cov_o) <= 1e-9 and np.array_equal(cov, cov.T)
         if L is not None:
             assert rel_fro(L, L_o) <= 1e-10
 
@@ -126,6 +131,19 @@ def test_process_grid_and_ownership():
     assert sorted(set(owners)) == list(range(8))
     assert sum(len(cyc.owned(r)) for r in range(8)) == 28
     assert cyc.panel_rows(2, 1) == [3, 5]
+
+
+def test_gradient_column_chunks_partition():
+    from paper_2505_00136_b200.distributed import gradient_column_chunks
+
+    for T, world in [(1, 1), (6, 2), (64, 8), (256, 8), (7, 3), (3, 4)]:
+        parts = gradient_column_chunks(T, world)
+        assert len(parts) == world and parts == gradient_column_chunks(T, world)
+        cols = sorted(c for p in parts for j0, j1 in p for c in range(j0, j1))
+        assert cols == list(range(T))  # every tile column exactly once
+        if T >= 4 * world:  # LPT keeps the per-rank cost within 2x of the mean
+            cost = [sum((T - j0) ** 2 * (j1 - j0) for j0, j1 in p) for p in parts]
+            assert max(cost) <= 2.0 * sum(cost) / world
 
 
 @pytest.mark.gpu

@@ -288,6 +288,36 @@ class TestGradientsAndAdam:
         expected = 0.5 * (np.trace(np.linalg.inv(k)) - alpha @ alpha)
         assert gpb.GPModel(ds(z, y), tiles_per_dim=4).loss_gradients()[2] == pytest.approx(expected, rel=1e-9)
 
+    @pytest.mark.parametrize("n,t,world", [(600, 6, 2), (1024, 4, 3), (2048, 4, 1)])
+    def test_column_panel_terms(self, runtime, n, t, world):
+        """gpb_loss_gradient_terms (the multi-GPU split of the gradient):
+        summed over every rank's panels it reproduces loss_gradients and the oracle."""
+        import ctypes
+
+        from paper_2505_00136_b200 import _lib
+        from paper_2505_00136_b200.distributed import gradient_column_chunks
+
+        rng = np.random.default_rng(n + t)
+        z, y = rng.normal(size=(n, 3)), rng.normal(size=n)
+        model = gpb.GPModel(ds(z, y), gpb.KernelParams(1.2, 0.9, 0.15), t)
+        whole = np.array(model.loss_gradients())
+        lay = _lib.layout(n, t)
+        lib, tot = _lib.load(), np.zeros(3)
+        for chunks in gradient_column_chunks(lay["T"], world):
+            for j0, j1 in chunks:
+                out = (ctypes.c_double * 3)()
+                _lib.check(lib.gpb_loss_gradient_terms(model._handle, j0, j1, out))
+                tot += np.array(out[:3])
+        p = model.params
+        alpha = np.linalg.solve(dense_k(z, 1.2, 0.9, 0.15), y)
+        split = np.array([0.5 * p.vertical_scale / p.lengthscale ** 3 * tot[0], 0.5 * tot[1],
+                          0.5 * (tot[2] - alpha @ alpha)])
+        assert rel(split, whole) <= 1e-11
+        assert rel(split, OracleGP(z, y, t, 1.2, 0.9, 0.15).loss_gradients()) <= TOL
+        with pytest.raises(gpb.errors.InvalidConfig):
+            lib_out = (ctypes.c_double * 3)()
+            _lib.check(lib.gpb_loss_gradient_terms(model._handle, 0, lay["T"] + 1, lib_out))
+
     def test_adam_semantics(self, runtime, rng):
         train = ds(rng.normal(size=(16, 3)), rng.normal(size=16))
         kp = gpb.KernelParams()
