@@ -77,15 +77,16 @@ int gpb_last_pivot(gpb_model* m, int64_t* pivot);
 int gpb_log_likelihood(gpb_model* m, double* out);
 /* dNLL/d(l, nu, s2) (model.py:341-435); zeros for non-trainable */
 int gpb_loss_gradients(gpb_model* m, double out[3]);
-/* Gradient terms of the internal K^-1 tile columns [col0, col1) (tiles of
- * gpb_layout's out[0] size), for splitting loss_gradients across ranks that
- * each hold the factor (model.py:362-432 restated per column panel):
+/* Gradient terms of a set of internal K^-1 tile columns (tiles of gpb_layout's
+ * out[0] size), for splitting loss_gradients across ranks that each hold the
+ * factor (model.py:362-432 restated per tile column):
  *   out[0] = sum w (K^-1 - a a^T) o E o D2,  out[1] = sum w (K^-1 - a a^T) o E,
- *   out[2] = sum of the real diagonal entries of K^-1   (w = 2 off the diagonal).
+ *   out[2] = sum of the real diagonal entries of K^-1   (w = 2 off the diagonal),
+ * each over the lower tiles (i >= J) of the columns J in cols (strictly increasing).
  * Summed over a partition of [0, T): dNLL/dl = nu / (2 l^3) out[0],
  * dNLL/dnu = out[1] / 2, dNLL/ds2 = (out[2] - |alpha|^2) / 2.
- * GPB_NO_MEMORY if the (n - col0 b) x (col1 - col0) b panel does not fit. */
-int gpb_loss_gradient_terms(gpb_model* m, int64_t col0, int64_t col1, double out[3]);
+ * GPB_NO_MEMORY if the (n - cols[0] b) x ncols b panel does not fit. */
+int gpb_loss_gradient_terms(gpb_model* m, const int* cols, int64_t ncols, double out[3]);
 /* Adam on log-parameters (model.py:437-485). history: iterations NLLs.
  * On GPB_NOT_PD the message is prefixed "iteration k: ". */
 int gpb_optimize(gpb_model* m, double learning_rate, double beta1, double beta2,

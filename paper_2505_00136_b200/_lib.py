@@ -51,7 +51,8 @@ SIGNATURES = {
                                                  ctypes.c_int64]),
     "gpb_cov_block_device": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp,
                                              ctypes.c_int64, _vp, ctypes.c_int64, _vp, ctypes.c_int64]),
-    "gpb_loss_gradient_terms": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, _c_double_p]),
+    "gpb_loss_gradient_terms": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int), ctypes.c_int64,
+                                               _c_double_p]),
     "gpb_optimize": (ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                     ctypes.c_double, ctypes.c_int64, _c_double_p]),
     "gpb_predict": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_int64, ctypes.c_int64,

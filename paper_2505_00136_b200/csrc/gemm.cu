@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_grouped_kernel(cons
   const int mb = local - nb * p.mblk;
   const GemmJob job = p.jobs[job_id];
   if (job.lower && nb > mb) return;
+  if (job.nlim > 0 && nb >= job.nlim) return;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;

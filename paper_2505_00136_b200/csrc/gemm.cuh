@@ -11,9 +11,10 @@
 //
 // A is M x K, B is N x K (so the product is "NT"); each operand is either
 // K-MAJOR (k contiguous: element (m,k) at base[m*ld + k]) or MN-MAJOR (m
-// contiguous: element (m,k) at base[k*ld + m]).  A K-MAJOR operand may be
-// "tiled in k": element (m,k) at base[(k/ktile)*kstride + m*ld + k%ktile],
-// which walks a row panel of packed lower tiles without a copy.
+// contiguous: element (m,k) at base[k*ld + m]).  Either operand may be
+// "tiled in k": k runs through consecutive ktile-deep tiles kstride apart
+// (K-MAJOR: element (m,k) at base[(k/ktile)*kstride + m*ld + k%ktile]), which
+// walks a row (or, transposed, a column) panel of packed tiles without a copy.
 #pragma once
 #include "common.cuh"
 
@@ -33,7 +34,8 @@ struct __align__(16) GemmJob {
   double* aux;         // EPI_SUMSQ: base of this job's partial rows
   int K;               // multiple of GBK, may be 0
   int lower;           // 1: skip blocks above the block diagonal (diagonal tiles)
-  int64_t pad_;
+  int nlim;            // > 0: only the first nlim 128-column blocks of this job
+  int pad_;
 };
 
 struct GemmParams {

@@ -684,7 +684,7 @@ int loss_gradients(gpb_model* m, double out[3]) {
     GPB_TRY(gemm(m, kp, false, false, EPI_AXPBY,
                  gemm_flops(int64_t(nb) * nb, int64_t(bi) * Ti * (Ti + 1) * (Ti + 2) / 6)));
     // fused trace pass (model.py:382-414 with covariance.py:196-220 regenerated)
-    CUDA_TRY(launch_trace(m->Kinv.as<double>(), m->tile_cm.as<int2>(), ntiles, TraceTiles{0, 0, 0},
+    CUDA_TRY(launch_trace(m->Kinv.as<double>(), m->tile_cm.as<int2>(), ntiles, TraceTiles{0, 0, 0, nullptr},
                           m->zp.as<double>(), m->alpha.as<double>(), static_cast<int>(m->d), bi,
                           m->pm, sek_params(m), m->part_l.as<double>(), m->part_v.as<double>(),
                           nullptr, m->st));
@@ -711,120 +711,148 @@ int loss_gradients(gpb_model* m, double out[3]) {
   return GPB_OK;
 }
 
-// ---- gradient terms over a range of K^-1 tile columns (multi-GPU split) ----
+// ---- gradient terms over a set of K^-1 tile columns (multi-GPU split) ------
 // The single-GPU gradient forms X = L^-1 then K^-1 = X^T X, which needs all of X
 // for every column of K^-1.  Split across ranks, each rank instead forms the
-// panel K^-1[:, J0*bi .. J1*bi) = L^-T (L^-1 E) directly from the (replicated)
-// factor: a forward solve of the identity panel from row block J0 (the
-// prediction sweep's jobs) and a right-looking backward solve with L^T, then
-// the trace pass over the panel's lower tiles.  Column panels are independent,
-// so ranks need no exchange until the three partial sums are combined.
+// tile columns J of K^-1 it is assigned, K^-1[:, J] = L^-T (L^-1 E_J), from the
+// (replicated) factor, one panel slot per column:
+//   forward  V = L^-1 E: row block i, slot J <= i:  H_J = E_iJ - L[i, J..i) V[J..i)_J
+//            (one GEMM job per slot, K = (i - J) b: no work on the zero rows above J),
+//            then V_i = Dinv_i H over the active slots;
+//   backward W = L^-T V: row block i (descending), the slots with J <= i at once:
+//            H = V_i - L[i+1.., i]^T W[i+1..]  (column i of L read from a
+//            column-major-tile copy kept in X, K = (T - 1 - i) b),  W_i = Dinv_i^T H;
+// then the fused trace pass over the slots' lower tiles (i >= J).  Columns are
+// independent, so ranks need no exchange until the three partial sums are added.
 // out = {sum w (K^-1 - a a^T) e d2, sum w (K^-1 - a a^T) e, sum of real diag K^-1}.
-int grad_partial(gpb_model* m, int J0, int J1, double out[3]) {
+int grad_partial(gpb_model* m, const int* cols, int ncols, double out[3]) {
   const int Ti = m->Ti, bi = m->bi, nb = bi / GBM;
-  if (J0 < 0 || J1 > Ti || J0 >= J1)
-    return fail(GPB_INVALID_CONFIG, "tile column range [" + std::to_string(J0) + ", " +
-                                        std::to_string(J1) + ") outside [0, " + std::to_string(Ti) +
-                                        ")");
+  if (ncols < 1 || !cols) return fail(GPB_INVALID_CONFIG, "empty tile column set");
+  for (int s = 0; s < ncols; ++s)
+    if (cols[s] < 0 || cols[s] >= Ti || (s > 0 && cols[s] <= cols[s - 1]))
+      return fail(GPB_INVALID_CONFIG, "tile columns must be increasing and inside [0, " +
+                                          std::to_string(Ti) + ")");
   GPB_TRY(ensure_weights(m));
   const int64_t bi2 = int64_t(bi) * bi;
-  const int64_t w = int64_t(J1 - J0) * bi;           // panel width
-  const int64_t rows = int64_t(Ti - J0) * bi;        // panel rows: global J0*bi ..
+  const int R0 = cols[0];
+  const int64_t w = int64_t(ncols) * bi;          // panel width: one slot per column
+  const int64_t rows = int64_t(Ti - R0) * bi;     // panel rows: global R0*bi ..
   if (m->gp_panel.ensure(sizeof(double) * rows * w) != cudaSuccess) {
     cudaGetLastError();
     return fail(GPB_NO_MEMORY, "gradient panel of " + std::to_string(rows) + " x " +
-                                   std::to_string(w) + " does not fit; use narrower column ranges");
+                                   std::to_string(w) + " does not fit; pass fewer tile columns");
   }
   CUDA_TRY(m->gp_h.ensure(sizeof(double) * bi * w));
   double* G = m->gp_panel.as<double>();
   double* H = m->gp_h.as<double>();
   double* L = m->L.as<double>();
   double* D = m->Dinv.as<double>();
-  // job table: forward (W, V per row block), backward (H, updates) per step
+  PhaseTimer pt(m, 5);
+  auto active = [&](int i) {  // slots with column <= i (a prefix: cols ascending)
+    return static_cast<int>(std::upper_bound(cols, cols + ncols, i) - cols);
+  };
+  const int nbt = bi / GBN;
   std::vector<GemmJob> jobs;
-  std::vector<int64_t> fw_off, bw_h_off, bw_u_off;
-  for (int i = J0; i < Ti; ++i) {
-    fw_off.push_back(jobs.size());
-    GemmJob g{};  // H = E_i - L[i, J0..i) V[J0..i)
-    g.A = L + h_tri_rm(i, J0) * bi2;
-    g.B = G;
-    g.Cin = G + int64_t(i - J0) * bi * w;
-    g.Cout = H;
-    g.K = (i - J0) * bi;
-    jobs.push_back(g);
-    for (int r = 0; r < nb; ++r) {  // V_i = Dinv_i H (lower: k < (r+1)*128)
+  std::vector<int64_t> fd_off, fu_off, bd_off, bu_off;
+  for (int i = R0; i < Ti; ++i) {  // forward, right-looking
+    const int a = active(i);
+    fd_off.push_back(jobs.size());
+    for (int r = 0; r < nb; ++r) {  // H = V_i = Dinv_i G_i  (lower: k < (r+1)*128)
       GemmJob v{};
       v.A = D + int64_t(i) * bi2 + int64_t(r) * GBM * bi;
-      v.B = H;
-      v.Cout = G + (int64_t(i - J0) * bi + r * GBM) * w;
+      v.B = G + int64_t(i - R0) * bi * w;
+      v.Cout = H + int64_t(r) * GBM * w;
       v.K = (r + 1) * GBM;
       jobs.push_back(v);
     }
+    fu_off.push_back(jobs.size());
+    for (int q = i + 1; q < Ti; ++q) {  // G_q -= L[q, i] V_i  (active slots only)
+      GemmJob u{};
+      u.A = L + h_tri_rm(q, i) * bi2;
+      u.B = H;
+      u.Cin = u.Cout = G + int64_t(q - R0) * bi * w;
+      u.K = bi;
+      u.nlim = a * nbt;
+      jobs.push_back(u);
+    }
   }
-  for (int i = Ti - 1; i >= J0; --i) {
-    bw_h_off.push_back(jobs.size());
-    for (int r = 0; r < nb; ++r) {  // H = Dinv_i^T G_i (upper: k >= r*128)
+  for (int i = Ti - 1; i >= R0; --i) {  // backward, right-looking
+    bd_off.push_back(jobs.size());
+    for (int r = 0; r < nb; ++r) {  // H = W_i = Dinv_i^T G_i  (upper: k >= r*128)
       GemmJob h{};
       h.A = D + int64_t(i) * bi2 + int64_t(r) * GBM * bi + r * GBM;
-      h.B = G + (int64_t(i - J0) * bi + r * GBM) * w;
+      h.B = G + (int64_t(i - R0) * bi + r * GBM) * w;
       h.Cout = H + int64_t(r) * GBM * w;
       h.K = bi - r * GBM;
       jobs.push_back(h);
     }
-    bw_u_off.push_back(jobs.size());
-    for (int r = J0; r < i; ++r) {  // G_r -= L[i, r]^T H
+    bu_off.push_back(jobs.size());
+    for (int q = R0; q < i; ++q) {  // G_q -= L[i, q]^T W_i  (slots with column <= q)
       GemmJob u{};
-      u.A = L + h_tri_rm(i, r) * bi2;
+      u.A = L + h_tri_rm(i, q) * bi2;
       u.B = H;
-      u.Cin = u.Cout = G + int64_t(r - J0) * bi * w;
+      u.Cin = u.Cout = G + int64_t(q - R0) * bi * w;
       u.K = bi;
+      u.nlim = active(q) * nbt;
       jobs.push_back(u);
     }
   }
   std::vector<int2> tl;
-  for (int j = J0; j < J1; ++j)
-    for (int i = j; i < Ti; ++i) tl.push_back(make_int2(i, j));
+  std::vector<int> slot;
+  for (int s = 0; s < ncols; ++s)
+    for (int i = cols[s]; i < Ti; ++i) {
+      tl.push_back(make_int2(i, cols[s]));
+      slot.push_back(s);
+    }
   const int64_t ntl = static_cast<int64_t>(tl.size());
   const int64_t nblk = ntl * (bi / kSekBlock) * (bi / kSekBlock);
   CUDA_TRY(m->gp_jobs.ensure(sizeof(GemmJob) * jobs.size()));
-  CUDA_TRY(m->gp_tiles.ensure(sizeof(int2) * tl.size()));
+  CUDA_TRY(m->gp_tiles.ensure((sizeof(int2) + sizeof(int)) * tl.size()));
   CUDA_TRY(m->part_l.ensure(sizeof(double) * nblk));
   CUDA_TRY(m->part_v.ensure(sizeof(double) * nblk));
   CUDA_TRY(m->part_x.ensure(sizeof(double) * nblk));
+  int2* d_tl = m->gp_tiles.as<int2>();
+  int* d_slot = reinterpret_cast<int*>(d_tl + ntl);
   CUDA_TRY(cudaMemcpyAsync(m->gp_jobs.p, jobs.data(), sizeof(GemmJob) * jobs.size(),
                            cudaMemcpyHostToDevice, m->st));
-  CUDA_TRY(cudaMemcpyAsync(m->gp_tiles.p, tl.data(), sizeof(int2) * tl.size(),
-                           cudaMemcpyHostToDevice, m->st));
+  CUDA_TRY(cudaMemcpyAsync(d_tl, tl.data(), sizeof(int2) * ntl, cudaMemcpyHostToDevice, m->st));
+  CUDA_TRY(cudaMemcpyAsync(d_slot, slot.data(), sizeof(int) * ntl, cudaMemcpyHostToDevice, m->st));
   const GemmJob* dj = m->gp_jobs.as<GemmJob>();
-  const int nbn = static_cast<int>(w / GBN);
-  PhaseTimer pt(m, 5);
   CUDA_TRY(cudaMemsetAsync(G, 0, sizeof(double) * rows * w, m->st));
-  CUDA_TRY(launch_set_diag(G, w, w, m->st));
-  ++m->launches;
-  for (int i = J0; i < Ti; ++i) {
-    const int64_t o = fw_off[i - J0];
-    GemmParams f = base_params(dj + o, 1, nb, nbn, bi, w, w, -1.0, 1.0);
-    f.a_ktile = bi;
-    f.a_kstride = bi2;
-    f.max_k = int64_t(i - J0) * bi;
-    GPB_TRY(gemm(m, f, true, false, EPI_AXPBY, gemm_flops(int64_t(nb) * nbn, int64_t(i - J0) * bi)));
-    GemmParams v = base_params(dj + o + 1, nb, 1, nbn, bi, w, w, 1.0, 0.0);
-    GPB_TRY(gemm(m, v, true, false, EPI_AXPBY, gemm_flops(nbn, int64_t(GBM) * nb * (nb + 1) / 2)));
-  }
-  for (int i = Ti - 1; i >= J0; --i) {
-    const int s = Ti - 1 - i;
-    GemmParams h = base_params(dj + bw_h_off[s], nb, 1, nbn, bi, w, w, 1.0, 0.0);
-    GPB_TRY(gemm(m, h, false, false, EPI_AXPBY, gemm_flops(nbn, int64_t(GBM) * nb * (nb + 1) / 2)));
-    CUDA_TRY(cudaMemcpyAsync(G + int64_t(i - J0) * bi * w, H, sizeof(double) * bi * w,
-                             cudaMemcpyDeviceToDevice, m->st));
-    if (i > J0) {
-      GemmParams u = base_params(dj + bw_u_off[s], i - J0, nb, nbn, bi, w, w, -1.0, 1.0);
+  for (int s = 0; s < ncols; ++s)  // E: identity block of column cols[s] in slot s
+    CUDA_TRY(launch_set_diag(G + int64_t(cols[s] - R0) * bi * w + int64_t(s) * bi, w, bi, m->st));
+  m->launches += ncols;
+  const size_t row_bytes = sizeof(double) * bi * w;
+  for (int i = R0; i < Ti; ++i) {
+    const int a = active(i);
+    const int64_t k = i - R0;
+    GemmParams v = base_params(dj + fd_off[k], nb, 1, a * nbt, bi, w, w, 1.0, 0.0);
+    GPB_TRY(gemm(m, v, true, false, EPI_AXPBY, gemm_flops(a * nbt, int64_t(GBM) * nb * (nb + 1) / 2)));
+    CUDA_TRY(cudaMemcpyAsync(G + k * bi * w, H, row_bytes, cudaMemcpyDeviceToDevice, m->st));
+    if (i + 1 < Ti) {
+      GemmParams u = base_params(dj + fu_off[k], Ti - 1 - i, nb, a * nbt, bi, w, w, -1.0, 1.0);
       u.max_k = bi;
-      GPB_TRY(gemm(m, u, false, false, EPI_AXPBY, gemm_flops(int64_t(i - J0) * nb * nbn, bi)));
+      GPB_TRY(gemm(m, u, true, false, EPI_AXPBY,
+                   gemm_flops(int64_t(Ti - 1 - i) * nb * a * nbt, bi)));
+    }
+  }
+  for (int i = Ti - 1; i >= R0; --i) {
+    const int a = active(i);
+    const int64_t s = Ti - 1 - i;
+    GemmParams h = base_params(dj + bd_off[s], nb, 1, a * nbt, bi, w, w, 1.0, 0.0);
+    GPB_TRY(gemm(m, h, false, false, EPI_AXPBY, gemm_flops(a * nbt, int64_t(GBM) * nb * (nb + 1) / 2)));
+    CUDA_TRY(cudaMemcpyAsync(G + int64_t(i - R0) * bi * w, H, row_bytes, cudaMemcpyDeviceToDevice,
+                             m->st));
+    if (i > R0) {
+      int64_t blocks = 0;
+      for (int q = R0; q < i; ++q) blocks += int64_t(nb) * active(q) * nbt;
+      GemmParams u = base_params(dj + bu_off[s], i - R0, nb, a * nbt, bi, w, w, -1.0, 1.0);
+      u.max_k = bi;
+      GPB_TRY(gemm(m, u, false, false, EPI_AXPBY, gemm_flops(blocks, bi)));
     }
   }
   double* red = m->red.as<double>();
-  CUDA_TRY(launch_trace(G, m->gp_tiles.as<int2>(), ntl, TraceTiles{w, J0, J0}, m->zp.as<double>(),
+  CUDA_TRY(launch_trace(G, d_tl, ntl, TraceTiles{w, R0, 0, d_slot}, m->zp.as<double>(),
                         m->alpha.as<double>(), static_cast<int>(m->d), bi, m->pm, sek_params(m),
                         m->part_l.as<double>(), m->part_v.as<double>(), m->part_x.as<double>(),
                         m->st));
@@ -1232,10 +1260,11 @@ int gpb_loss_gradients(gpb_model* m, double out[3]) {
   return loss_gradients(m, out);
 }
 
-int gpb_loss_gradient_terms(gpb_model* m, int64_t col0, int64_t col1, double out[3]) {
+int gpb_loss_gradient_terms(gpb_model* m, const int* cols, int64_t ncols, double out[3]) {
   GPB_TRY(check_live(m));
   if (!out) return fail(GPB_INVALID_CONFIG, "null output");
-  return grad_partial(m, static_cast<int>(col0), static_cast<int>(col1), out);
+  if (ncols > (int64_t(1) << 30)) return fail(GPB_INVALID_CONFIG, "too many tile columns");
+  return grad_partial(m, cols, static_cast<int>(ncols), out);
 }
 
 int gpb_optimize(gpb_model* m, double lr, double b1, double b2, double eps, int64_t iters,

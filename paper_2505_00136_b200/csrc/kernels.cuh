@@ -85,11 +85,13 @@ cudaError_t launch_prior2(double* S, int64_t lds, int64_t mpa, int64_t mpb, cons
 // part_l = w * sum (Kinv - alpha alpha^T) e d2,  part_v = w * sum (Kinv - ..) e,
 // part_t (optional) = sum of the real diagonal entries of Kinv (w = 2 off the diagonal).
 // Tile t = tile_ij[t] is read from packed tiles (ld == 0: kinv + t * bi^2, column-major
-// tile order) or from a dense row-major panel whose entry (0, 0) is global
-// position (row0 * bi, col0 * bi) (ld > 0).
+// tile order) or from a dense row-major panel (ld > 0) whose row 0 is global
+// position row0 * bi; tile t's columns start at panel column slot[t] * bi (slot
+// non-null) or at (j - col0) * bi.
 struct TraceTiles {
   int64_t ld;
   int row0, col0;
+  const int* slot;
 };
 cudaError_t launch_trace(const double* kinv, const int2* tile_ij, int64_t ntiles, TraceTiles tt,
                          const double* zp, const double* alpha, int d, int bi, PadMap pm,

@@ -273,10 +273,12 @@ __global__ void __launch_bounds__(ST) trace_kernel(const double* kinv, const int
   Frag d2;
   sq_dists_blk(d2, zp, P0, zp, Q0, d, sa, sb, tx, ty, tid);
   // packed tiles (ld == 0): tile t at kinv + t * bi^2; dense column panel
-  // (ld > 0): entry (P, Q) at kinv + (P - row0 * bi) * ld + (Q - col0 * bi)
+  // (ld > 0): row P at kinv + (P - row0 * bi) * ld, columns from slot[t] * bi
+  // (or Q - col0 * bi)
   const int64_t ldk = tt.ld > 0 ? tt.ld : bi;
-  const double* kt = tt.ld > 0 ? kinv + (P0 - static_cast<int64_t>(tt.row0) * bi) * tt.ld +
-                                     (Q0 - static_cast<int64_t>(tt.col0) * bi)
+  const int64_t pc = tt.slot ? static_cast<int64_t>(tt.slot[t]) * bi + cb * SB
+                             : Q0 - static_cast<int64_t>(tt.col0) * bi;
+  const double* kt = tt.ld > 0 ? kinv + (P0 - static_cast<int64_t>(tt.row0) * bi) * tt.ld + pc
                                : kinv + t * bi * bi + static_cast<int64_t>(rb * SB) * bi + cb * SB;
   double sl = 0.0, sv = 0.0, st = 0.0;
 #pragma unroll

@@ -20,11 +20,11 @@ owns; the partial vectors of segment i are all-gathered and summed in rank
 order (deterministic), then L_ii^-1 gives beta_i.  Log-determinant partials
 are gathered the same way.
 
-Gradients (model.py:341-435) are split by column panels of K^-1: each rank
-forms K^-1[:, panel] = L^-T (L^-1 E_panel) for the panels assigned to it
-(``gradient_column_chunks``) from its copy of the factor and runs the fused
-trace pass over them; the three partial sums are all-gathered and added in
-rank order.  Panels are independent, so this needs no other exchange.
+Gradients (model.py:341-435) are split by tile columns of K^-1: each rank
+forms K^-1[:, J] = L^-T (L^-1 E_J) for the columns assigned to it
+(``gradient_columns``) from its copy of the factor and runs the fused trace
+pass over them; the three partial sums are all-gathered and added in rank
+order.  Columns are independent, so this needs no other exchange.
 
 Prediction is sharded over test points (no collective during the solve):
 every rank gathers the full lower factor into a local single-GPU model
@@ -81,24 +81,16 @@ class BlockCyclic:
         return [i for i in range(k + 1, self.T) if i % self.P == p]
 
 
-def gradient_column_chunks(tiles: int, world: int, width: int | None = None) -> list[list[tuple[int, int]]]:
-    """Deterministic split of the internal tile columns of K^-1 into panels
-    [j0, j1) and their assignment to ranks for the distributed gradient.
-
-    A panel costs ~2 (T - j0)^2 (j1 - j0) tile GEMMs (forward + backward
-    solve from row block j0), so panels are narrow (T / (4 world) tiles) and
-    handed out longest-first to the least-loaded rank (LPT).
-    """
-    c = width or max(1, tiles // (4 * world))
-    chunks = [(j, min(tiles, j + c)) for j in range(0, tiles, c)]
-    cost = {ch: float(tiles - ch[0]) ** 2 * (ch[1] - ch[0]) for ch in chunks}
-    load = [0.0] * world
-    out: list[list[tuple[int, int]]] = [[] for _ in range(world)]
-    for ch in sorted(chunks, key=lambda ch: (-cost[ch], ch[0])):
-        r = min(range(world), key=lambda q: (load[q], q))
-        out[r].append(ch)
-        load[r] += cost[ch]
-    return [sorted(o) for o in out]
+def gradient_columns(tiles: int, world: int) -> list[list[int]]:
+    """Deterministic assignment of the internal tile columns of K^-1 to ranks
+    for the distributed gradient.  Column J costs ~2 (T - J)^2 tile GEMMs
+    (forward and backward solve below row block J), so columns are dealt in
+    snake order (0..p-1, p-1..0, ...) which balances the sums of squares."""
+    out: list[list[int]] = [[] for _ in range(world)]
+    for j in range(tiles):
+        r, lap = j % world, (j // world) % 2
+        out[world - 1 - r if lap else r].append(j)
+    return out
 
 
 class DeviceTileOps:
@@ -236,18 +228,20 @@ class _DeviceReplica:
         _lib.check(self.ops.lib.gpb_loss_gradients(self.h, out))
         return (float(out[0]), float(out[1]), float(out[2]))
 
-    def gradient_terms(self, j0: int, j1: int) -> np.ndarray:
-        """Trace partials of K^-1 tile columns [j0, j1) (gpb_loss_gradient_terms),
-        split into narrower panels when the (n - j0 b) x (j1 - j0) b panel would
-        not fit in device memory."""
+    def gradient_terms(self, cols: list[int]) -> np.ndarray:
+        """Trace partials of the K^-1 tile columns `cols` (gpb_loss_gradient_terms),
+        in groups whose (n - J0 b) x (len b) panel fits in device memory."""
         lay = _lib.layout(self.n, self.tiles_per_dim)
         free, _ = torch.cuda.mem_get_info(self.ops.device)
-        per_col = 8.0 * (lay["T"] - j0) * lay["b"] * lay["b"]
-        width = max(1, int(0.4 * free // max(per_col, 1.0)))
         acc = np.zeros(3)
-        for a in range(j0, j1, width):
+        rest = sorted(cols)
+        while rest:
+            per_col = 8.0 * (lay["T"] - rest[0]) * lay["b"] * lay["b"]
+            take = max(1, min(len(rest), int(0.4 * free // max(per_col, 1.0))))
+            group, rest = rest[:take], rest[take:]
+            arr = (ctypes.c_int * len(group))(*group)
             out = (ctypes.c_double * 3)()
-            _lib.check(self.ops.lib.gpb_loss_gradient_terms(self.h, a, min(j1, a + width), out))
+            _lib.check(self.ops.lib.gpb_loss_gradient_terms(self.h, arr, len(group), out))
             acc += np.array(out[:3])
         return acc
 
@@ -627,17 +621,16 @@ class DistributedGP:
     # -- training (model.py:341-485) ----------------------------------------------
     def loss_gradients(self) -> tuple[float, float, float]:
         """dNLL/d(l, nu, sigma^2) (model.py:341-435), split over ranks by
-        column panels of K^-1 (``gradient_column_chunks``): each rank sums
-        the trace terms of its panels, the partials are all-gathered and
-        added in rank order, so every rank returns the same values."""
+        tile columns of K^-1 (``gradient_columns``): each rank sums the trace
+        terms of its columns, the partials are all-gathered and added in rank
+        order, so every rank returns the same values."""
         tr = self.params.trainable
         if not (tr[0] or tr[1] or tr[2]):
             return (0.0, 0.0, 0.0)
         rep = self._ensure_replica()
         t0 = self._event()
-        acc = np.zeros(3)
-        for j0, j1 in gradient_column_chunks(self.T, self.world)[self.rank]:
-            acc += rep.gradient_terms(j0, j1)
+        mine = gradient_columns(self.T, self.world)[self.rank]
+        acc = rep.gradient_terms(mine) if mine else np.zeros(3)
         parts = self._allgather(self.ops.from_numpy(acc)).cpu().numpy()
         tot = np.zeros(3)
         for r in range(self.world):  # fixed rank order

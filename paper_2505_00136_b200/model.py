@@ -164,6 +164,12 @@ class GPModel:
                 self._push_params()
             raise
 
+    def close(self) -> None:
+        """Release the model's device buffers now (they are re-created on the next call)."""
+        h, self._handle = self._handle, None
+        if h is not None:
+            _lib.load().gpb_model_destroy(h)
+
     def __del__(self):
         h = getattr(self, "_handle", None)
         if h is not None:

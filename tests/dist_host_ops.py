@@ -172,7 +172,7 @@ class HostReplica:
         blk = prior - va.numpy()[:, : za.shape[0]].T @ vb.numpy()[:, : zb.shape[0]]
         rows[: za.shape[0], col0:col0 + zb.shape[0]] = torch.from_numpy(blk)
 
-    def gradient_terms(self, j0, j1):
+    def gradient_terms(self, cols):
         """Numpy restatement of gpb_loss_gradient_terms over padded positions."""
         b, n_p = self.lay["b"], self.lay["np"]
         lo, real = self._dense()
@@ -186,7 +186,7 @@ class HostReplica:
         full = lambda a: self._embed(a, real, n_p)  # noqa: E731
         ml, mv, kd = full(w * e * d2), full(w * e), full(np.diag(np.diag(kinv)))
         out = np.zeros(3)
-        for jj in range(j0, j1):
+        for jj in cols:
             for i in range(jj, self.lay["T"]):
                 blk = (slice(i * b, (i + 1) * b), slice(jj * b, (jj + 1) * b))
                 wt = 1.0 if i == jj else 2.0

@@ -133,17 +133,17 @@ def test_process_grid_and_ownership():
     assert cyc.panel_rows(2, 1) == [3, 5]
 
 
-def test_gradient_column_chunks_partition():
-    from paper_2505_00136_b200.distributed import gradient_column_chunks
+def test_gradient_columns_partition():
+    from paper_2505_00136_b200.distributed import gradient_columns
 
     for T, world in [(1, 1), (6, 2), (64, 8), (256, 8), (7, 3), (3, 4)]:
-        parts = gradient_column_chunks(T, world)
-        assert len(parts) == world and parts == gradient_column_chunks(T, world)
-        cols = sorted(c for p in parts for j0, j1 in p for c in range(j0, j1))
-        assert cols == list(range(T))  # every tile column exactly once
-        if T >= 4 * world:  # LPT keeps the per-rank cost within 2x of the mean
-            cost = [sum((T - j0) ** 2 * (j1 - j0) for j0, j1 in p) for p in parts]
-            assert max(cost) <= 2.0 * sum(cost) / world
+        parts = gradient_columns(T, world)
+        assert len(parts) == world and parts == gradient_columns(T, world)
+        assert sorted(c for p in parts for c in p) == list(range(T))  # each column once
+        assert all(p == sorted(p) for p in parts)
+        if T >= 4 * world:  # snake order balances sum (T - J)^2 within a few percent
+            cost = [sum((T - j) ** 2 for j in p) for p in parts]
+            assert max(cost) <= 1.1 * sum(cost) / world
 
 
 @pytest.mark.gpu

@@ -291,11 +291,11 @@ class TestGradientsAndAdam:
     @pytest.mark.parametrize("n,t,world", [(600, 6, 2), (1024, 4, 3), (2048, 4, 1)])
     def test_column_panel_terms(self, runtime, n, t, world):
         """gpb_loss_gradient_terms (the multi-GPU split of the gradient):
-        summed over every rank's panels it reproduces loss_gradients and the oracle."""
+        summed over every rank's tile columns it reproduces loss_gradients and the oracle."""
         import ctypes
 
         from paper_2505_00136_b200 import _lib
-        from paper_2505_00136_b200.distributed import gradient_column_chunks
+        from paper_2505_00136_b200.distributed import gradient_columns
 
         rng = np.random.default_rng(n + t)
         z, y = rng.normal(size=(n, 3)), rng.normal(size=n)
@@ -303,10 +303,11 @@ class TestGradientsAndAdam:
         whole = np.array(model.loss_gradients())
         lay = _lib.layout(n, t)
         lib, tot = _lib.load(), np.zeros(3)
-        for chunks in gradient_column_chunks(lay["T"], world):
-            for j0, j1 in chunks:
+        for cols in gradient_columns(lay["T"], world):
+            if cols:
                 out = (ctypes.c_double * 3)()
-                _lib.check(lib.gpb_loss_gradient_terms(model._handle, j0, j1, out))
+                arr = (ctypes.c_int * len(cols))(*cols)
+                _lib.check(lib.gpb_loss_gradient_terms(model._handle, arr, len(cols), out))
                 tot += np.array(out[:3])
         p = model.params
         alpha = np.linalg.solve(dense_k(z, 1.2, 0.9, 0.15), y)
@@ -315,8 +316,8 @@ class TestGradientsAndAdam:
         assert rel(split, whole) <= 1e-11
         assert rel(split, OracleGP(z, y, t, 1.2, 0.9, 0.15).loss_gradients()) <= TOL
         with pytest.raises(gpb.errors.InvalidConfig):
-            lib_out = (ctypes.c_double * 3)()
-            _lib.check(lib.gpb_loss_gradient_terms(model._handle, 0, lay["T"] + 1, lib_out))
+            bad = (ctypes.c_int * 2)(1, 0)  # not increasing
+            _lib.check(lib.gpb_loss_gradient_terms(model._handle, bad, 2, (ctypes.c_double * 3)()))
 
     def test_adam_semantics(self, runtime, rng):
         train = ds(rng.normal(size=(16, 3)), rng.normal(size=16))
