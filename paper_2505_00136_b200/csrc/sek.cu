@@ -20,6 +20,9 @@ namespace gpb {
 namespace {
 
 constexpr int SB = kSekBlock;  // entries per CTA side
+// staging row pitch: the transposing stores sa[dd][r] of 32 consecutive
+// features would all hit one bank with a pitch of 64 doubles
+constexpr int SBP = SB + 1;
 constexpr int DC = 32;  // feature chunk
 constexpr int R = SB / 16;  // entries per thread per dimension
 constexpr int ST = 256;  // threads
@@ -30,7 +33,7 @@ struct Frag {
 
 // d2[ii][jj] for rows ra0 + ty + 16 ii of za (ld d) and rows rb0 + tx + 16 jj of zb.
 GPB_DEVINL void sq_dists_blk(Frag& d2, const double* za, int64_t ra0, const double* zb, int64_t rb0,
-                            int d, double (*sa)[SB], double (*sb)[SB], int tx, int ty, int tid) {
+                            int d, double (*sa)[SBP], double (*sb)[SBP], int tx, int ty, int tid) {
 #pragma unroll
   for (int i = 0; i < R; ++i)
 #pragma unroll
@@ -84,7 +87,7 @@ GPB_DEVINL double block_sum(double v, double* red, int tid) {
 // one 64x64 block (rb, cb) of tile (ti, tj), written to `tile`
 GPB_DEVINL void assemble_block(double* tile, int ti, int tj, int rb, int cb, const double* zp,
                                int d, int bi, PadMap pm, SekParams sp, int add_noise,
-                               double (*sa)[SB], double (*sb)[SB]) {
+                               double (*sa)[SBP], double (*sb)[SBP]) {
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int64_t P0 = static_cast<int64_t>(ti) * bi + rb * SB;
   const int64_t Q0 = static_cast<int64_t>(tj) * bi + cb * SB;
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__(ST) assemble_lower_kernel(double* tiles, const
                                                             int64_t t0, const double* zp, int d,
                                                             int bi, PadMap pm, SekParams sp,
                                                             int add_noise) {
-  __shared__ double sa[DC][SB], sb[DC][SB];
+  __shared__ double sa[DC][SBP], sb[DC][SBP];
   const int nbs = bi / SB;
   const int64_t t = t0 + blockIdx.x / (nbs * nbs);
   const int blk = blockIdx.x % (nbs * nbs);
@@ -126,7 +129,7 @@ __global__ void __launch_bounds__(ST) assemble_lower_kernel(double* tiles, const
 __global__ void __launch_bounds__(ST) assemble_desc_kernel(const TileDesc* desc, const double* zp,
                                                            int d, int bi, PadMap pm, SekParams sp,
                                                            int add_noise) {
-  __shared__ double sa[DC][SB], sb[DC][SB];
+  __shared__ double sa[DC][SBP], sb[DC][SBP];
   const int nbs = bi / SB;
   const TileDesc td = desc[blockIdx.x / (nbs * nbs)];
   const int blk = blockIdx.x % (nbs * nbs);
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(ST) cross_kernel(double* B, int64_t ldb, doubl
                                                    const double* alpha, const double* zp,
                                                    const double* zt, int64_t mc, int d,
                                                    PadMap pm, SekParams sp) {
-  __shared__ double sa[DC][SB], sb[DC][SB];
+  __shared__ double sa[DC][SBP], sb[DC][SBP];
   __shared__ double red[16][SB];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int64_t P0 = static_cast<int64_t>(blockIdx.x) * SB;  // training rows
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(ST) cross_kernel(double* B, int64_t ldb, doubl
 __global__ void __launch_bounds__(ST) prior_kernel(double* S, int64_t lds, const double* za,
                                                    int64_t ma, const double* zb, int64_t mb, int d,
                                                    SekParams sp) {
-  __shared__ double sa[DC][SB], sb[DC][SB];
+  __shared__ double sa[DC][SBP], sb[DC][SBP];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int64_t R0 = static_cast<int64_t>(blockIdx.x) * SB;
   const int64_t C0 = static_cast<int64_t>(blockIdx.y) * SB;
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(ST) trace_kernel(const double* kinv, const int
                                                    const double* zp, const double* alpha, int d,
                                                    int bi, PadMap pm, SekParams sp, TraceTiles tt,
                                                    double* part_l, double* part_v, double* part_t) {
-  __shared__ double sa[DC][SB], sb[DC][SB];
+  __shared__ double sa[DC][SBP], sb[DC][SBP];
   __shared__ double red[ST];
   const int nbs = bi / SB;
   const int64_t t = blockIdx.x / (nbs * nbs);

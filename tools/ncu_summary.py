@@ -12,7 +12,10 @@ hdr, units = rows[0], rows[1]
 want = ["Kernel Name", "Grid Size", "gpu__time_duration.sum", "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
         "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct", "sm__cycles_elapsed.avg.per_second",
-        "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active"]
+        "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"]
 idx = {h: i for i, h in enumerate(hdr)}
 for r in rows[2:]:
     out = []
