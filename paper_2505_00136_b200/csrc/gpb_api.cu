@@ -520,8 +520,10 @@ int ensure_factor(gpb_model* m) {
     long long h[8];
     cudaStreamSynchronize(m->crit);
     cudaMemcpy(h, m->potrf_prof, sizeof(h), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "potrf cycles: update %lld diag %lld trsm %lld zero %lld trtri %lld\n", h[0], h[1],
-            h[2], h[3], h[4]);
+    fprintf(stderr,
+            "potrf cycles: update %lld diag-wait %lld trsm %lld trtri %lld zero %lld | warp0 chain %lld "
+            "inverse %lld stores %lld\n",
+            h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
     cudaMemset(m->potrf_prof, 0, sizeof(h));
   }
   // join: the main stream waits for the critical stream's last work

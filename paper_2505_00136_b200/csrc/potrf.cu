@@ -1,4 +1,5 @@
-// Diagonal-tile factorisation: POTRF + TRTRI of one bi x bi tile in one CTA.
+// Diagonal-tile factorisation: POTRF + TRTRI of one bi x bi tile by one
+// thread-block cluster (GPB_POTRF_CLUSTER CTAs, default 8, on as many SMs).
 //
 // Replaces taskgp tile_potrf (tiles.py:132-137 -> np.linalg.cholesky,
 // tiles.py:29-33) and provides the inverted diagonal tile that turns every
@@ -14,8 +15,14 @@
 //                   Dinv = L^-1 (TRTRI interleaved with the factorisation)
 //   C (all warps)   solve the rows below the diagonal block (x Li^T)
 // so the DMMA work of the update and of TRTRI runs while the pivot chain
-// advances.  Epilogue: Sigma log L_jj over real (non-padding) pivots and a
+// advances.  The warp jobs of every phase are dealt over all warps of the
+// cluster and the phases are separated by cluster barriers (release/acquire
+// at cluster scope orders the global-memory tile between the SMs), so the
+// lookahead DMMA work is spread over CL SMs while CTA 0's warp 0 runs the
+// pivot chain.  Epilogue: Sigma log L_jj over real (non-padding) pivots and a
 // LAPACK-style info word holding the first failing original pivot index.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -136,6 +143,15 @@ GPB_DEVINL void trtri_job(double* T, double* D, int bi, int I, int J, double* Sw
   __syncwarp();
 }
 
+// all threads of the cluster (a plain launch is a cluster of one CTA)
+GPB_DEVINL void cluster_barrier(bool clustered) {
+  if (clustered)
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                     : "memory");
+  else
+    __syncthreads();
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
@@ -143,21 +159,25 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
   double* Ld = sm;                 // [32][33] factor block
   double* Li = Ld + NB * SLD;      // [32][33] its inverse
   double* S = Li + NB * SLD;       // [8][32][33] per-warp scratch
-  __shared__ int s_fail;
-
+  // every CTA reads info before the first cluster barrier; only CTA 0
+  // writes it, and only after that barrier
   if (*a.info >= 0) return;  // an earlier tile already failed
   const int bi = a.bi;
   double* T = a.tile;
   double* D = a.dinv;
   const int P = bi / NB;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int cta = blockIdx.x, ncta = gridDim.x;
+  const bool clustered = ncta > 1;
+  const bool lead = cta == 0;
+  const int warp = cta * NW + (tid >> 5);  // warp index within the cluster
+  const int GW = ncta * NW;                // warps in the cluster
   const int g = lane >> 2, t = lane & 3;
   const bool factor = !a.trtri_only;
-  double* Sw = S + warp * NB * SLD;
-  if (tid == 0) s_fail = -1;
+  double* Sw = S + (tid >> 5) * NB * SLD;
   double logsum = 0.0;  // meaningful in lane 0 of warp 0
-  __syncthreads();
-  long long t_last = clock64(), t_acc[5] = {0, 0, 0, 0, 0};
+  cluster_barrier(clustered);
+  long long t_last = clock64(), t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #define PROF_MARK(i)                                   \
   if (a.prof && tid == 0) {                            \
     const long long now_ = clock64();                  \
@@ -169,7 +189,7 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
     const int c0 = p * NB;
     // A: last contribution (panel p-1) to panel p, rows >= c0
     if (p > 0 && factor) {
-      for (int rb = p + warp; rb < P; rb += NW) {
+      for (int rb = p + warp; rb < P; rb += GW) {
         double acc[4][4][2];
         zero_acc(acc);
         warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi + c0 - NB, bi,
@@ -177,14 +197,18 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
         store_acc(T + static_cast<int64_t>(rb) * NB * bi + c0, bi, acc, g, t, false, 1.0);
       }
     }
-    __syncthreads();
+    cluster_barrier(clustered);
     PROF_MARK(0)
     if (warp > 0) {
       // B, warps 1..7: lookahead update of panel p+1 (panels 0..p-1) and
       // block row p-1 of the inverse, dealt round-robin
       const int pre = (factor && p > 0 && p + 1 < P) ? P - p - 1 : 0;
       const int inv = (p >= 2) ? p - 1 : 0;  // jobs J = 0..p-2 of row I = p-1
-      for (int q = warp - 1; q < pre + inv; q += NW - 1) {
+      // clustered: CTA 0 keeps only the pivot chain so its SMSPs are not
+      // shared with DMMA warps; the other CTAs' warps take the jobs
+      const int w0 = clustered ? warp - NW : warp - 1;
+      const int nwk = clustered ? GW - NW : NW - 1;
+      for (int q = (w0 >= 0 ? w0 : pre + inv); q < pre + inv; q += nwk) {
         if (q < pre) {
           const int rb = p + 1 + q, c1 = c0 + NB;
           double acc[4][4][2];
@@ -196,7 +220,7 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
           trtri_job(T, D, bi, p - 1, q - pre, Sw, g, t);
         }
       }
-    } else {
+    } else if (lead) {
       // B, warp 0: lane i keeps row i of the diagonal block in registers,
       // shifted so that register 0 always holds the current pivot column
       // (short code: the pivot loop is not unrolled; LAPACK dpotf2 order)
@@ -229,6 +253,7 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
         const bool real = (pos % a.bp_user < a.b_user) && (fail < 0 || lane < fail);
         const double lsum = warp_sum(real ? log(my_l) : 0.0);
         if (lane == 0) logsum += lsum;
+        PROF_MARK(5)
       } else {  // trtri-only: the tile already holds L
 #pragma unroll
         for (int c = 0; c < NB; ++c) Ld[lane * SLD + c] = (c <= lane) ? r[c] : 0.0;
@@ -243,7 +268,7 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
       if (fail >= 0) {
         if (lane == 0) {
           const int pos = a.tile_off + c0 + fail;
-          s_fail = (pos / a.bp_user) * a.b_user + pos % a.bp_user;
+          *reinterpret_cast<volatile int*>(a.info) = (pos / a.bp_user) * a.b_user + pos % a.bp_user;
         }
       } else {
         // lane j forms column j of the inverse by forward substitution (rows
@@ -262,38 +287,37 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
           if (i != lane) Li[i * SLD + lane] = (i < lane) ? 0.0 : (s0 + s1) * di;
           __syncwarp();
         }
+        PROF_MARK(6)
         for (int c = 0; c < NB; ++c) {
           const int64_t o = static_cast<int64_t>(c0 + lane) * bi + c0 + c;
           if (factor) T[o] = Ld[lane * SLD + c];
           D[o] = Li[lane * SLD + c];
         }
+        PROF_MARK(7)
       }
     }
-    __syncthreads();
+    cluster_barrier(clustered);
     PROF_MARK(1)
-    if (s_fail >= 0) break;
+    if (*reinterpret_cast<volatile int*>(a.info) >= 0) return;  // set by CTA 0 above
     // C: below-diagonal panel rows, L[r][c0:c0+32] = T[r][c0:c0+32] * Li^T
-    for (int rb = p + 1 + warp; rb < (factor ? P : 0); rb += NW) {
+    // (Li read back from the diagonal block of D, written by CTA 0)
+    for (int rb = p + 1 + warp; rb < (factor ? P : 0); rb += GW) {
       double acc[4][4][2];
       zero_acc(acc);
       double* blk = T + static_cast<int64_t>(rb) * NB * bi + c0;
-      warp_nt(acc, blk, bi, Li, SLD, NB, g, t);
+      warp_nt(acc, blk, bi, D + static_cast<int64_t>(c0) * bi + c0, bi, NB, g, t);
       __syncwarp();
       store_acc(blk, bi, acc, g, t, true, 1.0);
     }
-    __syncthreads();
+    cluster_barrier(clustered);
     PROF_MARK(2)
-  }
-  if (s_fail >= 0) {
-    if (tid == 0) *a.info = s_fail;
-    return;
   }
   // last block row of the inverse (rows 1..P-2 were interleaved above)
   if (P >= 2)
-    for (int J = warp; J < P - 1; J += NW) trtri_job(T, D, bi, P - 1, J, Sw, g, t);
+    for (int J = warp; J < P - 1; J += GW) trtri_job(T, D, bi, P - 1, J, Sw, g, t);
   PROF_MARK(3)
   // zero strictly-upper 32-blocks of L and Dinv (lower-triangular results)
-  for (int r = warp; r < bi; r += NW) {
+  for (int r = warp; r < bi; r += GW) {
     const int c_begin = (r / NB + 1) * NB;
     for (int c = c_begin + 2 * lane; c < bi; c += 64) {
       const int64_t idx = static_cast<int64_t>(r) * bi + c;
@@ -302,17 +326,45 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
     }
   }
   PROF_MARK(4)
-  if (a.prof && tid == 0)
-    for (int i = 0; i < 5; ++i) a.prof[i] += t_acc[i];
-  if (tid == 0 && a.logdiag) a.logdiag[a.tile_index] = logsum;
+  if (a.prof && tid == 0 && lead)
+    for (int i = 0; i < 8; ++i) a.prof[i] += t_acc[i];
+  if (tid == 0 && lead && a.logdiag) a.logdiag[a.tile_index] = logsum;
 #undef PROF_MARK
 }
 
 size_t potrf_smem_bytes() { return sizeof(double) * (2 * NB * SLD + NW * NB * SLD); }
 
+static int g_cluster = 0;
+
+// CTAs per diagonal tile (GPB_POTRF_CLUSTER: 1 = single CTA, up to 8)
+static int potrf_cluster() {
+  if (g_cluster == 0) {
+    const char* e = getenv("GPB_POTRF_CLUSTER");
+    int c = e ? atoi(e) : 8;
+    g_cluster = (c == 1 || c == 2 || c == 4 || c == 8) ? c : 8;
+  }
+  return g_cluster;
+}
+
 cudaError_t launch_potrf(const PotrfArgs& a, cudaStream_t s) {
-  potrf_tile_kernel<<<1, PT, potrf_smem_bytes(), s>>>(a);
-  return cudaGetLastError();
+  const int cl = potrf_cluster();
+  if (cl == 1) {
+    potrf_tile_kernel<<<1, PT, potrf_smem_bytes(), s>>>(a);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cl);
+  cfg.blockDim = dim3(PT);
+  cfg.dynamicSmemBytes = potrf_smem_bytes();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, potrf_tile_kernel, a);
 }
 
 cudaError_t potrf_init_attributes() {
