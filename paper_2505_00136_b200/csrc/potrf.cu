@@ -6,12 +6,12 @@
 // triangular solve of the hot path (panel TRSM tiles.py:140-146, vector
 // solves tiles.py:170-180, panel solves tiles.py:182-185) into DMMA products.
 //
-// Blocked left-looking Cholesky with 32-column panels.  Per panel p:
+// Blocked Cholesky with 32-column panels.  Per panel p:
 //   A (all warps)   last contribution (panel p-1) to panel p, DMMA warp tiles
 //   B (warp 0)      factor + invert the 32x32 diagonal block -- the serial
 //                   pivot chain, kept in registers / shuffles
-//     (warps 1..7)  concurrently: contributions of panels 0..p-1 to panel p+1
-//                   (in-tile lookahead) and block row p-1 of the inverse
+//     (other warps) concurrently: panel p-1's contribution to every trailing
+//                   32-block right of panel p (right-looking) and block row p-1 of the inverse
 //                   Dinv = L^-1 (TRTRI interleaved with the factorisation)
 //   C (all warps)   solve the rows below the diagonal block (x Li^T)
 // so the DMMA work of the update and of TRTRI runs while the pivot chain
@@ -158,7 +158,10 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
   extern __shared__ double sm[];
   double* Ld = sm;                 // [32][33] factor block
   double* Li = Ld + NB * SLD;      // [32][33] its inverse
-  double* S = Li + NB * SLD;       // [8][32][33] per-warp scratch
+  double* rdg = Li + NB * SLD;     // [32] 1 / l_jj of the current panel
+  double* S = rdg + NB;            // [8][32][33] per-warp scratch
+  __shared__ volatile int prog_s;  // pivots of the chain published so far
+  volatile int* prog = &prog_s;
   // every CTA reads info before the first cluster barrier; only CTA 0
   // writes it, and only after that barrier
   if (*a.info >= 0) return;  // an earlier tile already failed
@@ -170,12 +173,14 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
   const int cta = blockIdx.x, ncta = gridDim.x;
   const bool clustered = ncta > 1;
   const bool lead = cta == 0;
-  const int warp = cta * NW + (tid >> 5);  // warp index within the cluster
+  const int lw = tid >> 5;                 // warp index within the CTA
+  const int warp = cta * NW + lw;          // warp index within the cluster
   const int GW = ncta * NW;                // warps in the cluster
   const int g = lane >> 2, t = lane & 3;
   const bool factor = !a.trtri_only;
   double* Sw = S + (tid >> 5) * NB * SLD;
   double logsum = 0.0;  // meaningful in lane 0 of warp 0
+  if (tid == 0) *prog = 0;
   cluster_barrier(clustered);
   long long t_last = clock64(), t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #define PROF_MARK(i)                                   \
@@ -199,102 +204,130 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
     }
     cluster_barrier(clustered);
     PROF_MARK(0)
-    if (warp > 0) {
-      // B, warps 1..7: lookahead update of panel p+1 (panels 0..p-1) and
-      // block row p-1 of the inverse, dealt round-robin
-      const int pre = (factor && p > 0 && p + 1 < P) ? P - p - 1 : 0;
+    if (!(lead && lw < 2)) {
+      // B, job warps (CTAs 1.. when clustered, else warps 2..7), dealt
+      // round-robin: panel p-1's rank-32 contribution to every trailing
+      // 32-block (rb, cb), p+1 <= cb <= rb (right-looking; panel p gets it
+      // in phase A), and block row p-1 of the inverse
+      const int m = P - p - 1;
+      const int pre = (factor && p > 0) ? m * (m + 1) / 2 : 0;
       const int inv = (p >= 2) ? p - 1 : 0;  // jobs J = 0..p-2 of row I = p-1
       // clustered: CTA 0 keeps only the pivot chain so its SMSPs are not
       // shared with DMMA warps; the other CTAs' warps take the jobs
-      const int w0 = clustered ? warp - NW : warp - 1;
-      const int nwk = clustered ? GW - NW : NW - 1;
+      const int w0 = clustered ? warp - NW : warp - 2;
+      const int nwk = clustered ? GW - NW : NW - 2;
       for (int q = (w0 >= 0 ? w0 : pre + inv); q < pre + inv; q += nwk) {
         if (q < pre) {
-          const int rb = p + 1 + q, c1 = c0 + NB;
+          int rr = static_cast<int>((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
+          while (rr * (rr + 1) / 2 > q) --rr;
+          while ((rr + 1) * (rr + 2) / 2 <= q) ++rr;
+          const int rb = p + 1 + rr, cb = p + 1 + (q - rr * (rr + 1) / 2);
           double acc[4][4][2];
           zero_acc(acc);
-          warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi, bi,
-                  T + static_cast<int64_t>(c1) * bi, bi, c0, g, t);
-          store_acc(T + static_cast<int64_t>(rb) * NB * bi + c1, bi, acc, g, t, false, 1.0);
+          warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi + c0 - NB, bi,
+                  T + static_cast<int64_t>(cb) * NB * bi + c0 - NB, bi, NB, g, t);
+          store_acc(T + static_cast<int64_t>(rb) * NB * bi + cb * NB, bi, acc, g, t, false, 1.0);
         } else {
           trtri_job(T, D, bi, p - 1, q - pre, Sw, g, t);
         }
       }
-    } else if (lead) {
-      // B, warp 0: lane i keeps row i of the diagonal block in registers,
+    } else if (lead && lw == 0) {
+      // B, chain: lane i keeps row i of the diagonal block in registers,
       // shifted so that register 0 always holds the current pivot column
-      // (short code: the pivot loop is not unrolled; LAPACK dpotf2 order)
+      // (short code: the pivot loop is not unrolled; LAPACK dpotf2 order).
+      // After pivot j, row j of L is complete: publish it to the inverse warp.
+      const int base = p * NB;
       double r[NB];
 #pragma unroll
       for (int c = 0; c < NB; ++c) r[c] = T[static_cast<int64_t>(c0 + lane) * bi + c0 + c];
       int fail = -1;
-      double my_l = 1.0, my_rinv = 0.0;
+      double my_l = 1.0;
       if (factor) {
-#pragma unroll 1
-        for (int j = 0; j < NB; ++j) {
-          const double piv = __shfl_sync(0xffffffffu, r[0], j);
+        // Two pivots per trip, then a shift by two.  Entries of lanes above
+        // the current row are updated too (they lie in the upper triangle,
+        // are never read again, and lcol = 0 leaves them unchanged for lanes
+        // < j), which drops the per-entry predicate.
+        auto pivot = [&](int j, int o) {  // register o holds column j
+          const double piv = __shfl_sync(0xffffffffu, r[o], j);
           if (fail < 0 && !(piv > 0.0)) fail = j;
           const double rinv = rsqrt(piv);
-          const double lcol = (lane == j) ? piv * rinv : (lane > j ? r[0] * rinv : 0.0);
+          const double lcol = (lane == j) ? piv * rinv : (lane > j ? r[o] * rinv : 0.0);
           if (lane == j) {
             my_l = lcol;
-            my_rinv = rinv;
+            rdg[j] = rinv;
           }
           Ld[lane * SLD + j] = lcol;
-#pragma unroll
-          for (int c = 1; c < NB; ++c) {
-            const double lcj = __shfl_sync(0xffffffffu, lcol, (j + c) & (NB - 1));
-            if (lane >= j + c) r[c] = fma(-lcol, lcj, r[c]);
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence_block();
+            *prog = base + j + 1;
           }
 #pragma unroll
-          for (int c = 0; c < NB - 1; ++c) r[c] = r[c + 1];
+          for (int c = o + 1; c < NB; ++c) {
+            // srcLane is taken modulo 32; columns past the panel hold garbage
+            const double lcj = __shfl_sync(0xffffffffu, lcol, j + c - o);
+            r[c] = fma(-lcol, lcj, r[c]);
+          }
+        };
+#pragma unroll 1
+        for (int j = 0; j < NB; j += 2) {
+          pivot(j, 0);
+          pivot(j + 1, 1);
+#pragma unroll
+          for (int c = 0; c < NB - 2; ++c) r[c] = r[c + 2];
         }
         const int pos = a.tile_off + c0 + lane;  // padded global position
         const bool real = (pos % a.bp_user < a.b_user) && (fail < 0 || lane < fail);
         const double lsum = warp_sum(real ? log(my_l) : 0.0);
         if (lane == 0) logsum += lsum;
         PROF_MARK(5)
+        __syncwarp();
+        for (int c = lane + 1; c < NB; ++c) Ld[lane * SLD + c] = 0.0;  // strictly upper
+        __syncwarp();
+        if (fail >= 0) {
+          if (lane == 0) {
+            const int fp = a.tile_off + c0 + fail;
+            *reinterpret_cast<volatile int*>(a.info) = (fp / a.bp_user) * a.b_user + fp % a.bp_user;
+          }
+        } else {
+#pragma unroll 4
+          for (int c = 0; c < NB; ++c) T[static_cast<int64_t>(c0 + lane) * bi + c0 + c] = Ld[lane * SLD + c];
+        }
       } else {  // trtri-only: the tile already holds L
 #pragma unroll
         for (int c = 0; c < NB; ++c) Ld[lane * SLD + c] = (c <= lane) ? r[c] : 0.0;
-        my_rinv = 1.0 / Ld[lane * SLD + lane];
-      }
-      if (factor) {
         __syncwarp();
-        for (int c = lane + 1; c < NB; ++c) Ld[lane * SLD + c] = 0.0;  // strictly upper
-      }
-      Li[lane * SLD + lane] = my_rinv;
-      __syncwarp();
-      if (fail >= 0) {
+        rdg[lane] = 1.0 / Ld[lane * SLD + lane];
+        __syncwarp();
         if (lane == 0) {
-          const int pos = a.tile_off + c0 + fail;
-          *reinterpret_cast<volatile int*>(a.info) = (pos / a.bp_user) * a.b_user + pos % a.bp_user;
+          __threadfence_block();
+          *prog = base + NB;
         }
-      } else {
-        // lane j forms column j of the inverse by forward substitution (rows
-        // of L broadcast from shared memory, the column in shared memory)
-#pragma unroll 1
-        for (int i = 0; i < NB; ++i) {
-          double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0;
-          int k = 0;
-          for (; k + 1 < i; k += 2) {
-            s0 = fma(-Ld[i * SLD + k], Li[k * SLD + lane], s0);
-            s1 = fma(-Ld[i * SLD + k + 1], Li[(k + 1) * SLD + lane], s1);
-          }
-          if (k < i) s0 = fma(-Ld[i * SLD + k], Li[k * SLD + lane], s0);
-          const double di = Li[i * SLD + i];
-          __syncwarp();
-          if (i != lane) Li[i * SLD + lane] = (i < lane) ? 0.0 : (s0 + s1) * di;
-          __syncwarp();
-        }
-        PROF_MARK(6)
-        for (int c = 0; c < NB; ++c) {
-          const int64_t o = static_cast<int64_t>(c0 + lane) * bi + c0 + c;
-          if (factor) T[o] = Ld[lane * SLD + c];
-          D[o] = Li[lane * SLD + c];
-        }
-        PROF_MARK(7)
       }
+      PROF_MARK(6)
+    } else if (lead && lw == 1) {
+      // B, inverse of the diagonal block, row i as soon as the chain has
+      // finished pivot i:  Li[i][k] = -(1 / l_ii) sum_{m<i} l_im Li[m][k]
+      // (Li[m][k] = 0 for k > m, so every lane runs the same loop)
+      const int base = p * NB;
+#pragma unroll 1
+      for (int i = 0; i < NB; ++i) {
+        while (*prog < base + i + 1) {
+        }
+        __threadfence_block();
+        double s0 = 0.0, s1 = 0.0;
+        int m = 0;
+        for (; m + 1 < i; m += 2) {
+          s0 = fma(Ld[i * SLD + m], Li[m * SLD + lane], s0);
+          s1 = fma(Ld[i * SLD + m + 1], Li[(m + 1) * SLD + lane], s1);
+        }
+        if (m < i) s0 = fma(Ld[i * SLD + m], Li[m * SLD + lane], s0);
+        const double di = rdg[i];
+        Li[i * SLD + lane] = lane < i ? -(s0 + s1) * di : (lane == i ? di : 0.0);
+        __syncwarp();
+      }
+#pragma unroll 4
+      for (int c = 0; c < NB; ++c) D[static_cast<int64_t>(c0 + lane) * bi + c0 + c] = Li[lane * SLD + c];
     }
     cluster_barrier(clustered);
     PROF_MARK(1)
@@ -332,7 +365,7 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
 #undef PROF_MARK
 }
 
-size_t potrf_smem_bytes() { return sizeof(double) * (2 * NB * SLD + NW * NB * SLD); }
+size_t potrf_smem_bytes() { return sizeof(double) * (2 * NB * SLD + NB + NW * NB * SLD); }
 
 static int g_cluster = 0;
 
