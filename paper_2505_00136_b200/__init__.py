@@ -12,9 +12,18 @@ computing on hand-written CUDA kernels through the C ABI in
     gpb.stop_runtime()
 """
 
-from . import errors
+from . import bench, errors
 from .covariance import KernelParams
-from .data import Dataset, lag_features, make_msd_dataset, msd_series
+from .data import (
+    Dataset,
+    LagSpec,
+    lag_embed,
+    lag_features,
+    load_csv,
+    make_msd_dataset,
+    msd_series,
+    save_csv,
+)
 from .model import GP, AdamConfig, GPModel, PredictionResult
 from .runtime import (
     Runtime,
@@ -30,6 +39,11 @@ __version__ = "0.1.0"
 
 __all__ = [
     "AdamConfig",
+    "LagSpec",
+    "bench",
+    "lag_embed",
+    "load_csv",
+    "save_csv",
     "B200TileKernels",
     "Dataset",
     "GP",

@@ -16,6 +16,11 @@ Conventions are pinned in SURVEY.md Appendix A:
 3. ``y_t = position_t + noise_t``.
 4. Feature row t = (u_t, u_{t-1}, ..., u_{t-n_reg+1}), u_{<0} = 0.
 5. Train = rows [0, n_train), test = rows [n_train, N) (a continuation).
+
+The reference's own lag embedding (``LagSpec``/``lag_embed``, data.py:131-161:
+rows t >= D only, the D preceding samples most recent first) and its CSV
+round trip (``save_csv``/``load_csv``, data.py:164-201) are provided with the
+same semantics so reference-produced files and series load unchanged.
 """
 
 from __future__ import annotations
@@ -24,7 +29,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .errors import DimensionMismatch, InvalidConfig
+from .errors import DimensionMismatch, InvalidConfig, ParseError
 
 
 @dataclass(frozen=True)
@@ -94,3 +99,67 @@ def make_msd_dataset(n_train: int, n_test: int, n_reg: int, seed: int = 0):
     train = Dataset(z=z[:n_train], y=y[:n_train])
     test = Dataset(z=z[n_train:], y=y[n_train:]) if n_test else None
     return train, test
+
+
+@dataclass(frozen=True)
+class LagSpec:
+    """Number of lagged samples used as features (data.py:131-141)."""
+
+    num_regressors: int
+
+    def __post_init__(self) -> None:
+        if self.num_regressors < 1:
+            raise InvalidConfig(f"num_regressors must be >= 1, got {self.num_regressors}")
+
+
+def lag_embed(series, spec: LagSpec) -> Dataset:
+    """Regression dataset of lagged windows of a series (data.py:144-161):
+    row t holds the D samples preceding sample t + D, most recent first, and
+    y[t] is that sample; a series of length L gives L - D rows."""
+    series = np.asarray(series, dtype=np.float64)
+    d = spec.num_regressors
+    if series.ndim != 1 or series.shape[0] <= d:
+        raise DimensionMismatch(f"need a 1-D series longer than {d} samples, got shape {series.shape}")
+    n = series.shape[0] - d
+    z = np.empty((n, d))
+    for j in range(d):
+        z[:, j] = series[d - 1 - j: d - 1 - j + n]
+    return Dataset(z=z, y=series[d:].copy())
+
+
+def save_csv(data: Dataset, path: str, header: bool = False) -> None:
+    """One row per sample, feature columns then y, floats via repr (loss-free)."""
+    with open(path, "w", encoding="utf-8") as fh:
+        if header:
+            fh.write(",".join([f"z{j}" for j in range(data.d)] + ["y"]) + "\n")
+        for row, target in zip(data.z, data.y):
+            fh.write(",".join(repr(float(v)) for v in row) + f",{float(target)!r}\n")
+
+
+def load_csv(path: str, header: bool = False) -> Dataset:
+    """Read a file written by save_csv; the last column is y.  ParseError
+    (with the line number) on ragged rows, bad numbers or an empty file."""
+    rows: list[list[float]] = []
+    width = None
+    with open(path, "r", encoding="utf-8") as fh:
+        for lineno, line in enumerate(fh, start=1):
+            if lineno == 1 and header:
+                continue
+            line = line.strip()
+            if not line:
+                continue
+            cols = line.split(",")
+            if width is None:
+                width = len(cols)
+                if width < 2:
+                    raise ParseError("need at least one feature column and y", lineno)
+            elif len(cols) != width:
+                raise ParseError(f"expected {width} columns, got {len(cols)}", lineno)
+            try:
+                rows.append([float(c) for c in cols])
+            except ValueError as exc:
+                raise ParseError(str(exc), lineno) from exc
+    if not rows:
+        raise ParseError("no data rows", 1)
+    arr = np.array(rows)
+    return Dataset(z=arr[:, :-1], y=arr[:, -1])
