@@ -79,3 +79,21 @@ def test_config3_factor_and_alpha_solve(runtime):
     nll_b, _ = _run(train, None, 128, 256)
     assert np.isfinite(nll_a)
     assert abs(nll_a - nll_b) <= 1e-10 * abs(nll_a)
+
+
+def test_config4_on_one_gpu(runtime):
+    """BASELINE config 4 (n = 131072, m = 8192, D = 16, T = 256: 69 GB of lower
+    tiles) on a single B200: loss, predictive mean/variance blocking-invariant
+    (internal tiles 512 vs 256), and the full posterior covariance consistent
+    with the variances (exactly symmetric, diagonal = variance)."""
+    train, test = gpb.make_msd_dataset(131072, 8192, 16, seed=0)
+    nll_a, pv_a = _run(train, test, 256, 512)
+    nll_b, pv_b = _run(train, test, 256, 256)
+    assert np.isfinite(nll_a) and abs(nll_a - nll_b) <= 1e-10 * abs(nll_a)
+    assert rel(pv_a.mean, pv_b.mean) <= 1e-9 and rel(pv_a.variance, pv_b.variance) <= 1e-9
+    assert np.all(pv_a.variance >= 0.0) and np.all(pv_a.variance <= 1.0 + 1e-12)
+    model = gpb.GPModel(train, gpb.KernelParams(1.0, 1.0, 0.1), 256)
+    fc = model.predict_with_full_cov(test)
+    assert np.array_equal(fc.full_covariance, fc.full_covariance.T)
+    assert rel(np.diagonal(fc.full_covariance), pv_a.variance) <= 1e-12
+    assert rel(fc.mean, pv_a.mean) <= 1e-12
