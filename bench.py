@@ -290,6 +290,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                              "tflops": pts * pred_flops_per_point(n, d) / 1e12},
         "phases_ms_per_step": {k: float(phase[i] / K) for i, k in enumerate(
             ("assembly", "factor", "solves", "cross_mean", "trsm_variance"))},
+        # the Cholesky rate also with assembly included, and
+        # predict+variance also cold (assembly + factor + solves + prediction)
+        "cholesky_with_assembly_tflops": world * K * chol_flops(n) / (float(phase[0] + phase[1]) * 1e-3) / 1e12
+        if world == 1 else None,
+        "predict_variance_cold_points_per_s": world * K * m / (float(sum(phase[:5])) * 1e-3)
+        if world == 1 else None,
         "e2e": {"value": chol_flops(n) / statistics.median(e2e_chol) / 1e12 if e2e_chol else None,
                 "unit": "TFLOP/s",
                 "predict_variance_points_per_s": m / statistics.median(e2e_pred) if e2e_pred else None,
