@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -50,21 +51,73 @@ int fail(int code, const std::string& msg) {
 constexpr double kHalfLog2Pi = 0.91893853320467274178;  // 0.5 * log(2 pi), model.py:35
 constexpr double kVarianceSlack = 1e-9;                  // model.py:33
 
+// Device-memory cache shared by all models of the process: model creation and
+// destruction (and plan resizes) reuse blocks instead of paying cudaMalloc /
+// cudaFree (which synchronises the device) on every small call.  A block is
+// handed out again only after a device synchronisation at release, so no
+// pending kernel can still touch it.  Cached blocks are returned to CUDA when
+// an allocation fails and at gpb_finalize.
+struct BlockCache {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_blocks;  // capacity -> pointer
+  size_t cached = 0;
+
+  cudaError_t alloc(size_t n, void** p, size_t* cap) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      const size_t limit = std::max(2 * n, n + (size_t(1) << 20));
+      auto it = free_blocks.lower_bound(n);
+      if (it != free_blocks.end() && it->first <= limit) {
+        *p = it->second;
+        *cap = it->first;
+        cached -= it->first;
+        free_blocks.erase(it);
+        return cudaSuccess;
+      }
+    }
+    cudaError_t e = cudaMalloc(p, n);
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      trim();
+      e = cudaMalloc(p, n);
+    }
+    if (e == cudaSuccess) *cap = n;
+    return e;
+  }
+  void release(void* p, size_t cap) {
+    cudaDeviceSynchronize();
+    std::lock_guard<std::mutex> lk(mu);
+    free_blocks.emplace(cap, p);
+    cached += cap;
+  }
+  void trim() {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& kv : free_blocks) cudaFree(kv.second);
+    free_blocks.clear();
+    cached = 0;
+  }
+};
+BlockCache g_cache;
+
 struct DevBuf {
   void* p = nullptr;
-  size_t bytes = 0;
+  size_t bytes = 0;  // capacity
   template <class T>
   T* as() const { return static_cast<T*>(p); }
   cudaError_t ensure(size_t nbytes) {
     if (nbytes <= bytes && p) return cudaSuccess;
     release();
-    cudaError_t e = cudaMalloc(&p, std::max<size_t>(nbytes, 16));
-    if (e == cudaSuccess) bytes = nbytes;
-    else p = nullptr;
+    void* q = nullptr;
+    size_t cap = 0;
+    cudaError_t e = g_cache.alloc(std::max<size_t>(nbytes, 16), &q, &cap);
+    if (e == cudaSuccess) {
+      p = q;
+      bytes = cap;
+    }
     return e;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) g_cache.release(p, bytes);
     p = nullptr;
     bytes = 0;
   }
@@ -924,7 +977,9 @@ int64_t pred_chunk(gpb_model* m, int64_t mt) {
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
   const double per_col = 8.0 * double(m->np_ + m->bi + m->np_ / kSekBlock + m->np_ / GBM + 4);
-  const double budget = std::min(48e9, 0.6 * (double(free_b) + double(m->Bv.bytes)));
+  // cached blocks are returned to CUDA if an allocation would otherwise fail
+  const double avail = double(free_b) + double(g_cache.cached) + double(m->Bv.bytes);
+  const double budget = std::min(48e9, 0.6 * avail);
   const int64_t c = std::max<int64_t>(GBM, int64_t(budget / per_col) / GBM * GBM);
   return std::min(c, all);
 }
@@ -1158,6 +1213,7 @@ int gpb_finalize(gpb_ctx* ctx) {
   cudaStreamDestroy(g_ctx->stream);
   delete g_ctx;
   g_ctx = nullptr;
+  g_cache.trim();  // blocks still owned by live models stay with them
   return GPB_OK;
 }
 
