@@ -165,6 +165,12 @@ int gpb_dev_potrf(gpb_ctx* ctx, void* stream, double* tile, double* dinv, int64_
 int gpb_dev_gemm(gpb_ctx* ctx, void* stream, const gpb_gemm_job* jobs, int64_t njobs, int64_t b,
                  int64_t lda, int64_t ldb, int64_t ldc, int a_kmajor, int b_kmajor, double alpha,
                  double beta);
+/* same with a tiled-k walk on both (K-major) operands: k runs through
+ * consecutive ktile-deep tiles kstride doubles apart -- the update of a tile
+ * by several panels held in one buffer, K = (number of panels) * ktile */
+int gpb_dev_gemm_tiled(gpb_ctx* ctx, void* stream, const gpb_gemm_job* jobs, int64_t njobs,
+                       int64_t b, int64_t lda, int64_t ldb, int64_t ldc, int a_kmajor, int b_kmajor,
+                       int64_t ktile, int64_t kstride, double alpha, double beta);
 /* batched tile GEMV: y (+)= alpha * op(a) x; outputs must be distinct per call */
 int gpb_dev_gemv(gpb_ctx* ctx, void* stream, const gpb_gemv_job* jobs, int64_t njobs, int64_t b,
                  int trans, double alpha, int accumulate);

@@ -76,6 +76,10 @@ SIGNATURES = {
     "gpb_dev_gemm": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                     ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_double, ctypes.c_double]),
+    "gpb_dev_gemm_tiled": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                          ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+                                          ctypes.c_double]),
     "gpb_dev_gemv": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                     ctypes.c_double, ctypes.c_int]),
     "gpb_dev_copy": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64]),

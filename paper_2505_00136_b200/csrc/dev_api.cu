@@ -197,9 +197,9 @@ int gpb_dev_potrf(gpb_ctx* ctx, void* stream, double* tile, double* dinv, int64_
   return GPB_OK;
 }
 
-int gpb_dev_gemm(gpb_ctx* ctx, void* stream, const gpb_gemm_job* jobs, int64_t njobs, int64_t b,
-                 int64_t lda, int64_t ldb, int64_t ldc, int a_kmajor, int b_kmajor, double alpha,
-                 double beta) {
+int gpb_dev_gemm_tiled(gpb_ctx* ctx, void* stream, const gpb_gemm_job* jobs, int64_t njobs,
+                       int64_t b, int64_t lda, int64_t ldb, int64_t ldc, int a_kmajor, int b_kmajor,
+                       int64_t ktile, int64_t kstride, double alpha, double beta) {
   if (int s = check_ctx(ctx)) return s;
   if (njobs <= 0) return GPB_OK;
   if (b % GBM) return gpb_plugin_fail(GPB_DIM, "tile size must be a multiple of 128");
@@ -228,12 +228,26 @@ int gpb_dev_gemm(gpb_ctx* ctx, void* stream, const gpb_gemm_job* jobs, int64_t n
   p.lda = lda;
   p.ldb = ldb;
   p.ldc = ldc;
-  p.a_ktile = p.b_ktile = int64_t(1) << 40;
+  if (ktile > 0) {
+    if (!a_kmajor || !b_kmajor || ktile % GBK)
+      return gpb_plugin_fail(GPB_DIM, "tiled-k walks need K-major operands and ktile % 32 == 0");
+    p.a_ktile = p.b_ktile = ktile;
+    p.a_kstride = p.b_kstride = kstride;
+  } else {
+    p.a_ktile = p.b_ktile = int64_t(1) << 40;
+  }
   p.alpha = alpha;
   p.beta = beta;
   p.max_k = maxk;
   DEV_TRY(launch_gemm(p, a_kmajor != 0, b_kmajor != 0, EPI_AXPBY, st));
   return GPB_OK;
+}
+
+int gpb_dev_gemm(gpb_ctx* ctx, void* stream, const gpb_gemm_job* jobs, int64_t njobs, int64_t b,
+                 int64_t lda, int64_t ldb, int64_t ldc, int a_kmajor, int b_kmajor, double alpha,
+                 double beta) {
+  return gpb_dev_gemm_tiled(ctx, stream, jobs, njobs, b, lda, ldb, ldc, a_kmajor, b_kmajor, 0, 0,
+                            alpha, beta);
 }
 
 int gpb_dev_gemv(gpb_ctx* ctx, void* stream, const gpb_gemv_job* jobs, int64_t njobs, int64_t b,

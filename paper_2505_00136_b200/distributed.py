@@ -42,6 +42,7 @@ from __future__ import annotations
 import contextlib
 import ctypes
 import math
+import os
 
 import numpy as np
 import torch
@@ -140,21 +141,31 @@ class DeviceTileOps:
                                           self._p(logdiag_slot), self._p(info)))
 
     def gemm(self, jobs, b, alpha, beta):
-        """jobs: (a, b_op, cin, cout, k, lower) on b x b tiles, NT product."""
+        """jobs: (a, b_op, cin, cout, k, lower), NT product on b x b tiles.
+        a / b_op may be (G, b, b) stacks of panel tiles (one panel buffer
+        slot per panel, a fixed stride apart): a tiled-k walk with K = G b."""
         if not jobs:
             return
         arr = (_lib.GemmJob * len(jobs))(*[
             _lib.GemmJob(a.data_ptr(), bb.data_ptr(), ci.data_ptr() if ci is not None else None,
                          co.data_ptr(), k, int(lo)) for a, bb, ci, co, k, lo in jobs])
-        _lib.check(self.lib.gpb_dev_gemm(self.rt.handle, self._s(), arr, len(jobs), b, b, b, b, 1,
-                                         1, alpha, beta))
+        strides = {a.stride(0) for a, bb, *_ in jobs if a.dim() == 3} | \
+                  {bb.stride(0) for a, bb, *_ in jobs if bb.dim() == 3}
+        if strides:
+            assert len(strides) == 1, "one panel stride per launch"
+            _lib.check(self.lib.gpb_dev_gemm_tiled(self.rt.handle, self._s(), arr, len(jobs), b, b, b,
+                                                   b, 1, 1, b, strides.pop(), alpha, beta))
+        else:
+            _lib.check(self.lib.gpb_dev_gemm(self.rt.handle, self._s(), arr, len(jobs), b, b, b, b,
+                                             1, 1, alpha, beta))
 
     _JOB_DTYPE = np.dtype([("a", "<u8"), ("b", "<u8"), ("cin", "<u8"), ("cout", "<u8"),
                            ("k", "<i4"), ("lower", "<i4")])  # gpb_gemm_job
 
-    def gemm_addr(self, a_addr, b_addr, c_addr, lower, k, b, alpha, beta):
+    def gemm_addr(self, a_addr, b_addr, c_addr, lower, k, b, alpha, beta, kstride=0):
         """Vectorised job table (device addresses as int64 arrays): the
-        trailing update of one step at large T without per-tile Python work."""
+        trailing update of one step at large T without per-tile Python work.
+        kstride > 0: operands walk K in b-deep tiles kstride doubles apart."""
         n = len(c_addr)
         if n == 0:
             return
@@ -162,8 +173,8 @@ class DeviceTileOps:
         tab["a"], tab["b"], tab["cin"], tab["cout"] = a_addr, b_addr, c_addr, c_addr
         tab["k"], tab["lower"] = k, lower
         assert tab.dtype.itemsize == ctypes.sizeof(_lib.GemmJob)
-        _lib.check(self.lib.gpb_dev_gemm(self.rt.handle, self._s(), tab.ctypes.data, n, b, b, b, b,
-                                         1, 1, alpha, beta))
+        _lib.check(self.lib.gpb_dev_gemm_tiled(self.rt.handle, self._s(), tab.ctypes.data, n, b, b, b,
+                                               b, 1, 1, b if kstride else 0, kstride, alpha, beta))
 
     def gemv(self, jobs, b, trans, alpha, accumulate):
         if not jobs:
@@ -362,10 +373,26 @@ class DistributedGP:
 
     # -- factorisation ---------------------------------------------------------
     def _factor(self):
+        """2D block-cyclic tiled Cholesky with panel groups (tiled.py:168-204).
+
+        Panels are factored in groups of G (GPB_DIST_PANELS, default 2) as on
+        one GPU: per panel k of group s, on the high-priority critical stream,
+        POTRF(k) on its owner, the L_kk^-1 broadcast, the panel TRSM on the
+        ranks of process column k mod Q, the per-process-row panel broadcasts
+        and the in-group update of the group's later columns (K = b); then
+        NEXT(s): the next group's columns updated with all G panels (K = G b).
+        The main stream applies UPD(s), the rest of the trailing update, with
+        K = G b: each operand walks the G panel tiles of its row, which sit a
+        fixed stride apart in the group's panel buffer (tile (i, k) in slot
+        i // P of process row i mod P), so C tiles are read and written once
+        per group.  Panel buffers alternate between two sets across groups.
+        """
         if self._factored:
             return
         ops, b, T, lay = self.ops, self.b, self.T, self.lay
+        P, Q = self.P, self.Q
         d = self.train.d
+        G = max(1, int(os.environ.get("GPB_DIST_PANELS", "2")))
         self.zp = ops.pad(ops.from_numpy(self.train.z), self.np_, d, lay)
         self.yp = ops.pad(ops.from_numpy(self.train.y), self.np_, 0, lay)
         self.L = ops.zeros(max(1, len(self.owned)), b, b)
@@ -374,17 +401,13 @@ class DistributedGP:
         info = ops.zeros(1, dtype=torch.int32) - 1
         ops.assemble(self.zp, d, lay, self.params, True,
                      [(i, j, self.L[s]) for s, (i, j) in enumerate(self.owned)])
-        rows_per = -(-T // self.P)
-        # panel buffers per process row, double-buffered across steps
-        panels = [[ops.zeros(max(1, rows_per), b, b) for _ in range(self.P)] for _ in range(2)]
-        my_p, my_q = divmod(self.rank, self.Q)
+        rows_per = -(-T // P)
+        # panel buffers: [set][process row] -> (G, rows_per, b, b)
+        panels = [[ops.zeros(G, rows_per, b, b) for _ in range(P)] for _ in range(2)]
+        my_p, my_q = divmod(self.rank, Q)
         by_col = {}
-        for s, (i, j) in enumerate(self.owned):
-            by_col.setdefault(j, []).append((s, i))
-        # Lookahead (as the single-GPU schedule): the critical stream runs
-        # POTRF(k), the L_kk^-1 / panel broadcasts, TRSM(k) and the update of
-        # column k+1 (COL); the main stream applies the rest of step k's
-        # trailing update (UPD), so the next panel's exchange overlaps it.
+        for s_, (i, j) in enumerate(self.owned):
+            by_col.setdefault(j, []).append((s_, i))
         cuda = getattr(ops, "device", None) is not None and ops.device.type == "cuda"
         main = torch.cuda.current_stream(ops.device) if cuda else None
         crit = torch.cuda.Stream(device=ops.device, priority=-1) if cuda else None
@@ -396,62 +419,74 @@ class DistributedGP:
             own_j = np.array([j for _, j in self.owned], dtype=np.int64)
             tile_bytes = b * b * 8
             c_addr = self.L.data_ptr() + np.arange(len(self.owned), dtype=np.int64) * tile_bytes
-            pbase = [np.array([panels[h][p].data_ptr() for p in range(self.P)], dtype=np.int64)
+            pbase = [np.array([panels[h][p].data_ptr() for p in range(P)], dtype=np.int64)
                      for h in range(2)]
         if cuda:
             crit.wait_stream(main)  # assembly
         t0 = self._event()
-        for k in range(T):
-            own = self.cyc.owner(k, k)
-            panel = panels[k % 2]
+        starts = list(range(0, T, G))
+        for s, k0 in enumerate(starts):
+            k1 = min(T, k0 + G) - 1
+            gs = k1 - k0 + 1
+            buf = panels[s % 2]
+
+            def stack(i, g_hi):  # panel tiles (i, k0 .. k0+g_hi-1) as a (g_hi, b, b) stack
+                return buf[i % P][:g_hi, i // P]
+
             with on_crit():
-                if self.rank == own:
-                    ops.potrf(self.L[self.slot[k, k]], self.dinv[k], lay, k * b,
-                              self.logdiag[k:k + 1], info)
-                self._bcast(self.dinv[k], own)
-                if k + 1 == T:
-                    break
-                if my_q == k % self.Q:  # this rank holds panel tiles of column k
-                    mine = self.cyc.panel_rows(k, my_p)
-                    ops.gemm([(self.L[self.slot[i, k]], self.dinv[k], None, panel[my_p][s], b, False)
-                              for s, i in enumerate(mine)], b, 1.0, 0.0)
-                    ops.copy([(panel[my_p][s], self.L[self.slot[i, k]]) for s, i in enumerate(mine)])
-                where = {}
-                for p in range(self.P):
-                    rows = self.cyc.panel_rows(k, p)
-                    for s, i in enumerate(rows):
-                        where[i] = panel[p][s]
-                    if rows:
-                        self._bcast(panel[p][:len(rows)], p * self.Q + k % self.Q)
-                # COL(k): column k+1 also needs UPD(k-1), which covered it
-                if cuda and k >= 1:
-                    crit.wait_event(ev_upd[k - 1])
-                ops.gemm([(where[i], where[k + 1], self.L[s], self.L[s], b, i == k + 1)
-                          for s, i in by_col.get(k + 1, [])], b, -1.0, 1.0)
+                for k in range(k0, k1 + 1):
+                    g = k - k0
+                    own = self.cyc.owner(k, k)
+                    if self.rank == own:
+                        ops.potrf(self.L[self.slot[k, k]], self.dinv[k], lay, k * b,
+                                  self.logdiag[k:k + 1], info)
+                    self._bcast(self.dinv[k], own)
+                    if k + 1 == T:
+                        break
+                    if my_q == k % Q:  # this rank holds panel tiles of column k
+                        mine = self.cyc.panel_rows(k, my_p)
+                        ops.gemm([(self.L[self.slot[i, k]], self.dinv[k], None, buf[my_p][g, i // P], b,
+                                   False) for i in mine], b, 1.0, 0.0)
+                        ops.copy([(buf[my_p][g, i // P], self.L[self.slot[i, k]]) for i in mine])
+                    for p in range(P):
+                        rows = self.cyc.panel_rows(k, p)
+                        if rows:
+                            self._bcast(buf[p][g, rows[0] // P: rows[-1] // P + 1], p * Q + k % Q)
+                    # in-group: the group's later columns get panel k (K = b)
+                    ops.gemm([(buf[i % P][g, i // P], buf[j % P][g, j // P], self.L[s_], self.L[s_], b,
+                               i == j) for j in range(k + 1, k1 + 1) for s_, i in by_col.get(j, [])],
+                             b, -1.0, 1.0)
+                if k1 + 1 < T:
+                    # NEXT(s): the next group's columns get all gs panels (K = gs b);
+                    # UPD(s-1) covered them too
+                    if cuda and s >= 1:
+                        crit.wait_event(ev_upd[s - 1])
+                    nxt_hi = min(T, k1 + 1 + G)
+                    ops.gemm([(stack(i, gs), stack(j, gs), self.L[s_], self.L[s_], gs * b, i == j)
+                              for j in range(k1 + 1, nxt_hi) for s_, i in by_col.get(j, [])],
+                             b, -1.0, 1.0)
                 if cuda:
                     ev_panel = torch.cuda.Event()
                     ev_panel.record(crit)
-            # UPD(k) on the main stream: owned tiles (i, j), j >= k+2
+            if k1 + 1 >= T:
+                break
+            # UPD(s) on the main stream: owned tiles (i, j), j beyond the next group
             if cuda:
                 main.wait_event(ev_panel)
+            j_lo = k1 + 1 + G
             if vector_upd:  # job table built with numpy (large T)
-                sel = own_j >= k + 2
+                sel = own_j >= j_lo
                 ii, jj = own_i[sel], own_j[sel]
-                base = pbase[k % 2]
-
-                def addr(x):
-                    p = x % self.P
-                    first = k + 1 + (p - (k + 1)) % self.P
-                    return base[p] + ((x - first) // self.P) * tile_bytes
-
-                ops.gemm_addr(addr(ii), addr(jj), c_addr[sel], (ii == jj).astype(np.int32), b, b,
-                              -1.0, 1.0)
+                base = pbase[s % 2]
+                addr = lambda x: base[x % P] + (x // P) * tile_bytes  # noqa: E731
+                ops.gemm_addr(addr(ii), addr(jj), c_addr[sel], (ii == jj).astype(np.int32), gs * b, b,
+                              -1.0, 1.0, kstride=rows_per * b * b)
             else:
-                ops.gemm([(where[i], where[j], self.L[s], self.L[s], b, i == j)
-                          for j in range(k + 2, T) for s, i in by_col.get(j, [])], b, -1.0, 1.0)
+                ops.gemm([(stack(i, gs), stack(j, gs), self.L[s_], self.L[s_], gs * b, i == j)
+                          for j in range(j_lo, T) for s_, i in by_col.get(j, [])], b, -1.0, 1.0)
             if cuda:
-                ev_upd[k] = torch.cuda.Event()
-                ev_upd[k].record(main)
+                ev_upd[s] = torch.cuda.Event()
+                ev_upd[s].record(main)
         if cuda:
             main.wait_stream(crit)
         t1 = self._event()

@@ -71,9 +71,15 @@ class HostTileOps:
         valid = [self._valid(tile_off + r, lay) for r in range(len(diag))]
         logdiag_slot[0] = float(np.sum(np.log(diag[valid])))
 
+    @staticmethod
+    def _k_operand(t):
+        """(G, b, b) stacks of panel tiles are one b x G b operand (tiled-k walk)."""
+        x = t.numpy()
+        return np.concatenate(list(x), axis=1) if x.ndim == 3 else x
+
     def gemm(self, jobs, b, alpha, beta):
         for a, bb, cin, cout, k, lower in jobs:
-            acc = alpha * (a.numpy()[:, :k] @ bb.numpy()[:, :k].T)
+            acc = alpha * (self._k_operand(a)[:, :k] @ self._k_operand(bb)[:, :k].T)
             if beta != 0.0:
                 acc = acc + beta * cin.numpy()
             cout.copy_(torch.from_numpy(acc))
