@@ -17,11 +17,13 @@ inside the timed region).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): the same config-2 problem factored 2D block-cyclic over all
-ranks with NCCL panel broadcasts and predicted sharded over test points
-(paper_2505_00136_b200/distributed.py, strong scaling); value = n^3/3 flops
-over the slowest rank's factorisation time.  GPB_REPLICAS=1 instead runs N
-independent single-GPU replicas.
+N > 1 (torchrun): config 2 weak-scaled -- n = m grow as N^(1/3) (multiples
+of 512) so the Cholesky flops per GPU stay those of config 2; N = 8 gives
+n = 65536, BASELINE config 3's size.  The problem is factored 2D
+block-cyclic over all ranks with NCCL panel broadcasts and predicted sharded
+over test points (paper_2505_00136_b200/distributed.py); value = total
+n^3/3 flops over the slowest rank's factorisation time.  GPB_REPLICAS=1
+instead runs N independent single-GPU replicas.
 """
 
 from __future__ import annotations
@@ -47,6 +49,14 @@ if os.environ.get("GPB_BENCH_SMALL"):  # plumbing checks only (tests); never a b
 WORKLOAD = ("config 2: n_train=32768, n_test=32768, n_regressors=128, 64 tiles of 512, FP64; "
             "step = SEK assembly + tiled Cholesky + alpha solves + loss + predict_with_uncertainty")
 DATA = "synthetic: BASELINE.json mass-spring-damper generator, seed 0 (stands in for the paper's MSD data)"
+
+
+def weak_cfg(world: int) -> dict:
+    """Config 2 weak-scaled to `world` GPUs: n = m = 512 * round(64 * world^(1/3))."""
+    if os.environ.get("GPB_BENCH_SMALL"):
+        return dict(CFG)
+    tiles = int(round(64 * world ** (1.0 / 3.0)))
+    return {"n": 512 * tiles, "m": 512 * tiles, "d": 128, "tiles": tiles}
 
 
 def chol_flops(n: int) -> float:
@@ -320,16 +330,18 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
 
 def run_distributed(args, rank: int, world: int, local_rank: int):
-    """N > 1: the config-2 problem factorised 2D block-cyclic over all ranks
-    (distributed.py) with NCCL panel broadcasts, prediction sharded over test
-    points.  Strong scaling: total work fixed, value = n^3/3 flops over the
-    slowest rank's factorisation time."""
+    """N > 1: config 2 weak-scaled (weak_cfg) and factorised 2D block-cyclic over
+    all ranks (distributed.py) with NCCL panel broadcasts, prediction sharded
+    over test points.  value = total n^3/3 flops over the slowest rank's
+    factorisation device time; e2e = the same through the public API from host
+    numpy (DistributedGP construction + log_likelihood, wall clock, max over
+    ranks), and predict_with_uncertainty's test points/s likewise."""
     import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2505_00136_b200 as gpb
-    from paper_2505_00136_b200.distributed import DistributedGP
+    from paper_2505_00136_b200.distributed import DistributedGP, process_grid
 
     backend = os.environ.get("GPB_DIST_BACKEND", "nccl")
     device = int(os.environ.get("GPB_FORCE_DEVICE", local_rank))
@@ -338,45 +350,63 @@ def run_distributed(args, rank: int, world: int, local_rank: int):
         dist.init_process_group("nccl", device_id=torch.device("cuda", device))
     else:
         dist.init_process_group(backend)
-    n, m, d, tiles = CFG["n"], CFG["m"], CFG["d"], CFG["tiles"]
+    cfg = weak_cfg(world)
+    n, m, d, tiles = cfg["n"], cfg["m"], cfg["d"], cfg["tiles"]
     train, test = gpb.make_msd_dataset(n, m, d, seed=0)
     rt = gpb.start_runtime(gpb.RuntimeConfig(device=device))
-    times = []
+    times, walls = [], []
+    launches = 0
     clocks = ClockSampler(device)
     for it in range(args.warmup + args.steps):
         if it == args.warmup:
             dist.barrier()
             torch.cuda.synchronize()
             clocks.start()
-        model = DistributedGP(train, gpb.KernelParams(1.0, 1.0, 0.1), tiles)
-        model.log_likelihood()
-        model.predict_with_uncertainty(test)
+        t0 = time.perf_counter()
+        model = DistributedGP(train, gpb.KernelParams(1.0, 1.0, 0.1), tiles)  # host numpy in
+        model.log_likelihood()                                                # loss back on the host
+        t1 = time.perf_counter()
+        model.predict_with_uncertainty(test)                                  # mean, variance on the host
+        t2 = time.perf_counter()
         if it >= args.warmup:
             times.append([model.timings["factor_ms"], model.timings["solve_ms"],
                           model.timings["predict_ms"]])
+            walls.append([t1 - t0, t2 - t1])
+            launches += model.launch_count()
         model.close()
         del model
     torch.cuda.synchronize()
     dist.barrier()
     clk = clocks.stop()
-    t = torch.tensor(np.array(times).sum(axis=0), dtype=torch.float64, device="cuda")
+    t = torch.tensor(np.concatenate([np.array(times).sum(axis=0), np.array(walls).sum(axis=0)]),
+                     dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    factor_ms, solve_ms, pred_ms = t.tolist()
+    factor_ms, solve_ms, pred_ms, wall_chol, wall_pred = t.tolist()
+    lt = torch.tensor([launches], dtype=torch.float64, device="cuda")
+    dist.all_reduce(lt, op=dist.ReduceOp.SUM)
     K = args.steps
     if rank == 0:
-        from paper_2505_00136_b200.distributed import process_grid
-
         p, q = process_grid(world)
         line = {
             "metric": METRIC, "value": K * chol_flops(n) / (factor_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
             "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": (factor_ms + solve_ms + pred_ms) / K, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
-            "config": {"workload": WORKLOAD, "parallelism": f"2D block-cyclic {p}x{q} Cholesky, "
-                       f"NCCL panel broadcasts; prediction sharded over test points"},
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": {"workload": f"config 2 weak-scaled to {world} GPUs (fixed Cholesky flops per GPU): "
+                       f"n_train = n_test = {n}, n_regressors = {d}, {tiles} tiles of 512, FP64; step = "
+                       "SEK assembly + tiled Cholesky + alpha solves + loss + predict_with_uncertainty",
+                       "l2": "inputs larger than L2", "parallelism": f"2D block-cyclic {p}x{q} Cholesky, "
+                       "NCCL panel broadcasts; prediction sharded over test points"},
             "predict_variance": {"value": K * m / (pred_ms * 1e-3), "unit": "test points/s"},
             "phases_ms_per_step": {"factor": factor_ms / K, "solves": solve_ms / K,
                                    "predict_variance": pred_ms / K},
+            "e2e": {"value": K * chol_flops(n) / wall_chol / 1e12, "unit": "TFLOP/s",
+                    "predict_variance_points_per_s": K * m / wall_pred,
+                    "h2d_bytes_per_step": 8 * world * (n * d + n + m * d),
+                    "d2h_bytes_per_step": 8 * world * (2 + 2 * m),
+                    "api": "DistributedGP(train).log_likelihood() then predict_with_uncertainty(test), "
+                           "host numpy on every rank"},
+            "gpu_launches": int(lt.item()),
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -101,6 +101,7 @@ class DeviceTileOps:
         self.rt = runtime
         self.device = torch.device("cuda", device)
         self.lib = _lib.load()
+        self.launches = 0  # kernels launched through gpb_dev_* (one per call)
 
     # buffers --------------------------------------------------------------
     def zeros(self, *shape, dtype=torch.float64):
@@ -122,6 +123,7 @@ class DeviceTileOps:
     # kernels --------------------------------------------------------------
     def pad(self, src, n_p: int, d: int, lay: dict):
         out = self.zeros(n_p, d) if d else self.zeros(n_p)
+        self.launches += 1
         _lib.check(self.lib.gpb_dev_pad(self.rt.handle, self._s(), self._p(src), n_p, d,
                                         lay["pad_bp"], lay["pad_b"], self._p(out)))
         return out
@@ -130,12 +132,14 @@ class DeviceTileOps:
         if not tiles:
             return
         arr = (_lib.TileDesc * len(tiles))(*[_lib.TileDesc(i, j, t.data_ptr()) for i, j, t in tiles])
+        self.launches += 1
         _lib.check(self.lib.gpb_dev_assemble(
             self.rt.handle, self._s(), self._p(zp), d, lay["b"], lay["pad_bp"], lay["pad_b"],
             params.lengthscale, params.vertical_scale, params.noise_variance, int(add_noise),
             arr, len(tiles)))
 
     def potrf(self, tile, dinv, lay, tile_off, logdiag_slot, info):
+        self.launches += 1
         _lib.check(self.lib.gpb_dev_potrf(self.rt.handle, self._s(), self._p(tile), self._p(dinv),
                                           lay["b"], tile_off, lay["pad_bp"], lay["pad_b"],
                                           self._p(logdiag_slot), self._p(info)))
@@ -153,9 +157,11 @@ class DeviceTileOps:
                   {bb.stride(0) for a, bb, *_ in jobs if bb.dim() == 3}
         if strides:
             assert len(strides) == 1, "one panel stride per launch"
+            self.launches += 1
             _lib.check(self.lib.gpb_dev_gemm_tiled(self.rt.handle, self._s(), arr, len(jobs), b, b, b,
                                                    b, 1, 1, b, strides.pop(), alpha, beta))
         else:
+            self.launches += 1
             _lib.check(self.lib.gpb_dev_gemm(self.rt.handle, self._s(), arr, len(jobs), b, b, b, b,
                                              1, 1, alpha, beta))
 
@@ -173,6 +179,7 @@ class DeviceTileOps:
         tab["a"], tab["b"], tab["cin"], tab["cout"] = a_addr, b_addr, c_addr, c_addr
         tab["k"], tab["lower"] = k, lower
         assert tab.dtype.itemsize == ctypes.sizeof(_lib.GemmJob)
+        self.launches += 1
         _lib.check(self.lib.gpb_dev_gemm_tiled(self.rt.handle, self._s(), tab.ctypes.data, n, b, b, b,
                                                b, 1, 1, b if kstride else 0, kstride, alpha, beta))
 
@@ -181,6 +188,7 @@ class DeviceTileOps:
             return
         arr = (_lib.GemvJob * len(jobs))(*[_lib.GemvJob(a.data_ptr(), x.data_ptr(), y.data_ptr())
                                            for a, x, y in jobs])
+        self.launches += 1
         _lib.check(self.lib.gpb_dev_gemv(self.rt.handle, self._s(), arr, len(jobs), b, int(trans),
                                          alpha, int(accumulate)))
 
@@ -189,9 +197,11 @@ class DeviceTileOps:
             return
         nbytes = pairs[0][0].numel() * 8
         arr = (_lib.CopyJob * len(pairs))(*[_lib.CopyJob(s.data_ptr(), d.data_ptr()) for s, d in pairs])
+        self.launches += 1
         _lib.check(self.lib.gpb_dev_copy(self.rt.handle, self._s(), arr, len(pairs), nbytes))
 
     def combine(self, base, parts, out):
+        self.launches += 1
         _lib.check(self.lib.gpb_dev_combine(self.rt.handle, self._s(), self._p(base), self._p(parts),
                                             parts.shape[0], base.numel(), self._p(out)))
 
@@ -720,6 +730,17 @@ class DistributedGP:
             except NotPositiveDefinite as exc:
                 raise NotPositiveDefinite(f"iteration {step_no}: {exc}") from exc
         return history
+
+    def launch_count(self) -> int:
+        """Kernels this instance launched: the device-level ABI calls of the
+        schedule plus the replica model's own launches (prediction, gradient)."""
+        n = getattr(self.ops, "launches", 0)
+        rep = self._replica
+        if rep is not None and getattr(rep, "h", None) is not None:
+            c = ctypes.c_int64()
+            self.ops.lib.gpb_model_launch_count(rep.h, ctypes.byref(c))
+            n += int(c.value)
+        return n
 
     def close(self):
         if self._replica is not None:

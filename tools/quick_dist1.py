@@ -10,7 +10,7 @@ n = int(os.environ.get("N", 32768)); d = int(os.environ.get("D", 128)); T = int(
 train, test = gpb.make_msd_dataset(n, m, d, seed=0)
 rt = gpb.start_runtime()
 flops = n**3/3
-for rep in range(3):
+for rep in range(int(os.environ.get("REPS", 3))):
     model = DistributedGP(train, gpb.KernelParams(), T)
     t0 = time.time(); ll = model.log_likelihood(); t1 = time.time()
     pv = model.predict_variance(test); t2 = time.time()
