@@ -123,23 +123,29 @@ GPB_DEVINL void store_acc(double* c, int64_t ldc, const double (&acc)[4][4][2], 
     }
 }
 
-// One TRTRI job: D[I][J] = -D[I][I] * sum_{K=J}^{I-1} L[I][K] D[K][J]  (32-blocks)
-GPB_DEVINL void trtri_job(double* T, double* D, int bi, int I, int J, double* Sw, int g, int t) {
+
+// Right-looking TRTRI of the tile, X = L^-1 by 32-blocks:
+//   X_IJ = -X_II sum_{K=J}^{I-1} L_IK X_KJ.
+// Block (I, J) of D accumulates -sum L_IK X_KJ one K per panel (K = p-2 in
+// phase A(p), once row K of X is final), and row I is finalised in phase
+// B(I+1) as X_II * D_IJ: every job has K = 32, so no single warp carries a
+// long dependency chain.
+GPB_DEVINL void trtri_acc(const double* T, double* D, int bi, int I, int J, int K, int g, int t) {
   double acc[4][4][2];
   zero_acc(acc);
-  warp_nn(acc, T + static_cast<int64_t>(I) * NB * bi + J * NB, bi,
-          D + static_cast<int64_t>(J) * NB * bi + J * NB, bi, (I - J) * NB, g, t);
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      Sw[(8 * i + g) * SLD + 8 * j + 2 * t] = acc[i][j][0];
-      Sw[(8 * i + g) * SLD + 8 * j + 2 * t + 1] = acc[i][j][1];
-    }
-  __syncwarp();
+  warp_nn(acc, T + static_cast<int64_t>(I) * NB * bi + K * NB, bi,
+          D + static_cast<int64_t>(K) * NB * bi + J * NB, bi, NB, g, t);
+  // first term assigns (D_IJ = -acc), later terms subtract
+  store_acc(D + static_cast<int64_t>(I) * NB * bi + J * NB, bi, acc, g, t, K == J, -1.0);
+}
+
+GPB_DEVINL void trtri_fin(double* D, int bi, int I, int J, int g, int t) {
+  double acc[4][4][2];
   zero_acc(acc);
-  warp_nn(acc, D + static_cast<int64_t>(I) * NB * bi + I * NB, bi, Sw, SLD, NB, g, t);
-  store_acc(D + static_cast<int64_t>(I) * NB * bi + J * NB, bi, acc, g, t, true, -1.0);
+  warp_nn(acc, D + static_cast<int64_t>(I) * NB * bi + I * NB, bi,
+          D + static_cast<int64_t>(I) * NB * bi + J * NB, bi, NB, g, t);
+  __syncwarp();  // every lane has read D_IJ before it is overwritten
+  store_acc(D + static_cast<int64_t>(I) * NB * bi + J * NB, bi, acc, g, t, true, 1.0);
   __syncwarp();
 }
 
@@ -156,10 +162,9 @@ GPB_DEVINL void cluster_barrier(bool clustered) {
 
 __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
   extern __shared__ double sm[];
-  double* Ld = sm;                 // [32][33] factor block
-  double* Li = Ld + NB * SLD;      // [32][33] its inverse
+  double* Ld = sm;                 // [64][33] factor block (rows 32..63: padding)
+  double* Li = Ld + 2 * NB * SLD;  // [32][33] its inverse
   double* rdg = Li + NB * SLD;     // [32] 1 / l_jj of the current panel
-  double* S = rdg + NB;            // [8][32][33] per-warp scratch
   __shared__ volatile int prog_s;  // pivots of the chain published so far
   volatile int* prog = &prog_s;
   // every CTA reads info before the first cluster barrier; only CTA 0
@@ -178,7 +183,6 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
   const int GW = ncta * NW;                // warps in the cluster
   const int g = lane >> 2, t = lane & 3;
   const bool factor = !a.trtri_only;
-  double* Sw = S + (tid >> 5) * NB * SLD;
   double logsum = 0.0;  // meaningful in lane 0 of warp 0
   if (tid == 0) *prog = 0;
   cluster_barrier(clustered);
@@ -192,14 +196,25 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
 
   for (int p = 0; p < P; ++p) {
     const int c0 = p * NB;
-    // A: last contribution (panel p-1) to panel p, rows >= c0
-    if (p > 0 && factor) {
-      for (int rb = p + warp; rb < P; rb += GW) {
-        double acc[4][4][2];
-        zero_acc(acc);
-        warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi + c0 - NB, bi,
-                T + static_cast<int64_t>(c0) * bi + c0 - NB, bi, NB, g, t);
-        store_acc(T + static_cast<int64_t>(rb) * NB * bi + c0, bi, acc, g, t, false, 1.0);
+    // A: last contribution (panel p-1) to panel p, rows >= c0; and the
+    // TRTRI term K = p-2 of row I = p-1 (finalised in B(p)); the same term of
+    // the later rows I >= p is accumulated by the job warps of B(p)
+    {
+      const int na = (factor && p > 0) ? P - p : 0;
+      const int nj = p >= 2 ? p - 1 : 0;
+      const int nw = nj;
+      for (int q = warp; q < na + nw; q += GW) {
+        if (q < na) {
+          const int rb = p + q;
+          double acc[4][4][2];
+          zero_acc(acc);
+          warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi + c0 - NB, bi,
+                  T + static_cast<int64_t>(c0) * bi + c0 - NB, bi, NB, g, t);
+          store_acc(T + static_cast<int64_t>(rb) * NB * bi + c0, bi, acc, g, t, false, 1.0);
+        } else {
+          const int w = q - na;
+          trtri_acc(T, D, bi, p - 1 + w / nj, w % nj, p - 2, g, t);
+        }
       }
     }
     cluster_barrier(clustered);
@@ -208,15 +223,16 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
       // B, job warps (CTAs 1.. when clustered, else warps 2..7), dealt
       // round-robin: panel p-1's rank-32 contribution to every trailing
       // 32-block (rb, cb), p+1 <= cb <= rb (right-looking; panel p gets it
-      // in phase A), and block row p-1 of the inverse
+      // in phase A), and the finalisation of block row p-1 of the inverse
       const int m = P - p - 1;
       const int pre = (factor && p > 0) ? m * (m + 1) / 2 : 0;
-      const int inv = (p >= 2) ? p - 1 : 0;  // jobs J = 0..p-2 of row I = p-1
+      const int inv = (p >= 2) ? p - 1 : 0;  // blocks J = 0..p-2 of row I = p-1
+      const int accn = (p >= 2) ? (P - p) * (p - 1) : 0;  // term K = p-2 of rows I >= p
       // clustered: CTA 0 keeps only the pivot chain so its SMSPs are not
       // shared with DMMA warps; the other CTAs' warps take the jobs
       const int w0 = clustered ? warp - NW : warp - 2;
       const int nwk = clustered ? GW - NW : NW - 2;
-      for (int q = (w0 >= 0 ? w0 : pre + inv); q < pre + inv; q += nwk) {
+      for (int q = (w0 >= 0 ? w0 : pre + inv + accn); q < pre + inv + accn; q += nwk) {
         if (q < pre) {
           int rr = static_cast<int>((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
           while (rr * (rr + 1) / 2 > q) --rr;
@@ -227,8 +243,11 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
           warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi + c0 - NB, bi,
                   T + static_cast<int64_t>(cb) * NB * bi + c0 - NB, bi, NB, g, t);
           store_acc(T + static_cast<int64_t>(rb) * NB * bi + cb * NB, bi, acc, g, t, false, 1.0);
+        } else if (q < pre + inv) {
+          trtri_fin(D, bi, p - 1, q - pre, g, t);
         } else {
-          trtri_job(T, D, bi, p - 1, q - pre, Sw, g, t);
+          const int w = q - pre - inv;
+          trtri_acc(T, D, bi, p + w / (p - 1), w % (p - 1), p - 2, g, t);
         }
       }
     } else if (lead && lw == 0) {
@@ -262,12 +281,12 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
             __threadfence_block();
             *prog = base + j + 1;
           }
+          // l_(j+c-o), j broadcast from shared memory (one address per load, no
+          // shuffles); rows past the panel read the padding rows of Ld and only
+          // feed registers that hold columns past the panel
+          const double* lrow = Ld + (j - o) * SLD + j;
 #pragma unroll
-          for (int c = o + 1; c < NB; ++c) {
-            // srcLane is taken modulo 32; columns past the panel hold garbage
-            const double lcj = __shfl_sync(0xffffffffu, lcol, j + c - o);
-            r[c] = fma(-lcol, lcj, r[c]);
-          }
+          for (int c = o + 1; c < NB; ++c) r[c] = fma(-lcol, lrow[c * SLD], r[c]);
         };
 #pragma unroll 1
         for (int j = 0; j < NB; j += 2) {
@@ -345,9 +364,10 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
     cluster_barrier(clustered);
     PROF_MARK(2)
   }
-  // last block row of the inverse (rows 1..P-2 were interleaved above)
-  if (P >= 2)
-    for (int J = warp; J < P - 1; J += GW) trtri_job(T, D, bi, P - 1, J, Sw, g, t);
+  // last block row of the inverse: its last term (K = P-2), then X_II * D_IJ
+  for (int J = warp; J < P - 1; J += GW) trtri_acc(T, D, bi, P - 1, J, P - 2, g, t);
+  cluster_barrier(clustered);
+  for (int J = warp; J < P - 1; J += GW) trtri_fin(D, bi, P - 1, J, g, t);
   PROF_MARK(3)
   // zero strictly-upper 32-blocks of L and Dinv (lower-triangular results)
   for (int r = warp; r < bi; r += GW) {
@@ -365,7 +385,7 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
 #undef PROF_MARK
 }
 
-size_t potrf_smem_bytes() { return sizeof(double) * (2 * NB * SLD + NB + NW * NB * SLD); }
+size_t potrf_smem_bytes() { return sizeof(double) * (3 * NB * SLD + NB); }
 
 static int g_cluster = 0;
 
