@@ -389,12 +389,12 @@ size_t potrf_smem_bytes() { return sizeof(double) * (3 * NB * SLD + NB); }
 
 static int g_cluster = 0;
 
-// CTAs per diagonal tile (GPB_POTRF_CLUSTER: 1 = single CTA, up to 8)
+// CTAs per diagonal tile (GPB_POTRF_CLUSTER: 1 = single CTA, 2, 4, 8 or 16)
 static int potrf_cluster() {
   if (g_cluster == 0) {
     const char* e = getenv("GPB_POTRF_CLUSTER");
     int c = e ? atoi(e) : 8;
-    g_cluster = (c == 1 || c == 2 || c == 4 || c == 8) ? c : 8;
+    g_cluster = (c == 1 || c == 2 || c == 4 || c == 8 || c == 16) ? c : 8;
   }
   return g_cluster;
 }
@@ -421,6 +421,8 @@ cudaError_t launch_potrf(const PotrfArgs& a, cudaStream_t s) {
 }
 
 cudaError_t potrf_init_attributes() {
+  cudaError_t e = cudaFuncSetAttribute(potrf_tile_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(potrf_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(potrf_smem_bytes()));
 }
