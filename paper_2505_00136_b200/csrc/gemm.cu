@@ -20,9 +20,12 @@ namespace gpb {
 
 // BN < 128 splits each logical 128x128 block over 128/BN CTAs, which lets
 // two CTAs share an SM (one's barrier or epilogue overlaps the other's DMMA).
-template <int WM_, int WN_, int BK_, int STAGES_, int BN_ = 128, int MINB_ = 1>
+template <int WM_, int WN_, int BK_, int STAGES_, int BN_ = 128, int MINB_ = 1, bool PAIR_ = false>
 struct GemmCfg {
   static constexpr int WM = WM_, WN = WN_, BK = BK_, STAGES = STAGES_;
+  // PAIR: each lane loads the k values of two consecutive k-steps with one
+  // 16-byte LDS from K-major stages (k-steps 2q / 2q+1 take k = 8q + 2t / +1)
+  static constexpr bool PAIR = PAIR_;
   static constexpr int BN = BN_, CPB = GBN / BN_, MINB = MINB_;
   static constexpr int THREADS = WM * WN * 32;
   static constexpr int FM = GBM / WM / 8;  // 8-row fragments per warp
@@ -31,8 +34,10 @@ struct GemmCfg {
 
 template <class C, bool KMAJ, int ROWS>
 struct StageLayout {
-  static constexpr int kLd = KMAJ ? (C::BK + 4) : (ROWS + 4);
-  static constexpr int kElems = KMAJ ? ROWS * (C::BK + 4) : C::BK * (ROWS + 4);
+  // K-major pitch: BK + 4 keeps 8-byte fragment loads conflict-free; the
+  // 16-byte loads of PAIR need BK + 8 (2 * pitch = 16 mod 32 banks)
+  static constexpr int kLd = KMAJ ? (C::BK + (C::PAIR ? 8 : 4)) : (ROWS + 4);
+  static constexpr int kElems = KMAJ ? ROWS * kLd : C::BK * (ROWS + 4);
 };
 
 // Streams one operand's BK-deep k chunks into shared memory.  Per-thread
@@ -89,6 +94,14 @@ template <class C, bool KMAJ, int ROWS>
 GPB_DEVINL double frag(const double* s, int row, int k) {
   using L = StageLayout<C, KMAJ, ROWS>;
   return KMAJ ? s[row * L::kLd + k] : s[k * L::kLd + row];
+}
+
+// values at k and k + 1 of one row (K-major: one 16-byte load)
+template <class C, bool KMAJ, int ROWS>
+GPB_DEVINL double2 frag2(const double* s, int row, int k) {
+  using L = StageLayout<C, KMAJ, ROWS>;
+  if constexpr (KMAJ) return *reinterpret_cast<const double2*>(s + row * L::kLd + k);
+  return make_double2(s[k * L::kLd + row], s[(k + 1) * L::kLd + row]);
 }
 
 template <class C, bool AK, bool BK, int EPI>
@@ -161,17 +174,36 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_grouped_kernel(cons
     cp_async_commit();
     const double* a_s = sA + (kc % C::STAGES) * LA::kElems;
     const double* b_s = sB + (kc % C::STAGES) * LB::kElems;
+    if constexpr (C::PAIR) {
 #pragma unroll
-    for (int k4 = 0; k4 < C::BK; k4 += 4) {
-      double af[FM], bf[FN];
+      for (int k8 = 0; k8 < C::BK; k8 += 8) {
+        double2 av[FM], bv[FN];
 #pragma unroll
-      for (int i = 0; i < FM; ++i) af[i] = frag<C, AK, GBM>(a_s, am0 + i * 8, k4 + t);
+        for (int i = 0; i < FM; ++i) av[i] = frag2<C, AK, GBM>(a_s, am0 + i * 8, k8 + 2 * t);
 #pragma unroll
-      for (int j = 0; j < FN; ++j) bf[j] = frag<C, BK, C::BN>(b_s, bn0 + j * 8, k4 + t);
+        for (int j = 0; j < FN; ++j) bv[j] = frag2<C, BK, C::BN>(b_s, bn0 + j * 8, k8 + 2 * t);
 #pragma unroll
-      for (int i = 0; i < FM; ++i)
+        for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+          for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[i].x, bv[j].x);
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[i].y, bv[j].y);
+      }
+    } else {
+#pragma unroll
+      for (int k4 = 0; k4 < C::BK; k4 += 4) {
+        double af[FM], bf[FN];
+#pragma unroll
+        for (int i = 0; i < FM; ++i) af[i] = frag<C, AK, GBM>(a_s, am0 + i * 8, k4 + t);
+#pragma unroll
+        for (int j = 0; j < FN; ++j) bf[j] = frag<C, BK, C::BN>(b_s, bn0 + j * 8, k4 + t);
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
     }
   }
   cp_async_wait<0>();
@@ -286,21 +318,28 @@ using Cfg4 = GemmCfg<4, 2, 16, 3, 64, 2>;  // 128x64 CTAs, 8 warps (32x32), 2 CT
 using Cfg5 = GemmCfg<2, 2, 16, 3, 64, 2>;  // 128x64 CTAs, 4 warps (64x32), 2 CTAs/SM
 using Cfg6 = GemmCfg<2, 4, 16, 5>;         // 8 warps, 5 stages
 using Cfg7 = GemmCfg<4, 2, 32, 2, 64, 2>;  // 128x64, 8 warps, BK 32, 2 stages, 2 CTAs/SM
+using Cfg8 = GemmCfg<4, 2, 16, 3, 64, 2, true>;  // Cfg4 with paired k loads
+using Cfg9 = GemmCfg<2, 2, 16, 3, 64, 2, true>;  // Cfg5 with paired k loads
 
 static int g_cfg = -1;
 
-// Default: two co-resident 128x64 CTAs per SM (measured fastest on B200 for
-// every shape of the hot path: tools/gemm_bench.cu, profiles/r01_gemm_configs.txt);
-// the 4-warp variant wins by ~1% on very long K.  GPB_GEMM_CFG forces one.
-static int gemm_cfg(const GemmParams& p) {
+// Default (tools/gemm_bench.cu, profiles/r01_gemm_configs.txt): two
+// co-resident 128x64 CTAs per SM with paired 16-byte k loads -- 4 warps of
+// 64x32 when K is long (>= 4096: the prediction sweep, +2.6% over unpaired),
+// else 8 warps of 32x32 when both operands are K-major (the Cholesky update),
+// else the unpaired 8-warp kernel.  GPB_GEMM_CFG forces one.
+static int gemm_cfg(const GemmParams& p, bool ak, bool bk) {
   if (g_cfg < 0) {
     const char* e = getenv("GPB_GEMM_CFG");
     g_cfg = e ? atoi(e) : 99;
-    if (g_cfg < 0 || (g_cfg > 7 && g_cfg != 99)) g_cfg = 99;
+    if (g_cfg < 0 || (g_cfg > 9 && g_cfg != 99)) g_cfg = 99;
   }
   if (g_cfg != 99) return g_cfg;
-  return p.max_k >= 4096 ? 5 : 4;
+  if (p.max_k >= 4096) return 9;
+  return (ak && bk) ? 8 : 4;
 }
+
+void gemm_force_config(int cfg) { g_cfg = cfg; }
 
 cudaError_t gemm_init_attributes() {
   cudaError_t e;
@@ -311,12 +350,14 @@ cudaError_t gemm_init_attributes() {
   if ((e = init_cfg<Cfg5>()) != cudaSuccess) return e;
   if ((e = init_cfg<Cfg6>()) != cudaSuccess) return e;
   if ((e = init_cfg<Cfg7>()) != cudaSuccess) return e;
+  if ((e = init_cfg<Cfg8>()) != cudaSuccess) return e;
+  if ((e = init_cfg<Cfg9>()) != cudaSuccess) return e;
   return init_cfg<Cfg3>();
 }
 
 cudaError_t launch_gemm(const GemmParams& p, bool a_kmajor, bool b_kmajor, int epi,
                         cudaStream_t s) {
-  switch (gemm_cfg(p)) {
+  switch (gemm_cfg(p, a_kmajor, b_kmajor)) {
     case 1: return dispatch<Cfg1>(p, a_kmajor, b_kmajor, epi, s);
     case 2: return dispatch<Cfg2>(p, a_kmajor, b_kmajor, epi, s);
     case 3: return dispatch<Cfg3>(p, a_kmajor, b_kmajor, epi, s);
@@ -324,6 +365,8 @@ cudaError_t launch_gemm(const GemmParams& p, bool a_kmajor, bool b_kmajor, int e
     case 5: return dispatch<Cfg5>(p, a_kmajor, b_kmajor, epi, s);
     case 6: return dispatch<Cfg6>(p, a_kmajor, b_kmajor, epi, s);
     case 7: return dispatch<Cfg7>(p, a_kmajor, b_kmajor, epi, s);
+    case 8: return dispatch<Cfg8>(p, a_kmajor, b_kmajor, epi, s);
+    case 9: return dispatch<Cfg9>(p, a_kmajor, b_kmajor, epi, s);
     default: return dispatch<Cfg0>(p, a_kmajor, b_kmajor, epi, s);
   }
 }

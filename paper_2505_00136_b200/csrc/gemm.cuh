@@ -54,5 +54,7 @@ struct GemmParams {
 cudaError_t launch_gemm(const GemmParams& p, bool a_kmajor, bool b_kmajor, int epi,
                         cudaStream_t stream);
 cudaError_t gemm_init_attributes();
+// tools only: force a kernel configuration (-1: GPB_GEMM_CFG / automatic)
+void gemm_force_config(int cfg);
 
 }  // namespace gpb

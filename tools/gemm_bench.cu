@@ -1,7 +1,10 @@
 // Standalone timing of the grouped DMMA GEMM (csrc/gemm.cu) on synthetic
 // device buffers: isolates kernel efficiency from the factorisation schedule.
 //   nvcc ... -o tools/gemm_bench tools/gemm_bench.cu paper_2505_00136_b200/csrc/gemm.cu
+#include <cmath>
 #include <cstdio>
+#include <cstring>
+#include <algorithm>
 #include <cstdlib>
 #include <vector>
 
@@ -32,6 +35,9 @@ int main(int argc, char** argv) {
       {"update K=1024, 1008 tiles", 1008, 1024, true, true, 1.0},
       {"long K=16384 KK, 64 tiles", 64, 16384, true, true, 0.0},
       {"long K=16384 K-MN (pred W), 64 tiles", 64, 16384, true, false, 1.0},
+      {"update K=2048 (chol G=4), 504 tiles", 504, 2048, true, true, 1.0},
+      {"K=2048 K-MN (pred W, early rows), 256 tiles", 256, 2048, true, false, 1.0},
+      {"K=4096 K-MN (pred W), 128 tiles", 128, 4096, true, false, 1.0},
   };
   double *A, *B, *C;
   size_t maxa = 0;
@@ -84,15 +90,30 @@ int main(int argc, char** argv) {
       best = std::min(best, ms);
     }
     const double flops = 2.0 * bi * bi * double(c.K) * c.ntiles;
-    // bitwise fingerprint of one launch from a fixed C (configs must agree)
+    // bitwise fingerprint of one launch from a fixed C, and the largest
+    // difference to the default configuration (cfg 4) relative to max |C|
     fill(C, size_t(c.ntiles) * bi2);
     launch_gemm(p, c.ak, c.bk, EPI_AXPBY, 0);
-    std::vector<unsigned long long> h(size_t(c.ntiles) * bi2);
+    std::vector<double> h(size_t(c.ntiles) * bi2), r(h.size());
     cudaMemcpy(h.data(), C, h.size() * 8, cudaMemcpyDeviceToHost);
     unsigned long long fp = 1469598103934665603ull;
-    for (auto v : h) fp = (fp ^ v) * 1099511628211ull;
-    printf("%-42s %8.3f ms  %6.2f TF/s  %s  fp=%016llx\n", c.name, best,
-           flops / (best * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()), fp);
+    for (double v : h) {
+      unsigned long long u;
+      memcpy(&u, &v, 8);
+      fp = (fp ^ u) * 1099511628211ull;
+    }
+    fill(C, size_t(c.ntiles) * bi2);
+    gemm_force_config(4);
+    launch_gemm(p, c.ak, c.bk, EPI_AXPBY, 0);
+    gemm_force_config(-1);
+    cudaMemcpy(r.data(), C, r.size() * 8, cudaMemcpyDeviceToHost);
+    double dmax = 0.0, cmax = 0.0;
+    for (size_t q = 0; q < h.size(); ++q) {
+      dmax = std::max(dmax, std::fabs(h[q] - r[q]));
+      cmax = std::max(cmax, std::fabs(r[q]));
+    }
+    printf("%-42s %8.3f ms  %6.2f TF/s  %s  fp=%016llx  vs cfg4 %.1e\n", c.name, best,
+           flops / (best * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()), fp, dmax / cmax);
   }
   return 0;
 }
