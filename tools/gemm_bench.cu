@@ -77,6 +77,7 @@ int main(int argc, char** argv) {
     p.a_ktile = p.b_ktile = int64_t(1) << 40;
     p.alpha = -1.0;
     p.beta = c.beta;
+    p.max_k = c.K;  // the library's automatic configuration choice uses it
     launch_gemm(p, c.ak, c.bk, EPI_AXPBY, 0);
     cudaDeviceSynchronize();
     float best = 1e30f;
