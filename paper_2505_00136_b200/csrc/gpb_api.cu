@@ -136,7 +136,7 @@ struct gpb_ctx {
 
 // One group of panels of the factorisation plan (build_chol_plan): job ranges
 // in the model's job array.
-constexpr int kMaxGroup = 4;
+constexpr int kMaxGroup = 8;
 struct CholGroup {
   int k0, np;
   int64_t trsm_off[kMaxGroup], trsm_cnt[kMaxGroup], in_off[kMaxGroup], in_cnt[kMaxGroup];
@@ -221,9 +221,10 @@ int apply_layout(gpb_model* m) {
   m->pm.b_user = static_cast<int>(lay[4]);
   m->bp = static_cast<int>(m->np_ / m->T);
   const char* pg = getenv("GPB_PANELS");
-  // G = 4 halves the C passes again (K = 4 bi: +0.5% at config 2, +1.5% at
-  // n = 65536); small grids keep G = 2 so the critical path stays short
-  m->G = std::max(1, std::min(kMaxGroup, pg ? atoi(pg) : (m->Ti >= 48 ? 4 : 2)));
+  // larger groups cut the C passes further (K = G bi): G = 4 gives +0.5% at
+  // config 2 and +1.5% at n = 65536, G = 6 another +0.4% there; small grids
+  // keep G = 2 so the critical path stays short
+  m->G = std::max(1, std::min(kMaxGroup, pg ? atoi(pg) : (m->Ti >= 96 ? 6 : m->Ti >= 48 ? 4 : 2)));
   return GPB_OK;
 }
 
@@ -333,8 +334,8 @@ int alloc_model_buffers(gpb_model* m) {
   return GPB_OK;
 }
 
-// Cholesky plan: panels are factored in groups of G (GPB_PANELS; default 4 for
-// T >= 48 internal tiles, else 2)
+// Cholesky plan: panels are factored in groups of G (GPB_PANELS; default 6 for
+// T >= 96 internal tiles, 4 for T >= 48, else 2)
 // and the trailing matrix is updated once per group with K = G * bi, which
 // halves the read-modify-write passes over C at G = 2.  For group s
 // (panels k0 .. k0+G'-1), with the panels solved into scratch set s % 2:
