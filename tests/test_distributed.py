@@ -167,3 +167,54 @@ def test_bench_distributed_branch_two_ranks_one_gpu():
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["scaling"] == "weak" and line["value"] > 0
     assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+
+
+def _nccl_one_rank(port, out_q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        import torch
+
+        import paper_2505_00136_b200 as gpb
+        from paper_2505_00136_b200.distributed import DistributedGP
+
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        rt = gpb.start_runtime(gpb.RuntimeConfig(device=0))
+        train, test = gpb.make_msd_dataset(4096, 512, 8, seed=5)
+        model = DistributedGP(train, gpb.KernelParams(1.1, 0.9, 0.2), 8)
+        ll = model.log_likelihood()
+        pv = model.predict_variance(test)
+        fc = model.predict_with_full_cov(test)
+        grads = model.loss_gradients()
+        model.close()
+        ref = gpb.GPModel(train, gpb.KernelParams(1.1, 0.9, 0.2), 8)
+        rpv = ref.predict_variance(test)
+        out_q.put((ll, ref.log_likelihood(), pv.mean, rpv.mean, pv.variance, rpv.variance,
+                   np.diagonal(fc.full_covariance), grads, ref.loss_gradients()))
+        rt.stop()
+        dist.destroy_process_group()
+    except BaseException:
+        import traceback
+
+        out_q.put(traceback.format_exc())
+        raise
+
+
+@pytest.mark.gpu
+def test_nccl_backend_one_rank_matches_single_gpu():
+    """The collectives through NCCL (world size 1: every call is a real NCCL
+    collective on the library's streams) against the fused single-GPU model."""
+    from oracle.tiled_gp import rel_fro
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_one_rank, args=(_free_port(), q))
+    p.start()
+    res = q.get(timeout=300)
+    p.join(timeout=60)
+    assert not isinstance(res, str), res
+    ll, rll, mean, rmean, var, rvar, fdiag, grads, rgrads = res
+    assert abs(ll - rll) <= 1e-10 * abs(rll)
+    assert rel_fro(mean, rmean) <= 1e-9 and rel_fro(var, rvar) <= 1e-10
+    assert rel_fro(fdiag, rvar) <= 1e-10
+    assert rel_fro(np.array(grads), np.array(rgrads)) <= 1e-10

@@ -3,7 +3,7 @@ import os, sys, time
 sys.path.insert(0, '.')
 os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29631")
 import numpy as np, torch, torch.distributed as dist
-dist.init_process_group("gloo", rank=0, world_size=1)
+dist.init_process_group(os.environ.get("BACKEND", "gloo"), rank=0, world_size=1, **({"device_id": __import__("torch").device("cuda", 0)} if os.environ.get("BACKEND") == "nccl" else {}))
 import paper_2505_00136_b200 as gpb
 from paper_2505_00136_b200.distributed import DistributedGP
 n = int(os.environ.get("N", 32768)); d = int(os.environ.get("D", 128)); T = int(os.environ.get("T", 64)); m = int(os.environ.get("M", 4096))
