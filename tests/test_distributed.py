@@ -152,6 +152,13 @@ def test_two_ranks_one_gpu_device_kernels():
 
 
 @pytest.mark.gpu
+def test_four_ranks_2x2_grid_one_gpu_device_kernels():
+    """P = 2 process rows: panel slots i // P, per-row broadcasts and the
+    tiled-k trailing update addresses on the real kernels."""
+    _check(_run(4, "dense", device=True), "dense")
+
+
+@pytest.mark.gpu
 def test_bench_distributed_branch_two_ranks_one_gpu():
     """bench.py's N>1 path end to end (torchrun, 2 ranks on cuda:0, gloo)."""
     import json
