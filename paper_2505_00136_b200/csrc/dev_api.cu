@@ -124,32 +124,27 @@ int gpb_layout(int64_t n, int64_t tiles_per_dim, int64_t out[6]) {
   if (tiles_per_dim < 1 || n < 1 || n % tiles_per_dim != 0)
     return gpb_plugin_fail(GPB_TILING, "tiles_per_dim must divide n");
   const int64_t b = n / tiles_per_dim;
-  int64_t bp = (b + kTileAlign - 1) / kTileAlign * kTileAlign;
-  int64_t bi = 0;
+  // Results are tiling-invariant to round-off, so the internal tile size is
+  // free: 512 from n = 4096 up, else 256 (128 for n <= 128), or GPB_TILE.
+  // When 128 divides the user tile the internal tile must divide n;
+  // otherwise n is padded once, at the end, with decoupled identity rows
+  // (not per user tile: tiny user tiles would inflate the problem).
   const char* env = getenv("GPB_TILE");
-  if (b % kTileAlign == 0) {
-    const int64_t want = env ? atoll(env) : (n >= 4096 ? 512 : 256);
-    for (int64_t c : {want, int64_t(512), int64_t(256), int64_t(128)})
-      if (c > 0 && c % kTileAlign == 0 && n % c == 0) {
-        bi = c;
-        break;
-      }
-    bp = b;
-  }
-  if (!bi)
-    for (int64_t c : {512, 384, 256, 128})
-      if (bp % c == 0) {
-        bi = c;
-        break;
-      }
-  const int64_t np_ = tiles_per_dim * bp;
+  const int64_t want = env ? atoll(env) : (n >= 4096 ? 512 : n > 128 ? 256 : 128);
   const bool dense = (b % kTileAlign == 0);
-  out[0] = bi;                                   // internal tile size
-  out[1] = np_ / bi;                             // internal tiles per dimension
-  out[2] = np_;                                  // padded order
-  out[3] = dense ? std::min<int64_t>(np_, int64_t(1) << 30) : bp;  // PadMap.bp_user
-  out[4] = dense ? out[3] : b;                   // PadMap.b_user
-  out[5] = b;                                    // user tile size
+  int64_t bi = 0;
+  for (int64_t c : {want, int64_t(512), int64_t(256), int64_t(128)})
+    if (c > 0 && c % kTileAlign == 0 && (!dense || n % c == 0)) {
+      bi = c;
+      break;
+    }
+  const int64_t np_ = dense ? n : (n + bi - 1) / bi * bi;
+  out[0] = bi;                                        // internal tile size
+  out[1] = np_ / bi;                                  // internal tiles per dimension
+  out[2] = np_;                                       // padded order
+  out[3] = std::min<int64_t>(np_, int64_t(1) << 30);  // PadMap.bp_user: one block
+  out[4] = dense ? out[3] : n;                        // PadMap.b_user: real rows P < n
+  out[5] = b;                                         // user tile size
   return GPB_OK;
 }
 

@@ -148,7 +148,7 @@ struct gpb_model {
   gpb_ctx* ctx = nullptr;
   uint64_t gen = 0;
   int64_t n = 0, d = 0, T = 0;
-  int b = 0, bp = 0, bi = 0, Ti = 0;
+  int b = 0, bi = 0, Ti = 0;
   int64_t np_ = 0;
   PadMap pm{};
   double l = 1.0, nu = 1.0, s2 = 0.1;
@@ -207,10 +207,10 @@ int check_live(gpb_model* m) {
   return GPB_OK;
 }
 
-// Internal layout (dev_api.cu gpb_layout): user tiles padded to multiples of
-// 128 with decoupled identity; when no padding is needed the internal tile
-// size is a free parameter (results are tiling-invariant to round-off,
-// test_acceptance.py:135-169).
+// Internal layout (dev_api.cu gpb_layout): the internal tile size is a free
+// parameter (results are tiling-invariant to round-off,
+// test_acceptance.py:135-169); when 128 does not divide the user tile, n is
+// padded once at the end with decoupled identity rows.
 int apply_layout(gpb_model* m) {
   int64_t lay[6];
   if (int s = gpb_layout(m->n, m->T, lay)) return s;
@@ -219,7 +219,6 @@ int apply_layout(gpb_model* m) {
   m->np_ = lay[2];
   m->pm.bp_user = static_cast<int>(lay[3]);
   m->pm.b_user = static_cast<int>(lay[4]);
-  m->bp = static_cast<int>(m->np_ / m->T);
   const char* pg = getenv("GPB_PANELS");
   // larger groups cut the C passes further (K = G bi): G = 4 gives +0.5% at
   // config 2 and +1.5% at n = 65536, G = 6 another +0.4% there; small grids

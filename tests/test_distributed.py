@@ -26,7 +26,7 @@ def _free_port():
 
 def _case(kind):
     rng = np.random.default_rng(11)
-    if kind == "padded":  # b = 100 -> tiles padded to 128 (6 x 6 grid)
+    if kind == "padded":  # b = 100: n padded once to 640 (5 x 5 grid of 128)
         n, t, d, m = 600, 6, 3, 37
     else:  # b = 128, no padding (GPB_TILE=128 forces an 8 x 8 grid)
         n, t, d, m = 1024, 8, 4, 50
