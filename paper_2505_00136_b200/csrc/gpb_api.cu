@@ -352,10 +352,24 @@ int build_chol_plan(gpb_model* m) {
   double* D = m->Dinv.as<double>();
   std::vector<GemmJob> jobs;
   m->groups.clear();
-  for (int k0 = 0, s = 0; k0 < Ti; k0 += G, ++s) {
+  // group sizes: G, shrinking near the end where the trailing update no
+  // longer hides the group's critical path (GPB_TAIL, default 8: at most
+  // r / 8 panels when r tiles remain; 0 = fixed G): +0.5% at config 2
+  std::vector<int> sizes;
+  {
+    const char* te = getenv("GPB_TAIL");
+    const int tail = te ? atoi(te) : 8;
+    for (int k0 = 0; k0 < Ti;) {
+      int g = std::min(G, Ti - k0);
+      if (tail > 0) g = std::max(1, std::min(g, (Ti - k0) / tail));
+      sizes.push_back(g);
+      k0 += g;
+    }
+  }
+  for (int k0 = 0, s = 0; k0 < Ti; k0 += sizes[s], ++s) {
     CholGroup grp{};
     grp.k0 = k0;
-    grp.np = std::min(G, Ti - k0);
+    grp.np = sizes[s];
     double* set = m->scratch.as<double>() + int64_t(s % 2) * G * pstride;
     auto panel_tile = [&](int g, int i) { return set + g * pstride + int64_t(i - (k0 + g) - 1) * bi2; };
     for (int g = 0; g < grp.np; ++g) {
@@ -386,7 +400,8 @@ int build_chol_plan(gpb_model* m) {
       grp.in_cnt[g] = jobs.size() - grp.in_off[g];
     }
     // trailing updates with the whole group (tiled-k walk across the G panels)
-    const int c_next = k0 + grp.np, c_upd = std::min(Ti, c_next + G);
+    const int c_next = k0 + grp.np;
+    const int c_upd = std::min(Ti, c_next + (s + 1 < static_cast<int>(sizes.size()) ? sizes[s + 1] : 0));
     auto add_upd = [&](int jlo, int jhi) {
       for (int i = jlo; i < Ti; ++i)
         for (int jj = jlo; jj <= std::min(i, jhi - 1); ++jj) {
