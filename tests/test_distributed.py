@@ -152,9 +152,12 @@ def test_two_ranks_one_gpu_device_kernels():
 
 
 @pytest.mark.gpu
-def test_four_ranks_2x2_grid_one_gpu_device_kernels():
+@pytest.mark.parametrize("panels", ["2", "3"])
+def test_four_ranks_2x2_grid_one_gpu_device_kernels(monkeypatch, panels):
     """P = 2 process rows: panel slots i // P, per-row broadcasts and the
-    tiled-k trailing update addresses on the real kernels."""
+    tiled-k trailing update addresses on the real kernels; 3-panel groups
+    leave a partial last group (T = 8)."""
+    monkeypatch.setenv("GPB_DIST_PANELS", panels)
     _check(_run(4, "dense", device=True), "dense")
 
 
