@@ -6,14 +6,17 @@
 // triangular solve of the hot path (panel TRSM tiles.py:140-146, vector
 // solves tiles.py:170-180, panel solves tiles.py:182-185) into DMMA products.
 //
-// Blocked Cholesky with 32-column panels.  Per panel p:
-//   A (all warps)   last contribution (panel p-1) to panel p, DMMA warp tiles
-//   B (warp 0)      factor + invert the 32x32 diagonal block -- the serial
-//                   pivot chain, kept in registers / shuffles
-//     (other warps) concurrently: panel p-1's contribution to every trailing
-//                   32-block right of panel p (right-looking) and block row p-1 of the inverse
-//                   Dinv = L^-1 (TRTRI interleaved with the factorisation)
-//   C (all warps)   solve the rows below the diagonal block (x Li^T)
+// Blocked Cholesky with 32-column panels.  Per panel p, two phases:
+//   B (CTA 0 warp 0) factor the 32x32 diagonal block -- the serial pivot
+//                   chain in registers, each new column broadcast through
+//                   shared memory;
+//     (CTA 0 warp 1) invert it row by row as the chain publishes rows;
+//     (other warps) panel p-1's rank-32 update of every 32-block below the
+//                   diagonal block (right-looking) and the TRTRI of Dinv
+//                   (finalise block row p-1, accumulate term p-2);
+//   C (all warps)   solve the rows below the diagonal block (x Li^T); the
+//                   warp of row block p+1 also applies panel p to the next
+//                   diagonal block, so B(p+1) can start at once;
 // so the DMMA work of the update and of TRTRI runs while the pivot chain
 // advances.  The warp jobs of every phase are dealt over all warps of the
 // cluster and the phases are separated by cluster barriers (release/acquire
@@ -126,10 +129,10 @@ GPB_DEVINL void store_acc(double* c, int64_t ldc, const double (&acc)[4][4][2], 
 
 // Right-looking TRTRI of the tile, X = L^-1 by 32-blocks:
 //   X_IJ = -X_II sum_{K=J}^{I-1} L_IK X_KJ.
-// Block (I, J) of D accumulates -sum L_IK X_KJ one K per panel (K = p-2 in
-// phase A(p), once row K of X is final), and row I is finalised in phase
-// B(I+1) as X_II * D_IJ: every job has K = 32, so no single warp carries a
-// long dependency chain.
+// Block (I, J) of D accumulates -sum L_IK X_KJ one K per panel (term K in
+// phase C(K+1) for row K+1 and in B(K+2) for the rows below, once row K of X
+// is final), and row I is finalised in phase B(I+1) as X_II * D_IJ: every
+// job has K = 32, so no single warp carries a long dependency chain.
 GPB_DEVINL void trtri_acc(const double* T, double* D, int bi, int I, int J, int K, int g, int t) {
   double acc[4][4][2];
   zero_acc(acc);
@@ -196,36 +199,15 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
 
   for (int p = 0; p < P; ++p) {
     const int c0 = p * NB;
-    // A: last contribution (panel p-1) to panel p, rows >= c0; and the
-    // TRTRI term K = p-2 of row I = p-1 (finalised in B(p)); the same term of
-    // the later rows I >= p is accumulated by the job warps of B(p)
-    {
-      const int na = (factor && p > 0) ? P - p : 0;
-      const int nj = p >= 2 ? p - 1 : 0;
-      const int nw = nj;
-      for (int q = warp; q < na + nw; q += GW) {
-        if (q < na) {
-          const int rb = p + q;
-          double acc[4][4][2];
-          zero_acc(acc);
-          warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi + c0 - NB, bi,
-                  T + static_cast<int64_t>(c0) * bi + c0 - NB, bi, NB, g, t);
-          store_acc(T + static_cast<int64_t>(rb) * NB * bi + c0, bi, acc, g, t, false, 1.0);
-        } else {
-          const int w = q - na;
-          trtri_acc(T, D, bi, p - 1 + w / nj, w % nj, p - 2, g, t);
-        }
-      }
-    }
-    cluster_barrier(clustered);
     PROF_MARK(0)
     if (!(lead && lw < 2)) {
       // B, job warps (CTAs 1.. when clustered, else warps 2..7), dealt
-      // round-robin: panel p-1's rank-32 contribution to every trailing
-      // 32-block (rb, cb), p+1 <= cb <= rb (right-looking; panel p gets it
-      // in phase A), and the finalisation of block row p-1 of the inverse
-      const int m = P - p - 1;
-      const int pre = (factor && p > 0) ? m * (m + 1) / 2 : 0;
+      // round-robin: panel p-1's rank-32 contribution to every 32-block
+      // (rb, cb), p <= cb <= rb, below the diagonal block (right-looking;
+      // the diagonal block (p, p) got it in C(p-1)), the finalisation of
+      // block row p-1 of the inverse, and the TRTRI term K = p-2 of rows I >= p
+      const int m = P - p;  // block rows p .. P-1; (p, p) excluded
+      const int pre = (factor && p > 0) ? m * (m + 1) / 2 - 1 : 0;
       const int inv = (p >= 2) ? p - 1 : 0;  // blocks J = 0..p-2 of row I = p-1
       const int accn = (p >= 2) ? (P - p) * (p - 1) : 0;  // term K = p-2 of rows I >= p
       // clustered: CTA 0 keeps only the pivot chain so its SMSPs are not
@@ -234,10 +216,11 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
       const int nwk = clustered ? GW - NW : NW - 2;
       for (int q = (w0 >= 0 ? w0 : pre + inv + accn); q < pre + inv + accn; q += nwk) {
         if (q < pre) {
-          int rr = static_cast<int>((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
-          while (rr * (rr + 1) / 2 > q) --rr;
-          while ((rr + 1) * (rr + 2) / 2 <= q) ++rr;
-          const int rb = p + 1 + rr, cb = p + 1 + (q - rr * (rr + 1) / 2);
+          const int qq = q + 1;  // skip (p, p)
+          int rr = static_cast<int>((sqrtf(8.0f * qq + 1.0f) - 1.0f) * 0.5f);
+          while (rr * (rr + 1) / 2 > qq) --rr;
+          while ((rr + 1) * (rr + 2) / 2 <= qq) ++rr;
+          const int rb = p + rr, cb = p + (qq - rr * (rr + 1) / 2);
           double acc[4][4][2];
           zero_acc(acc);
           warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi + c0 - NB, bi,
@@ -352,21 +335,37 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
     PROF_MARK(1)
     if (*reinterpret_cast<volatile int*>(a.info) >= 0) return;  // set by CTA 0 above
     // C: below-diagonal panel rows, L[r][c0:c0+32] = T[r][c0:c0+32] * Li^T
-    // (Li read back from the diagonal block of D, written by CTA 0)
-    for (int rb = p + 1 + warp; rb < (factor ? P : 0); rb += GW) {
-      double acc[4][4][2];
-      zero_acc(acc);
-      double* blk = T + static_cast<int64_t>(rb) * NB * bi + c0;
-      warp_nt(acc, blk, bi, D + static_cast<int64_t>(c0) * bi + c0, bi, NB, g, t);
-      __syncwarp();
-      store_acc(blk, bi, acc, g, t, true, 1.0);
+    // (Li read back from the diagonal block of D, written by CTA 0); the warp
+    // of row block p+1 then applies panel p to the next diagonal block
+    // (p+1, p+1), which is all the chain of B(p+1) needs.  Also the TRTRI
+    // term K = p-1 of row I = p, which B(p+1) finalises.
+    {
+      const int nt = factor ? P - p - 1 : 0;
+      const int na = p >= 1 ? p : 0;  // J = 0..p-1
+      for (int q = warp; q < nt + na; q += GW) {
+        if (q < nt) {
+          const int rb = p + 1 + q;
+          double acc[4][4][2];
+          zero_acc(acc);
+          double* blk = T + static_cast<int64_t>(rb) * NB * bi + c0;
+          warp_nt(acc, blk, bi, D + static_cast<int64_t>(c0) * bi + c0, bi, NB, g, t);
+          __syncwarp();
+          store_acc(blk, bi, acc, g, t, true, 1.0);
+          if (q == 0) {  // (p+1, p+1) -= X X^T with X = the block just stored
+            __syncwarp();
+            zero_acc(acc);
+            warp_nt(acc, blk, bi, blk, bi, NB, g, t);
+            store_acc(blk + NB, bi, acc, g, t, false, 1.0);
+          }
+        } else {
+          trtri_acc(T, D, bi, p, q - nt, p - 1, g, t);
+        }
+      }
     }
     cluster_barrier(clustered);
     PROF_MARK(2)
   }
-  // last block row of the inverse: its last term (K = P-2), then X_II * D_IJ
-  for (int J = warp; J < P - 1; J += GW) trtri_acc(T, D, bi, P - 1, J, P - 2, g, t);
-  cluster_barrier(clustered);
+  // last block row of the inverse (its last term came in C(P-1)): X_II * D_IJ
   for (int J = warp; J < P - 1; J += GW) trtri_fin(D, bi, P - 1, J, g, t);
   PROF_MARK(3)
   // zero strictly-upper 32-blocks of L and Dinv (lower-triangular results)
