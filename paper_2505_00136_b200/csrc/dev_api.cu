@@ -234,6 +234,36 @@ int gpb_dev_gemm_tiled(gpb_ctx* ctx, void* stream, const gpb_gemm_job* jobs, int
   p.alpha = alpha;
   p.beta = beta;
   p.max_k = maxk;
+  // TMA views: the operands' jobs come from arbitrary (torch) allocations, so
+  // the view starts at the lowest pointer and is used only if every job's
+  // block sits inside one row of the ld-wide view
+  auto view = [&](bool a_side, const double** base, int64_t* extent) {
+    const bool km = a_side ? a_kmajor != 0 : b_kmajor != 0;
+    const int64_t ld = a_side ? lda : ldb, rows = GBM;  // rows of one block (GBM == GBN)
+    const int64_t kt = a_side ? p.a_ktile : p.b_ktile, ks = a_side ? p.a_kstride : p.b_kstride;
+    const double* lo = nullptr;
+    for (const GemmJob& g : gj) {
+      const double* q = a_side ? g.A : g.B;
+      if (g.K > 0 && (!lo || q < lo)) lo = q;
+    }
+    if (!lo || ld <= 0) return;
+    int64_t hi = 0;
+    for (const GemmJob& g : gj) {
+      if (g.K <= 0) continue;
+      const int64_t off = (a_side ? g.A : g.B) - lo;
+      const int64_t col = off % ld;
+      const bool tiled = kt < (int64_t(1) << 30);
+      const int64_t kspan = tiled ? std::min<int64_t>(g.K, kt) : g.K;
+      const int64_t mspan = (a_side ? p.mblk : p.nblk) * rows;
+      if (km ? col + kspan > ld : col + mspan > ld) return;
+      const int64_t span = km ? (mspan * ld + (tiled ? (g.K / kt) * ks : 0)) : ((g.K + 1) * ld);
+      hi = std::max(hi, off + span);
+    }
+    *base = lo;
+    *extent = hi;
+  };
+  view(true, &p.a_base, &p.a_extent);
+  view(false, &p.b_base, &p.b_extent);
   DEV_TRY(launch_gemm(p, a_kmajor != 0, b_kmajor != 0, EPI_AXPBY, st));
   return GPB_OK;
 }

@@ -328,12 +328,16 @@ static int g_cfg = -1;
 // 64x32 when K is long (>= 4096: the prediction sweep, +2.6% over unpaired),
 // else 8 warps of 32x32 when both operands are K-major (the Cholesky update),
 // else the unpaired 8-warp kernel.  GPB_GEMM_CFG forces one.
-static int gemm_cfg(const GemmParams& p, bool ak, bool bk) {
+static void resolve_cfg() {
   if (g_cfg < 0) {
     const char* e = getenv("GPB_GEMM_CFG");
     g_cfg = e ? atoi(e) : 99;
     if (g_cfg < 0 || (g_cfg > 9 && g_cfg != 99)) g_cfg = 99;
   }
+}
+
+static int gemm_cfg(const GemmParams& p, bool ak, bool bk) {
+  resolve_cfg();
   if (g_cfg != 99) return g_cfg;
   if (p.max_k >= 4096) return 9;
   return (ak && bk) ? 8 : 4;
@@ -357,6 +361,12 @@ cudaError_t gemm_init_attributes() {
 
 cudaError_t launch_gemm(const GemmParams& p, bool a_kmajor, bool b_kmajor, int epi,
                         cudaStream_t s) {
+  resolve_cfg();
+  if (g_cfg == 99) {  // forced cp.async configurations bypass TMA
+    bool used = false;
+    const cudaError_t e = launch_gemm_tma(p, a_kmajor, b_kmajor, epi, s, &used);
+    if (used || e != cudaSuccess) return e;
+  }
   switch (gemm_cfg(p, a_kmajor, b_kmajor)) {
     case 1: return dispatch<Cfg1>(p, a_kmajor, b_kmajor, epi, s);
     case 2: return dispatch<Cfg2>(p, a_kmajor, b_kmajor, epi, s);

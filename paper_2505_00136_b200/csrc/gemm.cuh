@@ -48,12 +48,32 @@ struct GemmParams {
   double alpha, beta;
   int64_t aux_ld;            // EPI_SUMSQ: stride between 128-row partial rows
   int64_t max_k;             // largest job K (kernel-configuration hint), 0 if unknown
+  // TMA path (gemm_tma.cu): the buffers every job's A / B pointer lies in and
+  // their extents in doubles from those bases; null = cp.async kernel only
+  const double* a_base;
+  int64_t a_extent;
+  const double* b_base;
+  int64_t b_extent;
+};
+
+// one operand of the TMA kernel: a job pointer p maps to row (p - base) / ld,
+// column (p - base) % ld of the tensor map; a tiled-k walk advances kt_rows
+// rows per ktile-deep k tile
+struct TmaOperand {
+  const double* base;
+  int64_t ld, ktile, kt_rows;
 };
 
 // Host launcher (gemm.cu).  a_kmajor / b_kmajor choose operand layouts.
 cudaError_t launch_gemm(const GemmParams& p, bool a_kmajor, bool b_kmajor, int epi,
                         cudaStream_t stream);
 cudaError_t gemm_init_attributes();
+// TMA-fed kernel; *used = false when the launch does not qualify (no operand
+// bases, unaligned views, GPB_GEMM_TMA=0) and nothing was launched
+cudaError_t launch_gemm_tma(const GemmParams& p, bool a_kmajor, bool b_kmajor, int epi,
+                            cudaStream_t stream, bool* used);
+// tools only: 0 off, 1 four consumer warps, 2 eight, 3 automatic
+void gemm_force_tma(int mode);
 // tools only: force a kernel configuration (-1: GPB_GEMM_CFG / automatic)
 void gemm_force_config(int cfg);
 

@@ -245,6 +245,19 @@ GemmParams base_params(const GemmJob* jobs, int njobs, int mblk, int nblk, int64
   return p;
 }
 
+// TMA operand views (gemm_tma.cu): the buffers every A / B pointer of the
+// launch lies in; launches without them run the cp.async kernel
+GemmParams views(GemmParams p, const void* a, size_t a_bytes, const void* b, size_t b_bytes) {
+  p.a_base = static_cast<const double*>(a);
+  p.a_extent = static_cast<int64_t>(a_bytes / sizeof(double));
+  p.b_base = static_cast<const double*>(b);
+  p.b_extent = static_cast<int64_t>(b_bytes / sizeof(double));
+  return p;
+}
+GemmParams views(const GemmParams& p, const DevBuf& a, const DevBuf& b) {
+  return views(p, a.p, a.bytes, b.p, b.bytes);
+}
+
 enum KernelClass { KC_GEMM = 0, KC_POTRF = 1, KC_SEK = 2, KC_SOLVE = 3, KC_OTHER = 4 };
 
 cudaEvent_t prof_event(gpb_model* m) {
@@ -532,6 +545,7 @@ int ensure_factor(gpb_model* m) {
   CUDA_TRY(cudaEventRecord(ev_upd[ng], m->st));
   CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[ng], 0));
   auto walk = [&](GemmParams p) {  // [X]_i: tiled-k walk across the group's panels
+    p = views(p, m->scratch, m->scratch);
     p.a_ktile = p.b_ktile = bi;
     p.a_kstride = p.b_kstride = pstride - bi2;
     return p;
@@ -559,11 +573,13 @@ int ensure_factor(gpb_model* m) {
         CUDA_TRY(launch_potrf(a, m->crit));
       }
       ++m->launches;
-      GemmParams tp = base_params(jobs + grp.trsm_off[g], static_cast<int>(grp.trsm_cnt[g]), nb, 1,
-                                  bi, bi, bi, 1.0, 0.0);
+      GemmParams tp = views(base_params(jobs + grp.trsm_off[g], static_cast<int>(grp.trsm_cnt[g]), nb, 1,
+                                        bi, bi, bi, 1.0, 0.0),
+                            m->L, m->Dinv);
       GPB_TRY(gemm(m, tp, true, true, EPI_AXPBY, grp.trsm_fl[g], m->crit));
-      GemmParams ip = base_params(jobs + grp.in_off[g], static_cast<int>(grp.in_cnt[g]), nb, nb, bi,
-                                  bi, bi, -1.0, 1.0);
+      GemmParams ip = views(base_params(jobs + grp.in_off[g], static_cast<int>(grp.in_cnt[g]), nb, nb, bi,
+                                        bi, bi, -1.0, 1.0),
+                            m->scratch, m->scratch);
       GPB_TRY(gemm(m, ip, true, true, EPI_AXPBY, grp.in_fl[g], m->crit));
     }
     CUDA_TRY(cudaEventRecord(ev_panel[s], m->crit));
@@ -737,12 +753,13 @@ int loss_gradients(gpb_model* m, double out[3]) {
     CUDA_TRY(cudaMemcpyAsync(X + h_tri_cm(i, i, Ti) * bi2, D + int64_t(i) * bi2,
                              sizeof(double) * bi2, cudaMemcpyDeviceToDevice, m->st));
   for (int i = 1; i < Ti; ++i) {
-    GemmParams w = base_params(jobs + m->invw_off[i], i, nb, nb, bi, bi, bi, 1.0, 0.0);
+    GemmParams w = views(base_params(jobs + m->invw_off[i], i, nb, nb, bi, bi, bi, 1.0, 0.0), m->L, m->X);
     w.a_ktile = bi;
     w.a_kstride = bi2;
     w.max_k = int64_t(i) * bi;
     GPB_TRY(gemm(m, w, true, false, EPI_AXPBY, gemm_flops(int64_t(nb) * nb, int64_t(bi) * i * (i + 1) / 2)));
-    GemmParams x = base_params(jobs + m->invx_off[i], i * nb, 1, nb, bi, bi, bi, -1.0, 0.0);
+    GemmParams x = views(base_params(jobs + m->invx_off[i], i * nb, 1, nb, bi, bi, bi, -1.0, 0.0), m->Dinv,
+                         m->Wg);
     GPB_TRY(gemm(m, x, true, false, EPI_AXPBY,
                  gemm_flops(int64_t(i) * nb, int64_t(GBM) * nb * (nb + 1) / 2)));
   }
@@ -751,8 +768,9 @@ int loss_gradients(gpb_model* m, double out[3]) {
   const int64_t nblk = ntiles * (bi / kSekBlock) * (bi / kSekBlock);
   if (tl || tv) {
     // K^-1 = X^T X, lower tiles (model.py:362-380)
-    GemmParams kp = base_params(jobs + m->kinv_off, static_cast<int>(m->kinv_cnt), nb, nb, bi, bi,
-                                bi, 1.0, 0.0);
+    GemmParams kp = views(base_params(jobs + m->kinv_off, static_cast<int>(m->kinv_cnt), nb, nb, bi, bi,
+                                      bi, 1.0, 0.0),
+                          m->X, m->X);
     kp.max_k = int64_t(Ti) * bi;
     GPB_TRY(gemm(m, kp, false, false, EPI_AXPBY,
                  gemm_flops(int64_t(nb) * nb, int64_t(bi) * Ti * (Ti + 1) * (Ti + 2) / 6)));
@@ -899,11 +917,12 @@ int grad_partial(gpb_model* m, const int* cols, int ncols, double out[3]) {
   for (int i = R0; i < Ti; ++i) {
     const int a = active(i);
     const int64_t k = i - R0;
-    GemmParams v = base_params(dj + fd_off[k], nb, 1, a * nbt, bi, w, w, 1.0, 0.0);
+    GemmParams v = views(base_params(dj + fd_off[k], nb, 1, a * nbt, bi, w, w, 1.0, 0.0), m->Dinv, m->gp_panel);
     GPB_TRY(gemm(m, v, true, false, EPI_AXPBY, gemm_flops(a * nbt, int64_t(GBM) * nb * (nb + 1) / 2)));
     CUDA_TRY(cudaMemcpyAsync(G + k * bi * w, H, row_bytes, cudaMemcpyDeviceToDevice, m->st));
     if (i + 1 < Ti) {
-      GemmParams u = base_params(dj + fu_off[k], Ti - 1 - i, nb, a * nbt, bi, w, w, -1.0, 1.0);
+      GemmParams u = views(base_params(dj + fu_off[k], Ti - 1 - i, nb, a * nbt, bi, w, w, -1.0, 1.0), m->L,
+                           m->gp_h);
       u.max_k = bi;
       GPB_TRY(gemm(m, u, true, false, EPI_AXPBY,
                    gemm_flops(int64_t(Ti - 1 - i) * nb * a * nbt, bi)));
@@ -912,14 +931,14 @@ int grad_partial(gpb_model* m, const int* cols, int ncols, double out[3]) {
   for (int i = Ti - 1; i >= R0; --i) {
     const int a = active(i);
     const int64_t s = Ti - 1 - i;
-    GemmParams h = base_params(dj + bd_off[s], nb, 1, a * nbt, bi, w, w, 1.0, 0.0);
+    GemmParams h = views(base_params(dj + bd_off[s], nb, 1, a * nbt, bi, w, w, 1.0, 0.0), m->Dinv, m->gp_panel);
     GPB_TRY(gemm(m, h, false, false, EPI_AXPBY, gemm_flops(a * nbt, int64_t(GBM) * nb * (nb + 1) / 2)));
     CUDA_TRY(cudaMemcpyAsync(G + int64_t(i - R0) * bi * w, H, row_bytes, cudaMemcpyDeviceToDevice,
                              m->st));
     if (i > R0) {
       int64_t blocks = 0;
       for (int q = R0; q < i; ++q) blocks += int64_t(nb) * active(q) * nbt;
-      GemmParams u = base_params(dj + bu_off[s], i - R0, nb, a * nbt, bi, w, w, -1.0, 1.0);
+      GemmParams u = views(base_params(dj + bu_off[s], i - R0, nb, a * nbt, bi, w, w, -1.0, 1.0), m->L, m->gp_h);
       u.max_k = bi;
       GPB_TRY(gemm(m, u, false, false, EPI_AXPBY, gemm_flops(blocks, bi)));
     }
@@ -1023,17 +1042,18 @@ int predict_chunk(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var,
     PhaseTimer pt(m, 4);
     const GemmJob* jobs = m->pred_jobs.as<GemmJob>();
     for (int i = 0; i < Ti; ++i) {
-      GemmParams w = base_params(jobs + int64_t(i) * (1 + bi / GBM), 1, bi / GBM,
-                                 static_cast<int>(mcp / GBN), bi, mcp,
-                                 mcp, -1.0, 1.0);
+      GemmParams w = views(base_params(jobs + int64_t(i) * (1 + bi / GBM), 1, bi / GBM,
+                                       static_cast<int>(mcp / GBN), bi, mcp, mcp, -1.0, 1.0),
+                           m->L, m->Bv);
       w.a_ktile = bi;
       w.a_kstride = int64_t(bi) * bi;
       w.max_k = int64_t(i) * bi;
       const int64_t blocks = int64_t(bi / GBM) * (mcp / GBN);
       GPB_TRY(gemm(m, w, true, false, EPI_AXPBY, gemm_flops(blocks, int64_t(i) * bi)));
       const int nbr = bi / GBM;
-      GemmParams v = base_params(jobs + int64_t(i) * (1 + nbr) + 1, nbr, 1,
-                                 static_cast<int>(mcp / GBN), bi, mcp, mcp, 1.0, 0.0);
+      GemmParams v = views(base_params(jobs + int64_t(i) * (1 + nbr) + 1, nbr, 1,
+                                       static_cast<int>(mcp / GBN), bi, mcp, mcp, 1.0, 0.0),
+                           m->Dinv, m->W);
       v.aux_ld = mcp;
       GPB_TRY(gemm(m, v, true, false, EPI_SUMSQ,
                    gemm_flops(mcp / GBN, int64_t(GBM) * nbr * (nbr + 1) / 2)));
@@ -1100,8 +1120,9 @@ int full_cov(gpb_model* m, const double* zt_dev, int64_t mt, double* cov_host) {
   CUDA_TRY(launch_prior(S, mcp, zt_dev, mt, static_cast<int>(m->d), sek_params(m), m->st));
   ++m->launches;
   // Sigma = K** - V^T V (model.py:254-269), lower blocks
-  GemmParams p = base_params(m->fc_jobs.as<GemmJob>(), static_cast<int>(nbk * (nbk + 1) / 2), 1, 1,
-                             mcp, mcp, mcp, -1.0, 1.0);
+  GemmParams p = views(base_params(m->fc_jobs.as<GemmJob>(), static_cast<int>(nbk * (nbk + 1) / 2), 1, 1,
+                                   mcp, mcp, mcp, -1.0, 1.0),
+                       m->Bv, m->Bv);
   p.max_k = m->np_;
   GPB_TRY(gemm(m, p, false, false, EPI_AXPBY, gemm_flops(nbk * (nbk + 1) / 2, m->np_)));
   CUDA_TRY(launch_symmetrize(S, mcp, mt, m->st));
@@ -1471,8 +1492,9 @@ int gpb_cov_block_device(gpb_model* m, const double* za, int64_t ma, const doubl
   g.K = static_cast<int>(m->np_);
   CUDA_TRY(m->gp_jobs.ensure(sizeof(GemmJob)));
   CUDA_TRY(cudaMemcpyAsync(m->gp_jobs.p, &g, sizeof(g), cudaMemcpyHostToDevice, m->st));
-  GemmParams p = base_params(m->gp_jobs.as<GemmJob>(), 1, static_cast<int>(mpa / GBM),
-                             static_cast<int>(mpb / GBN), ldva, ldvb, mpb, -1.0, 1.0);
+  GemmParams p = views(base_params(m->gp_jobs.as<GemmJob>(), 1, static_cast<int>(mpa / GBM),
+                                   static_cast<int>(mpb / GBN), ldva, ldvb, mpb, -1.0, 1.0),
+                       Va, sizeof(double) * m->np_ * ldva, Vb, sizeof(double) * m->np_ * ldvb);
   p.max_k = m->np_;
   GPB_TRY(gemm(m, p, false, false, EPI_AXPBY, gemm_flops((mpa / GBM) * (mpb / GBN), m->np_)));
   CUDA_TRY(cudaMemcpy2DAsync(out, sizeof(double) * ldo, S, sizeof(double) * mpb, sizeof(double) * mb,

@@ -97,6 +97,10 @@ int run_gemm_nt(const double* a, const double* b, const double* c, int64_t m, in
   p.ldb = kp;
   p.ldc = np;
   p.a_ktile = p.b_ktile = int64_t(1) << 40;
+  p.a_base = da;
+  p.a_extent = mp * kp;
+  p.b_base = db;
+  p.b_extent = np * kp;
   p.alpha = -1.0;
   p.beta = 1.0;
   PL_TRY(launch_gemm(p, true, true, EPI_AXPBY, 0));

@@ -60,7 +60,7 @@ int main(int argc, char** argv) {
     const size_t amax = std::min(maxa, size_t(1) << 28);
     for (int t = 0; t < c.ntiles; ++t) {
       GemmJob j{};
-      j.A = A + (((size_t(t) * apanel) % (amax - apanel)) & ~size_t(63));
+      j.A = A + ((size_t(t) * apanel) % (amax - apanel)) / c.K * c.K;  // whole rows (TMA view)
       j.B = B;
       j.Cin = j.Cout = C + size_t(t) * bi2;
       j.K = c.K;
@@ -78,6 +78,10 @@ int main(int argc, char** argv) {
     p.alpha = -1.0;
     p.beta = c.beta;
     p.max_k = c.K;  // the library's automatic configuration choice uses it
+    p.a_base = A;
+    p.a_extent = static_cast<int64_t>(amax);
+    p.b_base = B;
+    p.b_extent = int64_t(bi) * 16384 * 2;
     launch_gemm(p, c.ak, c.bk, EPI_AXPBY, 0);
     cudaDeviceSynchronize();
     float best = 1e30f;
