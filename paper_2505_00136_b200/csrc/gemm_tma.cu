@@ -1,5 +1,5 @@
 // Grouped DMMA GEMM fed by TMA: one elected thread streams 128-byte-swizzled
-// k stages into shared memory with cp.async.bulk.tensor behind full/empty
+// k stages into shared memory with cp.async.bulk.tensor behind "full"
 // mbarriers; every warp runs DMMA.8x8x4 with no CTA-wide barrier in the
 // mainloop.  Same job semantics as dgemm_grouped_kernel (gemm.cuh):
 //
@@ -67,44 +67,56 @@ GPB_DEVINL void mbar_wait(uint64_t* b, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-GPB_DEVINL void tma_load(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+GPB_DEVINL void mbar_expect_tx_u32(uint32_t bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+GPB_DEVINL void tma_load(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-      "[%4];\n" ::"r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(bar))
+      "[%4];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
 }
 
 GPB_DEVINL int perm8(int g) { return (g >> 1) + ((g & 1) << 2); }
 
-// one operand's k-stage producer: fixed coordinates per job, k walk in place
-// Coordinates live in shared memory (only the producer thread touches them,
-// once per stage), which keeps them out of every warp's register budget.
-template <bool KMAJ, int ROWS>
+// One operand's k-stage producer state: the view coordinates of k = 0 and the
+// tiled-k walk.  It lives in shared memory (written once by thread 0, read by
+// whichever thread refills a stage), which keeps it out of every warp's
+// register budget.
 struct __align__(16) TmaWalk {
   int c_lo, c_hi;  // K-major: (column, row) of k = 0; MN-major: (m, k row)
   int ktile, kt_rows;
-  GPB_DEVINL void init(const double* ptr, const TmaOperand& o, int row0) {
-    const int64_t off = ptr - o.base;
-    const int64_t r = off / o.ld, c = off - r * o.ld;
-    c_lo = static_cast<int>(KMAJ ? c : c + row0);
-    c_hi = static_cast<int>(KMAJ ? r + row0 : r);
-    ktile = static_cast<int>(o.ktile);
-    kt_rows = static_cast<int>(o.kt_rows);
-  }
-  // k stage kc (k = 16 kc): column / k row inside the k tile, row jump per tile
-  GPB_DEVINL void issue(int kc, double* dst, const CUtensorMap* map, uint64_t* bar) const {
-    const int4 w = *reinterpret_cast<const int4*>(this);
-    const int k = kc * TBK;
-    const int kt = k / w.z, kin = k - kt * w.z;
-    if (KMAJ) {
-      tma_load(dst, map, bar, w.x + kin, w.y + kt * w.w);
-    } else {
-#pragma unroll
-      for (int h = 0; h < ROWS / 16; ++h) tma_load(dst + h * 256, map, bar, w.x + 16 * h, w.y + kin + kt * w.w);
-    }
-  }
 };
+
+template <bool KMAJ>
+GPB_DEVINL void walk_init(TmaWalk* w, const double* ptr, const TmaOperand& o, int row0) {
+  const int64_t off = ptr - o.base;
+  const int64_t r = off / o.ld, c = off - r * o.ld;
+  w->c_lo = static_cast<int>(KMAJ ? c : c + row0);
+  w->c_hi = static_cast<int>(KMAJ ? r + row0 : r);
+  w->ktile = static_cast<int>(o.ktile);
+  w->kt_rows = static_cast<int>(o.kt_rows);
+}
+
+// k stage kc (k = 16 kc) of one operand into the stage at shared address dst
+template <bool KMAJ, int ROWS>
+GPB_DEVINL void walk_issue(uint32_t walk, int kc, uint32_t dst, const CUtensorMap* map, uint32_t bar) {
+  int4 w;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+               : "r"(walk)
+               : "memory");
+  const int k = kc * TBK;
+  const int kt = k / w.z, kin = k - kt * w.z;
+  if (KMAJ) {
+    tma_load(dst, map, bar, w.x + kin, w.y + kt * w.w);
+  } else {
+#pragma unroll
+    for (int h = 0; h < ROWS / 16; ++h) tma_load(dst + h * 2048, map, bar, w.x + 16 * h, w.y + kin + kt * w.w);
+  }
+}
 
 // Fragments of one k step pair (k = 8q + 2t and 8q + 2t + 1) for F 8-row
 // fragments starting at stage row `base` (a multiple of 16).
@@ -147,7 +159,11 @@ struct TmaCfg {
   static constexpr int THREADS = CW * 32;
   static constexpr int FM = GBM / WM / 8, FN = BN / WN / 8, CPB = GBN / BN;
   static constexpr int A_BYTES = GBM * TBK * 8, B_BYTES = BN * TBK * 8;
-  static constexpr size_t SMEM = size_t(STAGES) * (A_BYTES + B_BYTES) + 2 * STAGES * 8 + 32 + kAtom;
+  // byte offsets from the 1024-aligned base: A stages, B stages, "full"
+  // barriers, per-stage release counters, the two TmaWalk records
+  static constexpr int B_OFF = STAGES * A_BYTES, FULL_OFF = STAGES * (A_BYTES + B_BYTES);
+  static constexpr int REL_OFF = FULL_OFF + 8 * STAGES, WALK_OFF = (REL_OFF + 4 * STAGES + 15) / 16 * 16;
+  static constexpr size_t SMEM = size_t(WALK_OFF) + 2 * sizeof(TmaWalk) + kAtom;
   static constexpr int kMinB = MINB, kStages = STAGES, kWM = WM, kWN = WN, kBN = BN;
 };
 
@@ -157,14 +173,20 @@ __global__ void __launch_bounds__(C::THREADS, C::kMinB)
                      const __grid_constant__ CUtensorMap map_b, const TmaOperand oa, const TmaOperand ob) {
   constexpr int FM = C::FM, FN = C::FN, BN = C::kBN, STAGES = C::kStages;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + kAtom - 1) & ~uintptr_t(kAtom - 1));
-  double* sA = reinterpret_cast<double*>(base);
-  double* sB = reinterpret_cast<double*>(base + STAGES * C::A_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * (C::A_BYTES + C::B_BYTES));
-  uint64_t* empty = full + STAGES;
-  TmaWalk<AK, GBM>* wa = reinterpret_cast<TmaWalk<AK, GBM>*>(empty + STAGES);
-  TmaWalk<BKM, C::kBN>* wb = reinterpret_cast<TmaWalk<BKM, C::kBN>*>(wa + 1);
+  // 1024-byte aligned stage base, derived from smem_raw so loads stay LDS
+  unsigned char* base = smem_raw + ((kAtom - (su32(smem_raw) & (kAtom - 1))) & (kAtom - 1));
+  const double* sA = reinterpret_cast<const double*>(base);
+  const double* sB = reinterpret_cast<const double*>(base + C::B_OFF);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + C::FULL_OFF);
+  unsigned* released = reinterpret_cast<unsigned*>(base + C::REL_OFF);  // warps done with a stage
+  const uint32_t sb = su32(base);
+  // stage `st` gets k chunk kc of both operands (one "full" phase)
+  auto fill = [&](int st, int kc) {
+    const uint32_t bar = sb + C::FULL_OFF + 8 * st;
+    mbar_expect_tx_u32(bar, C::A_BYTES + C::B_BYTES);
+    walk_issue<AK, GBM>(sb + C::WALK_OFF, kc, sb + st * C::A_BYTES, &map_a, bar);
+    walk_issue<BKM, C::kBN>(sb + C::WALK_OFF + 16, kc, sb + C::B_OFF + st * C::B_BYTES, &map_b, bar);
+  };
 
   const int per_job = p.mblk * p.nblk;
   const int lblock = blockIdx.x / C::CPB;
@@ -186,7 +208,7 @@ __global__ void __launch_bounds__(C::THREADS, C::kMinB)
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], C::CW);
+      released[s] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -202,20 +224,17 @@ __global__ void __launch_bounds__(C::THREADS, C::kMinB)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
     }
   }
-  // thread 0 is also the producer: it fills every stage up front, then at
-  // step kc refills the stage released at step kc - 1 (waiting for the other
-  // warps to release it, one step of slack), so no warp-wide role split costs
+  // no dedicated producer warp: thread 0 fills every stage up front, and the
+  // last warp to release a stage refills it at once (a shared counter per
+  // stage), so nobody waits for a free stage, no warp-wide role split costs
   // registers and no CTA barrier sits in the mainloop
   if (tid == 0 && nk > 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
-    wa->init(job.A, oa, arow0);
-    wb->init(job.B, ob, brow0);
-    for (int kc = 0; kc < STAGES && kc < nk; ++kc) {
-      mbar_expect_tx(&full[kc], C::A_BYTES + C::B_BYTES);
-      wa->issue(kc, sA + kc * (C::A_BYTES / 8), &map_a, &full[kc]);
-      wb->issue(kc, sB + kc * (C::B_BYTES / 8), &map_b, &full[kc]);
-    }
+    TmaWalk* w = reinterpret_cast<TmaWalk*>(base + C::WALK_OFF);
+    walk_init<AK>(w, job.A, oa, arow0);
+    walk_init<BKM>(w + 1, job.B, ob, brow0);
+    for (int kc = 0; kc < STAGES && kc < nk; ++kc) fill(kc, kc);
   }
   double acc[FM][FN][2];
 #pragma unroll
@@ -225,13 +244,6 @@ __global__ void __launch_bounds__(C::THREADS, C::kMinB)
   const int am0 = wm * (GBM / C::kWM), bn0 = wn * (BN / C::kWN);
   for (int kc = 0; kc < nk; ++kc) {
     const int st = kc % STAGES;
-    if (tid == 0 && kc >= 1 && kc - 1 + STAGES < nk) {
-      const int ps = (kc - 1) % STAGES;
-      mbar_wait(&empty[ps], ((kc - 1) / STAGES) & 1);
-      mbar_expect_tx(&full[ps], C::A_BYTES + C::B_BYTES);
-      wa->issue(kc - 1 + STAGES, sA + ps * (C::A_BYTES / 8), &map_a, &full[ps]);
-      wb->issue(kc - 1 + STAGES, sB + ps * (C::B_BYTES / 8), &map_b, &full[ps]);
-    }
     mbar_wait(&full[st], (kc / STAGES) & 1);
     const double* a_s = sA + st * (C::A_BYTES / 8);
     const double* b_s = sB + st * (C::B_BYTES / 8);
@@ -250,7 +262,17 @@ __global__ void __launch_bounds__(C::THREADS, C::kMinB)
         for (int j = 0; j < FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], av[i].y, bv[j].y);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
+    if (lane == 0 && kc + STAGES < nk) {
+      unsigned prev;
+      asm volatile("atom.shared.acq_rel.cta.add.u32 %0, [%1], 1;\n"
+                   : "=r"(prev)
+                   : "r"(su32(&released[st]))
+                   : "memory");
+      if (prev % C::CW == C::CW - 1) {  // every warp's reads of the stage are done
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        fill(st, kc + STAGES);
+      }
+    }
   }
   {
     // ---- epilogue: Cout = alpha * acc + beta * Cin ----
@@ -451,10 +473,10 @@ cudaError_t launch_gemm_tma(const GemmParams& p, bool ak, bool bk, int epi, cuda
   if (!operand(p.a_base, p.a_extent, p.lda, p.a_ktile, p.a_kstride, ak, GBM, &ma, &oa)) return cudaSuccess;
   if (!operand(p.b_base, p.b_extent, p.ldb, p.b_ktile, p.b_kstride, bk, Tma8::kBN, &mb, &ob)) return cudaSuccess;
   *used = true;
-  // mode 3 (automatic, tools/tma_sweep.sh): eight 32x32 warps when both
-  // operands are K-major and K is short (the Cholesky update and TRSM), else
-  // four 64x32 warps
-  const bool four = g_tma_mode == 1 || (g_tma_mode == 3 && !(ak && bk && p.max_k < 4096));
+  // mode 3 (automatic, profiles/r01_gemm_tma_sweep.txt): eight 32x32 warps
+  // for short K (the Cholesky update, TRSM and in-group updates), four 64x32
+  // warps from K = 4096 (the prediction sweep, the inverse)
+  const bool four = g_tma_mode == 1 || (g_tma_mode == 3 && p.max_k >= 4096);
   return four ? tma_dispatch<Tma4>(p, ak, bk, epi, ma, mb, oa, ob, s)
               : tma_dispatch<Tma8>(p, ak, bk, epi, ma, mb, oa, ob, s);
 }

@@ -14,7 +14,9 @@ for r in rows[hi + 1:]:
         continue
     name = r[ik]
     short = name.split("(")[0].replace("void ", "").replace("gpb::", "").replace("<unnamed>::", "")
-    if "GemmCfg<" in name:
+    if "TmaCfg<" in name:
+        short = "dgemm_tma_kernel<cfg " + name.split("TmaCfg<")[1].split(">")[0] + ">"
+    elif "GemmCfg<" in name:
         short = "dgemm_grouped_kernel<cfg " + name.split("GemmCfg<")[1].split(">")[0] + ">"
     tot[short] += float(r[iv].replace(",", "")) * scale.get(r[iu], 1e-6)
     cnt[short] += 1
