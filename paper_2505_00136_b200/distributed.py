@@ -412,8 +412,11 @@ class DistributedGP:
         ops.assemble(self.zp, d, lay, self.params, True,
                      [(i, j, self.L[s]) for s, (i, j) in enumerate(self.owned)])
         rows_per = -(-T // P)
-        # panel buffers: [set][process row] -> (G, rows_per, b, b)
-        panels = [[ops.zeros(G, rows_per, b, b) for _ in range(P)] for _ in range(2)]
+        # panel buffers: [set][process row] -> (G, rows_per, b, b), one
+        # allocation so every panel tile sits a whole number of tiles from
+        # the others (the GEMM's TMA view of the launch's operands needs that)
+        pall = ops.zeros(2, P, G, rows_per, b, b)
+        panels = [[pall[h, p] for p in range(P)] for h in range(2)]
         my_p, my_q = divmod(self.rank, Q)
         by_col = {}
         for s_, (i, j) in enumerate(self.owned):
