@@ -10,7 +10,7 @@
 //   B (CTA 0 warp 0) factor the 32x32 diagonal block -- the serial pivot
 //                   chain in registers, each new column broadcast through
 //                   shared memory;
-//     (CTA 0 warp 1) invert it row by row as the chain publishes rows;
+//     (CTA 0 warp 1) invert it by a column sweep one pivot behind the chain;
 //     (other warps) panel p-1's rank-32 update of every 32-block below the
 //                   diagonal block (right-looking) and the TRTRI of Dinv
 //                   (finalise block row p-1, accumulate term p-2);
@@ -166,8 +166,7 @@ GPB_DEVINL void cluster_barrier(bool clustered) {
 __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
   extern __shared__ double sm[];
   double* Ld = sm;                 // [64][33] factor block (rows 32..63: padding)
-  double* Li = Ld + 2 * NB * SLD;  // [32][33] its inverse
-  double* rdg = Li + NB * SLD;     // [32] 1 / l_jj of the current panel
+  double* rdg = Ld + 2 * NB * SLD;  // [32] 1 / l_jj of the current panel
   __shared__ volatile int prog_s;  // pivots of the chain published so far
   volatile int* prog = &prog_s;
   // every CTA reads info before the first cluster barrier; only CTA 0
@@ -190,16 +189,19 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
   if (tid == 0) *prog = 0;
   cluster_barrier(clustered);
   long long t_last = clock64(), t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  // per-phase cycles of thread 0 of CTA 0 (slots 0-7) and of CTA 1 (8-15)
 #define PROF_MARK(i)                                   \
-  if (a.prof && tid == 0) {                            \
+  if (a.prof && tid == 0 && cta < 2) {                 \
     const long long now_ = clock64();                  \
     t_acc[i] += now_ - t_last;                         \
     t_last = now_;                                     \
   }
 
+  long long t_phase = 0;  // profiling: start of phase B of this panel
   for (int p = 0; p < P; ++p) {
     const int c0 = p * NB;
     PROF_MARK(0)
+    if (a.prof && lane == 0) t_phase = clock64();
     if (!(lead && lw < 2)) {
       // B, job warps (CTAs 1.. when clustered, else warps 2..7), dealt
       // round-robin: panel p-1's rank-32 contribution to every 32-block
@@ -212,7 +214,9 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
       const int accn = (p >= 2) ? (P - p) * (p - 1) : 0;  // term K = p-2 of rows I >= p
       // clustered: CTA 0 keeps only the pivot chain so its SMSPs are not
       // shared with DMMA warps; the other CTAs' warps take the jobs
-      const int w0 = clustered ? warp - NW : warp - 2;
+      // consecutive jobs go to different CTAs first, then to different warps
+      // (SMSPs) of a CTA: a K = 32 job is DMMA-issue bound on its SMSP
+      const int w0 = clustered ? (lead ? -1 : (cta - 1) + (ncta - 1) * lw) : warp - 2;
       const int nwk = clustered ? GW - NW : NW - 2;
       for (int q = (w0 >= 0 ? w0 : pre + inv + accn); q < pre + inv + accn; q += nwk) {
         if (q < pre) {
@@ -233,6 +237,9 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
           trtri_acc(T, D, bi, p + w / (p - 1), w % (p - 1), p - 2, g, t);
         }
       }
+      PROF_MARK(5)
+      if (a.prof && lane == 0 && lw == 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.prof + 16 + cta),
+                                                    static_cast<unsigned long long>(clock64() - t_phase));
     } else if (lead && lw == 0) {
       // B, chain: lane i keeps row i of the diagonal block in registers,
       // shifted so that register 0 always holds the current pivot column
@@ -308,28 +315,28 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
       }
       PROF_MARK(6)
     } else if (lead && lw == 1) {
-      // B, inverse of the diagonal block, row i as soon as the chain has
-      // finished pivot i:  Li[i][k] = -(1 / l_ii) sum_{m<i} l_im Li[m][k]
-      // (Li[m][k] = 0 for k > m, so every lane runs the same loop)
+      // B, inverse of the diagonal block by a column sweep that trails the
+      // chain by one pivot: lane k holds column k of Li = L^-1 in registers
+      // (forward substitution of e_k), and step j needs only column j of L,
+      // published by the chain right after pivot j:
+      //   x_j *= 1 / l_jj;   x_i -= l_ij x_j  (i > j, independent FMAs)
       const int base = p * NB;
-#pragma unroll 1
-      for (int i = 0; i < NB; ++i) {
-        while (*prog < base + i + 1) {
+      double x[NB];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        while (*prog < base + j + 1) {
         }
         __threadfence_block();
-        double s0 = 0.0, s1 = 0.0;
-        int m = 0;
-        for (; m + 1 < i; m += 2) {
-          s0 = fma(Ld[i * SLD + m], Li[m * SLD + lane], s0);
-          s1 = fma(Ld[i * SLD + m + 1], Li[(m + 1) * SLD + lane], s1);
-        }
-        if (m < i) s0 = fma(Ld[i * SLD + m], Li[m * SLD + lane], s0);
-        const double di = rdg[i];
-        Li[i * SLD + lane] = lane < i ? -(s0 + s1) * di : (lane == i ? di : 0.0);
-        __syncwarp();
+        x[j] *= rdg[j];
+#pragma unroll
+        for (int i = j + 1; i < NB; ++i) x[i] = fma(-Ld[i * SLD + j], x[j], x[i]);
       }
-#pragma unroll 4
-      for (int c = 0; c < NB; ++c) D[static_cast<int64_t>(c0 + lane) * bi + c0 + c] = Li[lane * SLD + c];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) D[static_cast<int64_t>(c0 + i) * bi + c0 + lane] = x[i];
+      if (a.prof && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.prof + 32),
+                                         static_cast<unsigned long long>(clock64() - t_phase));
     }
     cluster_barrier(clustered);
     PROF_MARK(1)
@@ -342,7 +349,9 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
     {
       const int nt = factor ? P - p - 1 : 0;
       const int na = p >= 1 ? p : 0;  // J = 0..p-1
-      for (int q = warp; q < nt + na; q += GW) {
+      // dealt over CTAs first (job q on CTA q % ncta): the critical job q = 0
+      // and the others each get an SMSP of their own
+      for (int q = cta + ncta * lw; q < nt + na; q += GW) {
         if (q < nt) {
           const int rb = p + 1 + q;
           double acc[4][4][2];
@@ -362,6 +371,7 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
         }
       }
     }
+    PROF_MARK(7)
     cluster_barrier(clustered);
     PROF_MARK(2)
   }
@@ -378,13 +388,13 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
     }
   }
   PROF_MARK(4)
-  if (a.prof && tid == 0 && lead)
-    for (int i = 0; i < 8; ++i) a.prof[i] += t_acc[i];
+  if (a.prof && tid == 0 && cta < 2)
+    for (int i = 0; i < 8; ++i) a.prof[8 * cta + i] += t_acc[i];
   if (tid == 0 && lead && a.logdiag) a.logdiag[a.tile_index] = logsum;
 #undef PROF_MARK
 }
 
-size_t potrf_smem_bytes() { return sizeof(double) * (3 * NB * SLD + NB); }
+size_t potrf_smem_bytes() { return sizeof(double) * (2 * NB * SLD + NB); }
 
 static int g_cluster = 0;
 
