@@ -255,11 +255,16 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
         // Two pivots per trip, then a shift by two.  Entries of lanes above
         // the current row are updated too (they lie in the upper triangle,
         // are never read again, and lcol = 0 leaves them unchanged for lanes
-        // < j), which drops the per-entry predicate.
-        auto pivot = [&](int j, int o) {  // register o holds column j
-          const double piv = __shfl_sync(0xffffffffu, r[o], j);
+        // < j), which drops the per-entry predicate.  Software-pipelined:
+        // each pivot first updates the next pivot column, fetches the next
+        // pivot and starts its rsqrt, and only then updates the other
+        // columns, so the rsqrt latency hides behind those FMAs; the chain
+        // publishes its progress once per trip.
+        double piv = __shfl_sync(0xffffffffu, r[0], 0);
+        double rinv = rsqrt(piv);
+        // register o holds column j; returns with piv / rinv of pivot j + 1
+        auto pivot = [&](int j, int o) {
           if (fail < 0 && !(piv > 0.0)) fail = j;
-          const double rinv = rsqrt(piv);
           const double lcol = (lane == j) ? piv * rinv : (lane > j ? r[o] * rinv : 0.0);
           if (lane == j) {
             my_l = lcol;
@@ -267,7 +272,7 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
           }
           Ld[lane * SLD + j] = lcol;
           __syncwarp();
-          if (lane == 0) {
+          if (o == 1 && lane == 0) {
             __threadfence_block();
             *prog = base + j + 1;
           }
@@ -275,8 +280,13 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
           // shuffles); rows past the panel read the padding rows of Ld and only
           // feed registers that hold columns past the panel
           const double* lrow = Ld + (j - o) * SLD + j;
+          r[o + 1] = fma(-lcol, lrow[(o + 1) * SLD], r[o + 1]);
+          if (j + 1 < NB) {
+            piv = __shfl_sync(0xffffffffu, r[o + 1], j + 1);
+            rinv = rsqrt(piv);
+          }
 #pragma unroll
-          for (int c = o + 1; c < NB; ++c) r[c] = fma(-lcol, lrow[c * SLD], r[c]);
+          for (int c = o + 2; c < NB; ++c) r[c] = fma(-lcol, lrow[c * SLD], r[c]);
         };
 #pragma unroll 1
         for (int j = 0; j < NB; j += 2) {
