@@ -48,14 +48,6 @@ GPB_DEVINL uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_ge
 GPB_DEVINL void mbar_init(uint64_t* b, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(count) : "memory");
 }
-GPB_DEVINL void mbar_expect_tx(uint64_t* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)),
-               "r"(bytes)
-               : "memory");
-}
-GPB_DEVINL void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
-}
 GPB_DEVINL void mbar_wait(uint64_t* b, unsigned parity) {
   asm volatile(
       "{\n"

@@ -152,6 +152,76 @@ GPB_DEVINL void trtri_fin(double* D, int bi, int I, int J, int g, int t) {
   __syncwarp();
 }
 
+// 8-row fragments of the K = 32 block jobs: a 32x32 job is split into four
+// independent row fragments (acc[j][e] <-> C[g][8j+2t+e]) dealt to warps on
+// different SMSPs, since one warp's DMMAs are issue-bound on its SMSP.  All
+// 40 operand loads of a lane are issued before the DMMAs.
+GPB_DEVINL void frag_mma(double (&acc)[4][2], const double (&a)[8], const double (&b)[8][4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dmma884(acc[j][0], acc[j][1], a[s], b[s][j]);
+}
+
+// acc = A(8 x 32) * B(32 x 32)^T, both k-contiguous
+GPB_DEVINL void frag_nt(double (&acc)[4][2], const double* A, int64_t lda, const double* B, int64_t ldb,
+                        int g, int t) {
+  double a[8], b[8][4];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    a[s] = A[g * lda + 4 * s + t];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[s][j] = B[(8 * j + g) * ldb + 4 * s + t];
+  }
+  frag_mma(acc, a, b);
+}
+
+// acc = A(8 x 32) * B(32 x 32), A k-contiguous, B row-major (n contiguous)
+GPB_DEVINL void frag_nn(double (&acc)[4][2], const double* A, int64_t lda, const double* B, int64_t ldb,
+                        int g, int t) {
+  double a[8], b[8][4];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    a[s] = A[g * lda + 4 * s + t];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[s][j] = B[(4 * s + t) * ldb + 8 * j + g];
+  }
+  frag_mma(acc, a, b);
+}
+
+// C[8x32 at c, ldc] -= acc  (or = scale * acc when assign)
+GPB_DEVINL void store_frag(double* c, int64_t ldc, const double (&acc)[4][2], int g, int t, bool assign,
+                           double scale) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    double* q = c + static_cast<int64_t>(g) * ldc + 8 * j + 2 * t;
+    if (assign) {
+      q[0] = scale * acc[j][0];
+      q[1] = scale * acc[j][1];
+    } else {
+      q[0] -= acc[j][0];
+      q[1] -= acc[j][1];
+    }
+  }
+}
+
+// row fragment f of trtri_acc: D_IJ (-)= T_IK D_KJ (the first term, K == J, assigns)
+GPB_DEVINL void trtri_acc_frag(const double* T, double* D, int bi, int I, int J, int K, int f, int g,
+                               int t) {
+  double acc[4][2];
+  const int64_t r = static_cast<int64_t>(I) * NB + 8 * f;
+  frag_nn(acc, T + r * bi + K * NB, bi, D + static_cast<int64_t>(K) * NB * bi + J * NB, bi, g, t);
+  store_frag(D + r * bi + J * NB, bi, acc, g, t, K == J, -1.0);
+}
+
+// the cluster's warps except CTA 0's warps 0..3, numbered so that
+// consecutive indices sit on different CTAs first, then on different SMSPs
+GPB_DEVINL int c_worker(int cta, int ncta, int lw) {
+  return cta + ncta * lw - min(4, lw + (cta > 0 ? 1 : 0));
+}
+
 // all threads of the cluster (a plain launch is a cluster of one CTA)
 GPB_DEVINL void cluster_barrier(bool clustered) {
   if (clustered)
@@ -218,6 +288,8 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
       // (SMSPs) of a CTA: a K = 32 job is DMMA-issue bound on its SMSP
       const int w0 = clustered ? (lead ? -1 : (cta - 1) + (ncta - 1) * lw) : warp - 2;
       const int nwk = clustered ? GW - NW : NW - 2;
+      // whole 32x32 jobs here (row fragments would repeat the B operand's
+      // loads four times: this phase is load-bound, measured slower)
       for (int q = (w0 >= 0 ? w0 : pre + inv + accn); q < pre + inv + accn; q += nwk) {
         if (q < pre) {
           const int qq = q + 1;  // skip (p, p)
@@ -252,48 +324,65 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
       int fail = -1;
       double my_l = 1.0;
       if (factor) {
-        // Two pivots per trip, then a shift by two.  Entries of lanes above
-        // the current row are updated too (they lie in the upper triangle,
-        // are never read again, and lcol = 0 leaves them unchanged for lanes
-        // < j), which drops the per-entry predicate.  Software-pipelined:
-        // each pivot first updates the next pivot column, fetches the next
-        // pivot and starts its rsqrt, and only then updates the other
-        // columns, so the rsqrt latency hides behind those FMAs; the chain
-        // publishes its progress once per trip.
+        // Blocked by sub-panels of SP = 8 columns: a pivot updates only the
+        // columns of its own sub-panel; at the end of a sub-panel one rank-8
+        // update (the same FMAs in the same order, so results are unchanged)
+        // brings the later columns up to date, and the registers shift by 8.
+        // Entries of lanes above the current row are updated too (they lie in
+        // the upper triangle, are never read again, and lcol = 0 leaves them
+        // unchanged for lanes < j), which drops the per-entry predicate.
+        // Software-pipelined: the next pivot column is updated first, its
+        // pivot fetched and its rsqrt started, and only then the other
+        // columns, so the rsqrt latency hides behind those FMAs; progress is
+        // published every two pivots.
+        constexpr int SP = 8;
         double piv = __shfl_sync(0xffffffffu, r[0], 0);
         double rinv = rsqrt(piv);
-        // register o holds column j; returns with piv / rinv of pivot j + 1
-        auto pivot = [&](int j, int o) {
-          if (fail < 0 && !(piv > 0.0)) fail = j;
-          const double lcol = (lane == j) ? piv * rinv : (lane > j ? r[o] * rinv : 0.0);
-          if (lane == j) {
-            my_l = lcol;
-            rdg[j] = rinv;
-          }
-          Ld[lane * SLD + j] = lcol;
-          __syncwarp();
-          if (o == 1 && lane == 0) {
-            __threadfence_block();
-            *prog = base + j + 1;
-          }
-          // l_(j+c-o), j broadcast from shared memory (one address per load, no
-          // shuffles); rows past the panel read the padding rows of Ld and only
-          // feed registers that hold columns past the panel
-          const double* lrow = Ld + (j - o) * SLD + j;
-          r[o + 1] = fma(-lcol, lrow[(o + 1) * SLD], r[o + 1]);
-          if (j + 1 < NB) {
-            piv = __shfl_sync(0xffffffffu, r[o + 1], j + 1);
-            rinv = rsqrt(piv);
-          }
-#pragma unroll
-          for (int c = o + 2; c < NB; ++c) r[c] = fma(-lcol, lrow[c * SLD], r[c]);
-        };
 #pragma unroll 1
-        for (int j = 0; j < NB; j += 2) {
-          pivot(j, 0);
-          pivot(j + 1, 1);
+        for (int j0 = 0; j0 < NB; j0 += SP) {
+          double lc[SP];
 #pragma unroll
-          for (int c = 0; c < NB - 2; ++c) r[c] = r[c + 2];
+          for (int t = 0; t < SP; ++t) {  // register t holds column j = j0 + t
+            const int j = j0 + t;
+            if (fail < 0 && !(piv > 0.0)) fail = j;
+            const double lcol = (lane == j) ? piv * rinv : (lane > j ? r[t] * rinv : 0.0);
+            lc[t] = lcol;
+            if (lane == j) {
+              my_l = lcol;
+              rdg[j] = rinv;
+            }
+            Ld[lane * SLD + j] = lcol;
+            __syncwarp();
+            if ((t & 1) && lane == 0) {
+              __threadfence_block();
+              *prog = base + j + 1;
+            }
+            if (t + 1 < SP) {
+              // lrow[c * SLD] = l_(j0 + c), j from shared memory (one address
+              // per load)
+              const double* lrow = Ld + j0 * SLD + j;
+              r[t + 1] = fma(-lcol, lrow[(t + 1) * SLD], r[t + 1]);
+              piv = __shfl_sync(0xffffffffu, r[t + 1], j + 1);
+              rinv = rsqrt(piv);
+#pragma unroll
+              for (int c = t + 2; c < SP; ++c) r[c] = fma(-lcol, lrow[c * SLD], r[c]);
+            }
+          }
+          if (j0 + SP < NB) {
+            // rank-SP update of the later columns; rows past the panel read
+            // the padding rows of Ld and only feed registers past the panel
+            const double* lb = Ld + j0 * SLD + j0;  // lb[c * SLD + t] = l_(j0 + c), (j0 + t)
+#pragma unroll
+            for (int t = 0; t < SP; ++t) r[SP] = fma(-lc[t], lb[SP * SLD + t], r[SP]);
+            piv = __shfl_sync(0xffffffffu, r[SP], j0 + SP);
+            rinv = rsqrt(piv);
+#pragma unroll
+            for (int c = SP + 1; c < NB; ++c)
+#pragma unroll
+              for (int t = 0; t < SP; ++t) r[c] = fma(-lc[t], lb[c * SLD + t], r[c]);
+#pragma unroll
+            for (int c = 0; c < NB - SP; ++c) r[c] = r[c + SP];
+          }
         }
         const int pos = a.tile_off + c0 + lane;  // padded global position
         const bool real = (pos % a.bp_user < a.b_user) && (fail < 0 || lane < fail);
@@ -359,25 +448,40 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
     {
       const int nt = factor ? P - p - 1 : 0;
       const int na = p >= 1 ? p : 0;  // J = 0..p-1
-      // dealt over CTAs first (job q on CTA q % ncta): the critical job q = 0
-      // and the others each get an SMSP of their own
-      for (int q = cta + ncta * lw; q < nt + na; q += GW) {
-        if (q < nt) {
-          const int rb = p + 1 + q;
-          double acc[4][4][2];
-          zero_acc(acc);
-          double* blk = T + static_cast<int64_t>(rb) * NB * bi + c0;
-          warp_nt(acc, blk, bi, D + static_cast<int64_t>(c0) * bi + c0, bi, NB, g, t);
+      // The critical path, block row p+1 (which B(p+1) needs first), runs on
+      // CTA 0's warps 0..3, one 8-row fragment each: X = T * Li^T, then, after
+      // a named barrier of the four warps, (p+1, p+1) -= X X^T.  Every other
+      // row block and TRTRI term is split into row fragments dealt to the
+      // remaining warps (c_worker).
+      const double* Li = D + static_cast<int64_t>(c0) * bi + c0;
+      if (lead && lw < 4) {
+        if (nt > 0) {
+          double* blk = T + static_cast<int64_t>(p + 1) * NB * bi + c0;
+          double* mine = blk + static_cast<int64_t>(8 * lw) * bi;
+          double acc[4][2];
+          frag_nt(acc, mine, bi, Li, bi, g, t);
           __syncwarp();
-          store_acc(blk, bi, acc, g, t, true, 1.0);
-          if (q == 0) {  // (p+1, p+1) -= X X^T with X = the block just stored
+          store_frag(mine, bi, acc, g, t, true, 1.0);
+          __threadfence_block();
+          asm volatile("bar.sync 1, 128;\n" ::: "memory");
+          frag_nt(acc, mine, bi, blk, bi, g, t);
+          store_frag(mine + NB, bi, acc, g, t, false, 1.0);
+        }
+      } else {
+        const int nw = GW - 4;
+        const int nrow = nt > 0 ? 4 * (nt - 1) : 0;
+        const int nsub = nrow + 4 * na;
+        for (int q = c_worker(cta, ncta, lw); q < nsub; q += nw) {
+          const int f = q % 4;
+          if (q < nrow) {
+            double* mine = T + (static_cast<int64_t>(p + 2 + q / 4) * NB + 8 * f) * bi + c0;
+            double acc[4][2];
+            frag_nt(acc, mine, bi, Li, bi, g, t);
             __syncwarp();
-            zero_acc(acc);
-            warp_nt(acc, blk, bi, blk, bi, NB, g, t);
-            store_acc(blk + NB, bi, acc, g, t, false, 1.0);
+            store_frag(mine, bi, acc, g, t, true, 1.0);
+          } else {
+            trtri_acc_frag(T, D, bi, p, (q - nrow) / 4, p - 1, f, g, t);
           }
-        } else {
-          trtri_acc(T, D, bi, p, q - nt, p - 1, g, t);
         }
       }
     }
@@ -406,20 +510,24 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
 
 size_t potrf_smem_bytes() { return sizeof(double) * (2 * NB * SLD + NB); }
 
-static int g_cluster = 0;
+static int g_cluster = -1;
 
-// CTAs per diagonal tile (GPB_POTRF_CLUSTER: 1 = single CTA, 2, 4, 8 or 16)
-static int potrf_cluster() {
-  if (g_cluster == 0) {
+// CTAs per diagonal tile: GPB_POTRF_CLUSTER (1 = single CTA, 2, 4, 8 or 16),
+// else 16 when the factorisation has fewer than 48 diagonal tiles (POTRF on
+// the critical path: config 1 factor 8.8 -> 8.2 ms) and 8 otherwise (hidden
+// behind the trailing update, where 16 idle-heavy SMs would cost GEMM time)
+static int potrf_cluster(int tiles) {
+  if (g_cluster < 0) {
     const char* e = getenv("GPB_POTRF_CLUSTER");
-    int c = e ? atoi(e) : 8;
-    g_cluster = (c == 1 || c == 2 || c == 4 || c == 8 || c == 16) ? c : 8;
+    const int c = e ? atoi(e) : 0;
+    g_cluster = (c == 1 || c == 2 || c == 4 || c == 8 || c == 16) ? c : 0;
   }
-  return g_cluster;
+  if (g_cluster > 0) return g_cluster;
+  return (tiles > 0 && tiles < 48) ? 16 : 8;
 }
 
 cudaError_t launch_potrf(const PotrfArgs& a, cudaStream_t s) {
-  const int cl = potrf_cluster();
+  const int cl = potrf_cluster(a.tiles);
   if (cl == 1) {
     potrf_tile_kernel<<<1, PT, potrf_smem_bytes(), s>>>(a);
     return cudaGetLastError();
