@@ -167,7 +167,7 @@ struct gpb_model {
   int64_t last_pivot = -1;
 
   // gradient
-  DevBuf X, Kinv, Wg, part_l, part_v, part_x, inv_jobs;
+  DevBuf X, Kinv, part_l, part_v, part_x, inv_jobs;
   DevBuf gp_panel, gp_h, gp_jobs, gp_tiles;  // column-panel gradient terms (multi-GPU split)
   std::vector<int64_t> invw_off, invx_off;
   int64_t kinv_off = 0, kinv_cnt = 0;
@@ -693,7 +693,6 @@ int build_inv_plan(gpb_model* m) {
   const int64_t ntiles = int64_t(Ti) * (Ti + 1) / 2;
   CUDA_TRY(m->X.ensure(sizeof(double) * ntiles * bi2));
   CUDA_TRY(m->Kinv.ensure(sizeof(double) * ntiles * bi2));
-  CUDA_TRY(m->Wg.ensure(sizeof(double) * std::max(1, Ti - 1) * bi2));
   const int64_t nblk = ntiles * (m->bi / kSekBlock) * (m->bi / kSekBlock);
   CUDA_TRY(m->part_l.ensure(sizeof(double) * nblk));
   CUDA_TRY(m->part_v.ensure(sizeof(double) * nblk));
@@ -702,28 +701,35 @@ int build_inv_plan(gpb_model* m) {
   double* D = m->Dinv.as<double>();
   double* X = m->X.as<double>();
   double* Kv = m->Kinv.as<double>();
-  double* Wg = m->Wg.as<double>();
   std::vector<GemmJob> jobs;
-  m->invw_off.assign(Ti + 1, 0);
-  m->invx_off.assign(Ti + 1, 0);
-  for (int i = 1; i < Ti; ++i) {
-    m->invw_off[i] = jobs.size();
-    for (int j = 0; j < i; ++j) {  // W_j = L[i, j..i) X[j..i, j]
-      GemmJob g{};
-      g.A = L + h_tri_rm(i, j) * bi2;
-      g.B = X + h_tri_cm(j, j, Ti) * bi2;
-      g.Cout = Wg + int64_t(j) * bi2;
-      g.K = (i - j) * m->bi;
-      jobs.push_back(g);
-    }
-    m->invx_off[i] = jobs.size();
-    for (int j = 0; j < i; ++j)  // X[i, j] = -Dinv_i W_j, row block r needs k < (r+1)*128
+  // X = L^-1 right-looking, with the K^-1 buffer as the accumulator
+  // A(i, j) = -sum_{m=j}^{i-1} L(i, m) X(m, j):
+  //   F_k: X(k, j) = Dinv_k A(k, j), j < k (row block r needs k < (r+1)*128)
+  //   U_k: A(i, j) -= L(i, k) X(k, j), i > k, j <= k -- one launch of
+  //        (T-1-k)(k+1) equal K = bi tile products
+  // (the left-looking form put a K = i*bi job next to K = bi ones in one
+  // launch: at config 1 the long jobs left most SMs idle)
+  m->invw_off.assign(Ti + 1, 0);  // U_k
+  m->invx_off.assign(Ti + 1, 0);  // F_k
+  for (int k = 0; k < Ti; ++k) {
+    m->invx_off[k] = jobs.size();
+    for (int j = 0; j < k; ++j)
       for (int r = 0; r < m->bi / GBM; ++r) {
         GemmJob g{};
-        g.A = D + int64_t(i) * bi2 + int64_t(r) * GBM * m->bi;
-        g.B = Wg + int64_t(j) * bi2;
-        g.Cout = X + h_tri_cm(i, j, Ti) * bi2 + int64_t(r) * GBM * m->bi;
+        g.A = D + int64_t(k) * bi2 + int64_t(r) * GBM * m->bi;
+        g.B = Kv + h_tri_cm(k, j, Ti) * bi2;
+        g.Cout = X + h_tri_cm(k, j, Ti) * bi2 + int64_t(r) * GBM * m->bi;
         g.K = (r + 1) * GBM;
+        jobs.push_back(g);
+      }
+    m->invw_off[k] = jobs.size();
+    for (int i = k + 1; i < Ti; ++i)
+      for (int j = 0; j <= k; ++j) {
+        GemmJob g{};
+        g.A = L + h_tri_rm(i, k) * bi2;
+        g.B = X + h_tri_cm(k, j, Ti) * bi2;
+        g.Cin = g.Cout = Kv + h_tri_cm(i, j, Ti) * bi2;
+        g.K = m->bi;
         jobs.push_back(g);
       }
   }
@@ -762,16 +768,21 @@ int loss_gradients(gpb_model* m, double out[3]) {
   for (int i = 0; i < Ti; ++i)
     CUDA_TRY(cudaMemcpyAsync(X + h_tri_cm(i, i, Ti) * bi2, D + int64_t(i) * bi2,
                              sizeof(double) * bi2, cudaMemcpyDeviceToDevice, m->st));
-  for (int i = 1; i < Ti; ++i) {
-    GemmParams w = views(base_params(jobs + m->invw_off[i], i, nb, nb, bi, bi, bi, 1.0, 0.0), m->L, m->X);
-    w.a_ktile = bi;
-    w.a_kstride = bi2;
-    w.max_k = int64_t(i) * bi;
-    GPB_TRY(gemm(m, w, true, false, EPI_AXPBY, gemm_flops(int64_t(nb) * nb, int64_t(bi) * i * (i + 1) / 2)));
-    GemmParams x = views(base_params(jobs + m->invx_off[i], i * nb, 1, nb, bi, bi, bi, -1.0, 0.0), m->Dinv,
-                         m->Wg);
-    GPB_TRY(gemm(m, x, true, false, EPI_AXPBY,
-                 gemm_flops(int64_t(i) * nb, int64_t(GBM) * nb * (nb + 1) / 2)));
+  CUDA_TRY(cudaMemsetAsync(m->Kinv.p, 0, sizeof(double) * ntiles * bi2, m->st));
+  for (int k = 0; k < Ti; ++k) {
+    if (k > 0) {
+      GemmParams f = views(base_params(jobs + m->invx_off[k], k * nb, 1, nb, bi, bi, bi, 1.0, 0.0), m->Dinv,
+                           m->Kinv);
+      GPB_TRY(gemm(m, f, true, false, EPI_AXPBY,
+                   gemm_flops(int64_t(k) * nb, int64_t(GBM) * nb * (nb + 1) / 2)));
+    }
+    const int64_t nu = int64_t(Ti - 1 - k) * (k + 1);  // U_k tile products
+    if (nu > 0) {
+      GemmParams u = views(base_params(jobs + m->invw_off[k], static_cast<int>(nu), nb, nb, bi, bi, bi, -1.0, 1.0),
+                           m->L, m->X);
+      u.max_k = bi;
+      GPB_TRY(gemm(m, u, true, false, EPI_AXPBY, gemm_flops(nu * nb * nb, bi)));
+    }
   }
 
   double* red = m->red.as<double>();
@@ -1216,7 +1227,7 @@ int model_create(gpb_ctx* ctx, const double* z, const double* y, int64_t n, int6
 void free_model(gpb_model* m) {
   for (DevBuf* b : {&m->zp, &m->yp, &m->L, &m->Dinv, &m->scratch, &m->logdiag, &m->info, &m->yhat,
                     &m->beta, &m->alpha, &m->bhat, &m->red, &m->tile_rm, &m->tile_cm, &m->chol_jobs,
-                    &m->X, &m->Kinv, &m->Wg, &m->part_l, &m->part_v, &m->part_x, &m->inv_jobs,
+                    &m->X, &m->Kinv, &m->part_l, &m->part_v, &m->part_x, &m->inv_jobs,
                     &m->Bv, &m->W, &m->mpart, &m->sq, &m->pred_jobs, &m->zt, &m->mean, &m->var,
                     &m->S, &m->fc_jobs, &m->gp_panel, &m->gp_h, &m->gp_jobs, &m->gp_tiles})
     b->release();
