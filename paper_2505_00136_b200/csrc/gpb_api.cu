@@ -741,6 +741,7 @@ int build_inv_plan(gpb_model* m) {
       g.B = X + h_tri_cm(r, c, Ti) * bi2;
       g.Cout = Kv + h_tri_cm(r, c, Ti) * bi2;
       g.K = (Ti - r) * m->bi;
+      g.lower = (r == c);  // symmetric: the trace pass reads the lower triangle only
       jobs.push_back(g);
     }
   m->kinv_cnt = jobs.size() - m->kinv_off;

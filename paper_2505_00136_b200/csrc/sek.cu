@@ -271,6 +271,17 @@ __global__ void __launch_bounds__(ST) trace_kernel(const double* kinv, const int
   const int rb = blk / nbs, cb = blk % nbs;
   const int2 ij = tile_ij[t];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  // K^-1 and dK/dtheta are symmetric: in a diagonal tile only the blocks on
+  // and below the diagonal are read (strictly lower ones twice), so the
+  // K^-1 producer may leave the strictly upper blocks of diagonal tiles unset
+  if (ij.x == ij.y && rb < cb) {
+    if (tid == 0) {
+      part_l[blockIdx.x] = 0.0;
+      part_v[blockIdx.x] = 0.0;
+      if (part_t) part_t[blockIdx.x] = 0.0;
+    }
+    return;
+  }
   const int64_t P0 = static_cast<int64_t>(ij.x) * bi + rb * SB;
   const int64_t Q0 = static_cast<int64_t>(ij.y) * bi + cb * SB;
   Frag d2;
@@ -300,7 +311,7 @@ __global__ void __launch_bounds__(ST) trace_kernel(const double* kinv, const int
       }
     }
   }
-  const double w = (ij.x == ij.y) ? 1.0 : 2.0;
+  const double w = (ij.x == ij.y && rb == cb) ? 1.0 : 2.0;
   const double tl = block_sum(sl, red, tid);
   const double tv = block_sum(sv, red, tid);
   const double ts = part_t ? block_sum(st, red, tid) : 0.0;

@@ -410,3 +410,37 @@ def test_tma_gemm_matches_cpasync_gemm(tmp_path):
     assert rel(a["mean"], b["mean"]) <= 1e-12
     assert rel(a["var"], b["var"]) <= 1e-12
     assert rel(a["grads"], b["grads"]) <= 1e-12
+
+
+def test_device_gemm_views_and_fallback(runtime, rng):
+    """gpb_dev_gemm_tiled (the multi-GPU schedule's GEMM) builds TMA views from
+    the job pointers when every job's block sits inside one row of an
+    ld-wide view of one buffer, and falls back to the cp.async kernel when the
+    operands come from unrelated allocations at arbitrary offsets; both must
+    give C - A B^T (K-major x K-major, tiled-k walk over two panel tiles)."""
+    import torch
+
+    from paper_2505_00136_b200.distributed import DeviceTileOps
+
+    ops = DeviceTileOps(runtime, 0)
+    b = 128
+    a_h = rng.normal(size=(3, 2, b, b))  # 3 row tiles x 2 panels
+    c_h = rng.normal(size=(3, b, b))
+    want = np.stack([c_h[i] - np.concatenate(a_h[i], axis=1) @ np.concatenate(a_h[0], axis=1).T
+                     for i in range(3)])
+    # (1) one allocation: panel buffer (2, 3, b, b), walked with a stride of 3 tiles
+    pan = torch.from_numpy(np.ascontiguousarray(a_h.transpose(1, 0, 2, 3))).cuda()
+    c1 = torch.from_numpy(c_h.copy()).cuda()
+    ops.gemm([(pan[:, i], pan[:, 0], c1[i], c1[i], 2 * b, False) for i in range(3)], b, -1.0, 1.0)
+    # (2) separate allocations, each padded by an odd number of doubles
+    pads = [torch.zeros(2 * 3 * b * b + 8 * k + 2, dtype=torch.float64, device="cuda") for k in range(3)]
+    tiles = []
+    for i in range(3):
+        view = pads[i][2 + 8 * i:].view(-1)[: 2 * b * b].view(2, b, b)
+        view.copy_(torch.from_numpy(a_h[i]))
+        tiles.append(view)
+    c2 = torch.from_numpy(c_h.copy()).cuda()
+    ops.gemm([(tiles[i], tiles[0], c2[i], c2[i], 2 * b, False) for i in range(3)], b, -1.0, 1.0)
+    torch.cuda.synchronize()
+    for got in (c1, c2):
+        assert rel(got.cpu().numpy(), want) <= 1e-14
