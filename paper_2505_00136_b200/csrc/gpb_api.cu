@@ -575,6 +575,7 @@ int ensure_factor(gpb_model* m) {
       a.b_user = m->pm.b_user;
       a.prof = m->potrf_prof;
       a.tiles = Ti;
+      a.remaining = Ti - k;
       {
         ProfScope ps(m, KC_POTRF, 2.0 / 3.0 * double(bi) * bi * bi, m->crit);
         CUDA_TRY(launch_potrf(a, m->crit));

@@ -24,6 +24,7 @@ struct PotrfArgs {
   int trtri_only;   // 1: tile already holds L; only form dinv = L^-1
   long long* prof;  // optional per-phase cycle counters (GPB_POTRF_PROF), else null
   int tiles;        // diagonal tiles of the factorisation (cluster-size hint), 0 if unknown
+  int remaining;    // diagonal tiles from this one to the end (cluster-size hint), 0 if unknown
 };
 cudaError_t launch_potrf(const PotrfArgs& a, cudaStream_t s);
 cudaError_t potrf_init_attributes();

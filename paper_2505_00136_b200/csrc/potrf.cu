@@ -513,21 +513,22 @@ size_t potrf_smem_bytes() { return sizeof(double) * (2 * NB * SLD + NB); }
 static int g_cluster = -1;
 
 // CTAs per diagonal tile: GPB_POTRF_CLUSTER (1 = single CTA, 2, 4, 8 or 16),
-// else 16 when the factorisation has fewer than 48 diagonal tiles (POTRF on
-// the critical path: config 1 factor 8.8 -> 8.2 ms) and 8 otherwise (hidden
-// behind the trailing update, where 16 idle-heavy SMs would cost GEMM time)
-static int potrf_cluster(int tiles) {
+// else 16 where POTRF is on the critical path -- factorisations of fewer
+// than 48 diagonal tiles (config 1 factor 8.8 -> 8.2 ms) and the last 8 tiles
+// of larger ones -- and 8 otherwise (hidden behind the trailing update,
+// where 16 latency-bound SMs would cost GEMM time)
+static int potrf_cluster(int tiles, int remaining) {
   if (g_cluster < 0) {
     const char* e = getenv("GPB_POTRF_CLUSTER");
     const int c = e ? atoi(e) : 0;
     g_cluster = (c == 1 || c == 2 || c == 4 || c == 8 || c == 16) ? c : 0;
   }
   if (g_cluster > 0) return g_cluster;
-  return (tiles > 0 && tiles < 48) ? 16 : 8;
+  return ((tiles > 0 && tiles < 48) || (remaining > 0 && remaining <= 8)) ? 16 : 8;
 }
 
 cudaError_t launch_potrf(const PotrfArgs& a, cudaStream_t s) {
-  const int cl = potrf_cluster(a.tiles);
+  const int cl = potrf_cluster(a.tiles, a.remaining);
   if (cl == 1) {
     potrf_tile_kernel<<<1, PT, potrf_smem_bytes(), s>>>(a);
     return cudaGetLastError();
