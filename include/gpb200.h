@@ -171,6 +171,26 @@ int gpb_dev_gemm(gpb_ctx* ctx, void* stream, const gpb_gemm_job* jobs, int64_t n
 int gpb_dev_gemm_tiled(gpb_ctx* ctx, void* stream, const gpb_gemm_job* jobs, int64_t njobs,
                        int64_t b, int64_t lda, int64_t ldb, int64_t ldc, int a_kmajor, int b_kmajor,
                        int64_t ktile, int64_t kstride, double alpha, double beta);
+/* gpb_dev_gemm_tiled whose jobs also store their output tiles at mirror
+ * addresses: job j's element at offset o from its cout is written to
+ * mirrors[j * nmirror + r] + o for every non-null entry -- the TRSM of the
+ * multi-GPU schedule pushing its panel tiles into peer ranks' panel buffers
+ * (CUDA IPC mappings, NVLink stores) from the GEMM epilogue */
+int gpb_dev_gemm_mirror(gpb_ctx* ctx, void* stream, const gpb_gemm_job* jobs, int64_t njobs,
+                        int64_t b, int64_t lda, int64_t ldb, int64_t ldc, int a_kmajor, int b_kmajor,
+                        int64_t ktile, int64_t kstride, double alpha, double beta,
+                        double* const* mirrors, int64_t nmirror);
+/* peer memory and stream-ordered flags for the fused panel exchange:
+ * zeroed device memory with its CUDA IPC handle (GPB_IPC_HANDLE_BYTES bytes),
+ * a peer's mapping of it, and 64-bit flags written / awaited in stream order
+ * (cuStreamWriteValue64 after a fence; cuStreamWaitValue64 >=, no SM spins) */
+#define GPB_IPC_HANDLE_BYTES 64
+int gpb_dev_ipc_alloc(gpb_ctx* ctx, int64_t bytes, void** ptr, void* handle);
+int gpb_dev_ipc_open(gpb_ctx* ctx, const void* handle, void** ptr);
+int gpb_dev_ipc_close(gpb_ctx* ctx, void* ptr);
+int gpb_dev_free(gpb_ctx* ctx, void* ptr);
+int gpb_dev_signal(gpb_ctx* ctx, void* stream, uint64_t* flag, uint64_t value);
+int gpb_dev_wait(gpb_ctx* ctx, void* stream, const uint64_t* flag, uint64_t value);
 /* batched tile GEMV: y (+)= alpha * op(a) x; outputs must be distinct per call */
 int gpb_dev_gemv(gpb_ctx* ctx, void* stream, const gpb_gemv_job* jobs, int64_t njobs, int64_t b,
                  int trans, double alpha, int accumulate);

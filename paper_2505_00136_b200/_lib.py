@@ -80,6 +80,16 @@ SIGNATURES = {
                                           ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
                                           ctypes.c_double]),
+    "gpb_dev_gemm_mirror": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                           ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+                                           ctypes.c_double, _vp, ctypes.c_int64]),
+    "gpb_dev_ipc_alloc": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.POINTER(_vp), _vp]),
+    "gpb_dev_ipc_open": (ctypes.c_int, [_vp, _vp, ctypes.POINTER(_vp)]),
+    "gpb_dev_ipc_close": (ctypes.c_int, [_vp, _vp]),
+    "gpb_dev_free": (ctypes.c_int, [_vp, _vp]),
+    "gpb_dev_signal": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_uint64]),
+    "gpb_dev_wait": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_uint64]),
     "gpb_dev_gemv": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                     ctypes.c_double, ctypes.c_int]),
     "gpb_dev_copy": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64]),

@@ -13,6 +13,8 @@
 #include <mutex>
 #include <vector>
 
+#include <cuda.h>
+
 #include "gemm.cuh"
 #include "gpb200.h"
 #include "kernels.cuh"
@@ -195,7 +197,16 @@ int gpb_dev_potrf(gpb_ctx* ctx, void* stream, double* tile, double* dinv, int64_
 int gpb_dev_gemm_tiled(gpb_ctx* ctx, void* stream, const gpb_gemm_job* jobs, int64_t njobs,
                        int64_t b, int64_t lda, int64_t ldb, int64_t ldc, int a_kmajor, int b_kmajor,
                        int64_t ktile, int64_t kstride, double alpha, double beta) {
+  return gpb_dev_gemm_mirror(ctx, stream, jobs, njobs, b, lda, ldb, ldc, a_kmajor, b_kmajor, ktile,
+                             kstride, alpha, beta, nullptr, 0);
+}
+
+int gpb_dev_gemm_mirror(gpb_ctx* ctx, void* stream, const gpb_gemm_job* jobs, int64_t njobs,
+                        int64_t b, int64_t lda, int64_t ldb, int64_t ldc, int a_kmajor, int b_kmajor,
+                        int64_t ktile, int64_t kstride, double alpha, double beta,
+                        double* const* mirrors, int64_t nmirror) {
   if (int s = check_ctx(ctx)) return s;
+  if (nmirror < 0 || (nmirror > 0 && !mirrors)) return gpb_plugin_fail(GPB_INVALID_CONFIG, "bad mirror table");
   if (njobs <= 0) return GPB_OK;
   if (b % GBM) return gpb_plugin_fail(GPB_DIM, "tile size must be a multiple of 128");
   std::vector<GemmJob> gj(njobs);
@@ -234,6 +245,12 @@ int gpb_dev_gemm_tiled(gpb_ctx* ctx, void* stream, const gpb_gemm_job* jobs, int
   p.alpha = alpha;
   p.beta = beta;
   p.max_k = maxk;
+  if (nmirror > 0) {
+    const void* dm = g_ring.stage(mirrors, sizeof(double*) * njobs * nmirror, st, &e);
+    DEV_TRY(e);
+    p.mirror = static_cast<double* const*>(dm);
+    p.nmirror = static_cast<int>(nmirror);
+  }
   // TMA views: the operands' jobs come from arbitrary (torch) allocations, so
   // the view starts at the lowest pointer and is used only if every job's
   // block sits inside one row of the ld-wide view
@@ -293,6 +310,93 @@ int gpb_dev_combine(gpb_ctx* ctx, void* stream, const double* base, const double
                     int64_t nparts, int64_t len, double* out) {
   if (int s = check_ctx(ctx)) return s;
   DEV_TRY(launch_combine(base, parts, nparts, len, out, static_cast<cudaStream_t>(stream)));
+  return GPB_OK;
+}
+
+// ---- peer memory for the fused panel exchange (distributed.py, transport "p2p")
+
+int gpb_dev_ipc_alloc(gpb_ctx* ctx, int64_t bytes, void** ptr, void* handle) {
+  if (int s = check_ctx(ctx)) return s;
+  if (bytes <= 0 || !ptr || !handle) return gpb_plugin_fail(GPB_INVALID_CONFIG, "bad IPC allocation");
+  void* p = nullptr;
+  DEV_TRY(cudaMalloc(&p, static_cast<size_t>(bytes)));
+  DEV_TRY(cudaMemset(p, 0, static_cast<size_t>(bytes)));
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    DEV_TRY(e);
+  }
+  static_assert(sizeof(h) == GPB_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle, &h, sizeof(h));
+  *ptr = p;
+  return GPB_OK;
+}
+
+int gpb_dev_ipc_open(gpb_ctx* ctx, const void* handle, void** ptr) {
+  if (int s = check_ctx(ctx)) return s;
+  if (!handle || !ptr) return gpb_plugin_fail(GPB_INVALID_CONFIG, "bad IPC handle");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  DEV_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return GPB_OK;
+}
+
+int gpb_dev_ipc_close(gpb_ctx* ctx, void* ptr) {
+  if (int s = check_ctx(ctx)) return s;
+  if (ptr) DEV_TRY(cudaIpcCloseMemHandle(ptr));
+  return GPB_OK;
+}
+
+int gpb_dev_free(gpb_ctx* ctx, void* ptr) {
+  if (int s = check_ctx(ctx)) return s;
+  if (ptr) DEV_TRY(cudaFree(ptr));
+  return GPB_OK;
+}
+
+}  // extern "C"
+
+namespace {
+using StreamWrite64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+using StreamWait64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+template <class F>
+F driver_fn(const char* name) {
+  void* f = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPointByVersion(name, &f, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(f);
+}
+}  // namespace
+
+extern "C" {
+
+// *flag = value in stream order, after a memory fence covering the stream's
+// earlier work (flag may live in a peer rank's memory)
+int gpb_dev_signal(gpb_ctx* ctx, void* stream, uint64_t* flag, uint64_t value) {
+  if (int s = check_ctx(ctx)) return s;
+  static StreamWrite64 fn = driver_fn<StreamWrite64>("cuStreamWriteValue64");
+  if (!fn) return gpb_plugin_fail(GPB_CUDA, "cuStreamWriteValue64 unavailable");
+  if (fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value, 0) != CUDA_SUCCESS)
+    return gpb_plugin_fail(GPB_CUDA, "cuStreamWriteValue64 failed");
+  return GPB_OK;
+}
+
+// later work on the stream waits until *flag >= value (no SM is occupied)
+int gpb_dev_wait(gpb_ctx* ctx, void* stream, const uint64_t* flag, uint64_t value) {
+  if (int s = check_ctx(ctx)) return s;
+  static StreamWait64 fn = driver_fn<StreamWait64>("cuStreamWaitValue64");
+  if (!fn) return gpb_plugin_fail(GPB_CUDA, "cuStreamWaitValue64 unavailable");
+  static const unsigned flags = [] {
+    int dev = 0, can = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&can, cudaDevAttrCanFlushRemoteWrites, dev);
+    return can ? static_cast<unsigned>(CU_STREAM_WAIT_VALUE_FLUSH) : 0u;
+  }();
+  if (fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value,
+         CU_STREAM_WAIT_VALUE_GEQ | flags) != CUDA_SUCCESS)
+    return gpb_plugin_fail(GPB_CUDA, "cuStreamWaitValue64 failed");
   return GPB_OK;
 }
 

@@ -229,6 +229,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_grouped_kernel(cons
         v.y += beta * c.y;
       }
       *reinterpret_cast<double2*>(job.Cout + row * ldc + col) = v;
+      if (p.nmirror > 0) {
+        store_mirrors(p, job_id, row * ldc + col, v.x);
+        store_mirrors(p, job_id, row * ldc + col + 1, v.y);
+      }
       if (EPI == EPI_SUMSQ) {
         colsq[j][0] += v.x * v.x;
         colsq[j][1] += v.y * v.y;

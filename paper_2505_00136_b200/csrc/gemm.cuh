@@ -54,7 +54,21 @@ struct GemmParams {
   int64_t a_extent;
   const double* b_base;
   int64_t b_extent;
+  // mirror stores (the fused panel exchange of the multi-GPU schedule): every
+  // output element of job j is also stored at mirror[j * nmirror + r] + the
+  // same offset from Cout, for the non-null entries r < nmirror -- peer
+  // ranks' buffers mapped through CUDA IPC, written over NVLink
+  double* const* mirror;
+  int nmirror;
 };
+
+// mirror stores of one output element (offset `idx` from the job's Cout)
+GPB_DEVINL void store_mirrors(const GemmParams& p, int job_id, int64_t idx, double v) {
+  for (int r = 0; r < p.nmirror; ++r) {
+    double* m = p.mirror[static_cast<int64_t>(job_id) * p.nmirror + r];
+    if (m) m[idx] = v;
+  }
+}
 
 // one operand of the TMA kernel: a job pointer p maps to row (p - base) / ld,
 // column (p - base) % ld of the tensor map; a tiled-k walk advances kt_rows

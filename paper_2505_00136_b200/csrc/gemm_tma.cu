@@ -312,6 +312,12 @@ __global__ void __launch_bounds__(C::THREADS, C::kMinB)
           }
           if (EPI == EPI_SUMSQ) colsq[j][e] += v[j][e] * v[j][e];
         }
+      if (p.nmirror > 0) {
+#pragma unroll
+        for (int j = 0; j < FN; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) store_mirrors(p, job_id, off + frag_row<BKM>(j, 2 * t + e), v[j][e]);
+      }
     }
     if (EPI == EPI_SUMSQ) {
       double* red = reinterpret_cast<double*>(base);  // [WM][BN], pipeline smem is free

@@ -200,6 +200,48 @@ class DeviceTileOps:
         self.launches += 1
         _lib.check(self.lib.gpb_dev_copy(self.rt.handle, self._s(), arr, len(pairs), nbytes))
 
+    # peer memory / stream-ordered flags (transport "p2p") ------------------------
+    def ipc_alloc(self, nbytes: int):
+        ptr = ctypes.c_void_p()
+        handle = ctypes.create_string_buffer(64)
+        _lib.check(self.lib.gpb_dev_ipc_alloc(self.rt.handle, nbytes, ctypes.byref(ptr), handle))
+        return ptr.value, handle.raw
+
+    def ipc_open(self, handle: bytes) -> int:
+        ptr = ctypes.c_void_p()
+        _lib.check(self.lib.gpb_dev_ipc_open(self.rt.handle, handle, ctypes.byref(ptr)))
+        return ptr.value
+
+    def ipc_close(self, ptr: int):
+        _lib.check(self.lib.gpb_dev_ipc_close(self.rt.handle, ctypes.c_void_p(ptr)))
+
+    def free(self, ptr: int):
+        _lib.check(self.lib.gpb_dev_free(self.rt.handle, ctypes.c_void_p(ptr)))
+
+    def alias(self, ptr: int, shape):
+        return _alias(ptr, shape, self.device)
+
+    def signal(self, addr: int, value: int):
+        _lib.check(self.lib.gpb_dev_signal(self.rt.handle, self._s(), ctypes.c_void_p(addr), value))
+
+    def wait(self, addr: int, value: int):
+        _lib.check(self.lib.gpb_dev_wait(self.rt.handle, self._s(), ctypes.c_void_p(addr), value))
+
+    def gemm_mirror(self, jobs, b, alpha, beta, mirrors):
+        """gemm() whose job j also stores its output at the addresses
+        mirrors[j] (a list of ints, one per peer, 0 = skip)."""
+        if not jobs:
+            return
+        arr = (_lib.GemmJob * len(jobs))(*[
+            _lib.GemmJob(a.data_ptr(), bb.data_ptr(), ci.data_ptr() if ci is not None else None,
+                         co.data_ptr(), k, int(lo)) for a, bb, ci, co, k, lo in jobs])
+        nm = max(1, max(len(m) for m in mirrors))
+        tab = (ctypes.c_void_p * (len(jobs) * nm))(
+            *[m[r] if r < len(m) and m[r] else None for m in mirrors for r in range(nm)])
+        self.launches += 1
+        _lib.check(self.lib.gpb_dev_gemm_mirror(self.rt.handle, self._s(), arr, len(jobs), b, b, b, b, 1, 1,
+                                                0, 0, alpha, beta, tab, nm))
+
     def combine(self, base, parts, out):
         self.launches += 1
         _lib.check(self.lib.gpb_dev_combine(self.rt.handle, self._s(), self._p(base), self._p(parts),
@@ -355,6 +397,11 @@ class DistributedGP:
         self._factored = False
         self._replica = None
         self.timings = {}
+        # panel exchange: "nccl" (broadcasts) or "p2p" (the TRSM epilogue stores
+        # into peer ranks' panel buffers over CUDA IPC, stream-ordered flags)
+        self.transport = os.environ.get("GPB_DIST_TRANSPORT", "nccl")
+        self._p2p = None
+        self._epoch = 0
 
     # -- collectives (src/dst are global ranks of the group) --------------------
     def _bcast(self, t, src):
@@ -415,13 +462,26 @@ class DistributedGP:
         # panel buffers: [set][process row] -> (G, rows_per, b, b), one
         # allocation so every panel tile sits a whole number of tiles from
         # the others (the GEMM's TMA view of the launch's operands needs that)
-        pall = ops.zeros(2, P, G, rows_per, b, b)
+        cuda = getattr(ops, "device", None) is not None and ops.device.type == "cuda"
+        p2p = cuda and self.transport == "p2p" and self.world > 1
+        if p2p:
+            pall, flag_base, peer_base = self._p2p_buffers((2, P, G, rows_per, b, b))
+            self._epoch += 1
+            epoch = self._epoch << 24  # flag values grow across factorisations
+        else:
+            pall = ops.zeros(2, P, G, rows_per, b, b)
         panels = [[pall[h, p] for p in range(P)] for h in range(2)]
         my_p, my_q = divmod(self.rank, Q)
+
+        # flags of rank r: ready[src] at slot src, free[src] at slot world + src
+        def peer_flag(r, slot):
+            return peer_base[r] + pall.numel() * 8 + slot * 8
+
+        def my_flag(slot):
+            return flag_base + slot * 8
         by_col = {}
         for s_, (i, j) in enumerate(self.owned):
             by_col.setdefault(j, []).append((s_, i))
-        cuda = getattr(ops, "device", None) is not None and ops.device.type == "cuda"
         main = torch.cuda.current_stream(ops.device) if cuda else None
         crit = torch.cuda.Stream(device=ops.device, priority=-1) if cuda else None
         on_crit = (lambda: torch.cuda.stream(crit)) if cuda else contextlib.nullcontext
@@ -456,15 +516,38 @@ class DistributedGP:
                     self._bcast(self.dinv[k], own)
                     if k + 1 == T:
                         break
+                    if p2p and g == 0 and s >= 2:
+                        # panel set s % 2 is free once every rank has applied group s - 2
+                        for r in range(self.world):
+                            if r != self.rank:
+                                ops.wait(my_flag(self.world + r), epoch + s - 1)
                     if my_q == k % Q:  # this rank holds panel tiles of column k
                         mine = self.cyc.panel_rows(k, my_p)
-                        ops.gemm([(self.L[self.slot[i, k]], self.dinv[k], None, buf[my_p][g, i // P], b,
-                                   False) for i in mine], b, 1.0, 0.0)
+                        jobs = [(self.L[self.slot[i, k]], self.dinv[k], None, buf[my_p][g, i // P], b, False)
+                                for i in mine]
+                        if p2p:
+                            # fused TRSM + panel exchange: the epilogue also stores
+                            # every tile into each peer's panel buffer (NVLink)
+                            offs = [buf[my_p][g, i // P].data_ptr() - pall.data_ptr() for i in mine]
+                            ops.gemm_mirror(jobs, b, 1.0, 0.0,
+                                            [[peer_base[r] + o if r != self.rank else 0
+                                              for r in range(self.world)] for o in offs])
+                            for r in range(self.world):
+                                if r != self.rank:
+                                    ops.signal(peer_flag(r, self.rank), epoch + k + 1)
+                        else:
+                            ops.gemm(jobs, b, 1.0, 0.0)
                         ops.copy([(buf[my_p][g, i // P], self.L[self.slot[i, k]]) for i in mine])
                     for p in range(P):
                         rows = self.cyc.panel_rows(k, p)
-                        if rows:
-                            self._bcast(buf[p][g, rows[0] // P: rows[-1] // P + 1], p * Q + k % Q)
+                        src = p * Q + k % Q
+                        if not rows:
+                            continue
+                        if p2p:
+                            if src != self.rank:
+                                ops.wait(my_flag(src), epoch + k + 1)
+                        else:
+                            self._bcast(buf[p][g, rows[0] // P: rows[-1] // P + 1], src)
                     # in-group: the group's later columns get panel k (K = b)
                     ops.gemm([(buf[i % P][g, i // P], buf[j % P][g, j // P], self.L[s_], self.L[s_], b,
                                i == j) for j in range(k + 1, k1 + 1) for s_, i in by_col.get(j, [])],
@@ -497,6 +580,10 @@ class DistributedGP:
             else:
                 ops.gemm([(stack(i, gs), stack(j, gs), self.L[s_], self.L[s_], gs * b, i == j)
                           for j in range(j_lo, T) for s_, i in by_col.get(j, [])], b, -1.0, 1.0)
+            if p2p:  # this rank is done reading panel set s % 2
+                for r in range(self.world):
+                    if r != self.rank:
+                        ops.signal(peer_flag(r, self.world + self.rank), epoch + s + 1)
             if cuda:
                 ev_upd[s] = torch.cuda.Event()
                 ev_upd[s].record(main)
@@ -513,6 +600,34 @@ class DistributedGP:
         t3 = self._event()
         self.timings = {"factor_ms": self._elapsed(t0, t1), "solve_ms": self._elapsed(t2, t3)}
         self._factored = True
+
+    def _p2p_buffers(self, shape):
+        """This rank's IPC-shared panel buffer (plus 2 x world flag words after
+        it) and every peer's mapping of theirs; allocated once per instance."""
+        numel = int(np.prod(shape))
+        if self._p2p is None or self._p2p["shape"] != shape:
+            self._p2p_release()
+            ops = self.ops
+            ptr, handle = ops.ipc_alloc(numel * 8 + 2 * self.world * 8)
+            handles = [None] * self.world
+            dist.all_gather_object(handles, handle, group=self.group)
+            peers = [ptr if r == self.rank else ops.ipc_open(handles[r]) for r in range(self.world)]
+            self._p2p = {"shape": shape, "ptr": ptr, "peers": peers,
+                         "pall": ops.alias(ptr, shape)}
+        p = self._p2p
+        return p["pall"], p["ptr"] + numel * 8, p["peers"]
+
+    def _p2p_release(self):
+        if self._p2p is None:
+            return
+        torch.cuda.synchronize(self.ops.device)
+        dist.barrier(group=self.group)  # no peer still writes into our buffer
+        for r, q in enumerate(self._p2p["peers"]):
+            if r != self.rank:
+                self.ops.ipc_close(q)
+        dist.barrier(group=self.group)  # every mapping closed before the free
+        self.ops.free(self._p2p["ptr"])
+        self._p2p = None
 
     def _solve(self):
         ops, b, T = self.ops, self.b, self.T
@@ -693,7 +808,7 @@ class DistributedGP:
 
     def _set_params(self, params: KernelParams) -> None:
         self.params = params
-        self.close()
+        self._close_replica()
         self._factored = False
 
     def optimize(self, opt=None) -> list[float]:
@@ -745,10 +860,15 @@ class DistributedGP:
             n += int(c.value)
         return n
 
-    def close(self):
+    def _close_replica(self):
         if self._replica is not None:
             self._replica.close()
             self._replica = None
+
+    def close(self):
+        """Release the replica and the peer buffers (collective with p2p)."""
+        self._close_replica()
+        self._p2p_release()
 
 
 def _export(rep, n: int) -> np.ndarray:

@@ -162,6 +162,18 @@ def test_four_ranks_2x2_grid_one_gpu_device_kernels(monkeypatch, panels):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("world,kind", [(2, "padded"), (4, "dense")])
+def test_p2p_panel_exchange_one_gpu(monkeypatch, world, kind):
+    """Transport "p2p": the TRSM epilogue stores the panel tiles into the peer
+    ranks' panel buffers (CUDA IPC mappings), readiness and buffer reuse are
+    ordered by stream-written flags -- no broadcast of the panel.  Ranks share
+    cuda:0 here; every wait is a stream memory operation, not a spinning
+    kernel, so no rank's kernel waits on another's."""
+    monkeypatch.setenv("GPB_DIST_TRANSPORT", "p2p")
+    _check(_run(world, kind, device=True), kind)
+
+
+@pytest.mark.gpu
 def test_bench_distributed_branch_two_ranks_one_gpu():
     """bench.py's N>1 path end to end (torchrun, 2 ranks on cuda:0, gloo)."""
     import json
