@@ -281,7 +281,9 @@ int gpb_dev_gemm_mirror(gpb_ctx* ctx, void* stream, const gpb_gemm_job* jobs, in
   };
   view(true, &p.a_base, &p.a_extent);
   view(false, &p.b_base, &p.b_extent);
-  DEV_TRY(launch_gemm(p, a_kmajor != 0, b_kmajor != 0, EPI_AXPBY, st));
+  if (p.nmirror > 0 && !(a_kmajor && b_kmajor))
+    return gpb_plugin_fail(GPB_INVALID_CONFIG, "mirror stores need K-major operands");
+  DEV_TRY(launch_gemm(p, a_kmajor != 0, b_kmajor != 0, p.nmirror > 0 ? EPI_MIRROR : EPI_AXPBY, st));
   return GPB_OK;
 }
 

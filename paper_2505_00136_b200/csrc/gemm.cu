@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) dgemm_grouped_kernel(cons
         v.y += beta * c.y;
       }
       *reinterpret_cast<double2*>(job.Cout + row * ldc + col) = v;
-      if (p.nmirror > 0) {
+      if (EPI == EPI_MIRROR) {
         store_mirrors(p, job_id, row * ldc + col, v.x);
         store_mirrors(p, job_id, row * ldc + col + 1, v.y);
       }
@@ -296,12 +296,17 @@ static cudaError_t init_cfg() {
   GPB_SET(true, true, EPI_SUMSQ)
   GPB_SET(false, false, EPI_SUMSQ)
   GPB_SET(false, true, EPI_AXPBY)
+  GPB_SET(true, true, EPI_MIRROR)
 #undef GPB_SET
   return cudaSuccess;
 }
 
 template <class C>
 static cudaError_t dispatch(const GemmParams& p, bool ak, bool bk, int epi, cudaStream_t s) {
+  if (epi == EPI_MIRROR) {
+    if (ak && bk) return launch<C, true, true, EPI_MIRROR>(p, s);
+    return cudaErrorInvalidValue;
+  }
   if (epi == EPI_AXPBY) {
     if (ak && bk) return launch<C, true, true, EPI_AXPBY>(p, s);
     if (ak && !bk) return launch<C, true, false, EPI_AXPBY>(p, s);

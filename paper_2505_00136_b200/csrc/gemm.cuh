@@ -24,7 +24,8 @@ namespace gpb {
 // deepest k stage any kernel configuration uses).
 constexpr int GBM = 128, GBN = 128, GBK = 32;
 
-enum GemmEpi : int { EPI_AXPBY = 0, EPI_SUMSQ = 1 };
+// EPI_MIRROR: EPI_AXPBY plus the mirror stores of GemmParams (K-major A and B)
+enum GemmEpi : int { EPI_AXPBY = 0, EPI_SUMSQ = 1, EPI_MIRROR = 2 };
 
 struct __align__(16) GemmJob {
   const double* A;

@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(C::THREADS, C::kMinB)
           }
           if (EPI == EPI_SUMSQ) colsq[j][e] += v[j][e] * v[j][e];
         }
-      if (p.nmirror > 0) {
+      if (EPI == EPI_MIRROR) {
 #pragma unroll
         for (int j = 0; j < FN; ++j)
 #pragma unroll
@@ -448,6 +448,7 @@ cudaError_t tma_dispatch(const GemmParams& p, bool ak, bool bk, int epi, const C
   GPB_TMA(true, true, EPI_SUMSQ)
   GPB_TMA(true, false, EPI_SUMSQ)
   GPB_TMA(false, false, EPI_SUMSQ)
+  GPB_TMA(true, true, EPI_MIRROR)
 #undef GPB_TMA
   return cudaErrorInvalidValue;
 }
