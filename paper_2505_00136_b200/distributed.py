@@ -527,11 +527,16 @@ class DistributedGP:
                                 for i in mine]
                         if p2p:
                             # fused TRSM + panel exchange: the epilogue also stores
-                            # every tile into each peer's panel buffer (NVLink)
-                            offs = [buf[my_p][g, i // P].data_ptr() - pall.data_ptr() for i in mine]
-                            ops.gemm_mirror(jobs, b, 1.0, 0.0,
-                                            [[peer_base[r] + o if r != self.rank else 0
-                                              for r in range(self.world)] for o in offs])
+                            # tile i into the panel buffer of every peer that
+                            # reads it -- process row i mod P (its tiles (i, j))
+                            # and process column i mod Q (its tiles (r, i)) --
+                            # 1/P + 1/Q of the panel per rank instead of all of it
+                            def dest(i, r):
+                                return r != self.rank and (r // Q == i % P or r % Q == i % Q)
+
+                            ops.gemm_mirror(jobs, b, 1.0, 0.0, [
+                                [peer_base[r] + buf[my_p][g, i // P].data_ptr() - pall.data_ptr()
+                                 if dest(i, r) else 0 for r in range(self.world)] for i in mine])
                             for r in range(self.world):
                                 if r != self.rank:
                                     ops.signal(peer_flag(r, self.rank), epoch + k + 1)
