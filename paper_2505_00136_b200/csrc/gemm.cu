@@ -3,7 +3,9 @@
 //
 // The warp layout (WM x WN warps), k depth per stage (BK) and stage count are
 // template parameters (GemmCfg); launch_gemm selects the configuration that
-// measured fastest on B200 (profiles/README.md), GPB_GEMM_CFG overrides it.
+// measured fastest on B200 (profiles/r01_gemm_configs.txt), GPB_GEMM_CFG overrides it;
+// launches whose operands have tensor-map views run the TMA kernel instead
+// (gemm_tma.cu).
 //
 // Shared-memory layouts are padded so both DMMA fragment loads and the
 // 16-byte cp.async stores are bank-conflict free:
