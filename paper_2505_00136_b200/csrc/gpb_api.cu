@@ -612,7 +612,7 @@ int ensure_factor(gpb_model* m) {
     CUDA_TRY(cudaEventRecord(ev_upd[s], m->st));
   }
   if (m->potrf_prof) {  // GPB_POTRF_PROF: per-phase cycles of the tile kernel
-    long long h[33];
+    long long h[44];
     cudaStreamSynchronize(m->crit);
     cudaMemcpy(h, m->potrf_prof, sizeof(h), cudaMemcpyDeviceToHost);
     fprintf(stderr, "potrf B-phase end per CTA (warp 0):");
@@ -1214,8 +1214,8 @@ int model_create(gpb_ctx* ctx, const double* z, const double* y, int64_t n, int6
   }
   if (s == GPB_OK) s = alloc_model_buffers(m);
   if (s == GPB_OK && getenv("GPB_POTRF_PROF")) {
-    cudaMalloc(&m->potrf_prof, 33 * sizeof(long long));
-    cudaMemset(m->potrf_prof, 0, 33 * sizeof(long long));
+    cudaMalloc(&m->potrf_prof, 44 * sizeof(long long));
+    cudaMemset(m->potrf_prof, 0, 44 * sizeof(long long));
   }
   if (s == GPB_OK) s = upload_train(m, z, y, device_ptrs);
   if (s != GPB_OK) {

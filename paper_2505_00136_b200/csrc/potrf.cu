@@ -6,22 +6,21 @@
 // triangular solve of the hot path (panel TRSM tiles.py:140-146, vector
 // solves tiles.py:170-180, panel solves tiles.py:182-185) into DMMA products.
 //
-// Blocked Cholesky with 32-column panels.  Per panel p, two phases:
-//   B (CTA 0 warp 0) factor the 32x32 diagonal block -- the serial pivot
-//                   chain in registers, each new column broadcast through
-//                   shared memory;
-//     (CTA 0 warp 1) invert it by a column sweep one pivot behind the chain;
-//     (other warps) panel p-1's rank-32 update of every 32-block below the
-//                   diagonal block (right-looking) and the TRTRI of Dinv
-//                   (finalise block row p-1, accumulate term p-2);
-//   C (all warps)   solve the rows below the diagonal block (x Li^T); the
-//                   warp of row block p+1 also applies panel p to the next
-//                   diagonal block, so B(p+1) can start at once;
-// so the DMMA work of the update and of TRTRI runs while the pivot chain
-// advances.  The warp jobs of every phase are dealt over all warps of the
-// cluster and the phases are separated by cluster barriers (release/acquire
-// at cluster scope orders the global-memory tile between the SMs), so the
-// lookahead DMMA work is spread over CL SMs while CTA 0's warp 0 runs the
+// Blocked Cholesky with 32-column panels, two phases per panel separated by
+// cluster barriers (release/acquire at cluster scope orders the tile in
+// global memory between the SMs):
+//   B(p)  CTA 0 warp 0: pivot chain of the 32x32 diagonal block in registers;
+//         CTA 0 warp 1: its inverse by a column sweep one pivot behind;
+//         other CTAs: panel p-1's rank-32 update of every trailing 32-block
+//         (right-looking) and the TRTRI of Dinv; CTA 0 warps 2..5: panel
+//         p-1 applied to blocks (p+1, p) and (p+1, p+1), kept in shared
+//         memory;
+//   C(p)  CTA 0 warps 2..5: block row p+1 solved (x Li^T) and applied to
+//         (p+1, p+1) in shared memory -- all the next chain needs; other
+//         CTAs: the other rows and TRTRI terms, as 8-row fragments.
+// Lookahead: once the critical warps are done (named barrier), the chain and
+// inverse warps arrive at the C(p) barrier and run panel p+1 before waiting
+// on it, so the rest of C(p), the next B jobs and both barriers overlap the
 // pivot chain.  Epilogue: Sigma log L_jj over real (non-padding) pivots and a
 // LAPACK-style info word holding the first failing original pivot index.
 #include <cstdlib>
@@ -216,27 +215,19 @@ GPB_DEVINL void trtri_acc_frag(const double* T, double* D, int bi, int I, int J,
   store_frag(D + r * bi + J * NB, bi, acc, g, t, K == J, -1.0);
 }
 
-// the cluster's warps except CTA 0's warps 0..3, numbered so that
-// consecutive indices sit on different CTAs first, then on different SMSPs
-GPB_DEVINL int c_worker(int cta, int ncta, int lw) {
-  return cta + ncta * lw - min(4, lw + (cta > 0 ? 1 : 0));
-}
-
-// all threads of the cluster (a plain launch is a cluster of one CTA)
-GPB_DEVINL void cluster_barrier(bool clustered) {
-  if (clustered)
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
-                     : "memory");
-  else
-    __syncthreads();
-}
-
 }  // namespace
 
 __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
   extern __shared__ double sm[];
   double* Ld = sm;                 // [64][33] factor block (rows 32..63: padding)
   double* rdg = Ld + 2 * NB * SLD;  // [32] 1 / l_jj of the current panel
+  // CTA 0's critical path through shared memory ([32][33] each): Ls = Li of
+  // the current panel (from the inverse warp), Ts = block (p+1, p) and
+  // Dd = block (p+1, p+1) as updated by the critical warps, Xs = L(p+1, p)
+  double* Ls = rdg + NB;
+  double* Ts = Ls + NB * SLD;
+  double* Dd = Ts + NB * SLD;
+  double* Xs = Dd + NB * SLD;
   __shared__ volatile int prog_s;  // pivots of the chain published so far
   volatile int* prog = &prog_s;
   // every CTA reads info before the first cluster barrier; only CTA 0
@@ -247,17 +238,22 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
   double* D = a.dinv;
   const int P = bi / NB;
   const int tid = threadIdx.x, lane = tid & 31;
-  const int cta = blockIdx.x, ncta = gridDim.x;
-  const bool clustered = ncta > 1;
+  const int cta = blockIdx.x, ncta = gridDim.x;  // a cluster of >= 2 CTAs
   const bool lead = cta == 0;
   const int lw = tid >> 5;                 // warp index within the CTA
   const int warp = cta * NW + lw;          // warp index within the cluster
   const int GW = ncta * NW;                // warps in the cluster
   const int g = lane >> 2, t = lane & 3;
   const bool factor = !a.trtri_only;
+  // CTA 0: warp 0 runs the pivot chain, warp 1 the diagonal-block inverse,
+  // warps 2..5 (one per SMSP; the chain and inverse warps are idle while they
+  // work) the critical block row; the other CTAs' warps take every other job
+  const bool chain_w = lead && lw == 0, inv_w = lead && lw == 1;
+  const int crit = (lead && lw >= 2 && lw < 6) ? lw - 2 : -1;
+  const int wj = lead ? -1 : (cta - 1) + (ncta - 1) * lw;  // job-warp index, CTAs first
+  const int nwj = GW - NW;
   double logsum = 0.0;  // meaningful in lane 0 of warp 0
   if (tid == 0) *prog = 0;
-  cluster_barrier(clustered);
   long long t_last = clock64(), t_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   // per-phase cycles of thread 0 of CTA 0 (slots 0-7) and of CTA 1 (8-15)
 #define PROF_MARK(i)                                   \
@@ -266,61 +262,20 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
     t_acc[i] += now_ - t_last;                         \
     t_last = now_;                                     \
   }
+  auto arrive = [] { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); };
+  auto wait = [] { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); };
 
-  long long t_phase = 0;  // profiling: start of phase B of this panel
-  for (int p = 0; p < P; ++p) {
+  // B-phase pivot chain of diagonal block p (CTA 0 warp 0): lane i keeps row
+  // i of the block in registers, shifted so that register 0 always holds the
+  // current pivot column (LAPACK dpotf2 order); each new column of L is
+  // published to the inverse warp through Ld and the progress counter.
+  auto chain = [&](int p) {
     const int c0 = p * NB;
-    PROF_MARK(0)
-    if (a.prof && lane == 0) t_phase = clock64();
-    if (!(lead && lw < 2)) {
-      // B, job warps (CTAs 1.. when clustered, else warps 2..7), dealt
-      // round-robin: panel p-1's rank-32 contribution to every 32-block
-      // (rb, cb), p <= cb <= rb, below the diagonal block (right-looking;
-      // the diagonal block (p, p) got it in C(p-1)), the finalisation of
-      // block row p-1 of the inverse, and the TRTRI term K = p-2 of rows I >= p
-      const int m = P - p;  // block rows p .. P-1; (p, p) excluded
-      const int pre = (factor && p > 0) ? m * (m + 1) / 2 - 1 : 0;
-      const int inv = (p >= 2) ? p - 1 : 0;  // blocks J = 0..p-2 of row I = p-1
-      const int accn = (p >= 2) ? (P - p) * (p - 1) : 0;  // term K = p-2 of rows I >= p
-      // clustered: CTA 0 keeps only the pivot chain so its SMSPs are not
-      // shared with DMMA warps; the other CTAs' warps take the jobs
-      // consecutive jobs go to different CTAs first, then to different warps
-      // (SMSPs) of a CTA: a K = 32 job is DMMA-issue bound on its SMSP
-      const int w0 = clustered ? (lead ? -1 : (cta - 1) + (ncta - 1) * lw) : warp - 2;
-      const int nwk = clustered ? GW - NW : NW - 2;
-      // whole 32x32 jobs here (row fragments would repeat the B operand's
-      // loads four times: this phase is load-bound, measured slower)
-      for (int q = (w0 >= 0 ? w0 : pre + inv + accn); q < pre + inv + accn; q += nwk) {
-        if (q < pre) {
-          const int qq = q + 1;  // skip (p, p)
-          int rr = static_cast<int>((sqrtf(8.0f * qq + 1.0f) - 1.0f) * 0.5f);
-          while (rr * (rr + 1) / 2 > qq) --rr;
-          while ((rr + 1) * (rr + 2) / 2 <= qq) ++rr;
-          const int rb = p + rr, cb = p + (qq - rr * (rr + 1) / 2);
-          double acc[4][4][2];
-          zero_acc(acc);
-          warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi + c0 - NB, bi,
-                  T + static_cast<int64_t>(cb) * NB * bi + c0 - NB, bi, NB, g, t);
-          store_acc(T + static_cast<int64_t>(rb) * NB * bi + cb * NB, bi, acc, g, t, false, 1.0);
-        } else if (q < pre + inv) {
-          trtri_fin(D, bi, p - 1, q - pre, g, t);
-        } else {
-          const int w = q - pre - inv;
-          trtri_acc(T, D, bi, p + w / (p - 1), w % (p - 1), p - 2, g, t);
-        }
-      }
-      PROF_MARK(5)
-      if (a.prof && lane == 0 && lw == 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.prof + 16 + cta),
-                                                    static_cast<unsigned long long>(clock64() - t_phase));
-    } else if (lead && lw == 0) {
-      // B, chain: lane i keeps row i of the diagonal block in registers,
-      // shifted so that register 0 always holds the current pivot column
-      // (short code: the pivot loop is not unrolled; LAPACK dpotf2 order).
-      // After pivot j, row j of L is complete: publish it to the inverse warp.
       const int base = p * NB;
       double r[NB];
 #pragma unroll
-      for (int c = 0; c < NB; ++c) r[c] = T[static_cast<int64_t>(c0 + lane) * bi + c0 + c];
+      for (int c = 0; c < NB; ++c)  // panel 0 from the tile, later ones as the critical warps left them
+        r[c] = (p == 0 || !factor) ? T[static_cast<int64_t>(c0 + lane) * bi + c0 + c] : Dd[lane * SLD + c];
       int fail = -1;
       double my_l = 1.0;
       if (factor) {
@@ -412,13 +367,13 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
           *prog = base + NB;
         }
       }
-      PROF_MARK(6)
-    } else if (lead && lw == 1) {
-      // B, inverse of the diagonal block by a column sweep that trails the
-      // chain by one pivot: lane k holds column k of Li = L^-1 in registers
-      // (forward substitution of e_k), and step j needs only column j of L,
-      // published by the chain right after pivot j:
-      //   x_j *= 1 / l_jj;   x_i -= l_ij x_j  (i > j, independent FMAs)
+  };
+  // inverse of diagonal block p by a column sweep one pivot behind the chain
+  // (CTA 0 warp 1): lane k holds column k of Li = L^-1 in registers (forward
+  // substitution of e_k); step j needs only column j of L:
+  //   x_j *= 1 / l_jj;   x_i -= l_ij x_j  (i > j, independent FMAs)
+  auto inverse = [&](int p) {
+    const int c0 = p * NB;
       const int base = p * NB;
       double x[NB];
 #pragma unroll
@@ -433,45 +388,117 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
         for (int i = j + 1; i < NB; ++i) x[i] = fma(-Ld[i * SLD + j], x[j], x[i]);
       }
 #pragma unroll
-      for (int i = 0; i < NB; ++i) D[static_cast<int64_t>(c0 + i) * bi + c0 + lane] = x[i];
-      if (a.prof && lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.prof + 32),
-                                         static_cast<unsigned long long>(clock64() - t_phase));
-    }
-    cluster_barrier(clustered);
-    PROF_MARK(1)
-    if (*reinterpret_cast<volatile int*>(a.info) >= 0) return;  // set by CTA 0 above
-    // C: below-diagonal panel rows, L[r][c0:c0+32] = T[r][c0:c0+32] * Li^T
-    // (Li read back from the diagonal block of D, written by CTA 0); the warp
-    // of row block p+1 then applies panel p to the next diagonal block
-    // (p+1, p+1), which is all the chain of B(p+1) needs.  Also the TRTRI
-    // term K = p-1 of row I = p, which B(p+1) finalises.
-    {
-      const int nt = factor ? P - p - 1 : 0;
-      const int na = p >= 1 ? p : 0;  // J = 0..p-1
-      // The critical path, block row p+1 (which B(p+1) needs first), runs on
-      // CTA 0's warps 0..3, one 8-row fragment each: X = T * Li^T, then, after
-      // a named barrier of the four warps, (p+1, p+1) -= X X^T.  Every other
-      // row block and TRTRI term is split into row fragments dealt to the
-      // remaining warps (c_worker).
-      const double* Li = D + static_cast<int64_t>(c0) * bi + c0;
-      if (lead && lw < 4) {
-        if (nt > 0) {
-          double* blk = T + static_cast<int64_t>(p + 1) * NB * bi + c0;
-          double* mine = blk + static_cast<int64_t>(8 * lw) * bi;
-          double acc[4][2];
-          frag_nt(acc, mine, bi, Li, bi, g, t);
-          __syncwarp();
-          store_frag(mine, bi, acc, g, t, true, 1.0);
-          __threadfence_block();
-          asm volatile("bar.sync 1, 128;\n" ::: "memory");
-          frag_nt(acc, mine, bi, blk, bi, g, t);
-          store_frag(mine + NB, bi, acc, g, t, false, 1.0);
+      for (int i = 0; i < NB; ++i) {
+        D[static_cast<int64_t>(c0 + i) * bi + c0 + lane] = x[i];
+        Ls[i * SLD + lane] = x[i];
+      }
+  };
+
+  // Per panel p two phases separated by cluster barriers X_B(p), X_C(p):
+  //   B(p): chain(p) and inverse(p) (done one phase early, see below); the
+  //         job warps apply panel p-1's rank-32 update to every trailing
+  //         32-block except (p, p), (p+1, p), (p+1, p+1), finalise block row
+  //         p-1 of Dinv and add the TRTRI term K = p-2; the critical warps
+  //         apply panel p-1 to (p+1, p) and (p+1, p+1).
+  //   C(p): the critical warps solve block row p+1 (X = T(p+1,p) Li(p)^T, one
+  //         8-row fragment each) and apply it to (p+1, p+1) -- all the next
+  //         chain needs; the job warps solve the other rows and add the TRTRI
+  //         term K = p-1 of row p.
+  // Lookahead: the chain and inverse warps only wait for the critical warps
+  // (named barrier 2), arrive at X_C(p) and run chain(p+1) / inverse(p+1)
+  // before waiting for X_C(p), so the rest of C(p) and both barrier
+  // latencies overlap the next pivot chain.
+  arrive();
+  wait();
+  if (chain_w) chain(0);
+  if (inv_w) inverse(0);
+  for (int p = 0; p < P; ++p) {
+    const int c0 = p * NB;
+    const bool next = factor && p + 1 < P;  // block row p+1 exists: critical work in C(p)
+    PROF_MARK(0)
+    if (wj >= 0) {
+      const int m = P - p;  // block rows p .. P-1
+      const int skip = next ? 3 : 1;  // (p, p), and (p+1, p), (p+1, p+1) to the critical warps
+      const int pre = (factor && p > 0) ? m * (m + 1) / 2 - skip : 0;
+      const int inv = (p >= 2) ? p - 1 : 0;  // blocks J = 0..p-2 of row I = p-1
+      const int accn = (p >= 2) ? (P - p) * (p - 1) : 0;  // term K = p-2 of rows I >= p
+      for (int q = wj; q < pre + inv + accn; q += nwj) {
+        if (q < pre) {
+          const int qq = q + skip;
+          int rr = static_cast<int>((sqrtf(8.0f * qq + 1.0f) - 1.0f) * 0.5f);
+          while (rr * (rr + 1) / 2 > qq) --rr;
+          while ((rr + 1) * (rr + 2) / 2 <= qq) ++rr;
+          const int rb = p + rr, cb = p + (qq - rr * (rr + 1) / 2);
+          double acc[4][4][2];
+          zero_acc(acc);
+          warp_nt(acc, T + static_cast<int64_t>(rb) * NB * bi + c0 - NB, bi,
+                  T + static_cast<int64_t>(cb) * NB * bi + c0 - NB, bi, NB, g, t);
+          store_acc(T + static_cast<int64_t>(rb) * NB * bi + cb * NB, bi, acc, g, t, false, 1.0);
+        } else if (q < pre + inv) {
+          trtri_fin(D, bi, p - 1, q - pre, g, t);
+        } else {
+          const int w = q - pre - inv;
+          trtri_acc(T, D, bi, p + w / (p - 1), w % (p - 1), p - 2, g, t);
         }
-      } else {
-        const int nw = GW - 4;
-        const int nrow = nt > 0 ? 4 * (nt - 1) : 0;
+      }
+      PROF_MARK(5)
+    } else if (crit >= 0 && next) {
+      // blocks (p+1, p) and (p+1, p+1) into Ts / Dd, with panel p-1 applied
+      // (row fragment `crit`; they stay in shared memory for C(p))
+      const int64_t row = static_cast<int64_t>(p + 1) * NB + 8 * crit;
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const int cb = p + h;
+        double* sdst = (h ? Dd : Ts) + 8 * crit * SLD;
+        const double* src = T + row * bi + cb * NB;
+        double acc[4][2];
+        if (p > 0)
+          frag_nt(acc, T + row * bi + c0 - NB, bi, T + static_cast<int64_t>(cb) * NB * bi + c0 - NB, bi, g, t);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = 8 * j + 2 * t + e;
+            sdst[g * SLD + col] = src[static_cast<int64_t>(g) * bi + col] - (p > 0 ? acc[j][e] : 0.0);
+          }
+      }
+    }
+    arrive();  // X_B(p)
+    wait();
+    PROF_MARK(1)
+    if (*reinterpret_cast<volatile int*>(a.info) >= 0) return;  // set by the chain
+    const double* Li = D + static_cast<int64_t>(c0) * bi + c0;
+    if (chain_w || inv_w) {
+      if (next) asm volatile("bar.sync 2, 192;\n" ::: "memory");  // (p+1, p+1) is final
+      arrive();  // X_C(p)
+      if (p + 1 < P) {
+        if (chain_w) chain(p + 1);
+        else inverse(p + 1);
+      }
+      wait();
+    } else {
+      if (crit >= 0) {
+        if (next) {
+          // X = Ts Ls^T (row fragment `crit`) -> L(p+1, p) in T and in Xs
+          double* mine = T + (static_cast<int64_t>(p + 1) * NB + 8 * crit) * bi + c0;
+          double acc[4][2];
+          __syncwarp();
+          frag_nt(acc, Ts + 8 * crit * SLD, SLD, Ls, SLD, g, t);
+          store_frag(mine, bi, acc, g, t, true, 1.0);
+          store_frag(Xs + 8 * crit * SLD, SLD, acc, g, t, true, 1.0);
+          asm volatile("bar.sync 1, 128;\n" ::: "memory");  // the four fragments of X
+          // Dd -= X X^T: the next chain's input, left in shared memory
+          frag_nt(acc, Xs + 8 * crit * SLD, SLD, Xs, SLD, g, t);
+          store_frag(Dd + 8 * crit * SLD, SLD, acc, g, t, false, 1.0);
+          __threadfence_block();
+          asm volatile("bar.arrive 2, 192;\n" ::: "memory");
+        }
+      } else if (wj >= 0) {
+        const int nt = factor ? P - p - 1 : 0;
+        const int na = p >= 1 ? p : 0;  // J = 0..p-1
+        const int nrow = nt > 1 ? 4 * (nt - 1) : 0;  // rows p+2 .. P-1, 4 fragments each
         const int nsub = nrow + 4 * na;
-        for (int q = c_worker(cta, ncta, lw); q < nsub; q += nw) {
+        for (int q = wj; q < nsub; q += nwj) {
           const int f = q % 4;
           if (q < nrow) {
             double* mine = T + (static_cast<int64_t>(p + 2 + q / 4) * NB + 8 * f) * bi + c0;
@@ -484,9 +511,10 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
           }
         }
       }
+      PROF_MARK(7)
+      arrive();  // X_C(p)
+      wait();
     }
-    PROF_MARK(7)
-    cluster_barrier(clustered);
     PROF_MARK(2)
   }
   // last block row of the inverse (its last term came in C(P-1)): X_II * D_IJ
@@ -508,11 +536,11 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
 #undef PROF_MARK
 }
 
-size_t potrf_smem_bytes() { return sizeof(double) * (2 * NB * SLD + NB); }
+size_t potrf_smem_bytes() { return sizeof(double) * (6 * NB * SLD + NB); }
 
 static int g_cluster = -1;
 
-// CTAs per diagonal tile: GPB_POTRF_CLUSTER (1 = single CTA, 2, 4, 8 or 16),
+// CTAs per diagonal tile: GPB_POTRF_CLUSTER (2, 4, 8 or 16),
 // else 16 where POTRF is on the critical path -- factorisations of fewer
 // than 48 diagonal tiles (config 1 factor 8.8 -> 8.2 ms) and the last 8 tiles
 // of larger ones -- and 8 otherwise (hidden behind the trailing update,
@@ -521,7 +549,7 @@ static int potrf_cluster(int tiles, int remaining) {
   if (g_cluster < 0) {
     const char* e = getenv("GPB_POTRF_CLUSTER");
     const int c = e ? atoi(e) : 0;
-    g_cluster = (c == 1 || c == 2 || c == 4 || c == 8 || c == 16) ? c : 0;
+    g_cluster = (c == 2 || c == 4 || c == 8 || c == 16) ? c : 0;
   }
   if (g_cluster > 0) return g_cluster;
   return ((tiles > 0 && tiles < 48) || (remaining > 0 && remaining <= 8)) ? 16 : 8;
@@ -529,10 +557,6 @@ static int potrf_cluster(int tiles, int remaining) {
 
 cudaError_t launch_potrf(const PotrfArgs& a, cudaStream_t s) {
   const int cl = potrf_cluster(a.tiles, a.remaining);
-  if (cl == 1) {
-    potrf_tile_kernel<<<1, PT, potrf_smem_bytes(), s>>>(a);
-    return cudaGetLastError();
-  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(cl);
   cfg.blockDim = dim3(PT);
