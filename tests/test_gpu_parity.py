@@ -357,6 +357,22 @@ class TestTilePlugin:
         a = a @ a.T + 300 * np.eye(300)
         assert rel(gpb.B200TileKernels.potrf(a), np.linalg.cholesky(a)) <= 1e-13
 
+    @pytest.mark.parametrize("b,k", [(256, 5), (256, 40), (512, 33), (512, 300), (512, 511)])
+    def test_potrf_failure_deep_in_the_tile(self, runtime, b, k):
+        """A non-positive pivot in any panel of the tile kernel -- including the
+        panels the chain factors ahead, inside the previous panel's barrier
+        window -- raises NotPositiveDefinite naming that pivot, like LAPACK's
+        info (tiles.py:29-33)."""
+        rng = np.random.default_rng(k)
+        x = rng.normal(size=(b, b)) / np.sqrt(b)
+        a = x @ x.T + np.eye(b)
+        a[k, :] = a[:, k] = 0.0
+        a[k, k] = -1.0
+        with pytest.raises(NotPositiveDefinite, match=f"index {k}\\b"):
+            gpb.B200TileKernels.potrf(a)
+        a[k, k] = 2.0  # now positive definite again
+        assert rel(gpb.B200TileKernels.potrf(a), np.linalg.cholesky(a)) <= 1e-13
+
     def test_trsm_syrk_gemm(self, runtime):
         rng = np.random.default_rng(1)
         a = rng.normal(size=(200, 200))
