@@ -291,36 +291,64 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
         // columns, so the rsqrt latency hides behind those FMAs; progress is
         // published every two pivots.
         constexpr int SP = 8;
-        double piv = __shfl_sync(0xffffffffu, r[0], 0);
-        double rinv = rsqrt(piv);
+        // Pivots go in pairs (j, j+1): from A_jj, A_j+1,j and A_j+1,j+1 (three
+        // shuffles) l_jj, l_j+1,j and l_j+1,j+1 follow in registers, every lane
+        // forms both of its column entries, and one shared-memory exchange
+        // serves both pivots -- the same operations in the same order as
+        // pivoting one column at a time, so the factor is unchanged.
+        double av = __shfl_sync(0xffffffffu, r[0], 0);
+        double bv = __shfl_sync(0xffffffffu, r[0], 1);
+        double cv = __shfl_sync(0xffffffffu, r[1], 1);
 #pragma unroll 1
         for (int j0 = 0; j0 < NB; j0 += SP) {
           double lc[SP];
 #pragma unroll
-          for (int t = 0; t < SP; ++t) {  // register t holds column j = j0 + t
+          for (int t = 0; t < SP; t += 2) {  // registers t, t+1 hold columns j, j+1
             const int j = j0 + t;
-            if (fail < 0 && !(piv > 0.0)) fail = j;
-            const double lcol = (lane == j) ? piv * rinv : (lane > j ? r[t] * rinv : 0.0);
-            lc[t] = lcol;
+            if (fail < 0 && !(av > 0.0)) fail = j;
+            const double rinv0 = rsqrt(av);
+            const double l10 = bv * rinv0;
+            const double sv = fma(-l10, l10, cv);
+            if (fail < 0 && !(sv > 0.0)) fail = j + 1;
+            const double rinv1 = rsqrt(sv);
+            const double lcol0 = (lane == j) ? av * rinv0 : (lane > j ? r[t] * rinv0 : 0.0);
+            const double u = fma(-lcol0, l10, r[t + 1]);
+            const double lcol1 = (lane == j + 1) ? sv * rinv1 : (lane > j + 1 ? u * rinv1 : 0.0);
+            lc[t] = lcol0;
+            lc[t + 1] = lcol1;
             if (lane == j) {
-              my_l = lcol;
-              rdg[j] = rinv;
+              my_l = lcol0;
+              rdg[j] = rinv0;
             }
-            Ld[lane * SLD + j] = lcol;
+            if (lane == j + 1) {
+              my_l = lcol1;
+              rdg[j + 1] = rinv1;
+            }
+            Ld[lane * SLD + j] = lcol0;
+            Ld[lane * SLD + j + 1] = lcol1;
             __syncwarp();
-            if ((t & 1) && lane == 0) {
+            if (lane == 0) {
               __threadfence_block();
-              *prog = base + j + 1;
+              *prog = base + j + 2;
             }
-            if (t + 1 < SP) {
-              // lrow[c * SLD] = l_(j0 + c), j from shared memory (one address
-              // per load)
-              const double* lrow = Ld + j0 * SLD + j;
-              r[t + 1] = fma(-lcol, lrow[(t + 1) * SLD], r[t + 1]);
-              piv = __shfl_sync(0xffffffffu, r[t + 1], j + 1);
-              rinv = rsqrt(piv);
+            if (t + 2 < SP) {
+              // l0[c * SLD] = l_(j0 + c), j and l1[c * SLD] = l_(j0 + c), j+1 from
+              // shared memory (one address per load); the next pair's columns first
+              const double* l0 = Ld + j0 * SLD + j;
+              const double* l1 = l0 + 1;
 #pragma unroll
-              for (int c = t + 2; c < SP; ++c) r[c] = fma(-lcol, lrow[c * SLD], r[c]);
+              for (int c = t + 2; c < t + 4; ++c) {
+                r[c] = fma(-lcol0, l0[c * SLD], r[c]);
+                r[c] = fma(-lcol1, l1[c * SLD], r[c]);
+              }
+              av = __shfl_sync(0xffffffffu, r[t + 2], j + 2);
+              bv = __shfl_sync(0xffffffffu, r[t + 2], j + 3);
+              cv = __shfl_sync(0xffffffffu, r[t + 3], j + 3);
+#pragma unroll
+              for (int c = t + 4; c < SP; ++c) {
+                r[c] = fma(-lcol0, l0[c * SLD], r[c]);
+                r[c] = fma(-lcol1, l1[c * SLD], r[c]);
+              }
             }
           }
           if (j0 + SP < NB) {
@@ -328,11 +356,14 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
             // the padding rows of Ld and only feed registers past the panel
             const double* lb = Ld + j0 * SLD + j0;  // lb[c * SLD + t] = l_(j0 + c), (j0 + t)
 #pragma unroll
-            for (int t = 0; t < SP; ++t) r[SP] = fma(-lc[t], lb[SP * SLD + t], r[SP]);
-            piv = __shfl_sync(0xffffffffu, r[SP], j0 + SP);
-            rinv = rsqrt(piv);
+            for (int c = SP; c < SP + 2; ++c)
 #pragma unroll
-            for (int c = SP + 1; c < NB; ++c)
+              for (int t = 0; t < SP; ++t) r[c] = fma(-lc[t], lb[c * SLD + t], r[c]);
+            av = __shfl_sync(0xffffffffu, r[SP], j0 + SP);
+            bv = __shfl_sync(0xffffffffu, r[SP], j0 + SP + 1);
+            cv = __shfl_sync(0xffffffffu, r[SP + 1], j0 + SP + 1);
+#pragma unroll
+            for (int c = SP + 2; c < NB; ++c)
 #pragma unroll
               for (int t = 0; t < SP; ++t) r[c] = fma(-lc[t], lb[c * SLD + t], r[c]);
 #pragma unroll
