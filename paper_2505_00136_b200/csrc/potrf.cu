@@ -327,8 +327,8 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
             Ld[lane * SLD + j] = lcol0;
             Ld[lane * SLD + j + 1] = lcol1;
             __syncwarp();
-            if (lane == 0) {
-              __threadfence_block();
+            if (t == SP - 2 && lane == 0) {  // progress once per sub-panel (a fence costs ~90 cycles)
+              asm volatile("fence.acq_rel.cta;\n" ::: "memory");
               *prog = base + j + 2;
             }
             if (t + 2 < SP) {
@@ -409,11 +409,16 @@ __global__ void __launch_bounds__(PT, 1) potrf_tile_kernel(PotrfArgs a) {
       double x[NB];
 #pragma unroll
       for (int i = 0; i < NB; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
+      int avail = 0;  // columns of this panel published so far
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
-        while (*prog < base + j + 1) {
+        if (j >= avail) {  // the chain publishes every 8 pivots: one fence per batch
+          int v;
+          while ((v = *prog) < base + j + 1) {
+          }
+          asm volatile("fence.acq_rel.cta;\n" ::: "memory");
+          avail = v - base;
         }
-        __threadfence_block();
         x[j] *= rdg[j];
 #pragma unroll
         for (int i = j + 1; i < NB; ++i) x[i] = fma(-Ld[i * SLD + j], x[j], x[i]);
