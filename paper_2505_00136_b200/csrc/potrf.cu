@@ -578,8 +578,8 @@ static int g_cluster = -1;
 
 // CTAs per diagonal tile: GPB_POTRF_CLUSTER (2, 4, 8 or 16),
 // else 16 where POTRF is on the critical path -- factorisations of fewer
-// than 48 diagonal tiles (config 1 factor 8.8 -> 8.2 ms) and the last 8 tiles
-// of larger ones -- and 8 otherwise (hidden behind the trailing update,
+// than 48 diagonal tiles (config 1 factor 8.8 -> 8.2 ms), the first two and
+// the last 8 tiles of larger ones -- and 8 otherwise (hidden behind the trailing update,
 // where 16 latency-bound SMs would cost GEMM time)
 static int potrf_cluster(int tiles, int remaining) {
   if (g_cluster < 0) {
@@ -588,7 +588,8 @@ static int potrf_cluster(int tiles, int remaining) {
     g_cluster = (c == 2 || c == 4 || c == 8 || c == 16) ? c : 0;
   }
   if (g_cluster > 0) return g_cluster;
-  return ((tiles > 0 && tiles < 48) || (remaining > 0 && remaining <= 8)) ? 16 : 8;
+  const bool edge = remaining > 0 && (remaining <= 8 || remaining >= tiles - 1);  // exposed first/last tiles
+  return ((tiles > 0 && tiles < 48) || edge) ? 16 : 8;
 }
 
 cudaError_t launch_potrf(const PotrfArgs& a, cudaStream_t s) {
