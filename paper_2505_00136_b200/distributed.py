@@ -43,6 +43,7 @@ import contextlib
 import ctypes
 import math
 import os
+import time
 
 import numpy as np
 import torch
@@ -497,6 +498,7 @@ class DistributedGP:
         if cuda:
             crit.wait_stream(main)  # assembly
         t0 = self._event()
+        h0 = time.perf_counter()
         starts = list(range(0, T, G))
         for s, k0 in enumerate(starts):
             k1 = min(T, k0 + G) - 1
@@ -554,18 +556,34 @@ class DistributedGP:
                         else:
                             self._bcast(buf[p][g, rows[0] // P: rows[-1] // P + 1], src)
                     # in-group: the group's later columns get panel k (K = b)
-                    ops.gemm([(buf[i % P][g, i // P], buf[j % P][g, j // P], self.L[s_], self.L[s_], b,
-                               i == j) for j in range(k + 1, k1 + 1) for s_, i in by_col.get(j, [])],
-                             b, -1.0, 1.0)
+                    if vector_upd:  # job tables from address arithmetic (no per-tile Python work)
+                        sel = (own_j > k) & (own_j <= k1)
+                        ii, jj = own_i[sel], own_j[sel]
+                        base = pbase[s % 2]
+                        addr_g = lambda x: base[x % P] + (g * rows_per + x // P) * tile_bytes  # noqa: E731
+                        ops.gemm_addr(addr_g(ii), addr_g(jj), c_addr[sel], (ii == jj).astype(np.int32), b, b,
+                                      -1.0, 1.0, kstride=0)
+                    else:
+                        ops.gemm([(buf[i % P][g, i // P], buf[j % P][g, j // P], self.L[s_], self.L[s_], b,
+                                   i == j) for j in range(k + 1, k1 + 1) for s_, i in by_col.get(j, [])],
+                                 b, -1.0, 1.0)
                 if k1 + 1 < T:
                     # NEXT(s): the next group's columns get all gs panels (K = gs b);
                     # UPD(s-1) covered them too
                     if cuda and s >= 1:
                         crit.wait_event(ev_upd[s - 1])
                     nxt_hi = min(T, k1 + 1 + G)
-                    ops.gemm([(stack(i, gs), stack(j, gs), self.L[s_], self.L[s_], gs * b, i == j)
-                              for j in range(k1 + 1, nxt_hi) for s_, i in by_col.get(j, [])],
-                             b, -1.0, 1.0)
+                    if vector_upd:
+                        sel = (own_j > k1) & (own_j < nxt_hi)
+                        ii, jj = own_i[sel], own_j[sel]
+                        base = pbase[s % 2]
+                        addr0 = lambda x: base[x % P] + (x // P) * tile_bytes  # noqa: E731
+                        ops.gemm_addr(addr0(ii), addr0(jj), c_addr[sel], (ii == jj).astype(np.int32), gs * b, b,
+                                      -1.0, 1.0, kstride=rows_per * b * b)
+                    else:
+                        ops.gemm([(stack(i, gs), stack(j, gs), self.L[s_], self.L[s_], gs * b, i == j)
+                                  for j in range(k1 + 1, nxt_hi) for s_, i in by_col.get(j, [])],
+                                 b, -1.0, 1.0)
                 if cuda:
                     ev_panel = torch.cuda.Event()
                     ev_panel.record(crit)
@@ -594,6 +612,7 @@ class DistributedGP:
                 ev_upd[s].record(main)
         if cuda:
             main.wait_stream(crit)
+        h1 = time.perf_counter()  # host time to enqueue the schedule
         t1 = self._event()
         infos = self._allgather(info).view(-1).cpu().numpy()
         bad = [int(v) for v in infos if v >= 0]
@@ -603,7 +622,8 @@ class DistributedGP:
         t2 = self._event()
         self._solve()
         t3 = self._event()
-        self.timings = {"factor_ms": self._elapsed(t0, t1), "solve_ms": self._elapsed(t2, t3)}
+        self.timings = {"factor_ms": self._elapsed(t0, t1), "solve_ms": self._elapsed(t2, t3),
+                        "enqueue_ms": 1e3 * (h1 - h0)}
         self._factored = True
 
     def _p2p_buffers(self, shape):

@@ -14,7 +14,7 @@ for rep in range(int(os.environ.get("REPS", 3))):
     model = DistributedGP(train, gpb.KernelParams(), T)
     t0 = time.time(); ll = model.log_likelihood(); t1 = time.time()
     pv = model.predict_variance(test); t2 = time.time()
-    print(f"rep {rep}: ll {ll:.6f} factor {model.timings['factor_ms']:.1f} ms ({flops/model.timings['factor_ms']/1e9:.2f} TF) solve {model.timings['solve_ms']:.1f} ms wall {t1-t0:.2f}s predict {1e3*(t2-t1):.0f} ms", flush=True)
+    print(f"rep {rep}: ll {ll:.6f} enqueue {model.timings['enqueue_ms']:.1f} ms factor {model.timings['factor_ms']:.1f} ms ({flops/model.timings['factor_ms']/1e9:.2f} TF) solve {model.timings['solve_ms']:.1f} ms wall {t1-t0:.2f}s predict {1e3*(t2-t1):.0f} ms", flush=True)
     model.close()
 ref = gpb.GPModel(train, gpb.KernelParams(), T)
 print("single-GPU ll", -ref.compute_loss(), ref.device_timings()['factor'], "ms")
