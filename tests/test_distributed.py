@@ -174,12 +174,15 @@ def test_p2p_panel_exchange_one_gpu(monkeypatch, world, kind):
 
 
 @pytest.mark.gpu
-def test_bench_distributed_branch_two_ranks_one_gpu():
-    """bench.py's N>1 path end to end (torchrun, 2 ranks on cuda:0, gloo)."""
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_bench_distributed_branch_two_ranks_one_gpu(transport):
+    """bench.py's N>1 path end to end (torchrun, 2 ranks on cuda:0, gloo
+    collectives; the panel exchange by broadcasts or by the fused p2p path)."""
     import json
     import subprocess
 
-    env = dict(os.environ, GPB_DIST_BACKEND="gloo", GPB_FORCE_DEVICE="0", GPB_BENCH_SMALL="1")
+    env = dict(os.environ, GPB_DIST_BACKEND="gloo", GPB_FORCE_DEVICE="0", GPB_BENCH_SMALL="1",
+               GPB_DIST_TRANSPORT=transport)
     out = subprocess.run(
         [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
          "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
