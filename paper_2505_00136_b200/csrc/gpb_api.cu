@@ -611,17 +611,15 @@ int ensure_factor(gpb_model* m) {
     }
     CUDA_TRY(cudaEventRecord(ev_upd[s], m->st));
   }
-  if (m->potrf_prof) {  // GPB_POTRF_PROF: per-phase cycles of the tile kernel
-    long long h[44];
+  if (m->potrf_prof) {  // GPB_POTRF_PROF: per-phase cycles of the tile kernel (potrf.cu PROF_MARK)
+    long long h[16];
     cudaStreamSynchronize(m->crit);
     cudaMemcpy(h, m->potrf_prof, sizeof(h), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "potrf B-phase end per CTA (warp 0):");
-    for (int c = 0; c < 16; ++c) fprintf(stderr, " %lld", h[16 + c]);
-    fprintf(stderr, " | inverse warp end %lld\n", h[32]);
     fprintf(stderr,
-            "potrf cycles CTA0: B-wait %lld C-wait %lld trtri %lld zero %lld | chain %lld inverse %lld "
-            "C-jobs %lld | CTA1: B-jobs %lld B-wait %lld C-jobs %lld C-wait %lld\n",
-            h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[13], h[9], h[15], h[10]);
+            "potrf cycles, chain warp (CTA 0): B-barrier %lld, critical wait + chain %lld, C-barrier %lld, "
+            "trtri %lld, zero %lld | job warp 0 of CTA 1: B-jobs %lld, B-barrier %lld, C-jobs %lld, "
+            "C-barrier %lld\n",
+            h[1], h[5], h[2], h[3], h[4], h[13], h[9], h[15], h[10]);
     cudaMemset(m->potrf_prof, 0, sizeof(h));
   }
   // join: the main stream waits for the critical stream's last work
@@ -1214,8 +1212,8 @@ int model_create(gpb_ctx* ctx, const double* z, const double* y, int64_t n, int6
   }
   if (s == GPB_OK) s = alloc_model_buffers(m);
   if (s == GPB_OK && getenv("GPB_POTRF_PROF")) {
-    cudaMalloc(&m->potrf_prof, 44 * sizeof(long long));
-    cudaMemset(m->potrf_prof, 0, 44 * sizeof(long long));
+    cudaMalloc(&m->potrf_prof, 16 * sizeof(long long));
+    cudaMemset(m->potrf_prof, 0, 16 * sizeof(long long));
   }
   if (s == GPB_OK) s = upload_train(m, z, y, device_ptrs);
   if (s != GPB_OK) {
