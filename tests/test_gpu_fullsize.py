@@ -1,8 +1,10 @@
-"""Size-independent properties at the BASELINE.json full sizes (GPU).
+"""Full-size checks at the BASELINE.json sizes (GPU).
 
-The CPU oracle cannot run config 2 (n = 32768, D = 128) or config 3
-(n = 65536) in test time, so parity there rests on the scaled fixtures in
-test_gpu_parity.py plus these properties of the full-size runs:
+Direct oracle parity at the headline size (n = 32768, 64 tiles of 512, D = 8
+so that K is non-trivial; the oracle's tile DAG runs on every host core, ~50 s).
+Beyond that the CPU oracle cannot run config 2 with D = 128 predictions over
+32768 points or config 3/4 in test time, so parity there rests on the scaled
+fixtures in test_gpu_parity.py plus these properties of the full-size runs:
 
 * blocking invariance -- the same problem factored with internal tiles of 512
   and of 256 (a different schedule, different rounding) agrees to 1e-10;
@@ -97,3 +99,28 @@ def test_config4_on_one_gpu(runtime):
     assert np.array_equal(fc.full_covariance, fc.full_covariance.T)
     assert rel(np.diagonal(fc.full_covariance), pv_a.variance) <= 1e-12
     assert rel(fc.mean, pv_a.mean) <= 1e-12
+
+
+def test_config2_size_oracle_parity_d8(runtime):
+    """direct parity with the CPU oracle (the reference
+    algorithm, its tile DAG run by every host core through ThreadedCholesky,
+    runtime.py:180-181 threading) at the headline size n = 32768, 64 tiles of
+    512, with D = 8 so that K is far from diagonal: negative log-likelihood
+    (which carries log det L) and the predictive mean / variance of 256 test
+    points within the north-star tolerances."""
+    from oracle.tiled_gp import OracleGP, ThreadedCholesky
+
+    train, test = gpb.make_msd_dataset(32768, 256, 8, seed=4)
+    model = gpb.GPModel(train, gpb.KernelParams(1.0, 1.0, 0.1), 64)
+    nll = model.compute_loss()
+    pv = model.predict_with_uncertainty(test)
+    workers = max(1, len(os.sched_getaffinity(0)))
+    chol = ThreadedCholesky(workers)
+    ref = OracleGP(train.z, train.y, 64, cholesky=chol)
+    nll_ref = -ref.log_likelihood()
+    mean_ref, var_ref = ref.predict_variance(test.z, solver=chol.forward_solve_matrix)
+    print(f"n=32768 D=8 oracle parity: nll {abs(nll - nll_ref) / abs(nll_ref):.1e}, "
+          f"mean {rel(pv.mean, mean_ref):.1e}, variance {rel(pv.variance, var_ref):.1e}")
+    assert abs(nll - nll_ref) <= 1e-9 * abs(nll_ref)
+    assert rel(pv.mean, mean_ref) <= 1e-9
+    assert rel(pv.variance, var_ref) <= 1e-9
