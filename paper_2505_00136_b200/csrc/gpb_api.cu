@@ -169,7 +169,8 @@ struct gpb_model {
   // gradient
   DevBuf X, Kinv, part_l, part_v, part_x, inv_jobs;
   DevBuf gp_panel, gp_h, gp_jobs, gp_tiles;  // column-panel gradient terms (multi-GPU split)
-  std::vector<int64_t> invw_off, invx_off;
+  std::vector<int64_t> invw_off, invx_off, invd_off;  // U_k (j < k), F_k, U_k (j = k)
+  double kinv_fl = 0.0;
   int64_t kinv_off = 0, kinv_cnt = 0;
   bool inv_plan = false;
 
@@ -708,8 +709,9 @@ int build_inv_plan(gpb_model* m) {
   //        (T-1-k)(k+1) equal K = bi tile products
   // (the left-looking form put a K = i*bi job next to K = bi ones in one
   // launch: at config 1 the long jobs left most SMs idle)
-  m->invw_off.assign(Ti + 1, 0);  // U_k
+  m->invw_off.assign(Ti + 1, 0);  // U_k, j < k
   m->invx_off.assign(Ti + 1, 0);  // F_k
+  m->invd_off.assign(Ti + 1, 0);  // U_k, j = k
   for (int k = 0; k < Ti; ++k) {
     m->invx_off[k] = jobs.size();
     for (int j = 0; j < k; ++j)
@@ -723,7 +725,7 @@ int build_inv_plan(gpb_model* m) {
       }
     m->invw_off[k] = jobs.size();
     for (int i = k + 1; i < Ti; ++i)
-      for (int j = 0; j <= k; ++j) {
+      for (int j = 0; j < k; ++j) {
         GemmJob g{};
         g.A = L + h_tri_rm(i, k) * bi2;
         g.B = X + h_tri_cm(k, j, Ti) * bi2;
@@ -731,18 +733,39 @@ int build_inv_plan(gpb_model* m) {
         g.K = m->bi;
         jobs.push_back(g);
       }
+    // j = k: X(k, k) = Dinv_k is lower triangular, so output column block cb
+    // only needs k >= cb*128 -- one job per column block, K = bi - cb*128
+    m->invd_off[k] = jobs.size();
+    for (int i = k + 1; i < Ti; ++i)
+      for (int cb = 0; cb < m->bi / GBM; ++cb) {
+        const int64_t o = int64_t(cb) * GBM;
+        GemmJob g{};
+        g.A = L + h_tri_rm(i, k) * bi2 + o;
+        g.B = X + h_tri_cm(k, k, Ti) * bi2 + o * m->bi + o;
+        g.Cin = g.Cout = Kv + h_tri_cm(i, k, Ti) * bi2 + o;
+        g.K = m->bi - static_cast<int>(o);
+        jobs.push_back(g);
+      }
   }
+  // K^-1(r, c) = sum_{k >= r} X(k, r)^T X(k, c), one job per 128-row block rb
+  // of the output: X(r, r) is lower triangular, so the k sum starts at row
+  // rb*128 of the column panel; diagonal tiles only need the column blocks up
+  // to rb (symmetric: the trace pass reads their lower triangle only)
   m->kinv_off = jobs.size();
+  m->kinv_fl = 0.0;
   for (int r = 0; r < Ti; ++r)  // longest K first
-    for (int c = 0; c <= r; ++c) {
-      GemmJob g{};
-      g.A = X + h_tri_cm(r, r, Ti) * bi2;
-      g.B = X + h_tri_cm(r, c, Ti) * bi2;
-      g.Cout = Kv + h_tri_cm(r, c, Ti) * bi2;
-      g.K = (Ti - r) * m->bi;
-      g.lower = (r == c);  // symmetric: the trace pass reads the lower triangle only
-      jobs.push_back(g);
-    }
+    for (int c = 0; c <= r; ++c)
+      for (int rb = 0; rb < m->bi / GBM; ++rb) {
+        const int64_t o = int64_t(rb) * GBM;
+        GemmJob g{};
+        g.A = X + h_tri_cm(r, r, Ti) * bi2 + o * m->bi + o;
+        g.B = X + h_tri_cm(r, c, Ti) * bi2 + o * m->bi;
+        g.Cout = Kv + h_tri_cm(r, c, Ti) * bi2 + o * m->bi;
+        g.K = (Ti - r) * m->bi - static_cast<int>(o);
+        g.nlim = (r == c) ? rb + 1 : 0;
+        jobs.push_back(g);
+        m->kinv_fl += 2.0 * GBM * GBN * double(g.K) * (g.nlim ? g.nlim : m->bi / GBN);
+      }
   m->kinv_cnt = jobs.size() - m->kinv_off;
   CUDA_TRY(m->inv_jobs.ensure(sizeof(GemmJob) * jobs.size()));
   CUDA_TRY(cudaMemcpy(m->inv_jobs.p, jobs.data(), sizeof(GemmJob) * jobs.size(),
@@ -776,12 +799,20 @@ int loss_gradients(gpb_model* m, double out[3]) {
       GPB_TRY(gemm(m, f, true, false, EPI_AXPBY,
                    gemm_flops(int64_t(k) * nb, int64_t(GBM) * nb * (nb + 1) / 2)));
     }
-    const int64_t nu = int64_t(Ti - 1 - k) * (k + 1);  // U_k tile products
+    const int64_t nu = int64_t(Ti - 1 - k) * k;  // U_k tile products, j < k
     if (nu > 0) {
       GemmParams u = views(base_params(jobs + m->invw_off[k], static_cast<int>(nu), nb, nb, bi, bi, bi, -1.0, 1.0),
                            m->L, m->X);
       u.max_k = bi;
       GPB_TRY(gemm(m, u, true, false, EPI_AXPBY, gemm_flops(nu * nb * nb, bi)));
+    }
+    const int64_t nd = int64_t(Ti - 1 - k) * nb;  // j = k, one job per column block
+    if (nd > 0) {
+      GemmParams u = views(base_params(jobs + m->invd_off[k], static_cast<int>(nd), nb, 1, bi, bi, bi, -1.0, 1.0),
+                           m->L, m->X);
+      u.max_k = bi;
+      GPB_TRY(gemm(m, u, true, false, EPI_AXPBY,
+                   gemm_flops(int64_t(Ti - 1 - k) * nb, int64_t(GBM) * nb * (nb + 1) / 2)));
     }
   }
 
@@ -789,12 +820,11 @@ int loss_gradients(gpb_model* m, double out[3]) {
   const int64_t nblk = ntiles * (bi / kSekBlock) * (bi / kSekBlock);
   if (tl || tv) {
     // K^-1 = X^T X, lower tiles (model.py:362-380)
-    GemmParams kp = views(base_params(jobs + m->kinv_off, static_cast<int>(m->kinv_cnt), nb, nb, bi, bi,
+    GemmParams kp = views(base_params(jobs + m->kinv_off, static_cast<int>(m->kinv_cnt), 1, nb, bi, bi,
                                       bi, 1.0, 0.0),
                           m->X, m->X);
     kp.max_k = int64_t(Ti) * bi;
-    GPB_TRY(gemm(m, kp, false, false, EPI_AXPBY,
-                 gemm_flops(int64_t(nb) * nb, int64_t(bi) * Ti * (Ti + 1) * (Ti + 2) / 6)));
+    GPB_TRY(gemm(m, kp, false, false, EPI_AXPBY, m->kinv_fl));
     // fused trace pass (model.py:382-414 with covariance.py:196-220 regenerated)
     CUDA_TRY(launch_trace(m->Kinv.as<double>(), m->tile_cm.as<int2>(), ntiles, TraceTiles{0, 0, 0, nullptr},
                           m->zp.as<double>(), m->alpha.as<double>(), static_cast<int>(m->d), bi,
