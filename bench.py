@@ -278,13 +278,21 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     gemm_tf_exec = kfl[0] / (kms[0] * 1e-3) / 1e12 if kms[0] else 0.0
 
     # ---- e2e: public API, host buffers, copies inside the timed region
+    # inputs live in pinned host memory (the API's H2D copies read them there)
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+        t.numpy()[...] = a
+        return t.numpy()
+
+    train_h = gpb.Dataset(pinned(train.z), pinned(train.y))
+    test_h = gpb.Dataset(pinned(test.z), pinned(test.y))
     e2e_chol, e2e_pred = [], []
     for _ in range(min(K, 3) if rank == 0 else 0):
         t0 = time.perf_counter()
-        model = gpb.GPModel(train, gpb.KernelParams(1.0, 1.0, 0.1), tiles)
+        model = gpb.GPModel(train_h, gpb.KernelParams(1.0, 1.0, 0.1), tiles)
         model.compute_loss()  # H2D z, y; assemble; factor; solves; D2H loss terms
         t1 = time.perf_counter()
-        model.predict_with_uncertainty(test)  # H2D zt; predict; D2H mean + var
+        model.predict_with_uncertainty(test_h)  # H2D zt; predict; D2H mean + var
         t2 = time.perf_counter()
         e2e_chol.append(t1 - t0)
         e2e_pred.append(t2 - t1)
@@ -317,7 +325,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "unit": "TFLOP/s",
                 "predict_variance_points_per_s": m / statistics.median(e2e_pred) if e2e_pred else None,
                 "h2d_bytes_per_step": 8 * (n * d + n + m * d), "d2h_bytes_per_step": 8 * (2 + 2 * m),
-                "api": "GPModel(train).compute_loss() then predict_with_uncertainty(test), host numpy"},
+                "api": "GPModel(train).compute_loss() then predict_with_uncertainty(test), host numpy "
+                       "arrays in pinned memory"},
         "roofline": {"bound": "tensor", "kernel": "dgemm_tma_kernel (TMA-fed DMMA.8x8x4)",
                      "achieved": gemm_tf, "peak": peak.value, "unit": "TFLOP/s",
                      "frac": gemm_tf / peak.value if peak.value else None,
