@@ -243,6 +243,16 @@ class DeviceTileOps:
         _lib.check(self.lib.gpb_dev_gemm_mirror(self.rt.handle, self._s(), arr, len(jobs), b, b, b, b, 1, 1,
                                                 0, 0, alpha, beta, tab, nm))
 
+    def copy_addr(self, src_addr, dst_addr, nbytes: int):
+        """Batched device copies from address arrays (gpb_dev_copy)."""
+        n = len(src_addr)
+        if n == 0:
+            return
+        tab = np.empty(n, dtype=[("src", "<u8"), ("dst", "<u8")])
+        tab["src"], tab["dst"] = src_addr, dst_addr
+        self.launches += 1
+        _lib.check(self.lib.gpb_dev_copy(self.rt.handle, self._s(), tab.ctypes.data, n, nbytes))
+
     def combine(self, base, parts, out):
         self.launches += 1
         _lib.check(self.lib.gpb_dev_combine(self.rt.handle, self._s(), self._p(base), self._p(parts),
@@ -523,7 +533,16 @@ class DistributedGP:
                         for r in range(self.world):
                             if r != self.rank:
                                 ops.wait(my_flag(self.world + r), epoch + s - 1)
-                    if my_q == k % Q:  # this rank holds panel tiles of column k
+                    if my_q == k % Q and vector_upd and not p2p:
+                        # panel TRSM and its copy back into L from address tables
+                        sel = (own_j == k) & (own_i > k)
+                        ii = own_i[sel]
+                        pan = pbase[s % 2][my_p] + (g * rows_per + ii // P) * tile_bytes
+                        dk = np.full(len(ii), self.dinv[k].data_ptr(), dtype=np.int64)
+                        ops.gemm_addr(c_addr[sel], dk, pan, np.zeros(len(ii), dtype=np.int32), b, b, 1.0, 0.0,
+                                      kstride=0)
+                        ops.copy_addr(pan, c_addr[sel], tile_bytes)
+                    elif my_q == k % Q:  # this rank holds panel tiles of column k
                         mine = self.cyc.panel_rows(k, my_p)
                         jobs = [(self.L[self.slot[i, k]], self.dinv[k], None, buf[my_p][g, i // P], b, False)
                                 for i in mine]

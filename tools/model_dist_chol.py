@@ -13,12 +13,12 @@ E(p) = 1 / (imbalance * (1 + tail / T_p) * (1 + schedule overhead)), where
                single-GPU path (measured: 346.3 vs 337.3 ms at config 2).
 Inputs measured on one B200: factor rate 35.5 TF/s (configs 3/4), POTRF
 0.24 ms per 512 tile (8-CTA cluster), schedule overhead 2.7%, host enqueue
-0.95 ms per step."""
+0.33 ms per step."""
 import numpy as np
 
 RATE = 35.5e12          # DMMA GEMM rate on the trailing update, flop/s
 CRIT_MS = 0.40          # per-step critical path (POTRF 0.24 ms + TRSM + broadcasts), ms
-HOST_MS = 0.95          # host time to enqueue one step (measured: 121 ms for T = 128, quick_dist1.py)
+HOST_MS = 0.33          # host time to enqueue one step (measured: 42 ms for T = 128, quick_dist1.py)
 OVERHEAD = 346.3 / 337.3 - 1.0
 B = 512
 
