@@ -68,7 +68,8 @@ int gpb_model_get_params(gpb_model* m, double out[3]);
 
 /* ---- hot path ------------------------------------------------------------
  * gpb_cholesky: assemble K + tiled Cholesky (model.py:169-177), cached.
- *   L_out (n x n, lower, upper = 0) may be NULL.  GPB_NOT_PD on failure,
+ *   L_out (n x n, lower, upper = 0) may be NULL; it is written in strips of
+ *   rows through a bounded (<= 256 MB) device staging buffer.  GPB_NOT_PD on failure,
  *   with gpb_last_pivot giving the first failing index; the cache is
  *   invalidated (model.py:210-217). */
 int gpb_cholesky(gpb_model* m, double* L_out);
@@ -112,6 +113,15 @@ int gpb_predict_solve_device(gpb_model* m, const double* zt_dev, int64_t mt, int
 int gpb_cov_block_device(gpb_model* m, const double* za, int64_t ma, const double* Va, int64_t ldva,
                          const double* zb, int64_t mb, const double* Vb, int64_t ldvb, double* out,
                          int64_t ldo);
+
+/* _clamp_variances (model.py:488-496) on a host vector, in place: entries in
+ * [-1e-9, 0) become 0; GPB_NUMERIC (nothing changed) if any is below -1e-9.
+ * gpb_predict applies it to var and to the diagonal of cov. */
+int gpb_clamp_variances(double* v, int64_t n);
+/* Adam state of optimize (model.py:446-448: moments and step count persist
+ * across calls); get/set let a caller carry it across a model re-creation */
+int gpb_model_get_adam(gpb_model* m, double moment1[3], double moment2[3], int64_t* step);
+int gpb_model_set_adam(gpb_model* m, const double moment1[3], const double moment2[3], int64_t step);
 
 /* per-phase device times (ms, CUDA events on the model stream) of the last
  * calls: [0] assembly, [1] factorisation, [2] alpha solves, [3] predict

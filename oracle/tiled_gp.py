@@ -79,6 +79,25 @@ def assemble_covariance(z, l, nu, s2, t, include_noise=True):
     return grid
 
 
+def assemble_covariance_threaded(z, l, nu, s2, t, workers, include_noise=True):
+    """assemble_covariance with the independent tiles built by W threads (numpy
+    releases the GIL inside the ufunc loops); every tile is computed by the
+    same kernel_block call, so the grid is bitwise identical."""
+    blocks = row_blocks(z, t)
+    noise = s2 if include_noise else 0.0
+    pairs = [(i, j) for i in range(t) for j in range(i + 1)]
+
+    def one(ij):
+        i, j = ij
+        tile = kernel_block(blocks[i], blocks[j], l, nu)
+        if i == j and noise:
+            tile[np.diag_indices_from(tile)] += noise
+        return tile
+
+    with ThreadPoolExecutor(workers) as ex:
+        return dict(zip(pairs, ex.map(one, pairs)))
+
+
 def assemble_cross(zt, z, l, nu, row_tiles, col_tiles):
     """Test-by-train K* tiles (covariance.py:167-193)."""
     rows, cols = row_blocks(zt, row_tiles), row_blocks(z, col_tiles)
@@ -277,13 +296,14 @@ class OracleGP:
     """The reference GPModel's numerics (model.py:91-485) on numpy tiles."""
 
     def __init__(self, z, y, t, l=1.0, nu=1.0, s2=0.1, trainable=(True, True, True),
-                 cholesky=tiled_cholesky):
+                 cholesky=tiled_cholesky, assembly_workers=1):
         self.z = np.ascontiguousarray(z, dtype=np.float64)
         self.y = np.ascontiguousarray(y, dtype=np.float64)
         self.t = t
         self.l, self.nu, self.s2 = float(l), float(nu), float(s2)
         self.trainable = tuple(trainable)
         self._chol = cholesky
+        self._workers = assembly_workers
         self.adam_m = np.zeros(3)
         self.adam_v = np.zeros(3)
         self.adam_step = 0
@@ -300,8 +320,12 @@ class OracleGP:
 
     def ensure_factor(self):  # model.py:169-177
         if self.factor is None:
-            k = assemble_covariance(self.z, self.l, self.nu, self.s2, self.t)
+            if self._workers > 1:
+                k = assemble_covariance_threaded(self.z, self.l, self.nu, self.s2, self.t, self._workers)
+            else:
+                k = assemble_covariance(self.z, self.l, self.nu, self.s2, self.t)
             self.factor = self._chol(k, self.t)
+            del k
             self.beta = self.alpha = None
         return self.factor
 

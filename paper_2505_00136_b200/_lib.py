@@ -58,6 +58,9 @@ SIGNATURES = {
     "gpb_predict": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_int64, ctypes.c_int64,
                                    _c_double_p, _c_double_p, _c_double_p]),
     "gpb_predict_device": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, ctypes.c_int64, _vp, _vp]),
+    "gpb_clamp_variances": (ctypes.c_int, [_c_double_p, ctypes.c_int64]),
+    "gpb_model_get_adam": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, _c_i64_p]),
+    "gpb_model_set_adam": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, ctypes.c_int64]),
     "gpb_model_timings": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_int]),
     "gpb_model_launch_count": (ctypes.c_int, [_vp, _c_i64_p]),
     "gpb_model_stream": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),

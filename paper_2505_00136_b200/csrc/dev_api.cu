@@ -103,6 +103,13 @@ __global__ void copy_jobs_kernel(const gpb_copy_job* jobs, int64_t words16) {
 
 extern "C" {
 
+// gpb_finalize: the ring belongs to the runtime's GPU
+void gpb_dev_release_ring(void) {
+  std::lock_guard<std::mutex> lk(g_ring.mu);
+  g_ring.release();
+  g_ring.head = 0;
+}
+
 int gpb_dev_copy(gpb_ctx* ctx, void* stream, const gpb_copy_job* jobs, int64_t njobs, int64_t bytes) {
   if (int s = check_ctx(ctx)) return s;
   if (njobs <= 0 || bytes <= 0) return GPB_OK;

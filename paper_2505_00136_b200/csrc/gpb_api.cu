@@ -21,6 +21,8 @@
 
 using namespace gpb;
 
+extern "C" void gpb_dev_release_ring(void);  // dev_api.cu
+
 namespace {
 
 thread_local std::string g_err;
@@ -55,20 +57,28 @@ constexpr double kVarianceSlack = 1e-9;                  // model.py:33
 // destruction (and plan resizes) reuse blocks instead of paying cudaMalloc /
 // cudaFree (which synchronises the device) on every small call.  A block is
 // handed out again only after a device synchronisation at release, so no
-// pending kernel can still touch it.  Cached blocks are returned to CUDA when
-// an allocation fails and at gpb_finalize.
+// pending kernel can still touch it, and only to an allocation on the GPU it
+// lives on.  Cached blocks are returned to CUDA when an allocation fails and
+// at gpb_finalize.
 struct BlockCache {
+  struct Block {
+    void* p;
+    int device;
+  };
   std::mutex mu;
-  std::multimap<size_t, void*> free_blocks;  // capacity -> pointer
+  std::multimap<size_t, Block> free_blocks;  // capacity -> block
   size_t cached = 0;
 
-  cudaError_t alloc(size_t n, void** p, size_t* cap) {
+  cudaError_t alloc(size_t n, void** p, size_t* cap, int* device) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    *device = dev;
     {
       std::lock_guard<std::mutex> lk(mu);
       const size_t limit = std::max(2 * n, n + (size_t(1) << 20));
-      auto it = free_blocks.lower_bound(n);
-      if (it != free_blocks.end() && it->first <= limit) {
-        *p = it->second;
+      for (auto it = free_blocks.lower_bound(n); it != free_blocks.end() && it->first <= limit; ++it) {
+        if (it->second.device != dev) continue;
+        *p = it->second.p;
         *cap = it->first;
         cached -= it->first;
         free_blocks.erase(it);
@@ -84,15 +94,30 @@ struct BlockCache {
     if (e == cudaSuccess) *cap = n;
     return e;
   }
-  void release(void* p, size_t cap) {
-    cudaDeviceSynchronize();
-    std::lock_guard<std::mutex> lk(mu);
-    free_blocks.emplace(cap, p);
-    cached += cap;
+  // keep: false when the owning runtime is gone (the block is freed, not cached)
+  void release(void* p, size_t cap, int device, bool keep) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != device) cudaSetDevice(device);
+    if (!keep) {
+      cudaFree(p);
+    } else {
+      cudaDeviceSynchronize();
+      std::lock_guard<std::mutex> lk(mu);
+      free_blocks.emplace(cap, Block{p, device});
+      cached += cap;
+    }
+    if (cur != device) cudaSetDevice(cur);
   }
   void trim() {
     std::lock_guard<std::mutex> lk(mu);
-    for (auto& kv : free_blocks) cudaFree(kv.second);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& kv : free_blocks) {
+      cudaSetDevice(kv.second.device);
+      cudaFree(kv.second.p);
+    }
+    cudaSetDevice(cur);
     free_blocks.clear();
     cached = 0;
   }
@@ -102,6 +127,7 @@ BlockCache g_cache;
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;  // capacity
+  int device = 0;
   template <class T>
   T* as() const { return static_cast<T*>(p); }
   cudaError_t ensure(size_t nbytes) {
@@ -109,15 +135,15 @@ struct DevBuf {
     release();
     void* q = nullptr;
     size_t cap = 0;
-    cudaError_t e = g_cache.alloc(std::max<size_t>(nbytes, 16), &q, &cap);
+    cudaError_t e = g_cache.alloc(std::max<size_t>(nbytes, 16), &q, &cap, &device);
     if (e == cudaSuccess) {
       p = q;
       bytes = cap;
     }
     return e;
   }
-  void release() {
-    if (p) g_cache.release(p, bytes);
+  void release(bool keep = true) {
+    if (p) g_cache.release(p, bytes, device, keep);
     p = nullptr;
     bytes = 0;
   }
@@ -159,7 +185,8 @@ struct gpb_model {
   std::vector<cudaEvent_t> sync_ev;  // cross-stream dependencies (timing disabled)
 
   DevBuf zp, yp, L, Dinv, scratch, logdiag, info, yhat, beta, alpha, bhat, red, tile_rm, tile_cm,
-      chol_jobs;
+      chol_jobs, flow_flags;
+  int flow_R = -1;  // slice height of the one-launch solves (0: multi-launch path)
   int G = 2;  // panels per trailing-update group (GPB_PANELS)
   std::vector<CholGroup> groups;
   std::vector<double> chol_flops_exec;
@@ -656,6 +683,26 @@ int ensure_weights(gpb_model* m) {
   double* alpha = m->alpha.as<double>();
   double* bhat = m->bhat.as<double>();
   PhaseTimer pt(m, 2);
+  if (m->flow_R < 0) {
+    const char* fe = getenv("GPB_SOLVE_FLOW");
+    m->flow_R = (fe && atoi(fe) == 0) ? 0 : solve_flow_slice_rows(m->np_, bi);
+  }
+  if (m->flow_R > 0) {
+    bool launched = false;
+    CUDA_TRY(m->flow_flags.ensure(sizeof(int) * 4 * Ti));
+    {
+      ProfScope ps(m, KC_SOLVE, 0.0);
+      CUDA_TRY(launch_solve_flow(L, D, m->yp.as<double>(), beta, alpha, yhat, m->flow_flags.as<int>(), Ti,
+                                 bi, m->flow_R, m->st, &launched));
+    }
+    if (launched) {
+      m->launches += 1;
+      GPB_TRY(pt.stop());
+      m->weights_ok = true;
+      return GPB_OK;
+    }
+    m->flow_R = 0;
+  }
   CUDA_TRY(cudaMemcpyAsync(yhat, m->yp.p, sizeof(double) * m->np_, cudaMemcpyDeviceToDevice, m->st));
   for (int i = 0; i < Ti; ++i) {
     CUDA_TRY(launch_fwd_diag(D + i * bi2, yhat + int64_t(i) * bi, beta + int64_t(i) * bi, bi, m->st));
@@ -1254,13 +1301,14 @@ int model_create(gpb_ctx* ctx, const double* z, const double* y, int64_t n, int6
   return GPB_OK;
 }
 
-void free_model(gpb_model* m) {
+void free_model(gpb_model* m, bool keep = true) {
   for (DevBuf* b : {&m->zp, &m->yp, &m->L, &m->Dinv, &m->scratch, &m->logdiag, &m->info, &m->yhat,
                     &m->beta, &m->alpha, &m->bhat, &m->red, &m->tile_rm, &m->tile_cm, &m->chol_jobs,
+                    &m->flow_flags,
                     &m->X, &m->Kinv, &m->part_l, &m->part_v, &m->part_x, &m->inv_jobs,
                     &m->Bv, &m->W, &m->mpart, &m->sq, &m->pred_jobs, &m->zt, &m->mean, &m->var,
                     &m->S, &m->fc_jobs, &m->gp_panel, &m->gp_h, &m->gp_jobs, &m->gp_tiles})
-    b->release();
+    b->release(keep);
 }
 
 }  // namespace
@@ -1304,6 +1352,7 @@ int gpb_finalize(gpb_ctx* ctx) {
   delete g_ctx;
   g_ctx = nullptr;
   g_cache.trim();  // blocks still owned by live models stay with them
+  gpb_dev_release_ring();
   return GPB_OK;
 }
 
@@ -1326,8 +1375,15 @@ int gpb_model_create_device(gpb_ctx* ctx, const double* z_dev, const double* y_d
 
 int gpb_model_destroy(gpb_model* m) {
   if (!m) return GPB_OK;
+  bool live;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    live = g_ctx && g_ctx == m->ctx && g_ctx->gen == m->gen;
+  }
   if (m->st) cudaStreamSynchronize(m->st);
-  free_model(m);
+  // a model of a finalized runtime frees its blocks: a later runtime may run
+  // on another GPU and must not be handed this one's memory
+  free_model(m, live);
   for (cudaEvent_t e : m->evpool) cudaEventDestroy(e);
   for (cudaEvent_t e : m->sync_ev) cudaEventDestroy(e);
   if (m->crit) cudaStreamDestroy(m->crit);
@@ -1381,13 +1437,23 @@ int gpb_cholesky(gpb_model* m, double* L_out) {
   GPB_TRY(check_live(m));
   GPB_TRY(ensure_factor(m));
   if (L_out) {
-    DevBuf tmp;
-    CUDA_TRY(tmp.ensure(sizeof(double) * m->n * m->n));
-    CUDA_TRY(launch_export_lower(m->L.as<double>(), m->Ti, m->bi, m->n, m->pm, tmp.as<double>(), m->st));
-    ++m->launches;
-    CUDA_TRY(cudaMemcpyAsync(L_out, tmp.p, sizeof(double) * m->n * m->n, cudaMemcpyDeviceToHost, m->st));
+    // dense export in strips of rows through a bounded staging buffer
+    // (<= 256 MB on the device), so configs 3/4 export without an n x n temporary
+    const int64_t n = m->n;
+    const int64_t rows = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t(256) << 20) / (8 * n)));
+    DevBuf stage[2];
+    CUDA_TRY(stage[0].ensure(sizeof(double) * rows * n));
+    CUDA_TRY(stage[1].ensure(sizeof(double) * rows * n));
+    for (int64_t r0 = 0, s = 0; r0 < n; r0 += rows, ++s) {
+      const int64_t nr = std::min(rows, n - r0);
+      double* buf = stage[s % 2].as<double>();
+      CUDA_TRY(launch_export_lower(m->L.as<double>(), m->bi, n, r0, nr, m->pm, buf, m->st));
+      ++m->launches;
+      CUDA_TRY(cudaMemcpyAsync(L_out + r0 * n, buf, sizeof(double) * nr * n, cudaMemcpyDeviceToHost, m->st));
+    }
     CUDA_TRY(cudaStreamSynchronize(m->st));
-    tmp.release();
+    stage[0].release();
+    stage[1].release();
   }
   return GPB_OK;
 }
@@ -1589,6 +1655,31 @@ int gpb_model_mark_factored(gpb_model* m) {
   m->factor_ok = true;
   m->weights_ok = true;
   m->last_pivot = -1;
+  return GPB_OK;
+}
+
+int gpb_clamp_variances(double* v, int64_t n) {
+  if (n < 0 || (n > 0 && !v)) return fail(GPB_INVALID_CONFIG, "null argument");
+  return clamp_variances(v, n, 1);
+}
+
+int gpb_model_get_adam(gpb_model* m, double moment1[3], double moment2[3], int64_t* step) {
+  if (!m || !moment1 || !moment2 || !step) return fail(GPB_INVALID_CONFIG, "null argument");
+  for (int i = 0; i < 3; ++i) {
+    moment1[i] = m->adam_m[i];
+    moment2[i] = m->adam_v[i];
+  }
+  *step = m->adam_step;
+  return GPB_OK;
+}
+
+int gpb_model_set_adam(gpb_model* m, const double moment1[3], const double moment2[3], int64_t step) {
+  if (!m || !moment1 || !moment2 || step < 0) return fail(GPB_INVALID_CONFIG, "invalid Adam state");
+  for (int i = 0; i < 3; ++i) {
+    m->adam_m[i] = moment1[i];
+    m->adam_v[i] = moment2[i];
+  }
+  m->adam_step = step;
   return GPB_OK;
 }
 

@@ -112,6 +112,15 @@ cudaError_t launch_bwd_diag(const double* dinv, const double* bhat, double* alph
                             cudaStream_t s);
 cudaError_t launch_bwd_update(const double* ltiles, int i, int bi, const double* alpha_i,
                               double* bhat, cudaStream_t s);
+// Both vector solves in one cooperative launch (solve_flow.cu): beta = L^-1 y,
+// alpha = L^-T beta with per-block-row counters (flags: 4T ints, zeroed here;
+// xr: n_p doubles of exchange).  R = slice height from solve_flow_slice_rows
+// (0: the grid cannot be co-resident).  *launched = false: nothing was
+// launched and the caller must run the multi-launch solves.
+int solve_flow_slice_rows(int64_t np_, int bi);
+cudaError_t launch_solve_flow(const double* L, const double* dinv, const double* y, double* beta,
+                              double* alpha, double* xr, int* flags, int T, int bi, int R,
+                              cudaStream_t s, bool* launched);
 // out[0] = sum_k logdiag[k] (sequential k), out[1] = sum x^2 (fixed order)
 cudaError_t launch_loss_terms(const double* logdiag, int T, const double* x, int64_t n,
                               double* out, cudaStream_t s);
@@ -127,9 +136,10 @@ cudaError_t launch_symmetrize(double* S, int64_t mp, int64_t m, cudaStream_t s);
 cudaError_t launch_pad_vector(const double* src, double* dst, int64_t np_, PadMap pm, cudaStream_t s);
 cudaError_t launch_pad_rows(const double* src, double* dst, int64_t np_, int d, PadMap pm,
                             cudaStream_t s);
-// dense lower factor export: out[r][c] (n x n) from packed tiles
-cudaError_t launch_export_lower(const double* tiles, int T, int bi, int64_t n, PadMap pm,
-                                double* out, cudaStream_t s);
+// dense lower factor export, rows [row0, row0 + rows) of the n x n factor
+// (user indices): out[r - row0][c] from packed tiles
+cudaError_t launch_export_lower(const double* tiles, int bi, int64_t n, int64_t row0, int64_t rows,
+                                PadMap pm, double* out, cudaStream_t s);
 // G[c * ld + c] = 1 for c < count (identity right-hand side of a column panel)
 cudaError_t launch_set_diag(double* G, int64_t ld, int64_t count, cudaStream_t s);
 // copy the solved panel (scratch tiles q = 0..T-k-2) back to tiles (k+1+q, k)

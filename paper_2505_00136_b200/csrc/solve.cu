@@ -132,11 +132,11 @@ __global__ void pad_rows_kernel(const double* src, double* dst, int64_t np_, int
   dst[e] = pm.valid(P) ? src[((P / pm.bp_user) * pm.b_user + P % pm.bp_user) * d + k] : 0.0;
 }
 
-__global__ void export_lower_kernel(const double* tiles, int bi, int64_t n, PadMap pm,
-                                    double* out) {
+__global__ void export_lower_kernel(const double* tiles, int bi, int64_t n, int64_t row0,
+                                    int64_t rows, PadMap pm, double* out) {
   const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= n * n) return;
-  const int64_t r = e / n, c = e % n;
+  if (e >= rows * n) return;
+  const int64_t r = row0 + e / n, c = e % n;
   const int64_t P = (r / pm.b_user) * pm.bp_user + r % pm.b_user;
   const int64_t Q = (c / pm.b_user) * pm.bp_user + c % pm.b_user;
   const int64_t ti = P / bi, tj = Q / bi;
@@ -281,11 +281,12 @@ cudaError_t launch_pad_rows(const double* src, double* dst, int64_t np_, int d, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_export_lower(const double* tiles, int T, int bi, int64_t n, PadMap pm,
-                                double* out, cudaStream_t s) {
-  (void)T;
-  const int64_t e = n * n;
-  export_lower_kernel<<<static_cast<unsigned>((e + 255) / 256), 256, 0, s>>>(tiles, bi, n, pm, out);
+cudaError_t launch_export_lower(const double* tiles, int bi, int64_t n, int64_t row0, int64_t rows,
+                                PadMap pm, double* out, cudaStream_t s) {
+  const int64_t e = rows * n;
+  if (e <= 0) return cudaSuccess;
+  export_lower_kernel<<<static_cast<unsigned>((e + 255) / 256), 256, 0, s>>>(tiles, bi, n, row0, rows,
+                                                                              pm, out);
   return cudaGetLastError();
 }
 

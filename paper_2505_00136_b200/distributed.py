@@ -319,6 +319,11 @@ class _DeviceReplica:
             acc += np.array(out[:3])
         return acc
 
+    def _order(self):
+        """The model's entry points run on the library's own stream: work queued
+        on torch's current stream (buffer fills, uploads) must finish first."""
+        torch.cuda.current_stream(self.ops.device).synchronize()
+
     def publish(self):
         torch.cuda.current_stream(self.ops.device).synchronize()
         _lib.check(self.ops.lib.gpb_model_mark_factored(self.h))
@@ -328,8 +333,9 @@ class _DeviceReplica:
         if m == 0:
             return np.zeros(0), (np.zeros(0) if want_var else None)
         ztd = self.ops.from_numpy(zt)
-        mean = self.ops.zeros(m)
-        var = self.ops.zeros(m) if want_var else None
+        mean = torch.empty(m, dtype=torch.float64, device=self.ops.device)
+        var = torch.empty(m, dtype=torch.float64, device=self.ops.device) if want_var else None
+        self._order()
         _lib.check(self.ops.lib.gpb_predict_device(
             self.h, ctypes.c_void_p(ztd.data_ptr()), m, zt.shape[1],
             ctypes.c_void_p(mean.data_ptr()), ctypes.c_void_p(var.data_ptr()) if want_var else None))
@@ -343,6 +349,7 @@ class _DeviceReplica:
         mean = self.ops.zeros(max(1, m))
         if m:
             ztd = self.ops.from_numpy(zt)
+            self._order()
             _lib.check(self.ops.lib.gpb_predict_solve_device(
                 self.h, ctypes.c_void_p(ztd.data_ptr()), m, zt.shape[1], ctypes.c_void_p(mean.data_ptr()),
                 ctypes.c_void_p(v.data_ptr()), ldv))
@@ -352,6 +359,7 @@ class _DeviceReplica:
         """rows[:ma, col0:col0+mb] = K**(za, zb) - Va^T Vb (gpb_cov_block_device)."""
         zad, zbd = self.ops.from_numpy(za), self.ops.from_numpy(zb)
         ldo = rows.shape[1]
+        self._order()
         _lib.check(self.ops.lib.gpb_cov_block_device(
             self.h, ctypes.c_void_p(zad.data_ptr()), za.shape[0], ctypes.c_void_p(va.data_ptr()),
             va.shape[1], ctypes.c_void_p(zbd.data_ptr()), zb.shape[0], ctypes.c_void_p(vb.data_ptr()),

@@ -66,6 +66,15 @@ class PredictionResult:
     full_covariance: np.ndarray | None = None
 
 
+def _clamp_variances(variance: np.ndarray) -> np.ndarray:
+    """Round-off negatives in [-1e-9, 0) become 0; anything below raises
+    ``NumericalConsistencyError`` (model.py:488-496).  Runs the library's
+    clamp (``gpb_clamp_variances``, the one ``gpb_predict`` applies) on a copy."""
+    out = np.array(variance, dtype=np.float64, copy=True, order="C").reshape(-1)
+    _lib.check(_lib.load().gpb_clamp_variances(_lib.dptr(out), out.shape[0]))
+    return out.reshape(np.shape(variance))
+
+
 def _as_dataset(data) -> Dataset:
     if isinstance(data, Dataset):
         return data
@@ -90,7 +99,10 @@ class GPModel:
         self._tiles_per_dim = int(tiles_per_dim)
         self._handle = None  # ctypes.c_void_p of the bound gpb_model
         self._runtime = None
-        # Adam state lives in the C model; mirrored here across rebinds
+        # Adam moments and step count (model.py:446-448 keeps them on the
+        # model across optimize calls): read back from the C model after every
+        # optimize and restored into a re-created handle (close(), runtime restart)
+        self._adam = (np.zeros(3), np.zeros(3), 0)
         self._pending_train = False
 
     # -- attribute management (model.py:135-165) ---------------------------
@@ -147,6 +159,8 @@ class GPModel:
             self._runtime = rt
             self._pending_train = False
             self._push_params()
+            m1, m2, step = self._adam
+            _lib.check(lib.gpb_model_set_adam(h, _lib.dptr(m1), _lib.dptr(m2), step))
         elif self._pending_train:
             z, y = self._train.z, self._train.y
             _lib.check(lib.gpb_model_set_train(self._handle, _lib.dptr(z), _lib.dptr(y),
@@ -239,11 +253,14 @@ class GPModel:
         def call(lib, h):
             status = lib.gpb_optimize(h, opt.learning_rate, opt.beta1, opt.beta2, opt.epsilon,
                                       opt.iterations, _lib.dptr(hist))
-            # parameters advanced on the device side even on failure
+            # parameters and Adam state advanced on the device side even on failure
             got = (ctypes.c_double * 3)()
             lib.gpb_model_get_params(h, got)
             self._params = replace(self._params, lengthscale=float(got[0]),
                                    vertical_scale=float(got[1]), noise_variance=float(got[2]))
+            m1, m2, step = np.zeros(3), np.zeros(3), ctypes.c_int64()
+            lib.gpb_model_get_adam(h, _lib.dptr(m1), _lib.dptr(m2), ctypes.byref(step))
+            self._adam = (m1, m2, int(step.value))
             _lib.check(status)
 
         self._guarded(call)

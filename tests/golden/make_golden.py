@@ -16,6 +16,14 @@ Cases (BASELINE.json configs + the reference test corpus shapes):
   c2s       config 2 scaled: n=2048, m=512, D=128, T=4 (b=512)
   d8b512    n=4096, m=512, D=8, T=8 (b=512): non-degenerate K at the c2 tile size
   rand_*    random-normal instances as in pkg/tests/test_acceptance.py:28-32
+  c3s       config 3 scaled: n=8192, D=8, T=16 (b=512): factor, loss, gradients
+  c4s       config 4 scaled: n=8192, m=512, D=16, T=16 (b=512): + full covariance
+  accept_grid   test_acceptance.py:35-78 grid (n, m, T) in {16,64,256}x{16,64}x{1,4,8}
+                with the reference's dense-oracle values (pkg/tests/oracles.py)
+  determinism   test_acceptance.py:135-169 instance, tilings 1 and 4
+
+``python tests/golden/make_golden.py accept_grid determinism large`` regenerates
+only the named groups.
 """
 
 from __future__ import annotations
@@ -102,9 +110,88 @@ def run_case(name, train, test, t, full_store, do_full_cov=True, do_grad=True,
     print(f"{name}: {time.perf_counter() - tic:.1f}s  loglik={float(out['loglik']):.15g}")
 
 
+def _instance(seed, n, m, d=4):
+    """pkg/tests/test_acceptance.py:28-32 instance shapes."""
+    rng = np.random.default_rng(seed)
+    train = taskgp.Dataset(z=rng.normal(size=(n, d)), y=rng.normal(size=n))
+    test = taskgp.Dataset(z=rng.normal(size=(m, d)), y=np.zeros(m))
+    return train, test
+
+
+def acceptance_grid():
+    """The reference's oracle-equivalence grid (test_acceptance.py:35-78):
+    (n, m, T) in {16, 64, 256} x {16, 64} x {1, 4, 8}, reference outputs per
+    tiling plus the dense-oracle values the reference test compares them to
+    (pkg/tests/oracles.py DenseGP)."""
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    import oracles  # the reference's dense checker
+
+    out = {}
+    tic = time.perf_counter()
+    for n in (16, 64, 256):
+        for m in (16, 64):
+            train, test = _instance(n * 1000 + m, n, m)
+            key = f"n{n}_m{m}"
+            out[key + "_zsum"] = np.array([train.z.sum(), train.y.sum(), test.z.sum()])
+            o = oracles.DenseGP(train.z, train.y, 1.0, 1.0, 0.1)
+            out[key + "_dense_L"] = np.linalg.cholesky(o.k_train)
+            out[key + "_dense_mean"] = o.predict_mean(test.z)
+            out[key + "_dense_cov"] = o.posterior_cov(test.z)
+            out[key + "_dense_ll"] = np.array(o.log_likelihood())
+            for t in (1, 4, 8):
+                k = f"{key}_t{t}"
+                model = GPModel(train, taskgp.KernelParams(), tiles_per_dim=t)
+                out[k + "_L"] = factor(model)
+                full = model.predict_with_full_cov(test)
+                var = model.predict_variance(test)
+                out[k + "_mean"] = full.mean
+                out[k + "_cov"] = full.full_covariance
+                out[k + "_var"] = var.variance
+                out[k + "_ll"] = np.array(model.log_likelihood())
+                out[k + "_grads"] = np.array(model.loss_gradients())
+    np.savez_compressed(os.path.join(HERE, "accept_grid.npz"), **out)
+    print(f"accept_grid: {time.perf_counter() - tic:.1f}s")
+
+
+def determinism():
+    """test_acceptance.py:135-169: one instance, tilings 1 and 4, reference
+    outputs (the GPU test adds more tilings and compares them all)."""
+    train, test = _instance(2024, 64, 16)
+    out = {"zsum": np.array([train.z.sum(), train.y.sum(), test.z.sum()])}
+    for t in (1, 4):
+        model = GPModel(train, taskgp.KernelParams(lengthscale=0.9, noise_variance=0.15), tiles_per_dim=t)
+        full = model.predict_with_full_cov(test)
+        out[f"t{t}_mean"] = full.mean
+        out[f"t{t}_cov"] = full.full_covariance
+        out[f"t{t}_var"] = model.predict_variance(test).variance
+        out[f"t{t}_ll"] = np.array(model.log_likelihood())
+    np.savez_compressed(os.path.join(HERE, "determinism.npz"), **out)
+    print("determinism: done")
+
+
+def scaled_large_configs():
+    """Scaled shapes of BASELINE configs 3 and 4 at the benchmark tile size
+    (b = 512, T = 16): c3s n = 8192, D = 8 (cholesky + alpha solve + loss,
+    gradients); c4s n = 8192, m = 512 (config 4's m / n = 1/16), D = 16 with
+    full covariance and gradients."""
+    tr, _ = make_msd_dataset(8192, 0, 8, seed=0)
+    run_case("c3s", taskgp.Dataset(tr.z, tr.y), None, 16, full_store=False)
+    tr, te = make_msd_dataset(8192, 512, 16, seed=0)
+    run_case("c4s", taskgp.Dataset(tr.z, tr.y), taskgp.Dataset(te.z, te.y), 16, full_store=False)
+
+
 def main():
     taskgp.start_runtime(taskgp.RuntimeConfig(worker_count=os.cpu_count()))
     try:
+        only = sys.argv[1:]
+        if only:
+            for name in only:
+                {"accept_grid": acceptance_grid, "determinism": determinism,
+                 "large": scaled_large_configs}[name]()
+            return
+        acceptance_grid()
+        determinism()
+        scaled_large_configs()
         # reference-corpus random instances (test_acceptance.py:28-32 shapes)
         for n, m, t in ((16, 16, 4), (64, 16, 4), (64, 64, 8), (256, 64, 4), (48, 12, 4)):
             rng = np.random.default_rng(n * 1000 + m)

@@ -124,3 +124,70 @@ def test_config2_size_oracle_parity_d8(runtime):
     assert abs(nll - nll_ref) <= 1e-9 * abs(nll_ref)
     assert rel(pv.mean, mean_ref) <= 1e-9
     assert rel(pv.variance, var_ref) <= 1e-9
+
+
+def _rel_fro_tiles(L, grid, t):
+    """||L - L_oracle||_F / ||L_oracle||_F with the oracle factor as a lower
+    tile grid (no dense copy of it); the strictly upper tiles of L must be 0."""
+    b = L.shape[0] // t
+    num = den = 0.0
+    for i in range(t):
+        rows = slice(i * b, (i + 1) * b)
+        assert not np.any(L[rows, (i + 1) * b:])
+        for j in range(i + 1):
+            ref = grid[i, j]
+            num += float(np.sum((L[rows, j * b:(j + 1) * b] - ref) ** 2))
+            den += float(np.sum(ref * ref))
+    return (num / den) ** 0.5
+
+
+def _oracle(train, t):
+    from oracle.tiled_gp import OracleGP, ThreadedCholesky
+
+    workers = max(1, len(os.sched_getaffinity(0)))
+    return OracleGP(train.z, train.y, t, cholesky=ThreadedCholesky(workers), assembly_workers=workers)
+
+
+def test_config3_oracle_parity(runtime):
+    """BASELINE config 3 itself (n = 65536, D = 8, 128 tiles of 512) against the
+    oracle on the GPU host's cores: the whole factor by relative Frobenius and
+    the negative log-likelihood (which carries log det L and the alpha solve)."""
+    import time
+
+    train, _ = gpb.make_msd_dataset(65536, 0, 8, seed=0)
+    model = gpb.GPModel(train, gpb.KernelParams(1.0, 1.0, 0.1), 128)
+    nll = model.compute_loss()
+    L = model.cholesky()
+    model.close()
+    tic = time.perf_counter()
+    ref = _oracle(train, 128)
+    nll_ref = -ref.log_likelihood()
+    err = _rel_fro_tiles(L, ref.factor, 128)
+    print(f"config 3 oracle parity: L {err:.2e}, nll {abs(nll - nll_ref) / abs(nll_ref):.2e} "
+          f"(oracle {time.perf_counter() - tic:.0f} s)")
+    assert err <= 1e-10
+    assert abs(nll - nll_ref) <= 1e-9 * abs(nll_ref)
+
+
+def test_config2_d128_factor_oracle_parity(runtime):
+    """The headline shape itself (n = 32768, D = 128, 64 tiles of 512): the whole
+    factor against the oracle, plus mean / variance of 256 test points."""
+    from oracle.tiled_gp import ThreadedCholesky
+
+    train, test = gpb.make_msd_dataset(32768, 256, 128, seed=0)
+    model = gpb.GPModel(train, gpb.KernelParams(1.0, 1.0, 0.1), 64)
+    nll = model.compute_loss()
+    pv = model.predict_with_uncertainty(test)
+    L = model.cholesky()
+    model.close()
+    ref = _oracle(train, 64)
+    nll_ref = -ref.log_likelihood()
+    err = _rel_fro_tiles(L, ref.factor, 64)
+    chol = ThreadedCholesky(max(1, len(os.sched_getaffinity(0))))
+    mean_ref, var_ref = ref.predict_variance(test.z, solver=chol.forward_solve_matrix)
+    print(f"config 2 (D=128) oracle parity: L {err:.2e}, nll {abs(nll - nll_ref) / abs(nll_ref):.2e}, "
+          f"mean {rel(pv.mean, mean_ref):.2e}, variance {rel(pv.variance, var_ref):.2e}")
+    assert err <= 1e-10
+    assert abs(nll - nll_ref) <= 1e-9 * abs(nll_ref)
+    assert rel(pv.mean, mean_ref) <= 1e-9
+    assert rel(pv.variance, var_ref) <= 1e-9

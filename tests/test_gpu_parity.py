@@ -338,6 +338,24 @@ class TestGradientsAndAdam:
         fixed.optimize(gpb.AdamConfig(iterations=3))
         assert fixed.params.lengthscale == 1.5 and fixed.params.noise_variance == 0.3
 
+    def test_adam_state_survives_rebind(self, runtime, rng):
+        """Moments and step count persist across close() and a runtime restart
+        (model.py:446-448): optimize(1) + close() + optimize(1) == optimize(2)."""
+        train = ds(rng.normal(size=(32, 3)), rng.normal(size=32))
+        joint = gpb.GPModel(train, gpb.KernelParams(), 4)
+        h_joint = joint.optimize(gpb.AdamConfig(iterations=2))
+        split = gpb.GPModel(train, gpb.KernelParams(), 4)
+        h1 = split.optimize(gpb.AdamConfig(iterations=1))
+        split.close()
+        runtime.stop()
+        rt2 = gpb.start_runtime()
+        try:
+            h2 = split.optimize(gpb.AdamConfig(iterations=1))
+        finally:
+            rt2.stop()
+        assert h1 + h2 == h_joint
+        assert split.params == joint.params
+
     def test_failure_reports_iteration(self, runtime):
         kp = gpb.KernelParams(noise_variance=0.0, trainable=(False, False, False))
         model = gpb.GPModel(gpb.Dataset(z=np.ones((4, 2)), y=np.ones(4)), kp)
@@ -460,3 +478,26 @@ def test_device_gemm_views_and_fallback(runtime, rng):
     torch.cuda.synchronize()
     for got in (c1, c2):
         assert rel(got.cpu().numpy(), want) <= 1e-14
+
+
+@pytest.mark.parametrize("n,t,d", [(1024, 4, 8), (4096, 8, 8), (3000, 6, 3), (8192, 32, 8), (20000, 40, 5)])
+def test_one_launch_solves_match_multi_launch(runtime, monkeypatch, n, t, d):
+    """The cooperative one-launch alpha/beta solves (solve_flow.cu) against the
+    4T-launch blocked solves (solve.cu) and the oracle: same loss and mean to
+    round-off, bitwise reproducible run to run."""
+    rng = np.random.default_rng(n + t)
+    z, y, zt = rng.normal(size=(n, d)), rng.normal(size=n), rng.normal(size=(64, d))
+    out = {}
+    for flow in ("1", "0", "1"):
+        monkeypatch.setenv("GPB_SOLVE_FLOW", flow)
+        model = gpb.GPModel(ds(z, y), gpb.KernelParams(1.1, 0.9, 0.2), t)
+        res = (model.log_likelihood(), model.predict(ds(zt)).mean)
+        if flow in out:
+            assert res[0] == out[flow][0] and np.array_equal(res[1], out[flow][1])
+        out[flow] = res
+    assert abs(out["1"][0] - out["0"][0]) <= 1e-12 * abs(out["0"][0])
+    assert rel(out["1"][1], out["0"][1]) <= 1e-11
+    if n <= 4096:
+        o = OracleGP(z, y, t, 1.1, 0.9, 0.2)
+        assert abs(out["1"][0] - o.log_likelihood()) <= TOL * abs(o.log_likelihood())
+        assert rel(out["1"][1], o.predict(zt)) <= TOL

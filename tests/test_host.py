@@ -140,3 +140,28 @@ def test_product_path_does_not_import_oracle():
         if fn.endswith(".py"):
             src = open(os.path.join(pkg, fn)).read()
             assert "oracle" not in re.sub(r"#.*|\"\"\"[\s\S]*?\"\"\"", "", src), fn
+
+
+class TestVarianceClamp:
+    """test_model.py:165-172 on the library's clamp (gpb_clamp_variances, the
+    host routine gpb_predict applies to every variance it returns)."""
+
+    def test_round_off_clamped_to_zero(self):
+        from paper_2505_00136_b200.model import _clamp_variances
+
+        out = _clamp_variances(np.array([1.0, -1e-10, 0.0]))
+        np.testing.assert_array_equal(out, np.array([1.0, 0.0, 0.0]))
+
+    def test_genuinely_negative_raises(self):
+        from paper_2505_00136_b200.errors import NumericalConsistencyError
+        from paper_2505_00136_b200.model import _clamp_variances
+
+        with pytest.raises(NumericalConsistencyError):
+            _clamp_variances(np.array([0.5, -1e-6]))
+
+    def test_boundary_and_input_untouched(self):
+        from paper_2505_00136_b200.model import _clamp_variances
+
+        v = np.array([-1e-9, -0.0, 2.0])
+        np.testing.assert_array_equal(_clamp_variances(v), [0.0, 0.0, 2.0])
+        assert v[0] == -1e-9  # the caller's array is not modified

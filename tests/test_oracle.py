@@ -99,3 +99,62 @@ def test_oracle_known_answers():
     assert o.log_likelihood() == pytest.approx(-0.9189385332046727, abs=1e-15)
     o = OracleGP(np.zeros((1, 1)), np.ones(1), 1, nu=0.5, s2=0.5)
     assert o.log_likelihood() == pytest.approx(-1.4189385332046727, abs=1e-15)
+
+
+def acceptance_instance(seed, n, m, d=4):
+    """pkg/tests/test_acceptance.py:28-32 inputs."""
+    r = np.random.default_rng(seed)
+    return r.normal(size=(n, d)), r.normal(size=n), r.normal(size=(m, d))
+
+
+@pytest.mark.parametrize("n", [16, 64, 256])
+@pytest.mark.parametrize("m", [16, 64])
+def test_oracle_matches_reference_acceptance_grid(n, m):
+    """The reference's oracle-equivalence grid (test_acceptance.py:35-78): the
+    oracle reproduces taskgp's outputs for every tiling, and those agree with
+    the reference's dense checker within the reference test's 1e-8."""
+    g = load_golden("accept_grid")
+    key = f"n{n}_m{m}"
+    z, y, zt = acceptance_instance(n * 1000 + m, n, m)
+    np.testing.assert_array_equal([z.sum(), y.sum(), zt.sum()], g[key + "_zsum"])
+    for t in (1, 4, 8):
+        k = f"{key}_t{t}"
+        o = OracleGP(z, y, t)
+        assert rel_fro(o.factor_dense(), g[k + "_L"]) < 1e-13
+        mean, var = o.predict_variance(zt)
+        _, cov = o.predict_full_cov(zt)
+        np.testing.assert_allclose(mean, g[k + "_mean"], rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(var, g[k + "_var"], rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(cov, g[k + "_cov"], rtol=1e-12, atol=1e-14)
+        assert o.log_likelihood() == pytest.approx(float(g[k + "_ll"]), rel=1e-13)
+        np.testing.assert_allclose(o.loss_gradients(), g[k + "_grads"], rtol=1e-11, atol=1e-15)
+        worst = max(np.abs(g[k + "_L"] - g[key + "_dense_L"]).max(),
+                    np.abs(g[k + "_mean"] - g[key + "_dense_mean"]).max(),
+                    np.abs(g[k + "_cov"] - g[key + "_dense_cov"]).max(),
+                    abs(float(g[k + "_ll"]) - float(g[key + "_dense_ll"])))
+        assert worst <= 1e-8
+
+
+@pytest.mark.parametrize("name,m,d", [("c3s", 0, 8), ("c4s", 512, 16)])
+def test_oracle_matches_reference_scaled_large(name, m, d):
+    """Scaled config-3 / config-4 shapes (b = 512, T = 16) run by the reference."""
+    g = load_golden(name)
+    train, test = make_msd_dataset(8192, m, d, seed=0)
+    np.testing.assert_array_equal(train.z[:16], g["z_head"])
+    o = OracleGP(train.z, train.y, 16)
+    _check_summary("L", o.factor_dense(), g, 1e-12)
+    assert o.log_likelihood() == pytest.approx(float(g["loglik"]), rel=1e-13)
+    if m:
+        np.testing.assert_array_equal(test.z[:16], g["zt_head"])
+        mean, var = o.predict_variance(test.z)
+        np.testing.assert_allclose(mean, g["mean"], rtol=1e-11, atol=1e-14)
+        np.testing.assert_allclose(var, g["var"], rtol=1e-11, atol=1e-14)
+
+
+def test_oracle_clamp_matches_reference():
+    """_clamp_variances known answers (test_model.py:165-172)."""
+    from oracle.tiled_gp import clamp_variances
+
+    np.testing.assert_array_equal(clamp_variances(np.array([1.0, -1e-10, 0.0])), [1.0, 0.0, 0.0])
+    with pytest.raises(ArithmeticError):
+        clamp_variances(np.array([0.5, -1e-6]))
