@@ -24,6 +24,10 @@
 // order), so results are bitwise reproducible.  All slices must be resident at
 // once (cooperative launch); launch_solve_flow reports when they are not and
 // the caller keeps the multi-launch path.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "kernels.cuh"
 
 namespace gpb {
@@ -31,23 +35,47 @@ namespace gpb {
 namespace {
 
 constexpr int FT = 128;  // threads per CTA (4 warps)
+// bytes of factor tiles the active slices may hold in L2 through look-ahead
+// prefetches at once (of 126 MB): only the late, latency-bound phase uses them
+constexpr int64_t kL2Window = int64_t(48) << 20;
 constexpr int FW = FT / 32;
 
-GPB_DEVINL int ld_acquire(const int* p) {
+GPB_DEVINL int ld_relaxed(const int* p) {
   int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 
-GPB_DEVINL void wait_count(const int* flag, int want) {
+// thread 0 polls (relaxed loads: no L1 invalidation per poll), then one
+// gpu-scope fence orders the CTA's later loads after the observed count
+// (they read L2 through ld.cg, so no stale L1 lines are involved)
+GPB_DEVINL void wait_count(const int* flag, int want, bool hot = false) {
   if (threadIdx.x == 0) {
     int ns = 32;
-    while (ld_acquire(flag) < want) {
-      __nanosleep(ns);
-      ns = ns < 512 ? 2 * ns : 512;
+    while (ld_relaxed(flag) < want) {
+      if (!hot) {
+        __nanosleep(ns);
+        ns = ns < 256 ? 2 * ns : 256;
+      }
     }
+    __threadfence();
   }
   __syncthreads();
+}
+
+// bulk L2 prefetch of a contiguous range (16-byte multiple; thread 0 issues)
+GPB_DEVINL void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// L2 prefetch of `rows` rows of `width` doubles at stride ld (one 128-byte line per
+// thread per step: the column slices of the backward solve)
+GPB_DEVINL void prefetch_rows(const double* p, int rows, int width, int64_t ld) {
+  const int lines = (width * 8 + 127) / 128;
+  for (int e = threadIdx.x; e < rows * lines; e += blockDim.x) {
+    const char* a = reinterpret_cast<const char*>(p + static_cast<int64_t>(e / lines) * ld) + 128 * (e % lines);
+    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a));
+  }
 }
 
 // publish this CTA's stores: every thread's writes are fenced before the count
@@ -66,176 +94,252 @@ struct FlowArgs {
   double* xr;          // n_p exchange buffer (r of the forward, t of the backward)
   int* flags;          // 4T counters, zero on entry
   int T, bi, R;
+  unsigned long long* prof;  // optional: 4T globaltimer stamps (GPB_SOLVE_PROF)
 };
 
-// forward slice: rows [row0, row0 + R) of block row i, R / FW rows per warp
+GPB_DEVINL unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// 8 per-lane partial sums (rows 0..7 of a group) -> the total of row
+// 4*b4 + 2*b3 + b2 (bits of the lane index) in every lane: three halving
+// exchanges then two full butterflies -- 9 shuffles instead of 8 x 5, in a
+// fixed order (IEEE addition is commutative, so partner lanes agree bitwise)
+GPB_DEVINL double reduce8(const double (&p)[8], int lane) {
+  const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
+  double q4[4], q2[2];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    q4[k] = (h4 ? p[k + 4] : p[k]) + __shfl_xor_sync(0xffffffffu, h4 ? p[k] : p[k + 4], 16);
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+    q2[k] = (h3 ? q4[k + 2] : q4[k]) + __shfl_xor_sync(0xffffffffu, h3 ? q4[k] : q4[k + 2], 8);
+  double q = (h2 ? q2[1] : q2[0]) + __shfl_xor_sync(0xffffffffu, h2 ? q2[0] : q2[1], 4);
+  q += __shfl_xor_sync(0xffffffffu, q, 2);
+  q += __shfl_xor_sync(0xffffffffu, q, 1);
+  return q;
+}
+GPB_DEVINL int reduce8_row(int lane) { return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1); }
+
+// p[k] += M[row k][lane's columns] . v  for the 8 rows of a group (row-major
+// M, ld = bi); diag: M is lower triangular, only columns <= row are read
+template <bool kDiag>
+GPB_DEVINL void rows8_dot(const double* M, int bi, int row0, const double2* v, int nchunk, int lane,
+                          double (&p)[8]) {
+#pragma unroll 2
+  for (int c = 0; c < nchunk; ++c) {
+    const int col = 2 * (lane + 32 * c);
+    if (kDiag && col > row0 + 7) continue;
+    double2 x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const double2* r = reinterpret_cast<const double2*>(M + static_cast<int64_t>(row0 + k) * bi) + lane + 32 * c;
+      if (!kDiag || col <= row0 + k)
+        x[k] = kDiag ? __ldcg(r) : __ldcs(r);
+      else
+        x[k] = make_double2(0.0, 0.0);
+    }
+    const double2 vc = v[lane + 32 * c];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      p[k] = fma(x[k].x, vc.x, p[k]);
+      p[k] = fma(x[k].y, vc.y, p[k]);  // upper entries of Dinv are zero
+    }
+  }
+}
+
+// forward slice: rows [q R, q R + R) of block row i; each warp owns R / FW
+// rows in groups of 8 (lane l accumulates row 8g + reduce8_row(l) of group g)
 template <int R>
-__device__ void forward_slice(const FlowArgs& a, int i, int q) {
+__device__ void forward_slice(const FlowArgs& a, int i, int q, double2* vs) {
   const int bi = a.bi, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int RW = R / FW;  // rows per warp (<= 32: lane `k` owns row k of the warp)
+  constexpr int RW = R / FW;  // rows per warp
+  constexpr int G = RW / 8;   // groups of 8 rows
+  static_assert(RW % 8 == 0, "rows per warp must be a multiple of 8");
   const int64_t bi2 = static_cast<int64_t>(bi) * bi;
   const int rbase = q * R + warp * RW;  // first row of this warp inside block row i
-  double acc = 0.0;                     // sum for row rbase + lane (lane < RW)
   const int nchunk = bi / 64;           // double2 chunks per lane per row
   int* r_done = a.flags;
   int* b_done = a.flags + a.T;
   const int S = bi / R;
+  double acc[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) acc[g] = 0.0;
   for (int j = 0; j < i; ++j) {
-    wait_count(b_done + j, S);
+    if (j == i - 2 && threadIdx.x == 0)
+      prefetch_l2(a.L + tri_rm(i, i - 1) * bi2 + static_cast<int64_t>(q) * R * bi, sizeof(double) * R * bi);
+    if (j == i - 1 && threadIdx.x == 0) {
+      // the critical path of the solve runs through this slice from here on:
+      // stage its last tile and its rows of Dinv_i in L2 while beta_{i-1} is
+      // being produced, so they do not queue behind the bulk streaming reads
+      prefetch_l2(a.L + tri_rm(i, j) * bi2 + static_cast<int64_t>(q) * R * bi, sizeof(double) * R * bi);
+      prefetch_l2(a.dinv + static_cast<int64_t>(i) * bi2 + static_cast<int64_t>(q) * R * bi,
+                  sizeof(double) * R * bi);
+    }
+    else if (threadIdx.x == 0 && int64_t(a.T - 1 - j) * bi2 * 8 <= kL2Window)
+      // late phase (few block rows left): stream this band through L2 ahead of
+      // the loads, so the slice's rate is not bounded by its own load depth
+      prefetch_l2(a.L + tri_rm(i, j) * bi2 + static_cast<int64_t>(q) * R * bi, sizeof(double) * R * bi);
+    wait_count(b_done + j, S, j == i - 1);  // (its __syncthreads also retires the previous vs)
     const double* tile = a.L + tri_rm(i, j) * bi2;
     const double2* bj = reinterpret_cast<const double2*>(a.beta + static_cast<int64_t>(j) * bi);
-    double2 bv[8];
+    for (int e = threadIdx.x; e < bi / 2; e += FT) vs[e] = __ldcg(bj + e);
+    __syncthreads();
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
-      if (c < nchunk) bv[c] = __ldcg(bj + lane + 32 * c);
-#pragma unroll 2
-    for (int k = 0; k < RW; ++k) {
-      const double2* row = reinterpret_cast<const double2*>(tile + static_cast<int64_t>(rbase + k) * bi);
-      double p = 0.0;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < nchunk) {
-          const double2 v = __ldcs(row + lane + 32 * c);
-          p = fma(v.x, bv[c].x, p);
-          p = fma(v.y, bv[c].y, p);
-        }
-      p = warp_sum(p);
-      if (lane == k) acc += p;
+    for (int g = 0; g < G; ++g) {
+      double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      rows8_dot<false>(tile, bi, rbase + 8 * g, vs, nchunk, lane, p);
+      acc[g] += reduce8(p, lane);
     }
   }
   const int64_t g0 = static_cast<int64_t>(i) * bi;
-  if (lane < RW) a.xr[g0 + rbase + lane] = a.y[g0 + rbase + lane] - acc;
+  if (i == 0 && threadIdx.x == 0)
+    prefetch_l2(a.dinv + static_cast<int64_t>(q) * R * bi, sizeof(double) * R * bi);
+  const int mine = reduce8_row(lane);
+  if ((lane & 3) == 0) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int64_t r = g0 + rbase + 8 * g + mine;
+      a.xr[r] = a.y[r] - acc[g];
+    }
+  }
   signal_count(r_done + i);
-  wait_count(r_done + i, S);
+  if (a.prof && q == 0 && threadIdx.x == 0) a.prof[i] = gtimer();
+  wait_count(r_done + i, S, true);
   // beta_i[rows] = Dinv_i[rows, 0..row] r_i   (lower triangular)
   const double* D = a.dinv + static_cast<int64_t>(i) * bi2;
   const double2* rv = reinterpret_cast<const double2*>(a.xr + g0);
-  double2 r2[8];
+  for (int e = threadIdx.x; e < bi / 2; e += FT) vs[e] = __ldcg(rv + e);
+  __syncthreads();
 #pragma unroll
-  for (int c = 0; c < 8; ++c)
-    if (c < nchunk) r2[c] = __ldcg(rv + lane + 32 * c);
-  double out = 0.0;
-  for (int k = 0; k < RW; ++k) {
-    const int r = rbase + k;
-    const double2* row = reinterpret_cast<const double2*>(D + static_cast<int64_t>(r) * bi);
-    double p = 0.0;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int col = 2 * (lane + 32 * c);
-      if (c < nchunk && col <= r) {
-        const double2 v = __ldcg(row + lane + 32 * c);
-        p = fma(v.x, r2[c].x, p);
-        p = fma(v.y, r2[c].y, p);  // v.y = 0 above the diagonal
-      }
-    }
-    p = warp_sum(p);
-    if (lane == k) out = p;
+  for (int g = 0; g < G; ++g) {
+    double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    rows8_dot<true>(D, bi, rbase + 8 * g, vs, nchunk, lane, p);
+    const double out = reduce8(p, lane);
+    if ((lane & 3) == 0) a.beta[g0 + rbase + 8 * g + mine] = out;
   }
-  if (lane < RW) a.beta[g0 + rbase + lane] = out;
   signal_count(b_done + i);
+  if (a.prof && q == 0 && threadIdx.x == 0) a.prof[a.T + i] = gtimer();
 }
 
-// backward slice: columns [col0, col0 + R) of block row i; lanes own R/32
-// adjacent columns, warps split the bi rows of each tile
+// out[cols] += sum over `rows` rows r of M[r][cols] w[r] (ld = bi): lanes own
+// CPL adjacent columns (double2 loads), RPI rows per warp instruction; the
+// row weights come from w through warp shuffles (32 rows per load)
+template <int R, bool kStream>
+GPB_DEVINL void cols_dot(const double* M, int bi, int r_first, int rows, const double* w, int col0,
+                         int lane, double (&acc)[R / 32 > 2 ? R / 32 : 2]) {
+  constexpr int CPL = R / 32 > 2 ? R / 32 : 2;  // columns per lane
+  constexpr int LPR = R / CPL;                  // lanes per row
+  constexpr int RPI = 32 / LPR;                 // rows per instruction
+  const int sub = lane / LPR;                   // which of the RPI rows
+  const int cl = lane % LPR;
+  for (int rb = 0; rb < rows; rb += 32) {
+    const double wv = __ldcg(w + rb + lane);
+#pragma unroll 16
+    for (int k = 0; k < 32 / RPI; ++k) {
+      const int rr = RPI * k + sub;
+      const double wk = __shfl_sync(0xffffffffu, wv, rr);
+      const double* row = M + static_cast<int64_t>(r_first + rb + rr) * bi + col0 + cl * CPL;
+#pragma unroll
+      for (int c = 0; c < CPL; c += 2) {
+        const double2 x = kStream ? __ldcs(reinterpret_cast<const double2*>(row + c))
+                                  : __ldcg(reinterpret_cast<const double2*>(row + c));
+        acc[c] = fma(x.x, wk, acc[c]);
+        acc[c + 1] = fma(x.y, wk, acc[c + 1]);
+      }
+    }
+  }
+}
+
+// fixed-order sum of the warps' column partials: lanes of the same columns
+// (RPI > 1) first, then warps in index order; warp 0 gets the totals
+template <int R>
+GPB_DEVINL void cols_reduce(double (&acc)[R / 32 > 2 ? R / 32 : 2], double* red, int lane, int warp) {
+  constexpr int CPL = R / 32 > 2 ? R / 32 : 2;
+  constexpr int LPR = R / CPL;
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+  if (lane < LPR)
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) red[warp * R + lane * CPL + c] = acc[c];
+  __syncthreads();
+  if (warp == 0 && lane < LPR)
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      double s = 0.0;
+      for (int w = 0; w < FW; ++w) s += red[w * R + lane * CPL + c];
+      acc[c] = s;
+    }
+}
+
+// backward slice: columns [q R, q R + R) of block row i; warps split the bi
+// rows of each tile
 template <int R>
 __device__ void backward_slice(const FlowArgs& a, int i, int q, double* red) {
   const int bi = a.bi, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int CL = R / 32;  // columns per lane
+  constexpr int CPL = R / 32 > 2 ? R / 32 : 2;
+  constexpr int LPR = R / CPL;
   const int64_t bi2 = static_cast<int64_t>(bi) * bi;
-  const int col0 = q * R + lane * CL;
+  const int col0 = q * R;
   const int rows_w = bi / FW;  // rows of each tile per warp
   const int r0 = warp * rows_w;
   int* t_done = a.flags + 2 * a.T;
   int* a_done = a.flags + 3 * a.T;
   const int S = bi / R;
-  double acc[CL];
+  double acc[CPL];
 #pragma unroll
-  for (int c = 0; c < CL; ++c) acc[c] = 0.0;
+  for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
   wait_count(a.flags + a.T + i, S);  // beta_i complete (and r_i no longer read)
   for (int j = a.T - 1; j > i; --j) {
-    wait_count(a_done + j, S);
-    const double* tile = a.L + tri_rm(j, i) * bi2;
-    const double* aj = a.alpha + static_cast<int64_t>(j) * bi + r0;
-    for (int rb = 0; rb < rows_w; rb += 32) {
-      const double av = __ldcg(aj + rb + lane);
-#pragma unroll 16
-      for (int k = 0; k < 32; ++k) {
-        const double w = __shfl_sync(0xffffffffu, av, k);
-        const double* row = tile + static_cast<int64_t>(r0 + rb + k) * bi + col0;
-        if constexpr (CL == 1) {
-          acc[0] = fma(__ldcs(row), w, acc[0]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < CL; c += 2) {
-            const double2 v = __ldcs(reinterpret_cast<const double2*>(row + c));
-            acc[c] = fma(v.x, w, acc[c]);
-            acc[c + 1] = fma(v.y, w, acc[c + 1]);
-          }
-        }
-      }
+    if (j == i + 1) {  // critical from here on: stage the column slices in L2
+      prefetch_rows(a.L + tri_rm(j, i) * bi2 + col0, bi, R, bi);
+      prefetch_rows(a.dinv + static_cast<int64_t>(i) * bi2 + col0, bi, R, bi);
+    } else if (int64_t(j) * bi2 * 8 <= kL2Window) {  // late phase, as in the forward
+      prefetch_rows(a.L + tri_rm(j, i) * bi2 + col0, bi, R, bi);
     }
+    wait_count(a_done + j, S, j == i + 1);
+    cols_dot<R, true>(a.L + tri_rm(j, i) * bi2, bi, r0, rows_w, a.alpha + static_cast<int64_t>(j) * bi + r0,
+                      col0, lane, acc);
   }
-  // fixed-order cross-warp sum: t = beta - sum_w acc_w
+  if (i == a.T - 1) prefetch_rows(a.dinv + static_cast<int64_t>(i) * bi2 + col0, bi, R, bi);
   const int64_t g0 = static_cast<int64_t>(i) * bi;
+  cols_reduce<R>(acc, red, lane, warp);
+  if (warp == 0 && lane < LPR)
 #pragma unroll
-  for (int c = 0; c < CL; ++c) red[warp * R + lane * CL + c] = acc[c];
-  __syncthreads();
-  if (warp == 0) {
-#pragma unroll
-    for (int c = 0; c < CL; ++c) {
-      double s = 0.0;
-      for (int w = 0; w < FW; ++w) s += red[w * R + lane * CL + c];
-      a.xr[g0 + col0 + c] = __ldcg(a.beta + g0 + col0 + c) - s;
+    for (int c = 0; c < CPL; ++c) {
+      const int64_t e = g0 + col0 + lane * CPL + c;
+      a.xr[e] = __ldcg(a.beta + e) - acc[c];
     }
-  }
   signal_count(t_done + i);
-  wait_count(t_done + i, S);
-  // alpha_i[cols] = sum_{r >= col} Dinv_i[r][cols] t[r]
-  const double* D = a.dinv + static_cast<int64_t>(i) * bi2;
-  const double* tv = a.xr + g0 + r0;
+  if (a.prof && q == 0 && threadIdx.x == 0) a.prof[2 * a.T + i] = gtimer();
+  wait_count(t_done + i, S, true);
+  // alpha_i[cols] = sum_{r >= first col} Dinv_i[r][cols] t[r]  (Dinv_i lower)
 #pragma unroll
-  for (int c = 0; c < CL; ++c) acc[c] = 0.0;
-  const int first = q * R;  // rows above the slice's first column are zero in Dinv
-  for (int rb = 0; rb < rows_w; rb += 32) {
-    if (r0 + rb + 31 < first) continue;
-    const double tval = __ldcg(tv + rb + lane);
-#pragma unroll 8
-    for (int k = 0; k < 32; ++k) {
-      const double w = __shfl_sync(0xffffffffu, tval, k);
-      const double* row = D + static_cast<int64_t>(r0 + rb + k) * bi + col0;
-      if constexpr (CL == 1) {
-        acc[0] = fma(__ldcg(row), w, acc[0]);
-      } else {
-#pragma unroll
-        for (int c = 0; c < CL; c += 2) {
-          const double2 v = __ldcg(reinterpret_cast<const double2*>(row + c));
-          acc[c] = fma(v.x, w, acc[c]);
-          acc[c + 1] = fma(v.y, w, acc[c + 1]);
-        }
-      }
-    }
-  }
+  for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
+  const int lo = max(r0, col0 & ~31);  // rows above the slice's first column are zero
+  if (lo < r0 + rows_w)
+    cols_dot<R, false>(a.dinv + static_cast<int64_t>(i) * bi2, bi, lo, r0 + rows_w - lo, a.xr + g0 + lo, col0,
+                       lane, acc);
   __syncthreads();  // red is reused
+  cols_reduce<R>(acc, red, lane, warp);
+  if (warp == 0 && lane < LPR)
 #pragma unroll
-  for (int c = 0; c < CL; ++c) red[warp * R + lane * CL + c] = acc[c];
-  __syncthreads();
-  if (warp == 0) {
-#pragma unroll
-    for (int c = 0; c < CL; ++c) {
-      double s = 0.0;
-      for (int w = 0; w < FW; ++w) s += red[w * R + lane * CL + c];
-      a.alpha[g0 + col0 + c] = s;
-    }
-  }
+    for (int c = 0; c < CPL; ++c) a.alpha[g0 + col0 + lane * CPL + c] = acc[c];
   signal_count(a_done + i);
+  if (a.prof && q == 0 && threadIdx.x == 0) a.prof[3 * a.T + i] = gtimer();
 }
 
 template <int R>
 __global__ void __launch_bounds__(FT, 7) solve_flow_kernel(FlowArgs a) {
   __shared__ double red[FW * R];
+  __shared__ double2 vs[256];  // beta_j / r_i of the forward (bi <= 512)
   const int S = a.bi / R;
   const int s = blockIdx.x;
-  forward_slice<R>(a, s / S, s % S);
+  forward_slice<R>(a, s / S, s % S, vs);
   const int sb = gridDim.x - 1 - s;  // mirrored: early finishers start the backward
   backward_slice<R>(a, a.T - 1 - sb / S, sb % S, red);
 }
@@ -281,16 +385,33 @@ cudaError_t launch_solve_flow(const double* L, const double* dinv, const double*
                               cudaStream_t s, bool* launched) {
   *launched = false;
   if (R == 0 || bi % R != 0 || bi % 64 != 0 || bi > 512) return cudaSuccess;
-  FlowArgs a{L, dinv, y, beta, alpha, xr, flags, T, bi, R};
+  static unsigned long long* prof = nullptr;
+  static int prof_T = 0;
+  if (getenv("GPB_SOLVE_PROF") && prof_T != T) {
+    if (prof) cudaFree(prof);
+    cudaMalloc(&prof, sizeof(unsigned long long) * 4 * T);
+    prof_T = T;
+  }
+  FlowArgs a{L, dinv, y, beta, alpha, xr, flags, T, bi, R, getenv("GPB_SOLVE_PROF") ? prof : nullptr};
   cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * 4 * T, s);
   if (e != cudaSuccess) return e;
   const int nslices = T * (bi / R);
   switch (R) {
-    case 32: return launch_r<32>(a, nslices, s, launched);
-    case 64: return launch_r<64>(a, nslices, s, launched);
-    case 128: return launch_r<128>(a, nslices, s, launched);
-    default: return cudaSuccess;
+    case 32: e = launch_r<32>(a, nslices, s, launched); break;
+    case 64: e = launch_r<64>(a, nslices, s, launched); break;
+    case 128: e = launch_r<128>(a, nslices, s, launched); break;
+    default: break;
   }
+  if (a.prof && *launched) {  // per block row: r published, beta published, t published, alpha published
+    std::vector<unsigned long long> h(4 * T);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h.data(), a.prof, sizeof(unsigned long long) * 4 * T, cudaMemcpyDeviceToHost);
+    const unsigned long long t0 = h[0];
+    for (int i = 0; i < T; ++i)
+      fprintf(stderr, "flow row %3d: r %8.1f beta %8.1f | t %8.1f alpha %8.1f us\n", i, (h[i] - t0) * 1e-3,
+              (h[T + i] - t0) * 1e-3, (h[2 * T + i] - t0) * 1e-3, (h[3 * T + i] - t0) * 1e-3);
+  }
+  return e;
 }
 
 }  // namespace gpb
