@@ -51,6 +51,36 @@ WORKLOAD = ("config 2: n_train=32768, n_test=32768, n_regressors=128, 64 tiles o
 DATA = "synthetic: BASELINE.json mass-spring-damper generator, seed 0 (stands in for the paper's MSD data)"
 
 
+def workload_config(world: int) -> dict:
+    """The `config` object of the bench line (both arms print the same one)."""
+    if world == 1:
+        return {"workload": WORKLOAD, "l2": "inputs larger than L2 (lower K tiles 4.36 GB, "
+                "cross-covariance 8.6 GB per step)", "parallelism": "single GPU"}
+    c = strong_cfg()
+    p, q = _grid(world)
+    return {"workload": f"config 3 strong scaling: n_train={c['n']}, n_regressors={c['d']}, {c['tiles']} tiles "
+                        "of 512, FP64; step = SEK assembly + tiled Cholesky + alpha solve + loss "
+                        "(same n at every GPU count)",
+            "l2": "inputs larger than L2 (lower K tiles 17.3 GB)",
+            "parallelism": f"2D block-cyclic {p}x{q} tile grid, NCCL panel broadcasts on row/column communicators"}
+
+
+def _grid(world: int):
+    p = int(math.isqrt(world))
+    while world % p:
+        p -= 1
+    return p, world // p
+
+
+def strong_cfg() -> dict:
+    """BASELINE config 3 (GPB_BENCH_CONFIG=4: config 4's n = 131072, D = 16, T = 256)."""
+    if os.environ.get("GPB_BENCH_SMALL"):
+        return {"n": 4096, "d": 8, "tiles": 8}
+    if os.environ.get("GPB_BENCH_CONFIG") == "4":
+        return {"n": 131072, "d": 16, "tiles": 256}
+    return {"n": 65536, "d": 8, "tiles": 128}
+
+
 def weak_cfg(world: int) -> dict:
     """Config 2 weak-scaled to `world` GPUs: n = m = 512 * round(64 * world^(1/3))."""
     if os.environ.get("GPB_BENCH_SMALL"):
@@ -127,60 +157,121 @@ def _ncu_traffic():
 
 
 # ---------------------------------------------------------------- CPU side
-def cpu_cholesky_sample(n: int, d: int, tiles: int, seed: int = 0):
-    """Time the reference algorithm (oracle restatement of taskgp's tiled
-    Cholesky, runtime.py-style W workers, one BLAS thread each) on the host."""
-    import numpy as np
+# The CPU arm runs the reference itself when it is importable: taskgp 0.1.0
+# installed into baseline/_ref (pip install --target, git-ignored, travels to
+# the GPU box), through its public API with the protocol of BASELINE.md 3 /
+# start_runtime(RuntimeConfig(worker_count = all host cores))
+# (BLAS pinned to one thread per worker by the runtime, runtime.py:180-181) and
+# a fresh GPModel per repetition whose log_likelihood() assembles K, factors it
+# and runs the alpha solves -- the same work as the GPU arm's e2e
+# compute_loss().  Without it, the oracle port (oracle/tiled_gp.py, the same
+# tile algorithm: threaded assembly + ThreadedCholesky + blocked solves) runs.
+#
+# Sample: config 2 halved -- n = 16384, D = 128, 32 tiles of 512 (config 2's
+# tile size and feature count).  A full config-2 step takes ~2 min of taskgp
+# on the GPU box's 16 cores, so K + W of them do not fit the bench's few
+# minutes; the GPU arm reports its own rate on this same sample
+# ("e2e_at_cpu_sample") for the like-for-like ratio.
+CPU_SAMPLE = {"n": 16384, "d": 128, "tiles": 32}   # N = 1: config 2 halved
+CPU_SAMPLE_STRONG = {"n": 16384, "d": 8, "tiles": 32}  # N > 1: config 3 quartered
+if os.environ.get("GPB_BENCH_SMALL"):
+    CPU_SAMPLE = CPU_SAMPLE_STRONG = {"n": 2048, "d": 8, "tiles": 4}
 
-    from oracle.tiled_gp import ThreadedCholesky, row_blocks
-    from paper_2505_00136_b200.data import make_msd_dataset
 
-    train, _ = make_msd_dataset(n, 0, d, seed=seed)
-    z = train.z
-    sq = (z * z).sum(1)
-    d2 = np.maximum(sq[:, None] + sq[None, :] - 2.0 * (z @ z.T), 0.0)  # input prep, untimed
-    k = np.exp(d2 * -0.5) + 0.1 * np.eye(n)
-    b = n // tiles
-    grid = {(i, j): np.ascontiguousarray(k[i * b:(i + 1) * b, j * b:(j + 1) * b])
-            for i in range(tiles) for j in range(i + 1)}
-    del k, d2
-    workers = len(os.sched_getaffinity(0))
-    t0 = time.perf_counter()
-    ThreadedCholesky(workers)(grid, tiles)
-    dt = time.perf_counter() - t0
-    return chol_flops(n) / dt / 1e12, dt, workers
+def _taskgp():
+    """The reference package from baseline/_ref, or None."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "taskgp")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import taskgp
+        from taskgp.model import GPModel  # noqa: F401
+    except Exception:
+        return None
+    return taskgp
+
+
+class CpuArm:
+    """One step = assemble + factor + alpha solves of the CPU sample, the
+    reference's own code path when available."""
+
+    def __init__(self, sample=None):
+        from paper_2505_00136_b200.data import make_msd_dataset
+
+        c = sample or CPU_SAMPLE
+        self.n, self.d, self.tiles = c["n"], c["d"], c["tiles"]
+        self.train, _ = make_msd_dataset(self.n, 0, self.d, seed=0)
+        self.workers = len(os.sched_getaffinity(0))
+        self.tg = _taskgp()
+        self.kind = "reference" if self.tg else "port"
+        if self.tg:
+            self.tg.start_runtime(self.tg.RuntimeConfig(worker_count=self.workers))
+            self.ds = self.tg.Dataset(self.train.z, self.train.y)
+
+    def step(self) -> float:
+        t0 = time.perf_counter()
+        if self.tg:
+            from taskgp.model import GPModel
+
+            GPModel(self.ds, self.tg.KernelParams(1.0, 1.0, 0.1), tiles_per_dim=self.tiles).log_likelihood()
+        else:
+            from oracle.tiled_gp import OracleGP, ThreadedCholesky
+
+            OracleGP(self.train.z, self.train.y, self.tiles, cholesky=ThreadedCholesky(self.workers),
+                     assembly_workers=self.workers).log_likelihood()
+        return time.perf_counter() - t0
+
+    def close(self):
+        if self.tg:
+            self.tg.stop_runtime()
+
+    def describe(self, seconds: float) -> str:
+        who = ("taskgp 0.1.0 (the reference, baseline/_ref) GPModel(train, KernelParams(1, 1, 0.1), "
+               f"tiles_per_dim={self.tiles}).log_likelihood() under start_runtime(worker_count={self.workers})"
+               if self.tg else
+               f"oracle port of taskgp (threaded assembly + ThreadedCholesky + blocked solves, {self.workers} "
+               "workers x 1 BLAS thread)")
+        return (f"{who}: SEK assembly + tiled Cholesky + alpha solves at n={self.n}, D={self.d}, "
+                f"{self.tiles} tiles of {self.n // self.tiles}, {seconds:.1f} s per step; "
+                "flops counted as n^3/3 + n^2/2 + n/6")
 
 
 def run_reference(args, rank: int):
     if rank != 0:
         return
-    n, d, tiles = 8192, 128, 16
-    vals = []
-    for it in range(args.warmup + args.steps):
-        tf, dt, workers = cpu_cholesky_sample(n, d, tiles)
-        if it >= args.warmup:
-            vals.append((tf, dt))
-    tf = len(vals) * chol_flops(n) / sum(v[1] for v in vals) / 1e12
-    sample = (f"tiled Cholesky of the reference algorithm (oracle restatement of taskgp tiled.py:168-204, "
-              f"W={workers} workers x 1 BLAS thread) at n={n}, D={d}, {tiles} tiles of {n // tiles}; "
-              f"bounded sample of config 2 (n=32768 would take ~100 s per step)")
+    arm = CpuArm(CPU_SAMPLE if args.gpus == 1 else CPU_SAMPLE_STRONG)
+    try:
+        times = []
+        for it in range(args.warmup + args.steps):
+            dt = arm.step()
+            if it >= args.warmup:
+                times.append(dt)
+    finally:
+        arm.close()
+    tf = len(times) * chol_flops(arm.n) / sum(times) / 1e12
+    sample = arm.describe(sum(times) / len(times))
     line = {"metric": METRIC, "value": tf, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * sum(v[1] for v in vals) / len(vals),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": DATA, "config": {"workload": WORKLOAD, "sample": sample}, "impl": "reference",
-            "cpu_baseline": {"value": tf, "unit": "TFLOP/s", "cores": workers, "kind": "port",
+            "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": DATA, "config": workload_config(args.gpus), "impl": "reference",
+            "sample": sample,
+            "cpu_baseline": {"value": tf, "unit": "TFLOP/s", "cores": arm.workers, "kind": arm.kind,
                              "sample": sample},
             "e2e": {"value": tf, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline_block():
-    n, d, tiles = 16384, 128, 32
-    tf, dt, workers = cpu_cholesky_sample(n, d, tiles)
-    return {"value": tf, "unit": "TFLOP/s", "cores": workers, "kind": "port",
-            "sample": (f"oracle restatement of taskgp's tiled Cholesky (tiled.py:168-204), {workers} "
-                       f"worker threads x 1 BLAS thread, n={n}, D={d}, {tiles} tiles of {n // tiles}, "
-                       f"{dt:.1f} s")}
+    """One bounded step of the CPU arm (rank 0, N = 1)."""
+    arm = CpuArm()
+    try:
+        dt = arm.step()
+    finally:
+        arm.close()
+    return {"value": chol_flops(arm.n) / dt / 1e12, "unit": "TFLOP/s", "cores": arm.workers,
+            "kind": arm.kind, "sample": arm.describe(dt)}
 
 
 # ---------------------------------------------------------------- GPU side
@@ -257,7 +348,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     clk = clocks.stop()
     lib.gpb_model_launch_count(h, ctypes.byref(lc1))
     kms, kfl, kcnt = (ctypes.c_double * 8)(), (ctypes.c_double * 8)(), (ctypes.c_int64 * 8)()
+    kbusy = (ctypes.c_double * 8)()
     lib.gpb_model_kernel_stats(h, kms, kfl, kcnt)
+    lib.gpb_model_kernel_busy(h, kbusy)
     lib.gpb_model_set_profiling(h, 0)
     total_ms = ev0.elapsed_time(ev1)
     factor_ms, pred_ms = phase[1], phase[3] + phase[4]
@@ -271,11 +364,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # roofline.achieved from ALGORITHMIC flops: the step's GEMM work is the
     # Cholesky trailing updates and panel solves (n^3/3) plus the prediction
     # triangular solve (n^2 m); POTRF/TRTRI tiles (2 b^3/3 each, <0.1%) are
-    # not GEMM work.  The executed count (with the lower-triangular waste of
-    # 128-blocks) is reported beside it.
+    # not GEMM work.  Time base: the GEMM class's BUSY time, i.e. the length
+    # of the union of its launch intervals over both streams (CUDA events
+    # around every launch on its stream), so overlapping launches of the
+    # critical and main streams are not double-counted.  The executed count
+    # (with the lower-triangular waste of 128-blocks) is reported beside it.
     gemm_alg = K * (n ** 3 / 3.0 + float(n) * n * m)
-    gemm_tf = gemm_alg / (kms[0] * 1e-3) / 1e12 if kms[0] else 0.0
-    gemm_tf_exec = kfl[0] / (kms[0] * 1e-3) / 1e12 if kms[0] else 0.0
+    gemm_tf = gemm_alg / (kbusy[0] * 1e-3) / 1e12 if kbusy[0] else 0.0
+    gemm_tf_exec = kfl[0] / (kbusy[0] * 1e-3) / 1e12 if kbusy[0] else 0.0
 
     # ---- e2e: public API, host buffers, copies inside the timed region
     # inputs live in pinned host memory (the API's H2D copies read them there)
@@ -286,17 +382,35 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     train_h = gpb.Dataset(pinned(train.z), pinned(train.y))
     test_h = gpb.Dataset(pinned(test.z), pinned(test.y))
-    e2e_chol, e2e_pred = [], []
-    for _ in range(min(K, 3) if rank == 0 else 0):
-        t0 = time.perf_counter()
-        model = gpb.GPModel(train_h, gpb.KernelParams(1.0, 1.0, 0.1), tiles)
-        model.compute_loss()  # H2D z, y; assemble; factor; solves; D2H loss terms
-        t1 = time.perf_counter()
-        model.predict_with_uncertainty(test_h)  # H2D zt; predict; D2H mean + var
-        t2 = time.perf_counter()
-        e2e_chol.append(t1 - t0)
-        e2e_pred.append(t2 - t1)
-        del model
+
+    def e2e_reps(tr, te, t, reps):
+        chol, pred = [], []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            model = gpb.GPModel(tr, gpb.KernelParams(1.0, 1.0, 0.1), t)
+            model.compute_loss()  # H2D z, y; assemble; factor; solves; D2H loss terms
+            t1 = time.perf_counter()
+            if te is not None:
+                model.predict_with_uncertainty(te)  # H2D zt; predict; D2H mean + var
+            t2 = time.perf_counter()
+            chol.append(t1 - t0)
+            pred.append(t2 - t1)
+            model.close()
+        return chol, pred
+
+    e2e_chol, e2e_pred = e2e_reps(train_h, test_h, tiles, K) if rank == 0 else ([], [])
+    # the GPU arm on the CPU arm's sample (like-for-like ratio at the same n)
+    same = None
+    if rank == 0 and world == 1:
+        cs = CPU_SAMPLE
+        tr_s, _ = gpb.make_msd_dataset(cs["n"], 0, cs["d"], seed=0)
+        tr_s = gpb.Dataset(pinned(tr_s.z), pinned(tr_s.y))
+        e2e_reps(tr_s, None, cs["tiles"], 2)  # warm-up of that shape
+        sc, _ = e2e_reps(tr_s, None, cs["tiles"], K)
+        same = {"n": cs["n"], "d": cs["d"], "tiles": cs["tiles"], "unit": "TFLOP/s",
+                "value": chol_flops(cs["n"]) / statistics.median(sc) / 1e12,
+                "api": "GPModel(train).compute_loss(), host numpy in pinned memory (assembly + factor + "
+                       "solves + copies), median of K reps"}
     lib.gpb_model_destroy(h)
     if rank != 0:
         rt.stop()
@@ -308,9 +422,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
-        "config": {"workload": WORKLOAD, "l2": "inputs larger than L2 (lower K tiles 4.36 GB, "
-                   "cross-covariance 8.6 GB per step)",
-                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas"},
+        "config": workload_config(1) if world == 1 else dict(workload_config(1),
+                                                                 parallelism=f"{world} independent replicas"),
         "predict_variance": {"value": pts, "unit": "test points/s",
                              "tflops": pts * pred_flops_per_point(n, d) / 1e12},
         "phases_ms_per_step": {k: float(phase[i] / K) for i, k in enumerate(
@@ -326,16 +439,22 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "predict_variance_points_per_s": m / statistics.median(e2e_pred) if e2e_pred else None,
                 "h2d_bytes_per_step": 8 * (n * d + n + m * d), "d2h_bytes_per_step": 8 * (2 + 2 * m),
                 "api": "GPModel(train).compute_loss() then predict_with_uncertainty(test), host numpy "
-                       "arrays in pinned memory"},
+                       "arrays in pinned memory, median of K reps"},
+        "e2e_at_cpu_sample": same,
         "roofline": {"bound": "tensor", "kernel": "dgemm_tma_kernel (TMA-fed DMMA.8x8x4)",
                      "achieved": gemm_tf, "peak": peak.value, "unit": "TFLOP/s",
                      "frac": gemm_tf / peak.value if peak.value else None,
                      "traffic": _ncu_traffic(),
+                     "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the "
+                                       "prediction-sweep GEMM from the committed ncu --set full capture "
+                                       "(profiles/r01_gemm_traffic.json), not measured in this run",
                      "peak_source": "in-run FP64 DMMA probe (MEASURED_PEAKS.json has no FP64 entry)",
                      "achieved_executed_flops": gemm_tf_exec,
-                     "achieved_basis": "algorithmic flops n^3/3 + n^2 m per step over the summed GEMM "
-                                       "launch durations (CUDA events on the launching streams)",
-                     "launches": int(kcnt[0]), "share_of_step": kms[0] / total_ms if total_ms else None,
+                     "achieved_basis": "algorithmic flops n^3/3 + n^2 m per step over the GEMM busy time: "
+                                       "the union of the GEMM launch intervals on both streams (CUDA events "
+                                       "around every launch), so overlapping launches count once",
+                     "launches": int(kcnt[0]), "busy_ms": kbusy[0], "summed_launch_ms": kms[0],
+                     "share_of_step": kbusy[0] / total_ms if total_ms else None,
                      "cholesky_frac_of_peak": value / world / peak.value if peak.value else None},
         "kernel_classes_ms": {"gemm": kms[0], "potrf_trtri": kms[1], "sek": kms[2]},
         "clocks": clk,

@@ -137,6 +137,10 @@ int gpb_model_stream(gpb_model* m, void** stream);
  * (device ms, executed flops, launches) since then. */
 int gpb_model_set_profiling(gpb_model* m, int on);
 int gpb_model_kernel_stats(gpb_model* m, double ms[8], double flops[8], int64_t count[8]);
+/* per class: length of the union of its launch intervals since set_profiling
+ * (the launches of the critical and main streams overlap, so the summed
+ * durations of kernel_stats can exceed wall time; this cannot) */
+int gpb_model_kernel_busy(gpb_model* m, double busy_ms[8]);
 /* sustained FP64 tensor-pipe (DMMA.8x8x4) throughput of this GPU, TFLOP/s */
 int gpb_fp64_peak_probe(gpb_ctx* ctx, double seconds, double* tflops);
 

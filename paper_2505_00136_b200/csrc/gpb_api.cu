@@ -221,7 +221,8 @@ struct gpb_model {
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> evpool;
   size_t evnext = 0;
-  double cls_ms[8] = {0}, cls_flops[8] = {0};
+  cudaEvent_t prof_ref = nullptr;  // time origin of the launch intervals (on st)
+  double cls_ms[8] = {0}, cls_flops[8] = {0}, cls_busy[8] = {0};
   int64_t cls_n[8] = {0};
 };
 
@@ -320,15 +321,39 @@ struct ProfScope {
   }
 };
 
+// Sum of launch durations per kernel class, and the class's busy time: the
+// length of the union of its launch intervals across the model's streams
+// (launches on the critical and main streams overlap, so their durations do
+// not add up to wall time).
 int prof_collect(gpb_model* m) {
   if (m->recs.empty()) return GPB_OK;
-  CUDA_TRY(cudaStreamSynchronize(m->st));
+  CUDA_TRY(cudaDeviceSynchronize());
+  std::vector<std::pair<double, double>> iv[8];
   for (auto& r : m->recs) {
-    float ms = 0;
+    float ms = 0, t0 = 0, t1 = 0;
     cudaEventElapsedTime(&ms, r.a, r.b);
     m->cls_ms[r.cls] += ms;
     m->cls_flops[r.cls] += r.flops;
     m->cls_n[r.cls] += 1;
+    if (m->prof_ref && cudaEventElapsedTime(&t0, m->prof_ref, r.a) == cudaSuccess &&
+        cudaEventElapsedTime(&t1, m->prof_ref, r.b) == cudaSuccess)
+      iv[r.cls].push_back({t0, t1});
+  }
+  for (int c = 0; c < 8; ++c) {
+    auto& v = iv[c];
+    std::sort(v.begin(), v.end());
+    double busy = 0.0, lo = 0.0, hi = -1.0;
+    for (auto& x : v) {
+      if (x.first > hi) {
+        if (hi > lo) busy += hi - lo;
+        lo = x.first;
+        hi = x.second;
+      } else {
+        hi = std::max(hi, x.second);
+      }
+    }
+    if (hi > lo) busy += hi - lo;
+    m->cls_busy[c] += busy;
   }
   m->recs.clear();
   m->evnext = 0;
@@ -1386,6 +1411,7 @@ int gpb_model_destroy(gpb_model* m) {
   free_model(m, live);
   for (cudaEvent_t e : m->evpool) cudaEventDestroy(e);
   for (cudaEvent_t e : m->sync_ev) cudaEventDestroy(e);
+  if (m->prof_ref) cudaEventDestroy(m->prof_ref);
   if (m->crit) cudaStreamDestroy(m->crit);
   if (m->e0) cudaEventDestroy(m->e0);
   if (m->e1) cudaEventDestroy(m->e1);
@@ -1700,8 +1726,12 @@ int gpb_model_set_profiling(gpb_model* m, int on) {
   GPB_TRY(prof_collect(m));
   m->prof = on != 0;
   for (int i = 0; i < 8; ++i) {
-    m->cls_ms[i] = m->cls_flops[i] = 0.0;
+    m->cls_ms[i] = m->cls_flops[i] = m->cls_busy[i] = 0.0;
     m->cls_n[i] = 0;
+  }
+  if (m->prof) {
+    if (!m->prof_ref) CUDA_TRY(cudaEventCreate(&m->prof_ref));
+    CUDA_TRY(cudaEventRecord(m->prof_ref, m->st));
   }
   return GPB_OK;
 }
@@ -1714,6 +1744,13 @@ int gpb_model_kernel_stats(gpb_model* m, double ms[8], double flops[8], int64_t 
     if (flops) flops[i] = m->cls_flops[i];
     if (count) count[i] = m->cls_n[i];
   }
+  return GPB_OK;
+}
+
+int gpb_model_kernel_busy(gpb_model* m, double busy_ms[8]) {
+  if (!m || !busy_ms) return fail(GPB_INVALID_CONFIG, "null argument");
+  GPB_TRY(prof_collect(m));
+  for (int i = 0; i < 8; ++i) busy_ms[i] = m->cls_busy[i];
   return GPB_OK;
 }
 
