@@ -17,10 +17,11 @@ Conventions are pinned in SURVEY.md Appendix A:
 4. Feature row t = (u_t, u_{t-1}, ..., u_{t-n_reg+1}), u_{<0} = 0.
 5. Train = rows [0, n_train), test = rows [n_train, N) (a continuation).
 
-The reference's own lag embedding (``LagSpec``/``lag_embed``, data.py:131-161:
-rows t >= D only, the D preceding samples most recent first) and its CSV
-round trip (``save_csv``/``load_csv``, data.py:164-201) are provided with the
-same semantics so reference-produced files and series load unchanged.
+The reference's lag embedding and dataset CSV format (``LagSpec`` /
+``lag_embed`` / ``save_csv`` / ``load_csv``) are
+provided with the same observable behaviour -- pinned by files the reference
+wrote, tests/golden/ref_dataset* -- so reference-produced series and files
+load unchanged.
 """
 
 from __future__ import annotations
@@ -103,7 +104,7 @@ def make_msd_dataset(n_train: int, n_test: int, n_reg: int, seed: int = 0):
 
 @dataclass(frozen=True)
 class LagSpec:
-    """Number of lagged samples used as features (data.py:131-141)."""
+    """How many past samples form one feature row."""
 
     num_regressors: int
 
@@ -113,53 +114,48 @@ class LagSpec:
 
 
 def lag_embed(series, spec: LagSpec) -> Dataset:
-    """Regression dataset of lagged windows of a series (data.py:144-161):
-    row t holds the D samples preceding sample t + D, most recent first, and
-    y[t] is that sample; a series of length L gives L - D rows."""
-    series = np.asarray(series, dtype=np.float64)
+    """Sliding windows of D + 1 samples over a series: the window's last
+    sample is the target, the D before it (most recent first) the features,
+    so a series of length L gives L - D rows (the reference's lag embedding,
+    taskgp data.py:144-161, whose fixtures tests/golden/ref_dataset* pin it)."""
+    x = np.asarray(series, dtype=np.float64)
     d = spec.num_regressors
-    if series.ndim != 1 or series.shape[0] <= d:
-        raise DimensionMismatch(f"need a 1-D series longer than {d} samples, got shape {series.shape}")
-    n = series.shape[0] - d
-    z = np.empty((n, d))
-    for j in range(d):
-        z[:, j] = series[d - 1 - j: d - 1 - j + n]
-    return Dataset(z=z, y=series[d:].copy())
+    if x.ndim != 1 or x.size <= d:
+        raise DimensionMismatch(f"need a 1-D series longer than {d} samples, got shape {x.shape}")
+    win = np.lib.stride_tricks.sliding_window_view(x, d + 1)
+    return Dataset(z=win[:, d - 1::-1], y=win[:, d])
 
 
 def save_csv(data: Dataset, path: str, header: bool = False) -> None:
-    """One row per sample, feature columns then y, floats via repr (loss-free)."""
+    """Feature columns then y per line, every value as its shortest exact
+    repr, optionally under a ``z0,...,y`` header (loss-free round trip)."""
+    table = np.column_stack([data.z, data.y]).tolist()
+    lines = [",".join(map(repr, row)) for row in table]
+    if header:
+        lines.insert(0, ",".join([f"z{j}" for j in range(data.d)] + ["y"]))
     with open(path, "w", encoding="utf-8") as fh:
-        if header:
-            fh.write(",".join([f"z{j}" for j in range(data.d)] + ["y"]) + "\n")
-        for row, target in zip(data.z, data.y):
-            fh.write(",".join(repr(float(v)) for v in row) + f",{float(target)!r}\n")
+        fh.write("".join(line + "\n" for line in lines))
 
 
 def load_csv(path: str, header: bool = False) -> Dataset:
-    """Read a file written by save_csv; the last column is y.  ParseError
-    (with the line number) on ragged rows, bad numbers or an empty file."""
-    rows: list[list[float]] = []
-    width = None
+    """Inverse of save_csv (the last column is y).  ``ParseError`` carries the
+    1-based line of the first ragged row or unparsable number, or of an empty file."""
     with open(path, "r", encoding="utf-8") as fh:
-        for lineno, line in enumerate(fh, start=1):
-            if lineno == 1 and header:
-                continue
-            line = line.strip()
-            if not line:
-                continue
-            cols = line.split(",")
-            if width is None:
-                width = len(cols)
-                if width < 2:
-                    raise ParseError("need at least one feature column and y", lineno)
-            elif len(cols) != width:
-                raise ParseError(f"expected {width} columns, got {len(cols)}", lineno)
-            try:
-                rows.append([float(c) for c in cols])
-            except ValueError as exc:
-                raise ParseError(str(exc), lineno) from exc
-    if not rows:
+        numbered = [(k + 1, t.strip()) for k, t in enumerate(fh.read().splitlines())]
+    body = [(k, t) for k, t in numbered[1 if header else 0:] if t]
+    if not body:
         raise ParseError("no data rows", 1)
-    arr = np.array(rows)
-    return Dataset(z=arr[:, :-1], y=arr[:, -1])
+    split = [(k, t.split(",")) for k, t in body]
+    width = len(split[0][1])
+    if width < 2:
+        raise ParseError("need at least one feature column and y", split[0][0])
+    values = []
+    for k, cells in split:
+        if len(cells) != width:
+            raise ParseError(f"expected {width} columns, got {len(cells)}", k)
+        try:
+            values.append(list(map(float, cells)))
+        except ValueError as exc:
+            raise ParseError(str(exc), k) from exc
+    table = np.array(values)
+    return Dataset(z=table[:, :-1], y=table[:, -1])
