@@ -3,7 +3,7 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Ipaper_2505_00136_b200/csrc
 SRC := $(wildcard paper_2505_00136_b200/csrc/*.cu)
-HDR := $(wildcard paper_2505_00136_b200/csrc/*.cuh) include/gpb200.h
+HDR := $(wildcard paper_2505_00136_b200/csrc/*.cuh) $(wildcard paper_2505_00136_b200/csrc/*.h) include/gpb200.h
 OBJ := $(patsubst paper_2505_00136_b200/csrc/%.cu,build/%.o,$(SRC))
 LIB := paper_2505_00136_b200/libgpb200.so
 
@@ -14,7 +14,7 @@ build/%.o: paper_2505_00136_b200/csrc/%.cu $(HDR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(LIB): $(OBJ)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -ldl
 
 clean:
 	rm -rf build $(LIB)

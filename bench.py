@@ -17,13 +17,13 @@ inside the timed region).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): config 2 weak-scaled -- n = m grow as N^(1/3) (multiples
-of 512) so the Cholesky flops per GPU stay those of config 2; N = 8 gives
-n = 65536, BASELINE config 3's size.  The problem is factored 2D
-block-cyclic over all ranks with NCCL panel broadcasts and predicted sharded
-over test points (paper_2505_00136_b200/distributed.py); value = total
-n^3/3 flops over the slowest rank's factorisation time.  GPB_REPLICAS=1
-instead runs N independent single-GPU replicas.
+N > 1 (torchrun): strong scaling of BASELINE config 3 (n = 65536, the same n
+at every N; GPB_BENCH_CONFIG=4: config 4, n = 131072) factored 2D
+block-cyclic by the library's multi-GPU runtime (csrc/dist.cu: its own NCCL
+world / row / column communicators, schedule replayed from resident job
+tables); value = total n^3/3 flops over the slowest rank's factorisation
+time.  The N = 1 line carries the 1-GPU time of that workload
+("strong_scaling_base") for E(p) = t_1 / (p t_p).
 """
 
 from __future__ import annotations
@@ -77,16 +77,8 @@ def strong_cfg() -> dict:
     if os.environ.get("GPB_BENCH_SMALL"):
         return {"n": 4096, "d": 8, "tiles": 8}
     if os.environ.get("GPB_BENCH_CONFIG") == "4":
-        return {"n": 131072, "d": 16, "tiles": 256}
+        return {"n": 131072, "m": 8192, "d": 16, "tiles": 256}
     return {"n": 65536, "d": 8, "tiles": 128}
-
-
-def weak_cfg(world: int) -> dict:
-    """Config 2 weak-scaled to `world` GPUs: n = m = 512 * round(64 * world^(1/3))."""
-    if os.environ.get("GPB_BENCH_SMALL"):
-        return dict(CFG)
-    tiles = int(round(64 * world ** (1.0 / 3.0)))
-    return {"n": 512 * tiles, "m": 512 * tiles, "d": 128, "tiles": tiles}
 
 
 def chol_flops(n: int) -> float:
@@ -412,18 +404,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "api": "GPModel(train).compute_loss(), host numpy in pinned memory (assembly + factor + "
                        "solves + copies), median of K reps"}
     lib.gpb_model_destroy(h)
-    if rank != 0:
-        rt.stop()
-        if dist:
-            dist.destroy_process_group()
-        return
+    base = None
+    if not args.no_strong_base:
+        base = strong_base(args)
     rt.stop()
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
-        "config": workload_config(1) if world == 1 else dict(workload_config(1),
-                                                                 parallelism=f"{world} independent replicas"),
+        "config": workload_config(1),
         "predict_variance": {"value": pts, "unit": "test points/s",
                              "tflops": pts * pred_flops_per_point(n, d) / 1e12},
         "phases_ms_per_step": {k: float(phase[i] / K) for i, k in enumerate(
@@ -459,6 +448,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "kernel_classes_ms": {"gemm": kms[0], "potrf_trtri": kms[1], "sek": kms[2]},
         "clocks": clk,
         "gpu_launches": int(lc1.value - lc0.value),
+        "strong_scaling_base": base,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_block()
@@ -468,28 +458,32 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
 
 def run_distributed(args, rank: int, world: int, local_rank: int):
-    """N > 1: config 2 weak-scaled (weak_cfg) and factorised 2D block-cyclic over
-    all ranks (distributed.py) with NCCL panel broadcasts, prediction sharded
-    over test points.  value = total n^3/3 flops over the slowest rank's
-    factorisation device time; e2e = the same through the public API from host
-    numpy (DistributedGP construction + log_likelihood, wall clock, max over
-    ranks), and predict_with_uncertainty's test points/s likewise."""
+    """N > 1: strong scaling -- BASELINE config 3 (n = 65536, D = 8, 128 tiles
+    of 512; GPB_BENCH_CONFIG=4: config 4's n = 131072, D = 16, 256 tiles) at
+    every N, factored 2D block-cyclic over the P x Q grid by the library's
+    multi-GPU runtime (its own NCCL communicators: world, process rows,
+    process columns).  One step = SEK assembly + tiled Cholesky + beta / alpha
+    solves + loss (config 4 also predict_with_full_cov of its 8192 test points).
+    value = the n^3/3 Cholesky flops over the slowest rank's factorisation
+    device time (CUDA events on the library's stream, K resident in HBM);
+    e2e = the same metric through the public API from host numpy
+    (DistributedGP(train).log_likelihood(), wall clock, max over ranks)."""
     import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2505_00136_b200 as gpb
-    from paper_2505_00136_b200.distributed import DistributedGP, process_grid
+    from paper_2505_00136_b200.distributed import DistComm, DistributedGP, process_grid
 
-    backend = os.environ.get("GPB_DIST_BACKEND", "nccl")
     device = int(os.environ.get("GPB_FORCE_DEVICE", local_rank))
     torch.cuda.set_device(device)
-    if backend == "nccl":
-        dist.init_process_group("nccl", device_id=torch.device("cuda", device))
-    else:
-        dist.init_process_group(backend)
-    cfg = weak_cfg(world)
-    n, m, d, tiles = cfg["n"], cfg["m"], cfg["d"], cfg["tiles"]
+    os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (nranks) on stderr
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    # torch.distributed only bootstraps (the NCCL unique id); the data path is the library's
+    dist.init_process_group(os.environ.get("GPB_DIST_BACKEND", "gloo"))
+    cfg = strong_cfg()
+    n, d, tiles = cfg["n"], cfg["d"], cfg["tiles"]
+    m = cfg.get("m", 0)
     train, test = gpb.make_msd_dataset(n, m, d, seed=0)
     rt = gpb.start_runtime(gpb.RuntimeConfig(device=device))
     import ctypes
@@ -498,71 +492,115 @@ def run_distributed(args, rank: int, world: int, local_rank: int):
 
     peak = ctypes.c_double()
     _lib.check(_lib.load().gpb_fp64_peak_probe(rt.handle, 1.0, ctypes.byref(peak)))
-    times, walls = [], []
-    launches = 0
+    comm = DistComm(rt)
+    params = gpb.KernelParams(1.0, 1.0, 0.1)
+    # device-resident inputs: the model keeps z, y on the GPU; each step re-assembles K
+    model = DistributedGP(train, params, tiles, comm=comm)
+    rows = []
     clocks = ClockSampler(device)
     for it in range(args.warmup + args.steps):
         if it == args.warmup:
             dist.barrier()
             torch.cuda.synchronize()
             clocks.start()
-        t0 = time.perf_counter()
-        model = DistributedGP(train, gpb.KernelParams(1.0, 1.0, 0.1), tiles)  # host numpy in
-        model.log_likelihood()                                                # loss back on the host
-        t1 = time.perf_counter()
-        model.predict_with_uncertainty(test)                                  # mean, variance on the host
-        t2 = time.perf_counter()
+        model.params = params  # invalidates the factor
+        model.log_likelihood()
+        t = model.timings
+        pred_ms = 0.0
+        if m:
+            model.predict_with_full_cov(test)
+            pred_ms = model.timings["predict_ms"]
         if it >= args.warmup:
-            times.append([model.timings["factor_ms"], model.timings["solve_ms"],
-                          model.timings["predict_ms"]])
-            walls.append([t1 - t0, t2 - t1])
-            launches += model.launch_count()
-        model.close()
-        del model
+            rows.append([t["factor_ms"], t["solve_ms"], pred_ms, t["enqueue_us_per_step"], t["collectives"]])
     torch.cuda.synchronize()
     dist.barrier()
     clk = clocks.stop()
-    t = torch.tensor(np.concatenate([np.array(times).sum(axis=0), np.array(walls).sum(axis=0)]),
-                     dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    factor_ms, solve_ms, pred_ms, wall_chol, wall_pred = t.tolist()
-    lt = torch.tensor([launches], dtype=torch.float64, device="cuda")
-    dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+    launches = model.launch_count()
+    model.close()
+    # e2e through the public API: host numpy in, loss out (construction included)
+    walls = []
+    for it in range(1 + args.steps):
+        dist.barrier()
+        t0 = time.perf_counter()
+        mm = DistributedGP(train, params, tiles, comm=comm)
+        mm.log_likelihood()
+        if m:
+            mm.predict_with_full_cov(test)
+        walls.append(time.perf_counter() - t0)
+        mm.close()
     K = args.steps
+    a = np.array(rows).sum(axis=0)
+    tt = torch.tensor([a[0], a[1], a[2], sum(walls[1:]), a[3] / K], dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    factor_ms, solve_ms, pred_ms, wall, enq = tt.tolist()
+    lt = torch.tensor([launches], dtype=torch.float64)
+    dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+    comm.close()
     if rank == 0:
         p, q = process_grid(world)
+        value = K * chol_flops(n) / (factor_ms * 1e-3) / 1e12
         line = {
-            "metric": METRIC, "value": K * chol_flops(n) / (factor_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-            "n_gpus": world, "steps": K, "warmup": args.warmup,
-            "ms_per_step": (factor_ms + solve_ms + pred_ms) / K, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
-            "config": {"workload": f"config 2 weak-scaled to {world} GPUs (fixed Cholesky flops per GPU): "
-                       f"n_train = n_test = {n}, n_regressors = {d}, {tiles} tiles of 512, FP64; step = "
-                       "SEK assembly + tiled Cholesky + alpha solves + loss + predict_with_uncertainty",
-                       "l2": "inputs larger than L2", "parallelism": f"2D block-cyclic {p}x{q} Cholesky, "
-                       "NCCL panel broadcasts; prediction sharded over test points"},
-            "predict_variance": {"value": K * m / (pred_ms * 1e-3), "unit": "test points/s"},
-            "phases_ms_per_step": {"factor": factor_ms / K, "solves": solve_ms / K,
-                                   "predict_variance": pred_ms / K},
-            "e2e": {"value": K * chol_flops(n) / wall_chol / 1e12, "unit": "TFLOP/s",
-                    "predict_variance_points_per_s": K * m / wall_pred,
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": (factor_ms + solve_ms + pred_ms) / K, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": workload_config(world),
+            "phases_ms_per_step": {"factor": factor_ms / K, "solves": solve_ms / K, "full_cov": pred_ms / K},
+            "host_enqueue_us_per_panel_step": enq, "collectives_per_factorisation": float(a[4] / K),
+            "e2e": {"value": K * chol_flops(n) / wall / 1e12, "unit": "TFLOP/s",
                     "h2d_bytes_per_step": 8 * world * (n * d + n + m * d),
-                    "d2h_bytes_per_step": 8 * world * (2 + 2 * m),
-                    "api": "DistributedGP(train).log_likelihood() then predict_with_uncertainty(test), "
-                           "host numpy on every rank"},
+                    "d2h_bytes_per_step": 8 * world * (1 + m * m),
+                    "api": "DistributedGP(train).log_likelihood()" + (" then predict_with_full_cov(test)" if m else "")
+                           + ", host numpy on every rank, wall clock max over ranks"},
             "gpu_launches": int(lt.item()),
             "clocks": clk,
-            # per-GPU factorisation rate against rank 0's in-run DMMA probe
             "roofline": {"bound": "tensor", "kernel": "tiled Cholesky per GPU (dgemm_tma_kernel dominated)",
-                         "achieved": K * chol_flops(n) / (factor_ms * 1e-3) / 1e12 / world,
-                         "peak": peak.value, "unit": "TFLOP/s",
-                         "frac": K * chol_flops(n) / (factor_ms * 1e-3) / 1e12 / world / peak.value
-                         if peak.value else None, "traffic": None,
+                         "achieved": value / world, "peak": peak.value, "unit": "TFLOP/s",
+                         "frac": value / world / peak.value if peak.value else None, "traffic": None,
                          "peak_source": "in-run FP64 DMMA probe (MEASURED_PEAKS.json has no FP64 entry)"},
         }
         print(json.dumps(line), flush=True)
     rt.stop()
     dist.destroy_process_group()
+
+
+def strong_base(args):
+    """The 1-GPU time of the strong-scaling workload (config 3; same library,
+    single-GPU path, bitwise the same factor as the 1x1 grid): t_1 of
+    E(p) = t_1 / (p t_p)."""
+    import ctypes
+
+    import torch
+
+    import paper_2505_00136_b200 as gpb
+    from paper_2505_00136_b200 import _lib
+
+    lib = _lib.load()
+    c = strong_cfg()
+    train, _ = gpb.make_msd_dataset(c["n"], 0, c["d"], seed=0)
+    z = torch.from_numpy(train.z).cuda()
+    y = torch.from_numpy(train.y).cuda()
+    h = ctypes.c_void_p()
+    rt = gpb.current_runtime()
+    _lib.check(lib.gpb_model_create_device(rt.handle, ctypes.c_void_p(z.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                                           c["n"], c["d"], c["tiles"], ctypes.byref(h)))
+    flags = (ctypes.c_uint8 * 3)(1, 1, 1)
+    ll = ctypes.c_double()
+    tm = (ctypes.c_double * 8)()
+    fac, sol = [], []
+    try:
+        for it in range(3):
+            _lib.check(lib.gpb_model_set_params(h, 1.0, 1.0, 0.1, flags))
+            _lib.check(lib.gpb_log_likelihood(h, ctypes.byref(ll)))
+            lib.gpb_model_timings(h, tm, 8)
+            if it >= 1:
+                fac.append(tm[1])
+                sol.append(tm[2])
+    finally:
+        lib.gpb_model_destroy(h)
+    f, s_ = statistics.median(fac), statistics.median(sol)
+    return {"workload": f"config 3 on 1 GPU: n={c['n']}, D={c['d']}, {c['tiles']} tiles", "factor_ms": f,
+            "solves_ms": s_, "tflops": chol_flops(c["n"]) / (f * 1e-3) / 1e12,
+            "note": "t_1 of the strong-scaling efficiency E(p) = t_1 / (p t_p) (1 warm-up + 2 timed)"}
 
 
 def main():
@@ -572,6 +610,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-strong-base", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
@@ -581,7 +620,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
-    if world > 1 and os.environ.get("GPB_REPLICAS") != "1":
+    if world > 1:
         run_distributed(args, rank, world, local_rank)
         return
     run_ours(args, rank, world, local_rank)

@@ -225,6 +225,105 @@ int gpb_model_factor_buffers(gpb_model* m, double** tiles, double** dinv, double
                              double** beta, double** alpha);
 int gpb_model_mark_factored(gpb_model* m);
 
+/* ---- multi-GPU runtime: one process per GPU, 2D block-cyclic tile grid ------
+ * Replaces the reference's runtime lifecycle (runtime.py:369-403) and its
+ * task DAG (tiled.py:168-324, model.py:169-485) across the GPUs of one box.
+ * SURVEY.md 8(b) lists gpb_init(ndev, devs); here every rank runs its own
+ * process with its own gpb_init(device), and gpb_dist_init joins them: ranks
+ * form a P x Q process grid (rank = p * Q + q), lower tile (i, j) lives on
+ * rank (i mod P) * Q + (j mod Q), and the library creates its NCCL
+ * communicators itself -- the world communicator from a unique id that rank 0
+ * makes with gpb_nccl_unique_id and the caller passes to every rank out of
+ * band, then ncclCommSplit into the process-row and process-column
+ * communicators the panel exchanges run on.  NCCL is loaded at run time
+ * (GPB_NCCL_LIB, else libnccl.so.2); GPB_NCCL if it cannot be.
+ * gpb_dist_init_host runs the same schedule with host-staged collectives
+ * supplied by the caller (tests, or ranks without NCCL): buffers passed to the
+ * callbacks are host memory; group 0 = world, 1 = this rank's process row
+ * (ranks ordered by q), 2 = its process column (ordered by p); root and the
+ * callback's rank numbering are within the group.  A callback returns 0 on
+ * success.  Every gpb_dist_* call below is COLLECTIVE: all ranks make it with
+ * the same arguments, and results are returned on every rank. */
+typedef struct gpb_dist gpb_dist;
+typedef struct gpb_dmodel gpb_dmodel;
+#define GPB_NCCL_ID_BYTES 128
+typedef struct gpb_host_coll {
+  int (*bcast)(void* user, int group, void* buf, int64_t bytes, int root);
+  int (*reduce_sum)(void* user, int group, double* buf, int64_t count, int root);  /* in place, at root */
+  int (*allreduce_sum)(void* user, int group, double* buf, int64_t count);        /* in place */
+  void* user;
+} gpb_host_coll;
+int gpb_nccl_unique_id(void* id_out);  /* GPB_NCCL_ID_BYTES bytes */
+int gpb_dist_init(gpb_ctx* ctx, int rank, int world, int P, int Q, const void* nccl_id, gpb_dist** out);
+int gpb_dist_init_host(gpb_ctx* ctx, int rank, int world, int P, int Q, const gpb_host_coll* coll,
+                       gpb_dist** out);
+int gpb_dist_finalize(gpb_dist* dc);
+/* GPModel(train, params, tiles_per_dim) sharded: every rank passes the whole
+ * (replicated) z, y and keeps only its tiles of K / L */
+int gpb_dist_model_create(gpb_dist* dc, const double* z, const double* y, int64_t n, int64_t d,
+                          int64_t tiles_per_dim, gpb_dmodel** out);
+int gpb_dist_model_destroy(gpb_dmodel* m);
+int gpb_dist_set_params(gpb_dmodel* m, double lengthscale, double vertical_scale, double noise_variance,
+                        const uint8_t trainable[3]);
+int gpb_dist_get_params(gpb_dmodel* m, double out[3]);
+/* assemble + block-cyclic tiled Cholesky + beta / alpha solves (cached);
+ * GPB_NOT_PD as gpb_cholesky, the pivot is the smallest failing index over ranks */
+int gpb_dist_factor(gpb_dmodel* m);
+int gpb_dist_last_pivot(gpb_dmodel* m, int64_t* pivot);
+int gpb_dist_log_likelihood(gpb_dmodel* m, double* out);
+/* replica-free: distributed TRTRI + LAUUM on the block-cyclic tiles, trace
+ * pass on each rank's K^-1 tiles, all-reduce of three partial sums */
+int gpb_dist_loss_gradients(gpb_dmodel* m, double out[3]);
+int gpb_dist_optimize(gpb_dmodel* m, double learning_rate, double beta1, double beta2, double epsilon,
+                      int64_t iterations, double* history);
+/* test points sharded over ranks (each rank gathers the factor once into a
+ * local replica); mean / var / cov (m x m) as gpb_predict, on every rank */
+int gpb_dist_predict(gpb_dmodel* m, const double* zt, int64_t mt, int64_t d, double* mean, double* var,
+                     double* cov);
+/* dense n x n lower factor on every rank (through the replica) */
+int gpb_dist_cholesky(gpb_dmodel* m, double* L_out);
+/* device ms of the last calls: [0] assembly, [1] factorisation, [2] solves,
+ * [3] prediction, [4] gradient, [5] replica gather; [6] host enqueue us per
+ * panel step of the last factorisation; [7] collectives issued by this rank */
+int gpb_dist_timings(gpb_dmodel* m, double* ms_out, int n);
+int gpb_dist_launch_count(gpb_dmodel* m, int64_t* out);
+
+/* The schedule IR.  gpb_dist_plan emits, for one rank, the ordered operation
+ * list of a phase (0 factorisation, 1 beta / alpha solves, 2 gradient): what
+ * the device executor runs (kernels on two streams, collectives on the row /
+ * column / world communicators) and what the CPU interpreter of the tests
+ * replays on numpy tiles.  Host-only (no GPU needed).  Buffers are numbered
+ * GPB_BUF_*; offsets and counts are in doubles.  With ops == NULL only the
+ * counts are returned. meta (16): bi, Ti, n_p, P, Q, G, owned tiles, events,
+ * vector offsets {Y, BETA, ALPHA, LOGDIAG, ACC, TMP, RECV, RED}. */
+enum {
+  GPB_BUF_L = 0, GPB_BUF_DINV, GPB_BUF_ROW, GPB_BUF_COL, GPB_BUF_VEC, GPB_BUF_X, GPB_BUF_KINV,
+  GPB_BUF_XCOL, GPB_BUF_XROW, GPB_BUF_LCOL, GPB_NBUF
+};
+enum {
+  GPB_OP_ASSEMBLE = 1, GPB_OP_POTRF, GPB_OP_GEMM, GPB_OP_COPY, GPB_OP_GEMV, GPB_OP_COMBINE, GPB_OP_BCAST,
+  GPB_OP_REDUCE, GPB_OP_ALLREDUCE, GPB_OP_RECORD, GPB_OP_WAIT, GPB_OP_ZERO, GPB_OP_SOLVE_FLOW, GPB_OP_TRACE
+};
+typedef struct gpb_op {
+  int32_t kind, stream, group, root;  /* stream 0 main, 1 critical; group 0 world, 1 row, 2 column */
+  int32_t buf[3], flag;               /* flag: ASSEMBLE add_noise, GEMV trans */
+  int64_t off[3];
+  int64_t count, job0, njobs;         /* count: doubles (collectives, COPY per job, ZERO, COMBINE) */
+  int32_t mblk, nblk, ak, bk;         /* GEMM: blocks of 128 per job, K-major operands */
+  int64_t lda, ldb, ldc;
+  int64_t a_ktile, a_kstride, b_ktile, b_kstride; /* tiled-k walks (0: none) */
+  double alpha, beta;                 /* GEMM cout = alpha a b^T + beta cin; GEMV beta 1 = accumulate */
+  int32_t i, j;                       /* POTRF tile k; RECORD / WAIT event */
+} gpb_op;
+typedef struct gpb_op_job {
+  int32_t buf[4];                     /* A, B, Cin, Cout (-1: none) */
+  int64_t off[4];
+  int32_t k, lower, i, j;             /* GEMM depth and diagonal-tile flag; tile coordinates */
+} gpb_op_job;
+int gpb_dist_plan(int rank, int world, int P, int Q, int64_t n, int64_t tiles_per_dim, int phase,
+                  gpb_op* ops, int64_t* nops, gpb_op_job* jobs, int64_t* njobs, int64_t bufsz[GPB_NBUF],
+                  int64_t meta[16]);
+
 /* ---- tile-kernel plugin (tiles.py:23-46, 132-164) -------------------------
  * Host buffers, fresh outputs, inputs never mutated.  Square tiles b x b;
  * trsm solves X l^T = b_in for rows x b b_in. */

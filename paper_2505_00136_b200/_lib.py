@@ -14,6 +14,8 @@ import ctypes
 import os
 import threading
 
+import numpy as np
+
 from . import errors
 
 LIB_NAME = "libgpb200.so"
@@ -101,6 +103,32 @@ SIGNATURES = {
     "gpb_model_adopt_factor": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "gpb_model_factor_buffers": (ctypes.c_int, [_vp] + [ctypes.POINTER(_vp)] * 5),
     "gpb_model_mark_factored": (ctypes.c_int, [_vp]),
+    "gpb_nccl_unique_id": (ctypes.c_int, [_vp]),
+    "gpb_dist_init": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
+                                     ctypes.POINTER(_vp)]),
+    "gpb_dist_init_host": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
+                                          ctypes.POINTER(_vp)]),
+    "gpb_dist_finalize": (ctypes.c_int, [_vp]),
+    "gpb_dist_model_create": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, ctypes.c_int64, ctypes.c_int64,
+                                             ctypes.c_int64, ctypes.POINTER(_vp)]),
+    "gpb_dist_model_destroy": (ctypes.c_int, [_vp]),
+    "gpb_dist_set_params": (ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                           ctypes.POINTER(ctypes.c_uint8)]),
+    "gpb_dist_get_params": (ctypes.c_int, [_vp, _c_double_p]),
+    "gpb_dist_factor": (ctypes.c_int, [_vp]),
+    "gpb_dist_last_pivot": (ctypes.c_int, [_vp, _c_i64_p]),
+    "gpb_dist_log_likelihood": (ctypes.c_int, [_vp, _c_double_p]),
+    "gpb_dist_loss_gradients": (ctypes.c_int, [_vp, _c_double_p]),
+    "gpb_dist_optimize": (ctypes.c_int, [_vp, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_double, ctypes.c_int64, _c_double_p]),
+    "gpb_dist_predict": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_int64, ctypes.c_int64, _c_double_p,
+                                        _c_double_p, _c_double_p]),
+    "gpb_dist_cholesky": (ctypes.c_int, [_vp, _c_double_p]),
+    "gpb_dist_timings": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_int]),
+    "gpb_dist_launch_count": (ctypes.c_int, [_vp, _c_i64_p]),
+    "gpb_dist_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+                                     ctypes.c_int64, ctypes.c_int, _vp, _c_i64_p, _vp, _c_i64_p, _c_i64_p,
+                                     _c_i64_p]),
     "gpb_tile_potrf": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_int64, _c_double_p]),
     "gpb_tile_trsm": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, ctypes.c_int64,
                                      ctypes.c_int64, _c_double_p]),
@@ -145,6 +173,51 @@ class GemvJob(ctypes.Structure):
 class CopyJob(ctypes.Structure):
     """gpb_copy_job"""
     _fields_ = [("src", ctypes.c_void_p), ("dst", ctypes.c_void_p)]
+
+
+# gpb_host_coll callbacks (host-staged collectives of gpb_dist_init_host)
+BCAST_FN = ctypes.CFUNCTYPE(ctypes.c_int, _vp, ctypes.c_int, _vp, ctypes.c_int64, ctypes.c_int)
+REDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, _vp, ctypes.c_int, _c_double_p, ctypes.c_int64, ctypes.c_int)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, _vp, ctypes.c_int, _c_double_p, ctypes.c_int64)
+
+
+class HostColl(ctypes.Structure):
+    """gpb_host_coll"""
+    _fields_ = [("bcast", BCAST_FN), ("reduce_sum", REDUCE_FN), ("allreduce_sum", ALLREDUCE_FN),
+                ("user", _vp)]
+
+
+NCCL_ID_BYTES = 128  # GPB_NCCL_ID_BYTES
+BUFFERS = ("L", "DINV", "ROW", "COL", "VEC", "X", "KINV", "XCOL", "XROW", "LCOL")  # GPB_BUF_*
+OPS = {1: "ASSEMBLE", 2: "POTRF", 3: "GEMM", 4: "COPY", 5: "GEMV", 6: "COMBINE", 7: "BCAST", 8: "REDUCE",
+       9: "ALLREDUCE", 10: "RECORD", 11: "WAIT", 12: "ZERO", 13: "SOLVE_FLOW", 14: "TRACE"}  # GPB_OP_*
+# gpb_op / gpb_op_job as numpy records (the schedule IR of gpb_dist_plan)
+OP_DTYPE = np.dtype([("kind", "<i4"), ("stream", "<i4"), ("group", "<i4"), ("root", "<i4"),
+                     ("buf", "<i4", 3), ("flag", "<i4"), ("off", "<i8", 3), ("count", "<i8"),
+                     ("job0", "<i8"), ("njobs", "<i8"), ("mblk", "<i4"), ("nblk", "<i4"), ("ak", "<i4"),
+                     ("bk", "<i4"), ("lda", "<i8"), ("ldb", "<i8"), ("ldc", "<i8"), ("a_ktile", "<i8"),
+                     ("a_kstride", "<i8"), ("b_ktile", "<i8"), ("b_kstride", "<i8"), ("alpha", "<f8"),
+                     ("beta", "<f8"), ("i", "<i4"), ("j", "<i4")])
+JOB_DTYPE = np.dtype([("buf", "<i4", 4), ("off", "<i8", 4), ("k", "<i4"), ("lower", "<i4"), ("i", "<i4"),
+                      ("j", "<i4")])
+META = ("bi", "Ti", "np", "P", "Q", "G", "nown", "nevents", "Y", "BETA", "ALPHA", "LOGDIAG", "ACC", "TMP",
+        "RECV", "RED")
+
+
+def dist_plan(rank: int, world: int, p: int, q: int, n: int, tiles_per_dim: int, phase: int):
+    """One rank's operation list of a phase (gpb_dist_plan; host only, no GPU):
+    (ops, jobs, buffer sizes in doubles, meta dict)."""
+    lib = load()
+    nops, njobs = ctypes.c_int64(), ctypes.c_int64()
+    bufsz = (ctypes.c_int64 * len(BUFFERS))()
+    meta = (ctypes.c_int64 * 16)()
+    check(lib.gpb_dist_plan(rank, world, p, q, n, tiles_per_dim, phase, None, ctypes.byref(nops), None,
+                            ctypes.byref(njobs), bufsz, meta))
+    ops = np.zeros(nops.value, dtype=OP_DTYPE)
+    jobs = np.zeros(max(1, njobs.value), dtype=JOB_DTYPE)
+    check(lib.gpb_dist_plan(rank, world, p, q, n, tiles_per_dim, phase, ops.ctypes.data, ctypes.byref(nops),
+                            jobs.ctypes.data, ctypes.byref(njobs), bufsz, meta))
+    return ops, jobs[:njobs.value], dict(zip(BUFFERS, bufsz[:])), dict(zip(META, meta[:]))
 
 
 def layout(n: int, tiles_per_dim: int) -> dict:

@@ -1,0 +1,603 @@
+// Multi-GPU schedule of the tiled GP: the per-rank operation lists (gpb200.h
+// schedule IR) of the 2D block-cyclic tiled Cholesky, the beta / alpha solves
+// and the replica-free gradient.  Host code only; the device executor is
+// dist.cu, the CPU interpreter tests/dist_interp.py.
+//
+// Process grid P x Q, rank = p Q + q; lower tile (i, j) on rank
+// (i mod P) Q + (j mod Q).  Per panel k of the right-looking
+// tiled Cholesky (taskgp tiled.py:168-204):
+//   POTRF(k) on the owner of (k, k); L_kk^-1 down process column k mod Q;
+//   TRSM: column k mod Q solves its tiles (i, k) into the row-panel buffer;
+//   row stage: each process row p broadcasts its share of the panel from
+//     rank (p, k mod Q) along the row (row communicator, one call);
+//   column stage: rank (p', q) packs the panel tiles j = p' (mod P),
+//     j = q (mod Q) into the column-panel buffer and broadcasts them down
+//     process column q (column communicator, P calls);
+//   the trailing updates read A from the row panel and B from the column panel.
+// Panels are grouped exactly as on one GPU (plan_common.h): in-group updates
+// (K = b) and the next group's columns (K = G' b) on the high-priority critical
+// stream, the rest of the trailing update (K = G' b) on the main stream.  Every
+// tile receives the same sequence of GEMMs with the same K split as in the
+// single-GPU plan, so the factor is bitwise the single-GPU one.
+#include <algorithm>
+#include <string>
+
+#include "dist_plan.h"
+#include "plan_common.h"
+
+namespace gpb {
+
+namespace {
+
+constexpr int kBlk = 128;  // GEMM block (gemm.cuh GBM = GBN)
+enum { MAIN = 0, CRIT = 1 };
+enum { WORLD = 0, ROWG = 1, COLG = 2 };
+
+struct Ref {
+  int buf;
+  int64_t off;
+};
+
+class Builder {
+ public:
+  std::vector<gpb_op>* ops;
+  std::vector<gpb_op_job>* jobs;
+
+  gpb_op base(int kind, int stream) {
+    gpb_op o{};
+    o.kind = kind;
+    o.stream = stream;
+    o.buf[0] = o.buf[1] = o.buf[2] = -1;
+    return o;
+  }
+  void push(const gpb_op& o) { ops->push_back(o); }
+  void zero(int stream, Ref a, int64_t count) {
+    if (count <= 0) return;
+    gpb_op o = base(GPB_OP_ZERO, stream);
+    o.buf[0] = a.buf;
+    o.off[0] = a.off;
+    o.count = count;
+    push(o);
+  }
+  void record(int stream, int ev) {
+    gpb_op o = base(GPB_OP_RECORD, stream);
+    o.i = ev;
+    push(o);
+  }
+  void wait(int stream, int ev) {
+    gpb_op o = base(GPB_OP_WAIT, stream);
+    o.i = ev;
+    push(o);
+  }
+  void coll(int kind, int stream, int group, int root, Ref a, int64_t count) {
+    if (count <= 0) return;
+    gpb_op o = base(kind, stream);
+    o.group = group;
+    o.root = root;
+    o.buf[0] = a.buf;
+    o.off[0] = a.off;
+    o.count = count;
+    push(o);
+  }
+  // job list helpers: start a list, add jobs, close it into an op
+  size_t j0 = 0;
+  void begin() { j0 = jobs->size(); }
+  void job(Ref a, Ref b, Ref cin, Ref cout, int k = 0, int lower = 0, int i = 0, int j = 0) {
+    gpb_op_job q{};
+    const Ref r[4] = {a, b, cin, cout};
+    for (int t = 0; t < 4; ++t) {
+      q.buf[t] = r[t].buf;
+      q.off[t] = r[t].off;
+    }
+    q.k = k;
+    q.lower = lower;
+    q.i = i;
+    q.j = j;
+    jobs->push_back(q);
+  }
+  int64_t pending() const { return static_cast<int64_t>(jobs->size() - j0); }
+  // close the open job list into `o` (dropped when empty)
+  void close(gpb_op o) {
+    o.job0 = static_cast<int64_t>(j0);
+    o.njobs = pending();
+    if (o.njobs > 0) push(o);
+  }
+  gpb_op gemm(int stream, int mblk, int nblk, int64_t ld, bool ak, bool bk, double alpha, double beta) {
+    gpb_op o = base(GPB_OP_GEMM, stream);
+    o.mblk = mblk;
+    o.nblk = nblk;
+    o.lda = o.ldb = o.ldc = ld;
+    o.ak = ak;
+    o.bk = bk;
+    o.alpha = alpha;
+    o.beta = beta;
+    return o;
+  }
+};
+
+const Ref kNone{-1, 0};
+
+}  // namespace
+
+int dist_layout(int rank, int world, int P, int Q, int64_t n, int64_t T, DistLayout* out, std::string* err) {
+  DistLayout& L = *out;
+  if (world < 1 || P < 1 || Q < 1 || P * Q != world || rank < 0 || rank >= world) {
+    if (err) *err = "process grid " + std::to_string(P) + " x " + std::to_string(Q) + " does not match " +
+                    std::to_string(world) + " ranks (rank " + std::to_string(rank) + ")";
+    return GPB_INVALID_CONFIG;
+  }
+  int64_t lay[6];
+  if (int s = gpb_layout(n, T, lay)) {
+    if (err) *err = "tiles_per_dim=" + std::to_string(T) + " must divide the " + std::to_string(n) +
+                    " training points";
+    return s;
+  }
+  L = DistLayout();
+  L.rank = rank;
+  L.world = world;
+  L.P = P;
+  L.Q = Q;
+  L.my_p = rank / Q;
+  L.my_q = rank % Q;
+  L.n = n;
+  L.bi = static_cast<int>(lay[0]);
+  L.Ti = static_cast<int>(lay[1]);
+  L.np_ = lay[2];
+  L.bp_user = static_cast<int>(lay[3]);
+  L.b_user = static_cast<int>(lay[4]);
+  L.bi2 = int64_t(L.bi) * L.bi;
+  L.G = chol_panels(L.Ti);
+  const int Ti = L.Ti;
+  L.slot.assign(size_t(Ti) * Ti, -1);
+  for (int i = 0; i < Ti; ++i)
+    for (int j = 0; j <= i; ++j)
+      if (L.owner(i, j) == rank) {
+        L.slot[size_t(i) * Ti + j] = L.nown();
+        L.own_i.push_back(i);
+        L.own_j.push_back(j);
+      }
+  L.rows_per = (Ti + P - 1) / P;
+  std::vector<int> cnt(P, 0);
+  L.jpos.assign(Ti, -1);
+  for (int j = 0; j < Ti; ++j)
+    if (j % Q == L.my_q) L.jpos[j] = cnt[j % P]++;
+  L.cnt_max = *std::max_element(cnt.begin(), cnt.end());
+  std::vector<int> cr(Q, 0);
+  L.rpos.assign(Ti, -1);
+  for (int r = 0; r < Ti; ++r)
+    if (r % P == L.my_p) L.rpos[r] = cr[r % Q]++;
+  L.cntx = *std::max_element(cr.begin(), cr.end());
+  const int64_t bi2 = L.bi2, nown = std::max(1, L.nown());
+  L.bufsz[GPB_BUF_L] = nown * bi2;
+  L.bufsz[GPB_BUF_DINV] = int64_t(Ti) * bi2;
+  L.bufsz[GPB_BUF_ROW] = 2 * int64_t(L.G) * L.rows_per * bi2;
+  L.bufsz[GPB_BUF_COL] = P > 1 ? 2 * int64_t(P) * L.G * std::max(1, L.cnt_max) * bi2 : 0;
+  const int64_t np_ = L.np_;
+  L.vec[V_Y] = 0;
+  L.vec[V_BETA] = np_;
+  L.vec[V_ALPHA] = 2 * np_;
+  L.vec[V_LOGDIAG] = 3 * np_;
+  L.vec[V_ACC] = 3 * np_ + Ti;
+  L.vec[V_TMP] = 4 * np_ + Ti;
+  L.vec[V_RECV] = 4 * np_ + Ti + L.bi;
+  L.vec[V_RED] = 4 * np_ + Ti + 2 * L.bi;
+  L.bufsz[GPB_BUF_VEC] = L.vec[V_RED] + 8;
+  L.bufsz[GPB_BUF_X] = nown * bi2;
+  L.bufsz[GPB_BUF_KINV] = nown * bi2;
+  L.bufsz[GPB_BUF_XCOL] = P > 1 ? int64_t((Ti + Q - 1) / Q) * bi2 : 0;
+  L.bufsz[GPB_BUF_XROW] = Q > 1 ? int64_t(Q) * std::max(1, L.cntx) * bi2 : 0;
+  L.bufsz[GPB_BUF_LCOL] = Q > 1 ? int64_t(L.rows_per) * bi2 : 0;
+  const int ng = static_cast<int>(chol_group_sizes(Ti, L.G).size());
+  L.nevents = 2 * ng + 2;
+  return GPB_OK;
+}
+
+namespace {
+
+// ---- phase 0: assembly + factorisation ------------------------------------
+void plan_factor(const DistLayout& L, Builder& b) {
+  const int Ti = L.Ti, bi = L.bi, nb = bi / kBlk, P = L.P, Q = L.Q, G = L.G;
+  const int64_t bi2 = L.bi2;
+  auto slot = [&](int i, int j) { return L.slot[size_t(i) * Ti + j]; };
+  auto lt = [&](int i, int j) { return Ref{GPB_BUF_L, int64_t(slot(i, j)) * bi2}; };
+  auto rowt = [&](int set, int g, int i) {
+    return Ref{GPB_BUF_ROW, ((int64_t(set) * G + g) * L.rows_per + i / P) * bi2};
+  };
+  // column-panel tile j (j mod Q == my_q); with P == 1 the row panel holds every row
+  auto colt = [&](int set, int g, int j) {
+    if (P == 1) return rowt(set, g, j);
+    return Ref{GPB_BUF_COL, (((int64_t(set) * P + j % P) * G + g) * L.cnt_max + L.jpos[j]) * bi2};
+  };
+  const int64_t a_walk = int64_t(L.rows_per) * bi2;
+  const int64_t b_walk = P == 1 ? a_walk : int64_t(L.cnt_max) * bi2;
+  const std::vector<int> sizes = chol_group_sizes(Ti, G);
+  const int ng = static_cast<int>(sizes.size());
+  const int ev_start = 0, ev_end = 1 + 2 * ng;
+  auto ev_panel = [&](int s) { return 1 + s; };
+  auto ev_upd = [&](int s) { return 1 + ng + s; };
+
+  b.zero(MAIN, {GPB_BUF_VEC, L.vec[V_LOGDIAG]}, Ti);
+  b.begin();
+  for (int s = 0; s < L.nown(); ++s)
+    b.job(kNone, kNone, kNone, {GPB_BUF_L, s * bi2}, 0, 0, L.own_i[s], L.own_j[s]);
+  {
+    gpb_op o = b.base(GPB_OP_ASSEMBLE, MAIN);
+    o.flag = 1;  // noise on the global diagonal
+    b.close(o);
+  }
+  b.record(MAIN, ev_start);
+  b.wait(CRIT, ev_start);
+
+
+  for (int s = 0, k0 = 0; s < ng; k0 += sizes[s], ++s) {
+    const int gs = sizes[s], k1 = k0 + gs - 1, set = s % 2;
+    if (s >= 2) b.wait(CRIT, ev_upd(s - 2));
+    for (int g = 0; g < gs; ++g) {
+      const int k = k0 + g;
+      if (L.my_q == k % Q) {
+        if (L.rank == L.owner(k, k)) {
+          gpb_op o = b.base(GPB_OP_POTRF, CRIT);
+          o.buf[0] = GPB_BUF_L;
+          o.off[0] = lt(k, k).off;
+          o.buf[1] = GPB_BUF_DINV;
+          o.off[1] = int64_t(k) * bi2;
+          o.i = k;
+          b.push(o);
+        }
+        if (P > 1) b.coll(GPB_OP_BCAST, CRIT, COLG, k % P, {GPB_BUF_DINV, int64_t(k) * bi2}, bi2);
+        // TRSM X_i = L(i, k) L_kk^-T: Dinv_k is lower triangular, so output
+        // column block c needs k < (c + 1) 128 (one job per column block)
+        b.begin();
+        for (int i = k + 1; i < Ti; ++i) {
+          if (slot(i, k) < 0) continue;
+          for (int c = 0; c < nb; ++c)
+            b.job(lt(i, k), {GPB_BUF_DINV, int64_t(k) * bi2 + int64_t(c) * kBlk * bi}, kNone,
+                  {GPB_BUF_ROW, rowt(set, g, i).off + c * kBlk}, (c + 1) * kBlk, 0, i, k);
+        }
+        b.close(b.gemm(CRIT, nb, 1, bi, true, true, 1.0, 0.0));
+      }
+      if (k + 1 == Ti) break;
+      // row stage: this process row's panel tiles from rank (my_p, k mod Q)
+      if (Q > 1) {
+        int first = k + 1;
+        while (first < Ti && first % P != L.my_p) ++first;
+        const int64_t cnt = first < Ti ? (Ti - 1 - first) / P + 1 : 0;
+        if (cnt > 0) b.coll(GPB_OP_BCAST, CRIT, ROWG, k % Q, rowt(set, g, first), cnt * bi2);
+      }
+      // column stage: panel tiles j = p' (mod P), j = my_q (mod Q) from rank (p', my_q)
+      if (P > 1) {
+        for (int pp = 0; pp < P; ++pp) {
+          std::vector<int> js;
+          for (int j = k + 1; j < Ti; ++j)
+            if (j % P == pp && j % Q == L.my_q) js.push_back(j);
+          if (js.empty()) continue;
+          if (L.my_p == pp) {
+            b.begin();
+            for (int j : js) b.job(rowt(set, g, j), kNone, kNone, colt(set, g, j));
+            gpb_op o = b.base(GPB_OP_COPY, CRIT);
+            o.count = bi2;
+            b.close(o);
+          }
+          b.coll(GPB_OP_BCAST, CRIT, COLG, pp, colt(set, g, js.front()), int64_t(js.size()) * bi2);
+        }
+      }
+      // in-group update: the group's later columns get panel k (K = b)
+      b.begin();
+      for (int s2 = 0; s2 < L.nown(); ++s2) {
+        const int i = L.own_i[s2], j = L.own_j[s2];
+        if (j <= k || j > k1) continue;
+        b.job(rowt(set, g, i), colt(set, g, j), lt(i, j), lt(i, j), bi, i == j, i, j);
+      }
+      b.close(b.gemm(CRIT, nb, nb, bi, true, true, -1.0, 1.0));
+    }
+    b.record(CRIT, ev_panel(s));
+    const int c_next = k0 + gs;
+    const int c_upd = std::min(Ti, c_next + (s + 1 < ng ? sizes[s + 1] : 0));
+    auto update = [&](int stream, int jlo, int jhi) {
+      b.begin();
+      for (int s2 = 0; s2 < L.nown(); ++s2) {
+        const int i = L.own_i[s2], j = L.own_j[s2];
+        if (j < jlo || j >= jhi) continue;
+        b.job(rowt(set, 0, i), colt(set, 0, j), lt(i, j), lt(i, j), gs * bi, i == j, i, j);
+      }
+      gpb_op o = b.gemm(stream, nb, nb, bi, true, true, -1.0, 1.0);
+      // tiled-k walk: k tile g of row i is panel g's tile i, which keeps its
+      // slot in every panel (rowt(set, g, i) = rowt(set, 0, i) + g rows_per b^2)
+      o.a_ktile = o.b_ktile = bi;
+      o.a_kstride = a_walk;
+      o.b_kstride = b_walk;
+      b.close(o);
+    };
+    if (c_next < Ti) {
+      // lookahead: the next group's columns need UPD(s - 1), which covered them
+      if (s >= 1) b.wait(CRIT, ev_upd(s - 1));
+      update(CRIT, c_next, c_upd);
+    }
+    // main stream: copy the solved panel tiles back into L, then the rest of the update
+    b.wait(MAIN, ev_panel(s));
+    b.begin();
+    for (int g = 0; g < gs; ++g) {
+      const int k = k0 + g;
+      if (L.my_q != k % Q) continue;
+      for (int i = k + 1; i < Ti; ++i)
+        if (slot(i, k) >= 0) b.job(rowt(set, g, i), kNone, kNone, lt(i, k));
+    }
+    {
+      gpb_op o = b.base(GPB_OP_COPY, MAIN);
+      o.count = bi2;
+      b.close(o);
+    }
+    update(MAIN, c_upd, Ti);
+    b.record(MAIN, ev_upd(s));
+  }
+  b.record(CRIT, ev_end);
+  b.wait(MAIN, ev_end);
+  // every rank gets every L_kk^-1 (solves on the diagonal owners, gradient rows)
+  if (L.world > 1)
+    for (int k = 0; k < Ti; ++k)
+      b.coll(GPB_OP_BCAST, MAIN, WORLD, L.owner(k, k), {GPB_BUF_DINV, int64_t(k) * bi2}, bi2);
+}
+
+// ---- phase 1: beta = L^-1 y, alpha = L^-T beta (tiled.py:215-260) ----------
+void plan_solve(const DistLayout& L, Builder& b) {
+  const int Ti = L.Ti, bi = L.bi, P = L.P, Q = L.Q;
+  const int64_t bi2 = L.bi2;
+  if (L.world == 1) {  // one rank holds the packed factor: the one-launch dataflow solve
+    b.push(b.base(GPB_OP_SOLVE_FLOW, MAIN));
+    return;
+  }
+  auto slot = [&](int i, int j) { return L.slot[size_t(i) * Ti + j]; };
+  auto v = [&](int which, int64_t at = 0) { return Ref{GPB_BUF_VEC, L.vec[which] + at}; };
+  const Ref tmp = v(V_TMP), recv = v(V_RECV);
+  auto combine = [&](Ref base, Ref part) {  // TMP = base - part
+    gpb_op o = b.base(GPB_OP_COMBINE, MAIN);
+    o.buf[0] = base.buf;
+    o.off[0] = base.off;
+    o.buf[1] = part.buf;
+    o.off[1] = part.off;
+    o.buf[2] = tmp.buf;
+    o.off[2] = tmp.off;
+    o.count = bi;
+    b.push(o);
+  };
+  auto gemv = [&](bool trans, bool acc) {
+    gpb_op o = b.base(GPB_OP_GEMV, MAIN);
+    o.flag = trans;
+    o.alpha = 1.0;
+    o.beta = acc ? 1.0 : 0.0;
+    return o;
+  };
+  auto copy_vec = [&](Ref src, Ref dst) {
+    b.begin();
+    b.job(src, kNone, kNone, dst);
+    gpb_op o = b.base(GPB_OP_COPY, MAIN);
+    o.count = bi;
+    b.close(o);
+  };
+  b.zero(MAIN, v(V_BETA), 2 * L.np_);
+  b.zero(MAIN, v(V_ACC), L.np_);
+  // forward, right-looking: partial sums of row i reduced onto the diagonal
+  // owner along process row i mod P; beta_i down process column i mod Q
+  for (int i = 0; i < Ti; ++i) {
+    const int64_t seg = int64_t(i) * bi;
+    if (Q > 1 && L.my_p == i % P) b.coll(GPB_OP_REDUCE, MAIN, ROWG, i % Q, v(V_ACC, seg), bi);
+    if (L.rank == L.owner(i, i)) {
+      combine(v(V_Y, seg), v(V_ACC, seg));
+      b.begin();
+      b.job({GPB_BUF_DINV, int64_t(i) * bi2}, tmp, kNone, v(V_BETA, seg));
+      b.close(gemv(false, false));
+      copy_vec(v(V_BETA, seg), recv);
+    }
+    if (L.my_q == i % Q) {
+      if (P > 1) b.coll(GPB_OP_BCAST, MAIN, COLG, i % P, recv, bi);
+      b.begin();
+      for (int r = i + 1; r < Ti; ++r)
+        if (slot(r, i) >= 0) b.job({GPB_BUF_L, int64_t(slot(r, i)) * bi2}, recv, kNone, v(V_ACC, int64_t(r) * bi));
+      b.close(gemv(false, true));
+    }
+  }
+  b.zero(MAIN, v(V_ACC), L.np_);
+  // backward: partial sums of column i reduced along process column i mod Q;
+  // alpha_i along process row i mod P
+  for (int i = Ti - 1; i >= 0; --i) {
+    const int64_t seg = int64_t(i) * bi;
+    if (P > 1 && L.my_q == i % Q) b.coll(GPB_OP_REDUCE, MAIN, COLG, i % P, v(V_ACC, seg), bi);
+    if (L.rank == L.owner(i, i)) {
+      combine(v(V_BETA, seg), v(V_ACC, seg));
+      b.begin();
+      b.job({GPB_BUF_DINV, int64_t(i) * bi2}, tmp, kNone, v(V_ALPHA, seg));
+      b.close(gemv(true, false));
+      copy_vec(v(V_ALPHA, seg), recv);
+    }
+    if (L.my_p == i % P) {
+      if (Q > 1) b.coll(GPB_OP_BCAST, MAIN, ROWG, i % Q, recv, bi);
+      b.begin();
+      for (int j = 0; j < i; ++j)
+        if (slot(i, j) >= 0) b.job({GPB_BUF_L, int64_t(slot(i, j)) * bi2}, recv, kNone, v(V_ACC, int64_t(j) * bi));
+      b.close(gemv(true, true));
+    }
+  }
+  // beta, alpha and the per-tile log-diagonal sums live on the diagonal
+  // owners (zero elsewhere): one all-reduce replicates them exactly
+  b.coll(GPB_OP_ALLREDUCE, MAIN, WORLD, 0, v(V_BETA), 2 * L.np_ + Ti);
+}
+
+// ---- phase 2: gradient terms (model.py:341-435) ----------------------------
+// X = L^-1 right-looking with the K^-1 buffer as the accumulator
+// A(i, j) = -sum_{m=j}^{i-1} L(i, m) X(m, j), and K^-1 = X^T X in outer-product
+// form, both on the block-cyclic tiles.  Step k:
+//   F_k (process row k mod P): X(k, j) = Dinv_k A(k, j), j < k; X(k, k) = Dinv_k;
+//   row k of X down the process columns (root k mod P) and L(:, k) along the
+//     process rows (root k mod Q);
+//   U_k: A(i, j) -= L(i, k) X(k, j), i > k, j <= k;
+//   row k of X along the process rows (roots: rank (p, r mod Q) for tile r);
+//   LAUUM_k: K^-1(r, c) += X(k, r)^T X(k, c), c <= r <= k (written, not
+//     accumulated, at r == k: that slot's A(k, c) was consumed by F_k).
+// Then the fused trace pass over each rank's K^-1 tiles and an all-reduce of
+// the three partial sums.  No rank ever holds more than its own tiles plus one
+// tile row / column of X and L.
+void plan_gradient(const DistLayout& L, Builder& b) {
+  const int Ti = L.Ti, bi = L.bi, nb = bi / kBlk, P = L.P, Q = L.Q;
+  const int64_t bi2 = L.bi2;
+  auto slot = [&](int i, int j) { return L.slot[size_t(i) * Ti + j]; };
+  auto xt = [&](int i, int j) { return Ref{GPB_BUF_X, int64_t(slot(i, j)) * bi2}; };
+  auto kt = [&](int i, int j) { return Ref{GPB_BUF_KINV, int64_t(slot(i, j)) * bi2}; };
+  auto add = [](Ref r, int64_t o) { return Ref{r.buf, r.off + o}; };
+  b.zero(MAIN, {GPB_BUF_KINV, 0}, int64_t(L.nown()) * bi2);
+  for (int k = 0; k < Ti; ++k) {
+    // X(k, j) as the B operand on this rank (j mod Q == my_q, j <= k)
+    auto xk = [&](int j) { return P == 1 ? xt(k, j) : Ref{GPB_BUF_XCOL, int64_t(j / Q) * bi2}; };
+    // X(k, r) as the A operand (r mod P == my_p, r <= k)
+    auto xr = [&](int r) {
+      return Q == 1 ? xk(r) : Ref{GPB_BUF_XROW, (int64_t(r % Q) * L.cntx + L.rpos[r]) * bi2};
+    };
+    // L(i, k) as the A operand (i mod P == my_p, i > k)
+    auto lc = [&](int i) {
+      return Q == 1 ? Ref{GPB_BUF_L, int64_t(slot(i, k)) * bi2} : Ref{GPB_BUF_LCOL, int64_t(i / P) * bi2};
+    };
+    if (L.my_p == k % P) {
+      // F_k: Dinv_k is lower triangular, so output row block r needs k < (r + 1) 128
+      b.begin();
+      for (int j = 0; j < k; ++j) {
+        if (slot(k, j) < 0) continue;
+        for (int r = 0; r < nb; ++r)
+          b.job({GPB_BUF_DINV, int64_t(k) * bi2 + int64_t(r) * kBlk * bi}, kt(k, j), kNone,
+                add(xt(k, j), int64_t(r) * kBlk * bi), (r + 1) * kBlk, 0, k, j);
+      }
+      b.close(b.gemm(MAIN, 1, nb, bi, true, false, 1.0, 0.0));
+      if (L.rank == L.owner(k, k)) {
+        b.begin();
+        b.job({GPB_BUF_DINV, int64_t(k) * bi2}, kNone, kNone, xt(k, k));
+        gpb_op o = b.base(GPB_OP_COPY, MAIN);
+        o.count = bi2;
+        b.close(o);
+      }
+    }
+    if (P > 1) {  // row k of X down process column my_q (root: process row k mod P)
+      int cnt = 0;
+      b.begin();
+      for (int j = L.my_q; j <= k; j += Q) {
+        ++cnt;
+        if (L.my_p == k % P) b.job(xt(k, j), kNone, kNone, {GPB_BUF_XCOL, int64_t(j / Q) * bi2});
+      }
+      gpb_op o = b.base(GPB_OP_COPY, MAIN);
+      o.count = bi2;
+      b.close(o);
+      b.coll(GPB_OP_BCAST, MAIN, COLG, k % P, {GPB_BUF_XCOL, 0}, int64_t(cnt) * bi2);
+    }
+    if (Q > 1 && k + 1 < Ti) {  // L(:, k) along process row my_p (root: column k mod Q)
+      int first = k + 1;
+      while (first < Ti && first % P != L.my_p) ++first;
+      const int64_t cnt = first < Ti ? (Ti - 1 - first) / P + 1 : 0;
+      if (cnt > 0) {
+        b.begin();
+        if (L.my_q == k % Q)
+          for (int i = first; i < Ti; i += P) b.job({GPB_BUF_L, int64_t(slot(i, k)) * bi2}, kNone, kNone, lc(i));
+        gpb_op o = b.base(GPB_OP_COPY, MAIN);
+        o.count = bi2;
+        b.close(o);
+        b.coll(GPB_OP_BCAST, MAIN, ROWG, k % Q, lc(first), cnt * bi2);
+      }
+    }
+    // U_k, j < k
+    b.begin();
+    for (int s = 0; s < L.nown(); ++s) {
+      const int i = L.own_i[s], j = L.own_j[s];
+      if (i > k && j < k) b.job(lc(i), xk(j), kt(i, j), kt(i, j), bi, 0, i, j);
+    }
+    b.close(b.gemm(MAIN, nb, nb, bi, true, false, -1.0, 1.0));
+    // U_k, j = k: X(k, k) = Dinv_k is lower triangular, so output column block
+    // cb needs only k >= cb 128 (one job per column block, K = b - cb 128)
+    b.begin();
+    for (int i = k + 1; i < Ti; ++i) {
+      if (slot(i, k) < 0) continue;
+      for (int cb = 0; cb < nb; ++cb) {
+        const int64_t o = int64_t(cb) * kBlk;
+        b.job(add(lc(i), o), add(xk(k), o * bi + o), add(kt(i, k), o), add(kt(i, k), o),
+              bi - static_cast<int>(o), 0, i, k);
+      }
+    }
+    b.close(b.gemm(MAIN, nb, 1, bi, true, false, -1.0, 1.0));
+    if (Q > 1) {  // row k of X along process row my_p: tiles r = q' (mod Q) from rank (my_p, q')
+      for (int qq = 0; qq < Q; ++qq) {
+        int cnt = 0;
+        b.begin();
+        for (int r = 0; r <= k; ++r) {
+          if (r % P != L.my_p || r % Q != qq) continue;
+          ++cnt;
+          if (L.my_q == qq) b.job(xk(r), kNone, kNone, xr(r));
+        }
+        if (cnt == 0) continue;
+        gpb_op o = b.base(GPB_OP_COPY, MAIN);
+        o.count = bi2;
+        b.close(o);
+        b.coll(GPB_OP_BCAST, MAIN, ROWG, qq, {GPB_BUF_XROW, int64_t(qq) * L.cntx * bi2}, int64_t(cnt) * bi2);
+      }
+    }
+    // LAUUM_k: K^-1(r, c) (+)= X(k, r)^T X(k, c), both operands M/N-major
+    for (int fresh = 1; fresh >= 0; --fresh) {
+      b.begin();
+      for (int s = 0; s < L.nown(); ++s) {
+        const int r = L.own_i[s], c = L.own_j[s];
+        if (r > k || (r == k) != (fresh == 1)) continue;
+        b.job(xr(r), xk(c), fresh ? kNone : kt(r, c), kt(r, c), bi, r == c, r, c);
+      }
+      b.close(b.gemm(MAIN, nb, nb, bi, false, false, 1.0, fresh ? 0.0 : 1.0));
+    }
+  }
+  b.begin();
+  for (int s = 0; s < L.nown(); ++s)
+    b.job({GPB_BUF_KINV, int64_t(s) * bi2}, kNone, kNone, kNone, 0, 0, L.own_i[s], L.own_j[s]);
+  {
+    gpb_op o = b.base(GPB_OP_TRACE, MAIN);
+    o.buf[2] = GPB_BUF_VEC;
+    o.off[2] = L.vec[V_RED];
+    b.close(o);
+  }
+  if (L.world > 1) b.coll(GPB_OP_ALLREDUCE, MAIN, WORLD, 0, {GPB_BUF_VEC, L.vec[V_RED]}, 3);
+}
+
+}  // namespace
+
+void dist_plan(const DistLayout& L, int phase, std::vector<gpb_op>* ops, std::vector<gpb_op_job>* jobs) {
+  Builder b;
+  b.ops = ops;
+  b.jobs = jobs;
+  if (phase == 0) plan_factor(L, b);
+  if (phase == 1) plan_solve(L, b);
+  if (phase == 2) plan_gradient(L, b);
+}
+
+}  // namespace gpb
+
+extern "C" int gpb_plugin_fail(int code, const char* msg);
+
+extern "C" int gpb_dist_plan(int rank, int world, int P, int Q, int64_t n, int64_t tiles_per_dim, int phase,
+                             gpb_op* ops, int64_t* nops, gpb_op_job* jobs, int64_t* njobs,
+                             int64_t bufsz[GPB_NBUF], int64_t meta[16]) {
+  if (phase < 0 || phase > 2) return gpb_plugin_fail(GPB_INVALID_CONFIG, "phase must be 0, 1 or 2");
+  gpb::DistLayout L;
+  std::string err;
+  if (int s = gpb::dist_layout(rank, world, P, Q, n, tiles_per_dim, &L, &err))
+    return gpb_plugin_fail(s, err.c_str());
+  std::vector<gpb_op> o;
+  std::vector<gpb_op_job> j;
+  gpb::dist_plan(L, phase, &o, &j);
+  if (ops) {
+    if (!nops || !njobs || *nops < static_cast<int64_t>(o.size()) || *njobs < static_cast<int64_t>(j.size()))
+      return gpb_plugin_fail(GPB_INVALID_CONFIG, "operation buffers too small");
+    std::copy(o.begin(), o.end(), ops);
+    std::copy(j.begin(), j.end(), jobs);
+  }
+  if (nops) *nops = static_cast<int64_t>(o.size());
+  if (njobs) *njobs = static_cast<int64_t>(j.size());
+  if (bufsz)
+    for (int t = 0; t < GPB_NBUF; ++t) bufsz[t] = L.bufsz[t];
+  if (meta) {
+    const int64_t m[16] = {L.bi, L.Ti, L.np_, L.P, L.Q, L.G, L.nown(), L.nevents,
+                           L.vec[gpb::V_Y], L.vec[gpb::V_BETA], L.vec[gpb::V_ALPHA], L.vec[gpb::V_LOGDIAG],
+                           L.vec[gpb::V_ACC], L.vec[gpb::V_TMP], L.vec[gpb::V_RECV], L.vec[gpb::V_RED]};
+    std::copy(m, m + 16, meta);
+  }
+  return GPB_OK;
+}

@@ -18,6 +18,7 @@
 #include "gemm.cuh"
 #include "gpb200.h"
 #include "kernels.cuh"
+#include "plan_common.h"
 
 using namespace gpb;
 
@@ -162,7 +163,6 @@ struct gpb_ctx {
 
 // One group of panels of the factorisation plan (build_chol_plan): job ranges
 // in the model's job array.
-constexpr int kMaxGroup = 8;
 struct CholGroup {
   int k0, np;
   int64_t trsm_off[kMaxGroup], trsm_cnt[kMaxGroup], in_off[kMaxGroup], in_cnt[kMaxGroup];
@@ -248,11 +248,7 @@ int apply_layout(gpb_model* m) {
   m->np_ = lay[2];
   m->pm.bp_user = static_cast<int>(lay[3]);
   m->pm.b_user = static_cast<int>(lay[4]);
-  const char* pg = getenv("GPB_PANELS");
-  // larger groups cut the C passes further (K = G bi): G = 4 gives +0.5% at
-  // config 2 and +1.5% at n = 65536, G = 6 another +0.4% there; small grids
-  // keep G = 2 so the critical path stays short
-  m->G = std::max(1, std::min(kMaxGroup, pg ? atoi(pg) : (m->Ti >= 96 ? 6 : m->Ti >= 48 ? 4 : 2)));
+  m->G = chol_panels(m->Ti);  // plan_common.h
   return GPB_OK;
 }
 
@@ -418,26 +414,7 @@ int build_chol_plan(gpb_model* m) {
   double* D = m->Dinv.as<double>();
   std::vector<GemmJob> jobs;
   m->groups.clear();
-  // group sizes: G, shrinking near the end where the trailing update no
-  // longer hides the group's critical path (GPB_TAIL, default 8: at most
-  // r / 8 panels when r tiles remain; 0 = fixed G): +0.5% at config 2
-  std::vector<int> sizes;
-  {
-    const char* te = getenv("GPB_TAIL");
-    const int tail = te ? atoi(te) : 8;
-    // GPB_FIRST: size of the first group, whose critical path runs before
-    // any trailing update can start (default 1 panel from 32 tiles: config 2
-    // factor 338.8 -> 338.0 ms)
-    const char* fe = getenv("GPB_FIRST");
-    const int first = fe ? atoi(fe) : (Ti >= 32 ? 1 : 0);
-    for (int k0 = 0; k0 < Ti;) {
-      int g = std::min(G, Ti - k0);
-      if (k0 == 0 && first > 0) g = std::min(g, first);
-      if (tail > 0) g = std::max(1, std::min(g, (Ti - k0) / tail));
-      sizes.push_back(g);
-      k0 += g;
-    }
-  }
+  const std::vector<int> sizes = chol_group_sizes(Ti, G);  // plan_common.h
   for (int k0 = 0, s = 0; k0 < Ti; k0 += sizes[s], ++s) {
     CholGroup grp{};
     grp.k0 = k0;

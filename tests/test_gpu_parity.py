@@ -295,7 +295,13 @@ class TestGradientsAndAdam:
         import ctypes
 
         from paper_2505_00136_b200 import _lib
-        from paper_2505_00136_b200.distributed import gradient_columns
+
+        def gradient_columns(tiles, world):  # snake-order split of the tile columns
+            out = [[] for _ in range(world)]
+            for j in range(tiles):
+                r, lap = j % world, (j // world) % 2
+                out[world - 1 - r if lap else r].append(j)
+            return out
 
         rng = np.random.default_rng(n + t)
         z, y = rng.normal(size=(n, 3)), rng.normal(size=n)
@@ -452,11 +458,19 @@ def test_device_gemm_views_and_fallback(runtime, rng):
     ld-wide view of one buffer, and falls back to the cp.async kernel when the
     operands come from unrelated allocations at arbitrary offsets; both must
     give C - A B^T (K-major x K-major, tiled-k walk over two panel tiles)."""
+    import ctypes
+
     import torch
 
-    from paper_2505_00136_b200.distributed import DeviceTileOps
+    from paper_2505_00136_b200 import _lib
 
-    ops = DeviceTileOps(runtime, 0)
+    def gemm(jobs, b, alpha, beta):  # (a, b, cin, cout, k, lower); a / b are (2, b, b) panel stacks
+        arr = (_lib.GemmJob * len(jobs))(*[_lib.GemmJob(a.data_ptr(), bb.data_ptr(), ci.data_ptr(), co.data_ptr(),
+                                                        k, int(lo)) for a, bb, ci, co, k, lo in jobs])
+        stride = jobs[0][0].stride(0)
+        _lib.check(_lib.load().gpb_dev_gemm_tiled(runtime.handle, None, arr, len(jobs), b, b, b, b, 1, 1, b,
+                                                  stride, alpha, beta))
+
     b = 128
     a_h = rng.normal(size=(3, 2, b, b))  # 3 row tiles x 2 panels
     c_h = rng.normal(size=(3, b, b))
@@ -465,7 +479,7 @@ def test_device_gemm_views_and_fallback(runtime, rng):
     # (1) one allocation: panel buffer (2, 3, b, b), walked with a stride of 3 tiles
     pan = torch.from_numpy(np.ascontiguousarray(a_h.transpose(1, 0, 2, 3))).cuda()
     c1 = torch.from_numpy(c_h.copy()).cuda()
-    ops.gemm([(pan[:, i], pan[:, 0], c1[i], c1[i], 2 * b, False) for i in range(3)], b, -1.0, 1.0)
+    gemm([(pan[:, i], pan[:, 0], c1[i], c1[i], 2 * b, False) for i in range(3)], b, -1.0, 1.0)
     # (2) separate allocations, each padded by an odd number of doubles
     pads = [torch.zeros(2 * 3 * b * b + 8 * k + 2, dtype=torch.float64, device="cuda") for k in range(3)]
     tiles = []
@@ -474,7 +488,7 @@ def test_device_gemm_views_and_fallback(runtime, rng):
         view.copy_(torch.from_numpy(a_h[i]))
         tiles.append(view)
     c2 = torch.from_numpy(c_h.copy()).cuda()
-    ops.gemm([(tiles[i], tiles[0], c2[i], c2[i], 2 * b, False) for i in range(3)], b, -1.0, 1.0)
+    gemm([(tiles[i], tiles[0], c2[i], c2[i], 2 * b, False) for i in range(3)], b, -1.0, 1.0)
     torch.cuda.synchronize()
     for got in (c1, c2):
         assert rel(got.cpu().numpy(), want) <= 1e-14
