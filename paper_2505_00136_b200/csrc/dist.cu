@@ -648,7 +648,7 @@ int loss_gradients(gpb_dmodel* m, double out[3]) {
   DCUDA(launch_loss_terms(nullptr, 0, vec + L.vec[V_ALPHA], L.np_, m->red, m->st));
   ++m->launches;
   DCUDA(cudaEventRecord(m->t1, m->st));
-  double hh[3], aa[2];
+  double hh[3], aa[1];
   DCUDA(cudaMemcpyAsync(hh, vec + L.vec[V_RED], sizeof(hh), cudaMemcpyDeviceToHost, m->st));
   DCUDA(cudaMemcpyAsync(aa, m->red, sizeof(aa), cudaMemcpyDeviceToHost, m->st));
   DCUDA(cudaStreamSynchronize(m->st));
@@ -657,7 +657,7 @@ int loss_gradients(gpb_dmodel* m, double out[3]) {
   // dNLL/ds2 = (tr K^-1 - |alpha|^2) / 2
   if (tl) out[0] = 0.5 * (m->nu / (m->l * m->l * m->l)) * hh[0];
   if (tv) out[1] = 0.5 * hh[1];
-  if (tn) out[2] = 0.5 * (hh[2] - aa[1]);
+  if (tn) out[2] = 0.5 * (hh[2] - aa[0]);  // loss_terms without a log-diagonal: out[0] = sum x^2
   return GPB_OK;
 }
 

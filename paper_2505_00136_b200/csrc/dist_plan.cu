@@ -172,16 +172,19 @@ int dist_layout(int rank, int world, int P, int Q, int64_t n, int64_t T, DistLay
   L.bufsz[GPB_BUF_DINV] = int64_t(Ti) * bi2;
   L.bufsz[GPB_BUF_ROW] = 2 * int64_t(L.G) * L.rows_per * bi2;
   L.bufsz[GPB_BUF_COL] = P > 1 ? 2 * int64_t(P) * L.G * std::max(1, L.cnt_max) * bi2 : 0;
+  // vector slots start on 256-byte boundaries (the copy kernels move 16-byte words);
+  // BETA, ALPHA, LOGDIAG stay contiguous for the one replicating all-reduce
   const int64_t np_ = L.np_;
+  auto up = [](int64_t x) { return (x + 31) / 32 * 32; };
   L.vec[V_Y] = 0;
-  L.vec[V_BETA] = np_;
-  L.vec[V_ALPHA] = 2 * np_;
-  L.vec[V_LOGDIAG] = 3 * np_;
-  L.vec[V_ACC] = 3 * np_ + Ti;
-  L.vec[V_TMP] = 4 * np_ + Ti;
-  L.vec[V_RECV] = 4 * np_ + Ti + L.bi;
-  L.vec[V_RED] = 4 * np_ + Ti + 2 * L.bi;
-  L.bufsz[GPB_BUF_VEC] = L.vec[V_RED] + 8;
+  L.vec[V_BETA] = up(np_);
+  L.vec[V_ALPHA] = L.vec[V_BETA] + np_;
+  L.vec[V_LOGDIAG] = L.vec[V_ALPHA] + np_;
+  L.vec[V_ACC] = up(L.vec[V_LOGDIAG] + Ti);
+  L.vec[V_TMP] = up(L.vec[V_ACC] + np_);
+  L.vec[V_RECV] = up(L.vec[V_TMP] + L.bi);
+  L.vec[V_RED] = up(L.vec[V_RECV] + L.bi);
+  L.bufsz[GPB_BUF_VEC] = L.vec[V_RED] + 32;
   L.bufsz[GPB_BUF_X] = nown * bi2;
   L.bufsz[GPB_BUF_KINV] = nown * bi2;
   L.bufsz[GPB_BUF_XCOL] = P > 1 ? int64_t((Ti + Q - 1) / Q) * bi2 : 0;
@@ -419,7 +422,7 @@ void plan_solve(const DistLayout& L, Builder& b) {
   }
   // beta, alpha and the per-tile log-diagonal sums live on the diagonal
   // owners (zero elsewhere): one all-reduce replicates them exactly
-  b.coll(GPB_OP_ALLREDUCE, MAIN, WORLD, 0, v(V_BETA), 2 * L.np_ + Ti);
+  b.coll(GPB_OP_ALLREDUCE, MAIN, WORLD, 0, v(V_BETA), 2 * L.np_ + Ti);  // contiguous slots
 }
 
 // ---- phase 2: gradient terms (model.py:341-435) ----------------------------
