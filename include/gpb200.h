@@ -258,6 +258,13 @@ int gpb_dist_init(gpb_ctx* ctx, int rank, int world, int P, int Q, const void* n
 int gpb_dist_init_host(gpb_ctx* ctx, int rank, int world, int P, int Q, const gpb_host_coll* coll,
                        gpb_dist** out);
 int gpb_dist_finalize(gpb_dist* dc);
+/* Panel exchange of the factorisation for models created afterwards:
+ * 0 (default) collectives (row / column broadcasts); 1 peer memory -- the
+ * panel TRSM's epilogue stores every solved tile straight into the row- and
+ * column-panel buffers of the ranks that read it (CUDA IPC mappings, NVLink
+ * stores), readiness and buffer reuse ordered by stream-written 64-bit flags
+ * (no SM waits).  Needs every rank's GPU to map every other's memory. */
+int gpb_dist_set_exchange(gpb_dist* dc, int mode);
 /* GPModel(train, params, tiles_per_dim) sharded: every rank passes the whole
  * (replicated) z, y and keeps only its tiles of K / L */
 int gpb_dist_model_create(gpb_dist* dc, const double* z, const double* y, int64_t n, int64_t d,
@@ -302,7 +309,12 @@ enum {
 };
 enum {
   GPB_OP_ASSEMBLE = 1, GPB_OP_POTRF, GPB_OP_GEMM, GPB_OP_COPY, GPB_OP_GEMV, GPB_OP_COMBINE, GPB_OP_BCAST,
-  GPB_OP_REDUCE, GPB_OP_ALLREDUCE, GPB_OP_RECORD, GPB_OP_WAIT, GPB_OP_ZERO, GPB_OP_SOLVE_FLOW, GPB_OP_TRACE
+  GPB_OP_REDUCE, GPB_OP_ALLREDUCE, GPB_OP_RECORD, GPB_OP_WAIT, GPB_OP_ZERO, GPB_OP_SOLVE_FLOW, GPB_OP_TRACE,
+  /* peer-memory exchange: MIRROR lists extra stores of the preceding GEMM's outputs
+   * (job: k = index of the GEMM job, i = destination rank, buf[3] / off[3] = where
+   * in that rank's buffers); SIGNAL sets flag `j` (0 ready, 1 free) of rank i to
+   * count; WAITFLAG waits until this rank's flag j of source rank i reaches count */
+  GPB_OP_MIRROR, GPB_OP_SIGNAL, GPB_OP_WAITFLAG
 };
 typedef struct gpb_op {
   int32_t kind, stream, group, root;  /* stream 0 main, 1 critical; group 0 world, 1 row, 2 column */
@@ -320,7 +332,8 @@ typedef struct gpb_op_job {
   int64_t off[4];
   int32_t k, lower, i, j;             /* GEMM depth and diagonal-tile flag; tile coordinates */
 } gpb_op_job;
-int gpb_dist_plan(int rank, int world, int P, int Q, int64_t n, int64_t tiles_per_dim, int phase,
+/* exchange: as gpb_dist_set_exchange */
+int gpb_dist_plan(int rank, int world, int P, int Q, int64_t n, int64_t tiles_per_dim, int phase, int exchange,
                   gpb_op* ops, int64_t* nops, gpb_op_job* jobs, int64_t* njobs, int64_t bufsz[GPB_NBUF],
                   int64_t meta[16]);
 

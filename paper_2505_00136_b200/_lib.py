@@ -127,8 +127,9 @@ SIGNATURES = {
     "gpb_dist_timings": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_int]),
     "gpb_dist_launch_count": (ctypes.c_int, [_vp, _c_i64_p]),
     "gpb_dist_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
-                                     ctypes.c_int64, ctypes.c_int, _vp, _c_i64_p, _vp, _c_i64_p, _c_i64_p,
-                                     _c_i64_p]),
+                                     ctypes.c_int64, ctypes.c_int, ctypes.c_int, _vp, _c_i64_p, _vp, _c_i64_p,
+                                     _c_i64_p, _c_i64_p]),
+    "gpb_dist_set_exchange": (ctypes.c_int, [_vp, ctypes.c_int]),
     "gpb_tile_potrf": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_int64, _c_double_p]),
     "gpb_tile_trsm": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, ctypes.c_int64,
                                      ctypes.c_int64, _c_double_p]),
@@ -190,7 +191,8 @@ class HostColl(ctypes.Structure):
 NCCL_ID_BYTES = 128  # GPB_NCCL_ID_BYTES
 BUFFERS = ("L", "DINV", "ROW", "COL", "VEC", "X", "KINV", "XCOL", "XROW", "LCOL")  # GPB_BUF_*
 OPS = {1: "ASSEMBLE", 2: "POTRF", 3: "GEMM", 4: "COPY", 5: "GEMV", 6: "COMBINE", 7: "BCAST", 8: "REDUCE",
-       9: "ALLREDUCE", 10: "RECORD", 11: "WAIT", 12: "ZERO", 13: "SOLVE_FLOW", 14: "TRACE"}  # GPB_OP_*
+       9: "ALLREDUCE", 10: "RECORD", 11: "WAIT", 12: "ZERO", 13: "SOLVE_FLOW", 14: "TRACE", 15: "MIRROR",
+       16: "SIGNAL", 17: "WAITFLAG"}  # GPB_OP_*
 # gpb_op / gpb_op_job as numpy records (the schedule IR of gpb_dist_plan)
 OP_DTYPE = np.dtype([("kind", "<i4"), ("stream", "<i4"), ("group", "<i4"), ("root", "<i4"),
                      ("buf", "<i4", 3), ("flag", "<i4"), ("off", "<i8", 3), ("count", "<i8"),
@@ -204,19 +206,19 @@ META = ("bi", "Ti", "np", "P", "Q", "G", "nown", "nevents", "Y", "BETA", "ALPHA"
         "RECV", "RED")
 
 
-def dist_plan(rank: int, world: int, p: int, q: int, n: int, tiles_per_dim: int, phase: int):
+def dist_plan(rank: int, world: int, p: int, q: int, n: int, tiles_per_dim: int, phase: int, exchange: int = 0):
     """One rank's operation list of a phase (gpb_dist_plan; host only, no GPU):
-    (ops, jobs, buffer sizes in doubles, meta dict)."""
+    (ops, jobs, buffer sizes in doubles, meta dict).  exchange 1: peer-memory panels."""
     lib = load()
     nops, njobs = ctypes.c_int64(), ctypes.c_int64()
     bufsz = (ctypes.c_int64 * len(BUFFERS))()
     meta = (ctypes.c_int64 * 16)()
-    check(lib.gpb_dist_plan(rank, world, p, q, n, tiles_per_dim, phase, None, ctypes.byref(nops), None,
+    check(lib.gpb_dist_plan(rank, world, p, q, n, tiles_per_dim, phase, exchange, None, ctypes.byref(nops), None,
                             ctypes.byref(njobs), bufsz, meta))
     ops = np.zeros(nops.value, dtype=OP_DTYPE)
     jobs = np.zeros(max(1, njobs.value), dtype=JOB_DTYPE)
-    check(lib.gpb_dist_plan(rank, world, p, q, n, tiles_per_dim, phase, ops.ctypes.data, ctypes.byref(nops),
-                            jobs.ctypes.data, ctypes.byref(njobs), bufsz, meta))
+    check(lib.gpb_dist_plan(rank, world, p, q, n, tiles_per_dim, phase, exchange, ops.ctypes.data,
+                            ctypes.byref(nops), jobs.ctypes.data, ctypes.byref(njobs), bufsz, meta))
     return ops, jobs[:njobs.value], dict(zip(BUFFERS, bufsz[:])), dict(zip(META, meta[:]))
 
 

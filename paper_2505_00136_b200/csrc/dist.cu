@@ -213,6 +213,8 @@ __global__ void dist_copy_small_kernel(const CopyJob* jobs, int64_t count) {  //
 struct Phase {
   std::vector<gpb_op> ops;
   std::vector<int64_t> table;  // per op: byte offset of its device table, or -1
+  std::vector<int64_t> mirror; // per GEMM op: byte offset of its mirror-store table, or -1
+  std::vector<int> nmirror;    // ... and its stores per job
   void* dev = nullptr;
   size_t bytes = 0;
   int64_t launches_per_run = 0;
@@ -226,6 +228,7 @@ struct Phase {
 struct gpb_dist {
   gpb_ctx* ctx = nullptr;
   int rank = 0, world = 1, P = 1, Q = 1;
+  int exchange = 0;  // gpb_dist_set_exchange: 0 collectives, 1 peer memory
   Transport* tr = nullptr;
 };
 
@@ -256,6 +259,13 @@ struct gpb_dmodel {
   int64_t adam_step = 0;
   gpb_model* rep = nullptr;  // local replica of the factor for sharded prediction
   bool rep_ok = false;
+  // peer-memory panel exchange (L.p2p): this rank's flag words (ready[src] at
+  // src, free[src] at world + src) and every peer's row panel, column panel and
+  // flags mapped through CUDA IPC
+  uint64_t* flags = nullptr;
+  std::vector<void*> peer_row, peer_col, peer_flags;
+  bool p2p_ready = false;
+  uint64_t epoch = 0;
 };
 
 namespace {
@@ -290,6 +300,8 @@ int build_phase(gpb_dmodel* m, int phase) {
   std::vector<char> host;
   auto align = [&]() { host.resize((host.size() + 15) & ~size_t(15)); };
   P.table.assign(P.ops.size(), -1);
+  P.mirror.assign(P.ops.size(), -1);
+  P.nmirror.assign(P.ops.size(), 0);
   P.launches_per_run = 0;
   for (size_t q = 0; q < P.ops.size(); ++q) {
     const gpb_op& o = P.ops[q];
@@ -300,6 +312,28 @@ int build_phase(gpb_dmodel* m, int phase) {
       memcpy(host.data() + at, p, n);
     };
     switch (o.kind) {
+      case GPB_OP_MIRROR: {  // extra output stores of the preceding GEMM (peer panel buffers)
+        if (q == 0 || P.ops[q - 1].kind != GPB_OP_GEMM || !m->p2p_ready)
+          return fail(GPB_INVALID_CONFIG, "mirror stores without a preceding GEMM or peer mappings");
+        const int64_t ng = P.ops[q - 1].njobs;
+        std::vector<int> per(ng, 0);
+        for (int64_t t = 0; t < o.njobs; ++t) ++per[J[t].k];
+        const int nm = *std::max_element(per.begin(), per.end());
+        std::vector<double*> tab(ng * nm, nullptr);
+        std::fill(per.begin(), per.end(), 0);
+        for (int64_t t = 0; t < o.njobs; ++t) {
+          const int r = J[t].i, b = J[t].buf[3];
+          if (b != GPB_BUF_ROW && b != GPB_BUF_COL) return fail(GPB_INVALID_CONFIG, "mirror outside the panels");
+          char* base = r == m->L.rank ? reinterpret_cast<char*>(m->buf[b])
+                                      : static_cast<char*>(b == GPB_BUF_ROW ? m->peer_row[r] : m->peer_col[r]);
+          tab[J[t].k * nm + per[J[t].k]++] = reinterpret_cast<double*>(base) + J[t].off[3];
+        }
+        align();
+        P.mirror[q - 1] = static_cast<int64_t>(host.size());
+        P.nmirror[q - 1] = nm;
+        put(tab.data(), sizeof(double*) * tab.size());
+        break;
+      }
       case GPB_OP_GEMM: {
         align();
         P.table[q] = static_cast<int64_t>(host.size());
@@ -463,8 +497,26 @@ int run_phase(gpb_dmodel* m, int phase, double* enqueue_us = nullptr) {
         p.a_extent = ba >= 0 ? L.bufsz[ba] : 0;
         p.b_base = bb >= 0 ? m->buf[bb] : nullptr;
         p.b_extent = bb >= 0 ? L.bufsz[bb] : 0;
-        DCUDA(launch_gemm(p, o.ak != 0, o.bk != 0, EPI_AXPBY, s));
+        int epi = EPI_AXPBY;
+        if (P.mirror[q] >= 0) {  // fused panel exchange: stores into the peers' panels
+          p.mirror = reinterpret_cast<double* const*>(dev + P.mirror[q]);
+          p.nmirror = P.nmirror[q];
+          epi = EPI_MIRROR;
+        }
+        DCUDA(launch_gemm(p, o.ak != 0, o.bk != 0, epi, s));
         ++m->launches;
+        break;
+      }
+      case GPB_OP_MIRROR:  // merged into the preceding GEMM launch
+        break;
+      case GPB_OP_SIGNAL: {
+        uint64_t* f = static_cast<uint64_t*>(m->peer_flags[o.i]) + int64_t(o.j) * L.world + L.rank;
+        DTRY(gpb_dev_signal(m->dc->ctx, s, f, (m->epoch << 24) + static_cast<uint64_t>(o.count)));
+        break;
+      }
+      case GPB_OP_WAITFLAG: {
+        const uint64_t* f = m->flags + int64_t(o.j) * L.world + o.i;
+        DTRY(gpb_dev_wait(m->dc->ctx, s, f, (m->epoch << 24) + static_cast<uint64_t>(o.count)));
         break;
       }
       case GPB_OP_COPY:
@@ -558,10 +610,75 @@ float elapsed(gpb_dmodel* m) {
   return ms;
 }
 
+// Peer-memory exchange: export this rank's panel buffers and flag words
+// (CUDA IPC), broadcast the handles rank by rank, map every peer's.
+int setup_p2p(gpb_dmodel* m) {
+  if (m->p2p_ready) return GPB_OK;
+  const DistLayout& L = m->L;
+  const int W = L.world;
+  DCUDA(cudaMalloc(&m->flags, sizeof(uint64_t) * 2 * W));
+  DCUDA(cudaMemset(m->flags, 0, sizeof(uint64_t) * 2 * W));
+  constexpr int kH = sizeof(cudaIpcMemHandle_t);  // 64 bytes = 8 doubles
+  static_assert(kH % 8 == 0, "IPC handle size");
+  constexpr int kSlot = 3 * kH / 8;                // doubles per rank: row, column, flags
+  std::vector<cudaIpcMemHandle_t> mine(3);
+  memset(mine.data(), 0, sizeof(cudaIpcMemHandle_t) * 3);
+  DCUDA(cudaIpcGetMemHandle(&mine[0], m->buf[GPB_BUF_ROW]));
+  if (m->buf[GPB_BUF_COL]) DCUDA(cudaIpcGetMemHandle(&mine[1], m->buf[GPB_BUF_COL]));
+  DCUDA(cudaIpcGetMemHandle(&mine[2], m->flags));
+  double* dh = nullptr;
+  DCUDA(cudaMalloc(&dh, sizeof(double) * kSlot * W));
+  std::vector<double> all(size_t(kSlot) * W, 0.0);
+  memcpy(all.data() + size_t(kSlot) * L.rank, mine.data(), 3 * kH);
+  DCUDA(cudaMemcpy(dh, all.data(), sizeof(double) * all.size(), cudaMemcpyHostToDevice));
+  int s = GPB_OK;
+  for (int r = 0; r < W && s == GPB_OK; ++r) s = m->dc->tr->bcast(0, dh + size_t(kSlot) * r, kSlot, r, m->st);
+  if (s == GPB_OK && cudaStreamSynchronize(m->st) == cudaSuccess)
+    cudaMemcpy(all.data(), dh, sizeof(double) * all.size(), cudaMemcpyDeviceToHost);
+  cudaFree(dh);
+  DTRY(s);
+  m->peer_row.assign(W, nullptr);
+  m->peer_col.assign(W, nullptr);
+  m->peer_flags.assign(W, nullptr);
+  for (int r = 0; r < W; ++r) {
+    if (r == L.rank) {
+      m->peer_row[r] = m->buf[GPB_BUF_ROW];
+      m->peer_col[r] = m->buf[GPB_BUF_COL];
+      m->peer_flags[r] = m->flags;
+      continue;
+    }
+    cudaIpcMemHandle_t h[3];
+    memcpy(h, all.data() + size_t(kSlot) * r, 3 * kH);
+    DCUDA(cudaIpcOpenMemHandle(&m->peer_row[r], h[0], cudaIpcMemLazyEnablePeerAccess));
+    if (L.P > 1) DCUDA(cudaIpcOpenMemHandle(&m->peer_col[r], h[1], cudaIpcMemLazyEnablePeerAccess));
+    DCUDA(cudaIpcOpenMemHandle(&m->peer_flags[r], h[2], cudaIpcMemLazyEnablePeerAccess));
+  }
+  m->p2p_ready = true;
+  return GPB_OK;
+}
+
+// collective: no peer may still store into this rank's panels when they are freed
+void teardown_p2p(gpb_dmodel* m) {
+  if (!m->p2p_ready) return;
+  cudaDeviceSynchronize();
+  m->dc->tr->allreduce(0, m->red, 1, m->st);  // every rank has drained its streams
+  cudaStreamSynchronize(m->st);
+  for (int r = 0; r < m->L.world; ++r) {
+    if (r == m->L.rank) continue;
+    for (void* p : {m->peer_row[r], m->peer_col[r], m->peer_flags[r]})
+      if (p) cudaIpcCloseMemHandle(p);
+  }
+  m->dc->tr->allreduce(0, m->red, 1, m->st);  // every mapping closed before the owners free
+  cudaStreamSynchronize(m->st);
+  m->p2p_ready = false;
+}
+
 // assemble + factor + solves (model.py:169-186 _ensure_factor / _ensure_weights)
 int ensure_factor(gpb_dmodel* m) {
   if (m->factor_ok) return GPB_OK;
   const DistLayout& L = m->L;
+  if (L.p2p) DTRY(setup_p2p(m));
+  ++m->epoch;  // flag values grow across factorisations: nothing is reset
   DTRY(build_phase(m, 0));
   DTRY(build_phase(m, 1));
   m->rep_ok = false;
@@ -728,7 +845,7 @@ void release(gpb_dmodel* m) {
     }
   for (void* p : {static_cast<void*>(m->z), static_cast<void*>(m->y), static_cast<void*>(m->zp),
                   static_cast<void*>(m->info), static_cast<void*>(m->parts), static_cast<void*>(m->red),
-                  static_cast<void*>(m->flow_flags), static_cast<void*>(m->flow_x)})
+                  static_cast<void*>(m->flow_flags), static_cast<void*>(m->flow_x), static_cast<void*>(m->flags)})
     if (p) cudaFree(p);
   for (cudaEvent_t e : m->ev) cudaEventDestroy(e);
   if (m->t0) cudaEventDestroy(m->t0);
@@ -806,6 +923,13 @@ int gpb_dist_init_host(gpb_ctx* ctx, int rank, int world, int P, int Q, const gp
   return GPB_OK;
 }
 
+int gpb_dist_set_exchange(gpb_dist* dc, int mode) {
+  if (!dc) return fail(GPB_INVALID_CONFIG, "null runtime");
+  if (mode != 0 && mode != 1) return fail(GPB_INVALID_CONFIG, "exchange must be 0 (collectives) or 1 (peer memory)");
+  dc->exchange = mode;
+  return GPB_OK;
+}
+
 int gpb_dist_finalize(gpb_dist* dc) {
   if (!dc) return GPB_OK;
   cudaDeviceSynchronize();
@@ -824,7 +948,7 @@ int gpb_dist_model_create(gpb_dist* dc, const double* z, const double* y, int64_
   gpb_dmodel* m = new gpb_dmodel();
   m->dc = dc;
   std::string err;
-  if (int s = dist_layout(dc->rank, dc->world, dc->P, dc->Q, n, tiles_per_dim, &m->L, &err)) {
+  if (int s = dist_layout(dc->rank, dc->world, dc->P, dc->Q, n, tiles_per_dim, &m->L, &err, dc->exchange)) {
     delete m;
     return fail(s, err);
   }
@@ -891,6 +1015,7 @@ int gpb_dist_model_destroy(gpb_dmodel* m) {
   if (!m) return GPB_OK;
   if (m->st) cudaStreamSynchronize(m->st);
   if (m->crit) cudaStreamSynchronize(m->crit);
+  teardown_p2p(m);
   release(m);
   delete m;
   return GPB_OK;

@@ -119,7 +119,21 @@ const Ref kNone{-1, 0};
 
 }  // namespace
 
-int dist_layout(int rank, int world, int P, int Q, int64_t n, int64_t T, DistLayout* out, std::string* err) {
+int col_pos(const DistLayout& L, int j) {
+  int c = 0;
+  for (int t = 0; t < j; ++t)
+    if (t % L.P == j % L.P && t % L.Q == j % L.Q) ++c;
+  return c;
+}
+
+int col_cnt_max(const DistLayout& L, int q) {
+  std::vector<int> cnt(L.P, 0);
+  for (int j = q; j < L.Ti; j += L.Q) ++cnt[j % L.P];
+  return *std::max_element(cnt.begin(), cnt.end());
+}
+
+int dist_layout(int rank, int world, int P, int Q, int64_t n, int64_t T, DistLayout* out, std::string* err,
+                int exchange) {
   DistLayout& L = *out;
   if (world < 1 || P < 1 || Q < 1 || P * Q != world || rank < 0 || rank >= world) {
     if (err) *err = "process grid " + std::to_string(P) + " x " + std::to_string(Q) + " does not match " +
@@ -191,7 +205,8 @@ int dist_layout(int rank, int world, int P, int Q, int64_t n, int64_t T, DistLay
   L.bufsz[GPB_BUF_XROW] = Q > 1 ? int64_t(Q) * std::max(1, L.cntx) * bi2 : 0;
   L.bufsz[GPB_BUF_LCOL] = Q > 1 ? int64_t(L.rows_per) * bi2 : 0;
   const int ng = static_cast<int>(chol_group_sizes(Ti, L.G).size());
-  L.nevents = 2 * ng + 2;
+  L.p2p = exchange == 1 && world > 1;
+  L.nevents = 3 * ng + 2;
   return GPB_OK;
 }
 
@@ -215,9 +230,58 @@ void plan_factor(const DistLayout& L, Builder& b) {
   const int64_t b_walk = P == 1 ? a_walk : int64_t(L.cnt_max) * bi2;
   const std::vector<int> sizes = chol_group_sizes(Ti, G);
   const int ng = static_cast<int>(sizes.size());
-  const int ev_start = 0, ev_end = 1 + 2 * ng;
+  const int ev_start = 0, ev_end = 1 + 3 * ng;
   auto ev_panel = [&](int s) { return 1 + s; };
   auto ev_upd = [&](int s) { return 1 + ng + s; };
+  auto ev_next = [&](int s) { return 1 + 2 * ng + s; };
+
+  // ---- peer-memory exchange (L.p2p): who sends panel k's tiles to whom.
+  // Tile i > k of panel k is solved by rank (i mod P, k mod Q); process row
+  // i mod P reads it from its row panel, process column i mod Q from its
+  // column panel (with P == 1 the row panel serves both).
+  auto has_rows = [&](int pp, int k) {  // a panel tile i > k in process row pp
+    for (int i = k + 1; i < Ti; ++i)
+      if (i % P == pp) return true;
+    return false;
+  };
+  auto has_tiles = [&](int pp, int q, int k) {  // ... that process column q reads
+    for (int i = k + 1; i < Ti; ++i)
+      if (i % P == pp && i % Q == q) return true;
+    return false;
+  };
+  auto rank_of = [&](int p, int q) { return p * Q + q; };
+  // destinations (rank, buffer, offset) of tile i of panel g in set `set`
+  auto dests = [&](int set, int g, int i) {
+    std::vector<std::pair<int, Ref>> d;
+    const int pp = i % P;
+    if (Q > 1)  // the producer's process row (same row-panel layout on every member)
+      for (int q = 0; q < Q; ++q)
+        if (q != L.my_q) d.push_back({rank_of(pp, q), rowt(set, g, i)});
+    if (P > 1) {  // process column i mod Q, in its column-panel layout
+      const int q = i % Q;
+      const int64_t off = (((int64_t(set) * P + pp) * G + g) * col_cnt_max(L, q) + col_pos(L, i)) * bi2;
+      for (int p = 0; p < P; ++p) d.push_back({rank_of(p, q), Ref{GPB_BUF_COL, off}});
+    }
+    return d;
+  };
+  auto sources = [&](int k) {  // ranks whose stores this rank waits for at panel k
+    std::vector<int> src;
+    const int kq = k % Q;
+    if (Q > 1 && L.my_q != kq && has_rows(L.my_p, k)) src.push_back(rank_of(L.my_p, kq));
+    if (P > 1)
+      for (int pp = 0; pp < P; ++pp)
+        if (has_tiles(pp, L.my_q, k) && rank_of(pp, kq) != L.rank) src.push_back(rank_of(pp, kq));
+    std::sort(src.begin(), src.end());
+    src.erase(std::unique(src.begin(), src.end()), src.end());
+    return src;
+  };
+  auto flag_op = [&](int kind, int stream, int peer, int which, int64_t value) {
+    gpb_op o = b.base(kind, stream);
+    o.i = peer;
+    o.j = which;
+    o.count = value;
+    b.push(o);
+  };
 
   b.zero(MAIN, {GPB_BUF_VEC, L.vec[V_LOGDIAG]}, Ti);
   b.begin();
@@ -235,6 +299,20 @@ void plan_factor(const DistLayout& L, Builder& b) {
   for (int s = 0, k0 = 0; s < ng; k0 += sizes[s], ++s) {
     const int gs = sizes[s], k1 = k0 + gs - 1, set = s % 2;
     if (s >= 2) b.wait(CRIT, ev_upd(s - 2));
+    if (L.p2p && s >= 2) {
+      // this rank's stores of group s land in panel set s mod 2 of its peers:
+      // wait until each has finished group s - 2 (its "free" flag)
+      std::vector<int> tg;
+      for (int k = k0; k <= k1 && k + 1 < Ti; ++k)
+        if (L.my_q == k % Q)
+          for (int i = k + 1; i < Ti; ++i)
+            if (slot(i, k) >= 0)
+              for (auto& d : dests(set, k - k0, i))
+                if (d.first != L.rank) tg.push_back(d.first);
+      std::sort(tg.begin(), tg.end());
+      tg.erase(std::unique(tg.begin(), tg.end()), tg.end());
+      for (int r : tg) flag_op(GPB_OP_WAITFLAG, CRIT, r, 1, s - 1);
+    }
     for (int g = 0; g < gs; ++g) {
       const int k = k0 + g;
       if (L.my_q == k % Q) {
@@ -257,18 +335,39 @@ void plan_factor(const DistLayout& L, Builder& b) {
             b.job(lt(i, k), {GPB_BUF_DINV, int64_t(k) * bi2 + int64_t(c) * kBlk * bi}, kNone,
                   {GPB_BUF_ROW, rowt(set, g, i).off + c * kBlk}, (c + 1) * kBlk, 0, i, k);
         }
+        const int64_t trsm0 = static_cast<int64_t>(b.jobs->size()) - b.pending();
+        const int64_t ntrsm = b.pending();
         b.close(b.gemm(CRIT, nb, 1, bi, true, true, 1.0, 0.0));
+        if (L.p2p && ntrsm > 0) {
+          // the TRSM's epilogue also stores every tile where its readers keep it
+          std::vector<int> tg;
+          b.begin();
+          for (int64_t t = 0; t < ntrsm; ++t) {
+            const gpb_op_job jb = (*b.jobs)[trsm0 + t];
+            const int c = static_cast<int>((jb.off[3] - rowt(set, g, jb.i).off) / kBlk);
+            for (auto& d : dests(set, g, jb.i)) {
+              b.job(kNone, kNone, kNone, {d.second.buf, d.second.off + c * kBlk}, static_cast<int>(t), 0,
+                    d.first, 0);
+              if (d.first != L.rank) tg.push_back(d.first);
+            }
+          }
+          b.close(b.base(GPB_OP_MIRROR, CRIT));
+          std::sort(tg.begin(), tg.end());
+          tg.erase(std::unique(tg.begin(), tg.end()), tg.end());
+          for (int r : tg) flag_op(GPB_OP_SIGNAL, CRIT, r, 0, k + 1);  // panel k ready
+        }
       }
       if (k + 1 == Ti) break;
-      // row stage: this process row's panel tiles from rank (my_p, k mod Q)
-      if (Q > 1) {
+      if (L.p2p) {  // wait for the stores of every rank that solved tiles this rank reads
+        for (int r : sources(k)) flag_op(GPB_OP_WAITFLAG, CRIT, r, 0, k + 1);
+      } else if (Q > 1) {  // row stage: this process row's panel tiles from rank (my_p, k mod Q)
         int first = k + 1;
         while (first < Ti && first % P != L.my_p) ++first;
         const int64_t cnt = first < Ti ? (Ti - 1 - first) / P + 1 : 0;
         if (cnt > 0) b.coll(GPB_OP_BCAST, CRIT, ROWG, k % Q, rowt(set, g, first), cnt * bi2);
       }
       // column stage: panel tiles j = p' (mod P), j = my_q (mod Q) from rank (p', my_q)
-      if (P > 1) {
+      if (P > 1 && !L.p2p) {
         for (int pp = 0; pp < P; ++pp) {
           std::vector<int> js;
           for (int j = k + 1; j < Ti; ++j)
@@ -316,6 +415,7 @@ void plan_factor(const DistLayout& L, Builder& b) {
       if (s >= 1) b.wait(CRIT, ev_upd(s - 1));
       update(CRIT, c_next, c_upd);
     }
+    b.record(CRIT, ev_next(s));
     // main stream: copy the solved panel tiles back into L, then the rest of the update
     b.wait(MAIN, ev_panel(s));
     b.begin();
@@ -332,6 +432,12 @@ void plan_factor(const DistLayout& L, Builder& b) {
     }
     update(MAIN, c_upd, Ti);
     b.record(MAIN, ev_upd(s));
+    if (L.p2p && s + 2 < ng) {
+      // panel set s mod 2 is no longer read here (UPD(s) and NEXT(s) done): tell the peers
+      b.wait(MAIN, ev_next(s));
+      for (int r = 0; r < L.world; ++r)
+        if (r != L.rank) flag_op(GPB_OP_SIGNAL, MAIN, r, 1, s + 1);
+    }
   }
   b.record(CRIT, ev_end);
   b.wait(MAIN, ev_end);
@@ -576,12 +682,12 @@ void dist_plan(const DistLayout& L, int phase, std::vector<gpb_op>* ops, std::ve
 extern "C" int gpb_plugin_fail(int code, const char* msg);
 
 extern "C" int gpb_dist_plan(int rank, int world, int P, int Q, int64_t n, int64_t tiles_per_dim, int phase,
-                             gpb_op* ops, int64_t* nops, gpb_op_job* jobs, int64_t* njobs,
+                             int exchange, gpb_op* ops, int64_t* nops, gpb_op_job* jobs, int64_t* njobs,
                              int64_t bufsz[GPB_NBUF], int64_t meta[16]) {
   if (phase < 0 || phase > 2) return gpb_plugin_fail(GPB_INVALID_CONFIG, "phase must be 0, 1 or 2");
   gpb::DistLayout L;
   std::string err;
-  if (int s = gpb::dist_layout(rank, world, P, Q, n, tiles_per_dim, &L, &err))
+  if (int s = gpb::dist_layout(rank, world, P, Q, n, tiles_per_dim, &L, &err, exchange))
     return gpb_plugin_fail(s, err.c_str());
   std::vector<gpb_op> o;
   std::vector<gpb_op_job> j;

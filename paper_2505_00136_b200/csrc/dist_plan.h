@@ -29,13 +29,18 @@ struct DistLayout {
   int64_t bufsz[GPB_NBUF] = {0};
   int64_t vec[V_NSLOT] = {0};
   int nevents = 0;
+  bool p2p = false;                 // peer-memory panel exchange (gpb_dist_set_exchange)
   int owner(int i, int j) const { return (i % P) * Q + (j % Q); }
   int nown() const { return static_cast<int>(own_i.size()); }
 };
 
 // returns a gpb_status; fills the layout of rank `rank` of a P x Q grid
 int dist_layout(int rank, int world, int P, int Q, int64_t n, int64_t tiles_per_dim, DistLayout* out,
-                std::string* err);
+                std::string* err, int exchange = 0);
+// position of panel tile j in process column q's column-panel slot list
+// J(j mod P, q), and that list's largest length over the process rows
+int col_pos(const DistLayout& L, int j);
+int col_cnt_max(const DistLayout& L, int q);
 
 // phase 0: assembly + factorisation (+ replication of the inverse diagonal
 // tiles); 1: beta / alpha solves (+ replication of beta, alpha, log-diagonal);

@@ -13,6 +13,12 @@ partial sums) and prediction sharded over test points.  Python only creates
 the communicator bootstrap and maps results onto the reference's types
 (taskgp model.py:91-485).
 
+Panel exchange: "collective" (default; broadcasts on the row / column
+communicators) or "p2p" -- the panel TRSM's epilogue stores each solved tile
+straight into the panel buffers of the ranks that read it (CUDA IPC mappings,
+NVLink stores), ordered by stream-written flags; a rank then receives only
+the tiles its trailing update reads and no SM waits on a collective.
+
 Transports: "nccl" (default) -- rank 0 makes an NCCL unique id, the ranks
 exchange it over the torch.distributed group (any backend; the data path never
 touches torch), the library creates and splits its communicators.  "host" --
@@ -113,7 +119,8 @@ class DistComm:
     """A gpb_dist handle: this rank's place in the P x Q grid and the
     library's communicators.  Collective: every rank constructs it."""
 
-    def __init__(self, runtime=None, grid: tuple[int, int] | None = None, transport: str | None = None):
+    def __init__(self, runtime=None, grid: tuple[int, int] | None = None, transport: str | None = None,
+                 exchange: str | None = None):
         if runtime is None:
             from .runtime import require_runtime
 
@@ -142,6 +149,12 @@ class DistComm:
         else:
             raise ValueError(f"unknown transport {self.transport!r} (nccl or host)")
         self.handle = h
+        # panel exchange of the factorisation: "collective" (row / column broadcasts)
+        # or "p2p" (TRSM epilogue stores into the readers' panel buffers over CUDA IPC)
+        self.exchange = exchange or os.environ.get("GPB_DIST_EXCHANGE", "collective")
+        if self.exchange not in ("collective", "p2p"):
+            raise ValueError(f"unknown exchange {self.exchange!r} (collective or p2p)")
+        _lib.check(lib.gpb_dist_set_exchange(h, 1 if self.exchange == "p2p" else 0))
 
     def close(self):
         if self.handle:
@@ -159,14 +172,14 @@ class DistributedGP:
 
     def __init__(self, train, params: KernelParams | None = None, tiles_per_dim: int = 1,
                  comm: DistComm | None = None, grid: tuple[int, int] | None = None,
-                 transport: str | None = None):
+                 transport: str | None = None, exchange: str | None = None):
         train = train if isinstance(train, Dataset) else Dataset(np.asarray(train.z), np.asarray(train.y))
         if tiles_per_dim < 1 or train.n % tiles_per_dim != 0:
             raise TilingError(f"tiles_per_dim={tiles_per_dim} must divide the {train.n} training points")
         self.train = train
         self.tiles_per_dim = tiles_per_dim
         self._own_comm = comm is None
-        self.comm = comm or DistComm(grid=grid, transport=transport)
+        self.comm = comm or DistComm(grid=grid, transport=transport, exchange=exchange)
         self.rank, self.world = self.comm.rank, self.comm.world
         self.P, self.Q = self.comm.P, self.comm.Q
         self._lib = _lib.load()

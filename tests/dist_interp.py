@@ -68,13 +68,15 @@ class HostColl:
 class Interp:
     """One rank's buffers and the replay of its phases."""
 
-    def __init__(self, rank, world, p, q, z, y, tiles, params, coll):
+    def __init__(self, rank, world, p, q, z, y, tiles, params, coll, exchange=0):
         self.rank, self.world, self.P, self.Q = rank, world, p, q
         self.n, self.d = z.shape
         self.tiles = tiles
         self.l, self.nu, self.s2 = params
         self.coll = coll
-        self.plans = [_lib.dist_plan(rank, world, p, q, self.n, tiles, ph) for ph in range(3)]
+        self.plans = [_lib.dist_plan(rank, world, p, q, self.n, tiles, ph, exchange) for ph in range(3)]
+        self._last_gemm = []  # (buf, off, ld, values, mask) of the latest GEMM's jobs
+        self._sends = []
         _, _, bufsz, meta = self.plans[0]
         self.meta = meta
         self.bi, self.Ti, self.np_ = meta["bi"], meta["Ti"], meta["np"]
@@ -182,6 +184,58 @@ class Interp:
             outs.append((jb["buf"][3], jb["off"][3], r, mask))
         for b, off, r, mask in outs:  # jobs of one launch are independent
             self._set(b, off, o["ldc"], r, mask)
+        self._last_gemm = [(int(o["ldc"]), r, mask) for _, _, r, mask in outs]
+
+    # peer-memory exchange: a MIRROR's stores into another rank's buffers travel
+    # as one gloo message per destination, applied at that rank's WAITFLAG on
+    # this rank's "ready" flag (the flag orders them the same way on the GPU)
+    def op_mirror(self, o, jobs):
+        per = {}
+        for jb in jobs:
+            ld, r, mask = self._last_gemm[int(jb["k"])]
+            dst, b, off = int(jb["i"]), int(jb["buf"][3]), int(jb["off"][3])
+            if dst == self.rank:
+                self._set(b, off, ld, r, mask)
+            else:
+                per.setdefault(dst, []).append((b, off, ld, r, mask))
+        for dst, entries in per.items():
+            head = [len(entries)]
+            data = []
+            for b, off, ld, r, mask in entries:
+                m = np.ones(r.shape, bool) if mask is None else mask
+                head += [b, off, ld, r.shape[0], r.shape[1]]
+                data.append(np.where(m, r, np.nan).ravel())
+            h = torch.tensor(head, dtype=torch.int64)
+            d = torch.from_numpy(np.concatenate(data))
+            self._sends += [dist.isend(torch.tensor([len(head)], dtype=torch.int64), dst), dist.isend(h, dst),
+                            dist.isend(d, dst)]
+
+    def op_signal(self, o, jobs):
+        pass
+
+    def op_waitflag(self, o, jobs):
+        if int(o["j"]) != 0:  # "free" flags: buffer reuse cannot race here (messages are copies)
+            return
+        src = int(o["i"])
+        n = torch.zeros(1, dtype=torch.int64)
+        dist.recv(n, src)
+        h = torch.zeros(int(n.item()), dtype=torch.int64)
+        dist.recv(h, src)
+        head = h.tolist()
+        sizes = [head[1 + 5 * e + 3] * head[1 + 5 * e + 4] for e in range(head[0])]
+        d = torch.zeros(sum(sizes), dtype=torch.float64)
+        dist.recv(d, src)
+        vals, at = d.numpy(), 0
+        for e in range(head[0]):
+            b, off, ld, rows, cols = head[1 + 5 * e:6 + 5 * e]
+            r = vals[at:at + rows * cols].reshape(rows, cols)
+            at += rows * cols
+            self._set(b, off, ld, r, ~np.isnan(r))
+
+    def finish(self):
+        for w in self._sends:
+            w.wait()
+        self._sends = []
 
     def op_copy(self, o, jobs):
         c = int(o["count"])

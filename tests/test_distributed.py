@@ -72,14 +72,15 @@ def _entry(target, rank, world, port, args, out_q):
 
 
 # ---- CPU: the schedule IR under the numpy interpreter ---------------------------------
-def _interp_rank(rank, world, grid, kind):
+def _interp_rank(rank, world, grid, kind, exchange=0):
     from dist_interp import HostColl, Interp
 
     z, y, _, t = _case(kind)
     p, q = grid
     coll = HostColl(rank, world, p, q)
-    it = Interp(rank, world, p, q, z, y, t, PARAMS, coll)
+    it = Interp(rank, world, p, q, z, y, t, PARAMS, coll, exchange)
     it.run(0)
+    it.finish()
     assert it.info < 0
     it.run(1)
     it.run(2)
@@ -91,15 +92,19 @@ def _interp_rank(rank, world, grid, kind):
             "bi": it.bi, "np": it.np_, "alpha": vec[m["ALPHA"]:m["ALPHA"] + it.np_].copy(), "calls": coll.calls}
 
 
-@pytest.mark.parametrize("world,grid,kind", [(1, (1, 1), "dense"), (2, (1, 2), "padded"), (2, (2, 1), "dense"),
-                                             (3, (1, 3), "padded"), (4, (2, 2), "dense"), (4, (2, 2), "padded")])
-def test_schedule_ir_against_oracle_cpu(world, grid, kind):
+@pytest.mark.parametrize("world,grid,kind,exchange", [
+    (1, (1, 1), "dense", 0), (2, (1, 2), "padded", 0), (2, (2, 1), "dense", 0), (3, (1, 3), "padded", 0),
+    (4, (2, 2), "dense", 0), (4, (2, 2), "padded", 0),
+    (2, (1, 2), "dense", 1), (2, (2, 1), "padded", 1), (4, (2, 2), "dense", 1), (3, (1, 3), "padded", 1)])
+def test_schedule_ir_against_oracle_cpu(world, grid, kind, exchange):
     """Every rank's operation lists (factor, solves, gradient) replayed on CPU
     with gloo collectives reproduce the oracle; every rank ends with the same
-    replicated alpha, log-likelihood and gradient."""
+    replicated alpha, log-likelihood and gradient.  exchange 1: the panel
+    tiles travel as the TRSM's mirror stores into the readers' panel buffers
+    (one message per destination, applied at the reader's ready-flag wait)."""
     from oracle.tiled_gp import OracleGP, rel_fro
 
-    res = _spawn("_interp_rank", world, grid, kind)
+    res = _spawn("_interp_rank", world, grid, kind, exchange)
     z, y, _, t = _case(kind)
     n = len(y)
     o = OracleGP(z, y, t, *PARAMS)
@@ -132,19 +137,31 @@ def test_plan_structure_and_ownership():
         cyc = BlockCyclic(_lib.layout(n, t)["T"], p, q)
         owned = [cyc.owned(r) for r in range(world)]
         assert sorted(ij for o in owned for ij in o) == sorted((i, j) for i in range(cyc.T) for j in range(i + 1))
-        for phase in range(3):
-            seqs = {}
+        for phase, exchange in [(0, 0), (1, 0), (2, 0), (0, 1)]:
+            seqs, sig, wai = {}, {}, {}
             for r in range(world):
-                ops, jobs, bufsz, meta = _lib.dist_plan(r, world, p, q, n, t, phase)
+                ops, jobs, bufsz, meta = _lib.dist_plan(r, world, p, q, n, t, phase, exchange)
+                for o in ops:  # peer-memory flags: every wait has exactly one matching signal
+                    if o["kind"] == 16:
+                        sig.setdefault((r, int(o["i"]), int(o["j"]), int(o["count"])), 0)
+                        sig[(r, int(o["i"]), int(o["j"]), int(o["count"]))] += 1
+                    if o["kind"] == 17:
+                        wai.setdefault((int(o["i"]), r, int(o["j"]), int(o["count"])), 0)
+                        wai[(int(o["i"]), r, int(o["j"]), int(o["count"]))] += 1
                 assert meta["nown"] == len(owned[r])
                 for o in ops:  # every buffer reference inside its buffer
                     if o["kind"] in (7, 8, 9, 12):
                         b = _lib.BUFFERS[o["buf"][0]]
                         assert 0 <= o["off"][0] and o["off"][0] + o["count"] <= bufsz[b]
-                for jb in jobs:
+                mirror = np.zeros(len(jobs), bool)  # MIRROR jobs address the destination rank's buffers
+                for o in ops:
+                    if o["kind"] == 15:
+                        mirror[o["job0"]:o["job0"] + o["njobs"]] = True
+                for jb, mir in zip(jobs, mirror):
+                    sizes = _lib.dist_plan(int(jb["i"]), world, p, q, n, t, phase, exchange)[2] if mir else bufsz
                     for s in range(4):
                         if jb["buf"][s] >= 0:
-                            assert 0 <= jb["off"][s] < bufsz[_lib.BUFFERS[jb["buf"][s]]]
+                            assert 0 <= jb["off"][s] < sizes[_lib.BUFFERS[jb["buf"][s]]]
                 mp_, mq = divmod(r, q)
                 for o in ops:
                     if o["kind"] in (7, 8, 9):
@@ -152,6 +169,8 @@ def test_plan_structure_and_ownership():
                         key = (g, 0 if g == 0 else (mp_ if g == 1 else mq))
                         seqs.setdefault(key, {})
                         seqs[key].setdefault(r, []).append((int(o["kind"]), int(o["root"]), int(o["count"])))
+            assert all(sig.get(k, 0) == 1 for k in wai), f"unmatched flag waits (phase {phase})"
+            assert all(k in wai or k[2] == 1 for k in sig), f"ready signals nobody waits for (phase {phase})"
             for key, per_rank in seqs.items():
                 members = {0: range(world), 1: [key[1] * q + qq for qq in range(q)],
                            2: [pp * q + key[1] for pp in range(p)]}[key[0]]
@@ -160,14 +179,15 @@ def test_plan_structure_and_ownership():
 
 
 # ---- GPU: the device executor --------------------------------------------------------------
-def _device_rank(rank, world, grid, kind, transport):
+def _device_rank(rank, world, grid, kind, transport, exchange="collective"):
     import paper_2505_00136_b200 as gpb
     from paper_2505_00136_b200.distributed import DistributedGP
 
     z, y, zt, t = _case(kind)
     rt = gpb.start_runtime(gpb.RuntimeConfig(device=0))
     try:
-        model = DistributedGP(gpb.Dataset(z, y), gpb.KernelParams(*PARAMS), t, grid=grid, transport=transport)
+        model = DistributedGP(gpb.Dataset(z, y), gpb.KernelParams(*PARAMS), t, grid=grid, transport=transport,
+                              exchange=exchange)
         ll = model.log_likelihood()
         pv = model.predict_variance(gpb.Dataset(zt, np.zeros(len(zt))))
         L = model.cholesky()
@@ -213,6 +233,17 @@ def _check_device(res, kind):
                                              (3, (1, 3), "padded")])
 def test_device_executor_host_collectives_one_gpu(world, grid, kind):
     _check_device(_spawn("_device_rank", world, grid, kind, "host"), kind)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,grid,kind", [(2, (1, 2), "padded"), (4, (2, 2), "dense"), (2, (2, 1), "dense")])
+def test_device_executor_peer_memory_exchange_one_gpu(world, grid, kind):
+    """Exchange "p2p": the TRSM's epilogue stores every panel tile into the
+    row / column panels of the ranks that read it (CUDA IPC mappings), ready and
+    free flags written and awaited in stream order (cuStreamWrite/WaitValue64:
+    no kernel waits on another rank's kernel).  The factor stays bitwise the
+    single-GPU one."""
+    _check_device(_spawn("_device_rank", world, grid, kind, "host", "p2p"), kind)
 
 
 @pytest.mark.gpu
