@@ -337,6 +337,14 @@ int gpb_dist_plan(int rank, int world, int P, int Q, int64_t n, int64_t tiles_pe
                   gpb_op* ops, int64_t* nops, gpb_op_job* jobs, int64_t* njobs, int64_t bufsz[GPB_NBUF],
                   int64_t meta[16]);
 
+/* ---- BASELINE input generator on the device ---------
+ * u, noise: the n draws of the host generator (numpy default_rng, SURVEY.md
+ * Appendix A.1), device memory.  Writes y (n) = mass-spring-damper position +
+ * noise (semi-implicit Euler, bitwise the host recurrence) and z (n x n_reg)
+ * = lag features u_t, u_{t-1}, ... (0 before the start). */
+int gpb_msd_series_device(gpb_ctx* ctx, const double* u_dev, const double* noise_dev, int64_t n, int64_t n_reg,
+                          double dt, double mass, double damping, double stiffness, double* z_dev, double* y_dev);
+
 /* ---- tile-kernel plugin (tiles.py:23-46, 132-164) -------------------------
  * Host buffers, fresh outputs, inputs never mutated.  Square tiles b x b;
  * trsm solves X l^T = b_in for rows x b b_in. */

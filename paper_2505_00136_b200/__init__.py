@@ -21,6 +21,7 @@ from .data import (
     lag_features,
     load_csv,
     make_msd_dataset,
+    make_msd_dataset_device,
     msd_series,
     save_csv,
 )
@@ -56,6 +57,7 @@ __all__ = [
     "errors",
     "lag_features",
     "make_msd_dataset",
+    "make_msd_dataset_device",
     "msd_series",
     "run_as_root",
     "start_runtime",

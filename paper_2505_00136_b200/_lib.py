@@ -130,6 +130,8 @@ SIGNATURES = {
                                      ctypes.c_int64, ctypes.c_int, ctypes.c_int, _vp, _c_i64_p, _vp, _c_i64_p,
                                      _c_i64_p, _c_i64_p]),
     "gpb_dist_set_exchange": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "gpb_msd_series_device": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+                                             ctypes.c_double, ctypes.c_double, ctypes.c_double, _vp, _vp]),
     "gpb_tile_potrf": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_int64, _c_double_p]),
     "gpb_tile_trsm": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, ctypes.c_int64,
                                      ctypes.c_int64, _c_double_p]),

@@ -102,6 +102,35 @@ def make_msd_dataset(n_train: int, n_test: int, n_reg: int, seed: int = 0):
     return train, test
 
 
+def make_msd_dataset_device(n_train: int, n_test: int, n_reg: int, seed: int = 0, device: int | None = None):
+    """make_msd_dataset with the trajectory and the lag embedding computed on
+    the GPU (gpb_msd_series_device; bitwise the host arrays): returns torch
+    tensors (z_train, y_train, z_test, y_test) in device memory -- only the
+    2 N random draws cross PCIe.  Needs a running runtime."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .runtime import require_runtime
+
+    if n_train < 1 or n_test < 0 or n_reg < 1:
+        raise InvalidConfig("need n_train >= 1, n_test >= 0, n_reg >= 1")
+    rt = require_runtime()
+    dev = torch.device("cuda", rt.device if device is None else device)
+    n = n_train + n_test
+    rng = np.random.default_rng(seed)  # the draws of msd_series, in its order
+    u = torch.from_numpy(rng.uniform(-1.0, 1.0, size=n)).to(dev)
+    noise = torch.from_numpy(rng.normal(0.0, 0.1, size=n)).to(dev)
+    z = torch.empty((n, n_reg), dtype=torch.float64, device=dev)
+    y = torch.empty(n, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize(dev)  # the library works on its own stream
+    _lib.check(_lib.load().gpb_msd_series_device(rt.handle, ctypes.c_void_p(u.data_ptr()),
+                                                 ctypes.c_void_p(noise.data_ptr()), n, n_reg, 0.01, 1.0, 0.5,
+                                                 1.0, ctypes.c_void_p(z.data_ptr()), ctypes.c_void_p(y.data_ptr())))
+    return z[:n_train], y[:n_train], z[n_train:], y[n_train:]
+
+
 @dataclass(frozen=True)
 class LagSpec:
     """How many past samples form one feature row."""

@@ -515,3 +515,20 @@ def test_one_launch_solves_match_multi_launch(runtime, monkeypatch, n, t, d):
         o = OracleGP(z, y, t, 1.1, 0.9, 0.2)
         assert abs(out["1"][0] - o.log_likelihood()) <= TOL * abs(o.log_likelihood())
         assert rel(out["1"][1], o.predict(zt)) <= TOL
+
+
+@pytest.mark.parametrize("n_train,n_test,d,seed", [(1024, 1024, 8, 0), (8192, 0, 8, 3), (131072, 8192, 16, 0)])
+def test_device_generator_matches_host(runtime, n_train, n_test, d, seed):
+    """gpb_msd_series_device: the trajectory and the lag
+    embedding computed on the GPU are bitwise the host generator's arrays (up
+    to config 4's 139264 samples), and a model built from them gives the same
+    loss as one built from the host arrays."""
+    train, test = gpb.make_msd_dataset(n_train, n_test, d, seed=seed)
+    zt, yt, zs, ys = gpb.make_msd_dataset_device(n_train, n_test, d, seed=seed)
+    assert np.array_equal(zt.cpu().numpy(), train.z) and np.array_equal(yt.cpu().numpy(), train.y)
+    if n_test:
+        assert np.array_equal(zs.cpu().numpy(), test.z) and np.array_equal(ys.cpu().numpy(), test.y)
+    if n_train <= 8192:
+        ll_host = gpb.GPModel(train, tiles_per_dim=8).log_likelihood()
+        ll_dev = gpb.GPModel(gpb.Dataset(zt.cpu().numpy(), yt.cpu().numpy()), tiles_per_dim=8).log_likelihood()
+        assert ll_host == ll_dev
