@@ -183,6 +183,7 @@ __device__ void forward_slice(const FlowArgs& a, int i, int q, double2* vs) {
       // the loads, so the slice's rate is not bounded by its own load depth
       prefetch_l2(a.L + tri_rm(i, j) * bi2 + static_cast<int64_t>(q) * R * bi, sizeof(double) * R * bi);
     wait_count(b_done + j, S, j == i - 1);  // (its __syncthreads also retires the previous vs)
+    if (a.prof && j == i - 1 && q == 0 && threadIdx.x == 0) a.prof[4 * a.T + i] = gtimer();
     const double* tile = a.L + tri_rm(i, j) * bi2;
     const double2* bj = reinterpret_cast<const double2*>(a.beta + static_cast<int64_t>(j) * bi);
     for (int e = threadIdx.x; e < bi / 2; e += FT) vs[e] = __ldcg(bj + e);
@@ -208,6 +209,7 @@ __device__ void forward_slice(const FlowArgs& a, int i, int q, double2* vs) {
   signal_count(r_done + i);
   if (a.prof && q == 0 && threadIdx.x == 0) a.prof[i] = gtimer();
   wait_count(r_done + i, S, true);
+  if (a.prof && q == 0 && threadIdx.x == 0) a.prof[5 * a.T + i] = gtimer();
   // beta_i[rows] = Dinv_i[rows, 0..row] r_i   (lower triangular)
   const double* D = a.dinv + static_cast<int64_t>(i) * bi2;
   const double2* rv = reinterpret_cast<const double2*>(a.xr + g0);
@@ -389,7 +391,8 @@ cudaError_t launch_solve_flow(const double* L, const double* dinv, const double*
   static int prof_T = 0;
   if (getenv("GPB_SOLVE_PROF") && prof_T != T) {
     if (prof) cudaFree(prof);
-    cudaMalloc(&prof, sizeof(unsigned long long) * 4 * T);
+    cudaMalloc(&prof, sizeof(unsigned long long) * 6 * T);
+    cudaMemset(prof, 0, sizeof(unsigned long long) * 6 * T);
     prof_T = T;
   }
   FlowArgs a{L, dinv, y, beta, alpha, xr, flags, T, bi, R, getenv("GPB_SOLVE_PROF") ? prof : nullptr};
@@ -403,13 +406,14 @@ cudaError_t launch_solve_flow(const double* L, const double* dinv, const double*
     default: break;
   }
   if (a.prof && *launched) {  // per block row: r published, beta published, t published, alpha published
-    std::vector<unsigned long long> h(4 * T);
+    std::vector<unsigned long long> h(6 * T);
     cudaStreamSynchronize(s);
-    cudaMemcpy(h.data(), a.prof, sizeof(unsigned long long) * 4 * T, cudaMemcpyDeviceToHost);
+    cudaMemcpy(h.data(), a.prof, sizeof(unsigned long long) * 6 * T, cudaMemcpyDeviceToHost);
     const unsigned long long t0 = h[0];
+    auto at = [&](unsigned long long v) { return v ? (double(v) - double(t0)) * 1e-3 : -1.0; };
     for (int i = 0; i < T; ++i)
-      fprintf(stderr, "flow row %3d: r %8.1f beta %8.1f | t %8.1f alpha %8.1f us\n", i, (h[i] - t0) * 1e-3,
-              (h[T + i] - t0) * 1e-3, (h[2 * T + i] - t0) * 1e-3, (h[3 * T + i] - t0) * 1e-3);
+      fprintf(stderr, "flow row %3d: seen beta_{i-1} %8.1f r %8.1f all r %8.1f beta %8.1f | t %8.1f alpha %8.1f us\n",
+              i, at(h[4 * T + i]), at(h[i]), at(h[5 * T + i]), at(h[T + i]), at(h[2 * T + i]), at(h[3 * T + i]));
   }
   return e;
 }
