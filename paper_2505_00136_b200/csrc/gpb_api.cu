@@ -13,6 +13,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gemm.cuh"
@@ -159,6 +160,11 @@ struct gpb_ctx {
   uint64_t gen = 0;
   cudaStream_t stream = nullptr;
   std::mutex tile_mu;  // tile plugin calls share scratch
+  // pinned staging of the dense factor export (two strips), allocated on first use
+  std::mutex export_mu;
+  char* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  cudaEvent_t strip_ev[2] = {nullptr, nullptr};
 };
 
 // One group of panels of the factorisation plan (build_chol_plan): job ranges
@@ -1351,6 +1357,9 @@ int gpb_finalize(gpb_ctx* ctx) {
   if (!g_ctx || (ctx && ctx != g_ctx)) return fail(GPB_NOT_RUNNING, "no runtime is running");
   cudaDeviceSynchronize();
   cudaStreamDestroy(g_ctx->stream);
+  if (g_ctx->pinned) cudaFreeHost(g_ctx->pinned);
+  for (cudaEvent_t e : g_ctx->strip_ev)
+    if (e) cudaEventDestroy(e);
   delete g_ctx;
   g_ctx = nullptr;
   g_cache.trim();  // blocks still owned by live models stay with them
@@ -1436,23 +1445,71 @@ int gpb_model_get_params(gpb_model* m, double out[3]) {
   return GPB_OK;
 }
 
+namespace {
+// host copy of one strip, split over threads when large (the pageable user
+// array is written at host memory speed instead of the driver's bounce path)
+void host_copy(char* dst, const char* src, size_t bytes) {
+  const size_t chunk = size_t(4) << 20;
+  const int nt = static_cast<int>(std::min<size_t>(8, (bytes + chunk - 1) / chunk));
+  if (nt <= 1) {
+    memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t per = (bytes + nt - 1) / nt;
+  for (int t = 0; t < nt; ++t) {
+    const size_t lo = std::min(bytes, t * per), hi = std::min(bytes, lo + per);
+    th.emplace_back([=] { memcpy(dst + lo, src + lo, hi - lo); });
+  }
+  for (auto& x : th) x.join();
+}
+}  // namespace
+
 int gpb_cholesky(gpb_model* m, double* L_out) {
   GPB_TRY(check_live(m));
   GPB_TRY(ensure_factor(m));
   if (L_out) {
-    // dense export in strips of rows through a bounded staging buffer
-    // (<= 256 MB on the device), so configs 3/4 export without an n x n temporary
+    // Dense export in strips of rows: export kernel -> device strip -> pinned
+    // host strip (full PCIe rate) -> the caller's array (threaded memcpy),
+    // double-buffered so the host copy of strip s overlaps the device work of
+    // strip s + 1.  Bounded memory (2 x 32 MB device and pinned), so configs 3/4
+    // export without an n x n temporary.
+    gpb_ctx* ctx = m->ctx;
+    std::lock_guard<std::mutex> lk(ctx->export_mu);
     const int64_t n = m->n;
-    const int64_t rows = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t(256) << 20) / (8 * n)));
+    const size_t strip_cap = size_t(32) << 20;
+    const int64_t rows = std::max<int64_t>(1, std::min<int64_t>(n, int64_t(strip_cap / (8 * n))));
+    const size_t strip_bytes = sizeof(double) * rows * n;
+    if (ctx->pinned_bytes < 2 * strip_bytes) {
+      if (ctx->pinned) cudaFreeHost(ctx->pinned);
+      ctx->pinned = nullptr;
+      ctx->pinned_bytes = 0;
+      CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->pinned), 2 * strip_bytes, cudaHostAllocDefault));
+      ctx->pinned_bytes = 2 * strip_bytes;
+    }
+    for (cudaEvent_t& e : ctx->strip_ev)
+      if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     DevBuf stage[2];
-    CUDA_TRY(stage[0].ensure(sizeof(double) * rows * n));
-    CUDA_TRY(stage[1].ensure(sizeof(double) * rows * n));
-    for (int64_t r0 = 0, s = 0; r0 < n; r0 += rows, ++s) {
-      const int64_t nr = std::min(rows, n - r0);
+    CUDA_TRY(stage[0].ensure(strip_bytes));
+    CUDA_TRY(stage[1].ensure(strip_bytes));
+    const int64_t nstrips = (n + rows - 1) / rows;
+    auto issue = [&](int64_t s) -> int {
+      const int64_t r0 = s * rows, nr = std::min(rows, n - r0);
       double* buf = stage[s % 2].as<double>();
       CUDA_TRY(launch_export_lower(m->L.as<double>(), m->bi, n, r0, nr, m->pm, buf, m->st));
       ++m->launches;
-      CUDA_TRY(cudaMemcpyAsync(L_out + r0 * n, buf, sizeof(double) * nr * n, cudaMemcpyDeviceToHost, m->st));
+      CUDA_TRY(cudaMemcpyAsync(ctx->pinned + (s % 2) * strip_bytes, buf, sizeof(double) * nr * n,
+                               cudaMemcpyDeviceToHost, m->st));
+      CUDA_TRY(cudaEventRecord(ctx->strip_ev[s % 2], m->st));
+      return GPB_OK;
+    };
+    for (int64_t s = 0; s < std::min<int64_t>(2, nstrips); ++s) GPB_TRY(issue(s));
+    for (int64_t s = 0; s < nstrips; ++s) {
+      const int64_t r0 = s * rows, nr = std::min(rows, n - r0);
+      CUDA_TRY(cudaEventSynchronize(ctx->strip_ev[s % 2]));
+      host_copy(reinterpret_cast<char*>(L_out + r0 * n), ctx->pinned + (s % 2) * strip_bytes,
+                sizeof(double) * nr * n);
+      if (s + 2 < nstrips) GPB_TRY(issue(s + 2));  // this pinned slot is free again
     }
     CUDA_TRY(cudaStreamSynchronize(m->st));
     stage[0].release();
