@@ -292,6 +292,7 @@ class DistributedGP:
         return int(c.value)
 
     def close(self):
+        """Release the model (collective with the peer-memory exchange)."""
         if self._h:
             self._lib.gpb_dist_model_destroy(self._h)
             self._h = None
@@ -300,6 +301,11 @@ class DistributedGP:
             self.comm = None
 
     def __del__(self):
+        # with the peer-memory exchange, destroying a model is collective (no peer
+        # may still store into its panels): that needs an explicit close() on every
+        # rank, never a garbage-collection point that differs between ranks
+        if self.comm is not None and getattr(self.comm, "exchange", "collective") == "p2p":
+            return
         try:
             self.close()
         except Exception:  # noqa: BLE001 -- interpreter shutdown
