@@ -32,7 +32,9 @@ def _free_port():
 
 def _case(kind):
     rng = np.random.default_rng(11)
-    if kind == "padded":  # b = 100: n padded once to 640 (5 x 5 grid of 128)
+    if kind == "tiny":  # 2 x 2 tile grid: on a 2 x 2 process grid rank 1 owns no tile
+        n, t, d, m = 256, 2, 3, 9
+    elif kind == "padded":  # b = 100: n padded once to 640 (5 x 5 grid of 128)
         n, t, d, m = 600, 6, 3, 37
     else:  # b = 128, no padding (GPB_TILE=128 forces an 8 x 8 grid)
         n, t, d, m = 1024, 8, 4, 50
@@ -95,7 +97,8 @@ def _interp_rank(rank, world, grid, kind, exchange=0):
 @pytest.mark.parametrize("world,grid,kind,exchange", [
     (1, (1, 1), "dense", 0), (2, (1, 2), "padded", 0), (2, (2, 1), "dense", 0), (3, (1, 3), "padded", 0),
     (4, (2, 2), "dense", 0), (4, (2, 2), "padded", 0),
-    (2, (1, 2), "dense", 1), (2, (2, 1), "padded", 1), (4, (2, 2), "dense", 1), (3, (1, 3), "padded", 1)])
+    (2, (1, 2), "dense", 1), (2, (2, 1), "padded", 1), (4, (2, 2), "dense", 1), (3, (1, 3), "padded", 1),
+    (4, (2, 2), "tiny", 0), (4, (2, 2), "tiny", 1)])
 def test_schedule_ir_against_oracle_cpu(world, grid, kind, exchange):
     """Every rank's operation lists (factor, solves, gradient) replayed on CPU
     with gloo collectives reproduce the oracle; every rank ends with the same
@@ -230,7 +233,7 @@ def _check_device(res, kind):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,grid,kind", [(2, (1, 2), "padded"), (2, (2, 1), "dense"), (4, (2, 2), "dense"),
-                                             (3, (1, 3), "padded")])
+                                             (3, (1, 3), "padded"), (4, (2, 2), "tiny")])
 def test_device_executor_host_collectives_one_gpu(world, grid, kind):
     _check_device(_spawn("_device_rank", world, grid, kind, "host"), kind)
 
@@ -244,6 +247,47 @@ def test_device_executor_peer_memory_exchange_one_gpu(world, grid, kind):
     no kernel waits on another rank's kernel).  The factor stays bitwise the
     single-GPU one."""
     _check_device(_spawn("_device_rank", world, grid, kind, "host", "p2p"), kind)
+
+
+def _not_pd_rank(rank, world, grid):
+    import paper_2505_00136_b200 as gpb
+    from paper_2505_00136_b200.distributed import DistributedGP
+
+    rng = np.random.default_rng(3)
+    z = rng.normal(size=(512, 2))
+    z[1] = z[0]  # duplicate point, no noise: the second pivot is exactly 1 - 1 = 0 (rank 0's tile)
+    rt = gpb.start_runtime(gpb.RuntimeConfig(device=0))
+    try:
+        model = DistributedGP(gpb.Dataset(z, rng.normal(size=512)), gpb.KernelParams(1.0, 1.0, 0.0), 4, grid=grid,
+                              transport="host")
+        try:
+            model.log_likelihood()
+            raised = None
+        except gpb.errors.NotPositiveDefinite as exc:
+            raised = str(exc)
+        model.params = gpb.KernelParams(1.0, 1.0, 0.1)  # the cache was invalidated: a valid refactor works
+        ll = model.log_likelihood()
+        model.close()
+        return raised, ll
+    finally:
+        rt.stop()
+
+
+@pytest.mark.gpu
+def test_device_executor_not_positive_definite_on_every_rank():
+    """A failing pivot on one rank is reported as NotPositiveDefinite on every
+    rank (smallest failing index over the ranks, model.py:210-217), and the
+    model recovers after a parameter change."""
+    from oracle.tiled_gp import OracleGP
+
+    res = _spawn("_not_pd_rank", 2, (1, 2))
+    assert all(r[0] is not None and "non-positive pivot" in r[0] for r in res)
+    assert res[0][0] == res[1][0]
+    rng = np.random.default_rng(3)
+    z = rng.normal(size=(512, 2))
+    z[1] = z[0]
+    ll_o = OracleGP(z, rng.normal(size=512), 4, 1.0, 1.0, 0.1).log_likelihood()
+    assert all(abs(r[1] - ll_o) <= 1e-9 * abs(ll_o) for r in res)
 
 
 @pytest.mark.gpu
