@@ -202,7 +202,11 @@ struct gpb_model {
   // gradient
   DevBuf X, Kinv, part_l, part_v, part_x, inv_jobs;
   DevBuf gp_panel, gp_h, gp_jobs, gp_tiles;  // column-panel gradient terms (multi-GPU split)
-  std::vector<int64_t> invw_off, invx_off, invd_off;  // U_k (j < k), F_k, U_k (j = k)
+  std::vector<int64_t> invx_off;            // F_k
+  std::vector<int64_t> urow_off, urow_cnt;  // U_k on row k + 1 (the lookahead row)
+  std::vector<int64_t> urest_off, urest_cnt;  // U_k on rows > k + 1
+  std::vector<double> urow_fl, urest_fl;
+  std::vector<cudaEvent_t> grad_ev;         // [k] X(k, .) final (crit), [Ti + k] U_k rows > k+1 (main)
   double kinv_fl = 0.0;
   int64_t kinv_off = 0, kinv_cnt = 0;
   bool inv_plan = false;
@@ -760,13 +764,41 @@ int build_inv_plan(gpb_model* m) {
   // X = L^-1 right-looking, with the K^-1 buffer as the accumulator
   // A(i, j) = -sum_{m=j}^{i-1} L(i, m) X(m, j):
   //   F_k: X(k, j) = Dinv_k A(k, j), j < k (row block r needs k < (r+1)*128)
-  //   U_k: A(i, j) -= L(i, k) X(k, j), i > k, j <= k -- one launch of
-  //        (T-1-k)(k+1) equal K = bi tile products
+  //   U_k: A(i, j) -= L(i, k) X(k, j), i > k, j <= k, one job per 128-column
+  //        block of the output (K = bi; for j = k, X(k, k) = Dinv_k is lower
+  //        triangular, so column block cb needs only K = bi - cb*128)
+  // U_k is split into the lookahead row i = k + 1 (critical stream, followed by
+  // F_{k+1}) and the rows i > k + 1 (main stream), like the factorisation
   // (the left-looking form put a K = i*bi job next to K = bi ones in one
   // launch: at config 1 the long jobs left most SMs idle)
-  m->invw_off.assign(Ti + 1, 0);  // U_k, j < k
-  m->invx_off.assign(Ti + 1, 0);  // F_k
-  m->invd_off.assign(Ti + 1, 0);  // U_k, j = k
+  m->invx_off.assign(Ti + 1, 0);
+  m->urow_off.assign(Ti + 1, 0);
+  m->urow_cnt.assign(Ti + 1, 0);
+  m->urest_off.assign(Ti + 1, 0);
+  m->urest_cnt.assign(Ti + 1, 0);
+  m->urow_fl.assign(Ti + 1, 0.0);
+  m->urest_fl.assign(Ti + 1, 0.0);
+  const int nbk = m->bi / GBN;
+  auto add_u = [&](int k, int i, double* fl) {
+    for (int j = 0; j <= k; ++j)
+      for (int cb = 0; cb < nbk; ++cb) {
+        const int64_t o = int64_t(cb) * GBN;
+        GemmJob g{};
+        if (j < k) {
+          g.A = L + h_tri_rm(i, k) * bi2;
+          g.B = X + h_tri_cm(k, j, Ti) * bi2 + o;
+          g.Cin = g.Cout = Kv + h_tri_cm(i, j, Ti) * bi2 + o;
+          g.K = m->bi;
+        } else {
+          g.A = L + h_tri_rm(i, k) * bi2 + o;
+          g.B = X + h_tri_cm(k, k, Ti) * bi2 + o * m->bi + o;
+          g.Cin = g.Cout = Kv + h_tri_cm(i, k, Ti) * bi2 + o;
+          g.K = m->bi - static_cast<int>(o);
+        }
+        jobs.push_back(g);
+        *fl += 2.0 * GBM * GBN * double(g.K) * (m->bi / GBM);
+      }
+  };
   for (int k = 0; k < Ti; ++k) {
     m->invx_off[k] = jobs.size();
     for (int j = 0; j < k; ++j)
@@ -778,29 +810,17 @@ int build_inv_plan(gpb_model* m) {
         g.K = (r + 1) * GBM;
         jobs.push_back(g);
       }
-    m->invw_off[k] = jobs.size();
-    for (int i = k + 1; i < Ti; ++i)
-      for (int j = 0; j < k; ++j) {
-        GemmJob g{};
-        g.A = L + h_tri_rm(i, k) * bi2;
-        g.B = X + h_tri_cm(k, j, Ti) * bi2;
-        g.Cin = g.Cout = Kv + h_tri_cm(i, j, Ti) * bi2;
-        g.K = m->bi;
-        jobs.push_back(g);
-      }
-    // j = k: X(k, k) = Dinv_k is lower triangular, so output column block cb
-    // only needs k >= cb*128 -- one job per column block, K = bi - cb*128
-    m->invd_off[k] = jobs.size();
-    for (int i = k + 1; i < Ti; ++i)
-      for (int cb = 0; cb < m->bi / GBM; ++cb) {
-        const int64_t o = int64_t(cb) * GBM;
-        GemmJob g{};
-        g.A = L + h_tri_rm(i, k) * bi2 + o;
-        g.B = X + h_tri_cm(k, k, Ti) * bi2 + o * m->bi + o;
-        g.Cin = g.Cout = Kv + h_tri_cm(i, k, Ti) * bi2 + o;
-        g.K = m->bi - static_cast<int>(o);
-        jobs.push_back(g);
-      }
+    m->urow_off[k] = jobs.size();
+    if (k + 1 < Ti) add_u(k, k + 1, &m->urow_fl[k]);
+    m->urow_cnt[k] = jobs.size() - m->urow_off[k];
+    m->urest_off[k] = jobs.size();
+    for (int i = k + 2; i < Ti; ++i) add_u(k, i, &m->urest_fl[k]);
+    m->urest_cnt[k] = jobs.size() - m->urest_off[k];
+  }
+  while (m->grad_ev.size() < size_t(2 * Ti + 1)) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    m->grad_ev.push_back(e);
   }
   // K^-1(r, c) = sum_{k >= r} X(k, r)^T X(k, c), one job per 128-row block rb
   // of the output: X(r, r) is lower triangular, so the k sum starts at row
@@ -842,34 +862,39 @@ int loss_gradients(gpb_model* m, double out[3]) {
   double* D = m->Dinv.as<double>();
   const GemmJob* jobs = m->inv_jobs.as<GemmJob>();
   PhaseTimer pt(m, 5);
-  // X = L^-1 (tiled.py:263-298 with the identity RHS, model.py:358-361)
+  // X = L^-1 (tiled.py:263-298 with the identity RHS, model.py:358-361),
+  // with a one-row lookahead on the critical stream (build_inv_plan)
   for (int i = 0; i < Ti; ++i)
     CUDA_TRY(cudaMemcpyAsync(X + h_tri_cm(i, i, Ti) * bi2, D + int64_t(i) * bi2,
                              sizeof(double) * bi2, cudaMemcpyDeviceToDevice, m->st));
   CUDA_TRY(cudaMemsetAsync(m->Kinv.p, 0, sizeof(double) * ntiles * bi2, m->st));
+  cudaEvent_t* ev_x = m->grad_ev.data();       // [k]: X(k, .) final
+  cudaEvent_t* ev_u = m->grad_ev.data() + Ti;  // [k]: U_k applied to rows > k + 1
+  CUDA_TRY(cudaEventRecord(ev_x[0], m->st));   // X(0, 0) = Dinv_0
+  CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_x[0], 0));
+  auto ugemm = [&](int64_t off, int64_t cnt, double fl, cudaStream_t s) -> int {
+    if (cnt == 0) return GPB_OK;
+    GemmParams u = views(base_params(jobs + off, static_cast<int>(cnt), nb, 1, bi, bi, bi, -1.0, 1.0), m->L, m->X);
+    u.max_k = bi;
+    return gemm(m, u, true, false, EPI_AXPBY, fl, s);
+  };
   for (int k = 0; k < Ti; ++k) {
-    if (k > 0) {
-      GemmParams f = views(base_params(jobs + m->invx_off[k], k * nb, 1, nb, bi, bi, bi, 1.0, 0.0), m->Dinv,
-                           m->Kinv);
-      GPB_TRY(gemm(m, f, true, false, EPI_AXPBY,
-                   gemm_flops(int64_t(k) * nb, int64_t(GBM) * nb * (nb + 1) / 2)));
-    }
-    const int64_t nu = int64_t(Ti - 1 - k) * k;  // U_k tile products, j < k
-    if (nu > 0) {
-      GemmParams u = views(base_params(jobs + m->invw_off[k], static_cast<int>(nu), nb, nb, bi, bi, bi, -1.0, 1.0),
-                           m->L, m->X);
-      u.max_k = bi;
-      GPB_TRY(gemm(m, u, true, false, EPI_AXPBY, gemm_flops(nu * nb * nb, bi)));
-    }
-    const int64_t nd = int64_t(Ti - 1 - k) * nb;  // j = k, one job per column block
-    if (nd > 0) {
-      GemmParams u = views(base_params(jobs + m->invd_off[k], static_cast<int>(nd), nb, 1, bi, bi, bi, -1.0, 1.0),
-                           m->L, m->X);
-      u.max_k = bi;
-      GPB_TRY(gemm(m, u, true, false, EPI_AXPBY,
-                   gemm_flops(int64_t(Ti - 1 - k) * nb, int64_t(GBM) * nb * (nb + 1) / 2)));
+    // main: the bulk of U_k (rows > k + 1) once row k of X is final
+    CUDA_TRY(cudaStreamWaitEvent(m->st, ev_x[k], 0));
+    GPB_TRY(ugemm(m->urest_off[k], m->urest_cnt[k], m->urest_fl[k], m->st));
+    CUDA_TRY(cudaEventRecord(ev_u[k], m->st));
+    if (k + 1 < Ti) {
+      // critical: row k + 1 (it already has U_0 .. U_{k-1} from the main stream), then F_{k+1}
+      if (k >= 1) CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_u[k - 1], 0));
+      GPB_TRY(ugemm(m->urow_off[k], m->urow_cnt[k], m->urow_fl[k], m->crit));
+      GemmParams f = views(base_params(jobs + m->invx_off[k + 1], (k + 1) * nb, 1, nb, bi, bi, bi, 1.0, 0.0),
+                           m->Dinv, m->Kinv);
+      GPB_TRY(gemm(m, f, true, false, EPI_AXPBY, gemm_flops(int64_t(k + 1) * nb, int64_t(GBM) * nb * (nb + 1) / 2),
+                   m->crit));
+      CUDA_TRY(cudaEventRecord(ev_x[k + 1], m->crit));
     }
   }
+  CUDA_TRY(cudaStreamWaitEvent(m->st, ev_x[Ti - 1], 0));
 
   double* red = m->red.as<double>();
   const int64_t nblk = ntiles * (bi / kSekBlock) * (bi / kSekBlock);
@@ -1397,6 +1422,7 @@ int gpb_model_destroy(gpb_model* m) {
   free_model(m, live);
   for (cudaEvent_t e : m->evpool) cudaEventDestroy(e);
   for (cudaEvent_t e : m->sync_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : m->grad_ev) cudaEventDestroy(e);
   if (m->prof_ref) cudaEventDestroy(m->prof_ref);
   if (m->crit) cudaStreamDestroy(m->crit);
   if (m->e0) cudaEventDestroy(m->e0);
