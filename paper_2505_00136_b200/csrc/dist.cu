@@ -229,6 +229,7 @@ struct gpb_dist {
   gpb_ctx* ctx = nullptr;
   int rank = 0, world = 1, P = 1, Q = 1;
   int exchange = 0;  // gpb_dist_set_exchange: 0 collectives, 1 peer memory
+  int models = 0;    // live models (finalize refuses while any remains)
   Transport* tr = nullptr;
 };
 
@@ -932,6 +933,8 @@ int gpb_dist_set_exchange(gpb_dist* dc, int mode) {
 
 int gpb_dist_finalize(gpb_dist* dc) {
   if (!dc) return GPB_OK;
+  if (dc->models > 0)
+    return fail(GPB_INVALID_CONFIG, std::to_string(dc->models) + " model(s) still use this runtime: destroy them first");
   cudaDeviceSynchronize();
   delete dc->tr;
   delete dc;
@@ -1007,12 +1010,14 @@ int gpb_dist_model_create(gpb_dist* dc, const double* z, const double* y, int64_
     delete m;
     return s;
   }
+  ++dc->models;
   *out = m;
   return GPB_OK;
 }
 
 int gpb_dist_model_destroy(gpb_dmodel* m) {
   if (!m) return GPB_OK;
+  --m->dc->models;
   if (m->st) cudaStreamSynchronize(m->st);
   if (m->crit) cudaStreamSynchronize(m->crit);
   teardown_p2p(m);
