@@ -201,12 +201,13 @@ int dist_layout(int rank, int world, int P, int Q, int64_t n, int64_t T, DistLay
   L.bufsz[GPB_BUF_VEC] = L.vec[V_RED] + 32;
   L.bufsz[GPB_BUF_X] = nown * bi2;
   L.bufsz[GPB_BUF_KINV] = nown * bi2;
-  L.bufsz[GPB_BUF_XCOL] = P > 1 ? int64_t((Ti + Q - 1) / Q) * bi2 : 0;
-  L.bufsz[GPB_BUF_XROW] = Q > 1 ? int64_t(Q) * std::max(1, L.cntx) * bi2 : 0;
-  L.bufsz[GPB_BUF_LCOL] = Q > 1 ? int64_t(L.rows_per) * bi2 : 0;
+  // gradient exchange buffers: two sets (row k + 1 is published while step k reads row k)
+  L.bufsz[GPB_BUF_XCOL] = P > 1 ? 2 * int64_t((Ti + Q - 1) / Q) * bi2 : 0;
+  L.bufsz[GPB_BUF_XROW] = Q > 1 ? 2 * int64_t(Q) * std::max(1, L.cntx) * bi2 : 0;
+  L.bufsz[GPB_BUF_LCOL] = Q > 1 ? 2 * int64_t(L.rows_per) * bi2 : 0;
   const int ng = static_cast<int>(chol_group_sizes(Ti, L.G).size());
   L.p2p = exchange == 1 && world > 1;
-  L.nevents = 3 * ng + 2;
+  L.nevents = std::max(3 * ng + 2, 2 * Ti + 1);  // factorisation / gradient schedules
   return GPB_OK;
 }
 
@@ -534,17 +535,20 @@ void plan_solve(const DistLayout& L, Builder& b) {
 // ---- phase 2: gradient terms (model.py:341-435) ----------------------------
 // X = L^-1 right-looking with the K^-1 buffer as the accumulator
 // A(i, j) = -sum_{m=j}^{i-1} L(i, m) X(m, j), and K^-1 = X^T X in outer-product
-// form, both on the block-cyclic tiles.  Step k:
+// form, both on the block-cyclic tiles.  Row k of X is "published" by:
 //   F_k (process row k mod P): X(k, j) = Dinv_k A(k, j), j < k; X(k, k) = Dinv_k;
-//   row k of X down the process columns (root k mod P) and L(:, k) along the
-//     process rows (root k mod Q);
-//   U_k: A(i, j) -= L(i, k) X(k, j), i > k, j <= k;
-//   row k of X along the process rows (roots: rank (p, r mod Q) for tile r);
+//   row k of X down the process columns (root k mod P), L(:, k) along the
+//   process rows (root k mod Q), row k of X along the process rows (roots:
+//   rank (p, r mod Q) for tile r)  -- into exchange set k mod 2.
+// Step k then applies, on the main stream,
+//   U_k: A(i, j) -= L(i, k) X(k, j) for the rank's tiles i > k + 1, j <= k;
 //   LAUUM_k: K^-1(r, c) += X(k, r)^T X(k, c), c <= r <= k (written, not
-//     accumulated, at r == k: that slot's A(k, c) was consumed by F_k).
-// Then the fused trace pass over each rank's K^-1 tiles and an all-reduce of
-// the three partial sums.  No rank ever holds more than its own tiles plus one
-// tile row / column of X and L.
+//     accumulated, at r == k: that slot's A(k, c) was consumed by F_k),
+// while the critical stream runs U_k on row k + 1 and publishes row k + 1
+// (one-row lookahead, as in the single-GPU gradient).  Then the fused trace
+// pass over each rank's K^-1 tiles and an all-reduce of the three partial
+// sums.  No rank ever holds more than its own tiles plus two tile rows /
+// columns of X and L.
 void plan_gradient(const DistLayout& L, Builder& b) {
   const int Ti = L.Ti, bi = L.bi, nb = bi / kBlk, P = L.P, Q = L.Q;
   const int64_t bi2 = L.bi2;
@@ -552,18 +556,53 @@ void plan_gradient(const DistLayout& L, Builder& b) {
   auto xt = [&](int i, int j) { return Ref{GPB_BUF_X, int64_t(slot(i, j)) * bi2}; };
   auto kt = [&](int i, int j) { return Ref{GPB_BUF_KINV, int64_t(slot(i, j)) * bi2}; };
   auto add = [](Ref r, int64_t o) { return Ref{r.buf, r.off + o}; };
-  b.zero(MAIN, {GPB_BUF_KINV, 0}, int64_t(L.nown()) * bi2);
-  for (int k = 0; k < Ti; ++k) {
-    // X(k, j) as the B operand on this rank (j mod Q == my_q, j <= k)
-    auto xk = [&](int j) { return P == 1 ? xt(k, j) : Ref{GPB_BUF_XCOL, int64_t(j / Q) * bi2}; };
-    // X(k, r) as the A operand (r mod P == my_p, r <= k)
-    auto xr = [&](int r) {
-      return Q == 1 ? xk(r) : Ref{GPB_BUF_XROW, (int64_t(r % Q) * L.cntx + L.rpos[r]) * bi2};
-    };
-    // L(i, k) as the A operand (i mod P == my_p, i > k)
-    auto lc = [&](int i) {
-      return Q == 1 ? Ref{GPB_BUF_L, int64_t(slot(i, k)) * bi2} : Ref{GPB_BUF_LCOL, int64_t(i / P) * bi2};
-    };
+  const int64_t xcol_set = L.bufsz[GPB_BUF_XCOL] / 2, xrow_set = L.bufsz[GPB_BUF_XROW] / 2,
+                lcol_set = L.bufsz[GPB_BUF_LCOL] / 2;
+  // X(k, j) as the B operand on this rank (j mod Q == my_q, j <= k)
+  auto xk = [&](int k, int j) {
+    return P == 1 ? xt(k, j) : Ref{GPB_BUF_XCOL, (k % 2) * xcol_set + int64_t(j / Q) * bi2};
+  };
+  // X(k, r) as the A operand (r mod P == my_p, r <= k)
+  auto xr = [&](int k, int r) {
+    return Q == 1 ? xk(k, r)
+                  : Ref{GPB_BUF_XROW, (k % 2) * xrow_set + (int64_t(r % Q) * L.cntx + L.rpos[r]) * bi2};
+  };
+  // L(i, k) as the A operand (i mod P == my_p, i > k)
+  auto lc = [&](int k, int i) {
+    return Q == 1 ? Ref{GPB_BUF_L, int64_t(slot(i, k)) * bi2}
+                  : Ref{GPB_BUF_LCOL, (k % 2) * lcol_set + int64_t(i / P) * bi2};
+  };
+  const int ev_zero = 0;
+  auto ev_x = [&](int k) { return 1 + k; };       // row k of X published (critical stream)
+  auto ev_u = [&](int k) { return 1 + Ti + k; };  // step k applied to rows > k + 1 (main stream)
+  auto copy_op = [&](int stream) {
+    gpb_op o = b.base(GPB_OP_COPY, stream);
+    o.count = bi2;
+    b.close(o);
+  };
+  // U_k on the rank's tiles of rows [ilo, ihi): A(i, j) -= L(i, k) X(k, j), j <= k
+  auto update = [&](int stream, int k, int ilo, int ihi) {
+    b.begin();
+    for (int s = 0; s < L.nown(); ++s) {
+      const int i = L.own_i[s], j = L.own_j[s];
+      if (i >= ilo && i < ihi && j < k) b.job(lc(k, i), xk(k, j), kt(i, j), kt(i, j), bi, 0, i, j);
+    }
+    b.close(b.gemm(stream, nb, nb, bi, true, false, -1.0, 1.0));
+    // j = k: X(k, k) = Dinv_k is lower triangular, so output column block cb
+    // needs only k >= cb 128 (one job per column block, K = b - cb 128)
+    b.begin();
+    for (int i = std::max(ilo, k + 1); i < ihi; ++i) {
+      if (slot(i, k) < 0) continue;
+      for (int cb = 0; cb < nb; ++cb) {
+        const int64_t o = int64_t(cb) * kBlk;
+        b.job(add(lc(k, i), o), add(xk(k, k), o * bi + o), add(kt(i, k), o), add(kt(i, k), o),
+              bi - static_cast<int>(o), 0, i, k);
+      }
+    }
+    b.close(b.gemm(stream, nb, 1, bi, true, false, -1.0, 1.0));
+  };
+  // finalise row k of X on its process row and publish it with L(:, k) (exchange set k mod 2)
+  auto publish = [&](int k) {
     if (L.my_p == k % P) {
       // F_k: Dinv_k is lower triangular, so output row block r needs k < (r + 1) 128
       b.begin();
@@ -573,13 +612,11 @@ void plan_gradient(const DistLayout& L, Builder& b) {
           b.job({GPB_BUF_DINV, int64_t(k) * bi2 + int64_t(r) * kBlk * bi}, kt(k, j), kNone,
                 add(xt(k, j), int64_t(r) * kBlk * bi), (r + 1) * kBlk, 0, k, j);
       }
-      b.close(b.gemm(MAIN, 1, nb, bi, true, false, 1.0, 0.0));
+      b.close(b.gemm(CRIT, 1, nb, bi, true, false, 1.0, 0.0));
       if (L.rank == L.owner(k, k)) {
         b.begin();
         b.job({GPB_BUF_DINV, int64_t(k) * bi2}, kNone, kNone, xt(k, k));
-        gpb_op o = b.base(GPB_OP_COPY, MAIN);
-        o.count = bi2;
-        b.close(o);
+        copy_op(CRIT);
       }
     }
     if (P > 1) {  // row k of X down process column my_q (root: process row k mod P)
@@ -587,12 +624,10 @@ void plan_gradient(const DistLayout& L, Builder& b) {
       b.begin();
       for (int j = L.my_q; j <= k; j += Q) {
         ++cnt;
-        if (L.my_p == k % P) b.job(xt(k, j), kNone, kNone, {GPB_BUF_XCOL, int64_t(j / Q) * bi2});
+        if (L.my_p == k % P) b.job(xt(k, j), kNone, kNone, xk(k, j));
       }
-      gpb_op o = b.base(GPB_OP_COPY, MAIN);
-      o.count = bi2;
-      b.close(o);
-      b.coll(GPB_OP_BCAST, MAIN, COLG, k % P, {GPB_BUF_XCOL, 0}, int64_t(cnt) * bi2);
+      copy_op(CRIT);
+      b.coll(GPB_OP_BCAST, CRIT, COLG, k % P, xk(k, L.my_q), int64_t(cnt) * bi2);
     }
     if (Q > 1 && k + 1 < Ti) {  // L(:, k) along process row my_p (root: column k mod Q)
       int first = k + 1;
@@ -601,57 +636,54 @@ void plan_gradient(const DistLayout& L, Builder& b) {
       if (cnt > 0) {
         b.begin();
         if (L.my_q == k % Q)
-          for (int i = first; i < Ti; i += P) b.job({GPB_BUF_L, int64_t(slot(i, k)) * bi2}, kNone, kNone, lc(i));
-        gpb_op o = b.base(GPB_OP_COPY, MAIN);
-        o.count = bi2;
-        b.close(o);
-        b.coll(GPB_OP_BCAST, MAIN, ROWG, k % Q, lc(first), cnt * bi2);
+          for (int i = first; i < Ti; i += P) b.job({GPB_BUF_L, int64_t(slot(i, k)) * bi2}, kNone, kNone, lc(k, i));
+        copy_op(CRIT);
+        b.coll(GPB_OP_BCAST, CRIT, ROWG, k % Q, lc(k, first), cnt * bi2);
       }
     }
-    // U_k, j < k
-    b.begin();
-    for (int s = 0; s < L.nown(); ++s) {
-      const int i = L.own_i[s], j = L.own_j[s];
-      if (i > k && j < k) b.job(lc(i), xk(j), kt(i, j), kt(i, j), bi, 0, i, j);
-    }
-    b.close(b.gemm(MAIN, nb, nb, bi, true, false, -1.0, 1.0));
-    // U_k, j = k: X(k, k) = Dinv_k is lower triangular, so output column block
-    // cb needs only k >= cb 128 (one job per column block, K = b - cb 128)
-    b.begin();
-    for (int i = k + 1; i < Ti; ++i) {
-      if (slot(i, k) < 0) continue;
-      for (int cb = 0; cb < nb; ++cb) {
-        const int64_t o = int64_t(cb) * kBlk;
-        b.job(add(lc(i), o), add(xk(k), o * bi + o), add(kt(i, k), o), add(kt(i, k), o),
-              bi - static_cast<int>(o), 0, i, k);
-      }
-    }
-    b.close(b.gemm(MAIN, nb, 1, bi, true, false, -1.0, 1.0));
     if (Q > 1) {  // row k of X along process row my_p: tiles r = q' (mod Q) from rank (my_p, q')
       for (int qq = 0; qq < Q; ++qq) {
-        int cnt = 0;
+        int cnt = 0, first = -1;
         b.begin();
         for (int r = 0; r <= k; ++r) {
           if (r % P != L.my_p || r % Q != qq) continue;
+          if (first < 0) first = r;
           ++cnt;
-          if (L.my_q == qq) b.job(xk(r), kNone, kNone, xr(r));
+          if (L.my_q == qq) b.job(xk(k, r), kNone, kNone, xr(k, r));
         }
         if (cnt == 0) continue;
-        gpb_op o = b.base(GPB_OP_COPY, MAIN);
-        o.count = bi2;
-        b.close(o);
-        b.coll(GPB_OP_BCAST, MAIN, ROWG, qq, {GPB_BUF_XROW, int64_t(qq) * L.cntx * bi2}, int64_t(cnt) * bi2);
+        copy_op(CRIT);
+        b.coll(GPB_OP_BCAST, CRIT, ROWG, qq, xr(k, first), int64_t(cnt) * bi2);
       }
     }
+    b.record(CRIT, ev_x(k));
+  };
+
+  b.zero(MAIN, {GPB_BUF_KINV, 0}, int64_t(L.nown()) * bi2);
+  b.record(MAIN, ev_zero);
+  b.wait(CRIT, ev_zero);
+  publish(0);
+  for (int k = 0; k < Ti; ++k) {
+    // main: the bulk of step k once row k of X is published
+    b.wait(MAIN, ev_x(k));
+    update(MAIN, k, k + 2, Ti);
     // LAUUM_k: K^-1(r, c) (+)= X(k, r)^T X(k, c), both operands M/N-major
     for (int fresh = 1; fresh >= 0; --fresh) {
       b.begin();
       for (int s = 0; s < L.nown(); ++s) {
         const int r = L.own_i[s], c = L.own_j[s];
         if (r > k || (r == k) != (fresh == 1)) continue;
-        b.job(xr(r), xk(c), fresh ? kNone : kt(r, c), kt(r, c), bi, r == c, r, c);
+        b.job(xr(k, r), xk(k, c), fresh ? kNone : kt(r, c), kt(r, c), bi, r == c, r, c);
       }
       b.close(b.gemm(MAIN, nb, nb, bi, false, false, 1.0, fresh ? 0.0 : 1.0));
+    }
+    b.record(MAIN, ev_u(k));
+    if (k + 1 < Ti) {
+      // critical: row k + 1 has U_0 .. U_{k-1} from the main stream (and the main
+      // stream is done with exchange set (k + 1) mod 2); apply U_k to it, publish it
+      if (k >= 1) b.wait(CRIT, ev_u(k - 1));
+      update(CRIT, k, k + 1, k + 2);
+      publish(k + 1);
     }
   }
   b.begin();
