@@ -284,6 +284,7 @@ class DistributedGP:
                                                    opt.iterations, _lib.dptr(hist)))
         finally:
             self._sync_params()
+            self._collect_timings()
         return [float(v) for v in hist]
 
     def launch_count(self) -> int:
