@@ -1,7 +1,7 @@
 """Config 3 (n = 65536, T = 128) on the multi-GPU runtime with 2 ranks sharing
 one GPU (1x2 grid, host-staged collectives, peer-memory panel exchange): the
 full-size schedule end to end against the single-GPU model (loss, timings).
-Run: python tools/dist_c3_check.py [exchange]"""
+Run: python tools/dist_c3_check.py [exchange] [world]  (world 4: a 2x2 grid)"""
 import os
 import sys
 import time
@@ -38,15 +38,16 @@ def rank_main(rank, world, port, exchange, q):
 
 if __name__ == "__main__":
     exchange = sys.argv[1] if len(sys.argv) > 1 else "p2p"
+    world = int(sys.argv[2]) if len(sys.argv) > 2 else 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=rank_main, args=(r, 2, 29611, exchange, q)) for r in range(2)]
+    ps = [ctx.Process(target=rank_main, args=(r, world, 29611, exchange, q)) for r in range(world)]
     for p in ps:
         p.start()
     res = dict(q.get(timeout=1800) for _ in ps)
     for p in ps:
         p.join()
-    for r in (0, 1):
+    for r in range(world):
         print(f"rank {r}: ll {res[r]['ll']!r} wall {res[r]['wall']:.1f} s timings {res[r]['timings']}")
     rel = abs(res[0]["ll"] - res[0]["single"]) / abs(res[0]["single"])
-    print(f"single-GPU ll {res[0]['single']!r}; rel diff {rel:.2e}; ranks agree: {res[0]['ll'] == res[1]['ll']}")
+    print(f"single-GPU ll {res[0]['single']!r}; rel diff {rel:.2e}; ranks agree: {all(res[r]['ll'] == res[0]['ll'] for r in res)}")
