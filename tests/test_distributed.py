@@ -34,6 +34,8 @@ def _case(kind):
     rng = np.random.default_rng(11)
     if kind == "tiny":  # 2 x 2 tile grid: on a 2 x 2 process grid rank 1 owns no tile
         n, t, d, m = 256, 2, 3, 9
+    elif kind == "grid8":  # 12 x 12 tile grid for the 2 x 4 grid of an 8-GPU box (n padded 1500 -> 1536)
+        n, t, d, m = 1500, 12, 4, 20
     elif kind == "padded":  # b = 100: n padded once to 640 (5 x 5 grid of 128)
         n, t, d, m = 600, 6, 3, 37
     else:  # b = 128, no padding (GPB_TILE=128 forces an 8 x 8 grid)
@@ -98,7 +100,7 @@ def _interp_rank(rank, world, grid, kind, exchange=0):
     (1, (1, 1), "dense", 0), (2, (1, 2), "padded", 0), (2, (2, 1), "dense", 0), (3, (1, 3), "padded", 0),
     (4, (2, 2), "dense", 0), (4, (2, 2), "padded", 0),
     (2, (1, 2), "dense", 1), (2, (2, 1), "padded", 1), (4, (2, 2), "dense", 1), (3, (1, 3), "padded", 1),
-    (4, (2, 2), "tiny", 0), (4, (2, 2), "tiny", 1)])
+    (4, (2, 2), "tiny", 0), (4, (2, 2), "tiny", 1), (8, (2, 4), "grid8", 0), (8, (2, 4), "grid8", 1)])
 def test_schedule_ir_against_oracle_cpu(world, grid, kind, exchange):
     """Every rank's operation lists (factor, solves, gradient) replayed on CPU
     with gloo collectives reproduce the oracle; every rank ends with the same
