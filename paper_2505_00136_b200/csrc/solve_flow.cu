@@ -78,6 +78,19 @@ GPB_DEVINL void prefetch_rows(const double* p, int rows, int width, int64_t ld) 
   }
 }
 
+// L1 prefetch of this warp's part of a slice (rows of `width` doubles at stride ld):
+// the critical tile is read by one CTA per row slice with at most ~8 loads in
+// flight per lane (register cap of the co-resident grid), so from L2 its dot
+// costs ~8 us per block row; staged in L1 while the CTA waits for beta it is
+// read at L1 latency (the bulk loads are evict-first and do not displace it)
+GPB_DEVINL void prefetch_rows_l1(const double* p, int rows, int width, int64_t ld, int lane) {
+  const int lines = (width * 8 + 127) / 128;
+  for (int e = lane; e < rows * lines; e += 32) {
+    const char* q = reinterpret_cast<const char*>(p + static_cast<int64_t>(e / lines) * ld) + 128 * (e % lines);
+    asm volatile("prefetch.global.L1 [%0];\n" ::"l"(q));
+  }
+}
+
 // publish this CTA's stores: every thread's writes are fenced before the count
 GPB_DEVINL void signal_count(int* flag) {
   __threadfence();
@@ -95,6 +108,8 @@ struct FlowArgs {
   int* flags;          // 4T counters, zero on entry
   int T, bi, R;
   unsigned long long* prof;  // optional: 4T globaltimer stamps (GPB_SOLVE_PROF)
+  int pf;                    // steps ahead the critical tile is staged in L2 (GPB_FLOW_PREFETCH, default 2)
+  int l1;                    // stage the critical tile slices in L1 (GPB_FLOW_L1, default 1)
 };
 
 GPB_DEVINL unsigned long long gtimer() {
@@ -125,7 +140,10 @@ GPB_DEVINL int reduce8_row(int lane) { return ((lane >> 4) & 1) * 4 + ((lane >> 
 
 // p[k] += M[row k][lane's columns] . v  for the 8 rows of a group (row-major
 // M, ld = bi); diag: M is lower triangular, only columns <= row are read
-template <bool kDiag>
+// kL1: the rows were staged in L1 (critical tile): plain cached loads; otherwise
+// streaming (evict-first) loads.  All 8 loads of a chunk are issued before its
+// FMAs (the compiler would otherwise interleave them and keep ~3 in flight).
+template <bool kDiag, bool kL1 = false>
 GPB_DEVINL void rows8_dot(const double* M, int bi, int row0, const double2* v, int nchunk, int lane,
                           double (&p)[8]) {
 #pragma unroll 2
@@ -137,10 +155,11 @@ GPB_DEVINL void rows8_dot(const double* M, int bi, int row0, const double2* v, i
     for (int k = 0; k < 8; ++k) {
       const double2* r = reinterpret_cast<const double2*>(M + static_cast<int64_t>(row0 + k) * bi) + lane + 32 * c;
       if (!kDiag || col <= row0 + k)
-        x[k] = kDiag ? __ldcg(r) : __ldcs(r);
+        x[k] = kL1 ? __ldca(r) : (kDiag ? __ldcg(r) : __ldcs(r));
       else
         x[k] = make_double2(0.0, 0.0);
     }
+    asm volatile("" ::: "memory");
     const double2 vc = v[lane + 32 * c];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -168,7 +187,7 @@ __device__ void forward_slice(const FlowArgs& a, int i, int q, double2* vs) {
 #pragma unroll
   for (int g = 0; g < G; ++g) acc[g] = 0.0;
   for (int j = 0; j < i; ++j) {
-    if (j == i - 2 && threadIdx.x == 0)
+    if (j == i - a.pf && threadIdx.x == 0)
       prefetch_l2(a.L + tri_rm(i, i - 1) * bi2 + static_cast<int64_t>(q) * R * bi, sizeof(double) * R * bi);
     if (j == i - 1 && threadIdx.x == 0) {
       // the critical path of the solve runs through this slice from here on:
@@ -182,18 +201,25 @@ __device__ void forward_slice(const FlowArgs& a, int i, int q, double2* vs) {
       // late phase (few block rows left): stream this band through L2 ahead of
       // the loads, so the slice's rate is not bounded by its own load depth
       prefetch_l2(a.L + tri_rm(i, j) * bi2 + static_cast<int64_t>(q) * R * bi, sizeof(double) * R * bi);
+    if (j == i - 1 && a.l1)  // this warp's rows of the critical tile into L1 while beta_{i-1} is produced
+      prefetch_rows_l1(a.L + tri_rm(i, j) * bi2 + static_cast<int64_t>(rbase) * bi, RW, bi, bi, lane);
     wait_count(b_done + j, S, j == i - 1);  // (its __syncthreads also retires the previous vs)
     if (a.prof && j == i - 1 && q == 0 && threadIdx.x == 0) a.prof[4 * a.T + i] = gtimer();
     const double* tile = a.L + tri_rm(i, j) * bi2;
     const double2* bj = reinterpret_cast<const double2*>(a.beta + static_cast<int64_t>(j) * bi);
     for (int e = threadIdx.x; e < bi / 2; e += FT) vs[e] = __ldcg(bj + e);
     __syncthreads();
+    if (a.prof && j == i - 1 && q == 0 && threadIdx.x == 0) a.prof[6 * a.T + i] = gtimer();
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      rows8_dot<false>(tile, bi, rbase + 8 * g, vs, nchunk, lane, p);
+      if (j == i - 1 && a.l1)
+        rows8_dot<false, true>(tile, bi, rbase + 8 * g, vs, nchunk, lane, p);
+      else
+        rows8_dot<false>(tile, bi, rbase + 8 * g, vs, nchunk, lane, p);
       acc[g] += reduce8(p, lane);
     }
+    if (a.prof && j == i - 1 && q == 0 && threadIdx.x == 0) a.prof[7 * a.T + i] = gtimer();
   }
   const int64_t g0 = static_cast<int64_t>(i) * bi;
   if (i == 0 && threadIdx.x == 0)
@@ -229,7 +255,8 @@ __device__ void forward_slice(const FlowArgs& a, int i, int q, double2* vs) {
 // out[cols] += sum over `rows` rows r of M[r][cols] w[r] (ld = bi): lanes own
 // CPL adjacent columns (double2 loads), RPI rows per warp instruction; the
 // row weights come from w through warp shuffles (32 rows per load)
-template <int R, bool kStream>
+// kMode: 0 L2 (ldcg), 1 streaming (ldcs), 2 staged in L1 (ldca)
+template <int R, int kMode>
 GPB_DEVINL void cols_dot(const double* M, int bi, int r_first, int rows, const double* w, int col0,
                          int lane, double (&acc)[R / 32 > 2 ? R / 32 : 2]) {
   constexpr int CPL = R / 32 > 2 ? R / 32 : 2;  // columns per lane
@@ -246,8 +273,8 @@ GPB_DEVINL void cols_dot(const double* M, int bi, int r_first, int rows, const d
       const double* row = M + static_cast<int64_t>(r_first + rb + rr) * bi + col0 + cl * CPL;
 #pragma unroll
       for (int c = 0; c < CPL; c += 2) {
-        const double2 x = kStream ? __ldcs(reinterpret_cast<const double2*>(row + c))
-                                  : __ldcg(reinterpret_cast<const double2*>(row + c));
+        const double2* rp = reinterpret_cast<const double2*>(row + c);
+        const double2 x = kMode == 1 ? __ldcs(rp) : kMode == 2 ? __ldca(rp) : __ldcg(rp);
         acc[c] = fma(x.x, wk, acc[c]);
         acc[c + 1] = fma(x.y, wk, acc[c + 1]);
       }
@@ -304,7 +331,7 @@ __device__ void backward_slice(const FlowArgs& a, int i, int q, double* red) {
       prefetch_rows(a.L + tri_rm(j, i) * bi2 + col0, bi, R, bi);
     }
     wait_count(a_done + j, S, j == i + 1);
-    cols_dot<R, true>(a.L + tri_rm(j, i) * bi2, bi, r0, rows_w, a.alpha + static_cast<int64_t>(j) * bi + r0,
+    cols_dot<R, 1>(a.L + tri_rm(j, i) * bi2, bi, r0, rows_w, a.alpha + static_cast<int64_t>(j) * bi + r0,
                       col0, lane, acc);
   }
   if (i == a.T - 1) prefetch_rows(a.dinv + static_cast<int64_t>(i) * bi2 + col0, bi, R, bi);
@@ -324,8 +351,8 @@ __device__ void backward_slice(const FlowArgs& a, int i, int q, double* red) {
   for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
   const int lo = max(r0, col0 & ~31);  // rows above the slice's first column are zero
   if (lo < r0 + rows_w)
-    cols_dot<R, false>(a.dinv + static_cast<int64_t>(i) * bi2, bi, lo, r0 + rows_w - lo, a.xr + g0 + lo, col0,
-                       lane, acc);
+    cols_dot<R, 0>(a.dinv + static_cast<int64_t>(i) * bi2, bi, lo, r0 + rows_w - lo, a.xr + g0 + lo, col0, lane,
+                   acc);
   __syncthreads();  // red is reused
   cols_reduce<R>(acc, red, lane, warp);
   if (warp == 0 && lane < LPR)
@@ -391,11 +418,14 @@ cudaError_t launch_solve_flow(const double* L, const double* dinv, const double*
   static int prof_T = 0;
   if (getenv("GPB_SOLVE_PROF") && prof_T != T) {
     if (prof) cudaFree(prof);
-    cudaMalloc(&prof, sizeof(unsigned long long) * 6 * T);
-    cudaMemset(prof, 0, sizeof(unsigned long long) * 6 * T);
+    cudaMalloc(&prof, sizeof(unsigned long long) * 8 * T);
+    cudaMemset(prof, 0, sizeof(unsigned long long) * 8 * T);
     prof_T = T;
   }
-  FlowArgs a{L, dinv, y, beta, alpha, xr, flags, T, bi, R, getenv("GPB_SOLVE_PROF") ? prof : nullptr};
+  const char* pfe = getenv("GPB_FLOW_PREFETCH");
+  const char* l1e = getenv("GPB_FLOW_L1");
+  FlowArgs a{L, dinv, y, beta, alpha, xr, flags, T, bi, R, getenv("GPB_SOLVE_PROF") ? prof : nullptr,
+             pfe ? atoi(pfe) : 2, l1e ? atoi(l1e) : 1};
   cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * 4 * T, s);
   if (e != cudaSuccess) return e;
   const int nslices = T * (bi / R);
@@ -406,14 +436,17 @@ cudaError_t launch_solve_flow(const double* L, const double* dinv, const double*
     default: break;
   }
   if (a.prof && *launched) {  // per block row: r published, beta published, t published, alpha published
-    std::vector<unsigned long long> h(6 * T);
+    std::vector<unsigned long long> h(8 * T);
     cudaStreamSynchronize(s);
-    cudaMemcpy(h.data(), a.prof, sizeof(unsigned long long) * 6 * T, cudaMemcpyDeviceToHost);
+    cudaMemcpy(h.data(), a.prof, sizeof(unsigned long long) * 8 * T, cudaMemcpyDeviceToHost);
     const unsigned long long t0 = h[0];
     auto at = [&](unsigned long long v) { return v ? (double(v) - double(t0)) * 1e-3 : -1.0; };
     for (int i = 0; i < T; ++i)
-      fprintf(stderr, "flow row %3d: seen beta_{i-1} %8.1f r %8.1f all r %8.1f beta %8.1f | t %8.1f alpha %8.1f us\n",
-              i, at(h[4 * T + i]), at(h[i]), at(h[5 * T + i]), at(h[T + i]), at(h[2 * T + i]), at(h[3 * T + i]));
+      fprintf(stderr,
+              "flow row %3d: seen beta_{i-1} %8.1f loaded %8.1f dot %8.1f r %8.1f all r %8.1f beta %8.1f | t %8.1f "
+              "alpha %8.1f us\n",
+              i, at(h[4 * T + i]), at(h[6 * T + i]), at(h[7 * T + i]), at(h[i]), at(h[5 * T + i]), at(h[T + i]),
+              at(h[2 * T + i]), at(h[3 * T + i]));
   }
   return e;
 }
