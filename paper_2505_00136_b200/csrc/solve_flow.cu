@@ -201,8 +201,10 @@ __device__ void forward_slice(const FlowArgs& a, int i, int q, double2* vs) {
       // late phase (few block rows left): stream this band through L2 ahead of
       // the loads, so the slice's rate is not bounded by its own load depth
       prefetch_l2(a.L + tri_rm(i, j) * bi2 + static_cast<int64_t>(q) * R * bi, sizeof(double) * R * bi);
-    if (j == i - 1 && a.l1)  // this warp's rows of the critical tile into L1 while beta_{i-1} is produced
+    if (j == i - 1 && a.l1) {  // this warp's rows of the critical tile and of Dinv_i into L1
       prefetch_rows_l1(a.L + tri_rm(i, j) * bi2 + static_cast<int64_t>(rbase) * bi, RW, bi, bi, lane);
+      prefetch_rows_l1(a.dinv + static_cast<int64_t>(i) * bi2 + static_cast<int64_t>(rbase) * bi, RW, bi, bi, lane);
+    }
     wait_count(b_done + j, S, j == i - 1);  // (its __syncthreads also retires the previous vs)
     if (a.prof && j == i - 1 && q == 0 && threadIdx.x == 0) a.prof[4 * a.T + i] = gtimer();
     const double* tile = a.L + tri_rm(i, j) * bi2;
@@ -244,7 +246,7 @@ __device__ void forward_slice(const FlowArgs& a, int i, int q, double2* vs) {
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    rows8_dot<true>(D, bi, rbase + 8 * g, vs, nchunk, lane, p);
+    rows8_dot<true, true>(D, bi, rbase + 8 * g, vs, nchunk, lane, p);
     const double out = reduce8(p, lane);
     if ((lane & 3) == 0) a.beta[g0 + rbase + 8 * g + mine] = out;
   }
