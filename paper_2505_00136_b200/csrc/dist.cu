@@ -993,7 +993,7 @@ int gpb_dist_model_create(gpb_dist* dc, const double* z, const double* y, int64_
   dalloc(reinterpret_cast<void**>(&m->zp), sizeof(double) * L.np_ * d);
   dalloc(reinterpret_cast<void**>(&m->info), sizeof(int) * 4);
   dalloc(reinterpret_cast<void**>(&m->red), sizeof(double) * std::max(16, L.world));
-  dalloc(reinterpret_cast<void**>(&m->flow_flags), sizeof(int) * 4 * L.Ti);
+  dalloc(reinterpret_cast<void**>(&m->flow_flags), solve_flow_scratch_bytes(L.Ti, L.bi));
   dalloc(reinterpret_cast<void**>(&m->flow_x), sizeof(double) * L.np_);
   if (s == GPB_OK) step(ensure_buffers(m, {GPB_BUF_L, GPB_BUF_DINV, GPB_BUF_ROW, GPB_BUF_COL, GPB_BUF_VEC}));
   if (s == GPB_OK) {

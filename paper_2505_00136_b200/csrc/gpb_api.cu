@@ -701,10 +701,10 @@ int ensure_weights(gpb_model* m) {
   }
   if (m->flow_R > 0) {
     bool launched = false;
-    CUDA_TRY(m->flow_flags.ensure(sizeof(int) * 4 * Ti));
+    CUDA_TRY(m->flow_flags.ensure(solve_flow_scratch_bytes(Ti, bi)));
     {
       ProfScope ps(m, KC_SOLVE, 0.0);
-      CUDA_TRY(launch_solve_flow(L, D, m->yp.as<double>(), beta, alpha, yhat, m->flow_flags.as<int>(), Ti,
+      CUDA_TRY(launch_solve_flow(L, D, m->yp.as<double>(), beta, alpha, yhat, m->flow_flags.p, Ti,
                                  bi, m->flow_R, m->st, &launched));
     }
     if (launched) {

@@ -118,8 +118,9 @@ cudaError_t launch_bwd_update(const double* ltiles, int i, int bi, const double*
 // (0: the grid cannot be co-resident).  *launched = false: nothing was
 // launched and the caller must run the multi-launch solves.
 int solve_flow_slice_rows(int64_t np_, int bi);
+size_t solve_flow_scratch_bytes(int T, int bi);  // per-model scratch of launch_solve_flow
 cudaError_t launch_solve_flow(const double* L, const double* dinv, const double* y, double* beta,
-                              double* alpha, double* xr, int* flags, int T, int bi, int R,
+                              double* alpha, double* xr, void* scratch, int T, int bi, int R,
                               cudaStream_t s, bool* launched);
 // out[0] = sum_k logdiag[k] (sequential k), out[1] = sum x^2 (fixed order)
 cudaError_t launch_loss_terms(const double* logdiag, int T, const double* x, int64_t n,

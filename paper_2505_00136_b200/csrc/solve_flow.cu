@@ -105,11 +105,13 @@ struct FlowArgs {
   double* beta;        // n_p
   double* alpha;       // n_p
   double* xr;          // n_p exchange buffer (r of the forward, t of the backward)
-  int* flags;          // 4T counters, zero on entry
+  int* flags;          // 4T counters + T*S helper counters, zero on entry
+  double* part;        // helper partials of the critical tiles: [T][4][bi] (forward)
   int T, bi, R;
   unsigned long long* prof;  // optional: 4T globaltimer stamps (GPB_SOLVE_PROF)
   int pf;                    // steps ahead the critical tile is staged in L2 (GPB_FLOW_PREFETCH, default 2)
   int l1;                    // stage the critical tile slices in L1 (GPB_FLOW_L1, default 1)
+  int help;                  // helper quarters of the critical tiles (GPB_FLOW_HELP, default 1)
 };
 
 GPB_DEVINL unsigned long long gtimer() {
@@ -183,9 +185,19 @@ __device__ void forward_slice(const FlowArgs& a, int i, int q, double2* vs) {
   int* r_done = a.flags;
   int* b_done = a.flags + a.T;
   const int S = bi / R;
+  int* p_done = a.flags + 4 * a.T;  // [T][S]: helper quarters delivered for (block row, slice)
+  const int QC = bi / 4;            // columns of a quarter of the critical tile
   double acc[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) acc[g] = 0.0;
+  // Helpers: quarter h = 1..3 of the critical tile (i, i-1) of block row i (its
+  // columns [h QC, (h+1) QC)) is computed by slice q of block row i + h, which
+  // waits for beta_{i-1} anyway for its own tile (i + h, i - 1): the dot on the
+  // critical path shrinks to a quarter, spread over four CTAs
+  const int nhelp = a.help ? min(3, a.T - 1 - i) : 0;  // helpers row i gets
+  double crit[G], tail[G];  // own quarter 0; own quarters nhelp+1..3 (no helper below the last rows)
+#pragma unroll
+  for (int g = 0; g < G; ++g) crit[g] = tail[g] = 0.0;
   for (int j = 0; j < i; ++j) {
     if (j == i - a.pf && threadIdx.x == 0)
       prefetch_l2(a.L + tri_rm(i, i - 1) * bi2 + static_cast<int64_t>(q) * R * bi, sizeof(double) * R * bi);
@@ -212,6 +224,34 @@ __device__ void forward_slice(const FlowArgs& a, int i, int q, double2* vs) {
     for (int e = threadIdx.x; e < bi / 2; e += FT) vs[e] = __ldcg(bj + e);
     __syncthreads();
     if (a.prof && j == i - 1 && q == 0 && threadIdx.x == 0) a.prof[6 * a.T + i] = gtimer();
+    const int hh = i - 1 - j;  // this slice helps block row j + 1 with quarter hh
+    if (a.help && hh >= 1 && hh <= 3) {
+      const double* ct = a.L + tri_rm(j + 1, j) * bi2 + hh * QC;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        rows8_dot<false>(ct, bi, rbase + 8 * g, vs + hh * (QC / 2), QC / 64, lane, p);
+        const double out = reduce8(p, lane);
+        if ((lane & 3) == 0)
+          a.part[(static_cast<int64_t>(j + 1) * 4 + hh) * bi + rbase + 8 * g + reduce8_row(lane)] = out;
+      }
+      signal_count(p_done + (j + 1) * S + q);
+    }
+    if (j == i - 1 && a.help) {  // own critical tile: quarter 0 and the quarters without a helper
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        rows8_dot<false, true>(tile, bi, rbase + 8 * g, vs, QC / 64, lane, p);
+        crit[g] = reduce8(p, lane);
+        if (nhelp < 3) {
+          double pt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          rows8_dot<false, true>(tile + (nhelp + 1) * QC, bi, rbase + 8 * g, vs + (nhelp + 1) * (QC / 2),
+                                 (3 - nhelp) * QC / 64, lane, pt);
+          tail[g] = reduce8(pt, lane);
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -227,6 +267,17 @@ __device__ void forward_slice(const FlowArgs& a, int i, int q, double2* vs) {
   if (i == 0 && threadIdx.x == 0)
     prefetch_l2(a.dinv + static_cast<int64_t>(q) * R * bi, sizeof(double) * R * bi);
   const int mine = reduce8_row(lane);
+  if (a.help && i >= 1) {  // the critical tile's quarters, in a fixed order
+    if (nhelp > 0) wait_count(p_done + i * S + q, nhelp, true);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      double t = crit[g];
+      for (int h = 1; h <= 3; ++h)
+        t += h <= nhelp ? __ldcg(a.part + (static_cast<int64_t>(i) * 4 + h) * bi + rbase + 8 * g + mine)
+                        : (h == nhelp + 1 ? tail[g] : 0.0);
+      acc[g] += t;
+    }
+  }
   if ((lane & 3) == 0) {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -411,9 +462,16 @@ int solve_flow_slice_rows(int64_t np_, int bi) {
   return 0;
 }
 
+size_t solve_flow_scratch_bytes(int T, int bi) {
+  // helper partials [T][4][bi] doubles, then 4T + T (bi / 32) counters (the largest slice count)
+  return sizeof(double) * 4 * size_t(T) * bi + sizeof(int) * (4 * size_t(T) + size_t(T) * (bi / 32));
+}
+
 cudaError_t launch_solve_flow(const double* L, const double* dinv, const double* y, double* beta,
-                              double* alpha, double* xr, int* flags, int T, int bi, int R,
+                              double* alpha, double* xr, void* scratch, int T, int bi, int R,
                               cudaStream_t s, bool* launched) {
+  double* part = static_cast<double*>(scratch);
+  int* flags = reinterpret_cast<int*>(part + 4 * size_t(T) * bi);
   *launched = false;
   if (R == 0 || bi % R != 0 || bi % 64 != 0 || bi > 512) return cudaSuccess;
   static unsigned long long* prof = nullptr;
@@ -426,9 +484,10 @@ cudaError_t launch_solve_flow(const double* L, const double* dinv, const double*
   }
   const char* pfe = getenv("GPB_FLOW_PREFETCH");
   const char* l1e = getenv("GPB_FLOW_L1");
-  FlowArgs a{L, dinv, y, beta, alpha, xr, flags, T, bi, R, getenv("GPB_SOLVE_PROF") ? prof : nullptr,
-             pfe ? atoi(pfe) : 2, l1e ? atoi(l1e) : 1};
-  cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * 4 * T, s);
+  const char* hle = getenv("GPB_FLOW_HELP");
+  FlowArgs a{L, dinv, y, beta, alpha, xr, flags, part, T, bi, R, getenv("GPB_SOLVE_PROF") ? prof : nullptr,
+             pfe ? atoi(pfe) : 2, l1e ? atoi(l1e) : 1, hle ? atoi(hle) : 1};
+  cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (4 * T + T * (bi / R)), s);
   if (e != cudaSuccess) return e;
   const int nslices = T * (bi / R);
   switch (R) {
