@@ -106,7 +106,7 @@ struct FlowArgs {
   double* alpha;       // n_p
   double* xr;          // n_p exchange buffer (r of the forward, t of the backward)
   int* flags;          // 4T counters + T*S helper counters, zero on entry
-  double* part;        // helper partials of the critical tiles: [T][4][bi] (forward)
+  double* part;        // helper partials of the critical tiles: [2][T][4][bi] (forward, backward)
   int T, bi, R;
   unsigned long long* prof;  // optional: 4T globaltimer stamps (GPB_SOLVE_PROF)
   int pf;                    // steps ahead the critical tile is staged in L2 (GPB_FLOW_PREFETCH, default 2)
@@ -372,9 +372,16 @@ __device__ void backward_slice(const FlowArgs& a, int i, int q, double* red) {
   int* t_done = a.flags + 2 * a.T;
   int* a_done = a.flags + 3 * a.T;
   const int S = bi / R;
-  double acc[CPL];
+  int* pb_done = a.flags + 4 * a.T + a.T * S;  // [T][S] helper quarters (backward)
+  double* partb = a.part + 4 * static_cast<int64_t>(a.T) * bi;
+  const int QR = bi / 4;  // rows of a quarter of the critical column slice
+  // Helpers, as in the forward: rows quarter h = 1..3 of the critical column
+  // slice of tile (i + 1, i) is computed by slice q of block row i - h, which
+  // waits for alpha_{i+1} anyway; its four warps split the quarter's rows
+  const int nhelp = a.help ? min(3, i) : 0;
+  double acc[CPL], crit[CPL], tail[CPL];
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
+  for (int c = 0; c < CPL; ++c) acc[c] = crit[c] = tail[c] = 0.0;
   wait_count(a.flags + a.T + i, S);  // beta_i complete (and r_i no longer read)
   for (int j = a.T - 1; j > i; --j) {
     if (j == i + 1) {  // critical from here on: stage the column slices in L2
@@ -384,12 +391,56 @@ __device__ void backward_slice(const FlowArgs& a, int i, int q, double* red) {
       prefetch_rows(a.L + tri_rm(j, i) * bi2 + col0, bi, R, bi);
     }
     wait_count(a_done + j, S, j == i + 1);
+    const int hh = j - 1 - i;  // this slice helps block row j - 1 with quarter hh
+    if (a.help && hh >= 1 && hh <= 3) {
+      double hacc[CPL];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) hacc[c] = 0.0;
+      const int rq = hh * QR + warp * (QR / FW);
+      cols_dot<R, 1>(a.L + tri_rm(j, j - 1) * bi2, bi, rq, QR / FW, a.alpha + static_cast<int64_t>(j) * bi + rq, col0,
+                     lane, hacc);
+      __syncthreads();  // red is reused
+      cols_reduce<R>(hacc, red, lane, warp);
+      if (warp == 0 && lane < LPR)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+          partb[(static_cast<int64_t>(j - 1) * 4 + hh) * bi + col0 + lane * CPL + c] = hacc[c];
+      signal_count(pb_done + (j - 1) * S + q);
+    }
+    if (j == i + 1 && a.help) {  // own critical slice: rows quarter 0 and the quarters without a helper
+      const int rq = warp * (QR / FW);
+      cols_dot<R, 1>(a.L + tri_rm(j, i) * bi2, bi, rq, QR / FW, a.alpha + static_cast<int64_t>(j) * bi + rq, col0,
+                     lane, crit);
+      if (nhelp < 3) {
+        const int nt = (3 - nhelp) * QR / FW, rt = (nhelp + 1) * QR + warp * nt;
+        cols_dot<R, 1>(a.L + tri_rm(j, i) * bi2, bi, rt, nt, a.alpha + static_cast<int64_t>(j) * bi + rt, col0,
+                       lane, tail);
+      }
+      continue;
+    }
     cols_dot<R, 1>(a.L + tri_rm(j, i) * bi2, bi, r0, rows_w, a.alpha + static_cast<int64_t>(j) * bi + r0,
                       col0, lane, acc);
   }
   if (i == a.T - 1) prefetch_rows(a.dinv + static_cast<int64_t>(i) * bi2 + col0, bi, R, bi);
   const int64_t g0 = static_cast<int64_t>(i) * bi;
+  __syncthreads();  // red is reused
   cols_reduce<R>(acc, red, lane, warp);
+  if (a.help && i + 1 < a.T) {  // the critical slice's quarters, in a fixed order
+    __syncthreads();
+    cols_reduce<R>(crit, red, lane, warp);
+    __syncthreads();
+    cols_reduce<R>(tail, red, lane, warp);
+    if (nhelp > 0) wait_count(pb_done + i * S + q, nhelp, true);
+    if (warp == 0 && lane < LPR)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        double t = crit[c];
+        for (int h = 1; h <= 3; ++h)
+          t += h <= nhelp ? __ldcg(partb + (static_cast<int64_t>(i) * 4 + h) * bi + col0 + lane * CPL + c)
+                          : (h == nhelp + 1 ? tail[c] : 0.0);
+        acc[c] += t;
+      }
+  }
   if (warp == 0 && lane < LPR)
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
@@ -463,15 +514,15 @@ int solve_flow_slice_rows(int64_t np_, int bi) {
 }
 
 size_t solve_flow_scratch_bytes(int T, int bi) {
-  // helper partials [T][4][bi] doubles, then 4T + T (bi / 32) counters (the largest slice count)
-  return sizeof(double) * 4 * size_t(T) * bi + sizeof(int) * (4 * size_t(T) + size_t(T) * (bi / 32));
+  // helper partials [2][T][4][bi] doubles, then 4T + 2 T (bi / 32) counters (the largest slice count)
+  return sizeof(double) * 8 * size_t(T) * bi + sizeof(int) * (4 * size_t(T) + 2 * size_t(T) * (bi / 32));
 }
 
 cudaError_t launch_solve_flow(const double* L, const double* dinv, const double* y, double* beta,
                               double* alpha, double* xr, void* scratch, int T, int bi, int R,
                               cudaStream_t s, bool* launched) {
   double* part = static_cast<double*>(scratch);
-  int* flags = reinterpret_cast<int*>(part + 4 * size_t(T) * bi);
+  int* flags = reinterpret_cast<int*>(part + 8 * size_t(T) * bi);
   *launched = false;
   if (R == 0 || bi % R != 0 || bi % 64 != 0 || bi > 512) return cudaSuccess;
   static unsigned long long* prof = nullptr;
@@ -484,10 +535,12 @@ cudaError_t launch_solve_flow(const double* L, const double* dinv, const double*
   }
   const char* pfe = getenv("GPB_FLOW_PREFETCH");
   const char* l1e = getenv("GPB_FLOW_L1");
+  // helpers split the critical tiles in quarters of bi / 4 = 128 columns / rows,
+  // i.e. 32 rows per warp (the 32-row chunks of cols_dot): bi = 512 only
   const char* hle = getenv("GPB_FLOW_HELP");
   FlowArgs a{L, dinv, y, beta, alpha, xr, flags, part, T, bi, R, getenv("GPB_SOLVE_PROF") ? prof : nullptr,
-             pfe ? atoi(pfe) : 2, l1e ? atoi(l1e) : 1, hle ? atoi(hle) : 1};
-  cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (4 * T + T * (bi / R)), s);
+             pfe ? atoi(pfe) : 2, l1e ? atoi(l1e) : 1, bi == 512 ? (hle ? atoi(hle) : 1) : 0};
+  cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (4 * T + 2 * T * (bi / R)), s);
   if (e != cudaSuccess) return e;
   const int nslices = T * (bi / R);
   switch (R) {
