@@ -139,8 +139,8 @@ class ClockSampler:
 
 def _ncu_traffic():
     """DRAM bytes per launch of the dominant kernel from the committed ncu
-    --set full capture (profiles/r01_gemm_traffic.json), or None."""
-    path = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
+    --set full capture (profiles/r02_gemm_traffic.json), or None."""
+    path = os.path.join(ROOT, "profiles", "r02_gemm_traffic.json")
     try:
         with open(path) as f:
             return json.load(f)["traffic_bytes_per_launch"]
@@ -436,7 +436,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                      "traffic": _ncu_traffic(),
                      "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the "
                                        "prediction-sweep GEMM from the committed ncu --set full capture "
-                                       "(profiles/r01_gemm_traffic.json), not measured in this run",
+                                       "(profiles/r02_gemm_traffic.json), not measured in this run",
                      "peak_source": "in-run FP64 DMMA probe (MEASURED_PEAKS.json has no FP64 entry)",
                      "achieved_executed_flops": gemm_tf_exec,
                      "achieved_basis": "algorithmic flops n^3/3 + n^2 m per step over the GEMM busy time: "
