@@ -257,6 +257,10 @@ int gpb_nccl_unique_id(void* id_out);  /* GPB_NCCL_ID_BYTES bytes */
 int gpb_dist_init(gpb_ctx* ctx, int rank, int world, int P, int Q, const void* nccl_id, gpb_dist** out);
 int gpb_dist_init_host(gpb_ctx* ctx, int rank, int world, int P, int Q, const gpb_host_coll* coll,
                        gpb_dist** out);
+/* Timing emulation: rank `rank` of the grid alone on this GPU, every collective a
+ * no-op (results are meaningless; the schedule's kernels run as they would on
+ * that rank).  Measures each rank's compute time when only one GPU is at hand. */
+int gpb_dist_init_emulate(gpb_ctx* ctx, int rank, int world, int P, int Q, gpb_dist** out);
 int gpb_dist_finalize(gpb_dist* dc);  /* GPB_INVALID_CONFIG while models of dc are alive */
 /* Panel exchange of the factorisation for models created afterwards:
  * 0 (default) collectives (row / column broadcasts); 1 peer memory -- the

@@ -108,6 +108,8 @@ SIGNATURES = {
                                      ctypes.POINTER(_vp)]),
     "gpb_dist_init_host": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp,
                                           ctypes.POINTER(_vp)]),
+    "gpb_dist_init_emulate": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                             ctypes.POINTER(_vp)]),
     "gpb_dist_finalize": (ctypes.c_int, [_vp]),
     "gpb_dist_model_create": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, ctypes.c_int64, ctypes.c_int64,
                                              ctypes.c_int64, ctypes.POINTER(_vp)]),
