@@ -22,7 +22,7 @@ rt = gpb.start_runtime()
 lib = _lib.load()
 
 
-def factor_ms(rank, world, p, q):
+def factor_ms(rank, world, p, q, grad=False):
     dc, m = ctypes.c_void_p(), ctypes.c_void_p()
     _lib.check(lib.gpb_dist_init_emulate(rt.handle, rank, world, p, q, ctypes.byref(dc)))
     _lib.check(lib.gpb_dist_model_create(dc, _lib.dptr(train.z), _lib.dptr(train.y), n, d, T, ctypes.byref(m)))
@@ -36,18 +36,31 @@ def factor_ms(rank, world, p, q):
             pass  # meaningless data; the schedule ran to the end
         t = (ctypes.c_double * 8)()
         lib.gpb_dist_timings(m, t, 8)
-        best = (t[1], t[2], t[6]) if best is None or t[1] < best[0] else best
+        g = None
+        if grad:
+            out = (ctypes.c_double * 3)()
+            lib.gpb_dist_loss_gradients(m, out)  # runs after the factor even if "not PD" (meaningless data)
+            tg = (ctypes.c_double * 8)()
+            lib.gpb_dist_timings(m, tg, 8)
+            g = tg[4]
+        best = (t[1], t[2], t[6], g) if best is None or t[1] < best[0] else best
     lib.gpb_dist_model_destroy(m)
     lib.gpb_dist_finalize(dc)
     return best
 
 
-t1, s1, _ = factor_ms(0, 1, 1, 1)
-print(f"config {cfg} (n={n}, T={T}): 1 GPU factor {t1:.1f} ms, solves {s1:.1f} ms", flush=True)
+grad = len(sys.argv) > 2 and sys.argv[2] == "grad"
+t1, s1, _, g1 = factor_ms(0, 1, 1, 1, grad)
+print(f"config {cfg} (n={n}, T={T}): 1 GPU factor {t1:.1f} ms, solves {s1:.1f} ms"
+      + (f", gradient {g1:.1f} ms" if grad else ""), flush=True)
 for p, q in [(1, 2), (2, 2), (2, 4)]:
     w = p * q
-    res = [factor_ms(r, w, p, q) for r in range(w)]
+    res = [factor_ms(r, w, p, q, grad) for r in range(w)]
     f = np.array([x[0] for x in res])
-    print(f"{p}x{q}: per-rank factor ms {np.round(f, 1).tolist()}; max {f.max():.1f} -> E <= "
-          f"{t1 / (w * f.max()):.3f}; host enqueue {np.mean([x[2] for x in res]):.1f} us/step", flush=True)
+    line = (f"{p}x{q}: per-rank factor ms {np.round(f, 1).tolist()}; max {f.max():.1f} -> E <= "
+            f"{t1 / (w * f.max()):.3f}; host enqueue {np.mean([x[2] for x in res]):.1f} us/step")
+    if grad:
+        gr = np.array([x[3] for x in res])
+        line += f"; gradient per rank max {gr.max():.1f} ms -> E <= {g1 / (w * gr.max()):.3f}"
+    print(line, flush=True)
 rt.stop()
