@@ -188,21 +188,41 @@ struct HostTransport : Transport {
   }
 };
 
+// stream-ordered delay of `ns` nanoseconds (one thread polls the global timer)
+__global__ void delay_kernel(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(200);
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
 // No data exchange at all: one rank's schedule run alone on a GPU to time its
-// own kernels (gpb_dist_init_emulate).  Results are meaningless.
+// own kernels (gpb_dist_init_emulate).  Results are meaningless.  With
+// GPB_EMU_LINK="latency_us,GB/s" every collective instead occupies its stream for
+// latency + bytes / bandwidth (a modelled NVLink transfer, no data moved).
 struct NullTransport : Transport {
-  int bcast(int, double*, int64_t, int, cudaStream_t) override {
+  double lat_ns = 0.0, gbs = 0.0;
+  NullTransport() {
+    if (const char* e = getenv("GPB_EMU_LINK")) {
+      double lat = 0.0, bw = 0.0;
+      if (sscanf(e, "%lf,%lf", &lat, &bw) == 2 && bw > 0.0) {
+        lat_ns = lat * 1e3;
+        gbs = bw;
+      }
+    }
+  }
+  int wait(int64_t bytes, cudaStream_t s) {
     ++calls;
+    if (gbs <= 0.0) return GPB_OK;
+    delay_kernel<<<1, 1, 0, s>>>(static_cast<unsigned long long>(lat_ns + double(bytes) / gbs));
+    DCUDA(cudaGetLastError());
     return GPB_OK;
   }
-  int reduce(int, double*, int64_t, int, cudaStream_t) override {
-    ++calls;
-    return GPB_OK;
-  }
-  int allreduce(int, double*, int64_t, cudaStream_t) override {
-    ++calls;
-    return GPB_OK;
-  }
+  int bcast(int, double*, int64_t count, int, cudaStream_t s) override { return wait(count * 8, s); }
+  int reduce(int, double*, int64_t count, int, cudaStream_t s) override { return wait(count * 8, s); }
+  int allreduce(int, double*, int64_t count, cudaStream_t s) override { return wait(2 * count * 8, s); }
 };
 
 struct CopyJob {
