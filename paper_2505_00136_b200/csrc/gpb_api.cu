@@ -335,6 +335,7 @@ int prof_collect(gpb_model* m) {
   if (m->recs.empty()) return GPB_OK;
   CUDA_TRY(cudaDeviceSynchronize());
   std::vector<std::pair<double, double>> iv[8];
+  FILE* dump = getenv("GPB_PROF_DUMP") ? fopen(getenv("GPB_PROF_DUMP"), "a") : nullptr;
   for (auto& r : m->recs) {
     float ms = 0, t0 = 0, t1 = 0;
     cudaEventElapsedTime(&ms, r.a, r.b);
@@ -344,7 +345,9 @@ int prof_collect(gpb_model* m) {
     if (m->prof_ref && cudaEventElapsedTime(&t0, m->prof_ref, r.a) == cudaSuccess &&
         cudaEventElapsedTime(&t1, m->prof_ref, r.b) == cudaSuccess)
       iv[r.cls].push_back({t0, t1});
+    if (dump) fprintf(dump, "%d %.4f %.4f %.4g\n", r.cls, t0, t1, r.flops);
   }
+  if (dump) fclose(dump);
   for (int c = 0; c < 8; ++c) {
     auto& v = iv[c];
     std::sort(v.begin(), v.end());
