@@ -129,6 +129,15 @@ int gpb_model_set_adam(gpb_model* m, const double moment1[3], const double momen
 int gpb_model_timings(gpb_model* m, double* ms_out, int n);
 /* launches of this library's kernels since the model was created */
 int gpb_model_launch_count(gpb_model* m, int64_t* out);
+
+/* tcgen05 digit-plane products (csrc/ozaki.cuh): the long-k products of the
+ * prediction sweep (tiled.py:263-298) on the int8 tensor pipe from `slices`
+ * signed 7-bit digit planes per operand (8: every kept term of the FP64
+ * product; 0: off, every product on the FP64 DMMA kernels).  The default is
+ * GPB_OZAKI (unset: 0).  `fallbacks` counts predictions repeated on the DMMA
+ * kernels because an operand exceeded its fixed-point scale. */
+int gpb_model_set_ozaki(gpb_model* m, int slices);
+int gpb_model_get_ozaki(gpb_model* m, int* slices, int64_t* fallbacks);
 /* the CUDA stream (cudaStream_t) the model's kernels run on */
 int gpb_model_stream(gpb_model* m, void** stream);
 /* per-kernel-class profiling with CUDA events around every launch:

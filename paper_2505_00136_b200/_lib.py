@@ -65,6 +65,8 @@ SIGNATURES = {
     "gpb_model_set_adam": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, ctypes.c_int64]),
     "gpb_model_timings": (ctypes.c_int, [_vp, _c_double_p, ctypes.c_int]),
     "gpb_model_launch_count": (ctypes.c_int, [_vp, _c_i64_p]),
+    "gpb_model_set_ozaki": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "gpb_model_get_ozaki": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int), _c_i64_p]),
     "gpb_model_stream": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
     "gpb_model_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),
     "gpb_model_kernel_stats": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, _c_i64_p]),

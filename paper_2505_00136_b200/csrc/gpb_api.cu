@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "gemm.cuh"
+#include "ozaki.cuh"
 #include "gpb200.h"
 #include "kernels.cuh"
 #include "plan_common.h"
@@ -215,6 +216,15 @@ struct gpb_model {
   DevBuf Bv, W, mpart, sq, pred_jobs, zt, mean, var, S, fc_jobs;
   int64_t pred_mcp = -1, fc_mcp = -1;
 
+  // tcgen05 digit-plane products (ozaki.cuh): planes of the off-diagonal L
+  // tiles (same packing as L) and of V^T (one row per test point)
+  DevBuf Ls, Vs, ozflag;
+  int oz_slices = 0;   // 0: every product on the DMMA kernels
+  bool ls_ok = false;  // Ls holds the planes of the current factor
+  double oz_sa = 0.0, oz_sb = 0.0;
+  int64_t oz_min_k = 2048;  // shorter products stay on the DMMA kernels
+  int64_t oz_fallbacks = 0;
+
   double adam_m[3] = {0, 0, 0}, adam_v[3] = {0, 0, 0};
   int64_t adam_step = 0;
   double timing[8] = {0};
@@ -293,7 +303,7 @@ GemmParams views(const GemmParams& p, const DevBuf& a, const DevBuf& b) {
   return views(p, a.p, a.bytes, b.p, b.bytes);
 }
 
-enum KernelClass { KC_GEMM = 0, KC_POTRF = 1, KC_SEK = 2, KC_SOLVE = 3, KC_OTHER = 4 };
+enum KernelClass { KC_GEMM = 0, KC_POTRF = 1, KC_SEK = 2, KC_SOLVE = 3, KC_OTHER = 4, KC_OZAKI = 5 };
 
 cudaEvent_t prof_event(gpb_model* m) {
   if (m->evnext == m->evpool.size()) {
@@ -549,6 +559,7 @@ int upload_train(gpb_model* m, const double* z, const double* y, bool device_ptr
 void invalidate(gpb_model* m) {
   m->factor_ok = false;
   m->weights_ok = false;
+  m->ls_ok = false;
 }
 
 struct PhaseTimer {
@@ -682,6 +693,7 @@ int ensure_factor(gpb_model* m) {
   m->last_pivot = -1;
   m->factor_ok = true;
   m->weights_ok = false;
+  m->ls_ok = false;
   return GPB_OK;
 }
 
@@ -1097,6 +1109,79 @@ int grad_partial(gpb_model* m, const int* cols, int ncols, double out[3]) {
 }
 
 // ---- prediction (model.py:221-314) ----------------------------------------
+// smallest power of two >= x
+double pow2_ceil(double x) { return std::exp2(std::ceil(std::log2(x))); }
+
+// Digit planes of the off-diagonal factor tiles.  |L(i, j)| <= sqrt(K_ii) =
+// sqrt(vertical + noise) (1 on the decoupled padding rows), so one
+// fixed-point scale covers the whole factor.
+int ensure_l_planes(gpb_model* m) {
+  if (m->ls_ok) return GPB_OK;
+  const int64_t bi2 = int64_t(m->bi) * m->bi;
+  const int64_t ntiles = int64_t(m->Ti) * (m->Ti + 1) / 2;
+  CUDA_TRY(m->Ls.ensure(size_t(m->oz_slices) * ntiles * bi2));
+  if (!m->ozflag.p) {
+    CUDA_TRY(m->ozflag.ensure(sizeof(int)));
+    CUDA_TRY(cudaMemsetAsync(m->ozflag.p, 0, sizeof(int), m->st));
+  }
+  m->oz_sa = pow2_ceil(2.0 * std::max(1.0, std::sqrt(m->nu + m->s2)) * (1.0 + 1e-9));
+  ProfScope ps(m, KC_OTHER, 0.0);
+  for (int i = 1; i < m->Ti; ++i) {
+    const int64_t off = h_tri_rm(i, 0) * bi2;
+    CUDA_TRY(launch_ozaki_slice(m->L.as<double>() + off, int64_t(i) * bi2, m->oz_sa, m->Ls.as<int8_t>() + off,
+                                ntiles * bi2, m->oz_slices, m->ozflag.as<int>(), m->st));
+    ++m->launches;
+  }
+  m->ls_ok = true;
+  return GPB_OK;
+}
+
+// W = B_i - L[i, 0..i) V[0..i) on the tcgen05 pipe, in k segments of at most
+// kOzakiMaxK (int32 group sums stay exact); *done = false: not launched
+int ozaki_pred_w(gpb_model* m, int i, int64_t mcp, bool* done) {
+  *done = false;
+  const int bi = m->bi;
+  const int64_t bi2 = int64_t(bi) * bi;
+  const int64_t ntiles = int64_t(m->Ti) * (m->Ti + 1) / 2;
+  const int64_t K = int64_t(i) * bi;
+  double* W = m->W.as<double>();
+  for (int64_t k0 = 0; k0 < K; k0 += kOzakiMaxK) {
+    OzakiGemm g{};
+    g.a_planes = m->Ls.as<int8_t>();
+    g.a_pitch = bi;
+    g.a_rows = ntiles * bi;
+    g.a_row0 = (h_tri_rm(i, 0) + k0 / bi) * bi;
+    g.a_ktile = bi;
+    g.a_kt_rows = bi;
+    g.b_planes = m->Vs.as<int8_t>();
+    g.b_pitch = m->np_;
+    g.b_rows = mcp;
+    g.b_row0 = 0;
+    g.b_col0 = k0;
+    g.M = bi;
+    g.N = static_cast<int>(mcp);
+    g.K = static_cast<int>(std::min<int64_t>(kOzakiMaxK, K - k0));
+    g.slices = m->oz_slices;
+    g.alpha = -m->oz_sa * m->oz_sb;
+    g.beta = 1.0;
+    g.Cin = k0 == 0 ? m->Bv.as<double>() + int64_t(i) * bi * mcp : W;
+    g.Cout = W;
+    g.ldc_in = g.ldc_out = mcp;
+    bool used = false;
+    {
+      ProfScope ps(m, KC_OZAKI, 2.0 * double(bi) * double(mcp) * double(g.K));
+      CUDA_TRY(launch_ozaki_gemm(g, m->st, &used));
+    }
+    if (!used) {
+      if (k0 == 0) return GPB_OK;  // no tensor maps: the caller runs the DMMA product
+      return fail(GPB_CUDA, "tensor-map encoding failed in the middle of a digit-plane product");
+    }
+    ++m->launches;
+  }
+  *done = true;
+  return GPB_OK;
+}
+
 int build_pred_plan(gpb_model* m, int64_t mcp) {
   if (m->pred_mcp == mcp) return GPB_OK;
   const int Ti = m->Ti, bi = m->bi;
@@ -1147,7 +1232,8 @@ int64_t pred_chunk(gpb_model* m, int64_t mt) {
   }
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  const double per_col = 8.0 * double(m->np_ + m->bi + m->np_ / kSekBlock + m->np_ / GBM + 4);
+  const double per_col = 8.0 * double(m->np_ + m->bi + m->np_ / kSekBlock + m->np_ / GBM + 4) +
+                         double(m->oz_slices) * double(m->np_);
   // cached blocks are returned to CUDA if an allocation would otherwise fail
   const double avail = double(free_b) + double(g_cache.cached) + double(m->Bv.bytes);
   const double budget = std::min(48e9, 0.6 * avail);
@@ -1175,15 +1261,27 @@ int predict_chunk(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var,
   if (want_var) {
     PhaseTimer pt(m, 4);
     const GemmJob* jobs = m->pred_jobs.as<GemmJob>();
+    // tcgen05 digit-plane products for the long-k rows (ozaki.cuh); |V| <=
+    // sqrt(k(x*, x*)) = sqrt(vertical) since k*^T K^-1 k* <= k**
+    const bool oz = m->oz_slices > 0 && int64_t(Ti - 1) * bi >= m->oz_min_k;
+    if (oz) {
+      GPB_TRY(ensure_l_planes(m));
+      CUDA_TRY(m->Vs.ensure(size_t(m->oz_slices) * mcp * m->np_));
+      m->oz_sb = pow2_ceil(2.0 * std::sqrt(m->nu) * (1.0 + 1e-9));
+    }
     for (int i = 0; i < Ti; ++i) {
-      GemmParams w = views(base_params(jobs + int64_t(i) * (1 + bi / GBM), 1, bi / GBM,
-                                       static_cast<int>(mcp / GBN), bi, mcp, mcp, -1.0, 1.0),
-                           m->L, m->Bv);
-      w.a_ktile = bi;
-      w.a_kstride = int64_t(bi) * bi;
-      w.max_k = int64_t(i) * bi;
-      const int64_t blocks = int64_t(bi / GBM) * (mcp / GBN);
-      GPB_TRY(gemm(m, w, true, false, EPI_AXPBY, gemm_flops(blocks, int64_t(i) * bi)));
+      bool done = false;
+      if (oz && int64_t(i) * bi >= m->oz_min_k) GPB_TRY(ozaki_pred_w(m, i, mcp, &done));
+      if (!done) {
+        GemmParams w = views(base_params(jobs + int64_t(i) * (1 + bi / GBM), 1, bi / GBM,
+                                         static_cast<int>(mcp / GBN), bi, mcp, mcp, -1.0, 1.0),
+                             m->L, m->Bv);
+        w.a_ktile = bi;
+        w.a_kstride = int64_t(bi) * bi;
+        w.max_k = int64_t(i) * bi;
+        const int64_t blocks = int64_t(bi / GBM) * (mcp / GBN);
+        GPB_TRY(gemm(m, w, true, false, EPI_AXPBY, gemm_flops(blocks, int64_t(i) * bi)));
+      }
       const int nbr = bi / GBM;
       GemmParams v = views(base_params(jobs + int64_t(i) * (1 + nbr) + 1, nbr, 1,
                                        static_cast<int>(mcp / GBN), bi, mcp, mcp, 1.0, 0.0),
@@ -1191,6 +1289,13 @@ int predict_chunk(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var,
       v.aux_ld = mcp;
       GPB_TRY(gemm(m, v, true, false, EPI_SUMSQ,
                    gemm_flops(mcp / GBN, int64_t(GBM) * nbr * (nbr + 1) / 2)));
+      if (oz && i + 1 < Ti) {  // planes of V_i^T for the rows below
+        ProfScope ps(m, KC_OTHER, 0.0);
+        CUDA_TRY(launch_ozaki_slice_t(Bv + int64_t(i) * bi * mcp, bi, mcp, mcp, m->oz_sb, m->Vs.as<int8_t>(),
+                                      mcp * m->np_, m->np_, int64_t(i) * bi, m->oz_slices,
+                                      m->ozflag.as<int>(), m->st));
+        ++m->launches;
+      }
     }
     GPB_TRY(pt.stop());
     *t_trsm += m->timing[4];
@@ -1222,6 +1327,23 @@ int predict_core(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var,
     const int64_t mc = std::min(chunk, mt - c0);
     GPB_TRY(predict_chunk(m, zt_dev + c0 * m->d, mc, want_var, m->mean.as<double>() + c0,
                           m->var.as<double>() + c0, &t_cross, &t_trsm));
+  }
+  if (want_var && m->oz_slices > 0 && m->ozflag.p) {
+    // an operand beyond its fixed-point scale saturates its digits: never
+    // expected (the scales are mathematical bounds), but then the products
+    // are repeated on the DMMA kernels
+    int over = 0;
+    CUDA_TRY(cudaMemcpyAsync(&over, m->ozflag.p, sizeof(int), cudaMemcpyDeviceToHost, m->st));
+    CUDA_TRY(cudaStreamSynchronize(m->st));
+    if (over) {
+      CUDA_TRY(cudaMemsetAsync(m->ozflag.p, 0, sizeof(int), m->st));
+      const int keep = m->oz_slices;
+      m->oz_slices = 0;
+      ++m->oz_fallbacks;
+      int s = predict_core(m, zt_dev, mt, want_var, single_chunk);
+      m->oz_slices = keep;
+      return s;
+    }
   }
   m->timing[3] = t_cross;
   m->timing[4] = t_trsm;
@@ -1311,6 +1433,11 @@ int model_create(gpb_ctx* ctx, const double* z, const double* y, int64_t n, int6
   m->d = d;
   m->T = T;
   m->b = static_cast<int>(n / T);
+  if (const char* e = getenv("GPB_OZAKI")) {
+    const int v = atoi(e);
+    m->oz_slices = v <= 0 ? 0 : std::min(kOzakiMaxSlices, std::max(4, v));
+  }
+  if (const char* e = getenv("GPB_OZAKI_MIN_K")) m->oz_min_k = std::max<int64_t>(64, atoll(e));
   if (int s_l = apply_layout(m)) {
     delete m;
     return s_l;
@@ -1343,7 +1470,8 @@ void free_model(gpb_model* m, bool keep = true) {
                     &m->flow_flags,
                     &m->X, &m->Kinv, &m->part_l, &m->part_v, &m->part_x, &m->inv_jobs,
                     &m->Bv, &m->W, &m->mpart, &m->sq, &m->pred_jobs, &m->zt, &m->mean, &m->var,
-                    &m->S, &m->fc_jobs, &m->gp_panel, &m->gp_h, &m->gp_jobs, &m->gp_tiles})
+                    &m->S, &m->fc_jobs, &m->gp_panel, &m->gp_h, &m->gp_jobs, &m->gp_tiles,
+                    &m->Ls, &m->Vs, &m->ozflag})
     b->release(keep);
 }
 
@@ -1367,6 +1495,7 @@ int gpb_init(int device, gpb_ctx** out) {
   if (device < 0 || device >= ndev) return fail(GPB_INVALID_CONFIG, "no such CUDA device");
   CUDA_TRY(cudaSetDevice(device));
   CUDA_TRY(gemm_init_attributes());
+  CUDA_TRY(ozaki_init_attributes());
   CUDA_TRY(potrf_init_attributes());
   gpb_ctx* c = new gpb_ctx();
   c->device = device;
@@ -1723,6 +1852,7 @@ int gpb_model_adopt_factor(gpb_model* m, const double* tiles, const double* dinv
   CUDA_TRY(cudaStreamSynchronize(m->st));
   m->factor_ok = true;
   m->weights_ok = true;
+  m->ls_ok = false;
   m->last_pivot = -1;
   return GPB_OK;
 }
@@ -1743,6 +1873,7 @@ int gpb_model_mark_factored(gpb_model* m) {
   CUDA_TRY(cudaDeviceSynchronize());
   m->factor_ok = true;
   m->weights_ok = true;
+  m->ls_ok = false;
   m->last_pivot = -1;
   return GPB_OK;
 }
@@ -1814,6 +1945,22 @@ int gpb_model_kernel_busy(gpb_model* m, double busy_ms[8]) {
   if (!m || !busy_ms) return fail(GPB_INVALID_CONFIG, "null argument");
   GPB_TRY(prof_collect(m));
   for (int i = 0; i < 8; ++i) busy_ms[i] = m->cls_busy[i];
+  return GPB_OK;
+}
+
+int gpb_model_set_ozaki(gpb_model* m, int slices) {
+  GPB_TRY(check_live(m));
+  if (slices != 0 && (slices < 4 || slices > kOzakiMaxSlices))
+    return fail(GPB_INVALID_CONFIG, "digit planes: 0 (off) or 4..8");
+  if (slices != m->oz_slices) m->ls_ok = false;
+  m->oz_slices = slices;
+  return GPB_OK;
+}
+
+int gpb_model_get_ozaki(gpb_model* m, int* slices, int64_t* fallbacks) {
+  GPB_TRY(check_live(m));
+  if (slices) *slices = m->oz_slices;
+  if (fallbacks) *fallbacks = m->oz_fallbacks;
   return GPB_OK;
 }
 

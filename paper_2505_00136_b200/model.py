@@ -104,6 +104,7 @@ class GPModel:
         # optimize and restored into a re-created handle (close(), runtime restart)
         self._adam = (np.zeros(3), np.zeros(3), 0)
         self._pending_train = False
+        self._digit_planes = None  # None: the library default (GPB_OZAKI)
 
     # -- attribute management (model.py:135-165) ---------------------------
     @property
@@ -161,6 +162,8 @@ class GPModel:
             self._push_params()
             m1, m2, step = self._adam
             _lib.check(lib.gpb_model_set_adam(h, _lib.dptr(m1), _lib.dptr(m2), step))
+            if self._digit_planes is not None:
+                _lib.check(lib.gpb_model_set_ozaki(h, self._digit_planes))
         elif self._pending_train:
             z, y = self._train.z, self._train.y
             _lib.check(lib.gpb_model_set_train(self._handle, _lib.dptr(z), _lib.dptr(y),
@@ -296,6 +299,32 @@ class GPModel:
         names = ("assembly", "factor", "solves", "cross_mean", "trsm_variance", "gradient",
                  "full_cov")
         return {k: float(out[i]) for i, k in enumerate(names)}
+
+    # -- tcgen05 digit-plane products (csrc/ozaki.cuh) ----------------------
+    @property
+    def digit_planes(self) -> int:
+        """Planes per operand of the int8 tensor-core products (0: FP64 DMMA only)."""
+        if self._handle is None:
+            return self._digit_planes or 0
+        out = ctypes.c_int()
+        _lib.check(_lib.load().gpb_model_get_ozaki(self._handle, ctypes.byref(out), None))
+        return int(out.value)
+
+    @digit_planes.setter
+    def digit_planes(self, planes: int) -> None:
+        planes = int(planes)
+        if planes != 0 and not 4 <= planes <= 8:
+            raise InvalidConfig("digit_planes must be 0 (off) or 4..8")
+        self._digit_planes = planes
+        if self._handle is not None:
+            _lib.check(_lib.load().gpb_model_set_ozaki(self._handle, planes))
+
+    def digit_plane_fallbacks(self) -> int:
+        if self._handle is None:
+            return 0
+        out = ctypes.c_int64()
+        _lib.check(_lib.load().gpb_model_get_ozaki(self._handle, None, ctypes.byref(out)))
+        return int(out.value)
 
     def launch_count(self) -> int:
         if self._handle is None:
