@@ -219,6 +219,11 @@ struct gpb_model {
   // tcgen05 digit-plane products (ozaki.cuh): planes of the off-diagonal L
   // tiles (same packing as L) and of V^T (one row per test point)
   DevBuf Ls, Vs, ozflag;
+  // ... and of the solved panels of the current group (same element order as
+  // `scratch`), read by the trailing updates NEXT / UPD of the factorisation
+  DevBuf Ps, oz_jobs;
+  int64_t oz_chol_min_k = 1024;  // updates with a shorter K = np * bi stay on the DMMA kernel
+  bool oz_chol = true;           // GPB_OZAKI_CHOL=0: digit planes for the prediction sweep only
   int oz_slices = 0;   // 0: every product on the DMMA kernels
   bool ls_ok = false;  // Ls holds the planes of the current factor
   double oz_sa = 0.0, oz_sb = 0.0;
@@ -436,6 +441,7 @@ int build_chol_plan(gpb_model* m) {
   double* L = m->L.as<double>();
   double* D = m->Dinv.as<double>();
   std::vector<GemmJob> jobs;
+  std::vector<OzakiJob> ozjobs;  // same indices as `jobs`; meaningful for NEXT / UPD entries
   m->groups.clear();
   const std::vector<int> sizes = chol_group_sizes(Ti, G);  // plan_common.h
   for (int k0 = 0, s = 0; k0 < Ti; k0 += sizes[s], ++s) {
@@ -484,6 +490,15 @@ int build_chol_plan(gpb_model* m) {
           j.K = grp.np * bi;
           j.lower = (i == jj);
           jobs.push_back(j);
+          // rows of the panel-plane byte view (pitch bi): panel 0 of the set
+          OzakiJob o{};
+          const int64_t set_row = int64_t(s % 2) * G * (pstride / bi);
+          o.a_row0 = static_cast<int>(set_row + int64_t(i - k0 - 1) * bi);
+          o.b_row0 = static_cast<int>(set_row + int64_t(jj - k0 - 1) * bi);
+          o.C = j.Cout;
+          o.lower = j.lower;
+          ozjobs.resize(jobs.size());
+          ozjobs.back() = o;
         }
     };
     grp.next_off = jobs.size();
@@ -512,6 +527,11 @@ int build_chol_plan(gpb_model* m) {
   CUDA_TRY(m->chol_jobs.ensure(sizeof(GemmJob) * std::max<size_t>(1, jobs.size())));
   if (!jobs.empty())
     CUDA_TRY(cudaMemcpy(m->chol_jobs.p, jobs.data(), sizeof(GemmJob) * jobs.size(),
+                        cudaMemcpyHostToDevice));
+  ozjobs.resize(jobs.size());
+  CUDA_TRY(m->oz_jobs.ensure(sizeof(OzakiJob) * std::max<size_t>(1, ozjobs.size())));
+  if (!ozjobs.empty())
+    CUDA_TRY(cudaMemcpy(m->oz_jobs.p, ozjobs.data(), sizeof(OzakiJob) * ozjobs.size(),
                         cudaMemcpyHostToDevice));
   m->chol_flops_exec.assign(m->groups.size(), 0.0);
   // cross-stream events: per group "panels solved" and "trailing update done"
@@ -576,6 +596,9 @@ struct PhaseTimer {
   }
 };
 
+// smallest power of two >= x
+double pow2_ceil(double x) { return std::exp2(std::ceil(std::log2(x))); }
+
 // assemble + factor (model.py:169-177 _ensure_factor)
 int ensure_factor(gpb_model* m) {
   if (m->factor_ok) return GPB_OK;
@@ -610,9 +633,52 @@ int ensure_factor(gpb_model* m) {
     p.a_kstride = p.b_kstride = pstride - bi2;
     return p;
   };
+  // Trailing updates on the tcgen05 int8 pipe (ozaki.cuh): the solved panels
+  // are final entries of L, |L(i, j)| <= sqrt(K_ii) = sqrt(vertical + noise)
+  // (1 on the decoupled padding rows), so one fixed-point scale covers them.
+  bool oz = m->oz_slices > 0 && m->oz_chol;
+  const int64_t plane_stride = 2 * int64_t(m->G) * pstride;  // bytes per digit plane
+  if (oz) {
+    bool any = false;
+    for (const CholGroup& grp : m->groups)
+      any = any || (int64_t(grp.np) * bi >= m->oz_chol_min_k && grp.next_cnt + grp.upd_cnt > 0);
+    oz = any;
+  }
+  if (oz) {
+    CUDA_TRY(m->Ps.ensure(size_t(m->oz_slices) * plane_stride));
+    if (!m->ozflag.p) {
+      CUDA_TRY(m->ozflag.ensure(sizeof(int)));
+      CUDA_TRY(cudaMemsetAsync(m->ozflag.p, 0, sizeof(int), m->st));
+    }
+    m->oz_sa = pow2_ceil(2.0 * std::max(1.0, std::sqrt(m->nu + m->s2)) * (1.0 + 1e-9));
+  }
+  // L(i,j) -= [X]_i [X]_j^T for `cnt` plan jobs from `off`; *done = false: not launched
+  auto oz_update = [&](const CholGroup& grp, int64_t off, int64_t cnt, double flops, cudaStream_t s,
+                       bool* done) -> int {
+    *done = false;
+    OzakiGemm g{};
+    g.a_planes = g.b_planes = m->Ps.as<int8_t>();
+    g.a_pitch = g.b_pitch = bi;
+    g.a_rows = g.b_rows = plane_stride / bi;
+    g.a_ktile = g.b_ktile = bi;
+    g.a_kt_rows = g.b_kt_rows = static_cast<int>(pstride / bi - bi);
+    g.M = g.N = bi;
+    g.K = grp.np * bi;
+    g.slices = m->oz_slices;
+    g.alpha = -m->oz_sa * m->oz_sa;
+    g.beta = 1.0;
+    g.ldc_in = g.ldc_out = bi;
+    g.jobs = m->oz_jobs.as<OzakiJob>() + off;
+    g.njobs = static_cast<int>(cnt);
+    ProfScope ps(m, KC_OZAKI, flops, s);
+    CUDA_TRY(launch_ozaki_gemm(g, s, done));
+    if (*done) ++m->launches;
+    return GPB_OK;
+  };
   for (int s = 0; s < ng; ++s) {
     const CholGroup& grp = m->groups[s];
     double* set = m->scratch.as<double>() + int64_t(s % 2) * m->G * pstride;
+    const bool oz_grp = oz && int64_t(grp.np) * bi >= m->oz_chol_min_k && grp.next_cnt + grp.upd_cnt > 0;
     // the group's columns are complete once NEXT(s-1) (crit, in order) and UPD(s-2) are done
     if (s >= 2) CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[s - 2], 0));
     for (int g = 0; g < grp.np; ++g) {
@@ -644,13 +710,27 @@ int ensure_factor(gpb_model* m) {
                             m->scratch, m->scratch);
       GPB_TRY(gemm(m, ip, true, true, EPI_AXPBY, grp.in_fl[g], m->crit));
     }
+    if (oz_grp) {  // digit planes of the group's solved panels
+      ProfScope ps(m, KC_OTHER, 0.0, m->crit);
+      for (int g = 0; g < grp.np; ++g) {
+        const int64_t eoff = (set - m->scratch.as<double>()) + g * pstride;
+        CUDA_TRY(launch_ozaki_slice(m->scratch.as<double>() + eoff, int64_t(Ti - (grp.k0 + g) - 1) * bi2,
+                                    m->oz_sa, m->Ps.as<int8_t>() + eoff, plane_stride, m->oz_slices,
+                                    m->ozflag.as<int>(), m->crit));
+        ++m->launches;
+      }
+    }
     CUDA_TRY(cudaEventRecord(ev_panel[s], m->crit));
     // lookahead: the next group's columns need UPD(s-1), which covered them
     if (grp.next_cnt > 0) {
       if (s >= 1) CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[s - 1], 0));
-      GemmParams np = walk(base_params(jobs + grp.next_off, static_cast<int>(grp.next_cnt), nb, nb,
-                                       bi, bi, bi, -1.0, 1.0));
-      GPB_TRY(gemm(m, np, true, true, EPI_AXPBY, grp.next_fl, m->crit));
+      bool done = false;
+      if (oz_grp) GPB_TRY(oz_update(grp, grp.next_off, grp.next_cnt, grp.next_fl, m->crit, &done));
+      if (!done) {
+        GemmParams np = walk(base_params(jobs + grp.next_off, static_cast<int>(grp.next_cnt), nb, nb,
+                                         bi, bi, bi, -1.0, 1.0));
+        GPB_TRY(gemm(m, np, true, true, EPI_AXPBY, grp.next_fl, m->crit));
+      }
     }
     // main stream: copy the panels back and apply the rest of the trailing update
     CUDA_TRY(cudaStreamWaitEvent(m->st, ev_panel[s], 0));
@@ -659,9 +739,13 @@ int ensure_factor(gpb_model* m) {
       ++m->launches;
     }
     if (grp.upd_cnt > 0) {
-      GemmParams up = walk(base_params(jobs + grp.upd_off, static_cast<int>(grp.upd_cnt), nb, nb,
-                                       bi, bi, bi, -1.0, 1.0));
-      GPB_TRY(gemm(m, up, true, true, EPI_AXPBY, grp.upd_fl));
+      bool done = false;
+      if (oz_grp) GPB_TRY(oz_update(grp, grp.upd_off, grp.upd_cnt, grp.upd_fl, m->st, &done));
+      if (!done) {
+        GemmParams up = walk(base_params(jobs + grp.upd_off, static_cast<int>(grp.upd_cnt), nb, nb,
+                                         bi, bi, bi, -1.0, 1.0));
+        GPB_TRY(gemm(m, up, true, true, EPI_AXPBY, grp.upd_fl));
+      }
     }
     CUDA_TRY(cudaEventRecord(ev_upd[s], m->st));
   }
@@ -682,6 +766,22 @@ int ensure_factor(gpb_model* m) {
   GPB_TRY(pt.stop());
   int info = -1;
   CUDA_TRY(cudaMemcpy(&info, m->info.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (oz) {
+    // a panel entry beyond the fixed-point scale saturated its digits (only
+    // possible for a matrix that is not positive definite, or never): the
+    // factorisation is repeated on the DMMA kernels, which also report the pivot
+    int over = 0;
+    CUDA_TRY(cudaMemcpy(&over, m->ozflag.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (over) {
+      CUDA_TRY(cudaMemset(m->ozflag.p, 0, sizeof(int)));
+      ++m->oz_fallbacks;
+      const bool keep = m->oz_chol;
+      m->oz_chol = false;
+      const int st = ensure_factor(m);
+      m->oz_chol = keep;
+      return st;
+    }
+  }
   if (info >= 0) {
     m->last_pivot = info;
     invalidate(m);
@@ -1109,9 +1209,6 @@ int grad_partial(gpb_model* m, const int* cols, int ncols, double out[3]) {
 }
 
 // ---- prediction (model.py:221-314) ----------------------------------------
-// smallest power of two >= x
-double pow2_ceil(double x) { return std::exp2(std::ceil(std::log2(x))); }
-
 // Digit planes of the off-diagonal factor tiles.  |L(i, j)| <= sqrt(K_ii) =
 // sqrt(vertical + noise) (1 on the decoupled padding rows), so one
 // fixed-point scale covers the whole factor.
@@ -1438,6 +1535,8 @@ int model_create(gpb_ctx* ctx, const double* z, const double* y, int64_t n, int6
     m->oz_slices = v <= 0 ? 0 : std::min(kOzakiMaxSlices, std::max(4, v));
   }
   if (const char* e = getenv("GPB_OZAKI_MIN_K")) m->oz_min_k = std::max<int64_t>(64, atoll(e));
+  if (const char* e = getenv("GPB_OZAKI_CHOL")) m->oz_chol = atoi(e) != 0;
+  if (const char* e = getenv("GPB_OZAKI_CHOL_MIN_K")) m->oz_chol_min_k = std::max<int64_t>(64, atoll(e));
   if (int s_l = apply_layout(m)) {
     delete m;
     return s_l;
@@ -1471,7 +1570,7 @@ void free_model(gpb_model* m, bool keep = true) {
                     &m->X, &m->Kinv, &m->part_l, &m->part_v, &m->part_x, &m->inv_jobs,
                     &m->Bv, &m->W, &m->mpart, &m->sq, &m->pred_jobs, &m->zt, &m->mean, &m->var,
                     &m->S, &m->fc_jobs, &m->gp_panel, &m->gp_h, &m->gp_jobs, &m->gp_tiles,
-                    &m->Ls, &m->Vs, &m->ozflag})
+                    &m->Ls, &m->Vs, &m->ozflag, &m->Ps, &m->oz_jobs})
     b->release(keep);
 }
 

@@ -92,8 +92,9 @@ GPB_DEVINL uint64_t smem_desc(uint32_t addr) {
 
 struct OzakiArgs {
   int a_row0, a_rows, a_ktile, a_kt_rows;
-  int b_row0, b_rows, b_col0;
-  int kchunks, mtiles;
+  int b_row0, b_rows, b_col0, b_ktile, b_kt_rows;
+  int kchunks, mtiles, blocks_per_job;
+  const OzakiJob* jobs;
   double alpha, beta;
   const double* Cin;
   double* Cout;
@@ -110,7 +111,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t bars = base + kStages * kStageBytes;  // full[2], empty[2], accfull, tmem slot
   const uint32_t full0 = bars, empty0 = bars + 16, accfull = bars + 32, slot = bars + 40;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt = blockIdx.x % p.mtiles, nt = blockIdx.x / p.mtiles;
+  int mt = blockIdx.x % p.mtiles, nt = blockIdx.x / p.mtiles;
+  int a_row0 = p.a_row0, b_row0 = p.b_row0;
+  const double* Cin = p.Cin;
+  double* Cout = p.Cout;
+  if (p.jobs) {  // grouped: blocks_per_job consecutive CTAs per job
+    const int job = blockIdx.x / p.blocks_per_job, r = blockIdx.x - job * p.blocks_per_job;
+    mt = r % p.mtiles;
+    nt = r / p.mtiles;
+    const OzakiJob j = p.jobs[job];
+    if (j.lower && nt * kOzakiBN >= (mt + 1) * kOzakiBM) return;
+    a_row0 = j.a_row0;
+    b_row0 = j.b_row0;
+    Cin = Cout = j.C;
+  }
 
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -139,14 +153,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(fb, kStageBytes);
         const int kb = c * kOzakiBK;
         const int ax = kb % p.a_ktile;
-        const int ay = p.a_row0 + mt * kOzakiBM + (kb / p.a_ktile) * p.a_kt_rows;
+        const int ay = a_row0 + mt * kOzakiBM + (kb / p.a_ktile) * p.a_kt_rows;
         const uint32_t sa = base + st * kStageBytes;
 #pragma unroll
         for (int q = 0; q < S; ++q) tma_load(sa + q * kABox, &map_a, fb, ax, ay + q * p.a_rows);
         const uint32_t sb = sa + S * kABox;
-        const int by = p.b_row0 + nt * kOzakiBN;
+        const int bx = p.b_col0 + (p.b_ktile ? kb % p.b_ktile : kb);
+        const int by = b_row0 + nt * kOzakiBN + (p.b_ktile ? (kb / p.b_ktile) * p.b_kt_rows : 0);
 #pragma unroll
-        for (int q = 0; q < S; ++q) tma_load(sb + q * kBBox, &map_b, fb, p.b_col0 + kb, by + q * p.b_rows);
+        for (int q = 0; q < S; ++q) tma_load(sb + q * kBBox, &map_b, fb, bx, by + q * p.b_rows);
       }
     }
   } else if (warp == 1) {
@@ -174,13 +189,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     const int quarter = warp & 3;
-    const int row = mt * kOzakiBM + quarter * 32 + lane;
+    const int row = mt * kOzakiBM + quarter * 32 + lane;  // row of the job's C
     mbar_wait(accfull, 0);
     tc_fence_after();
     const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    double* out = p.Cout + static_cast<long long>(row) * p.ldc_out + static_cast<long long>(nt) * kOzakiBN;
-    const double* in = p.Cin ? p.Cin + static_cast<long long>(row) * p.ldc_in + static_cast<long long>(nt) * kOzakiBN
-                             : nullptr;
+    double* out = Cout + static_cast<long long>(row) * p.ldc_out + static_cast<long long>(nt) * kOzakiBN;
+    const double* in = Cin ? Cin + static_cast<long long>(row) * p.ldc_in + static_cast<long long>(nt) * kOzakiBN
+                           : nullptr;
 #pragma unroll 1
     for (int c8 = 0; c8 < kOzakiBN; c8 += 8) {
       int v[S][8];
@@ -422,6 +437,10 @@ cudaError_t launch_ozaki_gemm(const OzakiGemm& g, cudaStream_t st, bool* used) {
   a.b_row0 = static_cast<int>(g.b_row0);
   a.b_rows = static_cast<int>(g.b_rows);
   a.b_col0 = static_cast<int>(g.b_col0);
+  a.b_ktile = g.b_ktile;
+  a.b_kt_rows = g.b_kt_rows;
+  a.jobs = g.jobs;
+  a.blocks_per_job = (g.M / kOzakiBM) * (g.N / kOzakiBN);
   a.kchunks = g.K / kOzakiBK;
   a.mtiles = g.M / kOzakiBM;
   a.alpha = g.alpha * (1.0 / 16384.0);  // the first group's weight 2^-14
@@ -430,7 +449,8 @@ cudaError_t launch_ozaki_gemm(const OzakiGemm& g, cudaStream_t st, bool* used) {
   a.Cout = g.Cout;
   a.ldc_in = g.ldc_in;
   a.ldc_out = g.ldc_out;
-  const int blocks = (g.M / kOzakiBM) * (g.N / kOzakiBN);
+  if (g.jobs && (g.njobs <= 0 || g.beta == 0.0)) return cudaErrorInvalidValue;
+  const int blocks = (g.M / kOzakiBM) * (g.N / kOzakiBN) * (g.jobs ? g.njobs : 1);
   cudaError_t e = cudaSuccess;
   switch (g.slices) {
     case 4: e = launch_s<4>(ma, mb, a, blocks, st); break;

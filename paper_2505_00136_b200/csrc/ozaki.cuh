@@ -45,6 +45,12 @@ cudaError_t launch_ozaki_slice_t(const double* src, int rows, int64_t cols, int6
                                  int8_t* planes, int64_t plane_stride, int64_t out_ld, int64_t k0,
                                  int slices, int* flag, cudaStream_t st);
 
+struct OzakiJob {
+  int a_row0, b_row0;
+  double* C;
+  int lower, pad;
+};
+
 struct OzakiGemm {
   // A planes: 2-D byte view (a_pitch bytes per row, a_rows rows per plane,
   // planes stacked along rows); the M x K operand starts at row a_row0,
@@ -52,9 +58,11 @@ struct OzakiGemm {
   const int8_t* a_planes;
   int64_t a_pitch, a_rows, a_row0;
   int a_ktile, a_kt_rows;
-  // B planes: N x K rows starting at row b_row0, column b_col0 (plain walk)
+  // B planes: N x K rows starting at row b_row0, column b_col0; plain walk
+  // along the row when b_ktile == 0, else tiled like A
   const int8_t* b_planes;
   int64_t b_pitch, b_rows, b_row0, b_col0;
+  int b_ktile = 0, b_kt_rows = 0;
   int M, N, K;     // multiples of 128 / 64 / 64; K <= kOzakiMaxK
   int slices;
   double alpha;    // Cout = beta * Cin + alpha * sa sb * sum (caller folds sa sb in)
@@ -62,6 +70,13 @@ struct OzakiGemm {
   const double* Cin;
   double* Cout;
   int64_t ldc_in, ldc_out;
+  // grouped form (the factorisation's trailing update, tiled.py:187-204): njobs
+  // independent M x N products sharing the plane buffers, job j reading A rows
+  // from jobs[j].a_row0, B rows from jobs[j].b_row0 (a_row0 / b_row0 above are
+  // ignored) and updating C in place: C = beta C + alpha sum, ldc_in = ldc_out.
+  // A `lower` job skips the 128 x 64 blocks above the diagonal 128-block.
+  const OzakiJob* jobs = nullptr;  // device array
+  int njobs = 0;
 };
 
 // false (nothing launched) when the driver entry point for tensor maps is missing
