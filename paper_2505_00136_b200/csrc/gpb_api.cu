@@ -224,7 +224,7 @@ struct gpb_model {
   DevBuf Ps, oz_jobs;
   int64_t oz_chol_min_k = 1024;  // updates with a shorter K = np * bi stay on the DMMA kernel
   bool oz_chol = true;           // GPB_OZAKI_CHOL=0: digit planes for the prediction sweep only
-  int oz_slices = 0;   // 0: every product on the DMMA kernels
+  int oz_slices = 8;   // planes per operand (GPB_OZAKI; 0: every product on the FP64 DMMA kernels)
   bool ls_ok = false;  // Ls holds the planes of the current factor
   double oz_sa = 0.0, oz_sb = 0.0;
   int64_t oz_min_k = 2048;  // shorter products stay on the DMMA kernels

@@ -20,6 +20,7 @@
 
 #include <cudaTypedefs.h>
 
+#include <cmath>
 #include <cstdlib>
 #include <mutex>
 #include <unordered_map>
@@ -230,6 +231,158 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// ---- second kernel shape: 128 x 128 blocks, a window of digit groups per launch --
+// One tcgen05.mma of 128 x 64 x 32 reads 4 KB of A and 2 KB of B from shared
+// memory for 32 cycles of tensor work: 192 B/cycle, above what shared memory
+// delivers, so the 128 x 64 kernel above is operand-fetch bound (59% of the
+// int8 issue rate).  With N = 128 an MMA reads 8 KB for 64 cycles.  TMEM then
+// holds 4 accumulators of 128 columns, so the groups are computed in two
+// launches of up to four groups each, least significant first: launch one
+// loads all the planes and adds groups [G0, G0 + 4) to C, launch two loads
+// planes 0 .. 3 only and adds groups [0, G0).  K is walked in 32-byte chunks
+// (SWIZZLE_32B boxes of 128 rows) through a ring of 3-4 stages.
+constexpr int kBN2 = 128, kBK2 = 32;
+constexpr int kBox2 = 128 * kBK2;  // 4 KB per plane box, A and B alike
+
+// K-major operand box, 32-byte rows, SWIZZLE_32B (8-row atoms of 256 bytes)
+GPB_DEVINL uint64_t smem_desc32(uint32_t addr) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (1ull << 16) | (16ull << 32) | (1ull << 46) | (6ull << 61);
+}
+
+__host__ __device__ constexpr int stages2(int P) { return P >= 7 ? 3 : 4; }
+constexpr size_t smem_bytes2(int P) { return size_t(stages2(P)) * P * 2 * kBox2 + 1024 + 128; }
+
+template <int G0, int NG>
+__global__ void __launch_bounds__(kThreads, 1)
+    ozaki_gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                       const OzakiArgs p) {
+  constexpr int P = G0 + NG;  // planes of each operand the groups [G0, P) need
+  constexpr int NST = stages2(P);
+  constexpr int kStageBytes = P * 2 * kBox2;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = (su32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t bars = base + NST * kStageBytes;  // full[NST], empty[NST], accfull, tmem slot
+  const uint32_t full0 = bars, empty0 = bars + 8 * NST, accfull = bars + 16 * NST, slot = accfull + 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int mt = blockIdx.x % p.mtiles, nt = blockIdx.x / p.mtiles;
+  int a_row0 = p.a_row0, b_row0 = p.b_row0;
+  const double* Cin = p.Cin;
+  double* Cout = p.Cout;
+  if (p.jobs) {  // grouped: blocks_per_job consecutive CTAs per job
+    const int job = blockIdx.x / p.blocks_per_job, r = blockIdx.x - job * p.blocks_per_job;
+    mt = r % p.mtiles;
+    nt = r / p.mtiles;
+    const OzakiJob j = p.jobs[job];
+    if (j.lower && nt > mt) return;
+    a_row0 = j.a_row0;
+    b_row0 = j.b_row0;
+    Cin = Cout = j.C;
+  }
+
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(accfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(slot) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tmem;
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(tmem) : "r"(slot) : "memory");
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int st = 0, ph = 0;
+      for (int c = 0; c < p.kchunks; ++c) {
+        mbar_wait(empty0 + 8 * st, ph ^ 1);
+        const uint32_t fb = full0 + 8 * st;
+        mbar_expect_tx(fb, kStageBytes);
+        const int kb = c * kBK2;
+        const int ax = kb % p.a_ktile;
+        const int ay = a_row0 + mt * kOzakiBM + (kb / p.a_ktile) * p.a_kt_rows;
+        const uint32_t sa = base + st * kStageBytes;
+#pragma unroll
+        for (int q = 0; q < P; ++q) tma_load(sa + q * kBox2, &map_a, fb, ax, ay + q * p.a_rows);
+        const uint32_t sb = sa + P * kBox2;
+        const int bx = p.b_col0 + (p.b_ktile ? kb % p.b_ktile : kb);
+        const int by = b_row0 + nt * kBN2 + (p.b_ktile ? (kb / p.b_ktile) * p.b_kt_rows : 0);
+#pragma unroll
+        for (int q = 0; q < P; ++q) tma_load(sb + q * kBox2, &map_b, fb, bx, by + q * p.b_rows);
+        if (++st == NST) st = 0, ph ^= 1;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // s32 accumulate, signed 8-bit A and B, both K-major, N = 128, M = 128
+      constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((kBN2 >> 3) << 17) | ((kOzakiBM >> 4) << 24);
+      int st = 0, ph = 0;
+      for (int c = 0; c < p.kchunks; ++c) {
+        mbar_wait(full0 + 8 * st, ph);
+        tc_fence_after();
+        const uint32_t sa = base + st * kStageBytes, sb = sa + P * kBox2;
+#pragma unroll
+        for (int g = G0; g < P; ++g) {
+#pragma unroll
+          for (int q = 0; q <= g; ++q)
+            tc_mma_i8(tmem + (g - G0) * kBN2, smem_desc32(sa + q * kBox2), smem_desc32(sb + (g - q) * kBox2), idesc,
+                      (c | q) != 0);
+        }
+        tc_commit(empty0 + 8 * st);
+        if (++st == NST) st = 0, ph ^= 1;
+      }
+      tc_commit(accfull);
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int row = mt * kOzakiBM + quarter * 32 + lane;  // row of the job's C
+    mbar_wait(accfull, 0);
+    tc_fence_after();
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    double* out = Cout + static_cast<long long>(row) * p.ldc_out + static_cast<long long>(nt) * kBN2;
+    const double* in = Cin ? Cin + static_cast<long long>(row) * p.ldc_in + static_cast<long long>(nt) * kBN2
+                           : nullptr;
+#pragma unroll 1
+    for (int c8 = 0; c8 < kBN2; c8 += 8) {
+      int v[NG][8];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) tc_ld8(taddr + g * kBN2 + c8, v[g]);
+      tc_wait_ld();
+      double r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        double acc = static_cast<double>(v[NG - 1][j]);
+#pragma unroll
+        for (int g = NG - 2; g >= 0; --g) acc = fma(acc, 0.0078125, static_cast<double>(v[g][j]));
+        r[j] = p.alpha * acc;
+      }
+      if (in) {
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+          const double2 ci = *reinterpret_cast<const double2*>(in + c8 + j);
+          r[j] = fma(p.beta, ci.x, r[j]);
+          r[j + 1] = fma(p.beta, ci.y, r[j + 1]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) *reinterpret_cast<double2*>(out + c8 + j) = make_double2(r[j], r[j + 1]);
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+  }
+}
+
 // digits of f (|f| <= 1/2 in units of the scale): exact
 template <int MAXS>
 GPB_DEVINL void digits(double f, int slices, int (&d)[MAXS]) {
@@ -336,9 +489,10 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 struct MapKey {
   const void* base;
   int64_t pitch, rows;
-  int box_rows;
+  int box_rows, box_cols;
   bool operator==(const MapKey& o) const {
-    return base == o.base && pitch == o.pitch && rows == o.rows && box_rows == o.box_rows;
+    return base == o.base && pitch == o.pitch && rows == o.rows && box_rows == o.box_rows &&
+           box_cols == o.box_cols;
   }
 };
 struct MapKeyHash {
@@ -346,15 +500,16 @@ struct MapKeyHash {
     size_t h = reinterpret_cast<size_t>(k.base);
     h = h * 1000003u ^ static_cast<size_t>(k.pitch);
     h = h * 1000003u ^ static_cast<size_t>(k.rows);
-    return h * 1000003u ^ static_cast<size_t>(k.box_rows);
+    return h * 1000003u ^ static_cast<size_t>(k.box_rows * 131 + k.box_cols);
   }
 };
 
-// byte view (pitch bytes per row, `rows` rows), boxes of 64 bytes x box_rows, SWIZZLE_64B
-bool byte_map(const int8_t* base, int64_t pitch, int64_t rows, int box_rows, CUtensorMap* out) {
+// byte view (pitch bytes per row, `rows` rows), boxes of box_cols (64 or 32) bytes x box_rows,
+// swizzled over the box width
+bool byte_map(const int8_t* base, int64_t pitch, int64_t rows, int box_rows, int box_cols, CUtensorMap* out) {
   static std::mutex mu;
   static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
-  const MapKey key{base, pitch, rows, box_rows};
+  const MapKey key{base, pitch, rows, box_rows, box_cols};
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) {
@@ -366,10 +521,11 @@ bool byte_map(const int8_t* base, int64_t pitch, int64_t rows, int box_rows, CUt
   CUtensorMap m;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(pitch), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch)};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kOzakiBK), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
   if (fn(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides, box, estr,
-         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
   if (cache.size() > 1024) cache.clear();
@@ -386,10 +542,53 @@ cudaError_t launch_s(const CUtensorMap& ma, const CUtensorMap& mb, const OzakiAr
   return cudaGetLastError();
 }
 
+template <int G0, int NG>
+cudaError_t launch_w(const CUtensorMap& ma, const CUtensorMap& mb, const OzakiArgs& a, int blocks, cudaStream_t st) {
+  ozaki_gemm2_kernel<G0, NG><<<blocks, kThreads, smem_bytes2(G0 + NG), st>>>(ma, mb, a);
+  return cudaGetLastError();
+}
+
+// groups [g0, g0 + ng) of the 128 x 128 kernel
+cudaError_t launch_window(int g0, int ng, const CUtensorMap& ma, const CUtensorMap& mb, const OzakiArgs& a,
+                          int blocks, cudaStream_t st) {
+  if (g0 == 0) {
+    switch (ng) {
+      case 1: return launch_w<0, 1>(ma, mb, a, blocks, st);
+      case 2: return launch_w<0, 2>(ma, mb, a, blocks, st);
+      case 3: return launch_w<0, 3>(ma, mb, a, blocks, st);
+      case 4: return launch_w<0, 4>(ma, mb, a, blocks, st);
+    }
+  } else if (ng == 4) {
+    switch (g0) {
+      case 1: return launch_w<1, 4>(ma, mb, a, blocks, st);
+      case 2: return launch_w<2, 4>(ma, mb, a, blocks, st);
+      case 3: return launch_w<3, 4>(ma, mb, a, blocks, st);
+      case 4: return launch_w<4, 4>(ma, mb, a, blocks, st);
+    }
+  }
+  return cudaErrorInvalidValue;
+}
+
+// GPB_OZAKI_KERNEL=1: the 128 x 64 single-launch kernel for every product
+int kernel_shape() {
+  static const int v = [] {
+    const char* e = getenv("GPB_OZAKI_KERNEL");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
+}
+
 }  // namespace
 
 cudaError_t ozaki_init_attributes() {
   cudaError_t e;
+#define GPB_OZ_ATTR2(G0, NG)                                                                                  \
+  if ((e = cudaFuncSetAttribute(ozaki_gemm2_kernel<G0, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                static_cast<int>(smem_bytes2(G0 + NG)))) != cudaSuccess)                     \
+    return e;
+  GPB_OZ_ATTR2(0, 1) GPB_OZ_ATTR2(0, 2) GPB_OZ_ATTR2(0, 3) GPB_OZ_ATTR2(0, 4)
+  GPB_OZ_ATTR2(1, 4) GPB_OZ_ATTR2(2, 4) GPB_OZ_ATTR2(3, 4) GPB_OZ_ATTR2(4, 4)
+#undef GPB_OZ_ATTR2
 #define GPB_OZ_ATTR(S)                                                                              \
   if ((e = cudaFuncSetAttribute(ozaki_gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                 static_cast<int>(smem_bytes(S)))) != cudaSuccess)                  \
@@ -425,9 +624,11 @@ cudaError_t launch_ozaki_gemm(const OzakiGemm& g, cudaStream_t st, bool* used) {
   if (g.M % kOzakiBM || g.N % kOzakiBN || g.K % kOzakiBK || g.K <= 0 || g.K > kOzakiMaxK || g.slices < 4 ||
       g.slices > kOzakiMaxSlices)
     return cudaErrorInvalidValue;
+  if (g.jobs && (g.njobs <= 0 || g.beta == 0.0)) return cudaErrorInvalidValue;
+  const bool wide = kernel_shape() == 2 && g.N % kBN2 == 0;
   CUtensorMap ma, mb;
-  if (!byte_map(g.a_planes, g.a_pitch, g.a_rows * g.slices, kOzakiBM, &ma) ||
-      !byte_map(g.b_planes, g.b_pitch, g.b_rows * g.slices, kOzakiBN, &mb))
+  if (!byte_map(g.a_planes, g.a_pitch, g.a_rows * g.slices, kOzakiBM, wide ? kBK2 : kOzakiBK, &ma) ||
+      !byte_map(g.b_planes, g.b_pitch, g.b_rows * g.slices, wide ? kBN2 : kOzakiBN, wide ? kBK2 : kOzakiBK, &mb))
     return cudaSuccess;
   OzakiArgs a;
   a.a_row0 = static_cast<int>(g.a_row0);
@@ -449,7 +650,25 @@ cudaError_t launch_ozaki_gemm(const OzakiGemm& g, cudaStream_t st, bool* used) {
   a.Cout = g.Cout;
   a.ldc_in = g.ldc_in;
   a.ldc_out = g.ldc_out;
-  if (g.jobs && (g.njobs <= 0 || g.beta == 0.0)) return cudaErrorInvalidValue;
+  if (wide) {
+    // least significant groups first, then groups [0, S - 4) on top of the result
+    a.blocks_per_job = (g.M / kOzakiBM) * (g.N / kBN2);
+    a.kchunks = g.K / kBK2;
+    const int blocks = a.blocks_per_job * (g.jobs ? g.njobs : 1);
+    const int g0 = g.slices - 4;
+    const double unit = a.alpha;
+    a.alpha = std::ldexp(unit, -7 * g0);
+    cudaError_t e = launch_window(g0, 4, ma, mb, a, blocks, st);
+    if (e == cudaSuccess && g0 > 0) {
+      a.alpha = unit;
+      a.beta = 1.0;
+      a.Cin = g.Cout;
+      a.ldc_in = g.ldc_out;
+      e = launch_window(0, g0, ma, mb, a, blocks, st);
+    }
+    *used = e == cudaSuccess;
+    return e;
+  }
   const int blocks = (g.M / kOzakiBM) * (g.N / kOzakiBN) * (g.jobs ? g.njobs : 1);
   cudaError_t e = cudaSuccess;
   switch (g.slices) {
