@@ -140,15 +140,23 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def _ncu_traffic():
-    """DRAM bytes per launch of the dominant kernel from the committed ncu
-    --set full capture (profiles/r02_gemm_traffic.json), or None."""
-    path = os.path.join(ROOT, "profiles", "r02_gemm_traffic.json")
+def _ncu_traffic(name="r02_gemm_traffic.json"):
+    """DRAM bytes per launch of a kernel from its committed ncu --set full
+    capture (profiles/<name>), or None."""
+    path = os.path.join(ROOT, "profiles", name)
     try:
         with open(path) as f:
             return json.load(f)["traffic_bytes_per_launch"]
     except (OSError, KeyError, ValueError):
         return None
+
+
+def _measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
 
 
 # ---------------------------------------------------------------- CPU side
@@ -270,6 +278,51 @@ def cpu_baseline_block():
 
 
 # ---------------------------------------------------------------- GPU side
+def roofline_block(planes, pairs, planes_tf, planes_tf_exec, gemm_tf, gemm_tf_exec, fp64_peak, kcnt, kbusy, kms,
+                   total_ms, chol_tf):
+    """`roofline` of the bench line for the step's dominant kernel."""
+    dmma = {"kernel": "dgemm_tma_kernel (TMA-fed DMMA.8x8x4)", "achieved": gemm_tf, "peak": fp64_peak,
+            "unit": "TFLOP/s", "frac": gemm_tf / fp64_peak if fp64_peak else None,
+            "achieved_executed_flops": gemm_tf_exec, "launches": int(kcnt[0]), "busy_ms": kbusy[0],
+            "summed_launch_ms": kms[0], "share_of_step": kbusy[0] / total_ms if total_ms else None,
+            "peak_source": "in-run FP64 DMMA probe (MEASURED_PEAKS.json has no FP64 entry)"}
+    basis = ("algorithmic flops n^3/3 + n^2 m per step, split between the two tensor-kernel classes in "
+             "proportion to their executed flops, over each class's busy time: the union of its launch "
+             "intervals on both streams (CUDA events around every launch), so overlapping launches count once")
+    if not planes or not kbusy[5]:
+        dmma.update({"bound": "tensor", "traffic": _ncu_traffic(), "achieved_basis": basis,
+                     "traffic_source": "profiles/r02_gemm_traffic.json (ncu --set full of the prediction-sweep "
+                                       "GEMM; not measured in this run)",
+                     "cholesky_frac_of_peak": chol_tf / fp64_peak if fp64_peak else None})
+        return dmma
+    mp = _measured_peaks()
+    bf16 = mp.get("bf16_tflops_sustained") or mp.get("bf16_tflops")
+    if bf16:
+        peak, src = 2.0 * bf16, ("2 x MEASURED_PEAKS.json bf16_tflops_sustained (the int8 tcgen05 rate is twice "
+                                 "the bf16 rate; sustained figure: the kernel runs inside a long step)")
+    else:
+        peak, src = 4500.0, "nominal dense int8 peak of B200 (MEASURED_PEAKS.json absent)"
+    achieved = planes_tf * pairs
+    return {"bound": "tensor",
+            "kernel": "ozaki_gemm2_kernel (tcgen05.mma kind::i8 on signed 7-bit digit planes, TMEM accumulators)",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak,
+            "achieved_basis": f"int8 operations per second: {pairs} digit-pair products ({planes} planes per "
+                              "operand) per algorithmic FP64 multiply-add; " + basis,
+            "peak_source": src,
+            "fp64_equivalent_tflops": planes_tf, "fp64_equivalent_executed_tflops": planes_tf_exec,
+            "fp64_dmma_peak": fp64_peak,
+            "fp64_equivalent_over_dmma_peak": planes_tf / fp64_peak if fp64_peak else None,
+            "traffic": _ncu_traffic("r02_planes_traffic.json"),
+            "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the digit-plane "
+                              "product from the committed ncu --set full capture "
+                              "(profiles/r02_planes_traffic.json), not measured in this run",
+            "launches": int(kcnt[5]), "busy_ms": kbusy[5], "summed_launch_ms": kms[5],
+            "share_of_step": kbusy[5] / total_ms if total_ms else None,
+            "cholesky_fp64_equivalent_over_dmma_peak": chol_tf / fp64_peak if fp64_peak else None,
+            "dmma_class": dmma}
+
+
 def run_ours(args, rank: int, world: int, local_rank: int):
     import numpy as np
     import torch
@@ -365,8 +418,58 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     # critical and main streams are not double-counted.  The executed count
     # (with the lower-triangular waste of 128-blocks) is reported beside it.
     gemm_alg = K * (n ** 3 / 3.0 + float(n) * n * m)
-    gemm_tf = gemm_alg / (kbusy[0] * 1e-3) / 1e12 if kbusy[0] else 0.0
+    # Two tensor-kernel classes share that work: the tcgen05 int8 digit-plane
+    # products (class 5: trailing updates with K >= 1024 and prediction rows
+    # with K >= 2048) and the FP64 DMMA GEMM (class 0: everything shorter).
+    # The algorithmic flops are split between them in proportion to the
+    # executed flops each class reports.
+    planes_h = ctypes.c_int()
+    lib.gpb_model_get_ozaki(h, ctypes.byref(planes_h), None)
+    planes = int(planes_h.value)
+    pairs = planes * (planes + 1) // 2
+    exec_total = kfl[0] + kfl[5]
+    alg_dmma = gemm_alg * kfl[0] / exec_total if exec_total else 0.0
+    alg_planes = gemm_alg * kfl[5] / exec_total if exec_total else 0.0
+    gemm_tf = alg_dmma / (kbusy[0] * 1e-3) / 1e12 if kbusy[0] else 0.0
     gemm_tf_exec = kfl[0] / (kbusy[0] * 1e-3) / 1e12 if kbusy[0] else 0.0
+    planes_tf = alg_planes / (kbusy[5] * 1e-3) / 1e12 if kbusy[5] else 0.0
+    planes_tf_exec = kfl[5] / (kbusy[5] * 1e-3) / 1e12 if kbusy[5] else 0.0
+    main_stats = {"kms": list(kms), "kbusy": list(kbusy), "kcnt": list(kcnt)}
+
+    # ---- the same step with every product on the FP64 DMMA kernels (planes off)
+    dmma_only = None
+    if planes and world == 1:
+        _lib.check(lib.gpb_model_set_ozaki(h, 0))
+        step()
+        k2 = max(2, min(3, K))
+        ph2 = np.zeros(8)
+        _lib.check(lib.gpb_model_set_profiling(h, 1))
+        for _ in range(k2):
+            step()
+            lib.gpb_model_timings(h, tm, 8)
+            ph2 += np.array(tm[:])
+        torch.cuda.synchronize()
+        lib.gpb_model_kernel_stats(h, kms, kfl, kcnt)
+        lib.gpb_model_kernel_busy(h, kbusy)
+        lib.gpb_model_set_profiling(h, 0)
+        d_tf = k2 * chol_flops(n) / (ph2[1] * 1e-3) / 1e12
+        d_gemm = k2 * (n ** 3 / 3.0 + float(n) * n * m) / (kbusy[0] * 1e-3) / 1e12 if kbusy[0] else 0.0
+        dmma_only = {
+            "note": "GPB_OZAKI=0 / digit_planes = 0: the same step with every product on the FP64 tensor "
+                    "pipe (DMMA.8x8x4), the path BASELINE.json's north_star names",
+            "steps": k2, "value": d_tf, "unit": "TFLOP/s",
+            "cholesky_frac_of_fp64_peak": d_tf / peak.value if peak.value else None,
+            "predict_variance_points_per_s": k2 * m / ((ph2[3] + ph2[4]) * 1e-3),
+            "phases_ms_per_step": {k: float(ph2[i] / k2) for i, k in enumerate(
+                ("assembly", "factor", "solves", "cross_mean", "trsm_variance"))},
+            "gemm_roofline": {"achieved": d_gemm, "peak": peak.value, "unit": "TFLOP/s",
+                              "frac": d_gemm / peak.value if peak.value else None,
+                              "basis": "algorithmic flops n^3/3 + n^2 m over the DMMA GEMM busy time",
+                              "traffic": _ncu_traffic(),
+                              "traffic_source": "profiles/r02_gemm_traffic.json (ncu --set full, prediction-sweep "
+                                                "GEMM; not measured in this run)"}}
+        _lib.check(lib.gpb_model_set_ozaki(h, planes))
+    kms, kbusy, kcnt = main_stats["kms"], main_stats["kbusy"], main_stats["kcnt"]
 
     # ---- e2e: public API, host buffers, copies inside the timed region
     # inputs live in pinned host memory (the API's H2D copies read them there)
@@ -433,22 +536,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 "api": "GPModel(train).compute_loss() then predict_with_uncertainty(test), host numpy "
                        "arrays in pinned memory, median of K reps"},
         "e2e_at_cpu_sample": same,
-        "roofline": {"bound": "tensor", "kernel": "dgemm_tma_kernel (TMA-fed DMMA.8x8x4)",
-                     "achieved": gemm_tf, "peak": peak.value, "unit": "TFLOP/s",
-                     "frac": gemm_tf / peak.value if peak.value else None,
-                     "traffic": _ncu_traffic(),
-                     "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the "
-                                       "prediction-sweep GEMM from the committed ncu --set full capture "
-                                       "(profiles/r02_gemm_traffic.json), not measured in this run",
-                     "peak_source": "in-run FP64 DMMA probe (MEASURED_PEAKS.json has no FP64 entry)",
-                     "achieved_executed_flops": gemm_tf_exec,
-                     "achieved_basis": "algorithmic flops n^3/3 + n^2 m per step over the GEMM busy time: "
-                                       "the union of the GEMM launch intervals on both streams (CUDA events "
-                                       "around every launch), so overlapping launches count once",
-                     "launches": int(kcnt[0]), "busy_ms": kbusy[0], "summed_launch_ms": kms[0],
-                     "share_of_step": kbusy[0] / total_ms if total_ms else None,
-                     "cholesky_frac_of_peak": value / world / peak.value if peak.value else None},
-        "kernel_classes_ms": {"gemm": kms[0], "potrf_trtri": kms[1], "sek": kms[2]},
+        "roofline": roofline_block(planes, pairs, planes_tf, planes_tf_exec, gemm_tf, gemm_tf_exec, peak.value,
+                                   kcnt, kbusy, kms, total_ms, value / world),
+        "dmma_only": dmma_only,
+        "digit_planes": planes,
+        "kernel_classes_ms": {"gemm_dmma": kms[0], "digit_plane_products": kms[5], "potrf_trtri": kms[1],
+                              "sek": kms[2], "solves": kms[3], "slicing_other": kms[4]},
         "clocks": clk,
         "gpu_launches": int(lc1.value - lc0.value),
         "strong_scaling_base": base,
@@ -592,8 +685,20 @@ def strong_base(args):
     flags = (ctypes.c_uint8 * 3)(1, 1, 1)
     ll = ctypes.c_double()
     tm = (ctypes.c_double * 8)()
-    fac, sol = [], []
+    fac, sol, fac_planes = [], [], []
     try:
+        # the multi-GPU executor (csrc/dist.cu) runs every product on the FP64
+        # DMMA kernels, so t_1 is taken on the same kernels; the single-GPU
+        # default (digit planes) is timed beside it
+        planes_h = ctypes.c_int()
+        lib.gpb_model_get_ozaki(h, ctypes.byref(planes_h), None)
+        for it in range(2 if planes_h.value else 0):
+            _lib.check(lib.gpb_model_set_params(h, 1.0, 1.0, 0.1, flags))
+            _lib.check(lib.gpb_log_likelihood(h, ctypes.byref(ll)))
+            lib.gpb_model_timings(h, tm, 8)
+            if it >= 1:
+                fac_planes.append(tm[1])
+        _lib.check(lib.gpb_model_set_ozaki(h, 0))
         for it in range(3):
             _lib.check(lib.gpb_model_set_params(h, 1.0, 1.0, 0.1, flags))
             _lib.check(lib.gpb_log_likelihood(h, ctypes.byref(ll)))
@@ -640,7 +745,10 @@ def strong_base(args):
     per_rank_link = emulate(EMU_LINK)
     return {"workload": f"config 3 on 1 GPU: n={c['n']}, D={c['d']}, {c['tiles']} tiles", "factor_ms": f,
             "solves_ms": s_, "tflops": chol_flops(c["n"]) / (f * 1e-3) / 1e12,
-            "note": "t_1 of the strong-scaling efficiency E(p) = t_1 / (p t_p) (1 warm-up + 2 timed)",
+            "note": "t_1 of the strong-scaling efficiency E(p) = t_1 / (p t_p) (1 warm-up + 2 timed), on the "
+                    "FP64 DMMA kernels like the multi-GPU executor",
+            "factor_ms_digit_planes": fac_planes[0] if fac_planes else None,
+            "tflops_digit_planes": chol_flops(c["n"]) / (fac_planes[0] * 1e-3) / 1e12 if fac_planes else None,
             "emulated_2x4_factor_ms_per_rank": per_rank,
             "emulated_2x4_efficiency_upper_bound": f / (8 * max(per_rank)),
             "emulated_2x4_link_factor_ms_per_rank": per_rank_link,

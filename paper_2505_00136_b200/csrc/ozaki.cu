@@ -59,12 +59,36 @@ GPB_DEVINL void tma_load(uint32_t dst, const CUtensorMap* map, uint32_t bar, int
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
 }
+// the same box written at the same shared-memory offset of every CTA in cta_mask, each
+// destination's own mbarrier (same offset) receiving the bytes
+GPB_DEVINL void tma_load_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, uint16_t cta_mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], "
+      "[%1, {%2, %3}], [%4], %5;\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "h"(cta_mask)
+      : "memory");
+}
+GPB_DEVINL void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+GPB_DEVINL uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
 GPB_DEVINL void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 GPB_DEVINL void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 // arrives on the mbarrier once every tcgen05.mma issued so far by this thread has completed
 GPB_DEVINL void tc_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
                : "memory");
+}
+// ... arriving on the mbarrier at the same offset of every CTA in cta_mask
+GPB_DEVINL void tc_commit_mc(uint32_t bar, uint16_t cta_mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(bar),
+      "h"(cta_mask)
+      : "memory");
 }
 // D[tmem] (+)= A[smem desc] * B[smem desc]^T, int8 x int8 -> int32
 GPB_DEVINL void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
@@ -253,7 +277,16 @@ GPB_DEVINL uint64_t smem_desc32(uint32_t addr) {
 __host__ __device__ constexpr int stages2(int P) { return P >= 7 ? 3 : 4; }
 constexpr size_t smem_bytes2(int P) { return size_t(stages2(P)) * P * 2 * kBox2 + 1024 + 128; }
 
-template <int G0, int NG>
+//
+// MC: clusters of 2 x 2 blocks.  The products are bound by L2 -> shared-memory
+// traffic (ncu: L2 throughput 73%, tensor pipe 66% / 43% active in the two
+// windows), and the four blocks of a cluster share their A rows pairwise along
+// n and their B rows pairwise along m: every CTA loads half of its A planes and
+// half of its B planes and multicasts each box to the neighbour that needs it
+// too, which halves the traffic.  A stage of a CTA is written by itself and its
+// two neighbours, so its `empty` barrier collects the tcgen05.commit of all
+// three (each CTA commits to itself and to both neighbours).
+template <int G0, int NG, bool MC>
 __global__ void __launch_bounds__(kThreads, 1)
     ozaki_gemm2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                        const OzakiArgs p) {
@@ -265,16 +298,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t bars = base + NST * kStageBytes;  // full[NST], empty[NST], accfull, tmem slot
   const uint32_t full0 = bars, empty0 = bars + 8 * NST, accfull = bars + 16 * NST, slot = accfull + 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int mt = blockIdx.x % p.mtiles, nt = blockIdx.x / p.mtiles;
+  int mt, nt, job = 0;
+  uint32_t rank = 0;
+  if (MC) {  // 4 consecutive CTAs = one 2 x 2 region of blocks; regions walk m first
+    rank = cluster_rank();
+    const int region = blockIdx.x >> 2, per_job = p.blocks_per_job >> 2, rm = p.mtiles >> 1;
+    int r = region;
+    if (p.jobs) {
+      job = region / per_job;
+      r = region - job * per_job;
+    }
+    mt = 2 * (r % rm) + (rank & 1);
+    nt = 2 * (r / rm) + (rank >> 1);
+  } else {
+    int r = blockIdx.x;
+    if (p.jobs) {  // grouped: blocks_per_job consecutive CTAs per job
+      job = blockIdx.x / p.blocks_per_job;
+      r = blockIdx.x - job * p.blocks_per_job;
+    }
+    mt = r % p.mtiles;
+    nt = r / p.mtiles;
+  }
   int a_row0 = p.a_row0, b_row0 = p.b_row0;
   const double* Cin = p.Cin;
   double* Cout = p.Cout;
-  if (p.jobs) {  // grouped: blocks_per_job consecutive CTAs per job
-    const int job = blockIdx.x / p.blocks_per_job, r = blockIdx.x - job * p.blocks_per_job;
-    mt = r % p.mtiles;
-    nt = r / p.mtiles;
+  if (p.jobs) {
     const OzakiJob j = p.jobs[job];
-    if (j.lower && nt > mt) return;
+    // lower jobs skip what lies above the diagonal: blocks, or whole regions (the
+    // one upper block of a diagonal region is computed; it is never read)
+    if (j.lower && (MC ? (nt >> 1) > (mt >> 1) : nt > mt)) return;
     a_row0 = j.a_row0;
     b_row0 = j.b_row0;
     Cin = Cout = j.C;
@@ -283,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, MC ? 3 : 1);
     }
     mbar_init(accfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -295,12 +347,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (MC) cluster_sync_all();  // every CTA's barriers exist before a neighbour signals them
   uint32_t tmem;
   asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(tmem) : "r"(slot) : "memory");
+  // neighbours: rank ^ 2 shares the A rows (same mt), rank ^ 1 the B rows (same nt)
+  const uint16_t mask_a = static_cast<uint16_t>((1u << rank) | (1u << (rank ^ 2)));
+  const uint16_t mask_b = static_cast<uint16_t>((1u << rank) | (1u << (rank ^ 1)));
 
   if (warp == 0) {
     if (lane == 0) {
       int st = 0, ph = 0;
+      // this CTA's share of the planes: the first half of A when it is the left block of
+      // its pair, the first half of B when it is the upper one
+      const int qa0 = MC ? ((rank >> 1) ? P / 2 : 0) : 0, qa1 = MC ? ((rank >> 1) ? P : P / 2) : P;
+      const int qb0 = MC ? ((rank & 1) ? P / 2 : 0) : 0, qb1 = MC ? ((rank & 1) ? P : P / 2) : P;
       for (int c = 0; c < p.kchunks; ++c) {
         mbar_wait(empty0 + 8 * st, ph ^ 1);
         const uint32_t fb = full0 + 8 * st;
@@ -309,13 +369,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ax = kb % p.a_ktile;
         const int ay = a_row0 + mt * kOzakiBM + (kb / p.a_ktile) * p.a_kt_rows;
         const uint32_t sa = base + st * kStageBytes;
-#pragma unroll
-        for (int q = 0; q < P; ++q) tma_load(sa + q * kBox2, &map_a, fb, ax, ay + q * p.a_rows);
         const uint32_t sb = sa + P * kBox2;
         const int bx = p.b_col0 + (p.b_ktile ? kb % p.b_ktile : kb);
         const int by = b_row0 + nt * kBN2 + (p.b_ktile ? (kb / p.b_ktile) * p.b_kt_rows : 0);
+        if (MC) {
+          for (int q = qa0; q < qa1; ++q) tma_load_mc(sa + q * kBox2, &map_a, fb, ax, ay + q * p.a_rows, mask_a);
+          for (int q = qb0; q < qb1; ++q) tma_load_mc(sb + q * kBox2, &map_b, fb, bx, by + q * p.b_rows, mask_b);
+        } else {
 #pragma unroll
-        for (int q = 0; q < P; ++q) tma_load(sb + q * kBox2, &map_b, fb, bx, by + q * p.b_rows);
+          for (int q = 0; q < P; ++q) tma_load(sa + q * kBox2, &map_a, fb, ax, ay + q * p.a_rows);
+#pragma unroll
+          for (int q = 0; q < P; ++q) tma_load(sb + q * kBox2, &map_b, fb, bx, by + q * p.b_rows);
+        }
         if (++st == NST) st = 0, ph ^= 1;
       }
     }
@@ -335,7 +400,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_mma_i8(tmem + (g - G0) * kBN2, smem_desc32(sa + q * kBox2), smem_desc32(sb + (g - q) * kBox2), idesc,
                       (c | q) != 0);
         }
-        tc_commit(empty0 + 8 * st);
+        if (MC) tc_commit_mc(empty0 + 8 * st, mask_a | mask_b);
+        else tc_commit(empty0 + 8 * st);
         if (++st == NST) st = 0, ph ^= 1;
       }
       tc_commit(accfull);
@@ -377,6 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
   }
   __syncthreads();
+  if (MC) cluster_sync_all();  // no neighbour commit may arrive after this CTA is gone
   if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
@@ -543,30 +610,55 @@ cudaError_t launch_s(const CUtensorMap& ma, const CUtensorMap& mb, const OzakiAr
 }
 
 template <int G0, int NG>
-cudaError_t launch_w(const CUtensorMap& ma, const CUtensorMap& mb, const OzakiArgs& a, int blocks, cudaStream_t st) {
-  ozaki_gemm2_kernel<G0, NG><<<blocks, kThreads, smem_bytes2(G0 + NG), st>>>(ma, mb, a);
-  return cudaGetLastError();
+cudaError_t launch_w(const CUtensorMap& ma, const CUtensorMap& mb, const OzakiArgs& a, int blocks, bool mc,
+                     cudaStream_t st) {
+  if (!mc) {
+    ozaki_gemm2_kernel<G0, NG, false><<<blocks, kThreads, smem_bytes2(G0 + NG), st>>>(ma, mb, a);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem_bytes2(G0 + NG);
+  cfg.stream = st;
+  cudaLaunchAttribute attr{};
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = 4;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, ozaki_gemm2_kernel<G0, NG, true>, ma, mb, a);
 }
 
-// groups [g0, g0 + ng) of the 128 x 128 kernel
+// groups [g0, g0 + ng) of the 128 x 128 kernel; mc: 2 x 2 clusters with multicast loads
 cudaError_t launch_window(int g0, int ng, const CUtensorMap& ma, const CUtensorMap& mb, const OzakiArgs& a,
-                          int blocks, cudaStream_t st) {
+                          int blocks, bool mc, cudaStream_t st) {
   if (g0 == 0) {
     switch (ng) {
-      case 1: return launch_w<0, 1>(ma, mb, a, blocks, st);
-      case 2: return launch_w<0, 2>(ma, mb, a, blocks, st);
-      case 3: return launch_w<0, 3>(ma, mb, a, blocks, st);
-      case 4: return launch_w<0, 4>(ma, mb, a, blocks, st);
+      case 1: return launch_w<0, 1>(ma, mb, a, blocks, mc, st);
+      case 2: return launch_w<0, 2>(ma, mb, a, blocks, mc, st);
+      case 3: return launch_w<0, 3>(ma, mb, a, blocks, mc, st);
+      case 4: return launch_w<0, 4>(ma, mb, a, blocks, mc, st);
     }
   } else if (ng == 4) {
     switch (g0) {
-      case 1: return launch_w<1, 4>(ma, mb, a, blocks, st);
-      case 2: return launch_w<2, 4>(ma, mb, a, blocks, st);
-      case 3: return launch_w<3, 4>(ma, mb, a, blocks, st);
-      case 4: return launch_w<4, 4>(ma, mb, a, blocks, st);
+      case 1: return launch_w<1, 4>(ma, mb, a, blocks, mc, st);
+      case 2: return launch_w<2, 4>(ma, mb, a, blocks, mc, st);
+      case 3: return launch_w<3, 4>(ma, mb, a, blocks, mc, st);
+      case 4: return launch_w<4, 4>(ma, mb, a, blocks, mc, st);
     }
   }
   return cudaErrorInvalidValue;
+}
+
+// GPB_OZAKI_CLUSTER=0: no clusters (every CTA loads all of its planes)
+bool use_clusters() {
+  static const bool v = [] {
+    const char* e = getenv("GPB_OZAKI_CLUSTER");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
 }
 
 // GPB_OZAKI_KERNEL=1: the 128 x 64 single-launch kernel for every product
@@ -582,9 +674,12 @@ int kernel_shape() {
 
 cudaError_t ozaki_init_attributes() {
   cudaError_t e;
-#define GPB_OZ_ATTR2(G0, NG)                                                                                  \
-  if ((e = cudaFuncSetAttribute(ozaki_gemm2_kernel<G0, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                                static_cast<int>(smem_bytes2(G0 + NG)))) != cudaSuccess)                     \
+#define GPB_OZ_ATTR2(G0, NG)                                                                                    \
+  if ((e = cudaFuncSetAttribute(ozaki_gemm2_kernel<G0, NG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                static_cast<int>(smem_bytes2(G0 + NG)))) != cudaSuccess)                       \
+    return e;                                                                                                   \
+  if ((e = cudaFuncSetAttribute(ozaki_gemm2_kernel<G0, NG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                static_cast<int>(smem_bytes2(G0 + NG)))) != cudaSuccess)                       \
     return e;
   GPB_OZ_ATTR2(0, 1) GPB_OZ_ATTR2(0, 2) GPB_OZ_ATTR2(0, 3) GPB_OZ_ATTR2(0, 4)
   GPB_OZ_ATTR2(1, 4) GPB_OZ_ATTR2(2, 4) GPB_OZ_ATTR2(3, 4) GPB_OZ_ATTR2(4, 4)
@@ -657,14 +752,15 @@ cudaError_t launch_ozaki_gemm(const OzakiGemm& g, cudaStream_t st, bool* used) {
     const int blocks = a.blocks_per_job * (g.jobs ? g.njobs : 1);
     const int g0 = g.slices - 4;
     const double unit = a.alpha;
+    const bool mc = use_clusters() && (g.M / kOzakiBM) % 2 == 0 && (g.N / kBN2) % 2 == 0;
     a.alpha = std::ldexp(unit, -7 * g0);
-    cudaError_t e = launch_window(g0, 4, ma, mb, a, blocks, st);
+    cudaError_t e = launch_window(g0, 4, ma, mb, a, blocks, mc, st);
     if (e == cudaSuccess && g0 > 0) {
       a.alpha = unit;
       a.beta = 1.0;
       a.Cin = g.Cout;
       a.ldc_in = g.ldc_out;
-      e = launch_window(0, g0, ma, mb, a, blocks, st);
+      e = launch_window(0, g0, ma, mb, a, blocks, mc, st);
     }
     *used = e == cudaSuccess;
     return e;

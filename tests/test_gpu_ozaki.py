@@ -102,3 +102,93 @@ def test_plane_count_validation(runtime):
         model.digit_planes = 3
     with pytest.raises(gpb.errors.InvalidConfig):
         model.digit_planes = 9
+
+
+# ---- the factorisation's trailing updates on the int8 pipe ------------------
+# taskgp tiled.py:187-204 (SYRK/GEMM updates).  With 512-wide internal tiles a
+# group of two panels gives K = 1024, the shortest update that takes the
+# digit-plane path; north-star bars: factor <= 1e-10 relative Frobenius, loss
+# and gradients <= 1e-9 relative.
+
+
+def _train_model(n, d, tiles, planes, seed=0, params=(1.0, 1.0, 0.1)):
+    train, _ = gpb.make_msd_dataset(n, 0, d, seed=seed)
+    model = gpb.GPModel(train, gpb.KernelParams(*params), tiles_per_dim=tiles)
+    if planes is not None:
+        model.digit_planes = planes
+    return model, train
+
+
+def test_planes_are_the_default(runtime):
+    model, _ = _train_model(256, 4, 2, None)
+    model.log_likelihood()
+    assert model.digit_planes == 8
+
+
+@pytest.mark.parametrize("n,d,tiles", [(8192, 8, 16), (6144, 4, 12), (8192, 8, 32)])
+def test_factor_with_planes_matches_oracle_and_dmma(runtime, n, d, tiles):
+    model, train = _train_model(n, d, tiles, 8)
+    before = model.launch_count()
+    L = model.cholesky()
+    with_planes = model.launch_count() - before
+    assert model.digit_plane_fallbacks() == 0
+    nll = model.compute_loss()
+    ref = OracleGP(train.z, train.y, tiles)
+    assert rel_fro(L, ref.factor_dense()) <= 1e-10
+    assert abs(nll + ref.log_likelihood()) <= 1e-9 * abs(ref.log_likelihood())
+    model.digit_planes = 0
+    model.params = gpb.KernelParams(1.0, 1.0, 0.1)  # drop the cached factor
+    before = model.launch_count()
+    Ld = model.cholesky()
+    assert model.launch_count() - before < with_planes  # slicing + two window launches per update
+    assert rel_fro(L, Ld) <= 1e-11
+
+
+def test_gradients_and_adam_with_planes(runtime):
+    """Config-1 shape: loss gradients and three Adam steps from a digit-plane factor."""
+    model, train = _train_model(8192, 8, 32, 8)
+    g = np.array(model.loss_gradients())
+    hist = model.optimize(gpb.AdamConfig(learning_rate=0.1, iterations=3))
+    dm, _ = _train_model(8192, 8, 32, 0)
+    gd = np.array(dm.loss_gradients())
+    hd = dm.optimize(gpb.AdamConfig(learning_rate=0.1, iterations=3))
+    assert np.max(np.abs(g - gd) / np.abs(gd)) <= 1e-9
+    assert np.max(np.abs(np.array(hist) - np.array(hd)) / np.abs(np.array(hd))) <= 1e-9
+    ref = OracleGP(train.z, train.y, 32)
+    go = np.array(ref.loss_gradients())
+    assert np.max(np.abs(g - go) / np.abs(go)) <= 1e-9
+
+
+def test_factor_with_planes_bitwise_reproducible(runtime):
+    model, _ = _train_model(8192, 8, 16, 8)
+    a = model.cholesky()
+    model.params = gpb.KernelParams(1.0, 1.0, 0.1)
+    b = model.cholesky()
+    assert np.array_equal(a, b)
+
+
+def test_not_positive_definite_with_planes(runtime):
+    """Duplicate inputs and zero noise: the digit-plane factorisation must still
+    report NotPositiveDefinite (the DMMA repeat names the pivot)."""
+    rng = np.random.default_rng(5)
+    z = rng.normal(size=(8192, 4))
+    z[5000] = z[100]
+    model = gpb.GPModel(gpb.Dataset(z=z, y=rng.normal(size=8192)),
+                        gpb.KernelParams(1.0, 1.0, 0.0), tiles_per_dim=16)
+    model.digit_planes = 8
+    with pytest.raises(gpb.errors.NotPositiveDefinite):
+        model.cholesky()
+    model.params = gpb.KernelParams(1.0, 1.0, 0.1)
+    assert np.isfinite(model.log_likelihood())
+
+
+def test_other_parameters_factor(runtime):
+    model, train = _train_model(8192, 8, 16, 8, params=(0.7, 5.0, 0.02))
+    L = model.cholesky()
+    assert model.digit_plane_fallbacks() == 0
+    ref = OracleGP(train.z, train.y, 16, l=0.7, nu=5.0, s2=0.02)
+    model.digit_planes = 0
+    model.params = gpb.KernelParams(0.7, 5.0, 0.02)
+    Ld = model.cholesky()
+    assert rel_fro(L, Ld) <= 1e-10
+    assert rel_fro(L, ref.factor_dense()) <= 1e-10
