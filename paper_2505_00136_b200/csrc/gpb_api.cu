@@ -490,11 +490,11 @@ int build_chol_plan(gpb_model* m) {
           j.K = grp.np * bi;
           j.lower = (i == jj);
           jobs.push_back(j);
-          // rows of the panel-plane byte view (pitch bi): panel 0 of the set
+          // byte offsets into the panel planes (ensure_factor): tile slot of panel 0 of the set
           OzakiJob o{};
-          const int64_t set_row = int64_t(s % 2) * G * (pstride / bi);
-          o.a_row0 = static_cast<int>(set_row + int64_t(i - k0 - 1) * bi);
-          o.b_row0 = static_cast<int>(set_row + int64_t(jj - k0 - 1) * bi);
+          const int64_t tile_b = bi2 * m->oz_slices, panel_b = int64_t(std::max(1, Ti - 1)) * tile_b;
+          o.a_off = int64_t(s % 2) * G * panel_b + int64_t(i - k0 - 1) * tile_b;
+          o.b_off = int64_t(s % 2) * G * panel_b + int64_t(jj - k0 - 1) * tile_b;
           o.C = j.Cout;
           o.lower = j.lower;
           ozjobs.resize(jobs.size());
@@ -637,7 +637,10 @@ int ensure_factor(gpb_model* m) {
   // are final entries of L, |L(i, j)| <= sqrt(K_ii) = sqrt(vertical + noise)
   // (1 on the decoupled padding rows), so one fixed-point scale covers them.
   bool oz = m->oz_slices > 0 && m->oz_chol;
-  const int64_t plane_stride = 2 * int64_t(m->G) * pstride;  // bytes per digit plane
+  // panel planes (boxed layout, ozaki.cuh): per scratch set and panel g of the
+  // group, Ti - 1 tile slots of bi x bi; slot t of panel g holds L(k0 + 1 + t, k0 + g)
+  const int S = m->oz_slices;
+  const int64_t tile_bytes = bi2 * S, panel_bytes = int64_t(std::max(1, Ti - 1)) * tile_bytes;
   if (oz) {
     bool any = false;
     for (const CholGroup& grp : m->groups)
@@ -645,34 +648,28 @@ int ensure_factor(gpb_model* m) {
     oz = any;
   }
   if (oz) {
-    CUDA_TRY(m->Ps.ensure(size_t(m->oz_slices) * plane_stride));
+    CUDA_TRY(m->Ps.ensure(size_t(2) * m->G * panel_bytes));
     if (!m->ozflag.p) {
       CUDA_TRY(m->ozflag.ensure(sizeof(int)));
       CUDA_TRY(cudaMemsetAsync(m->ozflag.p, 0, sizeof(int), m->st));
     }
     m->oz_sa = pow2_ceil(2.0 * std::max(1.0, std::sqrt(m->nu + m->s2)) * (1.0 + 1e-9));
   }
-  // L(i,j) -= [X]_i [X]_j^T for `cnt` plan jobs from `off`; *done = false: not launched
-  auto oz_update = [&](const CholGroup& grp, int64_t off, int64_t cnt, double flops, cudaStream_t s,
-                       bool* done) -> int {
-    *done = false;
+  // L(i,j) -= [X]_i [X]_j^T for `cnt` plan jobs from `off`
+  auto oz_update = [&](const CholGroup& grp, int64_t off, int64_t cnt, double flops, cudaStream_t s) -> int {
     OzakiGemm g{};
-    g.a_planes = g.b_planes = m->Ps.as<int8_t>();
-    g.a_pitch = g.b_pitch = bi;
-    g.a_rows = g.b_rows = plane_stride / bi;
-    g.a_ktile = g.b_ktile = bi;
-    g.a_kt_rows = g.b_kt_rows = static_cast<int>(pstride / bi - bi);
+    g.a = g.b = {m->Ps.as<int8_t>(), panel_bytes, bi / kOzakiBK, int64_t(bi / kOzakiBK) * S * kOzakiBox};
     g.M = g.N = bi;
     g.K = grp.np * bi;
-    g.slices = m->oz_slices;
+    g.slices = S;
     g.alpha = -m->oz_sa * m->oz_sa;
     g.beta = 1.0;
     g.ldc_in = g.ldc_out = bi;
     g.jobs = m->oz_jobs.as<OzakiJob>() + off;
     g.njobs = static_cast<int>(cnt);
     ProfScope ps(m, KC_OZAKI, flops, s);
-    CUDA_TRY(launch_ozaki_gemm(g, s, done));
-    if (*done) ++m->launches;
+    CUDA_TRY(launch_ozaki_gemm(g, s));
+    m->launches += S > 4 ? 2 : 1;
     return GPB_OK;
   };
   for (int s = 0; s < ng; ++s) {
@@ -713,10 +710,9 @@ int ensure_factor(gpb_model* m) {
     if (oz_grp) {  // digit planes of the group's solved panels
       ProfScope ps(m, KC_OTHER, 0.0, m->crit);
       for (int g = 0; g < grp.np; ++g) {
-        const int64_t eoff = (set - m->scratch.as<double>()) + g * pstride;
-        CUDA_TRY(launch_ozaki_slice(m->scratch.as<double>() + eoff, int64_t(Ti - (grp.k0 + g) - 1) * bi2,
-                                    m->oz_sa, m->Ps.as<int8_t>() + eoff, plane_stride, m->oz_slices,
-                                    m->ozflag.as<int>(), m->crit));
+        int8_t* dst = m->Ps.as<int8_t>() + (int64_t(s % 2) * m->G + g) * panel_bytes + int64_t(g) * tile_bytes;
+        CUDA_TRY(launch_ozaki_slice_tiles(set + g * pstride, Ti - (grp.k0 + g) - 1, bi, bi, m->oz_sa, dst, S,
+                                          m->ozflag.as<int>(), m->crit));
         ++m->launches;
       }
     }
@@ -724,9 +720,9 @@ int ensure_factor(gpb_model* m) {
     // lookahead: the next group's columns need UPD(s-1), which covered them
     if (grp.next_cnt > 0) {
       if (s >= 1) CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[s - 1], 0));
-      bool done = false;
-      if (oz_grp) GPB_TRY(oz_update(grp, grp.next_off, grp.next_cnt, grp.next_fl, m->crit, &done));
-      if (!done) {
+      if (oz_grp) {
+        GPB_TRY(oz_update(grp, grp.next_off, grp.next_cnt, grp.next_fl, m->crit));
+      } else {
         GemmParams np = walk(base_params(jobs + grp.next_off, static_cast<int>(grp.next_cnt), nb, nb,
                                          bi, bi, bi, -1.0, 1.0));
         GPB_TRY(gemm(m, np, true, true, EPI_AXPBY, grp.next_fl, m->crit));
@@ -739,9 +735,9 @@ int ensure_factor(gpb_model* m) {
       ++m->launches;
     }
     if (grp.upd_cnt > 0) {
-      bool done = false;
-      if (oz_grp) GPB_TRY(oz_update(grp, grp.upd_off, grp.upd_cnt, grp.upd_fl, m->st, &done));
-      if (!done) {
+      if (oz_grp) {
+        GPB_TRY(oz_update(grp, grp.upd_off, grp.upd_cnt, grp.upd_fl, m->st));
+      } else {
         GemmParams up = walk(base_params(jobs + grp.upd_off, static_cast<int>(grp.upd_cnt), nb, nb,
                                          bi, bi, bi, -1.0, 1.0));
         GPB_TRY(gemm(m, up, true, true, EPI_AXPBY, grp.upd_fl));
@@ -1223,10 +1219,13 @@ int ensure_l_planes(gpb_model* m) {
   }
   m->oz_sa = pow2_ceil(2.0 * std::max(1.0, std::sqrt(m->nu + m->s2)) * (1.0 + 1e-9));
   ProfScope ps(m, KC_OTHER, 0.0);
+  // tile t of the packed factor -> tile t of the boxed planes; one launch per
+  // block row (its off-diagonal tiles are consecutive)
   for (int i = 1; i < m->Ti; ++i) {
-    const int64_t off = h_tri_rm(i, 0) * bi2;
-    CUDA_TRY(launch_ozaki_slice(m->L.as<double>() + off, int64_t(i) * bi2, m->oz_sa, m->Ls.as<int8_t>() + off,
-                                ntiles * bi2, m->oz_slices, m->ozflag.as<int>(), m->st));
+    const int64_t t0 = h_tri_rm(i, 0);
+    CUDA_TRY(launch_ozaki_slice_tiles(m->L.as<double>() + t0 * bi2, i, m->bi, m->bi, m->oz_sa,
+                                      m->Ls.as<int8_t>() + t0 * bi2 * m->oz_slices, m->oz_slices,
+                                      m->ozflag.as<int>(), m->st));
     ++m->launches;
   }
   m->ls_ok = true;
@@ -1234,46 +1233,35 @@ int ensure_l_planes(gpb_model* m) {
 }
 
 // W = B_i - L[i, 0..i) V[0..i) on the tcgen05 pipe, in k segments of at most
-// kOzakiMaxK (int32 group sums stay exact); *done = false: not launched
+// kOzakiMaxK (int32 group sums stay exact)
 int ozaki_pred_w(gpb_model* m, int i, int64_t mcp, bool* done) {
   *done = false;
   const int bi = m->bi;
   const int64_t bi2 = int64_t(bi) * bi;
-  const int64_t ntiles = int64_t(m->Ti) * (m->Ti + 1) / 2;
   const int64_t K = int64_t(i) * bi;
   double* W = m->W.as<double>();
+  const int S = m->oz_slices;
+  const int64_t kchunks = m->np_ / kOzakiBK;
   for (int64_t k0 = 0; k0 < K; k0 += kOzakiMaxK) {
     OzakiGemm g{};
-    g.a_planes = m->Ls.as<int8_t>();
-    g.a_pitch = bi;
-    g.a_rows = ntiles * bi;
-    g.a_row0 = (h_tri_rm(i, 0) + k0 / bi) * bi;
-    g.a_ktile = bi;
-    g.a_kt_rows = bi;
-    g.b_planes = m->Vs.as<int8_t>();
-    g.b_pitch = m->np_;
-    g.b_rows = mcp;
-    g.b_row0 = 0;
-    g.b_col0 = k0;
+    g.a = {m->Ls.as<int8_t>(), bi2 * S, bi / kOzakiBK, int64_t(bi / kOzakiBK) * S * kOzakiBox};
+    g.a_off = (h_tri_rm(i, 0) + k0 / bi) * bi2 * S;
+    g.b = {m->Vs.as<int8_t>(), 0, static_cast<int>(kchunks), kchunks * S * kOzakiBox};
+    g.b_off = (k0 / kOzakiBK) * S * kOzakiBox;
     g.M = bi;
     g.N = static_cast<int>(mcp);
     g.K = static_cast<int>(std::min<int64_t>(kOzakiMaxK, K - k0));
-    g.slices = m->oz_slices;
+    g.slices = S;
     g.alpha = -m->oz_sa * m->oz_sb;
     g.beta = 1.0;
     g.Cin = k0 == 0 ? m->Bv.as<double>() + int64_t(i) * bi * mcp : W;
     g.Cout = W;
     g.ldc_in = g.ldc_out = mcp;
-    bool used = false;
     {
       ProfScope ps(m, KC_OZAKI, 2.0 * double(bi) * double(mcp) * double(g.K));
-      CUDA_TRY(launch_ozaki_gemm(g, m->st, &used));
+      CUDA_TRY(launch_ozaki_gemm(g, m->st));
     }
-    if (!used) {
-      if (k0 == 0) return GPB_OK;  // no tensor maps: the caller runs the DMMA product
-      return fail(GPB_CUDA, "tensor-map encoding failed in the middle of a digit-plane product");
-    }
-    ++m->launches;
+    m->launches += S > 4 ? 2 : 1;
   }
   *done = true;
   return GPB_OK;
@@ -1389,8 +1377,8 @@ int predict_chunk(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var,
       if (oz && i + 1 < Ti) {  // planes of V_i^T for the rows below
         ProfScope ps(m, KC_OTHER, 0.0);
         CUDA_TRY(launch_ozaki_slice_t(Bv + int64_t(i) * bi * mcp, bi, mcp, mcp, m->oz_sb, m->Vs.as<int8_t>(),
-                                      mcp * m->np_, m->np_, int64_t(i) * bi, m->oz_slices,
-                                      m->ozflag.as<int>(), m->st));
+                                      m->np_ / kOzakiBK, int64_t(i) * bi, m->oz_slices, m->ozflag.as<int>(),
+                                      m->st));
         ++m->launches;
       }
     }
@@ -2051,7 +2039,7 @@ int gpb_model_set_ozaki(gpb_model* m, int slices) {
   GPB_TRY(check_live(m));
   if (slices != 0 && (slices < 4 || slices > kOzakiMaxSlices))
     return fail(GPB_INVALID_CONFIG, "digit planes: 0 (off) or 4..8");
-  if (slices != m->oz_slices) m->ls_ok = false;
+  if (slices != m->oz_slices) m->ls_ok = m->plan_ok = false;  // plane offsets depend on the count
   m->oz_slices = slices;
   return GPB_OK;
 }

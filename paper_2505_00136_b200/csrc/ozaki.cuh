@@ -1,9 +1,10 @@
 // FP64 products on the 5th-generation tensor cores (tcgen05.mma kind::i8,
-// accumulators in TMEM): the long-K prediction product
+// accumulators in TMEM): the long-K products of the path,
 //
-//   W = Cin - L[i, 0..i) V[0..i)            (taskgp tiled.py:263-298)
+//   W = Cin - L[i, 0..i) V[0..i)          prediction sweep   (taskgp tiled.py:263-298)
+//   L(i,j) -= [X]_i [X]_j^T               trailing updates   (taskgp tiled.py:187-204)
 //
-// computed from signed 7-bit digit planes of its operands (Ozaki splitting
+// computed from signed 7-bit digit planes of their operands (Ozaki splitting
 // with a fixed-point scale per operand buffer):
 //
 //   x = sx * sum_{p=1..S} d_p(x) 2^(-7p) + r,   d_p in [-64, 64],  |r| <= sx 2^(-7S-1)
@@ -12,13 +13,24 @@
 //
 // The digit extraction is exact (power-of-two scalings, round-to-nearest and
 // the subtraction of the rounded value), the int32 group sums are exact for
-// K <= kOzakiMaxK, and the groups are combined once, in FP64, least
-// significant first.  The only errors are the dropped remainder r of each
-// operand and the dropped digit pairs p+q > S+1: both below 2^(-7S+3) relative to
-// sa sb per term (S = 8: 2^-53).  No FP64 tcgen05 kind exists on sm_100a, so this is
-// how the path reaches the tcgen05 pipe at all; the DMMA kernels stay the
-// default and the reference for parity (GPB_OZAKI=1 / gpb_model_set_ozaki
-// opt in).
+// K <= kOzakiMaxK, and the groups are combined in FP64, least significant
+// first.  The only errors are the dropped remainder r of each operand and the
+// dropped digit pairs p+q > S+1: both below 2^(-7S+3) relative to sa sb per
+// term (S = 8: 2^-53).  No FP64 tcgen05 kind exists on sm_100a, so this is how
+// the path reaches the tcgen05 pipe at all; the FP64 DMMA kernels remain for
+// the short products and behind GPB_OZAKI=0 / gpb_model_set_ozaki(m, 0).
+//
+// Plane layout ("boxed").  An operand is a matrix of rows x K int8 digits per
+// plane, rows in blocks of 128, k in chunks of 32.  The S planes of one (row
+// block, k chunk) are S consecutive 4 KB boxes, each box the shared-memory
+// image the MMA reads (128 rows of 32 bytes, SWIZZLE_32B), so a CTA fetches
+// the planes of a chunk with ONE contiguous bulk copy per operand.  (Planes
+// kept in the operand's own row-major order and fetched as 128 x 32-byte TMA
+// boxes issue one L2 request per 32-byte row: ncu showed the L2 tag pipeline
+// at 73% with the tensor pipe 43-66% active.)  Operands are tiled: tile t
+// (tr rows x tc columns of k) occupies tr * tc * S bytes, its boxes ordered
+// [row block][k chunk][plane]; a k walk visits tc / 32 chunks of a tile, then
+// jumps tile_stride bytes to the next tile.
 #pragma once
 #include <cuda.h>
 
@@ -27,60 +39,58 @@
 namespace gpb {
 
 constexpr int kOzakiMaxSlices = 8;
-constexpr int kOzakiBM = 128, kOzakiBN = 64, kOzakiBK = 64;
+constexpr int kOzakiBM = 128, kOzakiBN = 128, kOzakiBK = 32;
+constexpr int kOzakiBox = kOzakiBM * kOzakiBK;  // bytes
 // |G_t| <= S * K * 64 * 64 < 2^31
 constexpr int64_t kOzakiMaxK = 32768;
 
-// Digit planes of a contiguous array, same element order as the source:
-// plane p (0-based) of element e at planes[p * plane_stride + e].
-// *flag is set to 1 when an element exceeds scale / 2 (digits saturate).
-cudaError_t launch_ozaki_slice(const double* src, int64_t count, double scale, int8_t* planes,
-                               int64_t plane_stride, int slices, int* flag, cudaStream_t st);
+// Digit planes of `ntiles` consecutive row-major tiles of tr x tc doubles
+// (tr a multiple of 128, tc of 32) into the boxed layout at `planes` (tile t
+// at planes + t * tr * tc * slices).  *flag is set to 1 when an element
+// exceeds scale / 2 (digits saturate).
+cudaError_t launch_ozaki_slice_tiles(const double* src, int64_t ntiles, int tr, int tc, double scale,
+                                     int8_t* planes, int slices, int* flag, cudaStream_t st);
 
-// Digit planes of a (rows x cols, row-major, ld) block, TRANSPOSED: plane p of
-// element (k, c) at planes[p * plane_stride + c * out_ld + k0 + k]  (the
-// K-major B operand of the product: one row per column c, k contiguous).
-// rows must be a multiple of 64, cols a multiple of 64.
+// Digit planes of a (rows x cols, row-major, ld) block of doubles TRANSPOSED:
+// operand row = source column c, k = k0 + source row.  One tile spans the
+// whole K range: box of (c / 128, k / 32) at planes + ((c / 128) * kchunks +
+// k / 32) * slices * 4096.  rows and k0 multiples of 64, cols of 128.
 cudaError_t launch_ozaki_slice_t(const double* src, int rows, int64_t cols, int64_t ld, double scale,
-                                 int8_t* planes, int64_t plane_stride, int64_t out_ld, int64_t k0,
-                                 int slices, int* flag, cudaStream_t st);
+                                 int8_t* planes, int64_t kchunks, int64_t k0, int slices, int* flag,
+                                 cudaStream_t st);
+
+struct OzakiOperand {
+  const int8_t* planes;
+  int64_t tile_stride;  // bytes from a tile to the next one along k
+  int chunks_per_tile;  // tc / 32
+  int64_t rb_stride;    // bytes from a row block to the next one inside a tile: chunks_per_tile * slices * 4096
+};
 
 struct OzakiJob {
-  int a_row0, b_row0;
+  int64_t a_off, b_off;  // byte offsets of the job's first row block at k = 0
   double* C;
   int lower, pad;
 };
 
 struct OzakiGemm {
-  // A planes: 2-D byte view (a_pitch bytes per row, a_rows rows per plane,
-  // planes stacked along rows); the M x K operand starts at row a_row0,
-  // column 0, and k walks a_ktile bytes per tile, a_kt_rows rows down per tile
-  const int8_t* a_planes;
-  int64_t a_pitch, a_rows, a_row0;
-  int a_ktile, a_kt_rows;
-  // B planes: N x K rows starting at row b_row0, column b_col0; plain walk
-  // along the row when b_ktile == 0, else tiled like A
-  const int8_t* b_planes;
-  int64_t b_pitch, b_rows, b_row0, b_col0;
-  int b_ktile = 0, b_kt_rows = 0;
-  int M, N, K;     // multiples of 128 / 64 / 64; K <= kOzakiMaxK
+  OzakiOperand a, b;     // A: M rows, B: N rows, both K-major
+  int64_t a_off, b_off;  // byte offsets of row block 0 at k = 0 (ignored with jobs)
+  int M, N, K;           // multiples of 128 / 128 / 32; K <= kOzakiMaxK
   int slices;
-  double alpha;    // Cout = beta * Cin + alpha * sa sb * sum (caller folds sa sb in)
+  double alpha;  // Cout = beta * Cin + alpha * sum (the caller folds the scales sa sb into alpha)
   double beta;
   const double* Cin;
   double* Cout;
   int64_t ldc_in, ldc_out;
-  // grouped form (the factorisation's trailing update, tiled.py:187-204): njobs
-  // independent M x N products sharing the plane buffers, job j reading A rows
-  // from jobs[j].a_row0, B rows from jobs[j].b_row0 (a_row0 / b_row0 above are
-  // ignored) and updating C in place: C = beta C + alpha sum, ldc_in = ldc_out.
-  // A `lower` job skips the 128 x 64 blocks above the diagonal 128-block.
+  // grouped form (the factorisation's trailing updates): njobs independent
+  // M x N products sharing the operand descriptions, job j reading its rows
+  // from jobs[j].a_off / b_off and updating C in place (beta != 0, ldc_in =
+  // ldc_out).  A `lower` job skips the blocks above the diagonal.
   const OzakiJob* jobs = nullptr;  // device array
   int njobs = 0;
 };
 
-// false (nothing launched) when the driver entry point for tensor maps is missing
-cudaError_t launch_ozaki_gemm(const OzakiGemm& g, cudaStream_t st, bool* used);
+cudaError_t launch_ozaki_gemm(const OzakiGemm& g, cudaStream_t st);
 cudaError_t ozaki_init_attributes();
 
 }  // namespace gpb
