@@ -221,9 +221,12 @@ struct gpb_model {
   DevBuf Ls, Vs, ozflag;
   // ... and of the solved panels of the current group (same element order as
   // `scratch`), read by the trailing updates NEXT / UPD of the factorisation
-  DevBuf Ps, oz_jobs;
-  int64_t oz_chol_min_k = 1024;  // updates with a shorter K = np * bi stay on the DMMA kernel
+  DevBuf Ps, oz_jobs, fc_oz_jobs;
+  bool vs_ok = false;  // Vs holds the planes of every row block of the current V (Bv)
+  int64_t oz_chol_min_k = 512;  // updates with a shorter K = np * bi stay on the DMMA kernel
   bool oz_chol = true;           // GPB_OZAKI_CHOL=0: digit planes for the prediction sweep only
+  bool oz_chol_in = true;        // GPB_OZAKI_CHOL_IN=0: in-group updates (K = bi) stay on the DMMA kernel
+  int64_t oz_chol_in_min_k = 512;
   int oz_slices = 8;   // planes per operand (GPB_OZAKI; 0: every product on the FP64 DMMA kernels)
   bool ls_ok = false;  // Ls holds the planes of the current factor
   double oz_sa = 0.0, oz_sb = 0.0;
@@ -265,6 +268,17 @@ int check_live(gpb_model* m) {
 // parameter (results are tiling-invariant to round-off,
 // test_acceptance.py:135-169); when 128 does not divide the user tile, n is
 // padded once at the end with decoupled identity rows.
+// Panels per trailing-update group.  On the DMMA kernels: plan_common.h (shared
+// with the multi-GPU schedule).  With the updates on the int8 pipe a longer
+// K = G bi amortises the block prologue / epilogue of the digit-plane product
+// and the in-group updates cost little there: 8 panels from 48 tiles (config
+// 2: 168.5 -> 162.7 ms against G = 4), 4 from 16.
+int choose_panels(const gpb_model* m) {
+  const int g = chol_panels(m->Ti);
+  if (getenv("GPB_PANELS") || m->oz_slices == 0 || !m->oz_chol) return g;
+  return m->Ti >= 48 ? 8 : m->Ti >= 16 ? 4 : g;
+}
+
 int apply_layout(gpb_model* m) {
   int64_t lay[6];
   if (int s = gpb_layout(m->n, m->T, lay)) return s;
@@ -273,7 +287,7 @@ int apply_layout(gpb_model* m) {
   m->np_ = lay[2];
   m->pm.bp_user = static_cast<int>(lay[3]);
   m->pm.b_user = static_cast<int>(lay[4]);
-  m->G = chol_panels(m->Ti);  // plan_common.h
+  m->G = choose_panels(m);
   return GPB_OK;
 }
 
@@ -474,6 +488,15 @@ int build_chol_plan(gpb_model* m) {
           j.K = bi;
           j.lower = (i == jj);
           jobs.push_back(j);
+          // the same update from the planes of panel g alone (K = bi: one tile)
+          OzakiJob o{};
+          const int64_t tile_b = bi2 * m->oz_slices, panel_b = int64_t(std::max(1, Ti - 1)) * tile_b;
+          o.a_off = (int64_t(s % 2) * G + g) * panel_b + int64_t(i - k0 - 1) * tile_b;
+          o.b_off = (int64_t(s % 2) * G + g) * panel_b + int64_t(jj - k0 - 1) * tile_b;
+          o.C = j.Cout;
+          o.lower = j.lower;
+          ozjobs.resize(jobs.size());
+          ozjobs.back() = o;
         }
       grp.in_cnt[g] = jobs.size() - grp.in_off[g];
     }
@@ -596,8 +619,9 @@ struct PhaseTimer {
   }
 };
 
-// smallest power of two >= x
-double pow2_ceil(double x) { return std::exp2(std::ceil(std::log2(x))); }
+// fixed-point scale of an operand bounded by `bound`: digits cover |x| <= scale * 127 / 128
+// (ozaki.cuh); the margin absorbs round-off in entries that reach the bound
+double plane_scale(double bound) { return bound * (128.0 / 127.0) * (1.0 + 1e-9); }
 
 // assemble + factor (model.py:169-177 _ensure_factor)
 int ensure_factor(gpb_model* m) {
@@ -653,14 +677,14 @@ int ensure_factor(gpb_model* m) {
       CUDA_TRY(m->ozflag.ensure(sizeof(int)));
       CUDA_TRY(cudaMemsetAsync(m->ozflag.p, 0, sizeof(int), m->st));
     }
-    m->oz_sa = pow2_ceil(2.0 * std::max(1.0, std::sqrt(m->nu + m->s2)) * (1.0 + 1e-9));
+    m->oz_sa = plane_scale(std::max(1.0, std::sqrt(m->nu + m->s2)));
   }
   // L(i,j) -= [X]_i [X]_j^T for `cnt` plan jobs from `off`
-  auto oz_update = [&](const CholGroup& grp, int64_t off, int64_t cnt, double flops, cudaStream_t s) -> int {
+  auto oz_update = [&](int K, int64_t off, int64_t cnt, double flops, cudaStream_t s) -> int {
     OzakiGemm g{};
     g.a = g.b = {m->Ps.as<int8_t>(), panel_bytes, bi / kOzakiBK, int64_t(bi / kOzakiBK) * S * kOzakiBox};
     g.M = g.N = bi;
-    g.K = grp.np * bi;
+    g.K = K;
     g.slices = S;
     g.alpha = -m->oz_sa * m->oz_sa;
     g.beta = 1.0;
@@ -676,6 +700,8 @@ int ensure_factor(gpb_model* m) {
     const CholGroup& grp = m->groups[s];
     double* set = m->scratch.as<double>() + int64_t(s % 2) * m->G * pstride;
     const bool oz_grp = oz && int64_t(grp.np) * bi >= m->oz_chol_min_k && grp.next_cnt + grp.upd_cnt > 0;
+    // in-group updates (K = bi) from the planes too when the group has them and bi is long enough
+    const bool oz_in = oz_grp && m->oz_chol_in && bi >= m->oz_chol_in_min_k;
     // the group's columns are complete once NEXT(s-1) (crit, in order) and UPD(s-2) are done
     if (s >= 2) CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[s - 2], 0));
     for (int g = 0; g < grp.np; ++g) {
@@ -702,18 +728,22 @@ int ensure_factor(gpb_model* m) {
                                         bi, bi, bi, 1.0, 0.0),
                             m->L, m->Dinv);
       GPB_TRY(gemm(m, tp, true, true, EPI_AXPBY, grp.trsm_fl[g], m->crit));
-      GemmParams ip = views(base_params(jobs + grp.in_off[g], static_cast<int>(grp.in_cnt[g]), nb, nb, bi,
-                                        bi, bi, -1.0, 1.0),
-                            m->scratch, m->scratch);
-      GPB_TRY(gemm(m, ip, true, true, EPI_AXPBY, grp.in_fl[g], m->crit));
-    }
-    if (oz_grp) {  // digit planes of the group's solved panels
-      ProfScope ps(m, KC_OTHER, 0.0, m->crit);
-      for (int g = 0; g < grp.np; ++g) {
+      if (oz_grp) {  // digit planes of the solved panel
+        ProfScope ps(m, KC_OTHER, 0.0, m->crit);
         int8_t* dst = m->Ps.as<int8_t>() + (int64_t(s % 2) * m->G + g) * panel_bytes + int64_t(g) * tile_bytes;
-        CUDA_TRY(launch_ozaki_slice_tiles(set + g * pstride, Ti - (grp.k0 + g) - 1, bi, bi, m->oz_sa, dst, S,
+        CUDA_TRY(launch_ozaki_slice_tiles(set + g * pstride, Ti - k - 1, bi, bi, m->oz_sa, dst, S,
                                           m->ozflag.as<int>(), m->crit));
         ++m->launches;
+      }
+      if (grp.in_cnt[g] > 0) {
+        if (oz_in) {
+          GPB_TRY(oz_update(bi, grp.in_off[g], grp.in_cnt[g], grp.in_fl[g], m->crit));
+        } else {
+          GemmParams ip = views(base_params(jobs + grp.in_off[g], static_cast<int>(grp.in_cnt[g]), nb, nb, bi,
+                                            bi, bi, -1.0, 1.0),
+                                m->scratch, m->scratch);
+          GPB_TRY(gemm(m, ip, true, true, EPI_AXPBY, grp.in_fl[g], m->crit));
+        }
       }
     }
     CUDA_TRY(cudaEventRecord(ev_panel[s], m->crit));
@@ -721,7 +751,7 @@ int ensure_factor(gpb_model* m) {
     if (grp.next_cnt > 0) {
       if (s >= 1) CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[s - 1], 0));
       if (oz_grp) {
-        GPB_TRY(oz_update(grp, grp.next_off, grp.next_cnt, grp.next_fl, m->crit));
+        GPB_TRY(oz_update(grp.np * bi, grp.next_off, grp.next_cnt, grp.next_fl, m->crit));
       } else {
         GemmParams np = walk(base_params(jobs + grp.next_off, static_cast<int>(grp.next_cnt), nb, nb,
                                          bi, bi, bi, -1.0, 1.0));
@@ -736,7 +766,7 @@ int ensure_factor(gpb_model* m) {
     }
     if (grp.upd_cnt > 0) {
       if (oz_grp) {
-        GPB_TRY(oz_update(grp, grp.upd_off, grp.upd_cnt, grp.upd_fl, m->st));
+        GPB_TRY(oz_update(grp.np * bi, grp.upd_off, grp.upd_cnt, grp.upd_fl, m->st));
       } else {
         GemmParams up = walk(base_params(jobs + grp.upd_off, static_cast<int>(grp.upd_cnt), nb, nb,
                                          bi, bi, bi, -1.0, 1.0));
@@ -1217,7 +1247,7 @@ int ensure_l_planes(gpb_model* m) {
     CUDA_TRY(m->ozflag.ensure(sizeof(int)));
     CUDA_TRY(cudaMemsetAsync(m->ozflag.p, 0, sizeof(int), m->st));
   }
-  m->oz_sa = pow2_ceil(2.0 * std::max(1.0, std::sqrt(m->nu + m->s2)) * (1.0 + 1e-9));
+  m->oz_sa = plane_scale(std::max(1.0, std::sqrt(m->nu + m->s2)));
   ProfScope ps(m, KC_OTHER, 0.0);
   // tile t of the packed factor -> tile t of the boxed planes; one launch per
   // block row (its off-diagonal tiles are consecutive)
@@ -1352,7 +1382,7 @@ int predict_chunk(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var,
     if (oz) {
       GPB_TRY(ensure_l_planes(m));
       CUDA_TRY(m->Vs.ensure(size_t(m->oz_slices) * mcp * m->np_));
-      m->oz_sb = pow2_ceil(2.0 * std::sqrt(m->nu) * (1.0 + 1e-9));
+      m->oz_sb = plane_scale(std::sqrt(m->nu));
     }
     for (int i = 0; i < Ti; ++i) {
       bool done = false;
@@ -1374,7 +1404,7 @@ int predict_chunk(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var,
       v.aux_ld = mcp;
       GPB_TRY(gemm(m, v, true, false, EPI_SUMSQ,
                    gemm_flops(mcp / GBN, int64_t(GBM) * nbr * (nbr + 1) / 2)));
-      if (oz && i + 1 < Ti) {  // planes of V_i^T for the rows below
+      if (oz) {  // planes of V_i^T for the rows below (and the full-covariance product)
         ProfScope ps(m, KC_OTHER, 0.0);
         CUDA_TRY(launch_ozaki_slice_t(Bv + int64_t(i) * bi * mcp, bi, mcp, mcp, m->oz_sb, m->Vs.as<int8_t>(),
                                       m->np_ / kOzakiBK, int64_t(i) * bi, m->oz_slices, m->ozflag.as<int>(),
@@ -1382,6 +1412,7 @@ int predict_chunk(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var,
         ++m->launches;
       }
     }
+    m->vs_ok = oz;
     GPB_TRY(pt.stop());
     *t_trsm += m->timing[4];
   }
@@ -1455,17 +1486,52 @@ int full_cov(gpb_model* m, const double* zt_dev, int64_t mt, double* cov_host) {
     CUDA_TRY(m->fc_jobs.ensure(sizeof(GemmJob) * jobs.size()));
     CUDA_TRY(cudaMemcpy(m->fc_jobs.p, jobs.data(), sizeof(GemmJob) * jobs.size(),
                         cudaMemcpyHostToDevice));
+    // the same lower blocks for the digit-plane product: rows r and c of V^T's planes
+    std::vector<OzakiJob> oj;
+    // (offsets for 8 planes per operand; with fewer planes the DMMA product runs)
+    const int64_t rb_stride = (m->np_ / kOzakiBK) * int64_t(kOzakiMaxSlices) * kOzakiBox;
+    for (int64_t r = 0; r < nbk; ++r)
+      for (int64_t c = 0; c <= r; ++c) {
+        OzakiJob o{};
+        o.a_off = r * rb_stride;
+        o.b_off = c * rb_stride;
+        o.C = S + r * GBM * mcp + c * GBM;
+        oj.push_back(o);
+      }
+    CUDA_TRY(m->fc_oz_jobs.ensure(sizeof(OzakiJob) * oj.size()));
+    CUDA_TRY(cudaMemcpy(m->fc_oz_jobs.p, oj.data(), sizeof(OzakiJob) * oj.size(), cudaMemcpyHostToDevice));
     m->fc_mcp = mcp;
   }
   PhaseTimer pt(m, 6);
   CUDA_TRY(launch_prior(S, mcp, zt_dev, mt, static_cast<int>(m->d), sek_params(m), m->st));
   ++m->launches;
   // Sigma = K** - V^T V (model.py:254-269), lower blocks
-  GemmParams p = views(base_params(m->fc_jobs.as<GemmJob>(), static_cast<int>(nbk * (nbk + 1) / 2), 1, 1,
-                                   mcp, mcp, mcp, -1.0, 1.0),
-                       m->Bv, m->Bv);
-  p.max_k = m->np_;
-  GPB_TRY(gemm(m, p, false, false, EPI_AXPBY, gemm_flops(nbk * (nbk + 1) / 2, m->np_)));
+  if (m->oz_slices == kOzakiMaxSlices && m->vs_ok && m->np_ >= m->oz_min_k) {
+    // V^T V from the planes of V^T the prediction sweep left in Vs (k in segments of kOzakiMaxK)
+    const int64_t kchunks = m->np_ / kOzakiBK;
+    for (int64_t k0 = 0; k0 < m->np_; k0 += kOzakiMaxK) {
+      OzakiGemm g{};
+      g.a = g.b = {m->Vs.as<int8_t>(), 0, static_cast<int>(kchunks), kchunks * m->oz_slices * kOzakiBox};
+      g.a_off = g.b_off = (k0 / kOzakiBK) * m->oz_slices * kOzakiBox;
+      g.M = g.N = GBM;
+      g.K = static_cast<int>(std::min<int64_t>(kOzakiMaxK, m->np_ - k0));
+      g.slices = m->oz_slices;
+      g.alpha = -m->oz_sb * m->oz_sb;
+      g.beta = 1.0;
+      g.ldc_in = g.ldc_out = mcp;
+      g.jobs = m->fc_oz_jobs.as<OzakiJob>();
+      g.njobs = static_cast<int>(nbk * (nbk + 1) / 2);
+      ProfScope ps(m, KC_OZAKI, gemm_flops(nbk * (nbk + 1) / 2, g.K));
+      CUDA_TRY(launch_ozaki_gemm(g, m->st));
+      m->launches += 2;
+    }
+  } else {
+    GemmParams p = views(base_params(m->fc_jobs.as<GemmJob>(), static_cast<int>(nbk * (nbk + 1) / 2), 1, 1,
+                                     mcp, mcp, mcp, -1.0, 1.0),
+                         m->Bv, m->Bv);
+    p.max_k = m->np_;
+    GPB_TRY(gemm(m, p, false, false, EPI_AXPBY, gemm_flops(nbk * (nbk + 1) / 2, m->np_)));
+  }
   CUDA_TRY(launch_symmetrize(S, mcp, mt, m->st));
   ++m->launches;
   GPB_TRY(pt.stop());
@@ -1524,6 +1590,7 @@ int model_create(gpb_ctx* ctx, const double* z, const double* y, int64_t n, int6
   }
   if (const char* e = getenv("GPB_OZAKI_MIN_K")) m->oz_min_k = std::max<int64_t>(64, atoll(e));
   if (const char* e = getenv("GPB_OZAKI_CHOL")) m->oz_chol = atoi(e) != 0;
+  if (const char* e = getenv("GPB_OZAKI_CHOL_IN")) m->oz_chol_in = atoi(e) != 0;
   if (const char* e = getenv("GPB_OZAKI_CHOL_MIN_K")) m->oz_chol_min_k = std::max<int64_t>(64, atoll(e));
   if (int s_l = apply_layout(m)) {
     delete m;
@@ -1558,7 +1625,7 @@ void free_model(gpb_model* m, bool keep = true) {
                     &m->X, &m->Kinv, &m->part_l, &m->part_v, &m->part_x, &m->inv_jobs,
                     &m->Bv, &m->W, &m->mpart, &m->sq, &m->pred_jobs, &m->zt, &m->mean, &m->var,
                     &m->S, &m->fc_jobs, &m->gp_panel, &m->gp_h, &m->gp_jobs, &m->gp_tiles,
-                    &m->Ls, &m->Vs, &m->ozflag, &m->Ps, &m->oz_jobs})
+                    &m->Ls, &m->Vs, &m->ozflag, &m->Ps, &m->oz_jobs, &m->fc_oz_jobs})
     b->release(keep);
 }
 
@@ -2039,7 +2106,19 @@ int gpb_model_set_ozaki(gpb_model* m, int slices) {
   GPB_TRY(check_live(m));
   if (slices != 0 && (slices < 4 || slices > kOzakiMaxSlices))
     return fail(GPB_INVALID_CONFIG, "digit planes: 0 (off) or 4..8");
-  if (slices != m->oz_slices) m->ls_ok = m->plan_ok = false;  // plane offsets depend on the count
+  if (slices != m->oz_slices) {
+    // plane offsets depend on the count, the panel grouping on whether planes are in use:
+    // a different grouping is a different (round-off level) factor, so the cached one goes
+    m->ls_ok = m->plan_ok = m->vs_ok = false;
+    m->oz_slices = slices;
+    const int g = choose_panels(m);
+    if (g != m->G) {
+      m->G = g;
+      invalidate(m);
+      const int64_t bi2 = int64_t(m->bi) * m->bi;
+      CUDA_TRY(m->scratch.ensure(sizeof(double) * 2 * m->G * std::max<int64_t>(1, m->Ti - 1) * bi2));
+    }
+  }
   m->oz_slices = slices;
   return GPB_OK;
 }

@@ -144,8 +144,8 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const OzakiArgs
   if (p.jobs) {
     const OzakiJob j = p.jobs[job];
     if (j.lower && nt > mt) return;
-    a_off = j.a_off;
-    b_off = j.b_off;
+    a_off += j.a_off;
+    b_off += j.b_off;
     Cin = Cout = j.C;
   }
 
@@ -249,7 +249,9 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const OzakiArgs
   }
 }
 
-// digits of f (|f| <= 1/2 in units of the scale): exact
+// digits of f (|f| <= 127/128 in units of the scale): exact; the first digit lies in
+// [-127, 127], the later ones in [-64, 64]
+constexpr double kMaxFraction = 127.0 / 128.0;
 template <int MAXS>
 GPB_DEVINL void digits(double f, int slices, int (&d)[MAXS]) {
 #pragma unroll
@@ -291,9 +293,9 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       double f = (h ? x.y : x.x) * inv_scale;
-      if (!(fabs(f) <= 0.5)) {
+      if (!(fabs(f) <= kMaxFraction)) {
         over = true;
-        f = f > 0.0 ? 0.5 : -0.5;
+        f = f > 0.0 ? kMaxFraction : -kMaxFraction;
       }
       int d[kOzakiMaxSlices];
       digits(f, slices, d);
@@ -330,9 +332,9 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       double f = src[(kb + kg * 4 + j) * ld + c0 + tx] * inv_scale;
-      if (!(fabs(f) <= 0.5)) {
+      if (!(fabs(f) <= kMaxFraction)) {
         over = true;
-        f = f > 0.0 ? 0.5 : -0.5;
+        f = f > 0.0 ? kMaxFraction : -kMaxFraction;
       }
       int d[kOzakiMaxSlices];
       digits(f, slices, d);

@@ -7,12 +7,14 @@
 // computed from signed 7-bit digit planes of their operands (Ozaki splitting
 // with a fixed-point scale per operand buffer):
 //
-//   x = sx * sum_{p=1..S} d_p(x) 2^(-7p) + r,   d_p in [-64, 64],  |r| <= sx 2^(-7S-1)
+//   x = sx * sum_{p=1..S} d_p(x) 2^(-7p) + r,   |x| <= sx 127/128,  |r| <= sx 2^(-7S-1),
+//       d_1 in [-127, 127], d_p in [-64, 64] for p > 1
 //   sum_k a_k b_k ~= sa sb sum_{t=2..S+1} 2^(-7t) G_t,
 //   G_t = sum_{p+q=t} sum_k d_p(a_k) d_q(b_k)   (exact int32 sums on the int8 pipe)
 //
-// The digit extraction is exact (power-of-two scalings, round-to-nearest and
-// the subtraction of the rounded value), the int32 group sums are exact for
+// The digit extraction of x / sx is exact (round-to-nearest and the
+// subtraction of the rounded value; the division by the scale itself rounds
+// once, 2^-53 relative, unless sx is a power of two), the int32 group sums are exact for
 // K <= kOzakiMaxK, and the groups are combined in FP64, least significant
 // first.  The only errors are the dropped remainder r of each operand and the
 // dropped digit pairs p+q > S+1: both below 2^(-7S+3) relative to sa sb per
@@ -41,13 +43,13 @@ namespace gpb {
 constexpr int kOzakiMaxSlices = 8;
 constexpr int kOzakiBM = 128, kOzakiBN = 128, kOzakiBK = 32;
 constexpr int kOzakiBox = kOzakiBM * kOzakiBK;  // bytes
-// |G_t| <= S * K * 64 * 64 < 2^31
+// |G_t| <= K (2 * 127 * 64 + 6 * 64 * 64) < 2^31 (at most two pairs of a group hold a first digit)
 constexpr int64_t kOzakiMaxK = 32768;
 
 // Digit planes of `ntiles` consecutive row-major tiles of tr x tc doubles
 // (tr a multiple of 128, tc of 32) into the boxed layout at `planes` (tile t
 // at planes + t * tr * tc * slices).  *flag is set to 1 when an element
-// exceeds scale / 2 (digits saturate).
+// exceeds scale * 127 / 128 (digits saturate).
 cudaError_t launch_ozaki_slice_tiles(const double* src, int64_t ntiles, int tr, int tc, double scale,
                                      int8_t* planes, int slices, int* flag, cudaStream_t st);
 
@@ -67,14 +69,14 @@ struct OzakiOperand {
 };
 
 struct OzakiJob {
-  int64_t a_off, b_off;  // byte offsets of the job's first row block at k = 0
+  int64_t a_off, b_off;  // byte offsets of the job's first row block at k = 0 (added to the launch's)
   double* C;
   int lower, pad;
 };
 
 struct OzakiGemm {
   OzakiOperand a, b;     // A: M rows, B: N rows, both K-major
-  int64_t a_off, b_off;  // byte offsets of row block 0 at k = 0 (ignored with jobs)
+  int64_t a_off, b_off;  // byte offsets of row block 0 at k = 0 (with jobs: a common offset, e.g. a k segment)
   int M, N, K;           // multiples of 128 / 128 / 32; K <= kOzakiMaxK
   int slices;
   double alpha;  // Cout = beta * Cin + alpha * sum (the caller folds the scales sa sb into alpha)
