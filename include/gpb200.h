@@ -131,17 +131,21 @@ int gpb_model_timings(gpb_model* m, double* ms_out, int n);
 int gpb_model_launch_count(gpb_model* m, int64_t* out);
 
 /* tcgen05 digit-plane products (csrc/ozaki.cuh): the long-k products of the
- * prediction sweep (tiled.py:263-298) on the int8 tensor pipe from `slices`
- * signed 7-bit digit planes per operand (8: every kept term of the FP64
- * product; 0: off, every product on the FP64 DMMA kernels).  The default is
- * GPB_OZAKI (unset: 0).  `fallbacks` counts predictions repeated on the DMMA
- * kernels because an operand exceeded its fixed-point scale. */
+ * path -- the factorisation's trailing updates (tiled.py:187-204), the
+ * prediction sweep (tiled.py:263-298) and the full-covariance V^T V
+ * (model.py:254-269) -- on the int8 tensor pipe from `slices` signed 7-bit
+ * digit planes per operand (8, the default: every kept term of the FP64
+ * product; 0: off, every product on the FP64 DMMA kernels).  GPB_OZAKI sets
+ * the default of new models.  Changing the count drops the cached factor
+ * when it changes the panel grouping.  `fallbacks` counts phases repeated on
+ * the DMMA kernels because an operand exceeded its fixed-point scale. */
 int gpb_model_set_ozaki(gpb_model* m, int slices);
 int gpb_model_get_ozaki(gpb_model* m, int* slices, int64_t* fallbacks);
 /* the CUDA stream (cudaStream_t) the model's kernels run on */
 int gpb_model_stream(gpb_model* m, void** stream);
 /* per-kernel-class profiling with CUDA events around every launch:
- * class 0 grouped DMMA GEMM, 1 POTRF/TRTRI tile, 2 SEK assembly, 3 solves.
+ * class 0 grouped DMMA GEMM, 1 POTRF/TRTRI tile, 2 SEK assembly, 3 solves,
+ * 4 plane slicing and other small kernels, 5 tcgen05 digit-plane products.
  * set_profiling resets the counters; kernel_stats returns the totals
  * (device ms, executed flops, launches) since then. */
 int gpb_model_set_profiling(gpb_model* m, int on);

@@ -102,7 +102,13 @@ GPB_DEVINL int box_offset(int row, int byte) {
 }
 
 __host__ __device__ constexpr int stages_for(int P) { return P >= 7 ? 3 : 4; }
-constexpr size_t smem_bytes(int P) { return size_t(stages_for(P)) * P * 2 * kOzakiBox + 1024 + 128; }
+// epilogue staging in the stage memory: 128 rows of 64 doubles, pitch 65 (conflict-free row-per-lane stores)
+constexpr int kEpiPitch = 65;
+constexpr size_t kEpiBytes = size_t(kOzakiBM) * kEpiPitch * sizeof(double);
+constexpr size_t smem_bytes(int P) {
+  return (size_t(stages_for(P)) * P * 2 * kOzakiBox > kEpiBytes ? size_t(stages_for(P)) * P * 2 * kOzakiBox : kEpiBytes) +
+         1024 + 128;
+}
 
 struct OperandArgs {
   const int8_t* planes;
@@ -129,7 +135,8 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const OzakiArgs
   constexpr int kStageBytes = 2 * kOperandBytes;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (su32(smem_raw) + 1023u) & ~1023u;
-  const uint32_t bars = base + NST * kStageBytes;  // full[NST], empty[NST], accfull, tmem slot
+  // full[NST], empty[NST], accfull, tmem slot: behind the stages (and the epilogue's staging tile)
+  const uint32_t bars = base + (NST * kStageBytes > static_cast<int>(kEpiBytes) ? NST * kStageBytes : static_cast<int>(kEpiBytes));
   const uint32_t full0 = bars, empty0 = bars + 8 * NST, accfull = bars + 16 * NST, slot = accfull + 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int r = blockIdx.x, job = 0;
@@ -207,38 +214,68 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const OzakiArgs
       tc_commit(accfull);
     }
   } else {
+    // Epilogue.  A thread owns one accumulator row (TMEM lane), but rows of C are
+    // ldc doubles apart: row-per-thread global accesses would be 32 scattered
+    // 16-byte pieces per instruction and one exposed memory latency per 8 columns
+    // (ncu: 33k of a K = 512 block's 60k cycles).  So the warp first pulls its 32
+    // rows of C towards L2 while the MMAs run, then, per half of the columns,
+    // combines the groups into the (by then free) stage memory and updates C
+    // from there with whole-row coalesced accesses, 16 rows in flight.
     const int quarter = warp & 3;
-    const int row = mt * kOzakiBM + quarter * 32 + lane;  // row of the job's C
+    const int row0 = mt * kOzakiBM + quarter * 32;  // first of the warp's rows of the job's C
+    double* cout = Cout + static_cast<long long>(row0) * p.ldc_out + static_cast<long long>(nt) * kOzakiBN;
+    const double* cin = Cin ? Cin + static_cast<long long>(row0) * p.ldc_in + static_cast<long long>(nt) * kOzakiBN
+                            : nullptr;
+    if (cin) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {  // 32 rows x 8 lines of 128 bytes
+        const int line = i * 32 + lane;
+        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(cin + static_cast<long long>(line >> 3) * p.ldc_in +
+                                                          (line & 7) * 16));
+      }
+    }
     mbar_wait(accfull, 0);
     tc_fence_after();
     const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    double* out = Cout + static_cast<long long>(row) * p.ldc_out + static_cast<long long>(nt) * kOzakiBN;
-    const double* in = Cin ? Cin + static_cast<long long>(row) * p.ldc_in + static_cast<long long>(nt) * kOzakiBN
-                           : nullptr;
+    double* tile = reinterpret_cast<double*>(smem_raw + (base - su32(smem_raw))) + quarter * 32 * kEpiPitch;
 #pragma unroll 1
-    for (int c8 = 0; c8 < kOzakiBN; c8 += 8) {
-      int v[NG][8];
+    for (int half = 0; half < 2; ++half) {
+      double* mine = tile + lane * kEpiPitch;
+#pragma unroll 1
+      for (int c8 = 0; c8 < 64; c8 += 8) {
+        int v[NG][8];
 #pragma unroll
-      for (int g = 0; g < NG; ++g) tc_ld8(taddr + g * kOzakiBN + c8, v[g]);
-      tc_wait_ld();
-      double rr[8];
+        for (int g = 0; g < NG; ++g) tc_ld8(taddr + g * kOzakiBN + half * 64 + c8, v[g]);
+        tc_wait_ld();
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        double acc = static_cast<double>(v[NG - 1][j]);
+        for (int j = 0; j < 8; ++j) {
+          double acc = static_cast<double>(v[NG - 1][j]);
 #pragma unroll
-        for (int g = NG - 2; g >= 0; --g) acc = fma(acc, 0.0078125, static_cast<double>(v[g][j]));
-        rr[j] = p.alpha * acc;
-      }
-      if (in) {
-#pragma unroll
-        for (int j = 0; j < 8; j += 2) {
-          const double2 ci = *reinterpret_cast<const double2*>(in + c8 + j);
-          rr[j] = fma(p.beta, ci.x, rr[j]);
-          rr[j + 1] = fma(p.beta, ci.y, rr[j + 1]);
+          for (int g = NG - 2; g >= 0; --g) acc = fma(acc, 0.0078125, static_cast<double>(v[g][j]));
+          mine[c8 + j] = p.alpha * acc;
         }
       }
+      __syncwarp();
+#pragma unroll 1
+      for (int r0 = 0; r0 < 32; r0 += 16) {
+        double x0[16], x1[16];
+        if (cin) {
 #pragma unroll
-      for (int j = 0; j < 8; j += 2) *reinterpret_cast<double2*>(out + c8 + j) = make_double2(rr[j], rr[j + 1]);
+          for (int r = 0; r < 16; ++r) {
+            const double* src = cin + static_cast<long long>(r0 + r) * p.ldc_in + half * 64;
+            x0[r] = src[lane];
+            x1[r] = src[lane + 32];
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const double* t = tile + (r0 + r) * kEpiPitch;
+          double* dst = cout + static_cast<long long>(r0 + r) * p.ldc_out + half * 64;
+          dst[lane] = cin ? fma(p.beta, x0[r], t[lane]) : t[lane];
+          dst[lane + 32] = cin ? fma(p.beta, x1[r], t[lane + 32]) : t[lane + 32];
+        }
+      }
+      __syncwarp();
     }
     tc_fence_before();
   }

@@ -24,6 +24,7 @@ constructor taking the raw training series plus ``n_regressors``.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, replace
 
 import numpy as np
@@ -303,9 +304,14 @@ class GPModel:
     # -- tcgen05 digit-plane products (csrc/ozaki.cuh) ----------------------
     @property
     def digit_planes(self) -> int:
-        """Planes per operand of the int8 tensor-core products (0: FP64 DMMA only)."""
+        """Planes per operand of the tcgen05 int8 products that carry the long
+        FP64 contractions (trailing updates, prediction sweep, full covariance);
+        8 by default (env ``GPB_OZAKI``), 0: every product on the FP64 DMMA kernels."""
         if self._handle is None:
-            return self._digit_planes or 0
+            if self._digit_planes is not None:
+                return self._digit_planes
+            env = os.environ.get("GPB_OZAKI")
+            return 8 if env is None else (0 if int(env) <= 0 else min(8, max(4, int(env))))
         out = ctypes.c_int()
         _lib.check(_lib.load().gpb_model_get_ozaki(self._handle, ctypes.byref(out), None))
         return int(out.value)

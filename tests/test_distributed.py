@@ -204,6 +204,7 @@ def _device_rank(rank, world, grid, kind, transport, exchange="collective"):
         single = None
         if rank == 0:  # the single-GPU model on the same inputs
             ref = gpb.GPModel(gpb.Dataset(z, y), gpb.KernelParams(*PARAMS), t)
+            ref.digit_planes = 0  # the multi-GPU executor runs every product on the FP64 DMMA kernels
             single = ref.cholesky()
             ref.close()
         return {"ll": ll, "mean": pv.mean, "var": pv.variance, "L": L if rank == 0 else None, "single": single,
