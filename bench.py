@@ -279,7 +279,7 @@ def cpu_baseline_block():
 
 # ---------------------------------------------------------------- GPU side
 def roofline_block(planes, pairs, planes_tf, planes_tf_exec, gemm_tf, gemm_tf_exec, fp64_peak, kcnt, kbusy, kms,
-                   total_ms, chol_tf):
+                   total_ms, chol_tf, clk=None):
     """`roofline` of the bench line for the step's dominant kernel."""
     dmma = {"kernel": "dgemm_tma_kernel (TMA-fed DMMA.8x8x4)", "achieved": gemm_tf, "peak": fp64_peak,
             "unit": "TFLOP/s", "frac": gemm_tf / fp64_peak if fp64_peak else None,
@@ -296,17 +296,26 @@ def roofline_block(planes, pairs, planes_tf, planes_tf_exec, gemm_tf, gemm_tf_ex
                      "cholesky_frac_of_peak": chol_tf / fp64_peak if fp64_peak else None})
         return dmma
     mp = _measured_peaks()
-    bf16 = mp.get("bf16_tflops_sustained") or mp.get("bf16_tflops")
+    # burst figure while the SM clock holds its maximum through the timed region (it does: the
+    # step mixes the int8 products with FP64 phases and stays under the power cap), else the
+    # sustained one
+    at_max = bool(clk and clk.get("sm_mhz") and clk.get("sm_max_mhz") and clk["sm_mhz"] >= 0.95 * clk["sm_max_mhz"])
+    key = "bf16_tflops" if at_max and mp.get("bf16_tflops") else "bf16_tflops_sustained"
+    bf16 = mp.get(key) or mp.get("bf16_tflops")
     if bf16:
-        peak, src = 2.0 * bf16, ("2 x MEASURED_PEAKS.json bf16_tflops_sustained (the int8 tcgen05 rate is twice "
-                                 "the bf16 rate; sustained figure: the kernel runs inside a long step)")
+        peak, src = 2.0 * bf16, (f"of measured: 2 x MEASURED_PEAKS.json {key} = 2 x {bf16} (the int8 tcgen05 rate is "
+                                 "twice the bf16 rate; burst figure because the SM clock stayed at its maximum "
+                                 "during the timed region, see `clocks`; the denominator is cuBLAS, so a kernel "
+                                 "can read a little above 1)" if key == "bf16_tflops" else
+                                 f"of measured: 2 x MEASURED_PEAKS.json {key} = 2 x {bf16} (sustained figure: the SM "
+                                 "clock dropped under load during the timed region)")
     else:
-        peak, src = 4500.0, "nominal dense int8 peak of B200 (MEASURED_PEAKS.json absent)"
+        peak, src = 4500.0, "of nominal: dense int8 peak of B200 (MEASURED_PEAKS.json absent)"
     achieved = planes_tf * pairs
     return {"bound": "tensor",
-            "kernel": "ozaki_gemm2_kernel (tcgen05.mma kind::i8 on signed 7-bit digit planes, TMEM accumulators)",
+            "kernel": "ozaki_gemm_kernel (tcgen05.mma kind::i8 on signed 7-bit digit planes, TMEM accumulators)",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak,
+            "frac": achieved / peak, "frac_of_nominal_int8_dense": achieved / 4500.0,
             "achieved_basis": f"int8 operations per second: {pairs} digit-pair products ({planes} planes per "
                               "operand) per algorithmic FP64 multiply-add; " + basis,
             "peak_source": src,
@@ -537,9 +546,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                        "arrays in pinned memory, median of K reps"},
         "e2e_at_cpu_sample": same,
         "roofline": roofline_block(planes, pairs, planes_tf, planes_tf_exec, gemm_tf, gemm_tf_exec, peak.value,
-                                   kcnt, kbusy, kms, total_ms, value / world),
+                                   kcnt, kbusy, kms, total_ms, value / world, clk),
         "dmma_only": dmma_only,
         "digit_planes": planes,
+        "arithmetic": ("FP64 inputs, outputs and accumulation across updates; long contractions (trailing updates, "
+                       "prediction sweep) as exact int32 sums of int8 digit-plane products on tcgen05 "
+                       f"({planes} signed 7-bit planes per operand, dropped tail < 2^-53 of the operand scales), "
+                       "everything else FP64 (DMMA / DFMA); parity with the FP64 oracle is tested at the bench "
+                       "sizes (factor <= 1e-10, loss / mean / variance <= 1e-9)") if planes else
+                      "FP64 throughout (DMMA / DFMA)",
         "kernel_classes_ms": {"gemm_dmma": kms[0], "digit_plane_products": kms[5], "potrf_trtri": kms[1],
                               "sek": kms[2], "solves": kms[3], "slicing_other": kms[4]},
         "clocks": clk,

@@ -173,6 +173,9 @@ struct gpb_ctx {
 struct CholGroup {
   int k0, np;
   int64_t trsm_off[kMaxGroup], trsm_cnt[kMaxGroup], in_off[kMaxGroup], in_cnt[kMaxGroup];
+  // left-looking in-group updates (digit-plane path): column k0 + g from the g panels before it
+  int64_t ll_off[kMaxGroup], ll_cnt[kMaxGroup];
+  double ll_fl[kMaxGroup];
   int64_t next_off, next_cnt, upd_off, upd_cnt;
   double trsm_fl[kMaxGroup], in_fl[kMaxGroup], next_fl, upd_fl;  // executed flops per launch
 };
@@ -524,6 +527,30 @@ int build_chol_plan(gpb_model* m) {
           ozjobs.back() = o;
         }
     };
+    // LL(g): L(i, k0+g) -= [X]_i [X]_{k0+g}^T over panels 0 .. g-1 of the group (K = g bi):
+    // what the right-looking IN launches add up to for that column, in one product
+    for (int g = 1; g < grp.np; ++g) {
+      grp.ll_off[g] = jobs.size();
+      const int k = k0 + g;
+      for (int i = k; i < Ti; ++i) {
+        GemmJob j{};
+        j.A = panel_tile(0, i);
+        j.B = panel_tile(0, k);
+        j.Cin = j.Cout = L + h_tri_rm(i, k) * bi2;
+        j.K = g * bi;
+        j.lower = (i == k);
+        jobs.push_back(j);
+        OzakiJob o{};
+        const int64_t tile_b = bi2 * m->oz_slices, panel_b = int64_t(std::max(1, Ti - 1)) * tile_b;
+        o.a_off = int64_t(s % 2) * G * panel_b + int64_t(i - k0 - 1) * tile_b;
+        o.b_off = int64_t(s % 2) * G * panel_b + int64_t(k - k0 - 1) * tile_b;
+        o.C = j.Cout;
+        o.lower = j.lower;
+        ozjobs.resize(jobs.size());
+        ozjobs.back() = o;
+      }
+      grp.ll_cnt[g] = jobs.size() - grp.ll_off[g];
+    }
     grp.next_off = jobs.size();
     add_upd(c_next, c_upd);
     grp.next_cnt = jobs.size() - grp.next_off;
@@ -542,6 +569,7 @@ int build_chol_plan(gpb_model* m) {
     for (int g = 0; g < grp.np; ++g) {
       grp.trsm_fl[g] = fl(grp.trsm_off[g], grp.trsm_cnt[g], nb);
       grp.in_fl[g] = fl(grp.in_off[g], grp.in_cnt[g], nb * nb);
+      grp.ll_fl[g] = g ? fl(grp.ll_off[g], grp.ll_cnt[g], nb * nb) : 0.0;
     }
     grp.next_fl = fl(grp.next_off, grp.next_cnt, nb * nb);
     grp.upd_fl = fl(grp.upd_off, grp.upd_cnt, nb * nb);
@@ -706,6 +734,9 @@ int ensure_factor(gpb_model* m) {
     if (s >= 2) CUDA_TRY(cudaStreamWaitEvent(m->crit, ev_upd[s - 2], 0));
     for (int g = 0; g < grp.np; ++g) {
       const int k = grp.k0 + g;
+      // digit-plane path: column k brought up to date from the group's earlier panels in one
+      // product (K = g bi) instead of g right-looking updates with K = bi
+      if (oz_in && g > 0) GPB_TRY(oz_update(g * bi, grp.ll_off[g], grp.ll_cnt[g], grp.ll_fl[g], m->crit));
       PotrfArgs a{};
       a.tile = L + h_tri_rm(k, k) * bi2;
       a.dinv = D + int64_t(k) * bi2;
@@ -735,15 +766,11 @@ int ensure_factor(gpb_model* m) {
                                           m->ozflag.as<int>(), m->crit));
         ++m->launches;
       }
-      if (grp.in_cnt[g] > 0) {
-        if (oz_in) {
-          GPB_TRY(oz_update(bi, grp.in_off[g], grp.in_cnt[g], grp.in_fl[g], m->crit));
-        } else {
-          GemmParams ip = views(base_params(jobs + grp.in_off[g], static_cast<int>(grp.in_cnt[g]), nb, nb, bi,
-                                            bi, bi, -1.0, 1.0),
-                                m->scratch, m->scratch);
-          GPB_TRY(gemm(m, ip, true, true, EPI_AXPBY, grp.in_fl[g], m->crit));
-        }
+      if (grp.in_cnt[g] > 0 && !oz_in) {
+        GemmParams ip = views(base_params(jobs + grp.in_off[g], static_cast<int>(grp.in_cnt[g]), nb, nb, bi,
+                                          bi, bi, -1.0, 1.0),
+                              m->scratch, m->scratch);
+        GPB_TRY(gemm(m, ip, true, true, EPI_AXPBY, grp.in_fl[g], m->crit));
       }
     }
     CUDA_TRY(cudaEventRecord(ev_panel[s], m->crit));
