@@ -27,7 +27,11 @@
 //     66% / 43% active in the two windows; 2 x 2 clusters with multicast loads
 //     of the shared rows: 73 TF/s (the L2 already merges neighbouring CTAs'
 //     requests; the cluster only adds lock-step);
-//   boxed planes + bulk copies (this file): see DESIGN.md section 4.
+//   boxed planes + bulk copies (this file): 99 TF/s; with the coalesced epilogue 100 TF/s
+//     (3.6 int8 POP/s) and 33k -> 10k cycles of epilogue per block;
+//   CTA pairs on top of that (cta_group::2, M = 256: each CTA holds half of the B rows,
+//     CTA 1 relays "stage full" to CTA 0, commits multicast to both): 91 TF/s, config 2
+//     factor 155 vs 139 ms, prediction sweep 383 vs 343 ms -- slower, dropped.
 #include "ozaki.cuh"
 
 #include <cmath>

@@ -26,11 +26,14 @@ inline int chol_panels(int Ti) {
 // when r tiles remain; 0 = fixed G): +0.5% at config 2.  GPB_FIRST: size of
 // the first group, whose critical path runs before any trailing update can
 // start (default 1 panel from 32 tiles: config 2 factor 338.8 -> 338.0 ms).
-inline std::vector<int> chol_group_sizes(int Ti, int G) {
+// The single-GPU plan passes other defaults when the trailing updates run on the
+// int8 pipe (gpb_api.cu): there the group's own work is cheap next to the K it
+// buys the update, so groups shrink later (r / 4) and the first one is full.
+inline std::vector<int> chol_group_sizes(int Ti, int G, int tail_default = 8, int first_default = -1) {
   const char* te = getenv("GPB_TAIL");
-  const int tail = te ? atoi(te) : 8;
+  const int tail = te ? atoi(te) : tail_default;
   const char* fe = getenv("GPB_FIRST");
-  const int first = fe ? atoi(fe) : (Ti >= 32 ? 1 : 0);
+  const int first = fe ? atoi(fe) : (first_default >= 0 ? first_default : (Ti >= 32 ? 1 : 0));
   std::vector<int> sizes;
   for (int k0 = 0; k0 < Ti;) {
     int g = std::min(G, Ti - k0);
