@@ -105,13 +105,16 @@ GPB_DEVINL int box_offset(int row, int byte) {
   return o ^ (((o >> 7) & 1) << 4);
 }
 
-__host__ __device__ constexpr int stages_for(int P) { return P >= 7 ? 3 : 4; }
+// as many stages as fit in ~200 KB (a stage: P planes of both operands, 8 KB per plane):
+// 3 for the 8-plane window, 6 for the 4-plane one -- its chunks hold only 10 MMAs (640
+// cycles), and 4 stages did not cover the L2-miss latency (tensor pipe 66% active)
+__host__ __device__ constexpr int stages_for(int P) { return 25 / P > 8 ? 8 : 25 / P; }
 // epilogue staging in the stage memory: 128 rows of 64 doubles, pitch 65 (conflict-free row-per-lane stores)
 constexpr int kEpiPitch = 65;
 constexpr size_t kEpiBytes = size_t(kOzakiBM) * kEpiPitch * sizeof(double);
 constexpr size_t smem_bytes(int P) {
   return (size_t(stages_for(P)) * P * 2 * kOzakiBox > kEpiBytes ? size_t(stages_for(P)) * P * 2 * kOzakiBox : kEpiBytes) +
-         1024 + 128;
+         1024 + 256;
 }
 
 struct OperandArgs {
