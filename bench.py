@@ -447,7 +447,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     # ---- the same step with every product on the FP64 DMMA kernels (planes off)
     dmma_only = None
-    if planes and world == 1:
+    if planes and world == 1 and not args.no_dmma_only:
         _lib.check(lib.gpb_model_set_ozaki(h, 0))
         step()
         k2 = max(2, min(3, K))
@@ -782,6 +782,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-strong-base", action="store_true")
+    ap.add_argument("--no-dmma-only", action="store_true", help="skip the extra pass with digit planes off")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
