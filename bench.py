@@ -700,20 +700,10 @@ def strong_base(args):
     flags = (ctypes.c_uint8 * 3)(1, 1, 1)
     ll = ctypes.c_double()
     tm = (ctypes.c_double * 8)()
-    fac, sol, fac_planes = [], [], []
+    fac, sol, fac_dmma = [], [], []
     try:
-        # the multi-GPU executor (csrc/dist.cu) runs every product on the FP64
-        # DMMA kernels, so t_1 is taken on the same kernels; the single-GPU
-        # default (digit planes) is timed beside it
-        planes_h = ctypes.c_int()
-        lib.gpb_model_get_ozaki(h, ctypes.byref(planes_h), None)
-        for it in range(2 if planes_h.value else 0):
-            _lib.check(lib.gpb_model_set_params(h, 1.0, 1.0, 0.1, flags))
-            _lib.check(lib.gpb_log_likelihood(h, ctypes.byref(ll)))
-            lib.gpb_model_timings(h, tm, 8)
-            if it >= 1:
-                fac_planes.append(tm[1])
-        _lib.check(lib.gpb_model_set_ozaki(h, 0))
+        # t_1 on the library default (digit planes for the long products, as the multi-GPU
+        # executor uses for 512-wide tiles); the FP64 DMMA-only time beside it
         for it in range(3):
             _lib.check(lib.gpb_model_set_params(h, 1.0, 1.0, 0.1, flags))
             _lib.check(lib.gpb_log_likelihood(h, ctypes.byref(ll)))
@@ -721,6 +711,16 @@ def strong_base(args):
             if it >= 1:
                 fac.append(tm[1])
                 sol.append(tm[2])
+        planes_h = ctypes.c_int()
+        lib.gpb_model_get_ozaki(h, ctypes.byref(planes_h), None)
+        if planes_h.value:
+            _lib.check(lib.gpb_model_set_ozaki(h, 0))
+            for it in range(2):
+                _lib.check(lib.gpb_model_set_params(h, 1.0, 1.0, 0.1, flags))
+                _lib.check(lib.gpb_log_likelihood(h, ctypes.byref(ll)))
+                lib.gpb_model_timings(h, tm, 8)
+                if it >= 1:
+                    fac_dmma.append(tm[1])
     finally:
         lib.gpb_model_destroy(h)
     f, s_ = statistics.median(fac), statistics.median(sol)
@@ -760,10 +760,12 @@ def strong_base(args):
     per_rank_link = emulate(EMU_LINK)
     return {"workload": f"config 3 on 1 GPU: n={c['n']}, D={c['d']}, {c['tiles']} tiles", "factor_ms": f,
             "solves_ms": s_, "tflops": chol_flops(c["n"]) / (f * 1e-3) / 1e12,
-            "note": "t_1 of the strong-scaling efficiency E(p) = t_1 / (p t_p) (1 warm-up + 2 timed), on the "
-                    "FP64 DMMA kernels like the multi-GPU executor",
-            "factor_ms_digit_planes": fac_planes[0] if fac_planes else None,
-            "tflops_digit_planes": chol_flops(c["n"]) / (fac_planes[0] * 1e-3) / 1e12 if fac_planes else None,
+            "note": "t_1 of the strong-scaling efficiency E(p) = t_1 / (p t_p) (1 warm-up + 2 timed): the "
+                    "single-GPU path at its default (long products on the digit planes, 8-panel groups, "
+                    "left-looking in-group updates); the multi-GPU executor also runs NEXT / UPD on the planes "
+                    "but keeps 6-panel groups and right-looking DMMA in-group updates",
+            "factor_ms_dmma_only": fac_dmma[0] if fac_dmma else None,
+            "tflops_dmma_only": chol_flops(c["n"]) / (fac_dmma[0] * 1e-3) / 1e12 if fac_dmma else None,
             "emulated_2x4_factor_ms_per_rank": per_rank,
             "emulated_2x4_efficiency_upper_bound": f / (8 * max(per_rank)),
             "emulated_2x4_link_factor_ms_per_rank": per_rank_link,

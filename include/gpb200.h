@@ -331,11 +331,16 @@ enum {
    * (job: k = index of the GEMM job, i = destination rank, buf[3] / off[3] = where
    * in that rank's buffers); SIGNAL sets flag `j` (0 ready, 1 free) of rank i to
    * count; WAITFLAG waits until this rank's flag j of source rank i reaches count */
-  GPB_OP_MIRROR, GPB_OP_SIGNAL, GPB_OP_WAITFLAG
+  GPB_OP_MIRROR, GPB_OP_SIGNAL, GPB_OP_WAITFLAG,
+  /* digit planes (csrc/ozaki.cuh): SLICE writes the planes of `count` consecutive
+   * bi x bi tiles from buf[0] / off[0] (a row or column panel) into the executor's
+   * plane buffer of that panel; a GEMM with flag = 1 is the same product computed
+   * from those planes on the int8 tensor pipe */
+  GPB_OP_SLICE
 };
 typedef struct gpb_op {
   int32_t kind, stream, group, root;  /* stream 0 main, 1 critical; group 0 world, 1 row, 2 column */
-  int32_t buf[3], flag;               /* flag: ASSEMBLE add_noise, GEMV trans */
+  int32_t buf[3], flag;               /* flag: ASSEMBLE add_noise, GEMV trans, GEMM digit planes */
   int64_t off[3];
   int64_t count, job0, njobs;         /* count: doubles (collectives, COPY per job, ZERO, COMBINE) */
   int32_t mblk, nblk, ak, bk;         /* GEMM: blocks of 128 per job, K-major operands */

@@ -198,7 +198,7 @@ NCCL_ID_BYTES = 128  # GPB_NCCL_ID_BYTES
 BUFFERS = ("L", "DINV", "ROW", "COL", "VEC", "X", "KINV", "XCOL", "XROW", "LCOL")  # GPB_BUF_*
 OPS = {1: "ASSEMBLE", 2: "POTRF", 3: "GEMM", 4: "COPY", 5: "GEMV", 6: "COMBINE", 7: "BCAST", 8: "REDUCE",
        9: "ALLREDUCE", 10: "RECORD", 11: "WAIT", 12: "ZERO", 13: "SOLVE_FLOW", 14: "TRACE", 15: "MIRROR",
-       16: "SIGNAL", 17: "WAITFLAG"}  # GPB_OP_*
+       16: "SIGNAL", 17: "WAITFLAG", 18: "SLICE"}  # GPB_OP_*
 # gpb_op / gpb_op_job as numpy records (the schedule IR of gpb_dist_plan)
 OP_DTYPE = np.dtype([("kind", "<i4"), ("stream", "<i4"), ("group", "<i4"), ("root", "<i4"),
                      ("buf", "<i4", 3), ("flag", "<i4"), ("off", "<i8", 3), ("count", "<i8"),

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "dist_plan.h"
+#include "ozaki.cuh"
 #include "gemm.cuh"
 #include "gpb200.h"
 #include "kernels.cuh"
@@ -254,6 +255,8 @@ struct Phase {
   std::vector<int> nmirror;    // ... and its stores per job
   void* dev = nullptr;
   size_t bytes = 0;
+  std::vector<int64_t> oz_table;  // per op: offset of the OzakiJob table of a flagged GEMM (-1: none)
+  std::vector<int> oz_k;          // ... and its depth K
   int64_t launches_per_run = 0;
   ~Phase() {
     if (dev) cudaFree(dev);
@@ -300,6 +303,10 @@ struct gpb_dmodel {
   // peer-memory panel exchange (L.p2p): this rank's flag words (ready[src] at
   // src, free[src] at world + src) and every peer's row panel, column panel and
   // flags mapped through CUDA IPC
+  // digit planes of the row / column panels (L.planes > 0; boxed layout, tile t of the panel
+  // buffer at t * bi2 * planes bytes) and the saturation flag of the slicing kernels
+  int8_t* planes[GPB_NBUF] = {nullptr};
+  int* ozflag = nullptr;
   uint64_t* flags = nullptr;
   std::vector<void*> peer_row, peer_col, peer_flags;
   bool p2p_ready = false;
@@ -340,6 +347,8 @@ int build_phase(gpb_dmodel* m, int phase) {
   P.table.assign(P.ops.size(), -1);
   P.mirror.assign(P.ops.size(), -1);
   P.nmirror.assign(P.ops.size(), 0);
+  P.oz_table.assign(P.ops.size(), -1);
+  P.oz_k.assign(P.ops.size(), 0);
   P.launches_per_run = 0;
   for (size_t q = 0; q < P.ops.size(); ++q) {
     const gpb_op& o = P.ops[q];
@@ -393,9 +402,28 @@ int build_phase(gpb_dmodel* m, int phase) {
           g.lower = J[t].lower;
           put(&g, sizeof(g));
         }
+        if (o.flag && m->L.planes > 0 && (ba == GPB_BUF_ROW || ba == GPB_BUF_COL) &&
+            (bb == GPB_BUF_ROW || bb == GPB_BUF_COL)) {
+          // the same jobs for the digit-plane product: byte offsets into the panels' planes
+          align();
+          P.oz_table[q] = static_cast<int64_t>(host.size());
+          P.oz_k[q] = J[0].k;
+          for (int64_t t = 0; t < o.njobs; ++t) {
+            OzakiJob z{};
+            z.a_off = J[t].off[0] * m->L.planes;
+            z.b_off = J[t].off[1] * m->L.planes;
+            z.C = ref(m, J[t].buf[3], J[t].off[3]);
+            z.lower = J[t].lower;
+            put(&z, sizeof(z));
+          }
+          ++P.launches_per_run;  // two group windows
+        }
         ++P.launches_per_run;
         break;
       }
+      case GPB_OP_SLICE:
+        ++P.launches_per_run;
+        break;
       case GPB_OP_COPY: {
         align();
         P.table[q] = static_cast<int64_t>(host.size());
@@ -514,7 +542,33 @@ int run_phase(gpb_dmodel* m, int phase, double* enqueue_us = nullptr) {
         ++m->launches;
         break;
       }
+      case GPB_OP_SLICE: {
+        const double scale = ozaki_plane_scale(std::max(1.0, std::sqrt(m->nu + m->s2)));
+        DCUDA(launch_ozaki_slice_tiles(ref(m, o.buf[0], o.off[0]), o.count, L.bi, L.bi, scale,
+                                       m->planes[o.buf[0]] + o.off[0] * L.planes, L.planes, m->ozflag, s));
+        ++m->launches;
+        break;
+      }
       case GPB_OP_GEMM: {
+        if (P.oz_table[q] >= 0) {
+          // L(i,j) -= [X]_i [X]_j^T from the digit planes of the row and column panels
+          const double scale = ozaki_plane_scale(std::max(1.0, std::sqrt(m->nu + m->s2)));
+          const int kc = L.bi / kOzakiBK;
+          OzakiGemm g{};
+          g.a = {m->planes[o.buf[0]], o.a_kstride * L.planes, kc, int64_t(kc) * L.planes * kOzakiBox};
+          g.b = {m->planes[o.buf[1]], o.b_kstride * L.planes, kc, int64_t(kc) * L.planes * kOzakiBox};
+          g.M = g.N = L.bi;
+          g.K = P.oz_k[q];
+          g.slices = L.planes;
+          g.alpha = o.alpha * scale * scale;
+          g.beta = o.beta;
+          g.ldc_in = g.ldc_out = o.ldc;
+          g.jobs = reinterpret_cast<const OzakiJob*>(dev + P.oz_table[q]);
+          g.njobs = static_cast<int>(o.njobs);
+          DCUDA(launch_ozaki_gemm(g, s));
+          m->launches += L.planes > 4 ? 2 : 1;
+          break;
+        }
         GemmParams p{};
         p.jobs = static_cast<const GemmJob*>(tab);
         p.njobs = static_cast<int>(o.njobs);
@@ -881,6 +935,13 @@ void release(gpb_dmodel* m) {
       cudaFree(b);
       b = nullptr;
     }
+  for (int8_t*& b : m->planes)
+    if (b) {
+      cudaFree(b);
+      b = nullptr;
+    }
+  if (m->ozflag) cudaFree(m->ozflag);
+  m->ozflag = nullptr;
   for (void* p : {static_cast<void*>(m->z), static_cast<void*>(m->y), static_cast<void*>(m->zp),
                   static_cast<void*>(m->info), static_cast<void*>(m->parts), static_cast<void*>(m->red),
                   static_cast<void*>(m->flow_flags), static_cast<void*>(m->flow_x), static_cast<void*>(m->flags)})
@@ -1046,6 +1107,12 @@ int gpb_dist_model_create(gpb_dist* dc, const double* z, const double* y, int64_
   dalloc(reinterpret_cast<void**>(&m->flow_flags), solve_flow_scratch_bytes(L.Ti, L.bi));
   dalloc(reinterpret_cast<void**>(&m->flow_x), sizeof(double) * L.np_);
   if (s == GPB_OK) step(ensure_buffers(m, {GPB_BUF_L, GPB_BUF_DINV, GPB_BUF_ROW, GPB_BUF_COL, GPB_BUF_VEC}));
+  if (L.planes > 0) {  // planes of the panel buffers, one byte per entry and plane
+    for (int b : {GPB_BUF_ROW, GPB_BUF_COL})
+      if (L.bufsz[b] > 0) dalloc(reinterpret_cast<void**>(&m->planes[b]), size_t(L.bufsz[b]) * L.planes);
+    dalloc(reinterpret_cast<void**>(&m->ozflag), sizeof(int));
+    if (s == GPB_OK && cudaMemset(m->ozflag, 0, sizeof(int)) != cudaSuccess) step(fail(GPB_CUDA, "memset failed"));
+  }
   if (s == GPB_OK) {
     cudaMemcpyAsync(m->z, z, sizeof(double) * n * d, cudaMemcpyHostToDevice, m->st);
     cudaMemcpyAsync(m->y, y, sizeof(double) * n, cudaMemcpyHostToDevice, m->st);

@@ -20,6 +20,7 @@
 // tile receives the same sequence of GEMMs with the same K split as in the
 // single-GPU plan, so the factor is bitwise the single-GPU one.
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "dist_plan.h"
@@ -119,6 +120,11 @@ const Ref kNone{-1, 0};
 
 }  // namespace
 
+// group sizes of the factorisation (plan_common.h; the planes' rule on large grids as on one GPU)
+std::vector<int> dist_group_sizes(const DistLayout& L) {
+  return L.planes > 0 && L.Ti >= 48 ? chol_group_sizes(L.Ti, L.G, 4, 0) : chol_group_sizes(L.Ti, L.G);
+}
+
 int col_pos(const DistLayout& L, int j) {
   int c = 0;
   for (int t = 0; t < j; ++t)
@@ -160,7 +166,19 @@ int dist_layout(int rank, int world, int P, int Q, int64_t n, int64_t T, DistLay
   L.bp_user = static_cast<int>(lay[3]);
   L.b_user = static_cast<int>(lay[4]);
   L.bi2 = int64_t(L.bi) * L.bi;
+  // Trailing updates on the tcgen05 int8 pipe (ozaki.cuh), as on one GPU: GPB_OZAKI planes
+  // per operand (default 8), for 512-wide tiles (the smaller grids of the tests keep the
+  // DMMA kernels and stay bitwise equal to the single-GPU DMMA factor); GPB_DIST_PLANES=0: off
+  {
+    const char* e = getenv("GPB_OZAKI");
+    int planes = e ? atoi(e) : 8;
+    planes = planes <= 0 ? 0 : std::min(8, std::max(4, planes));
+    const char* d = getenv("GPB_DIST_PLANES");
+    L.planes = (L.bi >= 512 && !(d && atoi(d) == 0)) ? planes : 0;
+  }
+  // panels per group: plan_common.h; with the planes the single-GPU rule (gpb_api.cu choose_panels)
   L.G = chol_panels(L.Ti);
+  if (L.planes > 0 && !getenv("GPB_PANELS")) L.G = L.Ti >= 48 ? 8 : L.Ti >= 16 ? 4 : L.G;
   const int Ti = L.Ti;
   L.slot.assign(size_t(Ti) * Ti, -1);
   for (int i = 0; i < Ti; ++i)
@@ -205,7 +223,7 @@ int dist_layout(int rank, int world, int P, int Q, int64_t n, int64_t T, DistLay
   L.bufsz[GPB_BUF_XCOL] = P > 1 ? 2 * int64_t((Ti + Q - 1) / Q) * bi2 : 0;
   L.bufsz[GPB_BUF_XROW] = Q > 1 ? 2 * int64_t(Q) * std::max(1, L.cntx) * bi2 : 0;
   L.bufsz[GPB_BUF_LCOL] = Q > 1 ? 2 * int64_t(L.rows_per) * bi2 : 0;
-  const int ng = static_cast<int>(chol_group_sizes(Ti, L.G).size());
+  const int ng = static_cast<int>(dist_group_sizes(L).size());
   L.p2p = exchange == 1 && world > 1;
   L.nevents = std::max(3 * ng + 2, 2 * Ti + 1);  // factorisation / gradient schedules
   return GPB_OK;
@@ -229,7 +247,7 @@ void plan_factor(const DistLayout& L, Builder& b) {
   };
   const int64_t a_walk = int64_t(L.rows_per) * bi2;
   const int64_t b_walk = P == 1 ? a_walk : int64_t(L.cnt_max) * bi2;
-  const std::vector<int> sizes = chol_group_sizes(Ti, G);
+  const std::vector<int> sizes = dist_group_sizes(L);
   const int ng = static_cast<int>(sizes.size());
   const int ev_start = 0, ev_end = 1 + 3 * ng;
   auto ev_panel = [&](int s) { return 1 + s; };
@@ -300,6 +318,35 @@ void plan_factor(const DistLayout& L, Builder& b) {
   for (int s = 0, k0 = 0; s < ng; k0 += sizes[s], ++s) {
     const int gs = sizes[s], k1 = k0 + gs - 1, set = s % 2;
     if (s >= 2) b.wait(CRIT, ev_upd(s - 2));
+    // Digit planes (L.planes > 0): every rank slices the row and column panel tiles it
+    // received right after panel g's exchange; NEXT / UPD run from the planes (flag 1), and
+    // the in-group updates become left-looking: before POTRF(k0 + g) one product with
+    // K = g bi brings column k0 + g up to date from panels 0 .. g - 1 (LL), instead of g
+    // right-looking DMMA updates with K = bi (the single-GPU schedule, gpb_api.cu).
+    const bool oz_grp = L.planes > 0 && int64_t(gs) * bi >= 512 && k1 + 1 < Ti;
+    auto slice_panel = [&](int g) {
+      const int k = k0 + g;
+      auto slice = [&](Ref first, int64_t cnt) {
+        gpb_op o = b.base(GPB_OP_SLICE, CRIT);
+        o.buf[0] = first.buf;
+        o.off[0] = first.off;
+        o.count = cnt;
+        b.push(o);
+      };
+      int first = k + 1;
+      while (first < Ti && first % P != L.my_p) ++first;
+      if (first < Ti) slice(rowt(set, g, first), (Ti - 1 - first) / P + 1);
+      if (P > 1)
+        for (int pp = 0; pp < P; ++pp) {
+          int j0 = -1, cnt = 0;
+          for (int j = k + 1; j < Ti; ++j)
+            if (j % P == pp && j % Q == L.my_q) {
+              if (j0 < 0) j0 = j;
+              ++cnt;
+            }
+          if (cnt > 0) slice(colt(set, g, j0), cnt);
+        }
+    };
     if (L.p2p && s >= 2) {
       // this rank's stores of group s land in panel set s mod 2 of its peers:
       // wait until each has finished group s - 2 (its "free" flag)
@@ -316,6 +363,20 @@ void plan_factor(const DistLayout& L, Builder& b) {
     }
     for (int g = 0; g < gs; ++g) {
       const int k = k0 + g;
+      if (oz_grp && g > 0) {  // LL(g): owned tiles of column k from the group's earlier panels
+        b.begin();
+        for (int s2 = 0; s2 < L.nown(); ++s2) {
+          const int i = L.own_i[s2], j = L.own_j[s2];
+          if (j != k) continue;
+          b.job(rowt(set, 0, i), colt(set, 0, j), lt(i, j), lt(i, j), g * bi, i == j, i, j);
+        }
+        gpb_op o = b.gemm(CRIT, nb, nb, bi, true, true, -1.0, 1.0);
+        o.a_ktile = o.b_ktile = bi;
+        o.a_kstride = a_walk;
+        o.b_kstride = b_walk;
+        o.flag = 1;
+        b.close(o);
+      }
       if (L.my_q == k % Q) {
         if (L.rank == L.owner(k, k)) {
           gpb_op o = b.base(GPB_OP_POTRF, CRIT);
@@ -384,6 +445,10 @@ void plan_factor(const DistLayout& L, Builder& b) {
           b.coll(GPB_OP_BCAST, CRIT, COLG, pp, colt(set, g, js.front()), int64_t(js.size()) * bi2);
         }
       }
+      if (oz_grp) {
+        slice_panel(g);
+        continue;
+      }
       // in-group update: the group's later columns get panel k (K = b)
       b.begin();
       for (int s2 = 0; s2 < L.nown(); ++s2) {
@@ -409,6 +474,7 @@ void plan_factor(const DistLayout& L, Builder& b) {
       o.a_ktile = o.b_ktile = bi;
       o.a_kstride = a_walk;
       o.b_kstride = b_walk;
+      o.flag = oz_grp ? 1 : 0;
       b.close(o);
     };
     if (c_next < Ti) {

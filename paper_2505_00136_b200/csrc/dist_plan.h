@@ -30,6 +30,7 @@ struct DistLayout {
   int64_t vec[V_NSLOT] = {0};
   int nevents = 0;
   bool p2p = false;                 // peer-memory panel exchange (gpb_dist_set_exchange)
+  int planes = 0;                   // digit planes per operand of the trailing updates (0: FP64 DMMA)
   int owner(int i, int j) const { return (i % P) * Q + (j % Q); }
   int nown() const { return static_cast<int>(own_i.size()); }
 };

@@ -650,9 +650,7 @@ struct PhaseTimer {
   }
 };
 
-// fixed-point scale of an operand bounded by `bound`: digits cover |x| <= scale * 127 / 128
-// (ozaki.cuh); the margin absorbs round-off in entries that reach the bound
-double plane_scale(double bound) { return bound * (128.0 / 127.0) * (1.0 + 1e-9); }
+double plane_scale(double bound) { return ozaki_plane_scale(bound); }
 
 // assemble + factor (model.py:169-177 _ensure_factor)
 int ensure_factor(gpb_model* m) {

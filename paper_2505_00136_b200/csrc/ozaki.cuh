@@ -61,6 +61,10 @@ cudaError_t launch_ozaki_slice_t(const double* src, int rows, int64_t cols, int6
                                  int8_t* planes, int64_t kchunks, int64_t k0, int slices, int* flag,
                                  cudaStream_t st);
 
+// fixed-point scale of an operand bounded by `bound`: digits cover |x| <= scale * 127 / 128;
+// the margin absorbs round-off in entries that reach the bound
+inline double ozaki_plane_scale(double bound) { return bound * (128.0 / 127.0) * (1.0 + 1e-9); }
+
 struct OzakiOperand {
   const int8_t* planes;
   int64_t tile_stride;  // bytes from a tile to the next one along k

@@ -213,6 +213,9 @@ class Interp:
     def op_signal(self, o, jobs):
         pass
 
+    def op_slice(self, o, jobs):
+        pass  # digit planes are an executor detail: a flagged GEMM is the same product
+
     def op_waitflag(self, o, jobs):
         if int(o["j"]) != 0:  # "free" flags: buffer reuse cannot race here (messages are copies)
             return

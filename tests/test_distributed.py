@@ -36,6 +36,8 @@ def _case(kind):
         n, t, d, m = 256, 2, 3, 9
     elif kind == "grid8":  # 12 x 12 tile grid for the 2 x 4 grid of an 8-GPU box (n padded 1500 -> 1536)
         n, t, d, m = 1500, 12, 4, 20
+    elif kind == "planes512":  # 512-wide tiles (6 x 6 grid): the trailing updates run on the digit planes
+        n, t, d, m = 3072, 6, 4, 40
     elif kind == "padded":  # b = 100: n padded once to 640 (5 x 5 grid of 128)
         n, t, d, m = 600, 6, 3, 37
     else:  # b = 128, no padding (GPB_TILE=128 forces an 8 x 8 grid)
@@ -100,7 +102,8 @@ def _interp_rank(rank, world, grid, kind, exchange=0):
     (1, (1, 1), "dense", 0), (2, (1, 2), "padded", 0), (2, (2, 1), "dense", 0), (3, (1, 3), "padded", 0),
     (4, (2, 2), "dense", 0), (4, (2, 2), "padded", 0),
     (2, (1, 2), "dense", 1), (2, (2, 1), "padded", 1), (4, (2, 2), "dense", 1), (3, (1, 3), "padded", 1),
-    (4, (2, 2), "tiny", 0), (4, (2, 2), "tiny", 1), (8, (2, 4), "grid8", 0), (8, (2, 4), "grid8", 1)])
+    (4, (2, 2), "tiny", 0), (4, (2, 2), "tiny", 1), (8, (2, 4), "grid8", 0), (8, (2, 4), "grid8", 1),
+    (2, (1, 2), "planes512", 0), (4, (2, 2), "planes512", 1)])
 def test_schedule_ir_against_oracle_cpu(world, grid, kind, exchange):
     """Every rank's operation lists (factor, solves, gradient) replayed on CPU
     with gloo collectives reproduce the oracle; every rank ends with the same
@@ -222,7 +225,10 @@ def _check_device(res, kind):
     ll_o, L_o, grads_o = o.log_likelihood(), o.factor_dense(), o.loss_gradients()
     _, cov_o = o.predict_full_cov(zt)
     hist_o = o.optimize(lr=0.1, iterations=2)  # changes o's parameters: last
-    assert np.array_equal(res[0]["L"], res[0]["single"]), "block-cyclic factor differs from the single-GPU one"
+    if kind == "planes512":  # int8 digit planes in the executor: same contract, not the same bits
+        assert rel_fro(res[0]["L"], res[0]["single"]) <= 1e-11
+    else:
+        assert np.array_equal(res[0]["L"], res[0]["single"]), "block-cyclic factor differs from the single-GPU one"
     assert rel_fro(res[0]["L"], L_o) <= 1e-10
     for r in res:  # every rank: the full result
         assert abs(r["ll"] - ll_o) <= 1e-9 * abs(ll_o)
@@ -250,6 +256,16 @@ def test_device_executor_peer_memory_exchange_one_gpu(world, grid, kind):
     no kernel waits on another rank's kernel).  The factor stays bitwise the
     single-GPU one."""
     _check_device(_spawn("_device_rank", world, grid, kind, "host", "p2p"), kind)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,grid,exchange", [(2, (1, 2), "collective"), (2, (2, 1), "p2p"), (4, (2, 2), "p2p"),
+                                                 (4, (2, 2), "collective")])
+def test_device_executor_digit_planes_one_gpu(world, grid, exchange):
+    """512-wide tiles: every rank slices the row / column panels it received into digit
+    planes (SLICE ops) and runs NEXT / UPD on the tcgen05 int8 pipe (GEMM ops with flag 1);
+    factor, loss, predictions, gradients and Adam history against the oracle."""
+    _check_device(_spawn("_device_rank", world, grid, "planes512", "host", exchange), "planes512")
 
 
 def _not_pd_rank(rank, world, grid):
