@@ -762,8 +762,8 @@ def strong_base(args):
             "solves_ms": s_, "tflops": chol_flops(c["n"]) / (f * 1e-3) / 1e12,
             "note": "t_1 of the strong-scaling efficiency E(p) = t_1 / (p t_p) (1 warm-up + 2 timed): the "
                     "single-GPU path at its default (long products on the digit planes, 8-panel groups, "
-                    "left-looking in-group updates); the multi-GPU executor also runs NEXT / UPD on the planes "
-                    "but keeps 6-panel groups and right-looking DMMA in-group updates",
+                    "left-looking in-group updates), which is also the multi-GPU executor's schedule for "
+                    "512-wide tiles",
             "factor_ms_dmma_only": fac_dmma[0] if fac_dmma else None,
             "tflops_dmma_only": chol_flops(c["n"]) / (fac_dmma[0] * 1e-3) / 1e12 if fac_dmma else None,
             "emulated_2x4_factor_ms_per_rank": per_rank,
@@ -771,7 +771,9 @@ def strong_base(args):
             "emulated_2x4_link_factor_ms_per_rank": per_rank_link,
             "emulated_2x4_link_efficiency": f / (8 * max(per_rank_link)),
             "emulation": "each rank of the 2 x 4 grid run alone on this GPU (its kernels' device time, "
-                         "no cross-rank waits): with no-op collectives E(8) <= t_1 / (8 max_r t_r); "
+                         "no cross-rank waits): with no-op collectives E(8) <= t_1 / (8 max_r t_r) -- a bound "
+                         "above 1 says that t_1 itself is not purely throughput-bound (the single-GPU critical "
+                         "path shows in it), not that 8 GPUs would scale super-linearly; "
                          f"the 'link' pass charges every collective {EMU_LINK.split(',')[0]} us + "
                          f"bytes / {EMU_LINK.split(',')[1]} GB/s on its stream (modelled NVLink transfer)"}
 
