@@ -154,6 +154,14 @@ struct DevBuf {
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
+// Allocation of an OPTIONAL buffer (digit planes: the FP64 DMMA kernels compute the same
+// products without them): false, with the CUDA error cleared, when the memory is not there.
+bool ensure_optional(DevBuf& b, size_t nbytes) {
+  if (b.ensure(nbytes) == cudaSuccess) return true;
+  cudaGetLastError();
+  return false;
+}
+
 }  // namespace
 
 struct gpb_ctx {
@@ -700,8 +708,8 @@ int ensure_factor(gpb_model* m) {
       any = any || (int64_t(grp.np) * bi >= m->oz_chol_min_k && grp.next_cnt + grp.upd_cnt > 0);
     oz = any;
   }
+  if (oz && !ensure_optional(m->Ps, size_t(2) * m->G * panel_bytes)) oz = false;  // no room: DMMA
   if (oz) {
-    CUDA_TRY(m->Ps.ensure(size_t(2) * m->G * panel_bytes));
     if (!m->ozflag.p) {
       CUDA_TRY(m->ozflag.ensure(sizeof(int)));
       CUDA_TRY(cudaMemsetAsync(m->ozflag.p, 0, sizeof(int), m->st));
@@ -1378,7 +1386,12 @@ int64_t pred_chunk(gpb_model* m, int64_t mt) {
   const double per_col = 8.0 * double(m->np_ + m->bi + m->np_ / kSekBlock + m->np_ / GBM + 4) +
                          double(m->oz_slices) * double(m->np_);
   // cached blocks are returned to CUDA if an allocation would otherwise fail
-  const double avail = double(free_b) + double(g_cache.cached) + double(m->Bv.bytes);
+  double avail = double(free_b) + double(g_cache.cached) + double(m->Bv.bytes);
+  if (m->oz_slices > 0 && int64_t(m->Ti - 1) * m->bi >= m->oz_min_k) {
+    // the planes of L (allocated on the first sweep) come out of the same memory
+    const double ls = double(m->oz_slices) * double(m->Ti) * (m->Ti + 1) / 2 * double(m->bi) * m->bi;
+    if (double(m->Ls.bytes) < ls && avail - ls > 0.25 * avail) avail -= ls;
+  }
   const double budget = std::min(48e9, 0.6 * avail);
   const int64_t c = std::max<int64_t>(GBM, int64_t(budget / per_col) / GBM * GBM);
   return std::min(c, all);
@@ -1406,10 +1419,15 @@ int predict_chunk(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var,
     const GemmJob* jobs = m->pred_jobs.as<GemmJob>();
     // tcgen05 digit-plane products for the long-k rows (ozaki.cuh); |V| <=
     // sqrt(k(x*, x*)) = sqrt(vertical) since k*^T K^-1 k* <= k**
-    const bool oz = m->oz_slices > 0 && int64_t(Ti - 1) * bi >= m->oz_min_k;
+    const bool oz_wanted = m->oz_slices > 0 && int64_t(Ti - 1) * bi >= m->oz_min_k;
+    bool oz = oz_wanted;
+    if (oz && !m->ls_ok) {  // planes of L and of V^T: optional, the DMMA sweep needs neither
+      const int64_t ntiles = int64_t(Ti) * (Ti + 1) / 2;
+      if (!ensure_optional(m->Ls, size_t(m->oz_slices) * ntiles * int64_t(bi) * bi)) oz = false;
+    }
+    if (oz && !ensure_optional(m->Vs, size_t(m->oz_slices) * mcp * m->np_)) oz = false;
     if (oz) {
       GPB_TRY(ensure_l_planes(m));
-      CUDA_TRY(m->Vs.ensure(size_t(m->oz_slices) * mcp * m->np_));
       m->oz_sb = plane_scale(std::sqrt(m->nu));
     }
     for (int i = 0; i < Ti; ++i) {
