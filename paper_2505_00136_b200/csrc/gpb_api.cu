@@ -157,6 +157,7 @@ int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 // Allocation of an OPTIONAL buffer (digit planes: the FP64 DMMA kernels compute the same
 // products without them): false, with the CUDA error cleared, when the memory is not there.
 bool ensure_optional(DevBuf& b, size_t nbytes) {
+  if (getenv("GPB_PLANES_ALLOC_FAIL")) return false;  // tests: behave as if the memory were not there
   if (b.ensure(nbytes) == cudaSuccess) return true;
   cudaGetLastError();
   return false;

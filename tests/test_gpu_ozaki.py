@@ -228,3 +228,20 @@ def test_toggling_planes_keeps_results_within_contract(runtime):
     c = model.compute_loss()
     assert a == c  # bitwise reproducible after the round trip
     assert abs(a - b) <= 1e-10 * abs(b)
+
+
+def test_planes_are_optional_when_memory_is_short(runtime, monkeypatch):
+    """The plane buffers are an optimisation: when they cannot be allocated the
+    same calls run on the FP64 DMMA kernels (bitwise the digit_planes = 0 results)."""
+    train, test = gpb.make_msd_dataset(4096, 300, 6, seed=2)
+    monkeypatch.setenv("GPB_PLANES_ALLOC_FAIL", "1")
+    a = gpb.GPModel(train, gpb.KernelParams(1.0, 1.0, 0.1), tiles_per_dim=8)
+    assert a.digit_planes == 8
+    ra = a.predict_with_full_cov(test)
+    la = a.compute_loss()
+    monkeypatch.delenv("GPB_PLANES_ALLOC_FAIL")
+    b = gpb.GPModel(train, gpb.KernelParams(1.0, 1.0, 0.1), tiles_per_dim=8)
+    b.digit_planes = 0
+    rb = b.predict_with_full_cov(test)
+    assert la == b.compute_loss()
+    assert np.array_equal(ra.mean, rb.mean) and np.array_equal(ra.full_covariance, rb.full_covariance)
