@@ -27,7 +27,7 @@ for rep in range(3):
     lib.gpb_model_kernel_busy(m._handle, busy)
     os.environ.pop("GPB_PROF_DUMP")
     dt = m.device_timings()
-names = {0: "GEMM", 1: "POTRF", 2: "SEK", 3: "SOLVE", 4: "OTHER"}
+names = {0: "GEMM", 1: "POTRF", 2: "SEK", 3: "SOLVE", 4: "OTHER", 5: "PLANES"}
 rows = [tuple(float(x) for x in line.split()) for line in open(dump)]
 rows.sort(key=lambda r: r[1])
 print(f"n={n}: factor {dt['factor']:.3f} ms assembly {dt['assembly']:.3f} solves {dt['solves']:.3f}")
