@@ -233,7 +233,9 @@ struct gpb_model {
   DevBuf Ls, Vs, ozflag;
   // ... and of the solved panels of the current group (same element order as
   // `scratch`), read by the trailing updates NEXT / UPD of the factorisation
-  DevBuf Ps, oz_jobs, fc_oz_jobs;
+  DevBuf Ps, oz_jobs, fc_oz_jobs, Xs, kinv_oz_jobs;  // Xs: planes of X = L^-1 (gradient)
+  std::vector<int64_t> kinv_oz_off, kinv_oz_cnt;  // per k segment of kOzakiMaxK: job range
+  int64_t oz_grad_min_n = 4096;                   // K^-1 = X^T X on the planes from this n
   bool vs_ok = false;  // Vs holds the planes of every row block of the current V (Bv)
   int64_t oz_chol_min_k = 512;  // updates with a shorter K = np * bi stay on the DMMA kernel
   bool oz_chol = true;           // GPB_OZAKI_CHOL=0: digit planes for the prediction sweep only
@@ -1039,6 +1041,39 @@ int build_inv_plan(gpb_model* m) {
         m->kinv_fl += 2.0 * GBM * GBN * double(g.K) * (g.nlim ? g.nlim : m->bi / GBN);
       }
   m->kinv_cnt = jobs.size() - m->kinv_off;
+  // The same product on the digit planes (ozaki.cuh): the planes of column panel c of X are
+  // sliced transposed (operand row = column of the panel, k = row), chunk major, so every
+  // panel has the same row-block stride; job (r, c) reads panel r from k = 0 and panel c
+  // from k = (r - c) bi, K = (Ti - r) bi, in segments of kOzakiMaxK (exact int32 sums).
+  {
+    const int S = std::max(m->oz_slices, 1);
+    const int nrb = m->bi / kOzakiBM;
+    const int64_t chunk_b = int64_t(nrb) * S * kOzakiBox;  // bytes per k chunk of a panel
+    const int64_t seg_chunks = kOzakiMaxK / kOzakiBK;
+    std::vector<OzakiJob> oj;
+    m->kinv_oz_off.clear();
+    m->kinv_oz_cnt.clear();
+    for (int64_t seg = 0; seg * kOzakiMaxK < int64_t(Ti) * m->bi; ++seg) {
+      m->kinv_oz_off.push_back(static_cast<int64_t>(oj.size()));
+      for (int r = 0; r < Ti; ++r) {  // longest K first
+        const int64_t chunks = int64_t(Ti - r) * m->bi / kOzakiBK - seg * seg_chunks;
+        if (chunks <= 0) continue;
+        for (int c = 0; c <= r; ++c) {
+          OzakiJob o{};
+          o.a_off = h_tri_cm(r, r, Ti) * bi2 * S + seg * seg_chunks * chunk_b;
+          o.b_off = h_tri_cm(c, c, Ti) * bi2 * S + (int64_t(r - c) * m->bi / kOzakiBK + seg * seg_chunks) * chunk_b;
+          o.C = Kv + h_tri_cm(r, c, Ti) * bi2;
+          o.lower = r == c;
+          o.kchunks = static_cast<int>(std::min(chunks, seg_chunks));
+          oj.push_back(o);
+        }
+      }
+      m->kinv_oz_cnt.push_back(static_cast<int64_t>(oj.size()) - m->kinv_oz_off.back());
+    }
+    CUDA_TRY(m->kinv_oz_jobs.ensure(sizeof(OzakiJob) * std::max<size_t>(1, oj.size())));
+    if (!oj.empty())
+      CUDA_TRY(cudaMemcpy(m->kinv_oz_jobs.p, oj.data(), sizeof(OzakiJob) * oj.size(), cudaMemcpyHostToDevice));
+  }
   CUDA_TRY(m->inv_jobs.ensure(sizeof(GemmJob) * jobs.size()));
   CUDA_TRY(cudaMemcpy(m->inv_jobs.p, jobs.data(), sizeof(GemmJob) * jobs.size(),
                       cudaMemcpyHostToDevice));
@@ -1097,11 +1132,57 @@ int loss_gradients(gpb_model* m, double out[3]) {
   const int64_t nblk = ntiles * (bi / kSekBlock) * (bi / kSekBlock);
   if (tl || tv) {
     // K^-1 = X^T X, lower tiles (model.py:362-380)
-    GemmParams kp = views(base_params(jobs + m->kinv_off, static_cast<int>(m->kinv_cnt), 1, nb, bi, bi,
-                                      bi, 1.0, 0.0),
-                          m->X, m->X);
-    kp.max_k = int64_t(Ti) * bi;
-    GPB_TRY(gemm(m, kp, false, false, EPI_AXPBY, m->kinv_fl));
+    // On the int8 pipe when the planes are on: |X_ij| <= ||L^-1||_2 <= 1 / sqrt(noise) (K >= noise I;
+    // 1 on the decoupled padding rows) bounds the operand; tiny noise keeps the FP64 kernels.
+    bool planes = m->oz_slices > 0 && m->np_ >= m->oz_grad_min_n && m->s2 >= 1e-6;
+    if (planes && !ensure_optional(m->Xs, size_t(m->oz_slices) * ntiles * bi2)) planes = false;
+    if (planes) {
+      if (!m->ozflag.p) {
+        CUDA_TRY(m->ozflag.ensure(sizeof(int)));
+        CUDA_TRY(cudaMemsetAsync(m->ozflag.p, 0, sizeof(int), m->st));
+      }
+      const int S = m->oz_slices, nrb = bi / kOzakiBM;
+      const double sx = plane_scale(std::max(1.0, 1.0 / std::sqrt(m->s2)));
+      {
+        ProfScope ps(m, KC_OTHER, 0.0);
+        for (int c = 0; c < Ti; ++c) {  // planes of column panel c of X, transposed
+          const int64_t e0 = h_tri_cm(c, c, Ti) * bi2;
+          CUDA_TRY(launch_ozaki_slice_t(X + e0, int64_t(Ti - c) * bi, bi, bi, sx, m->Xs.as<int8_t>() + e0 * S, 1,
+                                        nrb, 0, S, m->ozflag.as<int>(), m->st));
+          ++m->launches;
+        }
+      }
+      for (size_t seg = 0; seg < m->kinv_oz_off.size(); ++seg) {
+        OzakiGemm g{};
+        g.a = g.b = {m->Xs.as<int8_t>(), 0, int(1) << 30, int64_t(S) * kOzakiBox, int64_t(nrb) * S * kOzakiBox};
+        g.M = g.N = bi;
+        g.K = static_cast<int>(std::min<int64_t>(kOzakiMaxK, int64_t(Ti) * bi - int64_t(seg) * kOzakiMaxK));
+        g.slices = S;
+        g.alpha = sx * sx;
+        g.beta = seg == 0 ? 0.0 : 1.0;
+        g.ldc_in = g.ldc_out = bi;
+        g.jobs = m->kinv_oz_jobs.as<OzakiJob>() + m->kinv_oz_off[seg];
+        g.njobs = static_cast<int>(m->kinv_oz_cnt[seg]);
+        ProfScope ps(m, KC_OZAKI, seg == 0 ? m->kinv_fl : 0.0);
+        CUDA_TRY(launch_ozaki_gemm(g, m->st));
+        m->launches += 2;
+      }
+      int over = 0;
+      CUDA_TRY(cudaMemcpyAsync(&over, m->ozflag.p, sizeof(int), cudaMemcpyDeviceToHost, m->st));
+      CUDA_TRY(cudaStreamSynchronize(m->st));
+      if (over) {  // an entry beyond the bound: repeat on the FP64 kernels
+        CUDA_TRY(cudaMemsetAsync(m->ozflag.p, 0, sizeof(int), m->st));
+        ++m->oz_fallbacks;
+        planes = false;
+      }
+    }
+    if (!planes) {
+      GemmParams kp = views(base_params(jobs + m->kinv_off, static_cast<int>(m->kinv_cnt), 1, nb, bi, bi,
+                                        bi, 1.0, 0.0),
+                            m->X, m->X);
+      kp.max_k = int64_t(Ti) * bi;
+      GPB_TRY(gemm(m, kp, false, false, EPI_AXPBY, m->kinv_fl));
+    }
     // fused trace pass (model.py:382-414 with covariance.py:196-220 regenerated)
     CUDA_TRY(launch_trace(m->Kinv.as<double>(), m->tile_cm.as<int2>(), ntiles, TraceTiles{0, 0, 0, nullptr},
                           m->zp.as<double>(), m->alpha.as<double>(), static_cast<int>(m->d), bi,
@@ -1473,7 +1554,7 @@ int predict_chunk(gpb_model* m, const double* zt_dev, int64_t mt, bool want_var,
       if (oz) {  // planes of V_i^T for the rows below (and the full-covariance product)
         ProfScope ps(m, KC_OTHER, 0.0);
         CUDA_TRY(launch_ozaki_slice_t(Bv + int64_t(i) * bi * mcp, bi, mcp, mcp, m->oz_sb, m->Vs.as<int8_t>(),
-                                      m->np_ / kOzakiBK, int64_t(i) * bi, m->oz_slices, m->ozflag.as<int>(),
+                                      m->np_ / kOzakiBK, 1, int64_t(i) * bi, m->oz_slices, m->ozflag.as<int>(),
                                       m->st));
         ++m->launches;
       }
@@ -1691,7 +1772,7 @@ void free_model(gpb_model* m, bool keep = true) {
                     &m->X, &m->Kinv, &m->part_l, &m->part_v, &m->part_x, &m->inv_jobs,
                     &m->Bv, &m->W, &m->mpart, &m->sq, &m->pred_jobs, &m->zt, &m->mean, &m->var,
                     &m->S, &m->fc_jobs, &m->gp_panel, &m->gp_h, &m->gp_jobs, &m->gp_tiles,
-                    &m->Ls, &m->Vs, &m->ozflag, &m->Ps, &m->oz_jobs, &m->fc_oz_jobs})
+                    &m->Ls, &m->Vs, &m->ozflag, &m->Ps, &m->oz_jobs, &m->fc_oz_jobs, &m->Xs, &m->kinv_oz_jobs})
     b->release(keep);
 }
 
@@ -2175,7 +2256,7 @@ int gpb_model_set_ozaki(gpb_model* m, int slices) {
   if (slices != m->oz_slices) {
     // plane offsets depend on the count, the panel grouping on whether planes are in use:
     // a different grouping is a different (round-off level) factor, so the cached one goes
-    m->ls_ok = m->plan_ok = m->vs_ok = false;
+    m->ls_ok = m->plan_ok = m->vs_ok = m->inv_plan = false;
     m->oz_slices = slices;
     const int g = choose_panels(m);
     if (g != m->G) {

@@ -119,7 +119,7 @@ constexpr size_t smem_bytes(int P) {
 
 struct OperandArgs {
   const int8_t* planes;
-  long long tile_stride, rb_stride;
+  long long tile_stride, rb_stride, chunk_stride;
   int chunks_per_tile;
 };
 
@@ -155,12 +155,15 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const OzakiArgs
   long long a_off = p.a_off, b_off = p.b_off;
   const double* Cin = p.Cin;
   double* Cout = p.Cout;
+  int kchunks = p.kchunks;
   if (p.jobs) {
     const OzakiJob j = p.jobs[job];
     if (j.lower && nt > mt) return;
     a_off += j.a_off;
     b_off += j.b_off;
-    Cin = Cout = j.C;
+    Cout = j.C;
+    Cin = p.beta != 0.0 ? j.C : nullptr;
+    if (j.kchunks > 0) kchunks = j.kchunks;
   }
 
   if (warp == 1 && lane == 0) {
@@ -186,13 +189,13 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const OzakiArgs
       const int8_t* asrc = p.a.planes + a_off + mt * p.a.rb_stride;
       const int8_t* bsrc = p.b.planes + b_off + nt * p.b.rb_stride;
       int st = 0, ph = 0, ac = 0, bc = 0;  // chunk inside the current tile of A / B
-      for (int c = 0; c < p.kchunks; ++c) {
+      for (int c = 0; c < kchunks; ++c) {
         mbar_wait(empty0 + 8 * st, ph ^ 1);
         const uint32_t fb = full0 + 8 * st;
         mbar_expect_tx(fb, kStageBytes);
         const uint32_t sa = base + st * kStageBytes;
-        bulk_load(sa, asrc + static_cast<long long>(ac) * p.plane_bytes, kOperandBytes, fb);
-        bulk_load(sa + kOperandBytes, bsrc + static_cast<long long>(bc) * p.plane_bytes, kOperandBytes, fb);
+        bulk_load(sa, asrc + static_cast<long long>(ac) * p.a.chunk_stride, kOperandBytes, fb);
+        bulk_load(sa + kOperandBytes, bsrc + static_cast<long long>(bc) * p.b.chunk_stride, kOperandBytes, fb);
         if (++ac == p.a.chunks_per_tile) ac = 0, asrc += p.a.tile_stride;
         if (++bc == p.b.chunks_per_tile) bc = 0, bsrc += p.b.tile_stride;
         if (++st == NST) st = 0, ph ^= 1;
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1) ozaki_gemm_kernel(const OzakiArgs
       constexpr uint32_t idesc =
           (2u << 4) | (1u << 7) | (1u << 10) | ((kOzakiBN >> 3) << 17) | ((kOzakiBM >> 4) << 24);
       int st = 0, ph = 0;
-      for (int c = 0; c < p.kchunks; ++c) {
+      for (int c = 0; c < kchunks; ++c) {
         mbar_wait(full0 + 8 * st, ph);
         tc_fence_after();
         const uint32_t sa = base + st * kStageBytes, sb = sa + kOperandBytes;
@@ -362,11 +365,11 @@ __global__ void __launch_bounds__(256)
 // so that the stores run along the box rows (one 32-byte row per column)
 __global__ void __launch_bounds__(256)
     ozaki_slice_t_kernel(const double* __restrict__ src, long long ld, double inv_scale, int8_t* __restrict__ planes,
-                         long long kchunks, long long k0, int slices, int* flag) {
+                         long long rb_boxes, long long kc_boxes, long long k0, int slices, int* flag) {
   __shared__ unsigned stage[kOzakiMaxSlices][64][17];
   const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
   const long long c0 = static_cast<long long>(blockIdx.x) * 64;
-  const int kb = blockIdx.y * 64;
+  const long long kb = static_cast<long long>(blockIdx.y) * 64;
   bool over = false;
 #pragma unroll
   for (int kg = ty; kg < 16; kg += 4) {
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(256)
   const long long rb = c0 / kOzakiBM;
   const int row0 = static_cast<int>(c0 % kOzakiBM);
   for (int kc2 = 0; kc2 < 2; ++kc2) {
-    int8_t* box = planes + (rb * kchunks + (k0 + kb) / kOzakiBK + kc2) * slices * kOzakiBox;
+    int8_t* box = planes + (rb * rb_boxes + ((k0 + kb) / kOzakiBK + kc2) * kc_boxes) * slices * kOzakiBox;
     for (int p = 0; p < slices; ++p) {
 #pragma unroll
       for (int c = cr; c < 64; c += 32)
@@ -455,14 +458,15 @@ cudaError_t launch_ozaki_slice_tiles(const double* src, int64_t ntiles, int tr, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_ozaki_slice_t(const double* src, int rows, int64_t cols, int64_t ld, double scale,
-                                 int8_t* planes, int64_t kchunks, int64_t k0, int slices, int* flag,
-                                 cudaStream_t st) {
+cudaError_t launch_ozaki_slice_t(const double* src, int64_t rows, int64_t cols, int64_t ld, double scale,
+                                 int8_t* planes, int64_t rb_boxes, int64_t kc_boxes, int64_t k0, int slices,
+                                 int* flag, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (slices < 1 || slices > kOzakiMaxSlices || (rows & 63) || (cols & 127) || (k0 & 63))
     return cudaErrorInvalidValue;
   dim3 grid(static_cast<unsigned>(cols / 64), static_cast<unsigned>(rows / 64));
-  ozaki_slice_t_kernel<<<grid, 256, 0, st>>>(src, ld, 1.0 / scale, planes, kchunks, k0, slices, flag);
+  if (rows / 64 > 65535) return cudaErrorInvalidValue;
+  ozaki_slice_t_kernel<<<grid, 256, 0, st>>>(src, ld, 1.0 / scale, planes, rb_boxes, kc_boxes, k0, slices, flag);
   return cudaGetLastError();
 }
 
@@ -470,10 +474,11 @@ cudaError_t launch_ozaki_gemm(const OzakiGemm& g, cudaStream_t st) {
   if (g.M % kOzakiBM || g.N % kOzakiBN || g.K % kOzakiBK || g.K <= 0 || g.K > kOzakiMaxK || g.slices < 4 ||
       g.slices > kOzakiMaxSlices)
     return cudaErrorInvalidValue;
-  if (g.jobs && (g.njobs <= 0 || g.beta == 0.0)) return cudaErrorInvalidValue;
+  if (g.jobs && g.njobs <= 0) return cudaErrorInvalidValue;
   OzakiArgs a;
-  a.a = {g.a.planes, g.a.tile_stride, g.a.rb_stride, g.a.chunks_per_tile};
-  a.b = {g.b.planes, g.b.tile_stride, g.b.rb_stride, g.b.chunks_per_tile};
+  const long long boxes = static_cast<long long>(g.slices) * kOzakiBox;
+  a.a = {g.a.planes, g.a.tile_stride, g.a.rb_stride, g.a.chunk_stride ? g.a.chunk_stride : boxes, g.a.chunks_per_tile};
+  a.b = {g.b.planes, g.b.tile_stride, g.b.rb_stride, g.b.chunk_stride ? g.b.chunk_stride : boxes, g.b.chunks_per_tile};
   a.a_off = g.a_off;
   a.b_off = g.b_off;
   a.jobs = g.jobs;

@@ -55,11 +55,14 @@ cudaError_t launch_ozaki_slice_tiles(const double* src, int64_t ntiles, int tr, 
 
 // Digit planes of a (rows x cols, row-major, ld) block of doubles TRANSPOSED:
 // operand row = source column c, k = k0 + source row.  One tile spans the
-// whole K range: box of (c / 128, k / 32) at planes + ((c / 128) * kchunks +
-// k / 32) * slices * 4096.  rows and k0 multiples of 64, cols of 128.
-cudaError_t launch_ozaki_slice_t(const double* src, int rows, int64_t cols, int64_t ld, double scale,
-                                 int8_t* planes, int64_t kchunks, int64_t k0, int slices, int* flag,
-                                 cudaStream_t st);
+// whole K range: box of (c / 128, k / 32) at planes + ((c / 128) * rb_boxes +
+// (k / 32) * kc_boxes) * slices * 4096 -- row-block major (rb_boxes = chunks
+// of the whole K, kc_boxes = 1: the prediction's V^T) or chunk major (rb_boxes
+// = 1, kc_boxes = row blocks: operands of different K with one rb_stride, the
+// gradient's X panels).  rows and k0 multiples of 64, cols of 128.
+cudaError_t launch_ozaki_slice_t(const double* src, int64_t rows, int64_t cols, int64_t ld, double scale,
+                                 int8_t* planes, int64_t rb_boxes, int64_t kc_boxes, int64_t k0, int slices,
+                                 int* flag, cudaStream_t st);
 
 // fixed-point scale of an operand bounded by `bound`: digits cover |x| <= scale * 127 / 128;
 // the margin absorbs round-off in entries that reach the bound
@@ -70,12 +73,14 @@ struct OzakiOperand {
   int64_t tile_stride;  // bytes from a tile to the next one along k
   int chunks_per_tile;  // tc / 32
   int64_t rb_stride;    // bytes from a row block to the next one inside a tile: chunks_per_tile * slices * 4096
+  int64_t chunk_stride = 0;  // bytes from a k chunk to the next one inside a tile (0: slices * 4096)
 };
 
 struct OzakiJob {
   int64_t a_off, b_off;  // byte offsets of the job's first row block at k = 0 (added to the launch's)
   double* C;
-  int lower, pad;
+  int lower;
+  int kchunks;  // this job's depth in chunks of 32 (0: the launch's K)
 };
 
 struct OzakiGemm {
@@ -90,8 +95,8 @@ struct OzakiGemm {
   int64_t ldc_in, ldc_out;
   // grouped form (the factorisation's trailing updates): njobs independent
   // M x N products sharing the operand descriptions, job j reading its rows
-  // from jobs[j].a_off / b_off and updating C in place (beta != 0, ldc_in =
-  // ldc_out).  A `lower` job skips the blocks above the diagonal.
+  // from jobs[j].a_off / b_off and writing C = beta C + alpha sum in place
+  // (ldc_in = ldc_out).  A `lower` job skips the blocks above the diagonal.
   const OzakiJob* jobs = nullptr;  // device array
   int njobs = 0;
 };

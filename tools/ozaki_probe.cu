@@ -78,7 +78,7 @@ int run_case(int M, int N, int K, int kt, int S, bool time_only, int reps) {
   cudaEventElapsedTime(&ms_sa, e0, e1);
   CK(cudaEventRecord(e0, st));
   // B (K x N) -> planes [N][K]
-  CK(launch_ozaki_slice_t(B, K, N, N, sb, Bp, K / 32, 0, S, flag, st));
+  CK(launch_ozaki_slice_t(B, K, N, N, sb, Bp, K / 32, 1, 0, S, flag, st));
   CK(cudaEventRecord(e1, st));
   CK(cudaStreamSynchronize(st));
   float ms_sb;
