@@ -245,3 +245,25 @@ def test_planes_are_optional_when_memory_is_short(runtime, monkeypatch):
     rb = b.predict_with_full_cov(test)
     assert la == b.compute_loss()
     assert np.array_equal(ra.mean, rb.mean) and np.array_equal(ra.full_covariance, rb.full_covariance)
+
+
+def test_gradient_planes_across_k_segments(runtime):
+    """n = 36864 (72 tiles of 512): the K^-1 = X^T X products are deeper than one int32-exact
+    segment (32768), so the first columns run in two k segments; against the FP64 DMMA path."""
+    model, _ = _train_model(36864, 8, 72, 8)
+    g = np.array(model.loss_gradients())
+    assert model.digit_plane_fallbacks() == 0
+    model.digit_planes = 0
+    gd = np.array(model.loss_gradients())
+    assert np.max(np.abs(g - gd) / np.abs(gd)) <= 1e-10
+
+
+def test_gradient_with_tiny_noise_keeps_fp64(runtime):
+    """noise below 1e-6: no useful bound on L^-1, the K^-1 product stays on the FP64 kernels
+    (same launches as with the planes off)."""
+    train, _ = gpb.make_msd_dataset(4096, 0, 6, seed=4)
+    a = gpb.GPModel(train, gpb.KernelParams(1.0, 1.0, 1e-7), tiles_per_dim=8)
+    b = gpb.GPModel(train, gpb.KernelParams(1.0, 1.0, 1e-7), tiles_per_dim=8)
+    b.digit_planes = 0
+    ga, gb = np.array(a.loss_gradients()), np.array(b.loss_gradients())
+    assert np.max(np.abs(ga - gb) / np.abs(gb)) <= 1e-7  # conditioning 1e7: the factors differ at 1e-13
