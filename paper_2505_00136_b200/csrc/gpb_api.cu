@@ -236,6 +236,16 @@ struct gpb_model {
   DevBuf Ps, oz_jobs, fc_oz_jobs, Xs, kinv_oz_jobs;  // Xs: planes of X = L^-1 (gradient)
   std::vector<int64_t> kinv_oz_off, kinv_oz_cnt;  // per k segment of kOzakiMaxK: job range
   int64_t oz_grad_min_n = 4096;                   // K^-1 = X^T X on the planes from this n
+  // left-looking X = L^-1 on the planes (from oz_llx_min_tiles internal tiles): per row i and k
+  // segment the product jobs, per row the tiles to slice into Xs
+  DevBuf llx_jobs, llx_slices;
+  std::vector<std::vector<int64_t>> llx_off, llx_cnt;
+  std::vector<int64_t> llx_slice_off;
+  std::vector<OzakiSliceJob> llx_slices_host;  // `planes` = byte offset into Xs until uploaded
+  const void* llx_slices_base = nullptr;       // the Xs the uploaded table points into
+  std::vector<double> llx_fl;
+  int oz_llx_min_tiles = 32;
+  bool grad_fp64_only = false;  // transient: repeat of a gradient whose digits saturated
   bool vs_ok = false;  // Vs holds the planes of every row block of the current V (Bv)
   int64_t oz_chol_min_k = 512;  // updates with a shorter K = np * bi stay on the DMMA kernel
   bool oz_chol = true;           // GPB_OZAKI_CHOL=0: digit planes for the prediction sweep only
@@ -1073,6 +1083,46 @@ int build_inv_plan(gpb_model* m) {
     CUDA_TRY(m->kinv_oz_jobs.ensure(sizeof(OzakiJob) * std::max<size_t>(1, oj.size())));
     if (!oj.empty())
       CUDA_TRY(cudaMemcpy(m->kinv_oz_jobs.p, oj.data(), sizeof(OzakiJob) * oj.size(), cudaMemcpyHostToDevice));
+    // Left-looking X = L^-1 on the planes: A(i, j) = -sum_{m=j}^{i-1} L(i, m) X(m, j) for row i in one
+    // product per k segment (K = (i - j) bi: the planes of L's row panel from tile j against the planes
+    // of column panel j of X from k = 0), then F_i, then row i's tiles are sliced into the X planes.
+    std::vector<OzakiJob> lj;
+    std::vector<OzakiSliceJob> sj;
+    m->llx_off.assign(Ti, {});
+    m->llx_cnt.assign(Ti, {});
+    m->llx_slice_off.assign(Ti + 1, 0);
+    m->llx_fl.assign(Ti, 0.0);
+    const int64_t seg_tiles = kOzakiMaxK / m->bi;
+    for (int i = 0; i < Ti; ++i) {
+      for (int64_t seg = 0; seg * kOzakiMaxK < int64_t(i) * m->bi; ++seg) {
+        m->llx_off[i].push_back(static_cast<int64_t>(lj.size()));
+        for (int j = 0; j < i; ++j) {
+          const int64_t chunks = int64_t(i - j) * m->bi / kOzakiBK - seg * seg_chunks;
+          if (chunks <= 0) continue;
+          OzakiJob o{};
+          o.a_off = (h_tri_rm(i, 0) + j + seg * seg_tiles) * bi2 * S;
+          o.b_off = h_tri_cm(j, j, Ti) * bi2 * S + seg * seg_chunks * chunk_b;
+          o.C = Kv + h_tri_cm(i, j, Ti) * bi2;
+          o.kchunks = static_cast<int>(std::min(chunks, seg_chunks));
+          lj.push_back(o);
+          if (seg == 0) m->llx_fl[i] += 2.0 * double(bi2) * double(i - j) * m->bi;
+        }
+        m->llx_cnt[i].push_back(static_cast<int64_t>(lj.size()) - m->llx_off[i].back());
+      }
+      m->llx_slice_off[i] = static_cast<int64_t>(sj.size());
+      for (int j = 0; j <= i; ++j)
+        sj.push_back(OzakiSliceJob{X + h_tri_cm(i, j, Ti) * bi2, m->Xs.as<int8_t>(), int64_t(i - j) * m->bi});
+    }
+    m->llx_slice_off[Ti] = static_cast<int64_t>(sj.size());
+    // the plane pointers are filled in at launch time (Xs is allocated there): keep the panel
+    // offsets in `planes` for now
+    for (int i = 0, t = 0; i < Ti; ++i)
+      for (int j = 0; j <= i; ++j, ++t)
+        sj[t].planes = reinterpret_cast<int8_t*>(static_cast<intptr_t>(h_tri_cm(j, j, Ti) * bi2 * S));
+    CUDA_TRY(m->llx_jobs.ensure(sizeof(OzakiJob) * std::max<size_t>(1, lj.size())));
+    if (!lj.empty())
+      CUDA_TRY(cudaMemcpy(m->llx_jobs.p, lj.data(), sizeof(OzakiJob) * lj.size(), cudaMemcpyHostToDevice));
+    m->llx_slices_host = sj;
   }
   CUDA_TRY(m->inv_jobs.ensure(sizeof(GemmJob) * jobs.size()));
   CUDA_TRY(cudaMemcpy(m->inv_jobs.p, jobs.data(), sizeof(GemmJob) * jobs.size(),
@@ -1080,6 +1130,8 @@ int build_inv_plan(gpb_model* m) {
   m->inv_plan = true;
   return GPB_OK;
 }
+
+int ensure_l_planes(gpb_model* m);  // prediction section
 
 int loss_gradients(gpb_model* m, double out[3]) {
   const bool tl = m->trainable[0], tv = m->trainable[1], tn = m->trainable[2];
@@ -1094,12 +1146,65 @@ int loss_gradients(gpb_model* m, double out[3]) {
   double* D = m->Dinv.as<double>();
   const GemmJob* jobs = m->inv_jobs.as<GemmJob>();
   PhaseTimer pt(m, 5);
+  // The int8 pipe for the long products of the gradient when the planes are on: |X_ij| <= ||L^-1||_2
+  // <= 1 / sqrt(noise) (K >= noise I; 1 on the decoupled padding rows) bounds X; tiny noise keeps
+  // the FP64 kernels.  K^-1 = X^T X from n = oz_grad_min_n; X itself left-looking from
+  // oz_llx_min_tiles tiles (below that its per-row products are too small for the kernel).
+  bool planes = m->oz_slices > 0 && !m->grad_fp64_only && m->np_ >= m->oz_grad_min_n && m->s2 >= 1e-6;
+  if (planes && !ensure_optional(m->Xs, size_t(m->oz_slices) * ntiles * bi2)) planes = false;
+  bool llx = planes && Ti >= m->oz_llx_min_tiles;
+  if (llx && !m->ls_ok && !ensure_optional(m->Ls, size_t(m->oz_slices) * ntiles * bi2)) llx = false;
+  const int S = std::max(m->oz_slices, 1), nrb = bi / kOzakiBM;
+  const double sx = plane_scale(std::max(1.0, 1.0 / std::sqrt(std::max(m->s2, 1e-300))));
+  if (planes && !m->ozflag.p) {
+    CUDA_TRY(m->ozflag.ensure(sizeof(int)));
+    CUDA_TRY(cudaMemsetAsync(m->ozflag.p, 0, sizeof(int), m->st));
+  }
   // X = L^-1 (tiled.py:263-298 with the identity RHS, model.py:358-361),
   // with a one-row lookahead on the critical stream (build_inv_plan)
   for (int i = 0; i < Ti; ++i)
     CUDA_TRY(cudaMemcpyAsync(X + h_tri_cm(i, i, Ti) * bi2, D + int64_t(i) * bi2,
                              sizeof(double) * bi2, cudaMemcpyDeviceToDevice, m->st));
   CUDA_TRY(cudaMemsetAsync(m->Kinv.p, 0, sizeof(double) * ntiles * bi2, m->st));
+  if (llx) {
+    GPB_TRY(ensure_l_planes(m));
+    if (m->llx_slices_base != m->Xs.p) {  // slice-job table with this Xs
+      std::vector<OzakiSliceJob> sj = m->llx_slices_host;
+      for (auto& j : sj) j.planes = m->Xs.as<int8_t>() + reinterpret_cast<intptr_t>(j.planes);
+      CUDA_TRY(m->llx_slices.ensure(sizeof(OzakiSliceJob) * std::max<size_t>(1, sj.size())));
+      CUDA_TRY(cudaMemcpy(m->llx_slices.p, sj.data(), sizeof(OzakiSliceJob) * sj.size(), cudaMemcpyHostToDevice));
+      m->llx_slices_base = m->Xs.p;
+    }
+    auto slice_row = [&](int i) -> int {
+      ProfScope ps(m, KC_OTHER, 0.0);
+      CUDA_TRY(launch_ozaki_slice_t_batch(m->llx_slices.as<OzakiSliceJob>() + m->llx_slice_off[i], i + 1, bi, bi, bi, sx,
+                                          1, nrb, S, m->ozflag.as<int>(), m->st));
+      ++m->launches;
+      return GPB_OK;
+    };
+    GPB_TRY(slice_row(0));
+    for (int i = 1; i < Ti; ++i) {
+      for (size_t seg = 0; seg < m->llx_off[i].size(); ++seg) {
+        OzakiGemm g{};
+        g.a = {m->Ls.as<int8_t>(), bi2 * S, bi / kOzakiBK, int64_t(bi / kOzakiBK) * S * kOzakiBox};
+        g.b = {m->Xs.as<int8_t>(), 0, int(1) << 30, int64_t(S) * kOzakiBox, int64_t(nrb) * S * kOzakiBox};
+        g.M = g.N = bi;
+        g.K = static_cast<int>(std::min<int64_t>(kOzakiMaxK, int64_t(i) * bi - int64_t(seg) * kOzakiMaxK));
+        g.slices = S;
+        g.alpha = -m->oz_sa * sx;
+        g.beta = seg == 0 ? 0.0 : 1.0;
+        g.ldc_in = g.ldc_out = bi;
+        g.jobs = m->llx_jobs.as<OzakiJob>() + m->llx_off[i][seg];
+        g.njobs = static_cast<int>(m->llx_cnt[i][seg]);
+        ProfScope ps(m, KC_OZAKI, seg == 0 ? m->llx_fl[i] : 0.0);
+        CUDA_TRY(launch_ozaki_gemm(g, m->st));
+        m->launches += 2;
+      }
+      GemmParams f = views(base_params(jobs + m->invx_off[i], i * nb, 1, nb, bi, bi, bi, 1.0, 0.0), m->Dinv, m->Kinv);
+      GPB_TRY(gemm(m, f, true, false, EPI_AXPBY, gemm_flops(int64_t(i) * nb, int64_t(GBM) * nb * (nb + 1) / 2)));
+      GPB_TRY(slice_row(i));
+    }
+  } else {
   cudaEvent_t* ev_x = m->grad_ev.data();       // [k]: X(k, .) final
   cudaEvent_t* ev_u = m->grad_ev.data() + Ti;  // [k]: U_k applied to rows > k + 1
   CUDA_TRY(cudaEventRecord(ev_x[0], m->st));   // X(0, 0) = Dinv_0
@@ -1127,6 +1232,7 @@ int loss_gradients(gpb_model* m, double out[3]) {
     }
   }
   CUDA_TRY(cudaStreamWaitEvent(m->st, ev_x[Ti - 1], 0));
+  }
 
   double* red = m->red.as<double>();
   const int64_t nblk = ntiles * (bi / kSekBlock) * (bi / kSekBlock);
@@ -1134,16 +1240,8 @@ int loss_gradients(gpb_model* m, double out[3]) {
     // K^-1 = X^T X, lower tiles (model.py:362-380)
     // On the int8 pipe when the planes are on: |X_ij| <= ||L^-1||_2 <= 1 / sqrt(noise) (K >= noise I;
     // 1 on the decoupled padding rows) bounds the operand; tiny noise keeps the FP64 kernels.
-    bool planes = m->oz_slices > 0 && m->np_ >= m->oz_grad_min_n && m->s2 >= 1e-6;
-    if (planes && !ensure_optional(m->Xs, size_t(m->oz_slices) * ntiles * bi2)) planes = false;
     if (planes) {
-      if (!m->ozflag.p) {
-        CUDA_TRY(m->ozflag.ensure(sizeof(int)));
-        CUDA_TRY(cudaMemsetAsync(m->ozflag.p, 0, sizeof(int), m->st));
-      }
-      const int S = m->oz_slices, nrb = bi / kOzakiBM;
-      const double sx = plane_scale(std::max(1.0, 1.0 / std::sqrt(m->s2)));
-      {
+      if (!llx) {  // (the left-looking X phase sliced its rows as it went)
         ProfScope ps(m, KC_OTHER, 0.0);
         for (int c = 0; c < Ti; ++c) {  // planes of column panel c of X, transposed
           const int64_t e0 = h_tri_cm(c, c, Ti) * bi2;
@@ -1174,6 +1272,12 @@ int loss_gradients(gpb_model* m, double out[3]) {
         CUDA_TRY(cudaMemsetAsync(m->ozflag.p, 0, sizeof(int), m->st));
         ++m->oz_fallbacks;
         planes = false;
+        if (llx) {  // X itself came from saturated digits: the whole gradient again
+          m->grad_fp64_only = true;
+          const int st = loss_gradients(m, out);
+          m->grad_fp64_only = false;
+          return st;
+        }
       }
     }
     if (!planes) {
@@ -1772,7 +1876,7 @@ void free_model(gpb_model* m, bool keep = true) {
                     &m->X, &m->Kinv, &m->part_l, &m->part_v, &m->part_x, &m->inv_jobs,
                     &m->Bv, &m->W, &m->mpart, &m->sq, &m->pred_jobs, &m->zt, &m->mean, &m->var,
                     &m->S, &m->fc_jobs, &m->gp_panel, &m->gp_h, &m->gp_jobs, &m->gp_tiles,
-                    &m->Ls, &m->Vs, &m->ozflag, &m->Ps, &m->oz_jobs, &m->fc_oz_jobs, &m->Xs, &m->kinv_oz_jobs})
+                    &m->Ls, &m->Vs, &m->ozflag, &m->Ps, &m->oz_jobs, &m->fc_oz_jobs, &m->Xs, &m->kinv_oz_jobs, &m->llx_jobs, &m->llx_slices})
     b->release(keep);
 }
 

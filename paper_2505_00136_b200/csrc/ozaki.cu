@@ -365,8 +365,15 @@ __global__ void __launch_bounds__(256)
 // so that the stores run along the box rows (one 32-byte row per column)
 __global__ void __launch_bounds__(256)
     ozaki_slice_t_kernel(const double* __restrict__ src, long long ld, double inv_scale, int8_t* __restrict__ planes,
-                         long long rb_boxes, long long kc_boxes, long long k0, int slices, int* flag) {
+                         long long rb_boxes, long long kc_boxes, long long k0, int slices, int* flag,
+                         const OzakiSliceJob* __restrict__ jobs) {
   __shared__ unsigned stage[kOzakiMaxSlices][64][17];
+  if (jobs) {  // batched: one job per blockIdx.z
+    const OzakiSliceJob j = jobs[blockIdx.z];
+    src = j.src;
+    planes = j.planes;
+    k0 = j.k0;
+  }
   const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
   const long long c0 = static_cast<long long>(blockIdx.x) * 64;
   const long long kb = static_cast<long long>(blockIdx.y) * 64;
@@ -466,7 +473,19 @@ cudaError_t launch_ozaki_slice_t(const double* src, int64_t rows, int64_t cols, 
     return cudaErrorInvalidValue;
   dim3 grid(static_cast<unsigned>(cols / 64), static_cast<unsigned>(rows / 64));
   if (rows / 64 > 65535) return cudaErrorInvalidValue;
-  ozaki_slice_t_kernel<<<grid, 256, 0, st>>>(src, ld, 1.0 / scale, planes, rb_boxes, kc_boxes, k0, slices, flag);
+  ozaki_slice_t_kernel<<<grid, 256, 0, st>>>(src, ld, 1.0 / scale, planes, rb_boxes, kc_boxes, k0, slices, flag,
+                                             nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ozaki_slice_t_batch(const OzakiSliceJob* jobs, int njobs, int64_t rows, int64_t cols, int64_t ld,
+                                       double scale, int64_t rb_boxes, int64_t kc_boxes, int slices, int* flag,
+                                       cudaStream_t st) {
+  if (njobs <= 0) return cudaSuccess;
+  if (slices < 1 || slices > kOzakiMaxSlices || (rows & 63) || (cols & 127) || njobs > 65535 || rows / 64 > 65535)
+    return cudaErrorInvalidValue;
+  dim3 grid(static_cast<unsigned>(cols / 64), static_cast<unsigned>(rows / 64), static_cast<unsigned>(njobs));
+  ozaki_slice_t_kernel<<<grid, 256, 0, st>>>(nullptr, ld, 1.0 / scale, nullptr, rb_boxes, kc_boxes, 0, slices, flag, jobs);
   return cudaGetLastError();
 }
 

@@ -68,6 +68,17 @@ cudaError_t launch_ozaki_slice_t(const double* src, int64_t rows, int64_t cols, 
 // the margin absorbs round-off in entries that reach the bound
 inline double ozaki_plane_scale(double bound) { return bound * (128.0 / 127.0) * (1.0 + 1e-9); }
 
+// Batched form of launch_ozaki_slice_t: job t slices the rows x cols block at jobs[t].src into
+// jobs[t].planes at k offset jobs[t].k0 (same rows, cols, ld and box strides for every job).
+struct OzakiSliceJob {
+  const double* src;
+  int8_t* planes;
+  int64_t k0;
+};
+cudaError_t launch_ozaki_slice_t_batch(const OzakiSliceJob* jobs, int njobs, int64_t rows, int64_t cols, int64_t ld,
+                                       double scale, int64_t rb_boxes, int64_t kc_boxes, int slices, int* flag,
+                                       cudaStream_t st);
+
 struct OzakiOperand {
   const int8_t* planes;
   int64_t tile_stride;  // bytes from a tile to the next one along k
