@@ -244,7 +244,7 @@ struct gpb_model {
   std::vector<OzakiSliceJob> llx_slices_host;  // `planes` = byte offset into Xs until uploaded
   const void* llx_slices_base = nullptr;       // the Xs the uploaded table points into
   std::vector<double> llx_fl;
-  int oz_llx_min_tiles = 32;
+  int oz_llx_min_tiles = 16;
   bool grad_fp64_only = false;  // transient: repeat of a gradient whose digits saturated
   bool vs_ok = false;  // Vs holds the planes of every row block of the current V (Bv)
   int64_t oz_chol_min_k = 512;  // updates with a shorter K = np * bi stay on the DMMA kernel
@@ -1842,6 +1842,7 @@ int model_create(gpb_ctx* ctx, const double* z, const double* y, int64_t n, int6
   if (const char* e = getenv("GPB_OZAKI_MIN_K")) m->oz_min_k = std::max<int64_t>(64, atoll(e));
   if (const char* e = getenv("GPB_OZAKI_CHOL")) m->oz_chol = atoi(e) != 0;
   if (const char* e = getenv("GPB_OZAKI_CHOL_IN")) m->oz_chol_in = atoi(e) != 0;
+  if (const char* e = getenv("GPB_OZAKI_LLX_MIN_TILES")) m->oz_llx_min_tiles = std::max(2, atoi(e));
   if (const char* e = getenv("GPB_OZAKI_CHOL_MIN_K")) m->oz_chol_min_k = std::max<int64_t>(64, atoll(e));
   if (int s_l = apply_layout(m)) {
     delete m;
