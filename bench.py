@@ -480,6 +480,37 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         _lib.check(lib.gpb_model_set_ozaki(h, planes))
     kms, kbusy, kcnt = main_stats["kms"], main_stats["kbusy"], main_stats["kcnt"]
 
+    # ---- the same sizes on a DENSE covariance (D = 8).  Config 2's 128-feature K is nearly
+    # diagonal, so most digits of its planes are zero and the int8 pipe draws
+    # less power; on dense operands the chip touches its power cap and the digit-plane phases
+    # run slower (the FP64 DMMA path does not care).  Reported beside the headline for context.
+    dense = None
+    if planes and world == 1 and not args.no_dense_check:
+        d8 = 8
+        tr8, te8 = gpb.make_msd_dataset(n, m, d8, seed=0)
+        z8, y8, zt8 = (torch.from_numpy(a).cuda() for a in (tr8.z, tr8.y, te8.z))
+        h8 = ctypes.c_void_p()
+        _lib.check(lib.gpb_model_create_device(rt.handle, ctypes.c_void_p(z8.data_ptr()), ctypes.c_void_p(y8.data_ptr()),
+                                               n, d8, tiles, ctypes.byref(h8)))
+        ph8 = np.zeros(8)
+        reps8 = 2
+        for it in range(1 + reps8):
+            _lib.check(lib.gpb_model_set_params(h8, 1.0, 1.0, 0.1, flags))
+            _lib.check(lib.gpb_cholesky(h8, None))
+            _lib.check(lib.gpb_log_likelihood(h8, ctypes.byref(ll)))
+            _lib.check(lib.gpb_predict_device(h8, ctypes.c_void_p(zt8.data_ptr()), m, d8,
+                                              ctypes.c_void_p(mean_dev.data_ptr()), ctypes.c_void_p(var_dev.data_ptr())))
+            lib.gpb_model_timings(h8, tm, 8)
+            if it >= 1:
+                ph8 += np.array(tm[:])
+        lib.gpb_model_destroy(h8)
+        dense = {"workload": f"n_train = n_test = {n}, n_regressors = {d8}, {tiles} tiles: dense K (config 2's sizes)",
+                 "steps": reps8, "cholesky_tflops": reps8 * chol_flops(n) / (ph8[1] * 1e-3) / 1e12,
+                 "predict_variance_points_per_s": reps8 * m / ((ph8[3] + ph8[4]) * 1e-3),
+                 "factor_ms": float(ph8[1] / reps8), "trsm_variance_ms": float(ph8[4] / reps8),
+                 "note": "data-dependent power: with dense digit planes the SM clock dips under sw_power_cap during "
+                         "the int8 products (profiles/r02_planes_dense_clocks.txt)"}
+
     # ---- e2e: public API, host buffers, copies inside the timed region
     # inputs live in pinned host memory (the API's H2D copies read them there)
     def pinned(a):
@@ -548,6 +579,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "roofline": roofline_block(planes, pairs, planes_tf, planes_tf_exec, gemm_tf, gemm_tf_exec, peak.value,
                                    kcnt, kbusy, kms, total_ms, value / world, clk),
         "dmma_only": dmma_only,
+        "dense_k_check": dense,
         "digit_planes": planes,
         "arithmetic": ("FP64 inputs, outputs and accumulation across updates; long contractions (trailing updates, "
                        "prediction sweep) as exact int32 sums of int8 digit-plane products on tcgen05 "
@@ -787,6 +819,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-strong-base", action="store_true")
     ap.add_argument("--no-dmma-only", action="store_true", help="skip the extra pass with digit planes off")
+    ap.add_argument("--no-dense-check", action="store_true", help="skip the dense-covariance pass (D = 8)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
