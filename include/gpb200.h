@@ -156,6 +156,9 @@ int gpb_model_kernel_stats(gpb_model* m, double ms[8], double flops[8], int64_t 
 int gpb_model_kernel_busy(gpb_model* m, double busy_ms[8]);
 /* sustained FP64 tensor-pipe (DMMA.8x8x4) throughput of this GPU, TFLOP/s */
 int gpb_fp64_peak_probe(gpb_ctx* ctx, double seconds, double* tflops);
+/* the same for the int8 tcgen05 pipe: tcgen05.mma kind::i8 128 x 128 x 32 issued back to back from
+ * shared memory on every SM for about `seconds`; int8 operations per second, in units of 1e12 */
+int gpb_int8_peak_probe(gpb_ctx* ctx, double seconds, double* tops);
 
 /* ---- device-level tile operations (external schedulers) -------------------
  * Used by the multi-GPU driver (2D block-cyclic tiled Cholesky, tiled.py:168-204,

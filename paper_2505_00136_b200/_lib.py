@@ -72,6 +72,7 @@ SIGNATURES = {
     "gpb_model_kernel_stats": (ctypes.c_int, [_vp, _c_double_p, _c_double_p, _c_i64_p]),
     "gpb_model_kernel_busy": (ctypes.c_int, [_vp, _c_double_p]),
     "gpb_fp64_peak_probe": (ctypes.c_int, [_vp, ctypes.c_double, _c_double_p]),
+    "gpb_int8_peak_probe": (ctypes.c_int, [_vp, ctypes.c_double, _c_double_p]),
     "gpb_layout": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int64, _c_i64_p]),
     "gpb_dev_pad": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                    ctypes.c_int64, _vp]),
